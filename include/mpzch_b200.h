@@ -1,0 +1,179 @@
+/*
+ * mpzch_b200.h -- the C-ABI drop-in boundary of the B200 MPZCH remap path.
+ *
+ * Plain pointers and sizes only (no torch / C++ types).  The reference has no
+ * C ABI (it is a static C++ library); every entry point below names the
+ * reference C++ interface it replaces, relative to /root/reference/.  The
+ * C++ surface that keeps the reference's names and exception types sits on
+ * top of this header in include/mpzch_b200.hpp.
+ *
+ * Device model: one handle = one table resident on one B200 (or, for the
+ * row-sharded mode, the part of a table one rank owns).  Calls on a handle
+ * are stream-ordered and must be externally serialized, exactly like the
+ * reference's "mutations on a live table must be externally serialized"
+ * (proj/include/mpzch/table.hpp:38-40).  Validation errors are raised before
+ * any mutation (proj/src/batch_engine.cpp:146-147): the kernels carry a device
+ * error word and every mutating kernel is a no-op once it is set.
+ */
+#ifndef MPZCH_B200_H
+#define MPZCH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The C++ wrapper maps each to the reference's exception type
+ * with the identical message text (mpzch_last_error()). */
+typedef enum mpzch_status {
+    MPZCH_OK = 0,
+    MPZCH_EINVAL = 1,    /* std::invalid_argument */
+    MPZCH_EOVERFLOW = 2, /* std::overflow_error   */
+    MPZCH_ELENGTH = 3,   /* std::length_error     */
+    MPZCH_ELOGIC = 4,    /* std::logic_error      */
+    MPZCH_ERANGE = 5,    /* std::out_of_range     */
+    MPZCH_ECUDA = 6,     /* CUDA runtime failure  */
+    MPZCH_ENOMEM = 7,    /* std::bad_alloc / cudaErrorMemoryAllocation */
+    MPZCH_ENCCL = 8      /* NCCL failure (row-sharded mode) */
+} mpzch_status;
+
+/* EvictionMode, proj/include/mpzch/eviction.hpp:25 (same order) */
+enum { MPZCH_MODE_DISABLED = 0, MPZCH_MODE_TTL = 1, MPZCH_MODE_LRU = 2 };
+
+/* Outcome, proj/include/mpzch/probe_core.hpp:56 (same order, u8) */
+enum { MPZCH_FOUND = 0, MPZCH_INSERTED = 1, MPZCH_EVICTED = 2, MPZCH_COLLISION = 3 };
+
+/* Execution-path override (default AUTO: the fast claim path whenever it is
+ * exact for the batch, the per-shard ordered kernel otherwise). */
+enum { MPZCH_PATH_AUTO = 0, MPZCH_PATH_ORDERED = 1 };
+
+/* EvictionPolicy / TtlPolicy, proj/include/mpzch/eviction.hpp:13-46.
+ * per-feature TTLs are given as parallel arrays (feat_keys[i] -> feat_ttls[i]). */
+typedef struct mpzch_policy {
+    int32_t mode;          /* MPZCH_MODE_* */
+    uint32_t n_feat;       /* entries in the per-feature map */
+    uint64_t default_ttl;  /* TtlPolicy::default_ttl_seconds (TTL mode only) */
+    const uint32_t* feat_keys;
+    const uint64_t* feat_ttls;
+} mpzch_policy;
+
+/* Per-batch counters of the last process_batch call on a handle. */
+typedef struct mpzch_batch_stats {
+    uint64_t positions;
+    uint64_t new_positions;  /* positions that missed the pre-batch table */
+    uint64_t new_ids;        /* distinct ids among them (claim participants) */
+    uint64_t found, inserted, evicted, collision; /* per position */
+    uint64_t evicted_rows;   /* canonical evicted-list length */
+    uint32_t path;           /* MPZCH_PATH_* actually taken */
+    uint32_t reserved;
+} mpzch_batch_stats;
+
+typedef struct mpzch_table mpzch_table;
+
+/* ---- construction: MpzchTable(TableConfig), proj/include/mpzch/table.hpp:43,
+ *      proj/src/table.cpp:34-56; TableConfig proj/include/mpzch/table.hpp:18-28.
+ * Allocates identity (EMPTY), metadata (0), row_generation (0) and, when
+ * dim > 0, weights (draw_row for every row, bit-exact), momentum (0) and the
+ * trained flags (0) in HBM of `device`. */
+mpzch_status mpzch_table_create(const uint64_t* shard_capacities, uint32_t num_shards,
+                                uint32_t max_probe, uint64_t seed, uint32_t dim,
+                                uint64_t init_seed, int device, mpzch_table** out);
+mpzch_status mpzch_table_destroy(mpzch_table* t);
+
+/* layout accessors: table.hpp:48-56, TableLayout shard_router.hpp:13-29 */
+uint64_t mpzch_total_rows(const mpzch_table* t);
+uint32_t mpzch_num_shards(const mpzch_table* t);
+uint32_t mpzch_max_probe(const mpzch_table* t);
+uint32_t mpzch_dim(const mpzch_table* t);
+mpzch_status mpzch_shard_layout(const mpzch_table* t, uint64_t* capacities, uint64_t* offsets);
+
+/* ---- the hot path: process_batch(MpzchTable&, const IdBatch&, const EvictionPolicy&,
+ *      ExecMode) -> vector<ProbeResult>, proj/include/mpzch/batch_engine.hpp:44-46,
+ *      proj/src/batch_engine.cpp:141-221.
+ * ids[n], features[n] (NULL = feature 0 everywhere, IdBatch::ids BatchEntry),
+ * now = IdBatch::now.  Outputs per position: out_slots[n] (global row,
+ * ProbeResult::slot), out_outcomes[n] (ProbeResult::outcome; evicted ==
+ * (outcome == MPZCH_EVICTED)).  out_evicted receives the canonical evicted
+ * list: global rows of the (id, feature) uniques whose outcome is Evicted, in
+ * first-occurrence order, with multiplicity; *out_evicted_n is its full length
+ * even when it exceeds evicted_cap.  out_evicted / out_evicted_n may be NULL.
+ *
+ * mpzch_process_batch: HOST buffers; copies in, runs, copies out, returns when
+ * done (the reference call's semantics).
+ * mpzch_process_batch_device: DEVICE buffers on the table's device, enqueued on
+ * `stream` (cudaStream_t, NULL = the handle's stream); returns after the batch
+ * completed on that stream (it reports validation errors synchronously, like
+ * the reference).  out_evicted is a device pointer here. */
+mpzch_status mpzch_process_batch(mpzch_table* t, const uint64_t* ids, const uint32_t* features,
+                                 uint64_t n, uint64_t now, const mpzch_policy* policy,
+                                 uint64_t* out_slots, uint8_t* out_outcomes, uint64_t* out_evicted,
+                                 uint64_t evicted_cap, uint64_t* out_evicted_n);
+mpzch_status mpzch_process_batch_device(mpzch_table* t, const uint64_t* ids,
+                                        const uint32_t* features, uint64_t n, uint64_t now,
+                                        const mpzch_policy* policy, uint64_t* out_slots,
+                                        uint8_t* out_outcomes, uint64_t* out_evicted,
+                                        uint64_t evicted_cap, uint64_t* out_evicted_n,
+                                        void* stream);
+
+/* ---- lookup-only: MpzchTable::lookup(Id) const, table.hpp:65, table.cpp:150-156,
+ *      batched (semantics = one lookup per position, no writes). */
+mpzch_status mpzch_lookup(const mpzch_table* t, const uint64_t* ids, uint64_t n,
+                          uint64_t* out_slots, uint8_t* out_outcomes);
+mpzch_status mpzch_lookup_device(const mpzch_table* t, const uint64_t* ids, uint64_t n,
+                                 uint64_t* out_slots, uint8_t* out_outcomes, void* stream);
+
+/* ---- single-id training path: MpzchTable::lookup_or_insert(Id, FeatureOrdinal,
+ *      Timestamp, const EvictionPolicy&), table.hpp:61-62, table.cpp:98-110 */
+mpzch_status mpzch_lookup_or_insert(mpzch_table* t, uint64_t id, uint32_t feature, uint64_t now,
+                                    const mpzch_policy* policy, uint64_t* out_slot,
+                                    uint8_t* out_outcome);
+
+/* ---- state download (parity): identities(s)/metadata(s) table.hpp:89-90 (all
+ *      shards, concatenated in global-row order), embeddings() :92 weights,
+ *      momentum_row :87, row_trained :86; row_generation_ table.cpp:55. */
+mpzch_status mpzch_copy_identities(const mpzch_table* t, uint64_t* host_out);
+mpzch_status mpzch_copy_metadata(const mpzch_table* t, uint64_t* host_out);
+mpzch_status mpzch_copy_weights(const mpzch_table* t, uint64_t row0, uint64_t nrows,
+                                float* host_out);
+mpzch_status mpzch_copy_momentum(const mpzch_table* t, uint64_t row0, uint64_t nrows,
+                                 float* host_out);
+mpzch_status mpzch_copy_trained(const mpzch_table* t, uint8_t* host_out);
+mpzch_status mpzch_copy_row_generation(const mpzch_table* t, uint64_t* host_out);
+/* device pointers of the resident arrays (for fused consumers and the bench) */
+mpzch_status mpzch_device_arrays(const mpzch_table* t, uint64_t** identities,
+                                 uint64_t** metadata, float** weights);
+
+/* ---- raw state import (the reference's scenario tests write the arrays
+ *      directly, e.g. proj/tests/test_probe_core.cpp:113-121).  Writing raw
+ *      slots may create probe-window holes, so it switches the handle to the
+ *      hole-tolerant full-window semantics until mpzch_check_hole_free()
+ *      proves the no-hole invariant again. */
+mpzch_status mpzch_write_slots(mpzch_table* t, uint32_t shard, const uint64_t* local_slots,
+                               const uint64_t* identities, const uint64_t* metadata, uint64_t n);
+mpzch_status mpzch_check_hole_free(mpzch_table* t, int* out_hole_free);
+/* row payload write (stands in for training writes when testing resets) */
+mpzch_status mpzch_write_row(mpzch_table* t, uint64_t row, const float* weights,
+                             const float* momentum, uint8_t trained);
+
+/* ---- dirty tracking: make_cursor / dirty_rows_since, table.hpp:95-96,
+ *      table.cpp:209-225 (cursor = generation; the table uid is the handle). */
+mpzch_status mpzch_make_cursor(mpzch_table* t, uint64_t* out_generation);
+mpzch_status mpzch_dirty_rows_since(const mpzch_table* t, uint64_t generation, uint64_t* out,
+                                    uint64_t cap, uint64_t* out_n);
+
+/* ---- execution control / introspection */
+mpzch_status mpzch_set_path(mpzch_table* t, int path);
+mpzch_status mpzch_last_stats(const mpzch_table* t, mpzch_batch_stats* out);
+/* number of kernels this handle launched since creation (bench gpu_launches) */
+uint64_t mpzch_kernel_launches(const mpzch_table* t);
+/* thread-local text of the last error (the reference exception's what()) */
+const char* mpzch_last_error(void);
+/* library build string: "sm_100a <git-describe>" */
+const char* mpzch_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPZCH_B200_H */

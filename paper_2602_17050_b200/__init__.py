@@ -1,0 +1,461 @@
+"""paper_2602_17050_b200 -- B200-native MPZCH batched ID remap.
+
+Python mirror of the reference's C++ remap API (namespace ``mpzch``), over the
+C-ABI of ``include/mpzch_b200.h`` implemented by the sm_100a library
+``_lib/libmpzch_b200.so``.  Names, argument meaning and error behaviour follow
+the reference (paths relative to /root/reference/):
+
+=====================================  ==============================================
+this module                            reference
+=====================================  ==============================================
+``TableConfig`` / ``TableConfig.even`` proj/include/mpzch/table.hpp:18-28
+``EvictionPolicy.disabled/lru/ttl``    proj/include/mpzch/eviction.hpp:27-46
+``TtlPolicy``                          proj/include/mpzch/eviction.hpp:13-23
+``MpzchTable``                         proj/include/mpzch/table.hpp:41-131
+``process_batch``                      proj/include/mpzch/batch_engine.hpp:44-46
+``MpzchTable.lookup``                  proj/include/mpzch/table.hpp:65 (batched)
+``MpzchTable.lookup_or_insert``        proj/include/mpzch/table.hpp:61-62
+=====================================  ==============================================
+
+Exceptions mirror the reference's std exception types (``InvalidArgument`` for
+std::invalid_argument, ...).  There is no CPU fallback: importing this module
+without the built CUDA library raises ``ImportError``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Dict, Iterable, Optional, Sequence, Tuple
+
+import numpy as np
+
+__all__ = [
+    "FOUND", "INSERTED", "EVICTED", "COLLISION", "OUTCOME_NAMES",
+    "MpzchError", "InvalidArgument", "OverflowError_", "LengthError", "LogicError", "OutOfRange",
+    "CudaError", "TtlPolicy", "EvictionPolicy", "TableConfig", "MpzchTable", "process_batch",
+    "lib_path", "load_library", "even_capacities",
+]
+
+FOUND, INSERTED, EVICTED, COLLISION = 0, 1, 2, 3
+OUTCOME_NAMES = ("found", "inserted", "evicted", "collision")  # probe_core.cpp:17-25
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def lib_path() -> str:
+    return os.path.join(_HERE, "_lib", "libmpzch_b200.so")
+
+
+class MpzchError(RuntimeError):
+    pass
+
+
+class InvalidArgument(MpzchError, ValueError):      # std::invalid_argument
+    pass
+
+
+class OverflowError_(MpzchError, OverflowError):     # std::overflow_error
+    pass
+
+
+class LengthError(MpzchError, ValueError):           # std::length_error
+    pass
+
+
+class LogicError(MpzchError):                        # std::logic_error
+    pass
+
+
+class OutOfRange(MpzchError, IndexError):            # std::out_of_range
+    pass
+
+
+class CudaError(MpzchError):
+    pass
+
+
+class OutOfMemory(MpzchError, MemoryError):
+    pass
+
+
+_STATUS = {1: InvalidArgument, 2: OverflowError_, 3: LengthError, 4: LogicError, 5: OutOfRange,
+           6: CudaError, 7: OutOfMemory, 8: CudaError}
+
+
+class _Policy(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("n_feat", ctypes.c_uint32),
+                ("default_ttl", ctypes.c_uint64),
+                ("feat_keys", ctypes.POINTER(ctypes.c_uint32)),
+                ("feat_ttls", ctypes.POINTER(ctypes.c_uint64))]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("positions", ctypes.c_uint64), ("new_positions", ctypes.c_uint64),
+                ("new_ids", ctypes.c_uint64), ("found", ctypes.c_uint64),
+                ("inserted", ctypes.c_uint64), ("evicted", ctypes.c_uint64),
+                ("collision", ctypes.c_uint64), ("evicted_rows", ctypes.c_uint64),
+                ("path", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
+_LIB = None
+
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+_u8p = ctypes.POINTER(ctypes.c_uint8)
+_f32p = ctypes.POINTER(ctypes.c_float)
+_vp = ctypes.c_void_p
+
+# name -> (restype, argtypes); the exact exported surface of include/mpzch_b200.h
+_SIGS = {
+    "mpzch_table_create": (ctypes.c_int, [_u64p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64,
+                                          ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int,
+                                          ctypes.POINTER(_vp)]),
+    "mpzch_table_destroy": (ctypes.c_int, [_vp]),
+    "mpzch_total_rows": (ctypes.c_uint64, [_vp]),
+    "mpzch_num_shards": (ctypes.c_uint32, [_vp]),
+    "mpzch_max_probe": (ctypes.c_uint32, [_vp]),
+    "mpzch_dim": (ctypes.c_uint32, [_vp]),
+    "mpzch_shard_layout": (ctypes.c_int, [_vp, _u64p, _u64p]),
+    "mpzch_process_batch": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_uint64, ctypes.c_uint64,
+                                           ctypes.POINTER(_Policy), _vp, _vp, _vp,
+                                           ctypes.c_uint64, _u64p]),
+    "mpzch_process_batch_device": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_uint64, ctypes.c_uint64,
+                                                  ctypes.POINTER(_Policy), _vp, _vp, _vp,
+                                                  ctypes.c_uint64, _u64p, _vp]),
+    "mpzch_lookup": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _vp, _vp]),
+    "mpzch_lookup_device": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _vp, _vp, _vp]),
+    "mpzch_lookup_or_insert": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint32,
+                                              ctypes.c_uint64, ctypes.POINTER(_Policy), _u64p,
+                                              _u8p]),
+    "mpzch_copy_identities": (ctypes.c_int, [_vp, _vp]),
+    "mpzch_copy_metadata": (ctypes.c_int, [_vp, _vp]),
+    "mpzch_copy_weights": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, _vp]),
+    "mpzch_copy_momentum": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, _vp]),
+    "mpzch_copy_trained": (ctypes.c_int, [_vp, _vp]),
+    "mpzch_copy_row_generation": (ctypes.c_int, [_vp, _vp]),
+    "mpzch_device_arrays": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                           ctypes.POINTER(_vp)]),
+    "mpzch_write_slots": (ctypes.c_int, [_vp, ctypes.c_uint32, _vp, _vp, _vp, ctypes.c_uint64]),
+    "mpzch_check_hole_free": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int)]),
+    "mpzch_write_row": (ctypes.c_int, [_vp, ctypes.c_uint64, _vp, _vp, ctypes.c_uint8]),
+    "mpzch_make_cursor": (ctypes.c_int, [_vp, _u64p]),
+    "mpzch_dirty_rows_since": (ctypes.c_int, [_vp, ctypes.c_uint64, _vp, ctypes.c_uint64, _u64p]),
+    "mpzch_set_path": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "mpzch_last_stats": (ctypes.c_int, [_vp, ctypes.POINTER(_Stats)]),
+    "mpzch_kernel_launches": (ctypes.c_uint64, [_vp]),
+    "mpzch_last_error": (ctypes.c_char_p, []),
+    "mpzch_build_info": (ctypes.c_char_p, []),
+}
+
+
+def load_library():
+    """Load the sm_100a library; raise ImportError (no fallback) when it is absent."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = lib_path()
+    if not os.path.exists(path):
+        raise ImportError(f"MPZCH CUDA library not built ({path}); run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = _LIB.mpzch_last_error().decode()
+        raise _STATUS.get(rc, MpzchError)(msg)
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data) if a is not None and a.size else None
+
+
+@dataclass
+class TtlPolicy:
+    """TtlPolicy, proj/include/mpzch/eviction.hpp:13-23."""
+    default_ttl_seconds: int = 259200
+    per_feature_ttl: Dict[int, int] = field(default_factory=dict)
+
+    def ttl_for(self, feature: int) -> int:
+        return self.per_feature_ttl.get(feature, self.default_ttl_seconds)
+
+    def validate(self):  # eviction.cpp:8-18
+        if self.default_ttl_seconds == 0:
+            raise InvalidArgument("default TTL must be strictly positive")
+        for f, t in self.per_feature_ttl.items():
+            if t == 0:
+                raise InvalidArgument(f"per-feature TTL must be strictly positive (feature {f})")
+
+
+class EvictionPolicy:
+    """EvictionPolicy, proj/include/mpzch/eviction.hpp:27-46 (mode 0/1/2 = Disabled/Ttl/Lru)."""
+    DISABLED, TTL, LRU = 0, 1, 2
+
+    def __init__(self, mode: int, ttl: Optional[TtlPolicy] = None):
+        self.mode = mode
+        self.ttl = ttl or TtlPolicy()
+        keys = sorted(self.ttl.per_feature_ttl) if mode == self.TTL else []
+        self._keys = np.array(keys, dtype=np.uint32)
+        self._vals = np.array([self.ttl.per_feature_ttl[k] for k in keys], dtype=np.uint64)
+        self._c = _Policy(mode, len(keys), self.ttl.default_ttl_seconds if mode == self.TTL else 0,
+                          self._keys.ctypes.data_as(_u32p) if len(keys) else None,
+                          self._vals.ctypes.data_as(_u64p) if len(keys) else None)
+
+    @classmethod
+    def disabled(cls):
+        return cls(cls.DISABLED)
+
+    @classmethod
+    def lru(cls):
+        return cls(cls.LRU)
+
+    @classmethod
+    def ttl(cls, cfg: Optional[TtlPolicy] = None, **kw):
+        cfg = cfg or TtlPolicy(**kw)
+        cfg.validate()
+        return cls(cls.TTL, cfg)
+
+    def meta_for(self, now: int, feature: int = 0) -> int:
+        """make_metadata, proj/src/eviction.cpp:20-30."""
+        if self.mode != self.TTL:
+            return now
+        t = self.ttl.ttl_for(feature)
+        if t > (1 << 64) - 1 - now:
+            raise OverflowError_("TTL expiry overflows the 64-bit timestamp range")
+        return now + t
+
+
+def even_capacities(total_rows: int, num_shards: int) -> list:
+    """TableLayout::even, proj/src/shard_router.cpp:27-40."""
+    if num_shards == 0:
+        raise InvalidArgument("layout needs at least one shard")
+    if total_rows < num_shards:
+        raise InvalidArgument("fewer rows than shards")
+    caps = [total_rows // num_shards] * num_shards
+    for s in range(total_rows % num_shards):
+        caps[s] += 1
+    return caps
+
+
+@dataclass
+class TableConfig:
+    """TableConfig, proj/include/mpzch/table.hpp:18-28."""
+    shard_capacities: Sequence[int]
+    max_probe: int = 1
+    seed: int = 0
+    dim: int = 0
+    init_seed: int = 0
+
+    @classmethod
+    def even(cls, total_rows, num_shards, max_probe, seed, dim=0, init_seed=0):
+        return cls(even_capacities(total_rows, num_shards), max_probe, seed, dim, init_seed)
+
+
+class MpzchTable:
+    """Device-resident MpzchTable (proj/include/mpzch/table.hpp:41-131) on one B200."""
+
+    def __init__(self, cfg: TableConfig, device: int = 0):
+        lib = load_library()
+        caps = np.ascontiguousarray(np.array(list(cfg.shard_capacities), dtype=np.uint64))
+        h = _vp()
+        _check(lib.mpzch_table_create(caps.ctypes.data_as(_u64p) if caps.size else None,
+                                      len(caps), cfg.max_probe, cfg.seed, cfg.dim, cfg.init_seed,
+                                      device, ctypes.byref(h)))
+        self._h = h
+        self._lib = lib
+        self.cfg = cfg
+        self.device = device
+        self.num_shards = len(caps)
+        self.max_probe = cfg.max_probe
+        self.dim = cfg.dim
+        self.total_rows = int(lib.mpzch_total_rows(h))
+        self.shard_capacities = caps.copy()
+        offs = np.zeros(len(caps) + 1, dtype=np.uint64)
+        _check(lib.mpzch_shard_layout(h, caps.ctypes.data_as(_u64p), offs.ctypes.data_as(_u64p)))
+        self.shard_offsets = offs
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.mpzch_table_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def has_embeddings(self) -> bool:
+        return self.dim > 0
+
+    # ---- hot path ------------------------------------------------------------------------
+    def process_batch(self, ids, now: int, policy: EvictionPolicy, features=None,
+                      evicted_cap: Optional[int] = None) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """process_batch (batch_engine.cpp:141-221) on host buffers.
+
+        Returns (slots u64[n] global rows, outcomes u8[n], evicted u64[k]) where evicted is the
+        canonical evicted list (first-occurrence order, with multiplicity)."""
+        ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        n = ids.size
+        feats = None if features is None else np.ascontiguousarray(features, dtype=np.uint32)
+        if feats is not None and feats.size != n:
+            raise InvalidArgument("features must pair 1:1 with ids")
+        slots = np.empty(n, dtype=np.uint64)
+        oc = np.empty(n, dtype=np.uint8)
+        cap = n if evicted_cap is None else evicted_cap
+        ev = np.empty(max(cap, 1), dtype=np.uint64)
+        nev = ctypes.c_uint64(0)
+        _check(self._lib.mpzch_process_batch(self._h, _ptr(ids), _ptr(feats), n, now,
+                                             ctypes.byref(policy._c), _ptr(slots), _ptr(oc),
+                                             _ptr(ev), cap, ctypes.byref(nev)))
+        return slots, oc, ev[:min(nev.value, cap)].copy()
+
+    def process_batch_device(self, ids, now: int, policy: EvictionPolicy, features=None,
+                             out_slots=None, out_outcomes=None, out_evicted=None, stream=None):
+        """process_batch on device tensors (torch, on this table's device).  Returns the
+        evicted-list length; results land in out_slots / out_outcomes / out_evicted."""
+        import torch
+        n = ids.numel()
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        nev = ctypes.c_uint64(0)
+        _check(self._lib.mpzch_process_batch_device(
+            self._h, ctypes.c_void_p(ids.data_ptr()),
+            ctypes.c_void_p(features.data_ptr()) if features is not None else None, n, now,
+            ctypes.byref(policy._c), ctypes.c_void_p(out_slots.data_ptr()),
+            ctypes.c_void_p(out_outcomes.data_ptr()),
+            ctypes.c_void_p(out_evicted.data_ptr()) if out_evicted is not None else None,
+            out_evicted.numel() if out_evicted is not None else 0, ctypes.byref(nev),
+            ctypes.c_void_p(st.cuda_stream)))
+        return nev.value
+
+    def lookup(self, ids) -> Tuple[np.ndarray, np.ndarray]:
+        """Batched MpzchTable::lookup (table.cpp:150-156): (slots, outcomes), no writes."""
+        ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        slots = np.empty(ids.size, dtype=np.uint64)
+        oc = np.empty(ids.size, dtype=np.uint8)
+        _check(self._lib.mpzch_lookup(self._h, _ptr(ids), ids.size, _ptr(slots), _ptr(oc)))
+        return slots, oc
+
+    def lookup_device(self, ids, out_slots, out_outcomes, stream=None):
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _check(self._lib.mpzch_lookup_device(self._h, ctypes.c_void_p(ids.data_ptr()), ids.numel(),
+                                             ctypes.c_void_p(out_slots.data_ptr()),
+                                             ctypes.c_void_p(out_outcomes.data_ptr()),
+                                             ctypes.c_void_p(st.cuda_stream)))
+
+    def lookup_or_insert(self, id: int, feature: int, now: int, policy: EvictionPolicy):
+        """MpzchTable::lookup_or_insert (table.cpp:98-110): (global slot, outcome)."""
+        slot = ctypes.c_uint64(0)
+        oc = ctypes.c_uint8(0)
+        _check(self._lib.mpzch_lookup_or_insert(self._h, id, feature, now, ctypes.byref(policy._c),
+                                                ctypes.byref(slot), ctypes.byref(oc)))
+        return slot.value, oc.value
+
+    # ---- state (parity) ------------------------------------------------------------------
+    def identities_all(self) -> np.ndarray:
+        out = np.empty(self.total_rows, dtype=np.uint64)
+        _check(self._lib.mpzch_copy_identities(self._h, _ptr(out)))
+        return out
+
+    def metadata_all(self) -> np.ndarray:
+        out = np.empty(self.total_rows, dtype=np.uint64)
+        _check(self._lib.mpzch_copy_metadata(self._h, _ptr(out)))
+        return out
+
+    def identities(self, shard: int) -> np.ndarray:
+        self._check_shard(shard)
+        a, b = int(self.shard_offsets[shard]), int(self.shard_offsets[shard + 1])
+        return self.identities_all()[a:b]
+
+    def metadata(self, shard: int) -> np.ndarray:
+        self._check_shard(shard)
+        a, b = int(self.shard_offsets[shard]), int(self.shard_offsets[shard + 1])
+        return self.metadata_all()[a:b]
+
+    def _check_shard(self, shard):
+        if shard < 0 or shard >= self.num_shards:
+            raise OutOfRange("shard index out of range")
+
+    def weights(self, row0: int = 0, nrows: Optional[int] = None) -> np.ndarray:
+        nrows = self.total_rows - row0 if nrows is None else nrows
+        out = np.empty((nrows, max(self.dim, 1)), dtype=np.float32)
+        _check(self._lib.mpzch_copy_weights(self._h, row0, nrows, _ptr(out)))
+        return out
+
+    def momentum(self, row0: int = 0, nrows: Optional[int] = None) -> np.ndarray:
+        nrows = self.total_rows - row0 if nrows is None else nrows
+        out = np.empty((nrows, max(self.dim, 1)), dtype=np.float32)
+        _check(self._lib.mpzch_copy_momentum(self._h, row0, nrows, _ptr(out)))
+        return out
+
+    def trained(self) -> np.ndarray:
+        out = np.empty(self.total_rows, dtype=np.uint8)
+        _check(self._lib.mpzch_copy_trained(self._h, _ptr(out)))
+        return out
+
+    def row_generation(self) -> np.ndarray:
+        out = np.empty(self.total_rows, dtype=np.uint64)
+        _check(self._lib.mpzch_copy_row_generation(self._h, _ptr(out)))
+        return out
+
+    def device_arrays(self):
+        """(identity, metadata, weights) device pointers as ints."""
+        a, b, c = _vp(), _vp(), _vp()
+        _check(self._lib.mpzch_device_arrays(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return a.value, b.value, c.value
+
+    def write_slots(self, shard: int, local_slots, identities, metadata=None):
+        s = np.ascontiguousarray(local_slots, dtype=np.uint64)
+        i = np.ascontiguousarray(identities, dtype=np.uint64)
+        m = None if metadata is None else np.ascontiguousarray(metadata, dtype=np.uint64)
+        _check(self._lib.mpzch_write_slots(self._h, shard, _ptr(s), _ptr(i), _ptr(m), s.size))
+
+    def check_hole_free(self) -> bool:
+        v = ctypes.c_int(0)
+        _check(self._lib.mpzch_check_hole_free(self._h, ctypes.byref(v)))
+        return bool(v.value)
+
+    def write_row(self, row: int, weights=None, momentum=None, trained: int = 1):
+        w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float32)
+        m = None if momentum is None else np.ascontiguousarray(momentum, dtype=np.float32)
+        _check(self._lib.mpzch_write_row(self._h, row, _ptr(w), _ptr(m), trained))
+
+    def make_cursor(self) -> int:
+        g = ctypes.c_uint64(0)
+        _check(self._lib.mpzch_make_cursor(self._h, ctypes.byref(g)))
+        return g.value
+
+    def dirty_rows_since(self, cursor: int) -> np.ndarray:
+        out = np.empty(self.total_rows, dtype=np.uint64)
+        n = ctypes.c_uint64(0)
+        _check(self._lib.mpzch_dirty_rows_since(self._h, cursor, _ptr(out), out.size, ctypes.byref(n)))
+        return out[:n.value].copy()
+
+    def set_path(self, path: str):
+        _check(self._lib.mpzch_set_path(self._h, {"auto": 0, "ordered": 1}[path]))
+
+    def last_stats(self) -> dict:
+        s = _Stats()
+        _check(self._lib.mpzch_last_stats(self._h, ctypes.byref(s)))
+        d = {k: getattr(s, k) for k, _ in _Stats._fields_}
+        d["path"] = "fast" if s.path == 0 else "ordered"
+        return d
+
+    def kernel_launches(self) -> int:
+        return int(self._lib.mpzch_kernel_launches(self._h))
+
+
+def process_batch(table: MpzchTable, ids, now: int, policy: EvictionPolicy, features=None):
+    """Free-function spelling of the reference's process_batch (batch_engine.hpp:44-46)."""
+    return table.process_batch(ids, now, policy, features)
+
+
+def build_info() -> str:
+    return load_library().mpzch_build_info().decode()

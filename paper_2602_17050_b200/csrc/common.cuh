@@ -1,0 +1,117 @@
+// common.cuh -- device-side primitives shared by every MPZCH sm_100a kernel.
+//
+// Every constant below is pinned to the reference so hashes, homes, shards
+// and reset rows are bit-identical (paths relative to /root/reference/):
+//   kEmptySlot / salts / mix64   proj/include/mpzch/ids.hpp:16-43
+//   SplitMix64                    proj/include/mpzch/rng.hpp:10-30
+//   home_slot                     proj/src/probe_core.cpp:27-30
+//   shard_of                      proj/src/shard_router.cpp:42-46
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mpzch_b200 {
+
+constexpr uint64_t kEmpty = ~0ull;
+constexpr uint64_t kHomeSalt = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kShardSalt = 0xD1B54A32D192ED03ull;
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+constexpr uint32_t kNone32 = 0xffffffffu;
+
+enum : uint8_t { kFound = 0, kInserted = 1, kEvicted = 2, kCollision = 3 };
+enum : int { kModeDisabled = 0, kModeTtl = 1, kModeLru = 2 };
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t id, uint64_t seed) {
+    uint64_t x = id ^ seed;
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ull;
+    x ^= x >> 33;
+    return x;
+}
+
+// SplitMix64 output for an explicit state value (the generator's state after
+// k increments is s0 + k*golden, so element j of a stream is independent).
+__host__ __device__ __forceinline__ uint64_t splitmix_out(uint64_t state) {
+    uint64_t z = state;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// Exact 64-bit x mod d without the ~100-instruction software division:
+// m = floor((2^64-1)/d), q = umulhi(x, m) is floor(x/d) or at most 2 below it.
+struct FastMod {
+    uint64_t d;
+    uint64_t m;
+};
+
+inline FastMod make_fastmod(uint64_t d) { return FastMod{d, ~0ull / d}; }
+
+__device__ __forceinline__ uint64_t fastmod(uint64_t x, FastMod f) {
+    const uint64_t q = __umul64hi(x, f.m);
+    uint64_t r = x - q * f.d;
+    while (r >= f.d) r -= f.d;
+    return r;
+}
+
+// One logical shard: its global row range [offset, offset + cap).
+struct ShardDev {
+    uint64_t offset;
+    FastMod cap;
+};
+
+// The resident table, passed by value to every kernel.
+struct TableDev {
+    uint64_t* ident;     // identity per global row (EMPTY = ~0)
+    uint64_t* meta;      // metadata per global row
+    float* weights;      // rows x dim (dim > 0)
+    float* momentum;     // rows x dim
+    uint8_t* trained;    // rows
+    uint64_t* row_gen;   // rows
+    const ShardDev* shards;
+    FastMod nshards;
+    uint64_t seed;
+    uint64_t init_seed;
+    uint64_t total;
+    double bound;        // 1/sqrt(dim), computed on the host exactly as draw_row does
+    uint32_t P;          // max_probe
+    uint32_t dim;
+};
+
+__device__ __forceinline__ uint32_t shard_of(uint64_t id, const TableDev& t) {
+    return (uint32_t)fastmod(mix64(id ^ kShardSalt, t.seed), t.nshards);
+}
+
+__device__ __forceinline__ uint64_t home_of(uint64_t id, const ShardDev& s, uint64_t seed) {
+    return fastmod(mix64(id ^ kHomeSalt, seed), s.cap);
+}
+
+// Error word shared by all kernels of one batch.  Mutating kernels return
+// immediately when any field is set, so an invalid batch mutates nothing.
+struct BatchErr {
+    unsigned long long bad_pos;  // min invalid position, ~0 if none
+    unsigned int overflow;       // TTL expiry overflow seen
+    unsigned int too_many;       // fast-path capacity exceeded (never with sane n)
+};
+
+__device__ __forceinline__ bool batch_failed(const BatchErr* e) {
+    return e->bad_pos != ~0ull || e->overflow != 0;
+}
+
+// L2-coherent loads/stores for state that other threads mutate in the same kernel.
+__device__ __forceinline__ uint64_t ld_cg(const uint64_t* p) { return __ldcg(p); }
+
+// 32-byte (one sector) load of four consecutive slots: LDG.E.256 on sm_100.
+__device__ __forceinline__ void ld_sector(const uint64_t* p, uint64_t& a, uint64_t& b, uint64_t& c,
+                                          uint64_t& d) {
+    asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+                 : "l"(p));
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+}  // namespace mpzch_b200

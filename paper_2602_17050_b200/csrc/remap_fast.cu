@@ -1,0 +1,509 @@
+// remap_fast.cu -- the B200 fast path of process_batch (proj/src/batch_engine.cpp:141-221)
+// for hole-free tables under Disabled, or TTL with one metadata value per batch.
+//
+// Exactness argument: within a batch the set of slots a new id may
+// take only shrinks (EMPTY -> id, expired -> live), every unique probes its own window,
+// and the sequential reference gives each new id the first available slot of its
+// window not taken by a lower-rank unique.  The kernels below reach exactly that
+// assignment without any ordering pass:
+//
+//   K1 probe      one thread per POSITION, sector (32 B) loads from the home slot up to
+//                 the first match or EMPTY (hole-free early exit).  Hits on
+//                 live slots and full windows are final here; everything else goes to
+//                 the new list.  Read-only, so id validation is fused in.
+//   K2 dedup      new positions -> one entry per distinct id (64-bit atomicCAS key),
+//                 rank = first position (atomicMin).  (id, feature) secondaries are
+//                 resolved from the id's first position in K5.
+//   K3 claim      every entry claims slots in its window by 64-bit atomicCAS of a
+//                 rank-stamped claim word into the identity array itself.  A claim
+//                 with a lower rank replaces a higher one; the thread that displaces a
+//                 claim continues the displaced entry's scan ("takeover"), so the
+//                 fixpoint -- each entry on the first slot no lower rank holds -- is
+//                 reached in one launch with no grid barrier.
+//   K4 commit     claim words -> ids, outcomes (Inserted/Evicted/Found-owner), touch_row,
+//                 reset list, evicted flags by rank.
+//   K5 finalize   per new position result (+ secondary (id, f') rule).
+//   K6 meta       M[slot] = meta for every position (one value per batch => order-free).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "table.hpp"
+
+namespace mpzch_b200 {
+
+namespace {
+
+constexpr uint64_t kClaimBit = 1ull << 63;
+constexpr uint64_t kFlagEmpty = 1ull << 30;  // the claimed slot was EMPTY before the batch
+constexpr uint64_t kEntryMask = (1ull << 30) - 1;
+constexpr uint8_t kStateCollided = 1;
+
+__device__ __forceinline__ bool is_claim(uint64_t v) { return (v >> 63) != 0 && v != kEmpty; }
+__device__ __forceinline__ uint32_t claim_rank(uint64_t v) { return (uint32_t)(v >> 31); }
+__device__ __forceinline__ uint32_t claim_entry(uint64_t v) { return (uint32_t)(v & kEntryMask); }
+
+__device__ __forceinline__ uint64_t wrap_add(uint64_t h, uint64_t off, uint64_t cap) {
+    uint64_t x = h + off;
+    return x >= cap ? x - cap : x;
+}
+
+__device__ __forceinline__ uint64_t pick4(uint32_t j, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+    return j == 0 ? a : (j == 1 ? b : (j == 2 ? c : d));
+}
+
+// Id-table sizing: power of two >= 2 * count, at least 1024, at most the allocation.
+__device__ __forceinline__ uint64_t table_mask(unsigned count, uint64_t cap_alloc) {
+    uint64_t c = 1024;
+    while (c < 2ull * count && c < cap_alloc) c <<= 1;
+    return c - 1;
+}
+
+__global__ void k_init_counters(BatchCounters* c) {
+    if (threadIdx.x == 0) {
+        BatchCounters z{};
+        z.err.bad_pos = ~0ull;
+        *c = z;
+    }
+}
+
+// First offset in [0, limit) whose metadata is expired (stored < now), or limit.
+// Only called under TTL; reads one sector per 4 slots.
+__device__ __forceinline__ uint32_t first_expired(const uint64_t* __restrict__ meta, uint64_t base,
+                                                  uint64_t h, uint64_t cap, uint32_t limit,
+                                                  uint64_t now) {
+    uint32_t off = 0;
+    uint64_t g = base + h;
+    const uint64_t end = base + cap;
+    while (off < limit) {
+        const uint64_t a4 = g & ~3ull;
+        uint64_t w0, w1, w2, w3;
+        ld_sector(meta + a4, w0, w1, w2, w3);
+        do {
+            if (pick4((uint32_t)(g - a4), w0, w1, w2, w3) < now) return off;
+            ++off;
+            if (++g == end) g = base;
+        } while (off < limit && (g >> 2) == (a4 >> 2));
+    }
+    return limit;
+}
+
+// K1: one thread per position.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_probe(TableDev t, const uint64_t* __restrict__ ids,
+                                               uint64_t n, uint64_t now, BatchCounters* ctr,
+                                               uint64_t* __restrict__ out_slots,
+                                               uint8_t* __restrict__ out_oc,
+                                               uint32_t* __restrict__ newpos,
+                                               uint32_t* __restrict__ newa,
+                                               uint32_t* __restrict__ newm) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const unsigned lane = lane_id();
+    unsigned long long my_found = 0, my_coll = 0;
+    for (uint64_t base_i = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base_i < n;
+         base_i += stride) {
+        const uint64_t i = base_i + lane;
+        bool is_new = false;
+        uint32_t a_off = 0, m_off = kNone32;
+        if (i < n) {
+            const uint64_t id = ids[i];
+            if (id >> 63) {
+                atomicMin(&ctr->err.bad_pos, (unsigned long long)i);
+            } else {
+                const uint32_t s = shard_of(id, t);
+                const ShardDev sd = t.shards[s];
+                const uint64_t cap = sd.cap.d, base = sd.offset, end = base + cap;
+                const uint64_t h = home_of(id, sd, t.seed);
+                uint32_t off = 0, found = kNone32, empty = kNone32;
+                uint64_t g = base + h, gf = 0;
+                while (off < t.P) {
+                    const uint64_t a4 = g & ~3ull;
+                    uint64_t w0, w1, w2, w3;
+                    ld_sector(t.ident + a4, w0, w1, w2, w3);
+                    do {
+                        const uint64_t v = pick4((uint32_t)(g - a4), w0, w1, w2, w3);
+                        if (v == id) { found = off; gf = g; break; }
+                        if (v == kEmpty) { empty = off; break; }
+                        ++off;
+                        if (++g == end) g = base;
+                    } while (off < t.P && (g >> 2) == (a4 >> 2));
+                    if (found != kNone32 || empty != kNone32) break;
+                }
+                if (MODE == kModeDisabled) {
+                    if (found != kNone32) {
+                        out_slots[i] = gf;
+                        out_oc[i] = kFound;
+                        ++my_found;
+                    } else if (empty != kNone32) {
+                        is_new = true;
+                        a_off = empty;
+                    } else {
+                        out_slots[i] = base + h;
+                        out_oc[i] = kCollision;
+                        ++my_coll;
+                    }
+                } else {  // TTL, one meta value per batch
+                    if (found != kNone32) {
+                        if (__ldg(t.meta + gf) >= now) {  // live: nobody can take it this batch
+                            out_slots[i] = gf;
+                            out_oc[i] = kFound;
+                            ++my_found;
+                        } else {  // expired own slot: contested by lower-rank new ids
+                            is_new = true;
+                            m_off = found;
+                            a_off = first_expired(t.meta, base, h, cap, found, now);
+                        }
+                    } else {
+                        const uint32_t lim = empty != kNone32 ? empty : t.P;
+                        const uint32_t x = first_expired(t.meta, base, h, cap, lim, now);
+                        if (x < lim || empty != kNone32) {
+                            is_new = true;
+                            a_off = x;
+                        } else {
+                            out_slots[i] = base + h;
+                            out_oc[i] = kCollision;
+                            ++my_coll;
+                        }
+                    }
+                }
+            }
+        }
+        // warp-aggregated append to the new list
+        const unsigned mask = __ballot_sync(0xffffffffu, is_new);
+        if (mask) {
+            unsigned basek = 0;
+            if (lane == 0) basek = atomicAdd(&ctr->new_count, (unsigned)__popc(mask));
+            basek = __shfl_sync(0xffffffffu, basek, 0);
+            if (is_new) {
+                const unsigned k = basek + __popc(mask & ((1u << lane) - 1));
+                newpos[k] = (uint32_t)i;
+                newa[k] = a_off;
+                newm[k] = m_off;
+            }
+        }
+    }
+    // per-warp stat reduction
+    for (int o = 16; o; o >>= 1) {
+        my_found += __shfl_xor_sync(0xffffffffu, my_found, o);
+        my_coll += __shfl_xor_sync(0xffffffffu, my_coll, o);
+    }
+    if (lane == 0) {
+        if (my_found) atomicAdd(&ctr->found, my_found);
+        if (my_coll) atomicAdd(&ctr->collision, my_coll);
+    }
+}
+
+// K2: distinct-id table over the new positions.
+__global__ void __launch_bounds__(256) k_dedup(const uint64_t* __restrict__ ids, BatchCounters* ctr,
+                                               uint64_t tcap, const uint32_t* __restrict__ newpos,
+                                               const uint32_t* __restrict__ newa,
+                                               const uint32_t* __restrict__ newm,
+                                               uint32_t* __restrict__ newent, uint64_t* tkey,
+                                               unsigned* tmin, uint32_t* ta, uint32_t* tm,
+                                               uint32_t* elist) {
+    if (batch_failed(&ctr->err)) return;
+    const unsigned cnt = ctr->new_count;
+    const uint64_t mask = table_mask(cnt, tcap);
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
+        const uint32_t pos = newpos[k];
+        const uint64_t id = ids[pos];
+        uint64_t h = mix64(id, 0x2545F4914F6CDD1Dull) & mask;
+        uint32_t e;
+        for (;;) {
+            uint64_t cur = ld_cg(tkey + h);
+            if (cur == kEmpty) {
+                cur = atomicCAS((unsigned long long*)(tkey + h), (unsigned long long)kEmpty,
+                                (unsigned long long)id);
+                if (cur == kEmpty) {  // inserted: publish the entry's probe facts
+                    e = (uint32_t)h;
+                    ta[e] = newa[k];
+                    tm[e] = newm[k];
+                    const unsigned slot = atomicAdd(&ctr->entry_count, 1u);
+                    elist[slot] = e;
+                    break;
+                }
+            }
+            if (cur == id) {
+                e = (uint32_t)h;
+                break;
+            }
+            h = (h + 1) & mask;
+        }
+        atomicMin(tmin + e, pos);
+        newent[k] = e;
+    }
+}
+
+// K3: rank-priority claims with takeover.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCounters* ctr,
+                                               const uint32_t* __restrict__ elist,
+                                               const uint64_t* __restrict__ tkey,
+                                               const unsigned* __restrict__ tmin,
+                                               const uint32_t* __restrict__ ta,
+                                               const uint32_t* __restrict__ tm,
+                                               volatile uint32_t* theld, uint8_t* tstate) {
+    if (batch_failed(&ctr->err)) return;
+    const unsigned cnt = ctr->entry_count;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
+        uint32_t e = elist[k];
+        bool fresh = true;
+        uint32_t resume = 0;
+        for (;;) {
+            const uint64_t id = tkey[e];
+            const uint32_t rank = tmin[e];
+            const uint32_t s = shard_of(id, t);
+            const ShardDev sd = t.shards[s];
+            const uint64_t cap = sd.cap.d, base = sd.offset;
+            const uint64_t h = home_of(id, sd, t.seed);
+            const uint64_t cv = kClaimBit | ((uint64_t)rank << 31) | (uint64_t)e;
+            uint32_t next = kNone32;
+            uint64_t gnext = 0;
+            bool held = false;
+            uint32_t off;
+            if (MODE == kModeTtl && fresh && tm[e] != kNone32) {
+                // owner: try to keep (refresh) the expired slot holding our own id
+                const uint32_t m = tm[e];
+                const uint64_t gm = base + wrap_add(h, m, cap);
+                theld[e] = m;
+                __threadfence();
+                uint64_t v = ld_cg(t.ident + gm);
+                for (;;) {
+                    uint64_t nv;
+                    if (v == id) nv = cv;
+                    else if (is_claim(v) && claim_rank(v) > rank) nv = cv | (v & kFlagEmpty);
+                    else break;  // a lower rank evicted our id first
+                    const uint64_t old = atomicCAS((unsigned long long*)(t.ident + gm),
+                                                   (unsigned long long)v, (unsigned long long)nv);
+                    if (old == v) {
+                        held = true;
+                        if (is_claim(v)) { next = claim_entry(v); gnext = gm; }
+                        break;
+                    }
+                    v = old;
+                }
+                off = ta[e];
+            } else {
+                off = fresh ? ta[e] : resume;
+            }
+            if (!held) {
+                for (; off < t.P; ++off) {
+                    const uint64_t g = base + wrap_add(h, off, cap);
+                    uint64_t v = ld_cg(t.ident + g);
+                    for (;;) {
+                        uint64_t nv;
+                        if (v == kEmpty) {
+                            nv = cv | kFlagEmpty;
+                        } else if (v >> 63) {
+                            if (claim_rank(v) < rank) break;  // a lower rank holds it for good
+                            nv = cv | (v & kFlagEmpty);
+                        } else {
+                            if (MODE != kModeTtl) break;           // occupied
+                            if (!(ld_cg(t.meta + g) < now)) break;  // live
+                            nv = cv;                                 // expired foreign id
+                        }
+                        theld[e] = off;
+                        __threadfence();
+                        const uint64_t old = atomicCAS((unsigned long long*)(t.ident + g),
+                                                       (unsigned long long)v,
+                                                       (unsigned long long)nv);
+                        if (old == v) {
+                            held = true;
+                            if (is_claim(v)) { next = claim_entry(v); gnext = g; }
+                            break;
+                        }
+                        v = old;
+                    }
+                    if (held) break;
+                }
+                if (!held) tstate[e] = kStateCollided;
+            }
+            if (next == kNone32) break;
+            // take over the displaced entry: it resumes right after the slot it lost,
+            // or -- if it was an owner losing its own id's slot -- as a taker from its
+            // first available offset.
+            {
+                const uint64_t id2 = tkey[next];
+                const uint64_t h2 = home_of(id2, sd, t.seed);  // same shard as the slot
+                const uint64_t loc = gnext - base;
+                const uint32_t off2 = (uint32_t)(loc >= h2 ? loc - h2 : loc + cap - h2);
+                if (MODE == kModeTtl && tm[next] != kNone32 && off2 == tm[next])
+                    resume = ta[next];
+                else
+                    resume = off2 + 1;
+                e = next;
+                fresh = false;
+            }
+        }
+    }
+}
+
+// K4: commit claims.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
+                                                const uint32_t* __restrict__ elist,
+                                                const uint64_t* __restrict__ tkey,
+                                                const unsigned* __restrict__ tmin,
+                                                const uint32_t* __restrict__ tm,
+                                                const uint32_t* __restrict__ theld,
+                                                const uint8_t* __restrict__ tstate,
+                                                uint64_t* __restrict__ tslot,
+                                                uint8_t* __restrict__ toc, uint64_t gen_clock,
+                                                uint64_t* __restrict__ reset_rows,
+                                                uint8_t* __restrict__ evflag,
+                                                uint64_t* __restrict__ evslot) {
+    if (batch_failed(&ctr->err)) return;
+    const unsigned cnt = ctr->entry_count;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
+        const uint32_t e = elist[k];
+        const uint64_t id = tkey[e];
+        const uint32_t s = shard_of(id, t);
+        const ShardDev sd = t.shards[s];
+        const uint64_t cap = sd.cap.d, base = sd.offset;
+        const uint64_t h = home_of(id, sd, t.seed);
+        if (tstate[e] == kStateCollided) {
+            tslot[e] = base + h;
+            toc[e] = kCollision;
+            continue;
+        }
+        const uint32_t off = theld[e];
+        const uint64_t g = base + wrap_add(h, off, cap);
+        const uint64_t v = t.ident[g];
+        if (!is_claim(v) || claim_entry(v) != e || claim_rank(v) != tmin[e]) {
+            atomicExch(&ctr->err.too_many, 2u);  // internal invariant violated
+            continue;
+        }
+        uint8_t oc;
+        if (MODE == kModeTtl && tm[e] == off) oc = kFound;
+        else oc = (v & kFlagEmpty) ? kInserted : kEvicted;
+        t.ident[g] = id;
+        if (oc != kFound) t.row_gen[g] = gen_clock;
+        if (oc == kEvicted) {
+            const unsigned r = atomicAdd(&ctr->reset_count, 1u);
+            reset_rows[r] = g;
+            const uint32_t rank = tmin[e];
+            evflag[rank] = 1;
+            evslot[rank] = g;
+            atomicAdd(&ctr->evicted_count, 1u);
+        }
+        tslot[e] = g;
+        toc[e] = oc;
+    }
+}
+
+// K5: results of the new positions (+ (id, f') secondaries: same id, other feature, later
+// first position -> Found on the primary's slot, or Collision if the primary collided).
+__global__ void __launch_bounds__(256) k_finalize(BatchCounters* ctr,
+                                                  const uint32_t* __restrict__ feats,
+                                                  const uint32_t* __restrict__ newpos,
+                                                  const uint32_t* __restrict__ newent,
+                                                  const unsigned* __restrict__ tmin,
+                                                  const uint64_t* __restrict__ tslot,
+                                                  const uint8_t* __restrict__ toc,
+                                                  uint64_t* __restrict__ out_slots,
+                                                  uint8_t* __restrict__ out_oc) {
+    if (batch_failed(&ctr->err)) return;
+    const unsigned cnt = ctr->new_count;
+    unsigned long long c[4] = {0, 0, 0, 0};
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
+        const uint32_t pos = newpos[k];
+        const uint32_t e = newent[k];
+        uint8_t oc = toc[e];
+        if (feats && feats[pos] != feats[tmin[e]]) oc = oc == kCollision ? kCollision : kFound;
+        out_slots[pos] = tslot[e];
+        out_oc[pos] = oc;
+        ++c[oc];
+    }
+    for (int j = 0; j < 4; ++j)
+        for (int o = 16; o; o >>= 1) c[j] += __shfl_xor_sync(0xffffffffu, c[j], o);
+    if (lane_id() == 0) {
+        if (c[0]) atomicAdd(&ctr->found, c[0]);
+        if (c[1]) atomicAdd(&ctr->inserted, c[1]);
+        if (c[2]) atomicAdd(&ctr->evicted, c[2]);
+        if (c[3]) atomicAdd(&ctr->collision, c[3]);
+    }
+}
+
+// K6: every position writes its metadata word; all values are identical in a batch.
+__global__ void __launch_bounds__(256) k_meta(TableDev t, const BatchCounters* ctr, uint64_t n,
+                                              const uint64_t* __restrict__ out_slots,
+                                              uint64_t meta_value) {
+    if (batch_failed(&ctr->err)) return;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        t.meta[out_slots[i]] = meta_value;
+}
+
+// K9: return the id-table entries to EMPTY for the next batch.
+__global__ void __launch_bounds__(256) k_cleanup(BatchCounters* ctr, const uint32_t* __restrict__ elist,
+                                                 uint64_t* tkey, unsigned* tmin, uint8_t* tstate) {
+    const unsigned cnt = ctr->entry_count;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
+        const uint32_t e = elist[k];
+        tkey[e] = kEmpty;
+        tmin[e] = kNone32;
+        tstate[e] = 0;
+    }
+}
+
+}  // namespace
+
+void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
+    const uint64_t n = a.n;
+    t.ensure_fast_scratch(n);
+    const unsigned B = 256;
+    const unsigned gN = grid_for(n, B);
+    const unsigned gW = grid_for(n, B, 148u * 8u);  // count-driven kernels
+    k_init_counters<<<1, 32, 0, st>>>(t.d_ctr);
+    ++t.launches;
+    if (a.pol->mode == kModeTtl)
+        k_probe<kModeTtl><<<gN, B, 0, st>>>(t.dev, a.ids, n, a.now, t.d_ctr, a.out_slots, a.out_oc,
+                                            t.s_newpos.as<uint32_t>(), t.s_newa.as<uint32_t>(),
+                                            t.s_newm.as<uint32_t>());
+    else
+        k_probe<kModeDisabled><<<gN, B, 0, st>>>(t.dev, a.ids, n, a.now, t.d_ctr, a.out_slots,
+                                                 a.out_oc, t.s_newpos.as<uint32_t>(),
+                                                 t.s_newa.as<uint32_t>(), t.s_newm.as<uint32_t>());
+    ++t.launches;
+    if (a.overflow_all) return;  // validation only; the host reports the error
+    k_dedup<<<gW, B, 0, st>>>(a.ids, t.d_ctr, t.tcap, t.s_newpos.as<uint32_t>(),
+                              t.s_newa.as<uint32_t>(), t.s_newm.as<uint32_t>(),
+                              t.s_newent.as<uint32_t>(), t.s_tkey.as<uint64_t>(),
+                              t.s_tmin.as<unsigned>(), t.s_ta.as<uint32_t>(), t.s_tm.as<uint32_t>(),
+                              t.s_elist.as<uint32_t>());
+    ++t.launches;
+    if (a.pol->mode == kModeTtl) {
+        k_claim<kModeTtl><<<gW, B, 0, st>>>(t.dev, a.now, t.d_ctr, t.s_elist.as<uint32_t>(),
+                                            t.s_tkey.as<uint64_t>(), t.s_tmin.as<unsigned>(),
+                                            t.s_ta.as<uint32_t>(), t.s_tm.as<uint32_t>(),
+                                            t.s_theld.as<uint32_t>(), t.s_tstate.as<uint8_t>());
+        k_commit<kModeTtl><<<gW, B, 0, st>>>(
+            t.dev, t.d_ctr, t.s_elist.as<uint32_t>(), t.s_tkey.as<uint64_t>(),
+            t.s_tmin.as<unsigned>(), t.s_tm.as<uint32_t>(), t.s_theld.as<uint32_t>(),
+            t.s_tstate.as<uint8_t>(), t.s_tslot.as<uint64_t>(), t.s_toc.as<uint8_t>(), t.gen_clock,
+            t.s_reset.as<uint64_t>(), t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>());
+    } else {
+        k_claim<kModeDisabled><<<gW, B, 0, st>>>(
+            t.dev, a.now, t.d_ctr, t.s_elist.as<uint32_t>(), t.s_tkey.as<uint64_t>(),
+            t.s_tmin.as<unsigned>(), t.s_ta.as<uint32_t>(), t.s_tm.as<uint32_t>(),
+            t.s_theld.as<uint32_t>(), t.s_tstate.as<uint8_t>());
+        k_commit<kModeDisabled><<<gW, B, 0, st>>>(
+            t.dev, t.d_ctr, t.s_elist.as<uint32_t>(), t.s_tkey.as<uint64_t>(),
+            t.s_tmin.as<unsigned>(), t.s_tm.as<uint32_t>(), t.s_theld.as<uint32_t>(),
+            t.s_tstate.as<uint8_t>(), t.s_tslot.as<uint64_t>(), t.s_toc.as<uint8_t>(), t.gen_clock,
+            t.s_reset.as<uint64_t>(), t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>());
+    }
+    t.launches += 2;
+    k_finalize<<<gW, B, 0, st>>>(t.d_ctr, a.feats, t.s_newpos.as<uint32_t>(),
+                                 t.s_newent.as<uint32_t>(), t.s_tmin.as<unsigned>(),
+                                 t.s_tslot.as<uint64_t>(), t.s_toc.as<uint8_t>(), a.out_slots,
+                                 a.out_oc);
+    k_meta<<<gN, B, 0, st>>>(t.dev, t.d_ctr, n, a.out_slots, a.uniform_meta);
+    t.launches += 2;
+    if (t.dim > 0) launch_reset_rows(t, t.s_reset.as<uint64_t>(), &t.d_ctr->reset_count, st);
+    if (a.pol->mode == kModeTtl) enqueue_compact_evicted(t, n, a.out_ev, a.ev_cap, st);
+    k_cleanup<<<gW, B, 0, st>>>(t.d_ctr, t.s_elist.as<uint32_t>(), t.s_tkey.as<uint64_t>(),
+                                t.s_tmin.as<unsigned>(), t.s_tstate.as<uint8_t>());
+    ++t.launches;
+}
+
+}  // namespace mpzch_b200

@@ -1,0 +1,314 @@
+// remap_ordered.cu -- the general, always-exact path of process_batch
+// (proj/src/batch_engine.cpp:141-221) for the cases the fast claim path does not
+// cover: LRU, TTL with several per-feature TTLs in one batch (last-writer
+// metadata order), and tables whose raw-imported state may hold probe-window
+// holes (proj/tests/test_probe_core.cpp:113-121).
+//
+//   G1  validate + (id, feature) dedup: 128-bit atomicCAS key, rank = first
+//       position (atomicMin)                                   batch_engine.cpp:79-108
+//   G2  first occurrences -> uniques in dedup order (ordered compaction)
+//   G3  per-unique shard + metadata (make_metadata)           eviction.cpp:20-30
+//   G4  one warp per shard walks the uniques in rank order and runs the two-pass
+//       probe of probe_core.cpp:69-134 with 32-slot coalesced window loads and
+//       __ballot_sync/__ffs decisions; shards run concurrently (the OpenMP
+//       parallel-for of batch_engine.cpp:203-208)
+//   G5  scatter to positions                                   batch_engine.cpp:213-220
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "compact.cuh"
+#include "table.hpp"
+
+namespace mpzch_b200 {
+
+namespace {
+
+typedef unsigned __int128 u128;
+constexpr u128 kKeyEmpty = ~(u128)0;
+
+__device__ __forceinline__ uint64_t ttl_lookup(uint32_t f, uint64_t def, const uint32_t* keys,
+                                               const uint64_t* vals, uint32_t nk) {
+    for (uint32_t i = 0; i < nk; ++i)
+        if (keys[i] == f) return vals[i];
+    return def;
+}
+
+__global__ void k_init_counters_o(BatchCounters* c) {
+    if (threadIdx.x == 0) {
+        BatchCounters z{};
+        z.err.bad_pos = ~0ull;
+        *c = z;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_validate_dedup(const uint64_t* __restrict__ ids,
+                                                        const uint32_t* __restrict__ feats, uint64_t n,
+                                                        uint64_t now, int mode, uint64_t def_ttl,
+                                                        const uint32_t* fk, const uint64_t* fv,
+                                                        uint32_t nk, BatchCounters* ctr, u128* key,
+                                                        unsigned* kmin, uint32_t* posent,
+                                                        uint64_t mask) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t id = ids[i];
+        const uint32_t f = feats ? feats[i] : 0u;
+        if (id >> 63) {
+            atomicMin(&ctr->err.bad_pos, (unsigned long long)i);
+            posent[i] = kNone32;
+            continue;
+        }
+        if (mode == kModeTtl) {
+            const uint64_t ttl = ttl_lookup(f, def_ttl, fk, fv, nk);
+            if (ttl > ~0ull - now) atomicExch(&ctr->err.overflow, 1u);
+        }
+        const u128 k = ((u128)f << 64) | (u128)id;
+        uint64_t h = mix64(id ^ ((uint64_t)f << 32), 0) & mask;
+        for (;;) {
+            u128 cur = key[h];
+            if (cur == kKeyEmpty) {
+                cur = atomicCAS(key + h, kKeyEmpty, k);
+                if (cur == kKeyEmpty) break;
+            }
+            if (cur == k) break;
+            h = (h + 1) & mask;
+        }
+        atomicMin(kmin + h, (unsigned)i);
+        posent[i] = (uint32_t)h;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_first_flags(const BatchCounters* ctr, uint64_t n,
+                                                     const uint32_t* __restrict__ posent,
+                                                     const unsigned* __restrict__ kmin,
+                                                     uint8_t* __restrict__ flag) {
+    const bool failed = batch_failed(&ctr->err);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t e = posent[i];
+        flag[i] = (!failed && e != kNone32 && kmin[e] == (unsigned)i) ? 1 : 0;
+    }
+}
+
+struct EmitUnique {
+    uint32_t* upos;
+    uint32_t* entu;
+    const uint32_t* posent;
+    __device__ void operator()(uint64_t i, unsigned k) const {
+        upos[k] = (uint32_t)i;
+        entu[posent[i]] = k;
+    }
+};
+
+__global__ void __launch_bounds__(256) k_prep(TableDev t, const BatchCounters* ctr,
+                                              const uint64_t* __restrict__ ids,
+                                              const uint32_t* __restrict__ feats,
+                                              const uint32_t* __restrict__ upos, uint64_t now,
+                                              int mode, uint64_t def_ttl, const uint32_t* fk,
+                                              const uint64_t* fv, uint32_t nk,
+                                              uint32_t* __restrict__ ushard,
+                                              uint64_t* __restrict__ umeta) {
+    const unsigned u = ctr->entry_count;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < u; k += gridDim.x * blockDim.x) {
+        const uint32_t pos = upos[k];
+        const uint64_t id = ids[pos];
+        ushard[k] = shard_of(id, t);
+        umeta[k] = mode == kModeTtl
+                       ? now + ttl_lookup(feats ? feats[pos] : 0u, def_ttl, fk, fv, nk)
+                       : now;
+    }
+}
+
+// G4: one warp per shard, uniques in rank order, reference two-pass probe.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_ordered(TableDev t, BatchCounters* ctr,
+                                                 const uint64_t* __restrict__ ids,
+                                                 const uint32_t* __restrict__ upos,
+                                                 const uint32_t* __restrict__ ushard,
+                                                 const uint64_t* __restrict__ umeta, uint64_t now,
+                                                 uint64_t gen_clock, uint64_t* __restrict__ uslot,
+                                                 uint8_t* __restrict__ uoc,
+                                                 uint64_t* __restrict__ reset_rows,
+                                                 uint8_t* __restrict__ evflag,
+                                                 uint64_t* __restrict__ evslot) {
+    if (batch_failed(&ctr->err)) return;
+    const uint32_t shard = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (shard >= t.nshards.d) return;
+    const unsigned lane = lane_id();
+    const unsigned u = ctr->entry_count;
+    const ShardDev sd = t.shards[shard];
+    const uint64_t cap = sd.cap.d, base = sd.offset;
+    const uint32_t P = t.P;
+    for (unsigned k0 = 0; k0 < u; k0 += 32) {
+        const unsigned kk = k0 + lane;
+        unsigned mine = __ballot_sync(0xffffffffu, kk < u && ushard[kk] == shard);
+        while (mine) {
+            const unsigned k = k0 + __ffs(mine) - 1;
+            mine &= mine - 1;
+            const uint64_t id = ids[upos[k]];
+            const uint64_t meta_in = umeta[k];
+            const uint64_t h = home_of(id, sd, t.seed);
+            // Pass 1: discovery (probe_core.cpp:78-86)
+            bool exists = false;
+            for (uint32_t c = 0; c < P; c += 32) {
+                const uint32_t off = c + lane;
+                bool hit = false;
+                if (off < P) {
+                    uint64_t x = h + off;
+                    x = x >= cap ? x - cap : x;
+                    hit = ld_cg(t.ident + base + x) == id;
+                }
+                if (__ballot_sync(0xffffffffu, hit)) { exists = true; break; }
+            }
+            // Pass 2: update / insert / evict (probe_core.cpp:89-121)
+            uint8_t oc = kCollision;
+            uint64_t gslot = base + h;
+            bool decided = false;
+            uint64_t best_m = 0;
+            uint32_t best_off = kNone32;
+            for (uint32_t c = 0; c < P && !decided; c += 32) {
+                const uint32_t off = c + lane;
+                const bool valid = off < P;
+                uint64_t g = 0, v = 0, m = 0;
+                if (valid) {
+                    uint64_t x = h + off;
+                    x = x >= cap ? x - cap : x;
+                    g = base + x;
+                    v = ld_cg(t.ident + g);
+                    if (MODE != kModeDisabled) m = ld_cg(t.meta + g);
+                }
+                const bool is_match = valid && v == id;
+                const bool is_empty = valid && v == kEmpty;
+                const bool is_exp = valid && MODE == kModeTtl && !exists && !is_match && !is_empty &&
+                                    m < now;
+                const unsigned stop = __ballot_sync(0xffffffffu, is_match || is_empty || is_exp);
+                if (stop) {
+                    const int src = __ffs(stop) - 1;
+                    const uint64_t gs = __shfl_sync(0xffffffffu, g, src);
+                    const int kind = __shfl_sync(0xffffffffu, is_match ? 0 : (is_empty ? 1 : 2), src);
+                    gslot = gs;
+                    oc = kind == 0 ? kFound : (kind == 1 ? kInserted : kEvicted);
+                    decided = true;
+                } else if (MODE == kModeLru && !exists) {
+                    // first strict minimum over the window, ties -> lowest offset
+                    uint64_t bm = valid ? m : ~0ull;
+                    uint32_t bo = valid ? off : kNone32;
+                    for (int o = 16; o; o >>= 1) {
+                        const uint64_t om = __shfl_xor_sync(0xffffffffu, bm, o);
+                        const uint32_t oo = __shfl_xor_sync(0xffffffffu, bo, o);
+                        if (om < bm || (om == bm && oo < bo)) { bm = om; bo = oo; }
+                    }
+                    if (bo != kNone32 && (best_off == kNone32 || bm < best_m)) {
+                        best_m = bm;
+                        best_off = bo;
+                    }
+                }
+            }
+            if (!decided && MODE == kModeLru && best_off != kNone32) {
+                uint64_t x = h + best_off;
+                x = x >= cap ? x - cap : x;
+                gslot = base + x;
+                oc = kEvicted;  // LRU fallback, probe_core.cpp:125-129
+            }
+            if (lane == 0) {
+                if (oc == kInserted || oc == kEvicted) t.ident[gslot] = id;
+                t.meta[gslot] = meta_in;  // Found refresh / insert / evict / Collision at home
+                if (oc == kInserted || oc == kEvicted) t.row_gen[gslot] = gen_clock;
+                if (oc == kEvicted) {
+                    if (t.dim) reset_rows[atomicAdd(&ctr->reset_count, 1u)] = gslot;
+                    evflag[k] = 1;
+                    evslot[k] = gslot;
+                    atomicAdd(&ctr->evicted_count, 1u);
+                }
+                uslot[k] = gslot;
+                uoc[k] = oc;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_scatter(BatchCounters* ctr, uint64_t n,
+                                                 const uint32_t* __restrict__ posent,
+                                                 const uint32_t* __restrict__ entu,
+                                                 const uint64_t* __restrict__ uslot,
+                                                 const uint8_t* __restrict__ uoc,
+                                                 uint64_t* __restrict__ out_slots,
+                                                 uint8_t* __restrict__ out_oc) {
+    if (batch_failed(&ctr->err)) return;
+    unsigned long long c[4] = {0, 0, 0, 0};
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = entu[posent[i]];
+        out_slots[i] = uslot[k];
+        const uint8_t oc = uoc[k];
+        out_oc[i] = oc;
+        ++c[oc];
+    }
+    for (int j = 0; j < 4; ++j)
+        for (int o = 16; o; o >>= 1) c[j] += __shfl_xor_sync(0xffffffffu, c[j], o);
+    if (lane_id() == 0) {
+        if (c[0]) atomicAdd(&ctr->found, c[0]);
+        if (c[1]) atomicAdd(&ctr->inserted, c[1]);
+        if (c[2]) atomicAdd(&ctr->evicted, c[2]);
+        if (c[3]) atomicAdd(&ctr->collision, c[3]);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_cleanup_o(uint64_t n, const uint32_t* __restrict__ posent,
+                                                   u128* key, unsigned* kmin) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t e = posent[i];
+        if (e == kNone32) continue;
+        key[e] = kKeyEmpty;
+        kmin[e] = kNone32;
+    }
+}
+
+}  // namespace
+
+void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
+    const uint64_t n = a.n;
+    t.ensure_ordered_scratch(n);
+    const unsigned B = 256;
+    const unsigned gN = grid_for(n, B);
+    const Policy& p = *a.pol;
+    const uint32_t nk = (uint32_t)p.keys.size();
+    k_init_counters_o<<<1, 32, 0, st>>>(t.d_ctr);
+    uint64_t mask = 1024;
+    while (mask < 2 * n) mask <<= 1;
+    mask -= 1;
+    u128* key = t.o_key.as<u128>();
+    unsigned* kmin = t.o_min.as<unsigned>();
+    uint32_t* posent = t.o_posent.as<uint32_t>();
+    k_validate_dedup<<<gN, B, 0, st>>>(a.ids, a.feats, n, a.now, p.mode, p.default_ttl, a.d_featk,
+                                       a.d_featv, nk, t.d_ctr, key, kmin, posent, mask);
+    k_first_flags<<<gN, B, 0, st>>>(t.d_ctr, n, posent, kmin, t.o_flag.as<uint8_t>());
+    t.launches += 3;
+    EmitUnique em{t.o_upos.as<uint32_t>(), t.o_entu.as<uint32_t>(), posent};
+    compact_flags(t.o_flag.as<uint8_t>(), n, t.s_blk.as<unsigned>(), &t.d_ctr->entry_count, true, em,
+                  st, t.launches);
+    k_prep<<<gN, B, 0, st>>>(t.dev, t.d_ctr, a.ids, a.feats, t.o_upos.as<uint32_t>(), a.now, p.mode,
+                             p.default_ttl, a.d_featk, a.d_featv, nk, t.o_ushard.as<uint32_t>(),
+                             t.o_umeta.as<uint64_t>());
+    const unsigned gS = (unsigned)(((uint64_t)t.S * 32 + B - 1) / B);
+#define MPZCH_ORDERED(MODE)                                                                       \
+    k_ordered<MODE><<<gS, B, 0, st>>>(t.dev, t.d_ctr, a.ids, t.o_upos.as<uint32_t>(),             \
+                                      t.o_ushard.as<uint32_t>(), t.o_umeta.as<uint64_t>(), a.now, \
+                                      t.gen_clock, t.o_uslot.as<uint64_t>(), t.o_uoc.as<uint8_t>(), \
+                                      t.s_reset.as<uint64_t>(), t.s_evflag.as<uint8_t>(),           \
+                                      t.s_evslot.as<uint64_t>())
+    if (p.mode == kModeTtl) MPZCH_ORDERED(kModeTtl);
+    else if (p.mode == kModeLru) MPZCH_ORDERED(kModeLru);
+    else MPZCH_ORDERED(kModeDisabled);
+#undef MPZCH_ORDERED
+    k_scatter<<<gN, B, 0, st>>>(t.d_ctr, n, posent, t.o_entu.as<uint32_t>(), t.o_uslot.as<uint64_t>(),
+                                t.o_uoc.as<uint8_t>(), a.out_slots, a.out_oc);
+    t.launches += 3;
+    if (t.dim > 0) launch_reset_rows(t, t.s_reset.as<uint64_t>(), &t.d_ctr->reset_count, st);
+    if (p.mode != kModeDisabled) enqueue_compact_evicted(t, n, a.out_ev, a.ev_cap, st);
+    k_cleanup_o<<<gN, B, 0, st>>>(n, posent, key, kmin);
+    ++t.launches;
+}
+
+}  // namespace mpzch_b200

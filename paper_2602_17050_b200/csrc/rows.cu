@@ -1,0 +1,161 @@
+// rows.cu -- embedding-row payload kernels: table init and eviction reset.
+//
+// draw_row (proj/src/embedding_store.cpp:12-18) seeds SplitMix64 with
+// mix64(row, init_seed) and draws w[j] = float((2*u_j - 1) * (1/sqrt(dim))),
+// u_j = (next() >> 11) * 2^-53 (proj/include/mpzch/rng.hpp:23).  The stream
+// state after j+1 steps is s0 + (j+1)*golden, so every element is computed
+// independently and stored as 16-byte vectors.  2*u-1 is exact; the product
+// is one FP64 rounding (__dmul_rn: no contraction), then __double2float_rn,
+// exactly the reference's static_cast<float> sequence.
+// reset_row (embedding_store.cpp:62-68): redraw + momentum 0 + trained 0.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "table.hpp"
+
+namespace mpzch_b200 {
+
+namespace {
+
+__device__ __forceinline__ float draw_elem(uint64_t s0, uint64_t j, double bound) {
+    const uint64_t z = splitmix_out(s0 + (j + 1) * kGolden);
+    const double u = (double)(z >> 11) * 0x1.0p-53;
+    const double t = __dadd_rn(__dmul_rn(2.0, u), -1.0);
+    return __double2float_rn(__dmul_rn(t, bound));
+}
+
+// init: grid-stride over (row, quad) for dim % 4 == 0, else over elements
+__global__ void __launch_bounds__(256) k_draw_all(TableDev t) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if ((t.dim & 3u) == 0) {
+        const uint64_t quads = t.dim / 4;
+        const uint64_t nq = t.total * quads;
+        for (uint64_t q = tid; q < nq; q += stride) {
+            const uint64_t row = q / quads;
+            const uint64_t j = (q - row * quads) * 4;
+            const uint64_t s0 = mix64(row, t.init_seed);
+            float4 w;
+            w.x = draw_elem(s0, j, t.bound);
+            w.y = draw_elem(s0, j + 1, t.bound);
+            w.z = draw_elem(s0, j + 2, t.bound);
+            w.w = draw_elem(s0, j + 3, t.bound);
+            reinterpret_cast<float4*>(t.weights)[q] = w;
+        }
+    } else {
+        const uint64_t ne = t.total * t.dim;
+        for (uint64_t x = tid; x < ne; x += stride) {
+            const uint64_t row = x / t.dim;
+            const uint64_t j = x - row * t.dim;
+            t.weights[x] = draw_elem(mix64(row, t.init_seed), j, t.bound);
+        }
+    }
+}
+
+// reset: one warp per listed row; rows may repeat (LRU double eviction), the
+// operation is idempotent.
+__global__ void __launch_bounds__(256) k_reset_rows(TableDev t, const uint64_t* __restrict__ rows,
+                                                    const unsigned* __restrict__ count) {
+    const unsigned n = *count;
+    const unsigned lane = lane_id();
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t r = warp; r < n; r += nwarps) {
+        const uint64_t row = rows[r];
+        const uint64_t s0 = mix64(row, t.init_seed);
+        float* w = t.weights + row * t.dim;
+        float* m = t.momentum + row * t.dim;
+        if ((t.dim & 3u) == 0) {
+            float4* w4 = reinterpret_cast<float4*>(w);
+            float4* m4 = reinterpret_cast<float4*>(m);
+            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (uint32_t q = lane; q < t.dim / 4; q += 32) {
+                const uint64_t j = (uint64_t)q * 4;
+                float4 v;
+                v.x = draw_elem(s0, j, t.bound);
+                v.y = draw_elem(s0, j + 1, t.bound);
+                v.z = draw_elem(s0, j + 2, t.bound);
+                v.w = draw_elem(s0, j + 3, t.bound);
+                w4[q] = v;
+                m4[q] = z;
+            }
+        } else {
+            for (uint32_t j = lane; j < t.dim; j += 32) {
+                w[j] = draw_elem(s0, j, t.bound);
+                m[j] = 0.f;
+            }
+        }
+        if (lane == 0) t.trained[row] = 0;
+    }
+}
+
+__global__ void k_write_slots(TableDev t, const uint64_t* __restrict__ g, const uint64_t* __restrict__ ids,
+                              const uint64_t* __restrict__ metas, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        t.ident[g[i]] = ids[i];
+        t.meta[g[i]] = metas[i];
+    }
+}
+
+// Hole check: every id stored inside its own probe window at
+// offset o must see neither EMPTY nor another copy of itself in [home, home+o).
+__global__ void __launch_bounds__(256) k_hole_check(TableDev t, unsigned* bad) {
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < t.total;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t id = t.ident[g];
+        if (id == kEmpty) continue;
+        if (id >> 63) { atomicExch(bad, 1u); continue; }  // stray claim word
+        const uint32_t s = shard_of(id, t);
+        const ShardDev sd = t.shards[s];
+        // the id must live in its own shard's segment to be reachable; if it does
+        // not, it is a foreign occupant for everybody and cannot create a hole
+        if (g < sd.offset || g >= sd.offset + sd.cap.d) continue;
+        const uint64_t h = home_of(id, sd, t.seed);
+        const uint64_t loc = g - sd.offset;
+        const uint64_t o = loc >= h ? loc - h : loc + sd.cap.d - h;
+        if (o >= t.P) continue;  // outside its window: invisible, harmless
+        uint64_t x = h;
+        for (uint64_t k = 0; k < o; ++k) {
+            const uint64_t v = t.ident[sd.offset + x];
+            if (v == kEmpty || v == id) { atomicExch(bad, 1u); break; }
+            if (++x == sd.cap.d) x = 0;
+        }
+    }
+}
+
+}  // namespace
+
+void launch_init_table(Table& t) {
+    if (t.dim == 0 || t.total == 0) return;
+    k_draw_all<<<148 * 16, 256, 0, t.stream>>>(t.dev);
+    ++t.launches;
+    MPZCH_CUDA(cudaGetLastError());
+}
+
+void launch_reset_rows(Table& t, const uint64_t* rows, const unsigned* count, cudaStream_t st) {
+    k_reset_rows<<<148 * 8, 256, 0, st>>>(t.dev, rows, count);
+    ++t.launches;
+}
+
+void launch_write_slots(Table& t, const uint64_t* g, const uint64_t* ids, const uint64_t* metas,
+                        uint64_t n, cudaStream_t st) {
+    if (!n) return;
+    k_write_slots<<<grid_for(n, 256), 256, 0, st>>>(t.dev, g, ids, metas, n);
+    ++t.launches;
+}
+
+bool run_hole_check(Table& t) {
+    unsigned* d_bad = nullptr;
+    MPZCH_CUDA(cudaMallocAsync((void**)&d_bad, sizeof(unsigned), t.stream));
+    MPZCH_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned), t.stream));
+    k_hole_check<<<grid_for(t.total, 256), 256, 0, t.stream>>>(t.dev, d_bad);
+    ++t.launches;
+    unsigned bad = 0;
+    MPZCH_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(unsigned), cudaMemcpyDeviceToHost, t.stream));
+    MPZCH_CUDA(cudaFreeAsync(d_bad, t.stream));
+    MPZCH_CUDA(cudaStreamSynchronize(t.stream));
+    return bad == 0;
+}
+
+}  // namespace mpzch_b200

@@ -1,0 +1,730 @@
+// table.cu -- the C-ABI (include/mpzch_b200.h) over the device-resident table.
+//
+// Host-side control flow of the reference calls it replaces:
+//   MpzchTable ctor            proj/src/table.cpp:34-56
+//   process_batch              proj/src/batch_engine.cpp:141-221 (error order :143-158)
+//   MpzchTable::lookup         proj/src/table.cpp:150-156
+//   MpzchTable::lookup_or_insert proj/src/table.cpp:98-110
+//   make_cursor / dirty_rows_since proj/src/table.cpp:209-225
+// Every error is detected before the first mutation and reported with the
+// reference's exception category and what() text.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/mpzch_b200.h"
+#include "common.cuh"
+#include "compact.cuh"
+#include "table.hpp"
+
+#ifndef MPZCH_BUILD_INFO
+#define MPZCH_BUILD_INFO "sm_100a"
+#endif
+
+namespace mpzch_b200 {
+
+static thread_local std::string g_last_error;
+
+void throw_cuda(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation)
+        throw Error{MPZCH_ENOMEM, std::string("device allocation failed: ") + what};
+    throw Error{MPZCH_ECUDA, std::string(cudaGetErrorString(e)) + " in " + what};
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) MPZCH_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+void DevBuf::reserve(size_t want) {
+    if (want <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    MPZCH_CUDA(cudaMalloc(&p, want));
+    bytes = want;
+}
+
+DevBuf::~DevBuf() {
+    if (p) cudaFree(p);
+}
+
+static uint64_t pow2_at_least(uint64_t x) {
+    uint64_t c = 1024;
+    while (c < x) c <<= 1;
+    return c;
+}
+
+Table::Table(const uint64_t* cap_in, uint32_t num_shards, uint32_t max_probe, uint64_t seed_in,
+             uint32_t dim_in, uint64_t init_seed_in, int device_in) {
+    // TableLayout::with_capacities shard_router.cpp:8-25, ShardConfig::validate probe_core.cpp:8-15
+    if (num_shards == 0) throw Error{MPZCH_EINVAL, "layout needs at least one shard"};
+    for (uint32_t s = 0; s < num_shards; ++s)
+        if (cap_in[s] == 0) throw Error{MPZCH_EINVAL, "shard capacity must be >= 1"};
+    for (uint32_t s = 0; s < num_shards; ++s)
+        if (max_probe < 1 || max_probe > cap_in[s])
+            throw Error{MPZCH_EINVAL, "max_probe must satisfy 1 <= max_probe <= capacity"};
+    S = num_shards;
+    P = max_probe;
+    seed = seed_in;
+    dim = dim_in;
+    init_seed = init_seed_in;
+    device = device_in;
+    caps.assign(cap_in, cap_in + num_shards);
+    offsets.assign(num_shards + 1, 0);
+    for (uint32_t s = 0; s < S; ++s) offsets[s + 1] = offsets[s] + caps[s];
+    total = offsets[S];
+
+    DeviceGuard g(device);
+    MPZCH_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    MPZCH_CUDA(cudaMallocHost((void**)&h_ctr, sizeof(BatchCounters)));
+    MPZCH_CUDA(cudaMalloc((void**)&d_ctr, sizeof(BatchCounters)));
+    // identity/metadata padded so a 32-byte sector load at the last slot stays in bounds
+    const uint64_t padded = ((total + 3) & ~3ull) + 4;
+    MPZCH_CUDA(cudaMalloc((void**)&ident, padded * sizeof(uint64_t)));
+    MPZCH_CUDA(cudaMalloc((void**)&meta, padded * sizeof(uint64_t)));
+    MPZCH_CUDA(cudaMalloc((void**)&row_gen, total * sizeof(uint64_t)));
+    MPZCH_CUDA(cudaMemsetAsync(ident, 0xff, padded * sizeof(uint64_t), stream));
+    MPZCH_CUDA(cudaMemsetAsync(meta, 0, padded * sizeof(uint64_t), stream));
+    MPZCH_CUDA(cudaMemsetAsync(row_gen, 0, total * sizeof(uint64_t), stream));
+    if (dim > 0) {
+        MPZCH_CUDA(cudaMalloc((void**)&weights, total * dim * sizeof(float)));
+        MPZCH_CUDA(cudaMalloc((void**)&momentum, total * dim * sizeof(float)));
+        MPZCH_CUDA(cudaMalloc((void**)&trained, total));
+        MPZCH_CUDA(cudaMemsetAsync(momentum, 0, total * dim * sizeof(float), stream));
+        MPZCH_CUDA(cudaMemsetAsync(trained, 0, total, stream));
+    }
+    std::vector<ShardDev> hs(S);
+    for (uint32_t s = 0; s < S; ++s) hs[s] = ShardDev{offsets[s], make_fastmod(caps[s])};
+    MPZCH_CUDA(cudaMalloc((void**)&d_shards, S * sizeof(ShardDev)));
+    MPZCH_CUDA(cudaMemcpyAsync(d_shards, hs.data(), S * sizeof(ShardDev), cudaMemcpyHostToDevice, stream));
+    dev.ident = ident;
+    dev.meta = meta;
+    dev.weights = weights;
+    dev.momentum = momentum;
+    dev.trained = trained;
+    dev.row_gen = row_gen;
+    dev.shards = d_shards;
+    dev.nshards = make_fastmod(S);
+    dev.seed = seed;
+    dev.init_seed = init_seed;
+    dev.total = total;
+    // draw_row's bound, embedding_store.cpp:14 (IEEE sqrt and division are exact-rounded on the host)
+    dev.bound = dim ? 1.0 / std::sqrt(static_cast<double>(dim)) : 0.0;
+    dev.P = P;
+    dev.dim = dim;
+    launch_init_table(*this);
+    MPZCH_CUDA(cudaStreamSynchronize(stream));
+}
+
+Table::~Table() {
+    DeviceGuard g(device);
+    if (stream) cudaStreamSynchronize(stream);
+    cudaFree(ident);
+    cudaFree(meta);
+    cudaFree(row_gen);
+    cudaFree(weights);
+    cudaFree(momentum);
+    cudaFree(trained);
+    cudaFree(d_shards);
+    cudaFree(d_ctr);
+    if (h_ctr) cudaFreeHost(h_ctr);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+void Table::ensure_fast_scratch(uint64_t n) {
+    s_newpos.reserve(n * 4);
+    s_newa.reserve(n * 4);
+    s_newm.reserve(n * 4);
+    s_newent.reserve(n * 4);
+    const uint64_t want = pow2_at_least(2 * n);
+    if (want > tcap) {
+        s_tkey.reserve(want * 8);
+        s_tmin.reserve(want * 4);
+        s_ta.reserve(want * 4);
+        s_tm.reserve(want * 4);
+        s_theld.reserve(want * 4);
+        s_tstate.reserve(want);
+        s_tslot.reserve(want * 8);
+        s_toc.reserve(want);
+        s_elist.reserve(want * 4);
+        MPZCH_CUDA(cudaMemsetAsync(s_tkey.p, 0xff, want * 8, stream));
+        MPZCH_CUDA(cudaMemsetAsync(s_tmin.p, 0xff, want * 4, stream));
+        MPZCH_CUDA(cudaMemsetAsync(s_tstate.p, 0, want, stream));
+        tcap = want;
+    }
+    s_reset.reserve(n * 8);
+    const size_t fl = ((n + 15) & ~15ull) + 16;
+    if (s_evflag.bytes < fl) {
+        s_evflag.reserve(fl);
+        MPZCH_CUDA(cudaMemsetAsync(s_evflag.p, 0, fl, stream));
+    }
+    s_evslot.reserve(n * 8);
+    s_blk.reserve(((n + kCompactChunk - 1) / kCompactChunk + 1) * 4);
+    MPZCH_CUDA(cudaStreamSynchronize(stream));
+}
+
+void Table::ensure_ordered_scratch(uint64_t n) {
+    const uint64_t want = pow2_at_least(2 * n);
+    if (want > ocap) {
+        o_key.reserve(want * 16);
+        o_min.reserve(want * 4);
+        o_entu.reserve(want * 4);
+        MPZCH_CUDA(cudaMemsetAsync(o_key.p, 0xff, want * 16, stream));
+        MPZCH_CUDA(cudaMemsetAsync(o_min.p, 0xff, want * 4, stream));
+        ocap = want;
+    }
+    o_posent.reserve(n * 4);
+    const size_t fl = ((n + 15) & ~15ull) + 16;
+    if (o_flag.bytes < fl) {
+        o_flag.reserve(fl);
+        MPZCH_CUDA(cudaMemsetAsync(o_flag.p, 0, fl, stream));
+    }
+    o_upos.reserve(n * 4);
+    o_ushard.reserve(n * 4);
+    o_umeta.reserve(n * 8);
+    o_uslot.reserve(n * 8);
+    o_uoc.reserve(n);
+    s_reset.reserve(n * 8);
+    if (s_evflag.bytes < fl) {
+        s_evflag.reserve(fl);
+        MPZCH_CUDA(cudaMemsetAsync(s_evflag.p, 0, fl, stream));
+    }
+    s_evslot.reserve(n * 8);
+    s_blk.reserve(((n + kCompactChunk - 1) / kCompactChunk + 1) * 4);
+    MPZCH_CUDA(cudaStreamSynchronize(stream));
+}
+
+namespace {
+
+struct EmitEvicted {
+    const uint64_t* evslot;
+    uint64_t* out;
+    uint64_t cap;
+    __device__ void operator()(uint64_t i, unsigned k) const {
+        if (out && k < cap) out[k] = evslot[i];
+    }
+};
+
+__global__ void k_dirty_flags(const uint64_t* __restrict__ row_gen, uint64_t total, uint64_t gen,
+                              uint8_t* __restrict__ flags) {
+    for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < total;
+         r += (uint64_t)gridDim.x * blockDim.x)
+        flags[r] = row_gen[r] > gen ? 1 : 0;
+}
+
+struct EmitIndex {
+    uint64_t* out;
+    uint64_t cap;
+    __device__ void operator()(uint64_t i, unsigned k) const {
+        if (k < cap) out[k] = i;
+    }
+};
+
+Policy parse_policy(const mpzch_policy* p) {
+    Policy pol;
+    if (!p) return pol;  // Disabled
+    if (p->mode < 0 || p->mode > 2) throw Error{MPZCH_EINVAL, "unknown eviction mode"};
+    pol.mode = p->mode;
+    if (pol.mode != kModeTtl) return pol;
+    // TtlPolicy::validate, eviction.cpp:8-18
+    if (p->default_ttl == 0) throw Error{MPZCH_EINVAL, "default TTL must be strictly positive"};
+    pol.default_ttl = p->default_ttl;
+    for (uint32_t i = 0; i < p->n_feat; ++i) {
+        if (p->feat_ttls[i] == 0)
+            throw Error{MPZCH_EINVAL, "per-feature TTL must be strictly positive (feature " +
+                                          std::to_string(p->feat_keys[i]) + ")"};
+        for (uint32_t j = 0; j < i; ++j)
+            if (p->feat_keys[j] == p->feat_keys[i])
+                throw Error{MPZCH_EINVAL, "duplicate feature in per-feature TTL map"};
+        pol.keys.push_back(p->feat_keys[i]);
+        pol.ttls.push_back(p->feat_ttls[i]);
+    }
+    return pol;
+}
+
+void require_valid_id(uint64_t id) {  // ids.hpp:25-31
+    if ((id >> 63) == 0) return;
+    throw Error{MPZCH_EINVAL, id == ~0ull ? "id is the empty-slot sentinel"
+                                          : "id exceeds the 63-bit ID space"};
+}
+
+// The batch core shared by the host- and device-buffer entry points.
+void run_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n, uint64_t now,
+               const Policy& pol, uint64_t* out_slots, uint8_t* out_oc, uint64_t* out_ev,
+               uint64_t ev_cap, uint64_t* out_ev_n, cudaStream_t st) {
+    if (n > 0xffffffffull) throw Error{MPZCH_ELENGTH, "batch exceeds 2^32 - 1 positions"};
+    if (out_ev_n) *out_ev_n = 0;
+    t.last = mpzch_batch_stats{};
+    if (n == 0) return;
+    BatchArgs a{};
+    a.ids = ids;
+    a.feats = feats;
+    a.n = n;
+    a.now = now;
+    a.pol = &pol;
+    a.out_slots = out_slots;
+    a.out_oc = out_oc;
+    a.out_ev = out_ev;
+    a.ev_cap = out_ev ? ev_cap : 0;
+    // one metadata value for the whole batch? (make_metadata, eviction.cpp:20-30)
+    a.uniform = true;
+    uint64_t ttl = 0;
+    if (pol.mode == kModeTtl) {
+        if (!feats) {
+            ttl = pol.ttl_for(0);
+        } else {
+            ttl = pol.default_ttl;
+            for (uint64_t v : pol.ttls)
+                if (v != pol.default_ttl) a.uniform = false;
+        }
+        if (a.uniform) {
+            a.overflow_all = ttl > ~0ull - now;
+            a.uniform_meta = a.overflow_all ? 0 : now + ttl;
+        }
+    } else {
+        a.uniform_meta = now;
+    }
+    const uint32_t nk = (uint32_t)pol.keys.size();
+    if (nk) {
+        t.s_featk.reserve(nk * 4);
+        t.s_featv.reserve(nk * 8);
+        MPZCH_CUDA(cudaMemcpyAsync(t.s_featk.p, pol.keys.data(), nk * 4, cudaMemcpyHostToDevice, st));
+        MPZCH_CUDA(cudaMemcpyAsync(t.s_featv.p, pol.ttls.data(), nk * 8, cudaMemcpyHostToDevice, st));
+        a.d_featk = t.s_featk.as<uint32_t>();
+        a.d_featv = t.s_featv.as<uint64_t>();
+    }
+    const bool fast = t.path_override == MPZCH_PATH_AUTO && t.hole_free &&
+                      pol.mode != kModeLru && a.uniform && n <= (1ull << 29);
+    if (fast) enqueue_fast_batch(t, a, st);
+    else enqueue_ordered_batch(t, a, st);
+    MPZCH_CUDA(cudaGetLastError());
+    MPZCH_CUDA(cudaMemcpyAsync(t.h_ctr, t.d_ctr, sizeof(BatchCounters), cudaMemcpyDeviceToHost, st));
+    MPZCH_CUDA(cudaStreamSynchronize(st));
+    const BatchCounters& c = *t.h_ctr;
+    if (c.err.too_many == 2) throw Error{MPZCH_ECUDA, "internal error: claim invariant violated"};
+    if (c.err.bad_pos != ~0ull)
+        throw Error{MPZCH_EINVAL, "invalid id at batch position " + std::to_string(c.err.bad_pos)};
+    if (a.overflow_all || c.err.overflow)
+        throw Error{MPZCH_EOVERFLOW, "TTL expiry overflows the 64-bit timestamp range"};
+    if (out_ev_n) *out_ev_n = c.evicted_count;
+    mpzch_batch_stats& s = t.last;
+    s.positions = n;
+    s.new_positions = fast ? c.new_count : 0;
+    s.new_ids = c.entry_count;
+    s.found = c.found;
+    s.inserted = c.inserted;
+    s.evicted = c.evicted;
+    s.collision = c.collision;
+    s.evicted_rows = c.evicted_count;
+    s.path = fast ? MPZCH_PATH_AUTO : MPZCH_PATH_ORDERED;
+}
+
+template <class F>
+mpzch_status guarded(F&& f) {
+    try {
+        f();
+        return MPZCH_OK;
+    } catch (const Error& e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = e.what();
+        return MPZCH_ENOMEM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return MPZCH_EINVAL;
+    }
+}
+
+}  // namespace
+
+void enqueue_compact_evicted(Table& t, uint64_t n, uint64_t* out_ev, uint64_t ev_cap, cudaStream_t st) {
+    EmitEvicted em{t.s_evslot.as<uint64_t>(), out_ev, ev_cap};
+    compact_flags(t.s_evflag.as<uint8_t>(), n, t.s_blk.as<unsigned>(), &t.d_ctr->evicted_count, true,
+                  em, st, t.launches);
+}
+
+}  // namespace mpzch_b200
+
+using namespace mpzch_b200;
+
+struct mpzch_table {
+    Table* t;
+};
+
+#define CHECK_T(t)                                                     \
+    do {                                                               \
+        if (!(t) || !(t)->t) {                                         \
+            g_last_error = "null table handle";                        \
+            return MPZCH_EINVAL;                                       \
+        }                                                              \
+    } while (0)
+
+extern "C" {
+
+const char* mpzch_last_error(void) { return g_last_error.c_str(); }
+
+const char* mpzch_build_info(void) { return MPZCH_BUILD_INFO; }
+
+mpzch_status mpzch_table_create(const uint64_t* caps, uint32_t num_shards, uint32_t max_probe,
+                                uint64_t seed, uint32_t dim, uint64_t init_seed, int device,
+                                mpzch_table** out) {
+    if (!out) {
+        g_last_error = "null output pointer";
+        return MPZCH_EINVAL;
+    }
+    *out = nullptr;
+    return guarded([&] {
+        if (num_shards && !caps) throw Error{MPZCH_EINVAL, "null capacities"};
+        Table* t = new Table(caps, num_shards, max_probe, seed, dim, init_seed, device);
+        *out = new mpzch_table{t};
+    });
+}
+
+mpzch_status mpzch_table_destroy(mpzch_table* t) {
+    if (!t) return MPZCH_OK;
+    delete t->t;
+    delete t;
+    return MPZCH_OK;
+}
+
+uint64_t mpzch_total_rows(const mpzch_table* t) { return t && t->t ? t->t->total : 0; }
+uint32_t mpzch_num_shards(const mpzch_table* t) { return t && t->t ? t->t->S : 0; }
+uint32_t mpzch_max_probe(const mpzch_table* t) { return t && t->t ? t->t->P : 0; }
+uint32_t mpzch_dim(const mpzch_table* t) { return t && t->t ? t->t->dim : 0; }
+
+mpzch_status mpzch_shard_layout(const mpzch_table* t, uint64_t* capacities, uint64_t* offsets) {
+    CHECK_T(t);
+    if (capacities) std::memcpy(capacities, t->t->caps.data(), t->t->S * 8);
+    if (offsets) std::memcpy(offsets, t->t->offsets.data(), (t->t->S + 1) * 8);
+    return MPZCH_OK;
+}
+
+mpzch_status mpzch_process_batch_device(mpzch_table* t, const uint64_t* ids, const uint32_t* feats,
+                                        uint64_t n, uint64_t now, const mpzch_policy* policy,
+                                        uint64_t* out_slots, uint8_t* out_oc, uint64_t* out_ev,
+                                        uint64_t ev_cap, uint64_t* out_ev_n, void* stream) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        DeviceGuard g(T.device);
+        const Policy pol = parse_policy(policy);
+        run_batch(T, ids, feats, n, now, pol, out_slots, out_oc, out_ev, ev_cap, out_ev_n,
+                  stream ? (cudaStream_t)stream : T.stream);
+    });
+}
+
+mpzch_status mpzch_process_batch(mpzch_table* t, const uint64_t* ids, const uint32_t* feats,
+                                 uint64_t n, uint64_t now, const mpzch_policy* policy,
+                                 uint64_t* out_slots, uint8_t* out_oc, uint64_t* out_ev,
+                                 uint64_t ev_cap, uint64_t* out_ev_n) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        DeviceGuard g(T.device);
+        const Policy pol = parse_policy(policy);
+        if (n > 0xffffffffull) throw Error{MPZCH_ELENGTH, "batch exceeds 2^32 - 1 positions"};
+        if (out_ev_n) *out_ev_n = 0;
+        if (n == 0) {
+            T.last = mpzch_batch_stats{};
+            return;
+        }
+        cudaStream_t st = T.stream;
+        T.s_ids.reserve(n * 8);
+        T.s_oslot.reserve(n * 8);
+        T.s_ooc.reserve(n);
+        MPZCH_CUDA(cudaMemcpyAsync(T.s_ids.p, ids, n * 8, cudaMemcpyHostToDevice, st));
+        const uint32_t* dfe = nullptr;
+        if (feats) {
+            T.s_feats.reserve(n * 4);
+            MPZCH_CUDA(cudaMemcpyAsync(T.s_feats.p, feats, n * 4, cudaMemcpyHostToDevice, st));
+            dfe = T.s_feats.as<uint32_t>();
+        }
+        uint64_t* dev_ev = nullptr;
+        if (out_ev && ev_cap) {
+            T.s_oev.reserve(std::min<uint64_t>(ev_cap, n) * 8);
+            dev_ev = T.s_oev.as<uint64_t>();
+        }
+        uint64_t nev = 0;
+        run_batch(T, T.s_ids.as<uint64_t>(), dfe, n, now, pol, T.s_oslot.as<uint64_t>(),
+                  T.s_ooc.as<uint8_t>(), dev_ev, std::min<uint64_t>(ev_cap, n), &nev, st);
+        MPZCH_CUDA(cudaMemcpyAsync(out_slots, T.s_oslot.p, n * 8, cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaMemcpyAsync(out_oc, T.s_ooc.p, n, cudaMemcpyDeviceToHost, st));
+        if (dev_ev && nev)
+            MPZCH_CUDA(cudaMemcpyAsync(out_ev, dev_ev, std::min(nev, ev_cap) * 8,
+                                       cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaStreamSynchronize(st));
+        if (out_ev_n) *out_ev_n = nev;
+    });
+}
+
+mpzch_status mpzch_lookup_device(const mpzch_table* t, const uint64_t* ids, uint64_t n,
+                                 uint64_t* out_slots, uint8_t* out_oc, void* stream) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        DeviceGuard g(T.device);
+        if (n == 0) return;
+        cudaStream_t st = stream ? (cudaStream_t)stream : T.stream;
+        BatchErr init{~0ull, 0, 0};
+        MPZCH_CUDA(cudaMemcpyAsync(&T.d_ctr->err, &init, sizeof init, cudaMemcpyHostToDevice, st));
+        run_lookup(T, ids, n, out_slots, out_oc, &T.d_ctr->err, st);
+        ++T.launches;
+        MPZCH_CUDA(cudaGetLastError());
+        MPZCH_CUDA(cudaMemcpyAsync(&T.h_ctr->err, &T.d_ctr->err, sizeof(BatchErr),
+                                   cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaStreamSynchronize(st));
+        if (T.h_ctr->err.bad_pos != ~0ull) {
+            uint64_t bad = 0;
+            MPZCH_CUDA(cudaMemcpy(&bad, ids + T.h_ctr->err.bad_pos, 8, cudaMemcpyDeviceToHost));
+            require_valid_id(bad);
+        }
+    });
+}
+
+mpzch_status mpzch_lookup(const mpzch_table* t, const uint64_t* ids, uint64_t n, uint64_t* out_slots,
+                          uint8_t* out_oc) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        DeviceGuard g(T.device);
+        if (n == 0) return;
+        cudaStream_t st = T.stream;
+        T.s_ids.reserve(n * 8);
+        T.s_oslot.reserve(n * 8);
+        T.s_ooc.reserve(n);
+        MPZCH_CUDA(cudaMemcpyAsync(T.s_ids.p, ids, n * 8, cudaMemcpyHostToDevice, st));
+        BatchErr init{~0ull, 0, 0};
+        MPZCH_CUDA(cudaMemcpyAsync(&T.d_ctr->err, &init, sizeof init, cudaMemcpyHostToDevice, st));
+        run_lookup(T, T.s_ids.as<uint64_t>(), n, T.s_oslot.as<uint64_t>(), T.s_ooc.as<uint8_t>(),
+                   &T.d_ctr->err, st);
+        ++T.launches;
+        MPZCH_CUDA(cudaGetLastError());
+        MPZCH_CUDA(cudaMemcpyAsync(&T.h_ctr->err, &T.d_ctr->err, sizeof(BatchErr),
+                                   cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaMemcpyAsync(out_slots, T.s_oslot.p, n * 8, cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaMemcpyAsync(out_oc, T.s_ooc.p, n, cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaStreamSynchronize(st));
+        if (T.h_ctr->err.bad_pos != ~0ull) require_valid_id(ids[T.h_ctr->err.bad_pos]);
+    });
+}
+
+mpzch_status mpzch_lookup_or_insert(mpzch_table* t, uint64_t id, uint32_t feature, uint64_t now,
+                                    const mpzch_policy* policy, uint64_t* out_slot,
+                                    uint8_t* out_oc) {
+    CHECK_T(t);
+    return guarded([&] {
+        const Policy pol = parse_policy(policy);
+        require_valid_id(id);  // shard_of -> require_valid_id, table.cpp:101
+        if (pol.mode == kModeTtl && pol.ttl_for(feature) > ~0ull - now)  // make_metadata :102
+            throw Error{MPZCH_EOVERFLOW, "TTL expiry overflows the 64-bit timestamp range"};
+        mpzch_policy p2{pol.mode, (uint32_t)pol.keys.size(), pol.default_ttl, pol.keys.data(),
+                        pol.ttls.data()};
+        uint64_t nev = 0;
+        const mpzch_status rc =
+            mpzch_process_batch(t, &id, &feature, 1, now, &p2, out_slot, out_oc, nullptr, 0, &nev);
+        if (rc != MPZCH_OK) throw Error{rc, g_last_error};
+    });
+}
+
+mpzch_status mpzch_copy_identities(const mpzch_table* t, uint64_t* out) {
+    CHECK_T(t);
+    return guarded([&] {
+        DeviceGuard g(t->t->device);
+        MPZCH_CUDA(cudaStreamSynchronize(t->t->stream));
+        MPZCH_CUDA(cudaMemcpy(out, t->t->ident, t->t->total * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+mpzch_status mpzch_copy_metadata(const mpzch_table* t, uint64_t* out) {
+    CHECK_T(t);
+    return guarded([&] {
+        DeviceGuard g(t->t->device);
+        MPZCH_CUDA(cudaStreamSynchronize(t->t->stream));
+        MPZCH_CUDA(cudaMemcpy(out, t->t->meta, t->t->total * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+static void check_rows(const Table& T, uint64_t row0, uint64_t nrows) {
+    if (T.dim == 0) throw Error{MPZCH_ELOGIC, "table has no embedding payload (dim = 0)"};
+    if (row0 > T.total || nrows > T.total - row0)
+        throw Error{MPZCH_ERANGE, "embedding row out of range"};
+}
+
+mpzch_status mpzch_copy_weights(const mpzch_table* t, uint64_t row0, uint64_t nrows, float* out) {
+    CHECK_T(t);
+    return guarded([&] {
+        const Table& T = *t->t;
+        check_rows(T, row0, nrows);
+        DeviceGuard g(T.device);
+        MPZCH_CUDA(cudaStreamSynchronize(T.stream));
+        MPZCH_CUDA(cudaMemcpy(out, T.weights + row0 * T.dim, nrows * T.dim * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+mpzch_status mpzch_copy_momentum(const mpzch_table* t, uint64_t row0, uint64_t nrows, float* out) {
+    CHECK_T(t);
+    return guarded([&] {
+        const Table& T = *t->t;
+        check_rows(T, row0, nrows);
+        DeviceGuard g(T.device);
+        MPZCH_CUDA(cudaStreamSynchronize(T.stream));
+        MPZCH_CUDA(cudaMemcpy(out, T.momentum + row0 * T.dim, nrows * T.dim * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+mpzch_status mpzch_copy_trained(const mpzch_table* t, uint8_t* out) {
+    CHECK_T(t);
+    return guarded([&] {
+        const Table& T = *t->t;
+        check_rows(T, 0, 0);
+        DeviceGuard g(T.device);
+        MPZCH_CUDA(cudaStreamSynchronize(T.stream));
+        MPZCH_CUDA(cudaMemcpy(out, T.trained, T.total, cudaMemcpyDeviceToHost));
+    });
+}
+
+mpzch_status mpzch_copy_row_generation(const mpzch_table* t, uint64_t* out) {
+    CHECK_T(t);
+    return guarded([&] {
+        DeviceGuard g(t->t->device);
+        MPZCH_CUDA(cudaStreamSynchronize(t->t->stream));
+        MPZCH_CUDA(cudaMemcpy(out, t->t->row_gen, t->t->total * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+mpzch_status mpzch_device_arrays(const mpzch_table* t, uint64_t** identities, uint64_t** metadata,
+                                 float** weights) {
+    CHECK_T(t);
+    if (identities) *identities = t->t->ident;
+    if (metadata) *metadata = t->t->meta;
+    if (weights) *weights = t->t->weights;
+    return MPZCH_OK;
+}
+
+mpzch_status mpzch_write_slots(mpzch_table* t, uint32_t shard, const uint64_t* local_slots,
+                               const uint64_t* identities, const uint64_t* metadata, uint64_t n) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        if (shard >= T.S) throw Error{MPZCH_ERANGE, "shard index out of range"};
+        std::vector<uint64_t> g(n), m(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            if (local_slots[i] >= T.caps[shard])
+                throw Error{MPZCH_ERANGE, "local slot exceeds shard capacity"};
+            g[i] = T.offsets[shard] + local_slots[i];
+        }
+        if (!n) return;
+        DeviceGuard gd(T.device);
+        uint64_t* buf = nullptr;
+        MPZCH_CUDA(cudaMalloc((void**)&buf, n * 24));
+        MPZCH_CUDA(cudaMemcpyAsync(buf, g.data(), n * 8, cudaMemcpyHostToDevice, T.stream));
+        MPZCH_CUDA(cudaMemcpyAsync(buf + n, identities, n * 8, cudaMemcpyHostToDevice, T.stream));
+        if (metadata) MPZCH_CUDA(cudaMemcpyAsync(buf + 2 * n, metadata, n * 8, cudaMemcpyHostToDevice, T.stream));
+        else {
+            // keep the existing metadata words
+            MPZCH_CUDA(cudaStreamSynchronize(T.stream));
+            for (uint64_t i = 0; i < n; ++i)
+                MPZCH_CUDA(cudaMemcpy(&m[i], T.meta + g[i], 8, cudaMemcpyDeviceToHost));
+            MPZCH_CUDA(cudaMemcpyAsync(buf + 2 * n, m.data(), n * 8, cudaMemcpyHostToDevice, T.stream));
+        }
+        launch_write_slots(T, buf, buf + n, buf + 2 * n, n, T.stream);
+        MPZCH_CUDA(cudaStreamSynchronize(T.stream));
+        cudaFree(buf);
+        T.hole_free = false;
+    });
+}
+
+mpzch_status mpzch_check_hole_free(mpzch_table* t, int* out) {
+    CHECK_T(t);
+    return guarded([&] {
+        DeviceGuard g(t->t->device);
+        t->t->hole_free = run_hole_check(*t->t);
+        if (out) *out = t->t->hole_free ? 1 : 0;
+    });
+}
+
+mpzch_status mpzch_write_row(mpzch_table* t, uint64_t row, const float* w, const float* m,
+                             uint8_t trained) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        check_rows(T, row, 1);
+        DeviceGuard g(T.device);
+        MPZCH_CUDA(cudaStreamSynchronize(T.stream));
+        if (w) MPZCH_CUDA(cudaMemcpy(T.weights + row * T.dim, w, T.dim * 4, cudaMemcpyHostToDevice));
+        if (m) MPZCH_CUDA(cudaMemcpy(T.momentum + row * T.dim, m, T.dim * 4, cudaMemcpyHostToDevice));
+        MPZCH_CUDA(cudaMemcpy(T.trained + row, &trained, 1, cudaMemcpyHostToDevice));
+        // a training write stamps the row dirty, as sgd_step does (table.cpp:170-176)
+        MPZCH_CUDA(cudaMemcpy(T.row_gen + row, &T.gen_clock, 8, cudaMemcpyHostToDevice));
+    });
+}
+
+mpzch_status mpzch_make_cursor(mpzch_table* t, uint64_t* out_generation) {
+    CHECK_T(t);
+    *out_generation = t->t->gen_clock++;  // MpzchTable::make_cursor, table.cpp:209-214
+    return MPZCH_OK;
+}
+
+mpzch_status mpzch_dirty_rows_since(const mpzch_table* t, uint64_t gen, uint64_t* out, uint64_t cap,
+                                    uint64_t* out_n) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        // table.cpp:216-225
+        if (gen == 0 || gen >= T.gen_clock)
+            throw Error{MPZCH_EINVAL, "stale or unknown publication cursor"};
+        DeviceGuard g(T.device);
+        cudaStream_t st = T.stream;
+        DevBuf flags, rows, blk;
+        flags.reserve(((T.total + 15) & ~15ull) + 16);
+        MPZCH_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes, st));
+        rows.reserve(std::max<uint64_t>(cap, 1) * 8);
+        blk.reserve(((T.total + kCompactChunk - 1) / kCompactChunk + 1) * 4);
+        k_dirty_flags<<<grid_for(T.total, 256), 256, 0, st>>>(T.row_gen, T.total, gen,
+                                                               flags.as<uint8_t>());
+        ++T.launches;
+        unsigned* d_n = &T.d_ctr->pad;
+        EmitIndex em{rows.as<uint64_t>(), cap};
+        compact_flags(flags.as<uint8_t>(), T.total, blk.as<unsigned>(), d_n, false, em, st, T.launches);
+        unsigned nn = 0;
+        MPZCH_CUDA(cudaMemcpyAsync(&nn, d_n, 4, cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaStreamSynchronize(st));
+        if (cap && out) MPZCH_CUDA(cudaMemcpy(out, rows.p, std::min<uint64_t>(nn, cap) * 8, cudaMemcpyDeviceToHost));
+        *out_n = nn;
+    });
+}
+
+mpzch_status mpzch_set_path(mpzch_table* t, int path) {
+    CHECK_T(t);
+    if (path != MPZCH_PATH_AUTO && path != MPZCH_PATH_ORDERED) {
+        g_last_error = "unknown execution path";
+        return MPZCH_EINVAL;
+    }
+    t->t->path_override = path;
+    return MPZCH_OK;
+}
+
+mpzch_status mpzch_last_stats(const mpzch_table* t, mpzch_batch_stats* out) {
+    CHECK_T(t);
+    *out = t->t->last;
+    return MPZCH_OK;
+}
+
+uint64_t mpzch_kernel_launches(const mpzch_table* t) { return t && t->t ? t->t->launches : 0; }
+
+}  // extern "C"

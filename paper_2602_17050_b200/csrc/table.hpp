@@ -1,0 +1,155 @@
+// table.hpp -- host-side state of one device-resident MPZCH table handle.
+//
+// Mirrors the reference's MpzchTable members (proj/include/mpzch/table.hpp:115-131)
+// with the arrays resident in HBM: one contiguous identity array and one
+// metadata array in global-row order (shard s owns [offset[s], offset[s+1])),
+// so a global row is a direct index and a probe window never leaves its
+// shard's segment except through the explicit wrap at the shard end.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/mpzch_b200.h"
+#include "common.cuh"
+
+namespace mpzch_b200 {
+
+// Thrown inside the library, mapped to a status + thread-local text at the C boundary.
+struct Error {
+    mpzch_status code;
+    std::string msg;
+};
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what);
+
+#define MPZCH_CUDA(call)                                   \
+    do {                                                   \
+        cudaError_t e_ = (call);                           \
+        if (e_ != cudaSuccess) ::mpzch_b200::throw_cuda(e_, #call); \
+    } while (0)
+
+// Reusable device scratch, grown monotonically (the reference keeps
+// thread_local BatchScratch for the same reason, batch_engine.cpp:112-129).
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t want);
+    template <class T> T* as() const { return static_cast<T*>(p); }
+    ~DevBuf();
+};
+
+// Small pinned block the host reads once per batch.
+struct BatchCounters {
+    BatchErr err;
+    unsigned int new_count;      // positions appended to the new list by the probe
+    unsigned int entry_count;    // distinct new ids (claim participants)
+    unsigned int reset_count;    // rows to reset
+    unsigned int evicted_count;  // canonical evicted-list length
+    unsigned long long found, inserted, evicted, collision;  // per position
+    unsigned int overflow_list;  // claim-log overflow (defensive)
+    unsigned int pad;
+};
+
+struct Policy {
+    int mode = 0;
+    uint64_t default_ttl = 0;
+    std::vector<uint32_t> keys;
+    std::vector<uint64_t> ttls;
+    uint64_t ttl_for(uint32_t f) const {
+        for (size_t i = 0; i < keys.size(); ++i)
+            if (keys[i] == f) return ttls[i];
+        return default_ttl;
+    }
+};
+
+class Table {
+public:
+    Table(const uint64_t* caps, uint32_t num_shards, uint32_t max_probe, uint64_t seed,
+          uint32_t dim, uint64_t init_seed, int device);
+    ~Table();
+
+    // layout (TableLayout, proj/include/mpzch/shard_router.hpp:13-29)
+    std::vector<uint64_t> caps, offsets;
+    uint64_t total = 0;
+    uint32_t S = 0, P = 0, dim = 0;
+    uint64_t seed = 0, init_seed = 0;
+    int device = 0;
+    uint64_t gen_clock = 1;  // MpzchTable::generation_clock_
+    bool hole_free = true;   // SURVEY A.2 invariant; false after raw imports
+    int path_override = MPZCH_PATH_AUTO;
+    mpzch_batch_stats last{};
+    uint64_t launches = 0;
+
+    // resident arrays
+    uint64_t* ident = nullptr;
+    uint64_t* meta = nullptr;
+    float* weights = nullptr;
+    float* momentum = nullptr;
+    uint8_t* trained = nullptr;
+    uint64_t* row_gen = nullptr;
+    ShardDev* d_shards = nullptr;
+    TableDev dev{};
+
+    cudaStream_t stream = nullptr;
+    BatchCounters* h_ctr = nullptr;  // pinned
+    BatchCounters* d_ctr = nullptr;
+
+    // scratch
+    DevBuf s_newpos, s_newa, s_newm, s_newent;      // new-list (fast path)
+    DevBuf s_tkey, s_tmin, s_ta, s_tm, s_theld, s_tstate, s_tslot, s_toc, s_elist;  // id table
+    uint64_t tcap = 0;                               // allocated id-table capacity (pow2)
+    DevBuf s_reset;                                  // rows to reset
+    DevBuf s_evflag, s_evslot, s_blk;                // evicted-list compaction
+    DevBuf s_ids, s_feats, s_oslot, s_ooc, s_oev;    // staging for host-buffer calls
+    DevBuf s_featk, s_featv;                         // per-feature TTL map
+    // ordered path
+    DevBuf o_key, o_min, o_posent, o_flag, o_upos, o_entu, o_ushard, o_umeta, o_uslot, o_uoc;
+    uint64_t ocap = 0;
+
+    void ensure_fast_scratch(uint64_t n);
+    void ensure_ordered_scratch(uint64_t n);
+};
+
+// kernel entry points (each .cu file), all enqueued on t.stream / stream
+void launch_init_table(Table& t);
+void launch_reset_rows(Table& t, const uint64_t* rows, const unsigned int* count, cudaStream_t st);
+void launch_write_slots(Table& t, const uint64_t* gslots, const uint64_t* ids, const uint64_t* metas,
+                        uint64_t n, cudaStream_t st);
+bool run_hole_check(Table& t);
+void run_lookup(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots,
+                uint8_t* out_oc, BatchErr* err, cudaStream_t st);
+
+struct BatchArgs {
+    const uint64_t* ids;
+    const uint32_t* feats;
+    uint64_t n;
+    uint64_t now;
+    uint64_t uniform_meta;      // meta value when every unique shares it
+    bool uniform;               // all metadata writes carry the same value
+    bool overflow_all;          // uniform TTL expiry overflows: validate, then fail
+    const Policy* pol;
+    const uint32_t* d_featk;    // per-feature map on device
+    const uint64_t* d_featv;
+    uint64_t* out_slots;
+    uint8_t* out_oc;
+    uint64_t* out_ev;
+    uint64_t ev_cap;
+};
+
+// enqueue the whole batch; counters land in t.h_ctr after the stream syncs
+void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st);
+void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st);
+void enqueue_compact_evicted(Table& t, uint64_t n, uint64_t* out_ev, uint64_t ev_cap, cudaStream_t st);
+
+inline unsigned grid_for(uint64_t n, unsigned block, unsigned max_blocks = 148u * 32u) {
+    uint64_t g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > max_blocks) g = max_blocks;
+    return (unsigned)g;
+}
+
+}  // namespace mpzch_b200

@@ -1,0 +1,438 @@
+"""GPU parity: the sm_100a path, called through the C-ABI, against the oracle.
+
+Every comparison is bit-exact (integer slots/outcomes/evicted lists, identity and
+metadata words, fp32 weights/momentum bit patterns, trained flags, row generations).
+Checkers: the reference's own recorded outputs (tests/golden/ref_streams.npz) and the
+C restatement (oracle/, itself pinned by tests/test_oracle.py).
+"""
+import numpy as np
+import pytest
+
+import paper_2602_17050_b200 as mz
+from test_oracle import _fixture, replay_fixture
+
+pytestmark = pytest.mark.gpu
+
+EMPTY = np.uint64((1 << 64) - 1)
+
+
+def pol(mode, dttl=0, pf=None):
+    if mode == 1:
+        return mz.EvictionPolicy.ttl(mz.TtlPolicy(dttl, dict(pf or {})))
+    return mz.EvictionPolicy.lru() if mode == 2 else mz.EvictionPolicy.disabled()
+
+
+def gpu_state(t, dim):
+    d = dict(ident=t.identities_all(), meta=t.metadata_all())
+    if dim:
+        d.update(weights=t.weights().view(np.uint32), momentum=t.momentum().view(np.uint32),
+                 trained=t.trained())
+    return d
+
+
+def oracle_state(o, dim):
+    d = dict(ident=o.identities_all(), meta=o.metadata_all())
+    if dim:
+        d.update(weights=o.weights().view(np.uint32), momentum=o.momentum().view(np.uint32),
+                 trained=o.trained())
+    return d
+
+
+def assert_same_state(a, b, tag=""):
+    for k in a:
+        assert (a[k] == b[k]).all(), f"{tag} state {k} differs"
+
+
+# ---------------------------------------------------------------- reference fixtures
+
+@pytest.mark.parametrize("path", ["auto", "ordered"])
+def test_replay_reference_fixtures(path):
+    z, man = _fixture()
+    paths_seen = set()
+
+    def make(c):
+        t = mz.MpzchTable(mz.TableConfig(c["caps"], c["max_probe"], int(c["seed"]), c["dim"],
+                                         int(c["init_seed"])))
+        t.set_path(path)
+        return t
+
+    def run(t, c, ids, f, now, dttl, pf):
+        r = t.process_batch(ids, now, pol(c["mode"], dttl, pf), f)
+        paths_seen.add(t.last_stats()["path"])
+        return r
+
+    def state(t, c):
+        d = dict(ident=t.identities_all(), meta=t.metadata_all())
+        if c["dim"]:
+            d.update(weights=t.weights(), momentum=t.momentum(), trained=t.trained())
+        return d
+
+    n = replay_fixture(make, run, state, z, man)
+    assert n == len(z["batches"])
+    if path == "auto":
+        assert "fast" in paths_seen  # the claim path really ran
+
+
+# ---------------------------------------------------------------- probe-core scenarios
+# proj/tests/test_probe_core.cpp, expressed through the table API on one shard: the
+# window is written raw (mpzch_write_slots), then one id is remapped.
+
+def find_id_with_home(oracle, target, cap, seed, start=1):
+    L = oracle.lib("port")
+    i = start
+    while True:
+        if L["home_slot"](i, cap, seed) == target:
+            return i
+        i += 1
+
+
+def scenario(oracle, cap, P, seed, mode, slots, idents, metas, id, now, meta_in):
+    """Run one probe on GPU (fast path when the raw window is hole-free) and on the
+    oracle probe core; compare result and both arrays."""
+    t = mz.MpzchTable(mz.TableConfig([cap], P, seed))
+    if len(slots):
+        t.write_slots(0, slots, idents, metas)
+    t.check_hole_free()
+    I = np.full(cap, EMPTY, dtype=np.uint64)
+    M = np.zeros(cap, dtype=np.uint64)
+    I[list(slots)] = idents
+    M[list(slots)] = metas
+    s, o, I2, M2 = oracle.probe(id, meta_in, now, I, M, cap, P, seed, mode)
+    p = pol(mode, meta_in - now if mode == 1 else 0)
+    gs, go, _ = t.process_batch(np.array([id], dtype=np.uint64), now, p)
+    assert (int(gs[0]), int(go[0])) == (s, o)
+    assert (t.identities_all() == I2).all() and (t.metadata_all() == M2).all()
+    return s, o
+
+
+def test_insert_and_refresh(oracle):
+    cap, P, seed = 32, 8, 11
+    p = find_id_with_home(oracle, 9, cap, seed)
+    assert scenario(oracle, cap, P, seed, 1, [], [], [], p, 10, 110) == (9, mz.INSERTED)
+    assert scenario(oracle, cap, P, seed, 1, [9], [p], [110], p, 50, 150) == (9, mz.FOUND)
+
+
+def test_probes_past_occupied(oracle):
+    cap, P, seed = 32, 8, 23
+    p = find_id_with_home(oracle, 4, cap, seed)
+    assert scenario(oracle, cap, P, seed, 0, [4, 5], [p + 1000, p + 2000], [0, 0], p, 7, 7) == (6, 1)
+
+
+def test_pass1_shields_existing_entry(oracle):
+    cap, P, seed, now = 64, 8, 5, 100
+    p = find_id_with_home(oracle, 20, cap, seed)
+    slots = [20, 21, 22, 23, 24, 25]
+    ids = [1_000_000 + o for o in range(5)] + [p]
+    metas = [now + 50, now - 1, now + 50, now + 50, now + 50, now + 1]
+    assert scenario(oracle, cap, P, seed, 1, slots, ids, metas, p, now, now + 10) == (25, mz.FOUND)
+
+
+def test_ttl_first_expired_and_strict_boundary(oracle):
+    cap, P, seed, now = 64, 8, 5, 100
+    p = find_id_with_home(oracle, 20, cap, seed)
+    slots = list(range(20, 28))
+    ids = [1_000_000 + o for o in range(8)]
+    metas = [now + 50] * 8
+    metas[2] = now - 1
+    metas[4] = now - 30
+    assert scenario(oracle, cap, P, seed, 1, slots, ids, metas, p, now, now + 10) == (22, mz.EVICTED)
+    cap, P, seed, now = 16, 2, 3, 50
+    p = find_id_with_home(oracle, 6, cap, seed)
+    assert scenario(oracle, cap, P, seed, 1, [6, 7], [p + 500, p + 600], [now, now + 1], p, now,
+                    now + 10)[1] == mz.COLLISION
+    assert scenario(oracle, cap, P, seed, 1, [6, 7], [p + 500, p + 600], [now - 1, now + 1], p, now,
+                    now + 10) == (6, mz.EVICTED)
+
+
+def test_expired_before_empty_and_full_window(oracle):
+    cap, P, seed, now = 32, 4, 9, 40
+    p = find_id_with_home(oracle, 12, cap, seed)
+    assert scenario(oracle, cap, P, seed, 1, [12], [p + 100], [now - 2], p, now, now + 5) == (12, 2)
+    cap, P, seed, now = 64, 4, 5, 100
+    p = find_id_with_home(oracle, 30, cap, seed)
+    assert scenario(oracle, cap, P, seed, 1, [30, 31, 32, 33], [2_000_000 + o for o in range(4)],
+                    [now + 5 + o for o in range(4)], p, now, now + 10) == (30, mz.COLLISION)
+    cap, P, seed, now = 16, 3, 2, 9
+    p = find_id_with_home(oracle, 5, cap, seed)
+    assert scenario(oracle, cap, P, seed, 0, [5, 6, 7], [3_000_000 + o for o in range(3)], [1] * 3, p,
+                    now, now) == (5, mz.COLLISION)
+
+
+def test_lru_oldest_and_ties(oracle):
+    cap, P, seed = 64, 3, 5
+    p = find_id_with_home(oracle, 40, cap, seed)
+    ids = [4_000_000 + o for o in range(3)]
+    assert scenario(oracle, cap, P, seed, 2, [40, 41, 42], ids, [5, 9, 3], p, 20, 20) == (42, 2)
+    assert scenario(oracle, cap, P, seed, 2, [40, 41, 42], ids, [4, 4, 7], p, 20, 20) == (40, 2)
+
+
+def test_wrap_around_and_hole_lookup(oracle):
+    cap, P, seed = 13, 4, 17
+    p = find_id_with_home(oracle, 11, cap, seed)
+    assert scenario(oracle, cap, P, seed, 0, [11, 12], [9_000_000, 9_000_001], [0, 0], p, 1, 1) == (0, 1)
+    # hole: id at offset 2 behind two EMPTY slots must still be Found by lookup
+    # (test_probe_core.cpp:113-121)
+    cap, P, seed = 16, 4, 77
+    q = find_id_with_home(oracle, 3, cap, seed)
+    t = mz.MpzchTable(mz.TableConfig([cap], P, seed))
+    t.write_slots(0, [5], [q], [0])
+    assert not t.check_hole_free()
+    s, o = t.lookup(np.array([q], dtype=np.uint64))
+    assert (int(s[0]), int(o[0])) == (5, mz.FOUND)
+    t2 = mz.MpzchTable(mz.TableConfig([cap], P, seed))
+    t2.write_slots(0, [3 + P], [q], [0])  # one past the window: invisible
+    assert int(t2.lookup(np.array([q], dtype=np.uint64))[1][0]) == mz.COLLISION
+
+
+# ---------------------------------------------------------------- table/batch scenarios
+# proj/tests/test_table_batch.cpp
+
+def test_duplicates_share_one_probe_and_cascade(oracle):
+    t = mz.MpzchTable(mz.TableConfig.even(32, 1, 4, 13))
+    L = oracle.lib("port")
+    p = find_id_with_home(oracle, 7, 32, 13)
+    q = find_id_with_home(oracle, 7, 32, 13, p + 1)
+    s, o, _ = t.process_batch(np.array([p, q, p, p], dtype=np.uint64), 1, mz.EvictionPolicy.disabled())
+    assert list(o) == [1, 1, 1, 1] and list(s) == [7, 8, 7, 7]
+
+
+def test_dedup_key_is_id_feature(oracle):
+    t = mz.MpzchTable(mz.TableConfig.even(64, 1, 4, 2))
+    ids = np.array([11, 11, 12, 11], dtype=np.uint64)
+    f = np.array([5, 2, 2, 5], dtype=np.uint32)
+    s, o, _ = t.process_batch(ids, 100, mz.EvictionPolicy.ttl(mz.TtlPolicy(1000, {5: 60})), f)
+    assert list(o) == [1, 0, 1, 1] and s[0] == s[1] == s[3]
+    # per-feature TTL, last writer (the (11, 2) unique, rank 1) wins the metadata word
+    assert t.metadata_all()[s[0]] == 1100 and t.metadata_all()[s[2]] == 1100
+
+
+def test_validation_before_mutation():
+    t = mz.MpzchTable(mz.TableConfig.even(16, 2, 2, 4))
+    with pytest.raises(mz.InvalidArgument, match="invalid id at batch position 1"):
+        t.process_batch(np.array([1, 1 << 63], dtype=np.uint64), 5, mz.EvictionPolicy.disabled())
+    assert (t.identities_all() == EMPTY).all()
+    with pytest.raises(mz.OverflowError_):
+        t.process_batch(np.array([1], dtype=np.uint64), (1 << 64) - 6,
+                        mz.EvictionPolicy.ttl(mz.TtlPolicy(1000)))
+    assert (t.identities_all() == EMPTY).all() and (t.metadata_all() == 0).all()
+    # invalid id wins over overflow (dedup validation runs first, batch_engine.cpp:149-158)
+    with pytest.raises(mz.InvalidArgument):
+        t.process_batch(np.array([1, (1 << 64) - 1], dtype=np.uint64), (1 << 64) - 6,
+                        mz.EvictionPolicy.ttl(mz.TtlPolicy(1000)))
+    with pytest.raises(mz.InvalidArgument, match="empty-slot sentinel"):
+        t.lookup(np.array([5, (1 << 64) - 1], dtype=np.uint64))
+    # an empty batch is a no-op
+    s, o, e = t.process_batch(np.zeros(0, dtype=np.uint64), 5, mz.EvictionPolicy.disabled())
+    assert s.size == 0 and e.size == 0
+
+
+def test_singleton_batch_equals_single_id_path(oracle):
+    cfg = mz.TableConfig.even(48, 4, 4, 31, 2, 7)
+    a, b = mz.MpzchTable(cfg), mz.MpzchTable(cfg)
+    p = mz.EvictionPolicy.ttl(mz.TtlPolicy(50))
+    rng = oracle.SplitMix64(88)
+    uni = oracle.distinct_ids(55, 0, 40)
+    now = 1
+    for _ in range(300):
+        now += rng.next_below(4)
+        i = int(uni[rng.next_below(40)])
+        f = rng.next_below(3)
+        s, o, _ = a.process_batch(np.array([i], dtype=np.uint64), now, p, np.array([f], dtype=np.uint32))
+        assert (int(s[0]), int(o[0])) == b.lookup_or_insert(i, f, now, p)
+    assert_same_state(gpu_state(a, 2), gpu_state(b, 2))
+
+
+def test_eviction_resets_row_bit_exact(oracle):
+    cfg = mz.TableConfig([4, 4], 4, 3, 4, 9)
+    t, twin = mz.MpzchTable(cfg), mz.MpzchTable(cfg)
+    fresh = twin.weights()
+    lru = mz.EvictionPolicy.lru()
+    L = oracle.lib("port")
+    res, cur = [], 1
+    while len(res) < 4:  # fill shard 0 (test_table_batch.cpp:80-88)
+        i = cur
+        while not (L["shard_of"](i, 2, 3) == 0 and L["home_slot"](i, 4, 3) == len(res) % 4):
+            i += 1
+        cur = i + 1
+        s, o = t.lookup_or_insert(i, 0, 10 + len(res), lru)
+        if o == mz.INSERTED:
+            res.append(i)
+    for r in range(4):
+        t.write_row(r, np.full(4, 0.5, np.float32), np.full(4, 0.25, np.float32), 1)
+    i = cur
+    while not (L["shard_of"](i, 2, 3) == 0 and L["home_slot"](i, 4, 3) == 2):
+        i += 1
+    s, o = t.lookup_or_insert(i, 0, 100, lru)
+    assert o == mz.EVICTED and s < 4
+    assert t.identities_all()[s] == i
+    assert t.trained()[s] == 0 and (t.momentum()[s] == 0).all()
+    assert (t.weights()[s].view(np.uint32) == fresh[s].view(np.uint32)).all()
+    assert (t.weights()[s] == oracle.draw_row(4, s, 9)).all()
+
+
+def test_dirty_tracking(oracle):
+    t = mz.MpzchTable(mz.TableConfig.even(8, 1, 2, 5, 2, 0))
+    ttl = mz.EvictionPolicy.ttl(mz.TtlPolicy(100))
+    c1 = t.make_cursor()
+    assert t.dirty_rows_since(c1).size == 0
+    a = find_id_with_home(oracle, 1, 8, 5)
+    s, o = t.lookup_or_insert(a, 0, 10, ttl)
+    assert o == mz.INSERTED and list(t.dirty_rows_since(c1)) == [s]
+    c2 = t.make_cursor()
+    assert t.lookup_or_insert(a, 0, 20, ttl)[1] == mz.FOUND
+    assert t.dirty_rows_since(c2).size == 0
+    with pytest.raises(mz.InvalidArgument, match="stale or unknown publication cursor"):
+        t.dirty_rows_since(999)
+
+
+def test_construction_errors():
+    with pytest.raises(mz.InvalidArgument, match="layout needs at least one shard"):
+        mz.MpzchTable(mz.TableConfig([], 1, 0))
+    with pytest.raises(mz.InvalidArgument, match="shard capacity must be >= 1"):
+        mz.MpzchTable(mz.TableConfig([4, 0], 1, 0))
+    with pytest.raises(mz.InvalidArgument, match="max_probe must satisfy"):
+        mz.MpzchTable(mz.TableConfig([4, 4], 5, 0))
+
+
+def test_init_weights_bit_exact(oracle):
+    for dim in (1, 3, 8, 100, 128):
+        t = mz.MpzchTable(mz.TableConfig.even(96, 3, 4, 1, dim, 0xDEADBEEF))
+        w = t.weights()
+        o = oracle.OracleTable(t.shard_capacities, 4, 1, dim, 0xDEADBEEF)
+        assert (w.view(np.uint32) == o.weights().view(np.uint32)).all(), dim
+
+
+# ---------------------------------------------------------------- randomized streams
+
+def run_stream(oracle, caps, P, seed, dim, init_seed, batches, mode, dttl=0, pf=None, path="auto",
+               check_state_every=0):
+    t = mz.MpzchTable(mz.TableConfig(caps, P, seed, dim, init_seed))
+    t.set_path(path)
+    o = oracle.OracleTable(caps, P, seed, dim, init_seed)
+    p = pol(mode, dttl, pf)
+    for bi, (ids, f, now) in enumerate(batches):
+        gs, go, ge = t.process_batch(ids, now, p, f)
+        os_, oo, oe = o.process_batch(ids, now, mode, dttl, pf, f)
+        assert (gs == os_).all(), f"slots differ at batch {bi}"
+        assert (go == oo).all(), f"outcomes differ at batch {bi}"
+        assert (ge == oe).all(), f"evicted list differs at batch {bi}"
+        if check_state_every and bi % check_state_every == 0:
+            assert_same_state(gpu_state(t, dim), oracle_state(o, dim), f"batch {bi}")
+    assert_same_state(gpu_state(t, dim), oracle_state(o, dim), "final")
+    return t
+
+
+def test_c1_shape_stream(oracle):
+    """C1 at full table size (2^20 rows, P=128, 64K-position batches over a 0.8*2^20 pool,
+    Disabled) for 24 batches: cold fill through ~90% hits."""
+    import workloads
+    rows = 1 << 20
+    pool = int(0.8 * rows)
+    ids_pool = oracle.distinct_ids(1, 0, pool)
+    idx = workloads.uniform_stream(1, pool, 65536, 24)
+    batches = [(ids_pool[x], None, b + 1) for b, x in enumerate(idx)]
+    t = run_stream(oracle, [rows], 128, 7, 0, 0, batches, 0)
+    assert t.last_stats()["path"] == "fast"
+
+
+def test_c1_multi_shard_with_features(oracle):
+    import workloads
+    rows = 1 << 18
+    pool = int(0.9 * rows)
+    ids_pool = oracle.distinct_ids(11, 0, pool)
+    idx = workloads.uniform_stream(11, pool, 32768, 12)
+    rng = np.random.default_rng(3)
+    batches = [(ids_pool[x], rng.integers(0, 3, x.size).astype(np.uint32), b + 1)
+               for b, x in enumerate(idx)]
+    run_stream(oracle, mz.even_capacities(rows, 8), 32, 7, 0, 0, batches, 0)
+
+
+@pytest.mark.parametrize("path", ["auto", "ordered"])
+def test_ttl_eviction_reset_stream(oracle, path):
+    """C4 shape at reduced size: prefill 0.8 at now=1 (TTL 3600), then fresh ids at
+    now = 10000 + 600 t evict expired rows; dim 16 resets must be bit-exact."""
+    rows = 1 << 16
+    caps = mz.even_capacities(rows, 8)
+    pre = oracle.distinct_ids(4, 0, int(0.8 * rows))
+    fresh = oracle.distinct_ids(41, 0, 1 << 17)
+    rng = np.random.default_rng(5)
+    batches = [(pre[i:i + 8192], None, 1) for i in range(0, pre.size, 8192)]
+    for t_ in range(6):
+        batches.append((fresh[rng.integers(0, fresh.size, 16384)], None, 10000 + 600 * t_))
+    run_stream(oracle, caps, 128, 7, 16, 11, batches, 1, 3600, None, path)
+
+
+def test_ttl_mixed_hits_and_expiry(oracle):
+    """Zipf-like reuse with a short TTL: hits on live slots, refreshes of expired own
+    slots contested by lower-rank new ids (the owner path), evictions, collisions."""
+    rows = 1 << 12
+    uni = oracle.distinct_ids(2, 0, rows * 2)
+    rng = np.random.default_rng(9)
+    w = 1.0 / np.arange(1, uni.size + 1) ** 1.05
+    w /= w.sum()
+    batches = []
+    for b in range(40):
+        batches.append((uni[rng.choice(uni.size, 3000, p=w)], None, 1000 + 7 * b))
+    run_stream(oracle, mz.even_capacities(rows, 2), 16, 3, 0, 0, batches, 1, 20, None,
+               check_state_every=5)
+
+
+def test_lru_dense_stream(oracle):
+    rows = 1 << 10
+    uni = oracle.distinct_ids(8, 0, rows * 3)
+    rng = np.random.default_rng(2)
+    batches = [(uni[rng.integers(0, uni.size, 700)], rng.integers(0, 2, 700).astype(np.uint32),
+                5 + b // 2) for b in range(30)]
+    run_stream(oracle, [rows // 2, rows // 2], 8, 5, 4, 1, batches, 2)
+
+
+def test_lookup_matches_oracle(oracle):
+    rows = 1 << 16
+    caps = mz.even_capacities(rows, 4)
+    t = mz.MpzchTable(mz.TableConfig(caps, 64, 9))
+    o = oracle.OracleTable(caps, 64, 9)
+    ids = oracle.distinct_ids(3, 0, int(0.95 * rows))
+    for i in range(0, ids.size, 8192):
+        t.process_batch(ids[i:i + 8192], 1, mz.EvictionPolicy.disabled())
+        o.process_batch(ids[i:i + 8192], 1, 0)
+    q = np.concatenate([ids[::3], oracle.distinct_ids(3, ids.size, 20000)])
+    gs, go = t.lookup(q)
+    os_, oo = o.lookup(q)
+    assert (gs == os_).all() and (go == oo).all()
+    assert (t.identities_all() == o.identities_all()).all()
+
+
+def test_hole_import_uses_exact_path(oracle):
+    """After a raw import with a hole, remaps follow the full two-pass semantics
+    (pass 2 inserts at the EMPTY in front of an existing copy, probe_core.cpp:89-101)."""
+    cap, P, seed = 16, 4, 77
+    q = find_id_with_home(oracle, 3, cap, seed)
+    t = mz.MpzchTable(mz.TableConfig([cap], P, seed))
+    t.write_slots(0, [5], [q], [0])
+    o = oracle.OracleTable([cap], P, seed)
+    oracle_I = o  # port table: emulate the raw write through probe on arrays instead
+    I = np.full(cap, EMPTY, dtype=np.uint64)
+    M = np.zeros(cap, dtype=np.uint64)
+    I[5] = q
+    s, oc, I2, M2 = oracle.probe(q, 3, 3, I, M, cap, P, seed, 0)
+    gs, go, _ = t.process_batch(np.array([q], dtype=np.uint64), 3, mz.EvictionPolicy.disabled())
+    assert (int(gs[0]), int(go[0])) == (s, oc) == (3, mz.INSERTED)
+    assert (t.identities_all() == I2).all()
+
+
+def test_device_buffer_entry_point(oracle):
+    import torch
+    rows = 1 << 14
+    t = mz.MpzchTable(mz.TableConfig.even(rows, 2, 32, 5))
+    o = oracle.OracleTable(mz.even_capacities(rows, 2), 32, 5)
+    ids = oracle.distinct_ids(6, 0, 9000)
+    d = torch.from_numpy(ids.view(np.int64)).cuda()
+    slots = torch.empty(ids.size, dtype=torch.int64, device="cuda")
+    oc = torch.empty(ids.size, dtype=torch.uint8, device="cuda")
+    ev = torch.empty(ids.size, dtype=torch.int64, device="cuda")
+    nev = t.process_batch_device(d, 1, mz.EvictionPolicy.disabled(), None, slots, oc, ev)
+    torch.cuda.synchronize()
+    s, oo, e = o.process_batch(ids, 1, 0)
+    assert nev == 0 and (slots.cpu().numpy().view(np.uint64) == s).all()
+    assert (oc.cpu().numpy() == oo).all()
+    assert t.kernel_launches() > 0
