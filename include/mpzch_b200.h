@@ -163,6 +163,23 @@ mpzch_status mpzch_make_cursor(mpzch_table* t, uint64_t* out_generation);
 mpzch_status mpzch_dirty_rows_since(const mpzch_table* t, uint64_t generation, uint64_t* out,
                                     uint64_t cap, uint64_t* out_n);
 
+/* ---- in-library CUDA-event profiling (bench evidence).  When on, every batch records
+ * events on its own launch stream around the probe kernel, the claim/commit kernels
+ * and the whole batch, and the probe kernel counts the 32-byte sectors it reads. */
+typedef struct mpzch_profile {
+    uint64_t batches;       /* profiled batches since mpzch_set_profiling(t, 1) */
+    uint64_t probe_launches;
+    double probe_ms;        /* sum of probe-kernel event times */
+    double claim_ms;        /* dedup + claim + commit kernels */
+    double tail_ms;         /* finalize, metadata, reset, evicted list, cleanup */
+    double batch_ms;        /* first to last kernel of each batch */
+    uint64_t probe_sectors; /* 32-byte identity/metadata sectors the probe read */
+    uint64_t probe_bytes;   /* algorithmic bytes of the probe kernel (sectors + position I/O) */
+    uint64_t batch_bytes;   /* algorithmic bytes of the whole batch (SURVEY 8d terms) */
+} mpzch_profile;
+mpzch_status mpzch_set_profiling(mpzch_table* t, int on);
+mpzch_status mpzch_get_profile(const mpzch_table* t, mpzch_profile* out);
+
 /* ---- execution control / introspection */
 mpzch_status mpzch_set_path(mpzch_table* t, int path);
 mpzch_status mpzch_last_stats(const mpzch_table* t, mpzch_batch_stats* out);

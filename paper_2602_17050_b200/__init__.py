@@ -98,6 +98,14 @@ class _Stats(ctypes.Structure):
                 ("path", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
+class _Profile(ctypes.Structure):
+    _fields_ = [("batches", ctypes.c_uint64), ("probe_launches", ctypes.c_uint64),
+                ("probe_ms", ctypes.c_double), ("claim_ms", ctypes.c_double),
+                ("tail_ms", ctypes.c_double), ("batch_ms", ctypes.c_double),
+                ("probe_sectors", ctypes.c_uint64), ("probe_bytes", ctypes.c_uint64),
+                ("batch_bytes", ctypes.c_uint64)]
+
+
 _LIB = None
 
 _u64p = ctypes.POINTER(ctypes.c_uint64)
@@ -142,6 +150,8 @@ _SIGS = {
     "mpzch_make_cursor": (ctypes.c_int, [_vp, _u64p]),
     "mpzch_dirty_rows_since": (ctypes.c_int, [_vp, ctypes.c_uint64, _vp, ctypes.c_uint64, _u64p]),
     "mpzch_set_path": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "mpzch_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "mpzch_get_profile": (ctypes.c_int, [_vp, ctypes.POINTER(_Profile)]),
     "mpzch_last_stats": (ctypes.c_int, [_vp, ctypes.POINTER(_Stats)]),
     "mpzch_kernel_launches": (ctypes.c_uint64, [_vp]),
     "mpzch_last_error": (ctypes.c_char_p, []),
@@ -447,6 +457,15 @@ class MpzchTable:
         d = {k: getattr(s, k) for k, _ in _Stats._fields_}
         d["path"] = "fast" if s.path == 0 else "ordered"
         return d
+
+    def set_profiling(self, on: bool = True):
+        """CUDA events on the launch stream around the probe kernel / claims / whole batch."""
+        _check(self._lib.mpzch_set_profiling(self._h, int(on)))
+
+    def profile(self) -> dict:
+        p = _Profile()
+        _check(self._lib.mpzch_get_profile(self._h, ctypes.byref(p)))
+        return {k: getattr(p, k) for k, _ in _Profile._fields_}
 
     def kernel_launches(self) -> int:
         return int(self._lib.mpzch_kernel_launches(self._h))

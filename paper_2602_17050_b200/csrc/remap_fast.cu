@@ -70,7 +70,7 @@ __global__ void k_init_counters(BatchCounters* c) {
 // Only called under TTL; reads one sector per 4 slots.
 __device__ __forceinline__ uint32_t first_expired(const uint64_t* __restrict__ meta, uint64_t base,
                                                   uint64_t h, uint64_t cap, uint32_t limit,
-                                                  uint64_t now) {
+                                                  uint64_t now, unsigned long long& nsec) {
     uint32_t off = 0;
     uint64_t g = base + h;
     const uint64_t end = base + cap;
@@ -78,6 +78,7 @@ __device__ __forceinline__ uint32_t first_expired(const uint64_t* __restrict__ m
         const uint64_t a4 = g & ~3ull;
         uint64_t w0, w1, w2, w3;
         ld_sector(meta + a4, w0, w1, w2, w3);
+        ++nsec;
         do {
             if (pick4((uint32_t)(g - a4), w0, w1, w2, w3) < now) return off;
             ++off;
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(256) k_probe(TableDev t, const uint64_t* __res
                                                uint32_t* __restrict__ newm) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const unsigned lane = lane_id();
-    unsigned long long my_found = 0, my_coll = 0;
+    unsigned long long my_found = 0, my_coll = 0, my_isec = 0, my_msec = 0;
     for (uint64_t base_i = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base_i < n;
          base_i += stride) {
         const uint64_t i = base_i + lane;
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(256) k_probe(TableDev t, const uint64_t* __res
                     const uint64_t a4 = g & ~3ull;
                     uint64_t w0, w1, w2, w3;
                     ld_sector(t.ident + a4, w0, w1, w2, w3);
+                    ++my_isec;
                     do {
                         const uint64_t v = pick4((uint32_t)(g - a4), w0, w1, w2, w3);
                         if (v == id) { found = off; gf = g; break; }
@@ -143,6 +145,7 @@ __global__ void __launch_bounds__(256) k_probe(TableDev t, const uint64_t* __res
                     }
                 } else {  // TTL, one meta value per batch
                     if (found != kNone32) {
+                        ++my_msec;
                         if (__ldg(t.meta + gf) >= now) {  // live: nobody can take it this batch
                             out_slots[i] = gf;
                             out_oc[i] = kFound;
@@ -150,11 +153,11 @@ __global__ void __launch_bounds__(256) k_probe(TableDev t, const uint64_t* __res
                         } else {  // expired own slot: contested by lower-rank new ids
                             is_new = true;
                             m_off = found;
-                            a_off = first_expired(t.meta, base, h, cap, found, now);
+                            a_off = first_expired(t.meta, base, h, cap, found, now, my_msec);
                         }
                     } else {
                         const uint32_t lim = empty != kNone32 ? empty : t.P;
-                        const uint32_t x = first_expired(t.meta, base, h, cap, lim, now);
+                        const uint32_t x = first_expired(t.meta, base, h, cap, lim, now, my_msec);
                         if (x < lim || empty != kNone32) {
                             is_new = true;
                             a_off = x;
@@ -185,10 +188,14 @@ __global__ void __launch_bounds__(256) k_probe(TableDev t, const uint64_t* __res
     for (int o = 16; o; o >>= 1) {
         my_found += __shfl_xor_sync(0xffffffffu, my_found, o);
         my_coll += __shfl_xor_sync(0xffffffffu, my_coll, o);
+        my_isec += __shfl_xor_sync(0xffffffffu, my_isec, o);
+        my_msec += __shfl_xor_sync(0xffffffffu, my_msec, o);
     }
     if (lane == 0) {
         if (my_found) atomicAdd(&ctr->found, my_found);
         if (my_coll) atomicAdd(&ctr->collision, my_coll);
+        if (my_isec) atomicAdd(&ctr->id_sectors, my_isec);
+        if (my_msec) atomicAdd(&ctr->meta_sectors, my_msec);
     }
 }
 
@@ -455,6 +462,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     const unsigned gW = grid_for(n, B, 148u * 8u);  // count-driven kernels
     k_init_counters<<<1, 32, 0, st>>>(t.d_ctr);
     ++t.launches;
+    if (t.profiling) cudaEventRecord(t.ev[0], st);
     if (a.pol->mode == kModeTtl)
         k_probe<kModeTtl><<<gN, B, 0, st>>>(t.dev, a.ids, n, a.now, t.d_ctr, a.out_slots, a.out_oc,
                                             t.s_newpos.as<uint32_t>(), t.s_newa.as<uint32_t>(),
@@ -464,6 +472,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
                                                  a.out_oc, t.s_newpos.as<uint32_t>(),
                                                  t.s_newa.as<uint32_t>(), t.s_newm.as<uint32_t>());
     ++t.launches;
+    if (t.profiling) cudaEventRecord(t.ev[1], st);
     if (a.overflow_all) return;  // validation only; the host reports the error
     k_dedup<<<gW, B, 0, st>>>(a.ids, t.d_ctr, t.tcap, t.s_newpos.as<uint32_t>(),
                               t.s_newa.as<uint32_t>(), t.s_newm.as<uint32_t>(),
@@ -493,6 +502,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
             t.s_reset.as<uint64_t>(), t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>());
     }
     t.launches += 2;
+    if (t.profiling) cudaEventRecord(t.ev[2], st);
     k_finalize<<<gW, B, 0, st>>>(t.d_ctr, a.feats, t.s_newpos.as<uint32_t>(),
                                  t.s_newent.as<uint32_t>(), t.s_tmin.as<unsigned>(),
                                  t.s_tslot.as<uint64_t>(), t.s_toc.as<uint8_t>(), a.out_slots,
@@ -504,6 +514,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     k_cleanup<<<gW, B, 0, st>>>(t.d_ctr, t.s_elist.as<uint32_t>(), t.s_tkey.as<uint64_t>(),
                                 t.s_tmin.as<unsigned>(), t.s_tstate.as<uint8_t>());
     ++t.launches;
+    if (t.profiling) cudaEventRecord(t.ev[3], st);
 }
 
 }  // namespace mpzch_b200

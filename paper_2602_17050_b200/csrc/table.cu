@@ -142,6 +142,8 @@ Table::~Table() {
     cudaFree(d_shards);
     cudaFree(d_ctr);
     if (h_ctr) cudaFreeHost(h_ctr);
+    for (auto& e : ev)
+        if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -331,6 +333,32 @@ void run_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n,
     s.collision = c.collision;
     s.evicted_rows = c.evicted_count;
     s.path = fast ? MPZCH_PATH_AUTO : MPZCH_PATH_ORDERED;
+    if (t.profiling && fast) {
+        float a01 = 0, a12 = 0, a23 = 0, a03 = 0;
+        MPZCH_CUDA(cudaEventElapsedTime(&a01, t.ev[0], t.ev[1]));
+        MPZCH_CUDA(cudaEventElapsedTime(&a12, t.ev[1], t.ev[2]));
+        MPZCH_CUDA(cudaEventElapsedTime(&a23, t.ev[2], t.ev[3]));
+        MPZCH_CUDA(cudaEventElapsedTime(&a03, t.ev[0], t.ev[3]));
+        mpzch_profile& p = t.prof;
+        p.batches += 1;
+        p.probe_launches += 1;
+        p.probe_ms += a01;
+        p.claim_ms += a12;
+        p.tail_ms += a23;
+        p.batch_ms += a03;
+        const uint64_t sectors = c.id_sectors + c.meta_sectors;
+        const uint64_t n_final = n - c.new_count;
+        p.probe_sectors += sectors;
+        // probe kernel: sectors read + 8 B id per position + 9 B result per final
+        // position + 12 B new-list record per new position
+        p.probe_bytes += 32 * sectors + 8 * n + 9 * n_final + 12ull * c.new_count;
+        // whole batch (SURVEY 8d terms, counted per position): probe reads, 8 B id in,
+        // 9 B result out, one metadata sector written per position, one identity sector +
+        // 8 B row_generation per Inserted/Evicted position, 8*dim+1 B per reset row
+        p.batch_bytes += 32 * sectors + 8 * n + 9 * n + 32 * n +
+                         40ull * (c.inserted + c.evicted) +
+                         (uint64_t)c.reset_count * (8ull * t.dim + 1);
+    }
 }
 
 template <class F>
@@ -707,6 +735,24 @@ mpzch_status mpzch_dirty_rows_since(const mpzch_table* t, uint64_t gen, uint64_t
         if (cap && out) MPZCH_CUDA(cudaMemcpy(out, rows.p, std::min<uint64_t>(nn, cap) * 8, cudaMemcpyDeviceToHost));
         *out_n = nn;
     });
+}
+
+mpzch_status mpzch_set_profiling(mpzch_table* t, int on) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        DeviceGuard g(T.device);
+        if (on && !T.ev[0])
+            for (auto& e : T.ev) MPZCH_CUDA(cudaEventCreate(&e));
+        T.profiling = on != 0;
+        T.prof = mpzch_profile{};
+    });
+}
+
+mpzch_status mpzch_get_profile(const mpzch_table* t, mpzch_profile* out) {
+    CHECK_T(t);
+    *out = t->t->prof;
+    return MPZCH_OK;
 }
 
 mpzch_status mpzch_set_path(mpzch_table* t, int path) {

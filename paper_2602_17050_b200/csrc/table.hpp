@@ -52,6 +52,7 @@ struct BatchCounters {
     unsigned long long found, inserted, evicted, collision;  // per position
     unsigned int overflow_list;  // claim-log overflow (defensive)
     unsigned int pad;
+    unsigned long long id_sectors, meta_sectors;  // sectors the probe kernel read
 };
 
 struct Policy {
@@ -83,6 +84,9 @@ public:
     int path_override = MPZCH_PATH_AUTO;
     mpzch_batch_stats last{};
     uint64_t launches = 0;
+    bool profiling = false;
+    mpzch_profile prof{};
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
     // resident arrays
     uint64_t* ident = nullptr;
