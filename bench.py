@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""bench.py -- device-timed remapped IDs/s of the MPZCH batched remap path on B200.
+
+Workload (the north star's headline): a 1B-slot table (2^30 rows, S=8
+logical shards, max_probe=128, seed 7, eviction Disabled) prefilled through the API to
+load 0.8 with DistinctIdStream(5)[0, N_pre), then batches of 4,194,304 positions:
+90% uniform over the prefilled ids, 10% fresh ids (N_pre + k).  A step = one
+process_batch over one batch.  IDs/s counts input positions (duplicates included, as
+run_latency_bench does, proj/src/experiments.cpp:325,347).
+
+  value     device-resident inputs, CUDA events on the launch stream, K steps
+  e2e       the host-buffer C-ABI call (mpzch_process_batch) from pinned host memory:
+            H2D ids + D2H slots/outcomes inside the timed region
+  roofline  the probe kernel (dominant): algorithmic bytes (32-byte sectors it must read
+            + per-position I/O) / its CUDA-event launch time, vs MEASURED_PEAKS hbm_gbs
+  cpu_baseline / --impl reference
+            the REFERENCE library (oracle/_ref, /root/reference/proj/src compiled by
+            oracle/Makefile, OpenMP over all host cores) on a bounded sample of the same
+            workload (2^25 rows, same S/P/load/mix/batch size).
+
+Multi-GPU (torchrun, N>1): each rank remaps its own 4M-position batches against its own
+1B-slot table (replicas, weak scaling); ranks share nothing on the data path.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GOLD = -7046029254386353131          # 0x9E3779B97F4A7C15 as int64
+M1 = -49064778989728563              # 0xff51afd7ed558ccd
+M2 = -4265267296055464877            # 0xc4ceb9fe1a85ec53
+S1 = -4658895280553007687            # 0xBF58476D1CE4E5B9
+S2 = -7723592293110705685            # 0x94D049BB133111EB
+LOW31 = (1 << 31) - 1
+
+
+def _i64(v):
+    v &= (1 << 64) - 1
+    return v - (1 << 64) if v >= (1 << 63) else v
+
+
+def mix64_t(x, seed: int):
+    """ids.hpp:35-43 on int64 tensors (wrapping multiply; logical shifts via masks)."""
+    x = x ^ _i64(seed)
+    x = x ^ ((x >> 33) & ((1 << 31) - 1))
+    x = x * M1
+    x = x ^ ((x >> 33) & ((1 << 31) - 1))
+    x = x * M2
+    return x ^ ((x >> 33) & ((1 << 31) - 1))
+
+
+def distinct_ids_t(seed: int, idx):
+    """DistinctIdStream::at, rng.hpp:40-50, on an int64 index tensor."""
+    left = (idx >> 31) & LOW31
+    right = idx & LOW31
+    for r in range(4):
+        f = mix64_t(right | (r << 32), seed) & LOW31
+        left, right = right, left ^ f
+    return (left << 31) | right
+
+
+def splitmix_t(seed: int, k):
+    """k-th (0-based) output of SplitMix64(seed), rng.hpp:15-21."""
+    z = (k + 1) * GOLD + _i64(seed)
+    z = (z ^ ((z >> 30) & ((1 << 34) - 1))) * S1
+    z = (z ^ ((z >> 27) & ((1 << 37) - 1))) * S2
+    return z ^ ((z >> 31) & ((1 << 33) - 1))
+
+
+def batch_indices(torch, device, pool: int, batch: int, b: int, fresh_base: int, seed: int,
+                  fresh_pct: int = 10):
+    """Stream index of each position of batch b: with probability fresh_pct% a fresh index
+    (pool + running count), else uniform over [0, pool).  Two SplitMix64 draws per position
+    (coin, pick); returns (indices, fresh count)."""
+    k = torch.arange(2 * batch * b, 2 * batch * (b + 1), dtype=torch.int64, device=device)
+    d = splitmix_t(seed, k) & ((1 << 63) - 1)
+    coin = d[0::2] % 100
+    pick = d[1::2] % pool
+    fresh = coin < fresh_pct
+    rank = torch.cumsum(fresh.to(torch.int64), 0) - 1
+    idx = torch.where(fresh, fresh_base + rank, pick)
+    return idx, int(fresh.sum().item())
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per probe launch from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_probe_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------ workload
+
+ROWS = 1 << 30
+SHARDS = 8
+MAX_PROBE = 128
+TABLE_SEED = 7
+ID_SEED = 5
+BATCH = 4 * 1024 * 1024
+SAMPLER_SEED = 0x5CA1AB1E
+CPU_ROWS = 1 << 25
+
+
+def prefill_count(rows):
+    return int(0.8 * rows)
+
+
+def run_reference_sample(steps: int, warmup: int, rows: int = CPU_ROWS, log=print):
+    """The reference library (oracle/_ref, OpenMP process_batch) on the bounded sample."""
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    kind = "reference" if pyoracle.available("reference") else "port"
+    L = pyoracle.lib(kind)
+    cores = os.cpu_count() or 1
+    if kind == "reference":
+        L["set_threads"](cores)
+    else:
+        cores = 1
+    import paper_2602_17050_b200 as mz
+    caps = mz.even_capacities(rows, SHARDS)
+    t = pyoracle.OracleTable(caps, MAX_PROBE, TABLE_SEED, kind=kind)
+    npre = prefill_count(rows)
+    t0 = time.perf_counter()
+    for a in range(0, npre, BATCH):
+        ids = distinct_ids_t(ID_SEED, torch.arange(a, min(a + BATCH, npre), dtype=torch.int64))
+        t.process_batch(ids.numpy().view(np.uint64), 1, 0)
+    log(f"[ref] prefill {npre} ids in {time.perf_counter() - t0:.1f}s ({kind}, {cores} threads)")
+    fresh_base = npre
+    times = []
+    for b in range(warmup + steps):
+        idx, nf = batch_indices(torch, "cpu", npre, BATCH, b, fresh_base, SAMPLER_SEED)
+        fresh_base += nf
+        ids = distinct_ids_t(ID_SEED, idx).numpy().view(np.uint64)
+        s = time.perf_counter()
+        t.process_batch(ids, 2 + b, 0)
+        e = time.perf_counter() - s
+        if b >= warmup:
+            times.append(e)
+    tot = sum(times)
+    return dict(value=BATCH * len(times) / tot, kind=kind, cores=cores, ms=1e3 * tot / len(times),
+                sample=f"C5-shaped {rows}-row table (S={SHARDS}, P={MAX_PROBE}, load 0.8 prefilled "
+                       f"untimed), {len(times)} timed batches of {BATCH} positions 90% hit/10% fresh, "
+                       f"process_batch(ExecMode::Parallel)")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rows", type=int, default=ROWS)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    log = (lambda *a: print(*a, file=sys.stderr, flush=True))
+    metric = "remapped IDs/sec (insert+evict) and HBM GB/s fraction at 1/2/4/8 B200 vs CPU ref"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = run_reference_sample(args.steps, max(args.warmup, 1), log=log)
+        line = {"metric": metric, "value": r["value"], "unit": "IDs/s", "impl": "reference",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "config": {"workload": "C5 sample (reference CPU path)", "rows": CPU_ROWS,
+                           "num_shards": SHARDS, "max_probe": MAX_PROBE, "batch_positions": BATCH},
+                "cpu_baseline": {"value": r["value"], "unit": "IDs/s", "cores": r["cores"],
+                                 "kind": r["kind"], "sample": r["sample"]},
+                "e2e": {"value": r["value"], "unit": "IDs/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import paper_2602_17050_b200 as mz
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local if world > 1 else 0
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    rows = args.rows
+    caps = mz.even_capacities(rows, SHARDS)
+    t_build = time.perf_counter()
+    table = mz.MpzchTable(mz.TableConfig(caps, MAX_PROBE, TABLE_SEED), device=dev)
+    pol = mz.EvictionPolicy.disabled()
+    npre = prefill_count(rows)
+    id_seed = ID_SEED + 1000 * rank  # replicas draw disjoint streams
+    out_s = torch.empty(BATCH, dtype=torch.int64, device=dev)
+    out_o = torch.empty(BATCH, dtype=torch.uint8, device=dev)
+    for a in range(0, npre, BATCH):
+        ids = distinct_ids_t(id_seed, torch.arange(a, min(a + BATCH, npre), dtype=torch.int64,
+                                                   device=dev))
+        table.process_batch_device(ids, 1, pol, None, out_s, out_o, None, stream)
+    torch.cuda.synchronize(dev)
+    log(f"[rank {rank}] prefill {npre} ids into {rows} rows in {time.perf_counter() - t_build:.1f}s; "
+        f"stats {table.last_stats()}")
+
+    # pre-generate the W + K device batches (inputs resident in HBM before timing)
+    nb = args.warmup + args.steps
+    batches = []
+    fresh_base = npre
+    for b in range(nb):
+        idx, nf = batch_indices(torch, dev, npre, BATCH, b, fresh_base, SAMPLER_SEED + rank)
+        fresh_base += nf
+        batches.append(distinct_ids_t(id_seed, idx))
+    torch.cuda.synchronize(dev)
+
+    for b in range(args.warmup):
+        table.process_batch_device(batches[b], 2 + b, pol, None, out_s, out_o, None, stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+
+    table.set_profiling(True)
+    launches0 = table.kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    stats = []
+    with Clocks(dev) as clk:
+        torch.cuda.synchronize(dev)
+        ev0.record(stream)
+        for b in range(args.warmup, nb):
+            table.process_batch_device(batches[b], 2 + b, pol, None, out_s, out_o, None, stream)
+            stats.append(table.last_stats())
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms_total = ev0.elapsed_time(ev1)
+    launches = table.kernel_launches() - launches0
+    prof = table.profile()
+    table.set_profiling(False)
+    if world > 1:
+        tt = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms_total = float(tt.item())
+    ms_step = ms_total / args.steps
+    value = world * BATCH * args.steps / (ms_total / 1e3)
+
+    # e2e: host buffers through the reference-facing C-ABI call, pinned memory
+    e2e_steps = args.e2e_steps or max(3, args.steps // 2)
+    pin_ids = [batches[(args.warmup + i) % nb].cpu().pin_memory() for i in range(e2e_steps)]
+    pin_s = torch.empty(BATCH, dtype=torch.int64).pin_memory()
+    pin_o = torch.empty(BATCH, dtype=torch.uint8).pin_memory()
+    # fresh ids for the e2e steps so they stay insert+lookup mixes
+    e2e_batches = []
+    for i in range(e2e_steps):
+        idx, nf = batch_indices(torch, dev, npre, BATCH, nb + i, fresh_base, SAMPLER_SEED + rank)
+        fresh_base += nf
+        e2e_batches.append(distinct_ids_t(id_seed, idx).cpu().pin_memory())
+    del pin_ids
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for i in range(e2e_steps):
+        ids_np = e2e_batches[i].numpy().view(np.uint64)
+        s, o, _ = table.process_batch(ids_np, 100 + i, pol)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e_value = world * BATCH * e2e_steps / e2e_s
+
+    peak, peak_src = peaks()
+    probe_ms = prof["probe_ms"] / max(prof["probe_launches"], 1)
+    probe_bytes = prof["probe_bytes"] / max(prof["probe_launches"], 1)
+    achieved = probe_bytes / (probe_ms / 1e3) / 1e9
+    batch_bytes = prof["batch_bytes"] / max(prof["batches"], 1)
+    batch_ms = prof["batch_ms"] / max(prof["batches"], 1)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            r = run_reference_sample(3, 1, log=log)
+            cpu = {"value": r["value"], "unit": "IDs/s", "cores": r["cores"], "kind": r["kind"],
+                   "sample": r["sample"]}
+        except Exception as e:  # the baseline must not take the GPU number down with it
+            cpu = {"value": None, "unit": "IDs/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {e}"}
+
+    if rank == 0:
+        agg = {k: sum(s[k] for s in stats) for k in ("found", "inserted", "collision", "new_ids")}
+        line = {
+            "metric": metric, "value": value, "unit": "IDs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (DistinctIdStream ids, SplitMix64 sampler)",
+            "config": {"workload": "C5 per GPU: 1B-slot (2^30-row) table, S=8, max_probe=128, "
+                                   "load 0.8 prefilled via the API, 4M-position batches 90% hit / "
+                                   "10% fresh, eviction Disabled",
+                       "rows": rows, "num_shards": SHARDS, "max_probe": MAX_PROBE,
+                       "batch_positions": BATCH, "global_batch": BATCH * world,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (16 GiB identity+metadata, random probes)",
+                       "outcomes_per_step": {k: v / args.steps for k, v in agg.items()}},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(),
+                         "kernel": "k_probe<Disabled> (probe of every position)",
+                         "algorithmic_bytes_per_launch": probe_bytes,
+                         "probe_sectors_per_launch": prof["probe_sectors"] / max(prof["probe_launches"], 1),
+                         "launch_ms": probe_ms, "peak_source": peak_src,
+                         "share_of_step": probe_ms / ms_step,
+                         "batch_algorithmic_bytes": batch_bytes,
+                         "batch_gbs": batch_bytes / (batch_ms / 1e3) / 1e9,
+                         "claim_ms": prof["claim_ms"] / max(prof["batches"], 1),
+                         "tail_ms": prof["tail_ms"] / max(prof["batches"], 1)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "IDs/s", "h2d_bytes_per_step": BATCH * 8,
+                    "d2h_bytes_per_step": BATCH * 9, "steps": e2e_steps,
+                    "api": "mpzch_process_batch (host buffers, pinned)"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
