@@ -103,7 +103,8 @@ mpzch_status mpzch_shard_layout(const mpzch_table* t, uint64_t* capacities, uint
  * mpzch_process_batch: HOST buffers; copies in, runs, copies out, returns when
  * done (the reference call's semantics).
  * mpzch_process_batch_device: DEVICE buffers on the table's device, enqueued on
- * `stream` (cudaStream_t, NULL = the handle's stream); returns after the batch
+ * `stream` (cudaStream_t; 0 = the legacy default stream, the CUDA convention, so
+ * work the caller queued on it is ordered before the batch); returns after the batch
  * completed on that stream (it reports validation errors synchronously, like
  * the reference).  out_evicted is a device pointer here. */
 mpzch_status mpzch_process_batch(mpzch_table* t, const uint64_t* ids, const uint32_t* features,

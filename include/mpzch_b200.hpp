@@ -1,0 +1,313 @@
+// mpzch_b200.hpp -- header-only C++ surface over the C-ABI (mpzch_b200.h) that keeps
+// the reference's names, value types and exception types, so a caller of the
+// reference remap API (/root/reference/proj/include/mpzch/{table,batch_engine,
+// eviction}.hpp) switches by changing the namespace and the include:
+//
+//   reference                                     here
+//   mpzch::TableConfig (table.hpp:18-28)          mpzch_b200::TableConfig
+//   mpzch::EvictionPolicy (eviction.hpp:27-46)    mpzch_b200::EvictionPolicy
+//   mpzch::MpzchTable (table.hpp:41-131)          mpzch_b200::MpzchTable  (HBM-resident)
+//   mpzch::process_batch (batch_engine.hpp:44)    mpzch_b200::process_batch
+//   mpzch::ProbeResult / Outcome (probe_core.hpp) mpzch_b200::ProbeResult / Outcome
+//
+// Errors surface as the same std exception types with the same what() text.
+// The extra evicted-slot output of the batched remap is available through
+// process_batch_with_evicted().
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+#include "mpzch_b200.h"
+
+namespace mpzch_b200 {
+
+using Id = std::uint64_t;
+using SlotIndex = std::uint64_t;
+using Timestamp = std::uint64_t;
+using FeatureOrdinal = std::uint32_t;
+
+inline constexpr Id kEmptySlot = ~std::uint64_t{0};
+
+enum class Outcome : std::uint8_t { Found, Inserted, Evicted, Collision };
+
+struct ProbeResult {
+    SlotIndex slot = 0;
+    bool evicted = false;
+    Outcome outcome = Outcome::Found;
+    bool operator==(const ProbeResult&) const = default;
+};
+
+struct BatchEntry {
+    Id id = 0;
+    FeatureOrdinal feature = 0;
+    bool operator==(const BatchEntry&) const = default;
+};
+
+struct IdBatch {
+    std::vector<BatchEntry> ids;
+    Timestamp now = 0;
+};
+
+enum class ExecMode { Serial, Parallel };  // accepted for signature parity; both are exact
+
+[[noreturn]] inline void rethrow(mpzch_status rc) {
+    const std::string msg = mpzch_last_error();
+    switch (rc) {
+        case MPZCH_EINVAL: throw std::invalid_argument(msg);
+        case MPZCH_EOVERFLOW: throw std::overflow_error(msg);
+        case MPZCH_ELENGTH: throw std::length_error(msg);
+        case MPZCH_ELOGIC: throw std::logic_error(msg);
+        case MPZCH_ERANGE: throw std::out_of_range(msg);
+        case MPZCH_ENOMEM: throw std::bad_alloc();
+        default: throw std::runtime_error(msg);
+    }
+}
+
+inline void check(mpzch_status rc) {
+    if (rc != MPZCH_OK) rethrow(rc);
+}
+
+struct TtlPolicy {
+    std::uint64_t default_ttl_seconds = 259200;
+    std::unordered_map<FeatureOrdinal, std::uint64_t> per_feature_ttl;
+    std::uint64_t ttl_for(FeatureOrdinal f) const {
+        auto it = per_feature_ttl.find(f);
+        return it != per_feature_ttl.end() ? it->second : default_ttl_seconds;
+    }
+    void validate() const {
+        if (default_ttl_seconds == 0) throw std::invalid_argument("default TTL must be strictly positive");
+        for (const auto& [f, t] : per_feature_ttl)
+            if (t == 0)
+                throw std::invalid_argument("per-feature TTL must be strictly positive (feature " +
+                                            std::to_string(f) + ")");
+    }
+};
+
+enum class EvictionMode { Disabled, Ttl, Lru };
+
+class EvictionPolicy {
+public:
+    static EvictionPolicy disabled() { return EvictionPolicy(EvictionMode::Disabled, {}); }
+    static EvictionPolicy lru() { return EvictionPolicy(EvictionMode::Lru, {}); }
+    static EvictionPolicy ttl(TtlPolicy cfg) {
+        cfg.validate();
+        return EvictionPolicy(EvictionMode::Ttl, std::move(cfg));
+    }
+    EvictionMode mode() const { return mode_; }
+    const TtlPolicy& ttl_config() const { return ttl_; }
+
+    // C view; valid while *this lives
+    const mpzch_policy* c_policy() const { return &c_; }
+
+private:
+    EvictionPolicy(EvictionMode m, TtlPolicy t) : mode_(m), ttl_(std::move(t)) {
+        std::map<FeatureOrdinal, std::uint64_t> sorted(ttl_.per_feature_ttl.begin(),
+                                                       ttl_.per_feature_ttl.end());
+        for (const auto& [k, v] : sorted) {
+            keys_.push_back(k);
+            vals_.push_back(v);
+        }
+        c_.mode = static_cast<int32_t>(mode_);
+        c_.n_feat = mode_ == EvictionMode::Ttl ? static_cast<uint32_t>(keys_.size()) : 0;
+        c_.default_ttl = mode_ == EvictionMode::Ttl ? ttl_.default_ttl_seconds : 0;
+        c_.feat_keys = keys_.data();
+        c_.feat_ttls = vals_.data();
+    }
+    EvictionMode mode_;
+    TtlPolicy ttl_;
+    std::vector<std::uint32_t> keys_;
+    std::vector<std::uint64_t> vals_;
+    mpzch_policy c_{};
+};
+
+struct TableConfig {
+    std::vector<std::uint64_t> shard_capacities;
+    std::uint32_t max_probe = 1;
+    std::uint64_t seed = 0;
+    std::uint32_t dim = 0;
+    std::uint64_t init_seed = 0;
+    int device = 0;  // the B200 holding the table
+
+    static TableConfig even(std::uint64_t total_rows, std::uint32_t num_shards, std::uint32_t max_probe,
+                            std::uint64_t seed, std::uint32_t dim = 0, std::uint64_t init_seed = 0) {
+        if (num_shards == 0) throw std::invalid_argument("layout needs at least one shard");
+        if (total_rows < num_shards) throw std::invalid_argument("fewer rows than shards");
+        TableConfig c;
+        c.shard_capacities.assign(num_shards, total_rows / num_shards);
+        for (std::uint64_t s = 0; s < total_rows % num_shards; ++s) ++c.shard_capacities[s];
+        c.max_probe = max_probe;
+        c.seed = seed;
+        c.dim = dim;
+        c.init_seed = init_seed;
+        return c;
+    }
+};
+
+struct PublishCursor {
+    std::uint64_t generation = 0;
+};
+
+class MpzchTable {
+public:
+    explicit MpzchTable(const TableConfig& cfg) : dim_(cfg.dim) {
+        check(mpzch_table_create(cfg.shard_capacities.data(),
+                                 static_cast<std::uint32_t>(cfg.shard_capacities.size()),
+                                 cfg.max_probe, cfg.seed, cfg.dim, cfg.init_seed, cfg.device, &t_));
+        caps_ = cfg.shard_capacities;
+        offsets_.resize(caps_.size() + 1);
+        check(mpzch_shard_layout(t_, nullptr, offsets_.data()));
+    }
+    MpzchTable(const MpzchTable&) = delete;
+    MpzchTable& operator=(const MpzchTable&) = delete;
+    MpzchTable(MpzchTable&& o) noexcept { swap(o); }
+    MpzchTable& operator=(MpzchTable&& o) noexcept {
+        swap(o);
+        return *this;
+    }
+    ~MpzchTable() {
+        if (t_) mpzch_table_destroy(t_);
+    }
+
+    std::uint64_t total_rows() const { return mpzch_total_rows(t_); }
+    std::uint32_t num_shards() const { return mpzch_num_shards(t_); }
+    std::uint32_t max_probe() const { return mpzch_max_probe(t_); }
+    std::uint32_t dim() const { return dim_; }
+    bool has_embeddings() const { return dim_ > 0; }
+    bool frozen() const { return false; }
+
+    ProbeResult lookup_or_insert(Id id, FeatureOrdinal feature, Timestamp now,
+                                 const EvictionPolicy& policy) {
+        std::uint64_t s = 0;
+        std::uint8_t o = 0;
+        check(mpzch_lookup_or_insert(t_, id, feature, now, policy.c_policy(), &s, &o));
+        return {s, o == MPZCH_EVICTED, static_cast<Outcome>(o)};
+    }
+
+    ProbeResult lookup(Id id) const {
+        std::uint64_t s = 0;
+        std::uint8_t o = 0;
+        check(mpzch_lookup(t_, &id, 1, &s, &o));
+        return {s, false, static_cast<Outcome>(o)};
+    }
+
+    std::vector<ProbeResult> lookup(const std::vector<Id>& ids) const {
+        std::vector<std::uint64_t> s(ids.size());
+        std::vector<std::uint8_t> o(ids.size());
+        check(mpzch_lookup(t_, ids.data(), ids.size(), s.data(), o.data()));
+        std::vector<ProbeResult> r(ids.size());
+        for (std::size_t i = 0; i < ids.size(); ++i) r[i] = {s[i], false, static_cast<Outcome>(o[i])};
+        return r;
+    }
+
+    std::vector<Id> identities(std::uint32_t shard) const {
+        if (shard >= caps_.size()) throw std::out_of_range("shard index out of range");
+        std::vector<Id> all(total_rows());
+        check(mpzch_copy_identities(t_, all.data()));
+        return {all.begin() + offsets_[shard], all.begin() + offsets_[shard + 1]};
+    }
+
+    std::vector<std::uint64_t> metadata(std::uint32_t shard) const {
+        if (shard >= caps_.size()) throw std::out_of_range("shard index out of range");
+        std::vector<std::uint64_t> all(total_rows());
+        check(mpzch_copy_metadata(t_, all.data()));
+        return {all.begin() + offsets_[shard], all.begin() + offsets_[shard + 1]};
+    }
+
+    Id row_identity(std::uint64_t row) const {
+        if (row >= total_rows()) throw std::out_of_range("global row out of range");
+        std::vector<Id> all(total_rows());
+        check(mpzch_copy_identities(t_, all.data()));
+        return all[row];
+    }
+
+    std::vector<float> row(std::uint64_t r) const {
+        std::vector<float> w(dim_);
+        check(mpzch_copy_weights(t_, r, 1, w.data()));
+        return w;
+    }
+
+    std::vector<float> momentum_row(std::uint64_t r) const {
+        std::vector<float> m(dim_);
+        check(mpzch_copy_momentum(t_, r, 1, m.data()));
+        return m;
+    }
+
+    bool row_trained(std::uint64_t r) const {
+        if (dim_ == 0) throw std::logic_error("table has no embedding payload (dim = 0)");
+        std::vector<std::uint8_t> t(total_rows());
+        check(mpzch_copy_trained(t_, t.data()));
+        if (r >= t.size()) throw std::out_of_range("embedding row out of range");
+        return t[r] != 0;
+    }
+
+    PublishCursor make_cursor() {
+        PublishCursor c;
+        check(mpzch_make_cursor(t_, &c.generation));
+        return c;
+    }
+
+    std::vector<std::uint64_t> dirty_rows_since(const PublishCursor& c) const {
+        std::vector<std::uint64_t> rows(total_rows());
+        std::uint64_t n = 0;
+        check(mpzch_dirty_rows_since(t_, c.generation, rows.data(), rows.size(), &n));
+        rows.resize(n);
+        return rows;
+    }
+
+    mpzch_table* handle() const { return t_; }
+
+private:
+    void swap(MpzchTable& o) noexcept {
+        std::swap(t_, o.t_);
+        std::swap(dim_, o.dim_);
+        std::swap(caps_, o.caps_);
+        std::swap(offsets_, o.offsets_);
+    }
+    mpzch_table* t_ = nullptr;
+    std::uint32_t dim_ = 0;
+    std::vector<std::uint64_t> caps_, offsets_;
+};
+
+// process_batch (batch_engine.hpp:44-46): same signature, same results.
+inline std::vector<ProbeResult> process_batch_with_evicted(MpzchTable& table, const IdBatch& batch,
+                                                           const EvictionPolicy& policy,
+                                                           std::vector<std::uint64_t>* evicted) {
+    const std::size_t n = batch.ids.size();
+    std::vector<std::uint64_t> ids(n), slots(n);
+    std::vector<std::uint32_t> feats(n);
+    std::vector<std::uint8_t> oc(n);
+    bool any_feature = false;
+    for (std::size_t i = 0; i < n; ++i) {
+        ids[i] = batch.ids[i].id;
+        feats[i] = batch.ids[i].feature;
+        any_feature |= feats[i] != 0;
+    }
+    std::vector<std::uint64_t> ev(evicted ? n : 0);
+    std::uint64_t nev = 0;
+    check(mpzch_process_batch(table.handle(), ids.data(), any_feature ? feats.data() : nullptr, n,
+                              batch.now, policy.c_policy(), slots.data(), oc.data(),
+                              evicted ? ev.data() : nullptr, ev.size(), &nev));
+    std::vector<ProbeResult> out(n);
+    for (std::size_t i = 0; i < n; ++i)
+        out[i] = {slots[i], oc[i] == MPZCH_EVICTED, static_cast<Outcome>(oc[i])};
+    if (evicted) {
+        ev.resize(nev);
+        *evicted = std::move(ev);
+    }
+    return out;
+}
+
+inline std::vector<ProbeResult> process_batch(MpzchTable& table, const IdBatch& batch,
+                                              const EvictionPolicy& policy,
+                                              ExecMode = ExecMode::Parallel) {
+    return process_batch_with_evicted(table, batch, policy, nullptr);
+}
+
+}  // namespace mpzch_b200

@@ -98,7 +98,7 @@ struct BatchErr {
 };
 
 __device__ __forceinline__ bool batch_failed(const BatchErr* e) {
-    return e->bad_pos != ~0ull || e->overflow != 0;
+    return e->bad_pos != ~0ull || e->overflow != 0 || e->too_many != 0;
 }
 
 // L2-coherent loads/stores for state that other threads mutate in the same kernel.

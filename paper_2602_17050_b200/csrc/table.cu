@@ -451,8 +451,10 @@ mpzch_status mpzch_process_batch_device(mpzch_table* t, const uint64_t* ids, con
         Table& T = *t->t;
         DeviceGuard g(T.device);
         const Policy pol = parse_policy(policy);
+        // CUDA convention: 0 is the legacy default stream (torch's default stream has
+        // handle 0), so the caller's producer kernels are ordered before ours
         run_batch(T, ids, feats, n, now, pol, out_slots, out_oc, out_ev, ev_cap, out_ev_n,
-                  stream ? (cudaStream_t)stream : T.stream);
+                  (cudaStream_t)stream);
     });
 }
 
@@ -507,7 +509,7 @@ mpzch_status mpzch_lookup_device(const mpzch_table* t, const uint64_t* ids, uint
         Table& T = *t->t;
         DeviceGuard g(T.device);
         if (n == 0) return;
-        cudaStream_t st = stream ? (cudaStream_t)stream : T.stream;
+        cudaStream_t st = (cudaStream_t)stream;  // 0 = legacy default stream
         BatchErr init{~0ull, 0, 0};
         MPZCH_CUDA(cudaMemcpyAsync(&T.d_ctr->err, &init, sizeof init, cudaMemcpyHostToDevice, st));
         run_lookup(T, ids, n, out_slots, out_oc, &T.d_ctr->err, st);

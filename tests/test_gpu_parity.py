@@ -436,3 +436,20 @@ def test_device_buffer_entry_point(oracle):
     assert nev == 0 and (slots.cpu().numpy().view(np.uint64) == s).all()
     assert (oc.cpu().numpy() == oo).all()
     assert t.kernel_launches() > 0
+
+
+def test_default_stream_ordering(oracle):
+    """ids produced by torch on its default stream (handle 0) immediately before the call
+    must be seen complete: stream 0 means the legacy default stream, not a private one."""
+    import torch
+    import bench
+    rows = 1 << 22
+    t = mz.MpzchTable(mz.TableConfig.even(rows, 8, 128, 7))
+    B = 1 << 20
+    out_s = torch.empty(B, dtype=torch.int64, device="cuda")
+    out_o = torch.empty(B, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream()
+    for b in range(3):
+        ids = bench.distinct_ids_t(5, torch.arange(b * B, (b + 1) * B, dtype=torch.int64, device="cuda"))
+        t.process_batch_device(ids, 1, mz.EvictionPolicy.disabled(), None, out_s, out_o, None, st)
+        assert t.last_stats()["found"] == 0  # fresh distinct ids are never found
