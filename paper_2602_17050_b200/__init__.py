@@ -306,25 +306,29 @@ class MpzchTable:
 
     # ---- hot path ------------------------------------------------------------------------
     def process_batch(self, ids, now: int, policy: EvictionPolicy, features=None,
-                      evicted_cap: Optional[int] = None) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+                      evicted_cap: Optional[int] = None, out_slots=None, out_outcomes=None,
+                      out_evicted=None) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
         """process_batch (batch_engine.cpp:141-221) on host buffers.
 
         Returns (slots u64[n] global rows, outcomes u8[n], evicted u64[k]) where evicted is the
-        canonical evicted list (first-occurrence order, with multiplicity)."""
+        canonical evicted list (first-occurrence order, with multiplicity).  Output arrays may
+        be supplied (e.g. page-locked) to avoid allocation."""
         ids = np.ascontiguousarray(ids, dtype=np.uint64)
         n = ids.size
         feats = None if features is None else np.ascontiguousarray(features, dtype=np.uint32)
         if feats is not None and feats.size != n:
             raise InvalidArgument("features must pair 1:1 with ids")
-        slots = np.empty(n, dtype=np.uint64)
-        oc = np.empty(n, dtype=np.uint8)
+        slots = np.empty(n, dtype=np.uint64) if out_slots is None else out_slots
+        oc = np.empty(n, dtype=np.uint8) if out_outcomes is None else out_outcomes
+        assert slots.size >= n and oc.size >= n and slots.dtype == np.uint64 and oc.dtype == np.uint8
         cap = n if evicted_cap is None else evicted_cap
-        ev = np.empty(max(cap, 1), dtype=np.uint64)
+        ev = np.empty(max(cap, 1), dtype=np.uint64) if out_evicted is None else out_evicted
+        cap = min(cap, ev.size)
         nev = ctypes.c_uint64(0)
         _check(self._lib.mpzch_process_batch(self._h, _ptr(ids), _ptr(feats), n, now,
                                              ctypes.byref(policy._c), _ptr(slots), _ptr(oc),
                                              _ptr(ev), cap, ctypes.byref(nev)))
-        return slots, oc, ev[:min(nev.value, cap)].copy()
+        return slots[:n], oc[:n], ev[:min(nev.value, cap)].copy()
 
     def process_batch_device(self, ids, now: int, policy: EvictionPolicy, features=None,
                              out_slots=None, out_outcomes=None, out_evicted=None, stream=None):

@@ -26,8 +26,12 @@
 //   K6 meta       M[slot] = meta for every position (one value per batch => order-free).
 #include <cuda_runtime.h>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "table.hpp"
+
+namespace cg = cooperative_groups;
 
 namespace mpzch_b200 {
 
@@ -88,103 +92,142 @@ __device__ __forceinline__ uint32_t first_expired(const uint64_t* __restrict__ m
     return limit;
 }
 
-// K1: one thread per position.
-template <int MODE>
-__global__ void __launch_bounds__(256) k_probe(TableDev t, const uint64_t* __restrict__ ids,
-                                               uint64_t n, uint64_t now, BatchCounters* ctr,
+// K0: streaming validation of the batch (batch_engine.cpp:90-94): min invalid position.
+// Runs before anything mutates, so the probe can write metadata for final positions.
+__global__ void __launch_bounds__(256) k_validate(const uint64_t* __restrict__ ids, uint64_t n,
+                                                  BatchCounters* ctr) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long bad = ~0ull;
+    if ((reinterpret_cast<uintptr_t>(ids) & 15) == 0) {
+        const uint64_t n2 = n / 2;
+        const ulonglong2* v2 = reinterpret_cast<const ulonglong2*>(ids);
+        for (uint64_t q = tid; q < n2; q += stride) {
+            const ulonglong2 v = __ldcs(v2 + q);
+            if ((v.x | v.y) >> 63) bad = min(bad, (unsigned long long)(v.x >> 63 ? 2 * q : 2 * q + 1));
+        }
+        if (tid == 0 && (n & 1) && (ids[n - 1] >> 63)) bad = min(bad, (unsigned long long)(n - 1));
+    } else {
+        for (uint64_t i = tid; i < n; i += stride)
+            if (ids[i] >> 63) bad = min(bad, (unsigned long long)i);
+    }
+    if (bad != ~0ull) atomicMin(&ctr->err.bad_pos, bad);
+}
+
+// K1: probe; each thread keeps U positions in flight (independent sector loads), all
+// positions of a round are issued before any is scanned.
+template <int MODE, int U>
+__global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __restrict__ ids,
+                                               uint64_t n, uint64_t now, uint64_t meta_value,
+                                               BatchCounters* ctr,
                                                uint64_t* __restrict__ out_slots,
                                                uint8_t* __restrict__ out_oc,
                                                uint32_t* __restrict__ newpos,
                                                uint32_t* __restrict__ newa,
                                                uint32_t* __restrict__ newm) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    if (batch_failed(&ctr->err)) return;
+    constexpr uint8_t kPending = 0, kHit = 1, kEmptyHit = 2, kExhausted = 3, kIdle = 4;
     const unsigned lane = lane_id();
+    const uint64_t tile = (uint64_t)blockDim.x * U;
     unsigned long long my_found = 0, my_coll = 0, my_isec = 0, my_msec = 0;
-    for (uint64_t base_i = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base_i < n;
-         base_i += stride) {
-        const uint64_t i = base_i + lane;
-        bool is_new = false;
-        uint32_t a_off = 0, m_off = kNone32;
-        if (i < n) {
-            const uint64_t id = ids[i];
-            if (id >> 63) {
-                atomicMin(&ctr->err.bad_pos, (unsigned long long)i);
-            } else {
-                const uint32_t s = shard_of(id, t);
-                const ShardDev sd = t.shards[s];
-                const uint64_t cap = sd.cap.d, base = sd.offset, end = base + cap;
-                const uint64_t h = home_of(id, sd, t.seed);
-                uint32_t off = 0, found = kNone32, empty = kNone32;
-                uint64_t g = base + h, gf = 0;
-                while (off < t.P) {
-                    const uint64_t a4 = g & ~3ull;
-                    uint64_t w0, w1, w2, w3;
-                    ld_sector(t.ident + a4, w0, w1, w2, w3);
-                    ++my_isec;
-                    do {
-                        const uint64_t v = pick4((uint32_t)(g - a4), w0, w1, w2, w3);
-                        if (v == id) { found = off; gf = g; break; }
-                        if (v == kEmpty) { empty = off; break; }
-                        ++off;
-                        if (++g == end) g = base;
-                    } while (off < t.P && (g >> 2) == (a4 >> 2));
-                    if (found != kNone32 || empty != kNone32) break;
-                }
-                if (MODE == kModeDisabled) {
-                    if (found != kNone32) {
-                        out_slots[i] = gf;
-                        out_oc[i] = kFound;
-                        ++my_found;
-                    } else if (empty != kNone32) {
-                        is_new = true;
-                        a_off = empty;
-                    } else {
-                        out_slots[i] = base + h;
-                        out_oc[i] = kCollision;
-                        ++my_coll;
-                    }
-                } else {  // TTL, one meta value per batch
-                    if (found != kNone32) {
-                        ++my_msec;
-                        if (__ldg(t.meta + gf) >= now) {  // live: nobody can take it this batch
-                            out_slots[i] = gf;
-                            out_oc[i] = kFound;
-                            ++my_found;
-                        } else {  // expired own slot: contested by lower-rank new ids
-                            is_new = true;
-                            m_off = found;
-                            a_off = first_expired(t.meta, base, h, cap, found, now, my_msec);
-                        }
-                    } else {
-                        const uint32_t lim = empty != kNone32 ? empty : t.P;
-                        const uint32_t x = first_expired(t.meta, base, h, cap, lim, now, my_msec);
-                        if (x < lim || empty != kNone32) {
-                            is_new = true;
-                            a_off = x;
-                        } else {
-                            out_slots[i] = base + h;
-                            out_oc[i] = kCollision;
-                            ++my_coll;
-                        }
-                    }
-                }
+    for (uint64_t t0 = (uint64_t)blockIdx.x * tile; t0 < n; t0 += (uint64_t)gridDim.x * tile) {
+        uint64_t id[U], g[U], base[U], cap[U], h[U];
+        uint32_t off[U];
+        uint8_t st[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = t0 + (uint64_t)u * blockDim.x + threadIdx.x;
+            st[u] = kIdle;
+            off[u] = 0;
+            if (i < n) {
+                id[u] = ids[i];
+                const ShardDev sd = t.shards[shard_of(id[u], t)];
+                cap[u] = sd.cap.d;
+                base[u] = sd.offset;
+                h[u] = home_of(id[u], sd, t.seed);
+                g[u] = base[u] + h[u];
+                st[u] = kPending;
             }
         }
-        // warp-aggregated append to the new list
-        const unsigned mask = __ballot_sync(0xffffffffu, is_new);
-        if (mask) {
-            unsigned basek = 0;
-            if (lane == 0) basek = atomicAdd(&ctr->new_count, (unsigned)__popc(mask));
-            basek = __shfl_sync(0xffffffffu, basek, 0);
-            if (is_new) {
-                const unsigned k = basek + __popc(mask & ((1u << lane) - 1));
-                newpos[k] = (uint32_t)i;
-                newa[k] = a_off;
-                newm[k] = m_off;
+        // scan rounds: issue every pending position's next sector, then scan them
+        for (;;) {
+            uint64_t w[U][4];
+            bool any = false;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (st[u] == kPending) {
+                    ld_sector(t.ident + (g[u] & ~3ull), w[u][0], w[u][1], w[u][2], w[u][3]);
+                    ++my_isec;
+                }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (st[u] != kPending) continue;
+                const uint64_t a4 = g[u] & ~3ull, end = base[u] + cap[u];
+                do {
+                    const uint64_t v = pick4((uint32_t)(g[u] - a4), w[u][0], w[u][1], w[u][2], w[u][3]);
+                    if (v == id[u]) { st[u] = kHit; break; }
+                    if (v == kEmpty) { st[u] = kEmptyHit; break; }
+                    ++off[u];
+                    if (++g[u] == end) g[u] = base[u];
+                } while (off[u] < t.P && (g[u] >> 2) == (a4 >> 2));
+                if (st[u] == kPending) {
+                    if (off[u] >= t.P) st[u] = kExhausted;
+                    else any = true;
+                }
+            }
+            if (!any) break;
+        }
+        // decisions, final writes (result + metadata word) and the new list
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = t0 + (uint64_t)u * blockDim.x + threadIdx.x;
+            bool is_new = false;
+            uint32_t a_off = 0, m_off = kNone32;
+            if (st[u] != kIdle) {
+                uint64_t fslot = kEmpty;
+                uint8_t foc = kFound;
+                if (MODE == kModeDisabled) {
+                    if (st[u] == kHit) fslot = g[u];
+                    else if (st[u] == kEmptyHit) { is_new = true; a_off = off[u]; }
+                    else { fslot = base[u] + h[u]; foc = kCollision; }
+                } else {  // TTL with one metadata value per batch
+                    if (st[u] == kHit) {
+                        ++my_msec;
+                        if (__ldg(t.meta + g[u]) >= now) {
+                            fslot = g[u];  // live: nobody can take it in this batch
+                        } else {           // expired own slot: lower-rank new ids contest it
+                            is_new = true;
+                            m_off = off[u];
+                            a_off = first_expired(t.meta, base[u], h[u], cap[u], off[u], now, my_msec);
+                        }
+                    } else {
+                        const uint32_t lim = st[u] == kEmptyHit ? off[u] : t.P;
+                        const uint32_t x = first_expired(t.meta, base[u], h[u], cap[u], lim, now, my_msec);
+                        if (x < lim || st[u] == kEmptyHit) { is_new = true; a_off = x; }
+                        else { fslot = base[u] + h[u]; foc = kCollision; }
+                    }
+                }
+                if (fslot != kEmpty) {
+                    out_slots[i] = fslot;
+                    out_oc[i] = foc;
+                    t.meta[fslot] = meta_value;  // Found refresh / Collision at home
+                    if (foc == kFound) ++my_found; else ++my_coll;
+                }
+            }
+            const unsigned mask = __ballot_sync(0xffffffffu, is_new);
+            if (mask) {
+                unsigned basek = 0;
+                if (lane == 0) basek = atomicAdd(&ctr->new_count, (unsigned)__popc(mask));
+                basek = __shfl_sync(0xffffffffu, basek, 0);
+                if (is_new) {
+                    const unsigned k = basek + __popc(mask & ((1u << lane) - 1));
+                    newpos[k] = (uint32_t)i;
+                    newa[k] = a_off;
+                    newm[k] = m_off;
+                }
             }
         }
     }
-    // per-warp stat reduction
     for (int o = 16; o; o >>= 1) {
         my_found += __shfl_xor_sync(0xffffffffu, my_found, o);
         my_coll += __shfl_xor_sync(0xffffffffu, my_coll, o);
@@ -206,7 +249,7 @@ __global__ void __launch_bounds__(256) k_dedup(const uint64_t* __restrict__ ids,
                                                const uint32_t* __restrict__ newm,
                                                uint32_t* __restrict__ newent, uint64_t* tkey,
                                                unsigned* tmin, uint32_t* ta, uint32_t* tm,
-                                               uint32_t* elist) {
+                                               uint32_t* theld, uint32_t* elist) {
     if (batch_failed(&ctr->err)) return;
     const unsigned cnt = ctr->new_count;
     const uint64_t mask = table_mask(cnt, tcap);
@@ -224,8 +267,11 @@ __global__ void __launch_bounds__(256) k_dedup(const uint64_t* __restrict__ ids,
                     e = (uint32_t)h;
                     ta[e] = newa[k];
                     tm[e] = newm[k];
-                    const unsigned slot = atomicAdd(&ctr->entry_count, 1u);
-                    elist[slot] = e;
+                    theld[e] = 0;
+                    cg::coalesced_group grp = cg::coalesced_threads();  // one atomic per warp
+                    unsigned slot0 = 0;
+                    if (grp.thread_rank() == 0) slot0 = atomicAdd(&ctr->entry_count, grp.size());
+                    elist[grp.shfl(slot0, 0) + grp.thread_rank()] = e;
                     break;
                 }
             }
@@ -248,7 +294,7 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                                                const unsigned* __restrict__ tmin,
                                                const uint32_t* __restrict__ ta,
                                                const uint32_t* __restrict__ tm,
-                                               volatile uint32_t* theld, uint8_t* tstate) {
+                                               uint32_t* theld, uint8_t* tstate) {
     if (batch_failed(&ctr->err)) return;
     const unsigned cnt = ctr->entry_count;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
@@ -271,8 +317,6 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                 // owner: try to keep (refresh) the expired slot holding our own id
                 const uint32_t m = tm[e];
                 const uint64_t gm = base + wrap_add(h, m, cap);
-                theld[e] = m;
-                __threadfence();
                 uint64_t v = ld_cg(t.ident + gm);
                 for (;;) {
                     uint64_t nv;
@@ -308,12 +352,13 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                             if (!(ld_cg(t.meta + g) < now)) break;  // live
                             nv = cv;                                 // expired foreign id
                         }
-                        theld[e] = off;
-                        __threadfence();
                         const uint64_t old = atomicCAS((unsigned long long*)(t.ident + g),
                                                        (unsigned long long)v,
                                                        (unsigned long long)nv);
                         if (old == v) {
+                            // taker claims of one entry move strictly forward, so the max is the
+                            // slot it holds last (a late max from a displaced claim is harmless)
+                            atomicMax(theld + e, off);
                             held = true;
                             if (is_claim(v)) { next = claim_entry(v); gnext = g; }
                             break;
@@ -344,7 +389,9 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
     }
 }
 
-// K4: commit claims.
+// K4: commit claims: claim word -> id, outcome, the entry's metadata word (one value per
+// batch, so duplicates / (id, f') secondaries of the entry need no write of their own),
+// touch_row, reset list and rank-indexed evicted flags.
 template <int MODE>
 __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
                                                 const uint32_t* __restrict__ elist,
@@ -355,6 +402,7 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
                                                 const uint8_t* __restrict__ tstate,
                                                 uint64_t* __restrict__ tslot,
                                                 uint8_t* __restrict__ toc, uint64_t gen_clock,
+                                                uint64_t meta_value,
                                                 uint64_t* __restrict__ reset_rows,
                                                 uint8_t* __restrict__ evflag,
                                                 uint64_t* __restrict__ evslot) {
@@ -363,31 +411,36 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
         const uint32_t e = elist[k];
         const uint64_t id = tkey[e];
+        const uint32_t rank = tmin[e];
         const uint32_t s = shard_of(id, t);
         const ShardDev sd = t.shards[s];
         const uint64_t cap = sd.cap.d, base = sd.offset;
         const uint64_t h = home_of(id, sd, t.seed);
-        if (tstate[e] == kStateCollided) {
-            tslot[e] = base + h;
-            toc[e] = kCollision;
-            continue;
+        const uint64_t mine = kClaimBit | ((uint64_t)rank << 31) | (uint64_t)e;
+        uint8_t oc = kCollision;
+        uint64_t g = base + h;
+        uint64_t v = 0;
+        bool ok = true;
+        if (MODE == kModeTtl && tm[e] != kNone32 &&
+            ((v = t.ident[base + wrap_add(h, tm[e], cap)]) & ~kFlagEmpty) == mine) {
+            g = base + wrap_add(h, tm[e], cap);  // the owner kept (refreshed) its own slot
+            oc = kFound;
+        } else if (tstate[e] != kStateCollided) {
+            g = base + wrap_add(h, theld[e], cap);
+            v = t.ident[g];
+            ok = (v & ~kFlagEmpty) == mine;
+            oc = (v & kFlagEmpty) ? kInserted : kEvicted;
         }
-        const uint32_t off = theld[e];
-        const uint64_t g = base + wrap_add(h, off, cap);
-        const uint64_t v = t.ident[g];
-        if (!is_claim(v) || claim_entry(v) != e || claim_rank(v) != tmin[e]) {
+        if (!ok) {
             atomicExch(&ctr->err.too_many, 2u);  // internal invariant violated
             continue;
         }
-        uint8_t oc;
-        if (MODE == kModeTtl && tm[e] == off) oc = kFound;
-        else oc = (v & kFlagEmpty) ? kInserted : kEvicted;
-        t.ident[g] = id;
-        if (oc != kFound) t.row_gen[g] = gen_clock;
+        if (oc != kCollision) t.ident[g] = id;
+        t.meta[g] = meta_value;
+        if (oc == kInserted || oc == kEvicted) t.row_gen[g] = gen_clock;
         if (oc == kEvicted) {
             const unsigned r = atomicAdd(&ctr->reset_count, 1u);
             reset_rows[r] = g;
-            const uint32_t rank = tmin[e];
             evflag[rank] = 1;
             evslot[rank] = g;
             atomicAdd(&ctr->evicted_count, 1u);
@@ -430,16 +483,6 @@ __global__ void __launch_bounds__(256) k_finalize(BatchCounters* ctr,
     }
 }
 
-// K6: every position writes its metadata word; all values are identical in a batch.
-__global__ void __launch_bounds__(256) k_meta(TableDev t, const BatchCounters* ctr, uint64_t n,
-                                              const uint64_t* __restrict__ out_slots,
-                                              uint64_t meta_value) {
-    if (batch_failed(&ctr->err)) return;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        t.meta[out_slots[i]] = meta_value;
-}
-
 // K9: return the id-table entries to EMPTY for the next batch.
 __global__ void __launch_bounds__(256) k_cleanup(BatchCounters* ctr, const uint32_t* __restrict__ elist,
                                                  uint64_t* tkey, unsigned* tmin, uint8_t* tstate) {
@@ -455,62 +498,56 @@ __global__ void __launch_bounds__(256) k_cleanup(BatchCounters* ctr, const uint3
 }  // namespace
 
 void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
+    constexpr int kU = 2;  // positions in flight per probe thread
     const uint64_t n = a.n;
     t.ensure_fast_scratch(n);
     const unsigned B = 256;
-    const unsigned gN = grid_for(n, B);
     const unsigned gW = grid_for(n, B, 148u * 8u);  // count-driven kernels
+    const unsigned gP = grid_for((n + kU - 1) / kU, B, 148u * 16u);
+    const bool ttl = a.pol->mode == kModeTtl;
+    uint32_t* newpos = t.s_newpos.as<uint32_t>();
+    uint32_t* newa = t.s_newa.as<uint32_t>();
+    uint32_t* newm = t.s_newm.as<uint32_t>();
     k_init_counters<<<1, 32, 0, st>>>(t.d_ctr);
-    ++t.launches;
+    k_validate<<<grid_for(n / 2 + 1, B, 148u * 8u), B, 0, st>>>(a.ids, n, t.d_ctr);
+    t.launches += 2;
+    if (a.overflow_all) return;  // validation only; the host reports the error
     if (t.profiling) cudaEventRecord(t.ev[0], st);
-    if (a.pol->mode == kModeTtl)
-        k_probe<kModeTtl><<<gN, B, 0, st>>>(t.dev, a.ids, n, a.now, t.d_ctr, a.out_slots, a.out_oc,
-                                            t.s_newpos.as<uint32_t>(), t.s_newa.as<uint32_t>(),
-                                            t.s_newm.as<uint32_t>());
+    if (ttl)
+        k_probe<kModeTtl, kU><<<gP, B, 0, st>>>(t.dev, a.ids, n, a.now, a.uniform_meta, t.d_ctr,
+                                                a.out_slots, a.out_oc, newpos, newa, newm);
     else
-        k_probe<kModeDisabled><<<gN, B, 0, st>>>(t.dev, a.ids, n, a.now, t.d_ctr, a.out_slots,
-                                                 a.out_oc, t.s_newpos.as<uint32_t>(),
-                                                 t.s_newa.as<uint32_t>(), t.s_newm.as<uint32_t>());
+        k_probe<kModeDisabled, kU><<<gP, B, 0, st>>>(t.dev, a.ids, n, a.now, a.uniform_meta, t.d_ctr,
+                                                     a.out_slots, a.out_oc, newpos, newa, newm);
     ++t.launches;
     if (t.profiling) cudaEventRecord(t.ev[1], st);
-    if (a.overflow_all) return;  // validation only; the host reports the error
-    k_dedup<<<gW, B, 0, st>>>(a.ids, t.d_ctr, t.tcap, t.s_newpos.as<uint32_t>(),
-                              t.s_newa.as<uint32_t>(), t.s_newm.as<uint32_t>(),
-                              t.s_newent.as<uint32_t>(), t.s_tkey.as<uint64_t>(),
-                              t.s_tmin.as<unsigned>(), t.s_ta.as<uint32_t>(), t.s_tm.as<uint32_t>(),
+    k_dedup<<<gW, B, 0, st>>>(a.ids, t.d_ctr, t.tcap, newpos, newa, newm, t.s_newent.as<uint32_t>(),
+                              t.s_tkey.as<uint64_t>(), t.s_tmin.as<unsigned>(), t.s_ta.as<uint32_t>(),
+                              t.s_tm.as<uint32_t>(), t.s_theld.as<uint32_t>(),
                               t.s_elist.as<uint32_t>());
-    ++t.launches;
-    if (a.pol->mode == kModeTtl) {
-        k_claim<kModeTtl><<<gW, B, 0, st>>>(t.dev, a.now, t.d_ctr, t.s_elist.as<uint32_t>(),
-                                            t.s_tkey.as<uint64_t>(), t.s_tmin.as<unsigned>(),
-                                            t.s_ta.as<uint32_t>(), t.s_tm.as<uint32_t>(),
-                                            t.s_theld.as<uint32_t>(), t.s_tstate.as<uint8_t>());
-        k_commit<kModeTtl><<<gW, B, 0, st>>>(
-            t.dev, t.d_ctr, t.s_elist.as<uint32_t>(), t.s_tkey.as<uint64_t>(),
-            t.s_tmin.as<unsigned>(), t.s_tm.as<uint32_t>(), t.s_theld.as<uint32_t>(),
-            t.s_tstate.as<uint8_t>(), t.s_tslot.as<uint64_t>(), t.s_toc.as<uint8_t>(), t.gen_clock,
-            t.s_reset.as<uint64_t>(), t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>());
-    } else {
-        k_claim<kModeDisabled><<<gW, B, 0, st>>>(
-            t.dev, a.now, t.d_ctr, t.s_elist.as<uint32_t>(), t.s_tkey.as<uint64_t>(),
-            t.s_tmin.as<unsigned>(), t.s_ta.as<uint32_t>(), t.s_tm.as<uint32_t>(),
-            t.s_theld.as<uint32_t>(), t.s_tstate.as<uint8_t>());
-        k_commit<kModeDisabled><<<gW, B, 0, st>>>(
-            t.dev, t.d_ctr, t.s_elist.as<uint32_t>(), t.s_tkey.as<uint64_t>(),
-            t.s_tmin.as<unsigned>(), t.s_tm.as<uint32_t>(), t.s_theld.as<uint32_t>(),
-            t.s_tstate.as<uint8_t>(), t.s_tslot.as<uint64_t>(), t.s_toc.as<uint8_t>(), t.gen_clock,
-            t.s_reset.as<uint64_t>(), t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>());
-    }
-    t.launches += 2;
+#define MPZCH_CLAIM_COMMIT(MODE)                                                                   \
+    k_claim<MODE><<<gW, B, 0, st>>>(t.dev, a.now, t.d_ctr, t.s_elist.as<uint32_t>(),              \
+                                    t.s_tkey.as<uint64_t>(), t.s_tmin.as<unsigned>(),              \
+                                    t.s_ta.as<uint32_t>(), t.s_tm.as<uint32_t>(),                  \
+                                    t.s_theld.as<uint32_t>(), t.s_tstate.as<uint8_t>());           \
+    k_commit<MODE><<<gW, B, 0, st>>>(t.dev, t.d_ctr, t.s_elist.as<uint32_t>(),                    \
+                                     t.s_tkey.as<uint64_t>(), t.s_tmin.as<unsigned>(),             \
+                                     t.s_tm.as<uint32_t>(), t.s_theld.as<uint32_t>(),              \
+                                     t.s_tstate.as<uint8_t>(), t.s_tslot.as<uint64_t>(),           \
+                                     t.s_toc.as<uint8_t>(), t.gen_clock, a.uniform_meta,           \
+                                     t.s_reset.as<uint64_t>(), t.s_evflag.as<uint8_t>(),           \
+                                     t.s_evslot.as<uint64_t>())
+    if (ttl) { MPZCH_CLAIM_COMMIT(kModeTtl); }
+    else { MPZCH_CLAIM_COMMIT(kModeDisabled); }
+#undef MPZCH_CLAIM_COMMIT
+    t.launches += 3;
     if (t.profiling) cudaEventRecord(t.ev[2], st);
-    k_finalize<<<gW, B, 0, st>>>(t.d_ctr, a.feats, t.s_newpos.as<uint32_t>(),
-                                 t.s_newent.as<uint32_t>(), t.s_tmin.as<unsigned>(),
-                                 t.s_tslot.as<uint64_t>(), t.s_toc.as<uint8_t>(), a.out_slots,
-                                 a.out_oc);
-    k_meta<<<gN, B, 0, st>>>(t.dev, t.d_ctr, n, a.out_slots, a.uniform_meta);
-    t.launches += 2;
+    k_finalize<<<gW, B, 0, st>>>(t.d_ctr, a.feats, newpos, t.s_newent.as<uint32_t>(),
+                                 t.s_tmin.as<unsigned>(), t.s_tslot.as<uint64_t>(),
+                                 t.s_toc.as<uint8_t>(), a.out_slots, a.out_oc);
+    ++t.launches;
     if (t.dim > 0) launch_reset_rows(t, t.s_reset.as<uint64_t>(), &t.d_ctr->reset_count, st);
-    if (a.pol->mode == kModeTtl) enqueue_compact_evicted(t, n, a.out_ev, a.ev_cap, st);
+    if (ttl) enqueue_compact_evicted(t, n, a.out_ev, a.ev_cap, st);
     k_cleanup<<<gW, B, 0, st>>>(t.d_ctr, t.s_elist.as<uint32_t>(), t.s_tkey.as<uint64_t>(),
                                 t.s_tmin.as<unsigned>(), t.s_tstate.as<uint8_t>());
     ++t.launches;

@@ -349,9 +349,9 @@ void run_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n,
         const uint64_t sectors = c.id_sectors + c.meta_sectors;
         const uint64_t n_final = n - c.new_count;
         p.probe_sectors += sectors;
-        // probe kernel: sectors read + 8 B id per position + 9 B result per final
-        // position + 12 B new-list record per new position
-        p.probe_bytes += 32 * sectors + 8 * n + 9 * n_final + 12ull * c.new_count;
+        // probe kernel: sectors read + 8 B id per position + 9 B result and one metadata
+        // sector written per final position + 12 B new-list record per new position
+        p.probe_bytes += 32 * sectors + 8 * n + (9 + 32) * n_final + 12ull * c.new_count;
         // whole batch (SURVEY 8d terms, counted per position): probe reads, 8 B id in,
         // 9 B result out, one metadata sector written per position, one identity sector +
         // 8 B row_generation per Inserted/Evicted position, 8*dim+1 B per reset row

@@ -1,0 +1,93 @@
+// sector_bench.cu -- random-sector ceiling calibration on one B200 ("calibrate a
+// random-sector ceiling ... so the gap between the layout and the memory system is visible").
+// Uniform random 32/64/128-byte reads over a >= 16 GiB array with several load flavours and
+// L2 fetch-granularity limits; plus random 8-byte writes (metadata-word pattern).
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+
+__device__ __forceinline__ uint64_t mix(uint64_t x) {
+    x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull; x ^= x >> 33;
+    return x;
+}
+
+template <int FLAVOR, int U, int BYTES>
+__global__ void __launch_bounds__(256) k_read(const uint64_t* __restrict__ a, uint64_t nsec, uint64_t n, uint64_t salt,
+                                              unsigned long long* sink) {
+    uint64_t acc = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * U;
+    for (uint64_t base = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * U; base < n; base += stride) {
+        uint64_t v[U][BYTES / 8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t s = mix(base + u + salt) % nsec;  // sector-of-BYTES index
+            const uint64_t* p = a + s * (BYTES / 8);
+#pragma unroll
+            for (int q = 0; q < BYTES / 32; ++q) {
+                const uint64_t* pq = p + 4 * q;
+                if (FLAVOR == 0)
+                    asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(v[u][4*q]), "=l"(v[u][4*q+1]), "=l"(v[u][4*q+2]), "=l"(v[u][4*q+3]) : "l"(pq));
+                else if (FLAVOR == 1)
+                    asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(v[u][4*q]), "=l"(v[u][4*q+1]), "=l"(v[u][4*q+2]), "=l"(v[u][4*q+3]) : "l"(pq));
+                else if (FLAVOR == 2)
+                    asm volatile("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(v[u][4*q]), "=l"(v[u][4*q+1]), "=l"(v[u][4*q+2]), "=l"(v[u][4*q+3]) : "l"(pq));
+                else
+                    asm volatile("ld.global.cs.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(v[u][4*q]), "=l"(v[u][4*q+1]), "=l"(v[u][4*q+2]), "=l"(v[u][4*q+3]) : "l"(pq));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int q = 0; q < BYTES / 8; ++q) acc += v[u][q];
+    }
+    if (acc == 0x1234567) atomicAdd(sink, 1ull);
+}
+
+__global__ void __launch_bounds__(256) k_write8(uint64_t* a, uint64_t nslots, uint64_t n, uint64_t salt) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        a[mix(i + salt) % nslots] = i;
+}
+
+template <class F>
+float timeit(F f, int reps) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    f();
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) f();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    return ms / reps;
+}
+
+int main(int argc, char** argv) {
+    const uint64_t bytes = 16ull << 30;
+    uint64_t* a;
+    if (cudaMalloc(&a, bytes) != cudaSuccess) { printf("alloc failed\n"); return 1; }
+    cudaMemset(a, 1, bytes);
+    unsigned long long* sink; cudaMalloc(&sink, 8);
+    const uint64_t n = 16ull << 20;  // 16M random accesses per launch
+    int dev; cudaGetDevice(&dev);
+    int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    printf("{\"device_sms\": %d, \"array_gib\": 16, \"accesses_per_launch\": %llu, \"results\": [\n", sms, (unsigned long long)n);
+    bool first = true;
+    for (int gran : {0, 32, 64, 128}) {
+        if (gran) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran);
+        size_t cur = 0; cudaDeviceGetLimit(&cur, cudaLimitMaxL2FetchGranularity);
+#define RUN(FL, U, B, NAME) { \
+            const uint64_t nsec = bytes / B; \
+            const unsigned grid = sms * 8; \
+            float ms = timeit([&] { k_read<FL, U, B><<<grid, 256>>>(a, nsec, n, 12345, sink); }, 5); \
+            printf("%s{\"op\": \"read\", \"flavor\": \"%s\", \"unroll\": %d, \"bytes\": %d, \"l2_fetch_gran\": %zu, \"ms\": %.4f, \"useful_gbs\": %.1f, \"maccess_s\": %.1f}\n", first ? "" : ",", NAME, U, B, cur, ms, n * (double)B / ms / 1e6, n / ms / 1e3); first = false; }
+        RUN(0, 1, 32, "default") RUN(0, 4, 32, "default") RUN(1, 4, 32, "nc") RUN(2, 1, 32, "cg") RUN(2, 4, 32, "cg")
+        RUN(2, 8, 32, "cg") RUN(3, 4, 32, "cs") RUN(2, 4, 64, "cg") RUN(2, 2, 128, "cg") RUN(0, 4, 64, "default")
+        {
+            float ms = timeit([&] { k_write8<<<sms * 8, 256>>>(a, bytes / 8, n, 777); }, 5);
+            printf(",{\"op\": \"write8\", \"l2_fetch_gran\": %zu, \"ms\": %.4f, \"useful_gbs\": %.1f, \"maccess_s\": %.1f}\n", cur, ms, n * 8.0 / ms / 1e6, n / ms / 1e3);
+        }
+    }
+    printf("]}\n");
+    return 0;
+}
