@@ -164,6 +164,34 @@ mpzch_status mpzch_make_cursor(mpzch_table* t, uint64_t* out_generation);
 mpzch_status mpzch_dirty_rows_since(const mpzch_table* t, uint64_t generation, uint64_t* out,
                                     uint64_t cap, uint64_t* out_n);
 
+/* ---- row-sharded mode: one handle per rank holds the logical shards
+ *      [shard_lo, shard_hi) of the layout (global row numbering unchanged, so results are
+ *      identical for every number of ranks).  A rank routes its positions to owners with
+ *      mpzch_route_device + an all-to-all (NCCL), owners remap with
+ *      mpzch_process_batch_device_marked, results travel back; see
+ *      paper_2602_17050_b200/sharded.py.  Copies (mpzch_copy_*) return the held rows only. */
+mpzch_status mpzch_table_create_sharded(const uint64_t* shard_capacities, uint32_t num_shards,
+                                        uint32_t max_probe, uint64_t seed, uint32_t dim,
+                                        uint64_t init_seed, int device, uint32_t shard_lo,
+                                        uint32_t shard_hi, mpzch_table** out);
+mpzch_status mpzch_held_rows(const mpzch_table* t, uint64_t* row_lo, uint64_t* row_hi,
+                             uint32_t* shard_lo, uint32_t* shard_hi);
+/* validation pass only (batch_engine.cpp:90-94): *out_bad_pos = first invalid position or ~0 */
+mpzch_status mpzch_validate_device(const mpzch_table* t, const uint64_t* ids, uint64_t n,
+                                   uint64_t* out_bad_pos, void* stream);
+/* stable partition of positions by owning part: perm[n] (device) lists positions part by part
+ * in input order; counts[parts] (host) the part sizes; shard_to_part[S] (host) the owners */
+mpzch_status mpzch_route_device(const mpzch_table* t, const uint64_t* ids, uint64_t n,
+                                const uint32_t* shard_to_part, uint32_t parts, uint32_t* perm,
+                                uint64_t* counts, void* stream);
+/* process_batch on device buffers; out_first_evicted[n] (device, nullable) gets 1 at the first
+ * position of every Evicted (id, feature) unique (how the sharded evicted list is assembled) */
+mpzch_status mpzch_process_batch_device_marked(mpzch_table* t, const uint64_t* ids,
+                                               const uint32_t* features, uint64_t n, uint64_t now,
+                                               const mpzch_policy* policy, uint64_t* out_slots,
+                                               uint8_t* out_outcomes, uint8_t* out_first_evicted,
+                                               uint64_t* out_evicted_n, void* stream);
+
 /* ---- in-library CUDA-event profiling (bench evidence).  When on, every batch records
  * events on its own launch stream around the probe kernel, the claim/commit kernels
  * and the whole batch, and the probe kernel counts the 32-byte sectors it reads. */

@@ -149,6 +149,17 @@ _SIGS = {
     "mpzch_write_row": (ctypes.c_int, [_vp, ctypes.c_uint64, _vp, _vp, ctypes.c_uint8]),
     "mpzch_make_cursor": (ctypes.c_int, [_vp, _u64p]),
     "mpzch_dirty_rows_since": (ctypes.c_int, [_vp, ctypes.c_uint64, _vp, ctypes.c_uint64, _u64p]),
+    "mpzch_table_create_sharded": (ctypes.c_int, [_u64p, ctypes.c_uint32, ctypes.c_uint32,
+                                                  ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
+                                                  ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32,
+                                                  ctypes.POINTER(_vp)]),
+    "mpzch_held_rows": (ctypes.c_int, [_vp, _u64p, _u64p, _u32p, _u32p]),
+    "mpzch_validate_device": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _u64p, _vp]),
+    "mpzch_route_device": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _u32p, ctypes.c_uint32, _vp,
+                                          _u64p, _vp]),
+    "mpzch_process_batch_device_marked": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_uint64,
+                                                         ctypes.c_uint64, ctypes.POINTER(_Policy),
+                                                         _vp, _vp, _vp, _u64p, _vp]),
     "mpzch_set_path": (ctypes.c_int, [_vp, ctypes.c_int]),
     "mpzch_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),
     "mpzch_get_profile": (ctypes.c_int, [_vp, ctypes.POINTER(_Profile)]),
@@ -270,13 +281,19 @@ class TableConfig:
 class MpzchTable:
     """Device-resident MpzchTable (proj/include/mpzch/table.hpp:41-131) on one B200."""
 
-    def __init__(self, cfg: TableConfig, device: int = 0):
+    def __init__(self, cfg: TableConfig, device: int = 0, shard_range: Optional[Tuple[int, int]] = None):
+        """shard_range=(lo, hi): row-sharded mode, hold only logical shards [lo, hi)."""
         lib = load_library()
         caps = np.ascontiguousarray(np.array(list(cfg.shard_capacities), dtype=np.uint64))
         h = _vp()
-        _check(lib.mpzch_table_create(caps.ctypes.data_as(_u64p) if caps.size else None,
-                                      len(caps), cfg.max_probe, cfg.seed, cfg.dim, cfg.init_seed,
-                                      device, ctypes.byref(h)))
+        cp = caps.ctypes.data_as(_u64p) if caps.size else None
+        if shard_range is None:
+            _check(lib.mpzch_table_create(cp, len(caps), cfg.max_probe, cfg.seed, cfg.dim,
+                                          cfg.init_seed, device, ctypes.byref(h)))
+        else:
+            _check(lib.mpzch_table_create_sharded(cp, len(caps), cfg.max_probe, cfg.seed, cfg.dim,
+                                                  cfg.init_seed, device, shard_range[0],
+                                                  shard_range[1], ctypes.byref(h)))
         self._h = h
         self._lib = lib
         self.cfg = cfg
@@ -289,6 +306,13 @@ class MpzchTable:
         offs = np.zeros(len(caps) + 1, dtype=np.uint64)
         _check(lib.mpzch_shard_layout(h, caps.ctypes.data_as(_u64p), offs.ctypes.data_as(_u64p)))
         self.shard_offsets = offs
+        rl, rh = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        sl, sh = ctypes.c_uint32(0), ctypes.c_uint32(0)
+        _check(lib.mpzch_held_rows(h, ctypes.byref(rl), ctypes.byref(rh), ctypes.byref(sl),
+                                   ctypes.byref(sh)))
+        self.row_lo, self.row_hi = rl.value, rh.value
+        self.shard_lo, self.shard_hi = sl.value, sh.value
+        self.held_rows = self.row_hi - self.row_lo
 
     def close(self):
         if getattr(self, "_h", None):
@@ -348,6 +372,48 @@ class MpzchTable:
             ctypes.c_void_p(st.cuda_stream)))
         return nev.value
 
+    # ---- row-sharded helpers (device tensors) ------------------------------------------
+    def validate_device(self, ids, stream=None) -> Optional[int]:
+        """First invalid position of a device id tensor, or None."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        bad = ctypes.c_uint64(0)
+        _check(self._lib.mpzch_validate_device(self._h, ctypes.c_void_p(ids.data_ptr()), ids.numel(),
+                                               ctypes.byref(bad), ctypes.c_void_p(st.cuda_stream)))
+        return None if bad.value == (1 << 64) - 1 else bad.value
+
+    def route_device(self, ids, shard_to_part, parts: int, stream=None):
+        """(perm int32 device tensor, counts list): positions grouped by owning part, stable."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        perm = torch.empty(ids.numel(), dtype=torch.int32, device=ids.device)
+        s2p = np.ascontiguousarray(shard_to_part, dtype=np.uint32)
+        counts = np.zeros(parts, dtype=np.uint64)
+        _check(self._lib.mpzch_route_device(self._h, ctypes.c_void_p(ids.data_ptr()), ids.numel(),
+                                            s2p.ctypes.data_as(_u32p), parts,
+                                            ctypes.c_void_p(perm.data_ptr()),
+                                            counts.ctypes.data_as(_u64p),
+                                            ctypes.c_void_p(st.cuda_stream)))
+        return perm, [int(c) for c in counts]
+
+    def process_batch_device_marked(self, ids, now: int, policy: EvictionPolicy, features=None,
+                                    stream=None):
+        """(slots, outcomes, first_evicted_marks) device tensors for device ids."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        n = ids.numel()
+        slots = torch.empty(n, dtype=torch.int64, device=ids.device)
+        oc = torch.empty(n, dtype=torch.uint8, device=ids.device)
+        mark = torch.empty(n, dtype=torch.uint8, device=ids.device)
+        nev = ctypes.c_uint64(0)
+        _check(self._lib.mpzch_process_batch_device_marked(
+            self._h, ctypes.c_void_p(ids.data_ptr()),
+            ctypes.c_void_p(features.data_ptr()) if features is not None else None, n, now,
+            ctypes.byref(policy._c), ctypes.c_void_p(slots.data_ptr()), ctypes.c_void_p(oc.data_ptr()),
+            ctypes.c_void_p(mark.data_ptr()) if n else None, ctypes.byref(nev),
+            ctypes.c_void_p(st.cuda_stream)))
+        return slots, oc, mark
+
     def lookup(self, ids) -> Tuple[np.ndarray, np.ndarray]:
         """Batched MpzchTable::lookup (table.cpp:150-156): (slots, outcomes), no writes."""
         ids = np.ascontiguousarray(ids, dtype=np.uint64)
@@ -374,48 +440,53 @@ class MpzchTable:
 
     # ---- state (parity) ------------------------------------------------------------------
     def identities_all(self) -> np.ndarray:
-        out = np.empty(self.total_rows, dtype=np.uint64)
+        """identity words of the held rows [row_lo, row_hi) (all rows unless sharded)."""
+        out = np.empty(self.held_rows, dtype=np.uint64)
         _check(self._lib.mpzch_copy_identities(self._h, _ptr(out)))
         return out
 
     def metadata_all(self) -> np.ndarray:
-        out = np.empty(self.total_rows, dtype=np.uint64)
+        out = np.empty(self.held_rows, dtype=np.uint64)
         _check(self._lib.mpzch_copy_metadata(self._h, _ptr(out)))
         return out
 
     def identities(self, shard: int) -> np.ndarray:
         self._check_shard(shard)
-        a, b = int(self.shard_offsets[shard]), int(self.shard_offsets[shard + 1])
+        a, b = int(self.shard_offsets[shard]) - self.row_lo, int(self.shard_offsets[shard + 1]) - self.row_lo
         return self.identities_all()[a:b]
 
     def metadata(self, shard: int) -> np.ndarray:
         self._check_shard(shard)
-        a, b = int(self.shard_offsets[shard]), int(self.shard_offsets[shard + 1])
+        a, b = int(self.shard_offsets[shard]) - self.row_lo, int(self.shard_offsets[shard + 1]) - self.row_lo
         return self.metadata_all()[a:b]
 
     def _check_shard(self, shard):
         if shard < 0 or shard >= self.num_shards:
             raise OutOfRange("shard index out of range")
+        if shard < self.shard_lo or shard >= self.shard_hi:
+            raise OutOfRange("shard is not held by this handle")
 
-    def weights(self, row0: int = 0, nrows: Optional[int] = None) -> np.ndarray:
-        nrows = self.total_rows - row0 if nrows is None else nrows
+    def weights(self, row0: Optional[int] = None, nrows: Optional[int] = None) -> np.ndarray:
+        row0 = self.row_lo if row0 is None else row0
+        nrows = self.row_hi - row0 if nrows is None else nrows
         out = np.empty((nrows, max(self.dim, 1)), dtype=np.float32)
         _check(self._lib.mpzch_copy_weights(self._h, row0, nrows, _ptr(out)))
         return out
 
-    def momentum(self, row0: int = 0, nrows: Optional[int] = None) -> np.ndarray:
-        nrows = self.total_rows - row0 if nrows is None else nrows
+    def momentum(self, row0: Optional[int] = None, nrows: Optional[int] = None) -> np.ndarray:
+        row0 = self.row_lo if row0 is None else row0
+        nrows = self.row_hi - row0 if nrows is None else nrows
         out = np.empty((nrows, max(self.dim, 1)), dtype=np.float32)
         _check(self._lib.mpzch_copy_momentum(self._h, row0, nrows, _ptr(out)))
         return out
 
     def trained(self) -> np.ndarray:
-        out = np.empty(self.total_rows, dtype=np.uint8)
+        out = np.empty(self.held_rows, dtype=np.uint8)
         _check(self._lib.mpzch_copy_trained(self._h, _ptr(out)))
         return out
 
     def row_generation(self) -> np.ndarray:
-        out = np.empty(self.total_rows, dtype=np.uint64)
+        out = np.empty(self.held_rows, dtype=np.uint64)
         _check(self._lib.mpzch_copy_row_generation(self._h, _ptr(out)))
         return out
 
@@ -447,7 +518,7 @@ class MpzchTable:
         return g.value
 
     def dirty_rows_since(self, cursor: int) -> np.ndarray:
-        out = np.empty(self.total_rows, dtype=np.uint64)
+        out = np.empty(self.held_rows, dtype=np.uint64)
         n = ctypes.c_uint64(0)
         _check(self._lib.mpzch_dirty_rows_since(self._h, cursor, _ptr(out), out.size, ctypes.byref(n)))
         return out[:n.value].copy()

@@ -75,7 +75,11 @@ struct TableDev {
     FastMod nshards;
     uint64_t seed;
     uint64_t init_seed;
-    uint64_t total;
+    uint64_t total;      // rows of the whole layout (global row numbering)
+    uint64_t row_lo;     // rows this handle holds: [row_lo, row_hi) (all rows unless sharded)
+    uint64_t row_hi;
+    uint32_t shard_lo;   // logical shards this handle holds: [shard_lo, shard_hi)
+    uint32_t shard_hi;
     double bound;        // 1/sqrt(dim), computed on the host exactly as draw_row does
     uint32_t P;          // max_probe
     uint32_t dim;
@@ -85,6 +89,10 @@ __device__ __forceinline__ uint32_t shard_of(uint64_t id, const TableDev& t) {
     return (uint32_t)fastmod(mix64(id ^ kShardSalt, t.seed), t.nshards);
 }
 
+__device__ __forceinline__ bool holds_shard(const TableDev& t, uint32_t s) {
+    return s >= t.shard_lo && s < t.shard_hi;
+}
+
 __device__ __forceinline__ uint64_t home_of(uint64_t id, const ShardDev& s, uint64_t seed) {
     return fastmod(mix64(id ^ kHomeSalt, seed), s.cap);
 }
@@ -92,13 +100,14 @@ __device__ __forceinline__ uint64_t home_of(uint64_t id, const ShardDev& s, uint
 // Error word shared by all kernels of one batch.  Mutating kernels return
 // immediately when any field is set, so an invalid batch mutates nothing.
 struct BatchErr {
-    unsigned long long bad_pos;  // min invalid position, ~0 if none
-    unsigned int overflow;       // TTL expiry overflow seen
-    unsigned int too_many;       // fast-path capacity exceeded (never with sane n)
+    unsigned long long bad_pos;      // min invalid position, ~0 if none
+    unsigned int overflow;           // TTL expiry overflow seen
+    unsigned int too_many;           // internal invariant violated
+    unsigned long long foreign_pos;  // min position whose shard this handle does not hold
 };
 
 __device__ __forceinline__ bool batch_failed(const BatchErr* e) {
-    return e->bad_pos != ~0ull || e->overflow != 0 || e->too_many != 0;
+    return e->bad_pos != ~0ull || e->overflow != 0 || e->too_many != 0 || e->foreign_pos != ~0ull;
 }
 
 // L2-coherent loads/stores for state that other threads mutate in the same kernel.

@@ -31,6 +31,10 @@ __global__ void __launch_bounds__(256) k_lookup(TableDev t, const uint64_t* __re
             continue;
         }
         const uint32_t s = shard_of(id, t);
+        if (!holds_shard(t, s)) {
+            atomicMin(&err->foreign_pos, (unsigned long long)i);
+            continue;
+        }
         const ShardDev sd = t.shards[s];
         const uint64_t cap = sd.cap.d, base = sd.offset, end = base + cap;
         const uint64_t h = home_of(id, sd, t.seed);

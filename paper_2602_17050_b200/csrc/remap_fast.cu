@@ -66,6 +66,7 @@ __global__ void k_init_counters(BatchCounters* c) {
     if (threadIdx.x == 0) {
         BatchCounters z{};
         z.err.bad_pos = ~0ull;
+        z.err.foreign_pos = ~0ull;
         *c = z;
     }
 }
@@ -94,8 +95,8 @@ __device__ __forceinline__ uint32_t first_expired(const uint64_t* __restrict__ m
 
 // K0: streaming validation of the batch (batch_engine.cpp:90-94): min invalid position.
 // Runs before anything mutates, so the probe can write metadata for final positions.
-__global__ void __launch_bounds__(256) k_validate(const uint64_t* __restrict__ ids, uint64_t n,
-                                                  BatchCounters* ctr) {
+__global__ void __launch_bounds__(256) k_validate(TableDev t, const uint64_t* __restrict__ ids,
+                                                  uint64_t n, BatchCounters* ctr) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long bad = ~0ull;
@@ -112,6 +113,15 @@ __global__ void __launch_bounds__(256) k_validate(const uint64_t* __restrict__ i
             if (ids[i] >> 63) bad = min(bad, (unsigned long long)i);
     }
     if (bad != ~0ull) atomicMin(&ctr->err.bad_pos, bad);
+    // row-sharded handle: every id must route to a shard it holds
+    if (t.shard_lo != 0 || t.shard_hi != t.nshards.d) {
+        unsigned long long foreign = ~0ull;
+        for (uint64_t i = tid; i < n; i += stride) {
+            const uint64_t id = ids[i];
+            if (!(id >> 63) && !holds_shard(t, shard_of(id, t))) foreign = min(foreign, (unsigned long long)i);
+        }
+        if (foreign != ~0ull) atomicMin(&ctr->err.foreign_pos, foreign);
+    }
 }
 
 // K1: probe; each thread keeps U positions in flight (independent sector loads), all
@@ -497,6 +507,15 @@ __global__ void __launch_bounds__(256) k_cleanup(BatchCounters* ctr, const uint3
 
 }  // namespace
 
+void run_validate(Table& t, const uint64_t* ids, uint64_t n, cudaStream_t st) {
+    k_init_counters<<<1, 32, 0, st>>>(t.d_ctr);
+    k_validate<<<grid_for(n / 2 + 1, 256, 148u * 8u), 256, 0, st>>>(t.dev, ids, n, t.d_ctr);
+    t.launches += 2;
+    MPZCH_CUDA(cudaGetLastError());
+    MPZCH_CUDA(cudaMemcpyAsync(&t.h_ctr->err, &t.d_ctr->err, sizeof(BatchErr), cudaMemcpyDeviceToHost, st));
+    MPZCH_CUDA(cudaStreamSynchronize(st));
+}
+
 void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     constexpr int kU = 2;  // positions in flight per probe thread
     const uint64_t n = a.n;
@@ -509,7 +528,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     uint32_t* newa = t.s_newa.as<uint32_t>();
     uint32_t* newm = t.s_newm.as<uint32_t>();
     k_init_counters<<<1, 32, 0, st>>>(t.d_ctr);
-    k_validate<<<grid_for(n / 2 + 1, B, 148u * 8u), B, 0, st>>>(a.ids, n, t.d_ctr);
+    k_validate<<<grid_for(n / 2 + 1, B, 148u * 8u), B, 0, st>>>(t.dev, a.ids, n, t.d_ctr);
     t.launches += 2;
     if (a.overflow_all) return;  // validation only; the host reports the error
     if (t.profiling) cudaEventRecord(t.ev[0], st);
@@ -547,6 +566,10 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
                                  t.s_toc.as<uint8_t>(), a.out_slots, a.out_oc);
     ++t.launches;
     if (t.dim > 0) launch_reset_rows(t, t.s_reset.as<uint64_t>(), &t.d_ctr->reset_count, st);
+    if (a.out_mark) {  // first positions of Evicted uniques (row-sharded evicted list)
+        if (ttl) MPZCH_CUDA(cudaMemcpyAsync(a.out_mark, t.s_evflag.p, n, cudaMemcpyDeviceToDevice, st));
+        else MPZCH_CUDA(cudaMemsetAsync(a.out_mark, 0, n, st));
+    }
     if (ttl) enqueue_compact_evicted(t, n, a.out_ev, a.ev_cap, st);
     k_cleanup<<<gW, B, 0, st>>>(t.d_ctr, t.s_elist.as<uint32_t>(), t.s_tkey.as<uint64_t>(),
                                 t.s_tmin.as<unsigned>(), t.s_tstate.as<uint8_t>());

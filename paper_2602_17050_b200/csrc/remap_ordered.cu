@@ -37,11 +37,12 @@ __global__ void k_init_counters_o(BatchCounters* c) {
     if (threadIdx.x == 0) {
         BatchCounters z{};
         z.err.bad_pos = ~0ull;
+        z.err.foreign_pos = ~0ull;
         *c = z;
     }
 }
 
-__global__ void __launch_bounds__(256) k_validate_dedup(const uint64_t* __restrict__ ids,
+__global__ void __launch_bounds__(256) k_validate_dedup(TableDev t, const uint64_t* __restrict__ ids,
                                                         const uint32_t* __restrict__ feats, uint64_t n,
                                                         uint64_t now, int mode, uint64_t def_ttl,
                                                         const uint32_t* fk, const uint64_t* fv,
@@ -54,6 +55,11 @@ __global__ void __launch_bounds__(256) k_validate_dedup(const uint64_t* __restri
         const uint32_t f = feats ? feats[i] : 0u;
         if (id >> 63) {
             atomicMin(&ctr->err.bad_pos, (unsigned long long)i);
+            posent[i] = kNone32;
+            continue;
+        }
+        if (!holds_shard(t, shard_of(id, t))) {
+            atomicMin(&ctr->err.foreign_pos, (unsigned long long)i);
             posent[i] = kNone32;
             continue;
         }
@@ -131,8 +137,8 @@ __global__ void __launch_bounds__(256) k_ordered(TableDev t, BatchCounters* ctr,
                                                  uint8_t* __restrict__ evflag,
                                                  uint64_t* __restrict__ evslot) {
     if (batch_failed(&ctr->err)) return;
-    const uint32_t shard = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (shard >= t.nshards.d) return;
+    const uint32_t shard = t.shard_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (shard >= t.shard_hi) return;
     const unsigned lane = lane_id();
     const unsigned u = ctr->entry_count;
     const ShardDev sd = t.shards[shard];
@@ -254,6 +260,16 @@ __global__ void __launch_bounds__(256) k_scatter(BatchCounters* ctr, uint64_t n,
     }
 }
 
+__global__ void __launch_bounds__(256) k_mark_first(const BatchCounters* ctr,
+                                                    const uint32_t* __restrict__ upos,
+                                                    const uint8_t* __restrict__ evflag,
+                                                    uint8_t* __restrict__ mark) {
+    if (batch_failed(&ctr->err)) return;
+    const unsigned u = ctr->entry_count;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < u; k += gridDim.x * blockDim.x)
+        if (evflag[k]) mark[upos[k]] = 1;
+}
+
 __global__ void __launch_bounds__(256) k_cleanup_o(uint64_t n, const uint32_t* __restrict__ posent,
                                                    u128* key, unsigned* kmin) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -281,7 +297,7 @@ void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     u128* key = t.o_key.as<u128>();
     unsigned* kmin = t.o_min.as<unsigned>();
     uint32_t* posent = t.o_posent.as<uint32_t>();
-    k_validate_dedup<<<gN, B, 0, st>>>(a.ids, a.feats, n, a.now, p.mode, p.default_ttl, a.d_featk,
+    k_validate_dedup<<<gN, B, 0, st>>>(t.dev, a.ids, a.feats, n, a.now, p.mode, p.default_ttl, a.d_featk,
                                        a.d_featv, nk, t.d_ctr, key, kmin, posent, mask);
     k_first_flags<<<gN, B, 0, st>>>(t.d_ctr, n, posent, kmin, t.o_flag.as<uint8_t>());
     t.launches += 3;
@@ -291,7 +307,7 @@ void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     k_prep<<<gN, B, 0, st>>>(t.dev, t.d_ctr, a.ids, a.feats, t.o_upos.as<uint32_t>(), a.now, p.mode,
                              p.default_ttl, a.d_featk, a.d_featv, nk, t.o_ushard.as<uint32_t>(),
                              t.o_umeta.as<uint64_t>());
-    const unsigned gS = (unsigned)(((uint64_t)t.S * 32 + B - 1) / B);
+    const unsigned gS = (unsigned)(((uint64_t)(t.shard_hi - t.shard_lo) * 32 + B - 1) / B);
 #define MPZCH_ORDERED(MODE)                                                                       \
     k_ordered<MODE><<<gS, B, 0, st>>>(t.dev, t.d_ctr, a.ids, t.o_upos.as<uint32_t>(),             \
                                       t.o_ushard.as<uint32_t>(), t.o_umeta.as<uint64_t>(), a.now, \
@@ -306,6 +322,12 @@ void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
                                 t.o_uoc.as<uint8_t>(), a.out_slots, a.out_oc);
     t.launches += 3;
     if (t.dim > 0) launch_reset_rows(t, t.s_reset.as<uint64_t>(), &t.d_ctr->reset_count, st);
+    if (a.out_mark) {  // unique k's first position is upos[k]
+        MPZCH_CUDA(cudaMemsetAsync(a.out_mark, 0, n, st));
+        k_mark_first<<<gN, B, 0, st>>>(t.d_ctr, t.o_upos.as<uint32_t>(), t.s_evflag.as<uint8_t>(),
+                                       a.out_mark);
+        ++t.launches;
+    }
     if (p.mode != kModeDisabled) enqueue_compact_evicted(t, n, a.out_ev, a.ev_cap, st);
     k_cleanup_o<<<gN, B, 0, st>>>(n, posent, key, kmin);
     ++t.launches;

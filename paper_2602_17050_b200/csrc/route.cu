@@ -1,0 +1,147 @@
+// route.cu -- routing of a rank's positions to the ranks that own their logical shards
+// (row-sharded mode).  shard_of (proj/src/shard_router.cpp:42-46) decides the
+// shard; a host table maps shards to parts (ranks).  The permutation is STABLE: within a
+// part, positions keep their input order, so after the all-to-all the owner sees every
+// source's positions in global first-occurrence order (the reference's dedup order,
+// proj/src/batch_engine.cpp:100-106) without any sort.
+//
+//   k_route_count  one warp per 1024-position chunk: per-part counts (ballot + popc)
+//   k_route_scan   one block: part-major exclusive scan of the chunk counts
+//   k_route_write  one warp per chunk: ballot ranks -> perm[offset + rank] = position
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "table.hpp"
+
+namespace mpzch_b200 {
+
+namespace {
+
+constexpr unsigned kChunk = 1024;
+constexpr unsigned kMaxParts = 64;
+
+__device__ __forceinline__ uint32_t part_of(uint64_t id, const TableDev& t, const uint8_t* s2p) {
+    return s2p[shard_of(id, t)];
+}
+
+__global__ void __launch_bounds__(256) k_route_count(TableDev t, const uint64_t* __restrict__ ids,
+                                                     uint64_t n, const uint8_t* __restrict__ s2p,
+                                                     uint32_t parts, unsigned* __restrict__ cnt,
+                                                     uint64_t nchunks) {
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned lane = lane_id();
+    if (warp >= nchunks) return;
+    unsigned c = 0;  // lane p accumulates part p (parts <= 32 per lane slot, see below)
+    unsigned c2 = 0; // parts 32..63
+    for (uint64_t i0 = warp * kChunk; i0 < (warp + 1) * kChunk && i0 < n; i0 += 32) {
+        const uint64_t i = i0 + lane;
+        const uint32_t p = i < n ? part_of(ids[i], t, s2p) : kNone32;
+        for (uint32_t q = 0; q < parts; ++q) {
+            const unsigned m = __ballot_sync(0xffffffffu, p == q);
+            if (lane == (q & 31)) (q < 32 ? c : c2) += __popc(m);
+        }
+    }
+    if (lane < parts) cnt[(uint64_t)lane * nchunks + warp] = c;
+    if (lane + 32 < parts) cnt[(uint64_t)(lane + 32) * nchunks + warp] = c2;
+}
+
+__global__ void __launch_bounds__(256) k_route_write(TableDev t, const uint64_t* __restrict__ ids,
+                                                     uint64_t n, const uint8_t* __restrict__ s2p,
+                                                     uint32_t parts, const unsigned* __restrict__ off,
+                                                     uint64_t nchunks, uint32_t* __restrict__ perm) {
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned lane = lane_id();
+    if (warp >= nchunks) return;
+    unsigned base = lane < parts ? off[(uint64_t)lane * nchunks + warp] : 0;
+    unsigned base2 = lane + 32 < parts ? off[(uint64_t)(lane + 32) * nchunks + warp] : 0;
+    for (uint64_t i0 = warp * kChunk; i0 < (warp + 1) * kChunk && i0 < n; i0 += 32) {
+        const uint64_t i = i0 + lane;
+        const uint32_t p = i < n ? part_of(ids[i], t, s2p) : kNone32;
+        for (uint32_t q = 0; q < parts; ++q) {
+            const unsigned m = __ballot_sync(0xffffffffu, p == q);
+            if (!m) continue;
+            const unsigned b = __shfl_sync(0xffffffffu, q < 32 ? base : base2, q & 31);
+            if (p == q) perm[b + __popc(m & ((1u << lane) - 1))] = (uint32_t)i;
+            if (lane == (q & 31)) (q < 32 ? base : base2) += __popc(m);
+        }
+    }
+}
+
+}  // namespace
+
+// exclusive scan over cnt (part-major), declared in compact.cuh's style
+__global__ void k_route_scan(unsigned* cnt, uint64_t total, unsigned* part_totals, uint32_t parts,
+                             uint64_t nchunks);
+
+__global__ void __launch_bounds__(1024) k_route_scan(unsigned* cnt, uint64_t total,
+                                                     unsigned* part_totals, uint32_t parts,
+                                                     uint64_t nchunks) {
+    __shared__ unsigned wsum[32];
+    __shared__ unsigned carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint64_t b0 = 0; b0 < total; b0 += 1024) {
+        const uint64_t i = b0 + threadIdx.x;
+        const unsigned v = i < total ? cnt[i] : 0;
+        unsigned x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+            if ((threadIdx.x & 31) >= (unsigned)o) x += y;
+        }
+        if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = x;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            unsigned w = wsum[threadIdx.x];
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, w, o);
+                if (threadIdx.x >= (unsigned)o) w += y;
+            }
+            wsum[threadIdx.x] = w;
+        }
+        __syncthreads();
+        const unsigned incl = x + ((threadIdx.x >> 5) ? wsum[(threadIdx.x >> 5) - 1] : 0);
+        if (i < total) cnt[i] = carry + incl - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += incl;
+        __syncthreads();
+    }
+    // per-part totals: difference of consecutive part starts
+    if (threadIdx.x < parts) {
+        const uint64_t s = (uint64_t)threadIdx.x * nchunks;
+        const unsigned start = cnt[s];
+        const unsigned end = threadIdx.x + 1 < parts ? cnt[s + nchunks] : carry;
+        part_totals[threadIdx.x] = end - start;
+    }
+}
+
+void run_route(Table& t, const uint64_t* ids, uint64_t n, const uint32_t* shard_to_part,
+               uint32_t parts, uint32_t* perm, uint64_t* counts, cudaStream_t st) {
+    if (parts == 0 || parts > kMaxParts) throw Error{MPZCH_EINVAL, "route: 1..64 parts"};
+    for (uint32_t s = 0; s < t.S; ++s)
+        if (shard_to_part[s] >= parts) throw Error{MPZCH_EINVAL, "route: shard mapped to no part"};
+    const uint64_t nchunks = (n + kChunk - 1) / kChunk;
+    DevBuf s2p, cnt, tot;
+    s2p.reserve(t.S);
+    cnt.reserve(std::max<uint64_t>(1, nchunks * parts) * 4);
+    tot.reserve(parts * 4);
+    std::vector<uint8_t> h(t.S);
+    for (uint32_t s = 0; s < t.S; ++s) h[s] = (uint8_t)shard_to_part[s];
+    MPZCH_CUDA(cudaMemcpyAsync(s2p.p, h.data(), t.S, cudaMemcpyHostToDevice, st));
+    std::vector<unsigned> ht(parts, 0);
+    if (n) {
+        const unsigned blocks = (unsigned)((nchunks * 32 + 255) / 256);
+        k_route_count<<<blocks, 256, 0, st>>>(t.dev, ids, n, s2p.as<uint8_t>(), parts,
+                                              cnt.as<unsigned>(), nchunks);
+        k_route_scan<<<1, 1024, 0, st>>>(cnt.as<unsigned>(), nchunks * parts, tot.as<unsigned>(), parts,
+                                         nchunks);
+        k_route_write<<<blocks, 256, 0, st>>>(t.dev, ids, n, s2p.as<uint8_t>(), parts,
+                                              cnt.as<unsigned>(), nchunks, perm);
+        t.launches += 3;
+        MPZCH_CUDA(cudaGetLastError());
+        MPZCH_CUDA(cudaMemcpyAsync(ht.data(), tot.p, parts * 4, cudaMemcpyDeviceToHost, st));
+    }
+    MPZCH_CUDA(cudaStreamSynchronize(st));
+    for (uint32_t p = 0; p < parts; ++p) counts[p] = ht[p];
+}
+
+}  // namespace mpzch_b200

@@ -28,26 +28,28 @@ __device__ __forceinline__ float draw_elem(uint64_t s0, uint64_t j, double bound
 __global__ void __launch_bounds__(256) k_draw_all(TableDev t) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t held = t.row_hi - t.row_lo;
     if ((t.dim & 3u) == 0) {
         const uint64_t quads = t.dim / 4;
-        const uint64_t nq = t.total * quads;
+        const uint64_t nq = held * quads;
+        float4* w4 = reinterpret_cast<float4*>(t.weights + t.row_lo * t.dim);
         for (uint64_t q = tid; q < nq; q += stride) {
-            const uint64_t row = q / quads;
-            const uint64_t j = (q - row * quads) * 4;
+            const uint64_t row = t.row_lo + q / quads;
+            const uint64_t j = (q % quads) * 4;
             const uint64_t s0 = mix64(row, t.init_seed);
             float4 w;
             w.x = draw_elem(s0, j, t.bound);
             w.y = draw_elem(s0, j + 1, t.bound);
             w.z = draw_elem(s0, j + 2, t.bound);
             w.w = draw_elem(s0, j + 3, t.bound);
-            reinterpret_cast<float4*>(t.weights)[q] = w;
+            w4[q] = w;
         }
     } else {
-        const uint64_t ne = t.total * t.dim;
+        const uint64_t ne = held * t.dim;
         for (uint64_t x = tid; x < ne; x += stride) {
-            const uint64_t row = x / t.dim;
-            const uint64_t j = x - row * t.dim;
-            t.weights[x] = draw_elem(mix64(row, t.init_seed), j, t.bound);
+            const uint64_t row = t.row_lo + x / t.dim;
+            const uint64_t j = x % t.dim;
+            t.weights[row * t.dim + j] = draw_elem(mix64(row, t.init_seed), j, t.bound);
         }
     }
 }
@@ -101,7 +103,7 @@ __global__ void k_write_slots(TableDev t, const uint64_t* __restrict__ g, const 
 // Hole check: every id stored inside its own probe window at
 // offset o must see neither EMPTY nor another copy of itself in [home, home+o).
 __global__ void __launch_bounds__(256) k_hole_check(TableDev t, unsigned* bad) {
-    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < t.total;
+    for (uint64_t g = t.row_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < t.row_hi;
          g += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t id = t.ident[g];
         if (id == kEmpty) continue;
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(256) k_hole_check(TableDev t, unsigned* bad) {
 }  // namespace
 
 void launch_init_table(Table& t) {
-    if (t.dim == 0 || t.total == 0) return;
+    if (t.dim == 0 || t.held_rows() == 0) return;
     k_draw_all<<<148 * 16, 256, 0, t.stream>>>(t.dev);
     ++t.launches;
     MPZCH_CUDA(cudaGetLastError());
@@ -149,7 +151,7 @@ bool run_hole_check(Table& t) {
     unsigned* d_bad = nullptr;
     MPZCH_CUDA(cudaMallocAsync((void**)&d_bad, sizeof(unsigned), t.stream));
     MPZCH_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned), t.stream));
-    k_hole_check<<<grid_for(t.total, 256), 256, 0, t.stream>>>(t.dev, d_bad);
+    k_hole_check<<<grid_for(t.held_rows(), 256), 256, 0, t.stream>>>(t.dev, d_bad);
     ++t.launches;
     unsigned bad = 0;
     MPZCH_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(unsigned), cudaMemcpyDeviceToHost, t.stream));

@@ -69,7 +69,7 @@ static uint64_t pow2_at_least(uint64_t x) {
 }
 
 Table::Table(const uint64_t* cap_in, uint32_t num_shards, uint32_t max_probe, uint64_t seed_in,
-             uint32_t dim_in, uint64_t init_seed_in, int device_in) {
+             uint32_t dim_in, uint64_t init_seed_in, int device_in, uint32_t lo, uint32_t hi) {
     // TableLayout::with_capacities shard_router.cpp:8-25, ShardConfig::validate probe_core.cpp:8-15
     if (num_shards == 0) throw Error{MPZCH_EINVAL, "layout needs at least one shard"};
     for (uint32_t s = 0; s < num_shards; ++s)
@@ -87,36 +87,50 @@ Table::Table(const uint64_t* cap_in, uint32_t num_shards, uint32_t max_probe, ui
     offsets.assign(num_shards + 1, 0);
     for (uint32_t s = 0; s < S; ++s) offsets[s + 1] = offsets[s] + caps[s];
     total = offsets[S];
+    if (hi == ~0u) hi = S;
+    if (lo >= hi || hi > S) throw Error{MPZCH_ERANGE, "shard range out of range"};
+    shard_lo = lo;
+    shard_hi = hi;
+    row_lo = offsets[lo];
+    row_hi = offsets[hi];
+    row_base = row_lo & ~3ull;
+    const uint64_t held = row_hi - row_lo;
 
     DeviceGuard g(device);
     MPZCH_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     MPZCH_CUDA(cudaMallocHost((void**)&h_ctr, sizeof(BatchCounters)));
     MPZCH_CUDA(cudaMalloc((void**)&d_ctr, sizeof(BatchCounters)));
-    // identity/metadata padded so a 32-byte sector load at the last slot stays in bounds
-    const uint64_t padded = ((total + 3) & ~3ull) + 4;
+    // identity/metadata start 4-row aligned and are padded so a 32-byte sector load at the
+    // first or last held slot stays in bounds
+    const uint64_t padded = ((row_hi - row_base + 3) & ~3ull) + 4;
     MPZCH_CUDA(cudaMalloc((void**)&ident, padded * sizeof(uint64_t)));
     MPZCH_CUDA(cudaMalloc((void**)&meta, padded * sizeof(uint64_t)));
-    MPZCH_CUDA(cudaMalloc((void**)&row_gen, total * sizeof(uint64_t)));
+    MPZCH_CUDA(cudaMalloc((void**)&row_gen, held * sizeof(uint64_t)));
     MPZCH_CUDA(cudaMemsetAsync(ident, 0xff, padded * sizeof(uint64_t), stream));
     MPZCH_CUDA(cudaMemsetAsync(meta, 0, padded * sizeof(uint64_t), stream));
-    MPZCH_CUDA(cudaMemsetAsync(row_gen, 0, total * sizeof(uint64_t), stream));
+    MPZCH_CUDA(cudaMemsetAsync(row_gen, 0, held * sizeof(uint64_t), stream));
     if (dim > 0) {
-        MPZCH_CUDA(cudaMalloc((void**)&weights, total * dim * sizeof(float)));
-        MPZCH_CUDA(cudaMalloc((void**)&momentum, total * dim * sizeof(float)));
-        MPZCH_CUDA(cudaMalloc((void**)&trained, total));
-        MPZCH_CUDA(cudaMemsetAsync(momentum, 0, total * dim * sizeof(float), stream));
-        MPZCH_CUDA(cudaMemsetAsync(trained, 0, total, stream));
+        MPZCH_CUDA(cudaMalloc((void**)&weights, held * dim * sizeof(float)));
+        MPZCH_CUDA(cudaMalloc((void**)&momentum, held * dim * sizeof(float)));
+        MPZCH_CUDA(cudaMalloc((void**)&trained, held));
+        MPZCH_CUDA(cudaMemsetAsync(momentum, 0, held * dim * sizeof(float), stream));
+        MPZCH_CUDA(cudaMemsetAsync(trained, 0, held, stream));
     }
     std::vector<ShardDev> hs(S);
     for (uint32_t s = 0; s < S; ++s) hs[s] = ShardDev{offsets[s], make_fastmod(caps[s])};
     MPZCH_CUDA(cudaMalloc((void**)&d_shards, S * sizeof(ShardDev)));
     MPZCH_CUDA(cudaMemcpyAsync(d_shards, hs.data(), S * sizeof(ShardDev), cudaMemcpyHostToDevice, stream));
-    dev.ident = ident;
-    dev.meta = meta;
-    dev.weights = weights;
-    dev.momentum = momentum;
-    dev.trained = trained;
-    dev.row_gen = row_gen;
+    // global-row-indexed views of the held allocations
+    dev.ident = ident - row_base;
+    dev.meta = meta - row_base;
+    dev.weights = weights ? weights - row_lo * dim : nullptr;
+    dev.momentum = momentum ? momentum - row_lo * dim : nullptr;
+    dev.trained = trained ? trained - row_lo : nullptr;
+    dev.row_gen = row_gen - row_lo;
+    dev.row_lo = row_lo;
+    dev.row_hi = row_hi;
+    dev.shard_lo = shard_lo;
+    dev.shard_hi = shard_hi;
     dev.shards = d_shards;
     dev.nshards = make_fastmod(S);
     dev.seed = seed;
@@ -231,8 +245,9 @@ __global__ void k_dirty_flags(const uint64_t* __restrict__ row_gen, uint64_t tot
 struct EmitIndex {
     uint64_t* out;
     uint64_t cap;
+    uint64_t offset;
     __device__ void operator()(uint64_t i, unsigned k) const {
-        if (k < cap) out[k] = i;
+        if (k < cap) out[k] = offset + i;
     }
 };
 
@@ -267,7 +282,7 @@ void require_valid_id(uint64_t id) {  // ids.hpp:25-31
 // The batch core shared by the host- and device-buffer entry points.
 void run_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n, uint64_t now,
                const Policy& pol, uint64_t* out_slots, uint8_t* out_oc, uint64_t* out_ev,
-               uint64_t ev_cap, uint64_t* out_ev_n, cudaStream_t st) {
+               uint64_t ev_cap, uint64_t* out_ev_n, cudaStream_t st, uint8_t* out_mark = nullptr) {
     if (n > 0xffffffffull) throw Error{MPZCH_ELENGTH, "batch exceeds 2^32 - 1 positions"};
     if (out_ev_n) *out_ev_n = 0;
     t.last = mpzch_batch_stats{};
@@ -282,6 +297,7 @@ void run_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n,
     a.out_oc = out_oc;
     a.out_ev = out_ev;
     a.ev_cap = out_ev ? ev_cap : 0;
+    a.out_mark = out_mark;
     // one metadata value for the whole batch? (make_metadata, eviction.cpp:20-30)
     a.uniform = true;
     uint64_t ttl = 0;
@@ -320,6 +336,9 @@ void run_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n,
     if (c.err.too_many == 2) throw Error{MPZCH_ECUDA, "internal error: claim invariant violated"};
     if (c.err.bad_pos != ~0ull)
         throw Error{MPZCH_EINVAL, "invalid id at batch position " + std::to_string(c.err.bad_pos)};
+    if (c.err.foreign_pos != ~0ull)
+        throw Error{MPZCH_ERANGE, "id at batch position " + std::to_string(c.err.foreign_pos) +
+                                      " routes to a shard this handle does not hold"};
     if (a.overflow_all || c.err.overflow)
         throw Error{MPZCH_EOVERFLOW, "TTL expiry overflows the 64-bit timestamp range"};
     if (out_ev_n) *out_ev_n = c.evicted_count;
@@ -423,6 +442,72 @@ mpzch_status mpzch_table_create(const uint64_t* caps, uint32_t num_shards, uint3
     });
 }
 
+mpzch_status mpzch_table_create_sharded(const uint64_t* caps, uint32_t num_shards,
+                                        uint32_t max_probe, uint64_t seed, uint32_t dim,
+                                        uint64_t init_seed, int device, uint32_t shard_lo,
+                                        uint32_t shard_hi, mpzch_table** out) {
+    if (!out) {
+        g_last_error = "null output pointer";
+        return MPZCH_EINVAL;
+    }
+    *out = nullptr;
+    return guarded([&] {
+        if (num_shards && !caps) throw Error{MPZCH_EINVAL, "null capacities"};
+        Table* t = new Table(caps, num_shards, max_probe, seed, dim, init_seed, device, shard_lo,
+                             shard_hi);
+        *out = new mpzch_table{t};
+    });
+}
+
+mpzch_status mpzch_held_rows(const mpzch_table* t, uint64_t* row_lo, uint64_t* row_hi,
+                             uint32_t* shard_lo, uint32_t* shard_hi) {
+    CHECK_T(t);
+    if (row_lo) *row_lo = t->t->row_lo;
+    if (row_hi) *row_hi = t->t->row_hi;
+    if (shard_lo) *shard_lo = t->t->shard_lo;
+    if (shard_hi) *shard_hi = t->t->shard_hi;
+    return MPZCH_OK;
+}
+
+mpzch_status mpzch_validate_device(const mpzch_table* t, const uint64_t* ids, uint64_t n,
+                                   uint64_t* out_bad_pos, void* stream) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        DeviceGuard g(T.device);
+        *out_bad_pos = ~0ull;
+        if (n == 0) return;
+        run_validate(T, ids, n, (cudaStream_t)stream);
+        *out_bad_pos = T.h_ctr->err.bad_pos;
+    });
+}
+
+mpzch_status mpzch_route_device(const mpzch_table* t, const uint64_t* ids, uint64_t n,
+                                const uint32_t* shard_to_part, uint32_t parts, uint32_t* perm,
+                                uint64_t* counts, void* stream) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        DeviceGuard g(T.device);
+        run_route(T, ids, n, shard_to_part, parts, perm, counts, (cudaStream_t)stream);
+    });
+}
+
+mpzch_status mpzch_process_batch_device_marked(mpzch_table* t, const uint64_t* ids,
+                                               const uint32_t* feats, uint64_t n, uint64_t now,
+                                               const mpzch_policy* policy, uint64_t* out_slots,
+                                               uint8_t* out_oc, uint8_t* out_first_evicted,
+                                               uint64_t* out_ev_n, void* stream) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        DeviceGuard g(T.device);
+        const Policy pol = parse_policy(policy);
+        run_batch(T, ids, feats, n, now, pol, out_slots, out_oc, nullptr, 0, out_ev_n,
+                  (cudaStream_t)stream, out_first_evicted);
+    });
+}
+
 mpzch_status mpzch_table_destroy(mpzch_table* t) {
     if (!t) return MPZCH_OK;
     delete t->t;
@@ -510,7 +595,7 @@ mpzch_status mpzch_lookup_device(const mpzch_table* t, const uint64_t* ids, uint
         DeviceGuard g(T.device);
         if (n == 0) return;
         cudaStream_t st = (cudaStream_t)stream;  // 0 = legacy default stream
-        BatchErr init{~0ull, 0, 0};
+        BatchErr init{~0ull, 0, 0, ~0ull};
         MPZCH_CUDA(cudaMemcpyAsync(&T.d_ctr->err, &init, sizeof init, cudaMemcpyHostToDevice, st));
         run_lookup(T, ids, n, out_slots, out_oc, &T.d_ctr->err, st);
         ++T.launches;
@@ -523,6 +608,9 @@ mpzch_status mpzch_lookup_device(const mpzch_table* t, const uint64_t* ids, uint
             MPZCH_CUDA(cudaMemcpy(&bad, ids + T.h_ctr->err.bad_pos, 8, cudaMemcpyDeviceToHost));
             require_valid_id(bad);
         }
+        if (T.h_ctr->err.foreign_pos != ~0ull)
+            throw Error{MPZCH_ERANGE, "id at batch position " + std::to_string(T.h_ctr->err.foreign_pos) +
+                                          " routes to a shard this handle does not hold"};
     });
 }
 
@@ -538,7 +626,7 @@ mpzch_status mpzch_lookup(const mpzch_table* t, const uint64_t* ids, uint64_t n,
         T.s_oslot.reserve(n * 8);
         T.s_ooc.reserve(n);
         MPZCH_CUDA(cudaMemcpyAsync(T.s_ids.p, ids, n * 8, cudaMemcpyHostToDevice, st));
-        BatchErr init{~0ull, 0, 0};
+        BatchErr init{~0ull, 0, 0, ~0ull};
         MPZCH_CUDA(cudaMemcpyAsync(&T.d_ctr->err, &init, sizeof init, cudaMemcpyHostToDevice, st));
         run_lookup(T, T.s_ids.as<uint64_t>(), n, T.s_oslot.as<uint64_t>(), T.s_ooc.as<uint8_t>(),
                    &T.d_ctr->err, st);
@@ -550,6 +638,9 @@ mpzch_status mpzch_lookup(const mpzch_table* t, const uint64_t* ids, uint64_t n,
         MPZCH_CUDA(cudaMemcpyAsync(out_oc, T.s_ooc.p, n, cudaMemcpyDeviceToHost, st));
         MPZCH_CUDA(cudaStreamSynchronize(st));
         if (T.h_ctr->err.bad_pos != ~0ull) require_valid_id(ids[T.h_ctr->err.bad_pos]);
+        if (T.h_ctr->err.foreign_pos != ~0ull)
+            throw Error{MPZCH_ERANGE, "id at batch position " + std::to_string(T.h_ctr->err.foreign_pos) +
+                                          " routes to a shard this handle does not hold"};
     });
 }
 
@@ -576,7 +667,9 @@ mpzch_status mpzch_copy_identities(const mpzch_table* t, uint64_t* out) {
     return guarded([&] {
         DeviceGuard g(t->t->device);
         MPZCH_CUDA(cudaStreamSynchronize(t->t->stream));
-        MPZCH_CUDA(cudaMemcpy(out, t->t->ident, t->t->total * 8, cudaMemcpyDeviceToHost));
+        const Table& T = *t->t;
+        MPZCH_CUDA(cudaMemcpy(out, T.ident + (T.row_lo - T.row_base), T.held_rows() * 8,
+                              cudaMemcpyDeviceToHost));
     });
 }
 
@@ -585,13 +678,16 @@ mpzch_status mpzch_copy_metadata(const mpzch_table* t, uint64_t* out) {
     return guarded([&] {
         DeviceGuard g(t->t->device);
         MPZCH_CUDA(cudaStreamSynchronize(t->t->stream));
-        MPZCH_CUDA(cudaMemcpy(out, t->t->meta, t->t->total * 8, cudaMemcpyDeviceToHost));
+        const Table& T = *t->t;
+        MPZCH_CUDA(cudaMemcpy(out, T.meta + (T.row_lo - T.row_base), T.held_rows() * 8,
+                              cudaMemcpyDeviceToHost));
     });
 }
 
+// row0 is a global row; the range must lie inside the rows this handle holds
 static void check_rows(const Table& T, uint64_t row0, uint64_t nrows) {
     if (T.dim == 0) throw Error{MPZCH_ELOGIC, "table has no embedding payload (dim = 0)"};
-    if (row0 > T.total || nrows > T.total - row0)
+    if (row0 < T.row_lo || row0 > T.row_hi || nrows > T.row_hi - row0)
         throw Error{MPZCH_ERANGE, "embedding row out of range"};
 }
 
@@ -602,7 +698,7 @@ mpzch_status mpzch_copy_weights(const mpzch_table* t, uint64_t row0, uint64_t nr
         check_rows(T, row0, nrows);
         DeviceGuard g(T.device);
         MPZCH_CUDA(cudaStreamSynchronize(T.stream));
-        MPZCH_CUDA(cudaMemcpy(out, T.weights + row0 * T.dim, nrows * T.dim * 4, cudaMemcpyDeviceToHost));
+        MPZCH_CUDA(cudaMemcpy(out, T.dev.weights + row0 * T.dim, nrows * T.dim * 4, cudaMemcpyDeviceToHost));
     });
 }
 
@@ -613,7 +709,7 @@ mpzch_status mpzch_copy_momentum(const mpzch_table* t, uint64_t row0, uint64_t n
         check_rows(T, row0, nrows);
         DeviceGuard g(T.device);
         MPZCH_CUDA(cudaStreamSynchronize(T.stream));
-        MPZCH_CUDA(cudaMemcpy(out, T.momentum + row0 * T.dim, nrows * T.dim * 4, cudaMemcpyDeviceToHost));
+        MPZCH_CUDA(cudaMemcpy(out, T.dev.momentum + row0 * T.dim, nrows * T.dim * 4, cudaMemcpyDeviceToHost));
     });
 }
 
@@ -621,10 +717,10 @@ mpzch_status mpzch_copy_trained(const mpzch_table* t, uint8_t* out) {
     CHECK_T(t);
     return guarded([&] {
         const Table& T = *t->t;
-        check_rows(T, 0, 0);
+        check_rows(T, T.row_lo, 0);
         DeviceGuard g(T.device);
         MPZCH_CUDA(cudaStreamSynchronize(T.stream));
-        MPZCH_CUDA(cudaMemcpy(out, T.trained, T.total, cudaMemcpyDeviceToHost));
+        MPZCH_CUDA(cudaMemcpy(out, T.trained, T.held_rows(), cudaMemcpyDeviceToHost));
     });
 }
 
@@ -633,7 +729,7 @@ mpzch_status mpzch_copy_row_generation(const mpzch_table* t, uint64_t* out) {
     return guarded([&] {
         DeviceGuard g(t->t->device);
         MPZCH_CUDA(cudaStreamSynchronize(t->t->stream));
-        MPZCH_CUDA(cudaMemcpy(out, t->t->row_gen, t->t->total * 8, cudaMemcpyDeviceToHost));
+        MPZCH_CUDA(cudaMemcpy(out, t->t->row_gen, t->t->held_rows() * 8, cudaMemcpyDeviceToHost));
     });
 }
 
@@ -652,6 +748,8 @@ mpzch_status mpzch_write_slots(mpzch_table* t, uint32_t shard, const uint64_t* l
     return guarded([&] {
         Table& T = *t->t;
         if (shard >= T.S) throw Error{MPZCH_ERANGE, "shard index out of range"};
+        if (shard < T.shard_lo || shard >= T.shard_hi)
+            throw Error{MPZCH_ERANGE, "shard is not held by this handle"};
         std::vector<uint64_t> g(n), m(n);
         for (uint64_t i = 0; i < n; ++i) {
             if (local_slots[i] >= T.caps[shard])
@@ -669,7 +767,7 @@ mpzch_status mpzch_write_slots(mpzch_table* t, uint32_t shard, const uint64_t* l
             // keep the existing metadata words
             MPZCH_CUDA(cudaStreamSynchronize(T.stream));
             for (uint64_t i = 0; i < n; ++i)
-                MPZCH_CUDA(cudaMemcpy(&m[i], T.meta + g[i], 8, cudaMemcpyDeviceToHost));
+                MPZCH_CUDA(cudaMemcpy(&m[i], T.dev.meta + g[i], 8, cudaMemcpyDeviceToHost));
             MPZCH_CUDA(cudaMemcpyAsync(buf + 2 * n, m.data(), n * 8, cudaMemcpyHostToDevice, T.stream));
         }
         launch_write_slots(T, buf, buf + n, buf + 2 * n, n, T.stream);
@@ -696,11 +794,11 @@ mpzch_status mpzch_write_row(mpzch_table* t, uint64_t row, const float* w, const
         check_rows(T, row, 1);
         DeviceGuard g(T.device);
         MPZCH_CUDA(cudaStreamSynchronize(T.stream));
-        if (w) MPZCH_CUDA(cudaMemcpy(T.weights + row * T.dim, w, T.dim * 4, cudaMemcpyHostToDevice));
-        if (m) MPZCH_CUDA(cudaMemcpy(T.momentum + row * T.dim, m, T.dim * 4, cudaMemcpyHostToDevice));
-        MPZCH_CUDA(cudaMemcpy(T.trained + row, &trained, 1, cudaMemcpyHostToDevice));
+        if (w) MPZCH_CUDA(cudaMemcpy(T.dev.weights + row * T.dim, w, T.dim * 4, cudaMemcpyHostToDevice));
+        if (m) MPZCH_CUDA(cudaMemcpy(T.dev.momentum + row * T.dim, m, T.dim * 4, cudaMemcpyHostToDevice));
+        MPZCH_CUDA(cudaMemcpy(T.dev.trained + row, &trained, 1, cudaMemcpyHostToDevice));
         // a training write stamps the row dirty, as sgd_step does (table.cpp:170-176)
-        MPZCH_CUDA(cudaMemcpy(T.row_gen + row, &T.gen_clock, 8, cudaMemcpyHostToDevice));
+        MPZCH_CUDA(cudaMemcpy(T.dev.row_gen + row, &T.gen_clock, 8, cudaMemcpyHostToDevice));
     });
 }
 
@@ -721,16 +819,17 @@ mpzch_status mpzch_dirty_rows_since(const mpzch_table* t, uint64_t gen, uint64_t
         DeviceGuard g(T.device);
         cudaStream_t st = T.stream;
         DevBuf flags, rows, blk;
-        flags.reserve(((T.total + 15) & ~15ull) + 16);
+        const uint64_t held = T.held_rows();
+        flags.reserve(((held + 15) & ~15ull) + 16);
         MPZCH_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes, st));
         rows.reserve(std::max<uint64_t>(cap, 1) * 8);
-        blk.reserve(((T.total + kCompactChunk - 1) / kCompactChunk + 1) * 4);
-        k_dirty_flags<<<grid_for(T.total, 256), 256, 0, st>>>(T.row_gen, T.total, gen,
-                                                               flags.as<uint8_t>());
+        blk.reserve(((held + kCompactChunk - 1) / kCompactChunk + 1) * 4);
+        k_dirty_flags<<<grid_for(held, 256), 256, 0, st>>>(T.row_gen, held, gen,
+                                                            flags.as<uint8_t>());
         ++T.launches;
         unsigned* d_n = &T.d_ctr->pad;
-        EmitIndex em{rows.as<uint64_t>(), cap};
-        compact_flags(flags.as<uint8_t>(), T.total, blk.as<unsigned>(), d_n, false, em, st, T.launches);
+        EmitIndex em{rows.as<uint64_t>(), cap, T.row_lo};
+        compact_flags(flags.as<uint8_t>(), held, blk.as<unsigned>(), d_n, false, em, st, T.launches);
         unsigned nn = 0;
         MPZCH_CUDA(cudaMemcpyAsync(&nn, d_n, 4, cudaMemcpyDeviceToHost, st));
         MPZCH_CUDA(cudaStreamSynchronize(st));

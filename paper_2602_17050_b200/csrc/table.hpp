@@ -70,7 +70,8 @@ struct Policy {
 class Table {
 public:
     Table(const uint64_t* caps, uint32_t num_shards, uint32_t max_probe, uint64_t seed,
-          uint32_t dim, uint64_t init_seed, int device);
+          uint32_t dim, uint64_t init_seed, int device, uint32_t shard_lo = 0,
+          uint32_t shard_hi = ~0u);
     ~Table();
 
     // layout (TableLayout, proj/include/mpzch/shard_router.hpp:13-29)
@@ -79,6 +80,12 @@ public:
     uint32_t S = 0, P = 0, dim = 0;
     uint64_t seed = 0, init_seed = 0;
     int device = 0;
+    // row-sharded mode: this handle holds logical shards [shard_lo, shard_hi), i.e. global
+    // rows [row_lo, row_hi); the device pointers in `dev` are offset so that global row
+    // numbers index them directly (identity/metadata allocations start 4-row aligned)
+    uint32_t shard_lo = 0, shard_hi = 0;
+    uint64_t row_lo = 0, row_hi = 0, row_base = 0;
+    uint64_t held_rows() const { return row_hi - row_lo; }
     uint64_t gen_clock = 1;  // MpzchTable::generation_clock_
     bool hole_free = true;   // SURVEY A.2 invariant; false after raw imports
     int path_override = MPZCH_PATH_AUTO;
@@ -142,12 +149,16 @@ struct BatchArgs {
     uint8_t* out_oc;
     uint64_t* out_ev;
     uint64_t ev_cap;
+    uint8_t* out_mark = nullptr;  // optional: 1 at the first position of every Evicted unique
 };
 
 // enqueue the whole batch; counters land in t.h_ctr after the stream syncs
 void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st);
 void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st);
 void enqueue_compact_evicted(Table& t, uint64_t n, uint64_t* out_ev, uint64_t ev_cap, cudaStream_t st);
+void run_route(Table& t, const uint64_t* ids, uint64_t n, const uint32_t* shard_to_part,
+               uint32_t parts, uint32_t* perm, uint64_t* counts, cudaStream_t st);
+void run_validate(Table& t, const uint64_t* ids, uint64_t n, cudaStream_t st);
 
 inline unsigned grid_for(uint64_t n, unsigned block, unsigned max_blocks = 148u * 32u) {
     uint64_t g = (n + block - 1) / block;

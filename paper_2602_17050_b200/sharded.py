@@ -1,0 +1,232 @@
+"""Row-sharded MPZCH table over G ranks (one process per GPU) -- SURVEY 8e.
+
+The S logical shards of one table layout (proj/include/mpzch/shard_router.hpp:13-29) are
+spread over G ranks in contiguous blocks (rank r holds shards s with s*G//S == r).  Global
+row numbers are those of the single-table layout, so every remapped slot is identical for
+G = 1, 2, 4, 8.  A batch of N positions is split into G contiguous slices (rank r holds
+positions [base_r, base_r + n_r)); one process_batch is:
+
+  1. validate the slice (mpzch_validate_device) and agree on the first invalid GLOBAL
+     position (all-reduce MIN): every rank raises the reference's
+     "invalid id at batch position N" before anything is mutated
+     (proj/src/batch_engine.cpp:90-94, 146-147);
+  2. route: stable partition of the slice by owner (mpzch_route_device, shard_of
+     proj/src/shard_router.cpp:42-46) and an all-to-all of (id, feature) -- NCCL over
+     NVLink.  Because slices are rank-ordered and the partition is stable, each owner
+     receives its positions in global first-occurrence order, which is exactly the
+     order the reference's dedup gives (batch_engine.cpp:100-106), so the owner's claim
+     ranks reproduce the single-table result with no sort;
+  3. the owner remaps (mpzch_process_batch_device_marked) -- shards are independent
+     (proj/include/mpzch/batch_engine.hpp:39-43), so no other exchange is needed;
+  4. (slot, outcome, first-evicted mark) travel back by the reverse all-to-all and are
+     scattered to the slice; the canonical evicted list is the rank-ordered
+     concatenation of each rank's marked positions (an all-gather).
+
+The communication and the per-rank engine are parameters, so the same protocol runs
+with torch.distributed (NCCL on GPUs, gloo on CPU in the tests), with in-process
+threads on one GPU (tests), and with any engine exposing validate/route/remap.
+"""
+from __future__ import annotations
+
+import threading
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import (EvictionPolicy, InvalidArgument, LengthError, MpzchTable, OverflowError_,
+               TableConfig)
+
+INF = (1 << 64) - 1
+
+
+def shard_owner(shard: int, num_shards: int, parts: int) -> int:
+    return shard * parts // num_shards
+
+
+def held_shards(rank: int, num_shards: int, parts: int) -> Tuple[int, int]:
+    """[lo, hi) of the contiguous shard block rank `rank` holds."""
+    owned = [s for s in range(num_shards) if shard_owner(s, num_shards, parts) == rank]
+    if not owned:
+        raise InvalidArgument("row-sharded mode needs at least one logical shard per rank "
+                              f"(S={num_shards}, G={parts})")
+    return owned[0], owned[-1] + 1
+
+
+# ------------------------------------------------------------------------------ comms
+
+class TorchComm:
+    """Collectives over torch.distributed (NCCL for CUDA tensors, gloo for CPU tensors)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def _dev(self, like):
+        return like.device
+
+    def all_gather_int(self, x: int, like) -> List[int]:
+        import torch
+        t = torch.tensor([x], dtype=torch.int64, device=self._dev(like))
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [int(v.item()) for v in out]
+
+    def all_reduce_min(self, x: int, like) -> int:
+        import torch
+        t = torch.tensor([x if x < (1 << 63) else (1 << 63) - 1], dtype=torch.int64,
+                         device=self._dev(like))
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        v = int(t.item())
+        return INF if v == (1 << 63) - 1 else v
+
+    def all_to_all(self, send, send_counts: Sequence[int], recv_counts: Sequence[int]):
+        import torch
+        out = torch.empty((sum(recv_counts),) + tuple(send.shape[1:]), dtype=send.dtype,
+                          device=send.device)
+        self.dist.all_to_all_single(out, send.contiguous(), list(recv_counts), list(send_counts),
+                                    group=self.group)
+        return out
+
+    def all_gather_v(self, t, counts: Sequence[int]):
+        import torch
+        m = max(counts) if counts else 0
+        pad = torch.zeros(max(m, 1), dtype=t.dtype, device=t.device)
+        pad[:t.numel()] = t
+        outs = [torch.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(outs, pad, group=self.group)
+        return torch.cat([o[:c] for o, c in zip(outs, counts)])
+
+
+class ThreadComm:
+    """In-process collectives for G logical ranks driven by G threads (one GPU tests)."""
+
+    class _Hub:
+        def __init__(self, world):
+            self.world = world
+            self.barrier = threading.Barrier(world)
+            self.slots = [None] * world
+
+    def __init__(self, hub: "_Hub", rank: int):
+        self.hub = hub
+        self.rank = rank
+        self.world = hub.world
+
+    @classmethod
+    def group(cls, world: int):
+        hub = cls._Hub(world)
+        return [cls(hub, r) for r in range(world)]
+
+    def _exchange(self, obj):
+        self.hub.barrier.wait()
+        self.hub.slots[self.rank] = obj
+        self.hub.barrier.wait()
+        got = list(self.hub.slots)
+        self.hub.barrier.wait()
+        return got
+
+    def all_gather_int(self, x, like):
+        return [int(v) for v in self._exchange(int(x))]
+
+    def all_reduce_min(self, x, like):
+        return min(self._exchange(int(x)))
+
+    def all_to_all(self, send, send_counts, recv_counts):
+        import torch
+        offs = np.concatenate([[0], np.cumsum(send_counts)]).astype(np.int64)
+        chunks = [send[offs[d]:offs[d + 1]] for d in range(self.world)]
+        allc = self._exchange(chunks)
+        return torch.cat([allc[src][self.rank] for src in range(self.world)])
+
+    def all_gather_v(self, t, counts):
+        import torch
+        return torch.cat(self._exchange(t))
+
+
+# ------------------------------------------------------------------------------ engines
+
+class GpuEngine:
+    """The per-rank engine: the rank's sm_100a table handle (held shards only)."""
+
+    def __init__(self, cfg: TableConfig, rank: int, world: int, device: int):
+        lo, hi = held_shards(rank, len(cfg.shard_capacities), world)
+        self.table = MpzchTable(cfg, device=device, shard_range=(lo, hi))
+        self.device = device
+
+    def validate(self, ids) -> Optional[int]:
+        return self.table.validate_device(ids)
+
+    def route(self, ids, shard_to_part, parts):
+        return self.table.route_device(ids, shard_to_part, parts)
+
+    def remap(self, ids, features, now, policy):
+        return self.table.process_batch_device_marked(ids, now, policy, features)
+
+
+# ------------------------------------------------------------------------------ protocol
+
+class ShardedMpzchTable:
+    """One rank's view of a row-sharded MpzchTable (proj/include/mpzch/table.hpp:41-131)."""
+
+    def __init__(self, cfg: TableConfig, comm, engine=None, device: int = 0):
+        self.cfg = cfg
+        self.comm = comm
+        self.rank, self.world = comm.rank, comm.world
+        self.num_shards = len(cfg.shard_capacities)
+        self.shard_to_part = np.array([shard_owner(s, self.num_shards, self.world)
+                                       for s in range(self.num_shards)], dtype=np.uint32)
+        self.engine = engine if engine is not None else GpuEngine(cfg, self.rank, self.world, device)
+
+    def process_batch(self, ids, now: int, policy: EvictionPolicy, features=None):
+        """Remap this rank's slice of the global batch.  Returns (slots, outcomes,
+        evicted) where evicted is the GLOBAL canonical evicted list (identical on every
+        rank)."""
+        import torch
+        comm = self.comm
+        n = ids.numel()
+        sizes = comm.all_gather_int(n, ids)
+        base = sum(sizes[:self.rank])
+        if sum(sizes) > 0xFFFFFFFF:  # batch_engine.cpp:82-83
+            raise LengthError("batch exceeds 2^32 - 1 positions")
+        bad = self.engine.validate(ids) if n else None
+        gbad = comm.all_reduce_min(INF if bad is None else base + bad, ids)
+        if gbad != INF:
+            raise InvalidArgument(f"invalid id at batch position {gbad}")
+        if policy.mode == EvictionPolicy.TTL:
+            # make_metadata (eviction.cpp:20-30) over the features present anywhere in the
+            # batch: decided globally so every rank raises (or not) together
+            limit = (1 << 64) - 1 - now
+            present = [0] if features is None else [int(f) for f in torch.unique(features).tolist()]
+            over = any(policy.ttl.ttl_for(f) > limit for f in present) if n else False
+            if comm.all_reduce_min(0 if over else 1, ids) == 0:
+                raise OverflowError_("TTL expiry overflows the 64-bit timestamp range")
+        perm, send_counts = self.engine.route(ids, self.shard_to_part, self.world)
+        recv_counts = self._exchange_counts(send_counts, ids)
+        permi = perm.long()
+        rid = comm.all_to_all(ids[permi], send_counts, recv_counts)
+        rfeat = None
+        if features is not None:
+            rfeat = comm.all_to_all(features[permi], send_counts, recv_counts)
+        rs, ro, rm = self.engine.remap(rid, rfeat, now, policy)
+        bs = comm.all_to_all(rs, recv_counts, send_counts)
+        bo = comm.all_to_all(ro, recv_counts, send_counts)
+        bm = comm.all_to_all(rm, recv_counts, send_counts)
+        slots = torch.empty_like(bs)
+        oc = torch.empty_like(bo)
+        mark = torch.empty_like(bm)
+        slots[permi] = bs
+        oc[permi] = bo
+        mark[permi] = bm
+        mine = slots[mark.bool()]
+        counts = comm.all_gather_int(mine.numel(), ids)
+        evicted = comm.all_gather_v(mine, counts)
+        return slots, oc, evicted
+
+    def _exchange_counts(self, send_counts, like):
+        import torch
+        t = torch.tensor(send_counts, dtype=torch.int64, device=like.device)
+        ones = [1] * self.world
+        got = self.comm.all_to_all(t, ones, ones)
+        return [int(v) for v in got.tolist()]
