@@ -18,8 +18,10 @@ run_latency_bench does, proj/src/experiments.cpp:325,347).
             oracle/Makefile, OpenMP over all host cores) on a bounded sample of the same
             workload (2^25 rows, same S/P/load/mix/batch size).
 
-Multi-GPU (torchrun, N>1): each rank remaps its own 4M-position batches against its own
-1B-slot table (replicas, weak scaling); ranks share nothing on the data path.
+Multi-GPU (torchrun, N>1): the same 1B-slot table row-sharded over the N ranks (each holds
+8/N logical shards), every 4M-position batch split into N slices, ids routed to owners and
+results routed back by NCCL all-to-all (paper_2602_17050_b200/sharded.py) -- strong
+scaling of the fixed C5 workload.
 """
 import argparse
 import json
@@ -260,7 +262,7 @@ def main():
         r = run_reference_sample(args.steps, max(args.warmup, 1), log=log)
         line = {"metric": metric, "value": r["value"], "unit": "IDs/s", "impl": "reference",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "weak",
+                "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "u64", "data": "synthetic",
                 "config": {"workload": "C5 sample (reference CPU path)", "rows": CPU_ROWS,
                            "num_shards": SHARDS, "max_probe": MAX_PROBE, "batch_positions": BATCH},
@@ -283,62 +285,88 @@ def main():
 
     rows = args.rows
     caps = mz.even_capacities(rows, SHARDS)
-    t_build = time.perf_counter()
-    table = mz.MpzchTable(mz.TableConfig(caps, MAX_PROBE, TABLE_SEED), device=dev)
+    cfg = mz.TableConfig(caps, MAX_PROBE, TABLE_SEED)
     pol = mz.EvictionPolicy.disabled()
-    npre = prefill_count(rows)
-    id_seed = ID_SEED + 1000 * rank  # replicas draw disjoint streams
+    t_build = time.perf_counter()
     out_s = torch.empty(BATCH, dtype=torch.int64, device=dev)
     out_o = torch.empty(BATCH, dtype=torch.uint8, device=dev)
-    for a in range(0, npre, BATCH):
-        ids = distinct_ids_t(id_seed, torch.arange(a, min(a + BATCH, npre), dtype=torch.int64,
-                                                   device=dev))
-        table.process_batch_device(ids, 1, pol, None, out_s, out_o, None, stream)
-    torch.cuda.synchronize(dev)
-    log(f"[rank {rank}] prefill {npre} ids into {rows} rows in {time.perf_counter() - t_build:.1f}s; "
-        f"stats {table.last_stats()}")
+    if world == 1:
+        table = mz.MpzchTable(cfg, device=dev)
+        probe_table = table
 
-    # pre-generate the W + K device batches (inputs resident in HBM before timing)
+        def remap(ids, now):
+            table.process_batch_device(ids, now, pol, None, out_s, out_o, None, stream)
+    else:
+        # C5 row-sharded: the S=8 logical shards of ONE 1B-slot table spread over the ranks;
+        # every global batch of BATCH positions is split into rank slices (strong scaling)
+        from paper_2602_17050_b200.sharded import ShardedMpzchTable, TorchComm
+        sharded = ShardedMpzchTable(cfg, TorchComm(), device=dev)
+        probe_table = sharded.engine.table
+
+        def remap(ids, now):
+            sharded.process_batch(ids, now, pol)
+
+    def my_slice(lo, hi):
+        n = hi - lo
+        return lo + rank * n // world, lo + (rank + 1) * n // world
+
+    npre = prefill_count(rows)
+    for a in range(0, npre, BATCH):
+        s0, s1 = my_slice(a, min(a + BATCH, npre))
+        ids = distinct_ids_t(ID_SEED, torch.arange(s0, s1, dtype=torch.int64, device=dev))
+        remap(ids, 1)
+    torch.cuda.synchronize(dev)
+    log(f"[rank {rank}] prefill {npre} ids into {rows} rows ({world} rank(s)) in "
+        f"{time.perf_counter() - t_build:.1f}s; stats {probe_table.last_stats()}")
+
+    # pre-generate the W + K batches: the same global batch on every rank, each keeps its slice
     nb = args.warmup + args.steps
     batches = []
     fresh_base = npre
+    b0, b1 = my_slice(0, BATCH)
     for b in range(nb):
-        idx, nf = batch_indices(torch, dev, npre, BATCH, b, fresh_base, SAMPLER_SEED + rank)
+        idx, nf = batch_indices(torch, dev, npre, BATCH, b, fresh_base, SAMPLER_SEED)
         fresh_base += nf
-        batches.append(distinct_ids_t(id_seed, idx))
+        batches.append(distinct_ids_t(ID_SEED, idx[b0:b1]).contiguous())
     torch.cuda.synchronize(dev)
 
     for b in range(args.warmup):
-        table.process_batch_device(batches[b], 2 + b, pol, None, out_s, out_o, None, stream)
+        remap(batches[b], 2 + b)
     torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
 
-    table.set_profiling(True)
-    launches0 = table.kernel_launches()
+    probe_table.set_profiling(True)
+    launches0 = probe_table.kernel_launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     stats = []
     with Clocks(dev) as clk:
         clk.wait_first()
+        if world > 1:
+            torch.distributed.barrier()
         torch.cuda.synchronize(dev)
         w0 = time.time()
         ev0.record(stream)
         for b in range(args.warmup, nb):
-            table.process_batch_device(batches[b], 2 + b, pol, None, out_s, out_o, None, stream)
-            stats.append(table.last_stats())
+            remap(batches[b], 2 + b)
+            stats.append(probe_table.last_stats())
         ev1.record(stream)
         torch.cuda.synchronize(dev)
         ms_total = ev0.elapsed_time(ev1)
-        launches = table.kernel_launches() - launches0
-        prof = table.profile()
-        table.set_profiling(False)
+        launches = probe_table.kernel_launches() - launches0
+        prof = probe_table.profile()
+        probe_table.set_profiling(False)
         # the timed region is short next to nvidia-smi's sampling period: keep the same load
         # running (re-remapping the timed batches, untimed) until >= 3 samples fall inside
         k = 0
-        while len([t for t, _ in clk.rows if t >= w0]) < 4 and k < 2000:
-            table.process_batch_device(batches[args.warmup + k % args.steps], 2 + nb, pol, None,
-                                       out_s, out_o, None, stream)
+        while k < 2000:
+            more = len([t for t, _ in clk.rows if t >= w0]) < 4
+            if world > 1:
+                more = bool(_allreduce_max_int(torch, int(more), dev))
+            if not more:
+                break
+            remap(batches[args.warmup + k % args.steps], 2 + nb)
             k += 1
         torch.cuda.synchronize(dev)
         clk.windows.append((w0, time.time()))
@@ -347,41 +375,45 @@ def main():
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         ms_total = float(tt.item())
     ms_step = ms_total / args.steps
-    value = world * BATCH * args.steps / (ms_total / 1e3)
+    value = BATCH * args.steps / (ms_total / 1e3)
 
-    # e2e: host buffers through the reference-facing C-ABI call, pinned memory
+    # e2e: host buffers in, host buffers out, through the public API (pinned memory)
     e2e_steps = args.e2e_steps or max(3, args.steps // 2)
-    pin_ids = [batches[(args.warmup + i) % nb].cpu().pin_memory() for i in range(e2e_steps)]
-    pin_s = torch.empty(BATCH, dtype=torch.int64).pin_memory()
-    pin_o = torch.empty(BATCH, dtype=torch.uint8).pin_memory()
-    # fresh ids for the e2e steps so they stay insert+lookup mixes
     e2e_batches = []
     for i in range(e2e_steps):
-        idx, nf = batch_indices(torch, dev, npre, BATCH, nb + i, fresh_base, SAMPLER_SEED + rank)
+        idx, nf = batch_indices(torch, dev, npre, BATCH, nb + i, fresh_base, SAMPLER_SEED)
         fresh_base += nf
-        e2e_batches.append(distinct_ids_t(id_seed, idx).cpu().pin_memory())
-    del pin_ids
+        e2e_batches.append(distinct_ids_t(ID_SEED, idx[b0:b1]).cpu().pin_memory())
+    nloc = b1 - b0
+    pin_s = torch.empty(nloc, dtype=torch.int64).pin_memory()
+    pin_o = torch.empty(nloc, dtype=torch.uint8).pin_memory()
+    pin_ev = torch.empty(16, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
     if world > 1:
         torch.distributed.barrier()
-    pin_s_np = pin_s.numpy().view(np.uint64)
-    pin_o_np = pin_o.numpy()
-    pin_ev = torch.empty(16, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+    torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     for i in range(e2e_steps):
-        ids_np = e2e_batches[i].numpy().view(np.uint64)
-        table.process_batch(ids_np, 100 + i, pol, out_slots=pin_s_np, out_outcomes=pin_o_np,
-                            out_evicted=pin_ev)
+        if world == 1:
+            table.process_batch(e2e_batches[i].numpy().view(np.uint64), 100 + i, pol,
+                                out_slots=pin_s.numpy().view(np.uint64), out_outcomes=pin_o.numpy(),
+                                out_evicted=pin_ev)
+        else:
+            d = e2e_batches[i].to(dev, non_blocking=True)
+            s_, o_, _ = sharded.process_batch(d, 100 + i, pol)
+            pin_s.copy_(s_, non_blocking=True)
+            pin_o.copy_(o_, non_blocking=True)
+            torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t0
     if world > 1:
         tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(tt.item())
-    e2e_value = world * BATCH * e2e_steps / e2e_s
+    e2e_value = BATCH * e2e_steps / e2e_s
 
     peak, peak_src = peaks()
     probe_ms = prof["probe_ms"] / max(prof["probe_launches"], 1)
     probe_bytes = prof["probe_bytes"] / max(prof["probe_launches"], 1)
-    achieved = probe_bytes / (probe_ms / 1e3) / 1e9
+    achieved = probe_bytes / (probe_ms / 1e3) / 1e9 if probe_ms else 0.0
     batch_bytes = prof["batch_bytes"] / max(prof["batches"], 1)
     batch_ms = prof["batch_ms"] / max(prof["batches"], 1)
 
@@ -400,38 +432,47 @@ def main():
         line = {
             "metric": metric, "value": value, "unit": "IDs/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (DistinctIdStream ids, SplitMix64 sampler)",
-            "config": {"workload": "C5 per GPU: 1B-slot (2^30-row) table, S=8, max_probe=128, "
-                                   "load 0.8 prefilled via the API, 4M-position batches 90% hit / "
-                                   "10% fresh, eviction Disabled",
+            "config": {"workload": "C5: 1B-slot (2^30-row) table, S=8 logical shards, "
+                                   "max_probe=128, load 0.8 prefilled via the API, 4M-position "
+                                   "batches 90% hit / 10% fresh, eviction Disabled"
+                                   + ("" if world == 1 else f"; row-sharded over {world} GPUs, "
+                                      "NCCL all-to-all id routing"),
                        "rows": rows, "num_shards": SHARDS, "max_probe": MAX_PROBE,
-                       "batch_positions": BATCH, "global_batch": BATCH * world,
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "batch_positions": BATCH, "global_batch": BATCH,
+                       "parallelism": "single GPU" if world == 1 else f"row-sharded x{world}",
                        "l2": "inputs larger than L2 (16 GiB identity+metadata, random probes)",
-                       "outcomes_per_step": {k: v / args.steps for k, v in agg.items()}},
+                       "outcomes_per_step_rank0_owner": {k: v / args.steps for k, v in agg.items()}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(),
-                         "kernel": "k_probe<Disabled> (probe of every position)",
+                         "frac": achieved / peak, "traffic": ncu_traffic() if world == 1 else None,
+                         "kernel": "k_probe<Disabled,2> (probe of every position; rank 0)",
                          "algorithmic_bytes_per_launch": probe_bytes,
                          "probe_sectors_per_launch": prof["probe_sectors"] / max(prof["probe_launches"], 1),
                          "launch_ms": probe_ms, "peak_source": peak_src,
                          "random_sector_ceiling_gbs": random_sector_ceiling(),
                          "share_of_step": probe_ms / ms_step,
                          "batch_algorithmic_bytes": batch_bytes,
-                         "batch_gbs": batch_bytes / (batch_ms / 1e3) / 1e9,
+                         "batch_gbs": batch_bytes / (batch_ms / 1e3) / 1e9 if batch_ms else 0.0,
                          "claim_ms": prof["claim_ms"] / max(prof["batches"], 1),
                          "tail_ms": prof["tail_ms"] / max(prof["batches"], 1)},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "IDs/s", "h2d_bytes_per_step": BATCH * 8,
                     "d2h_bytes_per_step": BATCH * 9, "steps": e2e_steps,
-                    "api": "mpzch_process_batch (host buffers, pinned)"},
+                    "api": "mpzch_process_batch (host buffers, pinned)" if world == 1 else
+                           "ShardedMpzchTable.process_batch (pinned host slices, H2D/D2H timed)"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def _allreduce_max_int(torch, x, dev):
+    t = torch.tensor([x], device=dev, dtype=torch.int64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return int(t.item())
 
 
 if __name__ == "__main__":
