@@ -1,0 +1,224 @@
+#!/usr/bin/env python
+"""Measure every BASELINE.json config (C5 is bench.py) on one B200.
+
+Prints one JSON object per config: device-timed positions/s (CUDA events on the launch
+stream, inputs resident in HBM), per-batch kernel split from the in-library profiler,
+outcome counts, and -- where a bounded sample is feasible -- the reference library
+(oracle/_ref, OpenMP, all host cores) on the same stream.  Used for profiles/configs_r*.json.
+
+  C1  2^20 rows, S=1 and S=8, P=128, Disabled, 64K-position batches uniform over a
+      0.8*2^20 pool (run_latency_bench's sampler); cold fill (batches 0-15) and steady
+      state (16 warm-up, 64 timed).
+  C2  2^26 rows, S=8, P=128, TTL, Zipf(1.05) over 2^27 ranks, 1M-position batches,
+      now = 1e6 + 60 t; TTL chosen so live occupancy settles near 0.8 (reported).
+  C3  2^28 rows, S=8, P=256, Disabled, prefilled to 0.95; (i) lookup-only 4M positions
+      over the prefilled ids, (i') 50% absent, (ii) insert-heavy 4M positions 50% fresh.
+  C4  2^27 rows, S=8, P=128, dim 128 fp32, init_seed 11, TTL 3600, prefill 0.8 at now=1,
+      then 1M-position batches uniform over 2^27 fresh ids at now = 10000 + 600 t:
+      evictions reset 512 B weights + 512 B momentum per row.
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+import bench  # noqa: E402  (id generators)
+import paper_2602_17050_b200 as mz  # noqa: E402
+
+
+def ev_time(fn, stream):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def run_batches(t, batches, nows, pol, stream, timed_from=0, feats=None):
+    n = max(b.numel() for b in batches)
+    out_s = torch.empty(n, dtype=torch.int64, device="cuda")
+    out_o = torch.empty(n, dtype=torch.uint8, device="cuda")
+    out_e = torch.empty(n, dtype=torch.int64, device="cuda")
+    for b in range(timed_from):
+        t.process_batch_device(batches[b], nows[b], pol, None, out_s, out_o, out_e, stream)
+    t.set_profiling(True)
+    stats = []
+
+    def body():
+        for b in range(timed_from, len(batches)):
+            t.process_batch_device(batches[b], nows[b], pol, None, out_s, out_o, out_e, stream)
+            stats.append(t.last_stats())
+    ms = ev_time(body, stream)
+    prof = t.profile()
+    t.set_profiling(False)
+    pos = sum(b.numel() for b in batches[timed_from:])
+    agg = {k: int(sum(s[k] for s in stats)) for k in ("found", "inserted", "evicted", "collision", "new_ids", "evicted_rows")}
+    nb = max(prof["batches"], 1)
+    return dict(ids_per_s=pos / (ms / 1e3), ms_per_batch=ms / max(len(stats), 1), positions=pos,
+                outcomes=agg, path=stats[-1]["path"] if stats else None,
+                probe_ms=prof["probe_ms"] / nb, claim_ms=prof["claim_ms"] / nb,
+                tail_ms=prof["tail_ms"] / nb,
+                probe_gbs=(prof["probe_bytes"] / nb) / (prof["probe_ms"] / nb / 1e3) / 1e9 if prof["probe_ms"] else None,
+                batch_gbs=(prof["batch_bytes"] / nb) / (prof["batch_ms"] / nb / 1e3) / 1e9 if prof["batch_ms"] else None)
+
+
+def ref_time(caps, P, batches_np, nows, mode, ttl, dim=0, init_seed=0, warm=0):
+    """The reference library on the same host stream (bounded)."""
+    import pyoracle
+    if not pyoracle.available("reference"):
+        return None
+    L = pyoracle.lib("reference")
+    L["set_threads"](os.cpu_count() or 1)
+    t = pyoracle.OracleTable(caps, P, 7, dim, init_seed, kind="reference")
+    tot, pos = 0.0, 0
+    for i, (b, now) in enumerate(zip(batches_np, nows)):
+        s = time.perf_counter()
+        t.process_batch(b, now, mode, ttl)
+        if i >= warm:
+            tot += time.perf_counter() - s
+            pos += b.size
+    return dict(ids_per_s=pos / tot, cores=os.cpu_count(), kind="reference")
+
+
+def c1(shards):
+    rows = 1 << 20
+    pool = int(0.8 * rows)
+    ids_pool = bench.distinct_ids_t(1, torch.arange(pool, dtype=torch.int64, device="cuda"))
+    B, nb = 65536, 16 + 64
+    k = torch.arange(nb * B, dtype=torch.int64, device="cuda")
+    seed = int(bench.mix64_t(torch.tensor([1]), 0x5CA1AB1E).item()) & ((1 << 64) - 1)
+    d = bench.splitmix_t(seed, k) & ((1 << 63) - 1)
+    idx = d % pool
+    batches = [ids_pool[idx[b * B:(b + 1) * B]].contiguous() for b in range(nb)]
+    nows = [b + 1 for b in range(nb)]
+    pol = mz.EvictionPolicy.disabled()
+    st = torch.cuda.current_stream()
+    caps = mz.even_capacities(rows, shards)
+    t = mz.MpzchTable(mz.TableConfig(caps, 128, 7))
+    cold = run_batches(t, batches[:16], nows[:16], pol, st)
+    t2 = mz.MpzchTable(mz.TableConfig(caps, 128, 7))
+    steady = run_batches(t2, batches, nows, pol, st, timed_from=16)
+    bn = [b.cpu().numpy().view(np.uint64) for b in batches]
+    ref = ref_time(caps, 128, bn, nows, 0, 0, warm=16)
+    return dict(config=f"C1 S={shards}", cold_fill=cold, steady=steady, reference=ref)
+
+
+def zipf_ranks(n, s, universe, seed):
+    # inverse CDF on a precomputed table, SplitMix64(3).next_unit()
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    u = torch.rand(n, generator=g, device="cuda", dtype=torch.float64)
+    return torch.searchsorted(zipf_ranks.cdf, u).clamp_(max=universe - 1)
+
+
+def c2():
+    rows = 1 << 26
+    universe = 1 << 27
+    w = torch.arange(1, universe + 1, dtype=torch.float64, device="cuda").pow_(-1.05)
+    zipf_ranks.cdf = torch.cumsum(w, 0) / w.sum()
+    del w
+    B = 1 << 20
+    ttl = 86400
+    pol = mz.EvictionPolicy.ttl(mz.TtlPolicy(ttl))
+    st = torch.cuda.current_stream()
+    caps = mz.even_capacities(rows, 8)
+    t = mz.MpzchTable(mz.TableConfig(caps, 128, 7))
+    # warm up to steady state: 2 TTL periods of batches at 60 s spacing would be 2880
+    # batches; run 1440 untimed batches, then time 64
+    warm, timed = 1440, 64
+    batches = []
+    nows = []
+    res = None
+    for b in range(warm + timed):
+        r = zipf_ranks(B, 1.05, universe, 1000 + b)
+        batches.append(bench.distinct_ids_t(2, r).contiguous())
+        nows.append(10**6 + 60 * b)
+        if b == warm - 1:
+            run_batches(t, batches, nows, pol, st)
+            batches, nows = [], []
+    res = run_batches(t, batches, nows, pol, st)
+    live = int((torch.from_numpy(t.metadata_all().view(np.int64)) >= nows[-1]).sum())
+    return dict(config="C2", ttl=ttl, live_occupancy=live / rows, steady=res)
+
+
+def c3():
+    rows = 1 << 28
+    caps = mz.even_capacities(rows, 8)
+    t = mz.MpzchTable(mz.TableConfig(caps, 256, 7))
+    pol = mz.EvictionPolicy.disabled()
+    st = torch.cuda.current_stream()
+    npre = int(0.95 * rows)
+    out_s = torch.empty(1 << 22, dtype=torch.int64, device="cuda")
+    out_o = torch.empty(1 << 22, dtype=torch.uint8, device="cuda")
+    t0 = time.perf_counter()
+    for a in range(0, npre, 1 << 22):
+        ids = bench.distinct_ids_t(3, torch.arange(a, min(a + (1 << 22), npre), dtype=torch.int64, device="cuda"))
+        t.process_batch_device(ids, 1, pol, None, out_s, out_o, None, st)
+    torch.cuda.synchronize()
+    prefill_s = time.perf_counter() - t0
+    B = 1 << 22
+    g = torch.Generator(device="cuda").manual_seed(5)
+    hit_idx = torch.randint(0, npre, (B,), generator=g, device="cuda")
+    hits = bench.distinct_ids_t(3, hit_idx)
+    half = torch.cat([hits[:B // 2], bench.distinct_ids_t(3, torch.arange(npre, npre + B // 2, device="cuda"))])
+
+    def look(q):
+        return ev_time(lambda: [t.lookup_device(q, out_s, out_o, st) for _ in range(8)], st) / 8
+    lk = look(hits)
+    lk_half = look(half)
+    fresh = bench.distinct_ids_t(3, torch.arange(npre + B, npre + B + B // 2, device="cuda"))
+    ins = [torch.cat([hits[:B // 2], fresh]).contiguous()]
+    for i in range(1, 5):
+        f2 = bench.distinct_ids_t(3, torch.arange(npre + (i + 1) * B, npre + (i + 1) * B + B // 2, device="cuda"))
+        ins.append(torch.cat([hits[B // 2:], f2]).contiguous())
+    r = run_batches(t, ins, [2 + i for i in range(5)], pol, st, timed_from=1)
+    return dict(config="C3", prefill_s=prefill_s, lookup_ids_per_s=B / (lk / 1e3),
+                lookup_50pct_absent_ids_per_s=B / (lk_half / 1e3), insert_heavy=r)
+
+
+def c4():
+    rows = 1 << 27
+    caps = mz.even_capacities(rows, 8)
+    t0 = time.perf_counter()
+    t = mz.MpzchTable(mz.TableConfig(caps, 128, 7, 128, 11))
+    torch.cuda.synchronize()
+    init_s = time.perf_counter() - t0
+    pol = mz.EvictionPolicy.ttl(mz.TtlPolicy(3600))
+    st = torch.cuda.current_stream()
+    npre = int(0.8 * rows)
+    out_s = torch.empty(1 << 22, dtype=torch.int64, device="cuda")
+    out_o = torch.empty(1 << 22, dtype=torch.uint8, device="cuda")
+    for a in range(0, npre, 1 << 22):
+        ids = bench.distinct_ids_t(4, torch.arange(a, min(a + (1 << 22), npre), dtype=torch.int64, device="cuda"))
+        t.process_batch_device(ids, 1, pol, None, out_s, out_o, None, st)
+    torch.cuda.synchronize()
+    B = 1 << 20
+    g = torch.Generator(device="cuda").manual_seed(41)
+    batches = [bench.distinct_ids_t(41, torch.randint(0, 1 << 27, (B,), generator=g, device="cuda"))
+               for _ in range(17)]
+    nows = [10000 + 600 * i for i in range(17)]
+    r = run_batches(t, batches, nows, pol, st, timed_from=1)
+    reset_bytes = r["outcomes"]["evicted_rows"] * (128 * 8 + 1) / max(len(batches) - 1, 1)
+    r["reset_bytes_per_batch"] = reset_bytes
+    return dict(config="C4", init_draw_s=init_s, steady=r)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["c1", "c2", "c3", "c4"]
+    out = []
+    for w in which:
+        torch.cuda.empty_cache()
+        if w == "c1":
+            out.append(c1(1))
+            out.append(c1(8))
+        else:
+            out.append(globals()[w]())
+        print(json.dumps(out[-1]), flush=True)

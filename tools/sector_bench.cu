@@ -44,6 +44,22 @@ __global__ void __launch_bounds__(256) k_read(const uint64_t* __restrict__ a, ui
     if (acc == 0x1234567) atomicAdd(sink, 1ull);
 }
 
+// read one random 32-byte sector and write 8 bytes at: MODE 0 the same sector, MODE 1 the
+// other sector of the same 64-byte pair, MODE 2 an unrelated random sector (SoA metadata)
+template <int MODE>
+__global__ void __launch_bounds__(256) k_read_write(uint64_t* a, uint64_t nsec, uint64_t n, uint64_t salt) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s = mix(i + salt) % nsec;
+        uint64_t w0, w1, w2, w3;
+        asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3) : "l"(a + 4 * s));
+        uint64_t t;
+        if (MODE == 0) t = 4 * s + 1;
+        else if (MODE == 1) t = 4 * (s ^ 1) + 1;
+        else t = 4 * (mix(i + salt + 999) % nsec) + 1;
+        a[t] = w0 + w1 + w2 + w3;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_write8(uint64_t* a, uint64_t nslots, uint64_t n, uint64_t salt) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         a[mix(i + salt) % nslots] = i;
@@ -73,7 +89,7 @@ int main(int argc, char** argv) {
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     printf("{\"device_sms\": %d, \"array_gib\": 16, \"accesses_per_launch\": %llu, \"results\": [\n", sms, (unsigned long long)n);
     bool first = true;
-    for (int gran : {0, 32, 64, 128}) {
+    for (int gran : {0, 128}) {
         if (gran) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran);
         size_t cur = 0; cudaDeviceGetLimit(&cur, cudaLimitMaxL2FetchGranularity);
 #define RUN(FL, U, B, NAME) { \
@@ -83,6 +99,16 @@ int main(int argc, char** argv) {
             printf("%s{\"op\": \"read\", \"flavor\": \"%s\", \"unroll\": %d, \"bytes\": %d, \"l2_fetch_gran\": %zu, \"ms\": %.4f, \"useful_gbs\": %.1f, \"maccess_s\": %.1f}\n", first ? "" : ",", NAME, U, B, cur, ms, n * (double)B / ms / 1e6, n / ms / 1e3); first = false; }
         RUN(0, 1, 32, "default") RUN(0, 4, 32, "default") RUN(1, 4, 32, "nc") RUN(2, 1, 32, "cg") RUN(2, 4, 32, "cg")
         RUN(2, 8, 32, "cg") RUN(3, 4, 32, "cs") RUN(2, 4, 64, "cg") RUN(2, 2, 128, "cg") RUN(0, 4, 64, "default")
+        for (int mode = 0; mode < 3; ++mode) {
+            const uint64_t nsec = bytes / 32;
+            float ms = timeit([&] {
+                if (mode == 0) k_read_write<0><<<sms * 8, 256>>>(a, nsec, n, 4242);
+                else if (mode == 1) k_read_write<1><<<sms * 8, 256>>>(a, nsec, n, 4242);
+                else k_read_write<2><<<sms * 8, 256>>>(a, nsec, n, 4242);
+            }, 5);
+            const char* nm[3] = {"read32+write8_same_sector", "read32+write8_pair_sector", "read32+write8_random_sector"};
+            printf(",{\"op\": \"%s\", \"l2_fetch_gran\": %zu, \"ms\": %.4f, \"maccess_s\": %.1f}\n", nm[mode], cur, ms, n / ms / 1e3);
+        }
         {
             float ms = timeit([&] { k_write8<<<sms * 8, 256>>>(a, bytes / 8, n, 777); }, 5);
             printf(",{\"op\": \"write8\", \"l2_fetch_gran\": %zu, \"ms\": %.4f, \"useful_gbs\": %.1f, \"maccess_s\": %.1f}\n", cur, ms, n * 8.0 / ms / 1e6, n / ms / 1e3);
