@@ -42,6 +42,19 @@ constexpr uint64_t kFlagEmpty = 1ull << 30;  // the claimed slot was EMPTY befor
 constexpr uint64_t kEntryMask = (1ull << 30) - 1;
 constexpr uint8_t kStateCollided = 1;
 
+// Id table (one entry per distinct new id): an epoch-tagged 128-bit key (epoch << 64 | id)
+// -- any entry whose epoch is not the current batch's is empty, so no cleanup pass is
+// needed -- and an epoch-tagged rank word (epoch << 32 | ~first_position) updated with
+// atomicMax, which keeps the current epoch and the smallest first position.
+typedef unsigned __int128 u128;
+
+__device__ __forceinline__ u128 make_key(uint64_t epoch, uint64_t id) {
+    return ((u128)epoch << 64) | (u128)id;
+}
+__device__ __forceinline__ uint64_t key_id(u128 k) { return (uint64_t)k; }
+__device__ __forceinline__ uint64_t key_epoch(u128 k) { return (uint64_t)(k >> 64); }
+__device__ __forceinline__ uint32_t rank_of(uint64_t tr) { return ~(uint32_t)tr; }
+
 __device__ __forceinline__ bool is_claim(uint64_t v) { return (v >> 63) != 0 && v != kEmpty; }
 __device__ __forceinline__ uint32_t claim_rank(uint64_t v) { return (uint32_t)(v >> 31); }
 __device__ __forceinline__ uint32_t claim_entry(uint64_t v) { return (uint32_t)(v & kEntryMask); }
@@ -133,10 +146,13 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
                                                uint64_t* __restrict__ out_slots,
                                                uint8_t* __restrict__ out_oc,
                                                uint32_t* __restrict__ newpos,
+                                               uint64_t* __restrict__ newid,
                                                uint32_t* __restrict__ newa,
                                                uint32_t* __restrict__ newm) {
     if (batch_failed(&ctr->err)) return;
     constexpr uint8_t kPending = 0, kHit = 1, kEmptyHit = 2, kExhausted = 3, kIdle = 4;
+    __shared__ unsigned s_cnt[32];
+    __shared__ unsigned s_base;
     const unsigned lane = lane_id();
     const uint64_t tile = (uint64_t)blockDim.x * U;
     unsigned long long my_found = 0, my_coll = 0, my_isec = 0, my_msec = 0;
@@ -224,18 +240,29 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
                     if (foc == kFound) ++my_found; else ++my_coll;
                 }
             }
+            // block-aggregated append of the new positions (one global atomic per block-tile)
             const unsigned mask = __ballot_sync(0xffffffffu, is_new);
-            if (mask) {
-                unsigned basek = 0;
-                if (lane == 0) basek = atomicAdd(&ctr->new_count, (unsigned)__popc(mask));
-                basek = __shfl_sync(0xffffffffu, basek, 0);
-                if (is_new) {
-                    const unsigned k = basek + __popc(mask & ((1u << lane) - 1));
-                    newpos[k] = (uint32_t)i;
-                    newa[k] = a_off;
-                    newm[k] = m_off;
+            const unsigned wid = threadIdx.x >> 5;
+            if (lane == 0) s_cnt[wid] = __popc(mask);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned tot = 0;
+                for (unsigned w = 0; w < blockDim.x / 32; ++w) {
+                    const unsigned c = s_cnt[w];
+                    s_cnt[w] = tot;
+                    tot += c;
                 }
+                s_base = tot ? atomicAdd(&ctr->new_count, tot) : 0;
             }
+            __syncthreads();
+            if (is_new) {
+                const unsigned k = s_base + s_cnt[wid] + __popc(mask & ((1u << lane) - 1));
+                newpos[k] = (uint32_t)i;
+                newid[k] = id[u];
+                newa[k] = a_off;
+                newm[k] = m_off;
+            }
+            __syncthreads();
         }
     }
     for (int o = 16; o; o >>= 1) {
@@ -252,68 +279,77 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
     }
 }
 
-// K2: distinct-id table over the new positions.
-__global__ void __launch_bounds__(256) k_dedup(const uint64_t* __restrict__ ids, BatchCounters* ctr,
-                                               uint64_t tcap, const uint32_t* __restrict__ newpos,
+// K2: distinct-id table over the new positions (128-bit CAS on an epoch-tagged key).
+__global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap, uint64_t epoch,
+                                               const uint32_t* __restrict__ newpos,
+                                               const uint64_t* __restrict__ newid,
                                                const uint32_t* __restrict__ newa,
                                                const uint32_t* __restrict__ newm,
-                                               uint32_t* __restrict__ newent, uint64_t* tkey,
-                                               unsigned* tmin, uint32_t* ta, uint32_t* tm,
-                                               uint32_t* theld, uint32_t* elist) {
+                                               uint32_t* __restrict__ newent, u128* tkey,
+                                               unsigned long long* trank, uint32_t* ta,
+                                               uint32_t* tm, uint32_t* theld, uint8_t* tstate) {
     if (batch_failed(&ctr->err)) return;
     const unsigned cnt = ctr->new_count;
     const uint64_t mask = table_mask(cnt, tcap);
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
-        const uint32_t pos = newpos[k];
-        const uint64_t id = ids[pos];
+        const uint64_t id = newid[k];
+        const u128 mine = make_key(epoch, id);
         uint64_t h = mix64(id, 0x2545F4914F6CDD1Dull) & mask;
         uint32_t e;
         for (;;) {
-            uint64_t cur = ld_cg(tkey + h);
-            if (cur == kEmpty) {
-                cur = atomicCAS((unsigned long long*)(tkey + h), (unsigned long long)kEmpty,
-                                (unsigned long long)id);
-                if (cur == kEmpty) {  // inserted: publish the entry's probe facts
+            // atomic 128-bit read (a CAS that can only write back the value it found):
+            // a plain 16-byte load is not guaranteed single-copy atomic
+            u128 cur = atomicCAS(tkey + h, (u128)0, (u128)0);
+            if (key_epoch(cur) != epoch) {  // empty for this batch: try to take it
+                const u128 old = atomicCAS(tkey + h, cur, mine);
+                if (old == cur) {  // inserted: publish the entry's probe facts
                     e = (uint32_t)h;
                     ta[e] = newa[k];
                     tm[e] = newm[k];
                     theld[e] = 0;
-                    cg::coalesced_group grp = cg::coalesced_threads();  // one atomic per warp
-                    unsigned slot0 = 0;
-                    if (grp.thread_rank() == 0) slot0 = atomicAdd(&ctr->entry_count, grp.size());
-                    elist[grp.shfl(slot0, 0) + grp.thread_rank()] = e;
+                    tstate[e] = 0;
                     break;
                 }
+                cur = old;
+                if (key_epoch(cur) != epoch) continue;  // raced with a stale value: retry
             }
-            if (cur == id) {
+            if (key_id(cur) == id) {
                 e = (uint32_t)h;
                 break;
             }
             h = (h + 1) & mask;
         }
-        atomicMin(tmin + e, pos);
+        atomicMax(trank + e, (unsigned long long)((epoch << 32) | (uint32_t)~newpos[k]));
         newent[k] = e;
     }
+}
+
+// The primary item of an entry (the new-list item at the id's first position) does the
+// entry's work in K3/K4; every other item of the same id only reads the result in K5.
+__device__ __forceinline__ bool is_primary(const unsigned long long* trank, uint32_t e, uint32_t pos) {
+    return rank_of(trank[e]) == pos;
 }
 
 // K3: rank-priority claims with takeover.
 template <int MODE>
 __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCounters* ctr,
-                                               const uint32_t* __restrict__ elist,
-                                               const uint64_t* __restrict__ tkey,
-                                               const unsigned* __restrict__ tmin,
+                                               const uint32_t* __restrict__ newpos,
+                                               const uint32_t* __restrict__ newent,
+                                               const u128* __restrict__ tkey,
+                                               const unsigned long long* __restrict__ trank,
                                                const uint32_t* __restrict__ ta,
                                                const uint32_t* __restrict__ tm,
                                                uint32_t* theld, uint8_t* tstate) {
     if (batch_failed(&ctr->err)) return;
-    const unsigned cnt = ctr->entry_count;
+    const unsigned cnt = ctr->new_count;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
-        uint32_t e = elist[k];
+        uint32_t e = newent[k];
+        if (!is_primary(trank, e, newpos[k])) continue;
         bool fresh = true;
         uint32_t resume = 0;
         for (;;) {
-            const uint64_t id = tkey[e];
-            const uint32_t rank = tmin[e];
+            const uint64_t id = key_id(tkey[e]);
+            const uint32_t rank = rank_of(trank[e]);
             const uint32_t s = shard_of(id, t);
             const ShardDev sd = t.shards[s];
             const uint64_t cap = sd.cap.d, base = sd.offset;
@@ -384,7 +420,7 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
             // or -- if it was an owner losing its own id's slot -- as a taker from its
             // first available offset.
             {
-                const uint64_t id2 = tkey[next];
+                const uint64_t id2 = key_id(tkey[next]);
                 const uint64_t h2 = home_of(id2, sd, t.seed);  // same shard as the slot
                 const uint64_t loc = gnext - base;
                 const uint32_t off2 = (uint32_t)(loc >= h2 ? loc - h2 : loc + cap - h2);
@@ -404,9 +440,10 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
 // touch_row, reset list and rank-indexed evicted flags.
 template <int MODE>
 __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
-                                                const uint32_t* __restrict__ elist,
-                                                const uint64_t* __restrict__ tkey,
-                                                const unsigned* __restrict__ tmin,
+                                                const uint32_t* __restrict__ newpos,
+                                                const uint64_t* __restrict__ newid,
+                                                const uint32_t* __restrict__ newent,
+                                                const unsigned long long* __restrict__ trank,
                                                 const uint32_t* __restrict__ tm,
                                                 const uint32_t* __restrict__ theld,
                                                 const uint8_t* __restrict__ tstate,
@@ -417,11 +454,12 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
                                                 uint8_t* __restrict__ evflag,
                                                 uint64_t* __restrict__ evslot) {
     if (batch_failed(&ctr->err)) return;
-    const unsigned cnt = ctr->entry_count;
+    const unsigned cnt = ctr->new_count;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
-        const uint32_t e = elist[k];
-        const uint64_t id = tkey[e];
-        const uint32_t rank = tmin[e];
+        const uint32_t e = newent[k];
+        const uint32_t rank = newpos[k];
+        if (!is_primary(trank, e, rank)) continue;
+        const uint64_t id = newid[k];
         const uint32_t s = shard_of(id, t);
         const ShardDev sd = t.shards[s];
         const uint64_t cap = sd.cap.d, base = sd.offset;
@@ -466,7 +504,7 @@ __global__ void __launch_bounds__(256) k_finalize(BatchCounters* ctr,
                                                   const uint32_t* __restrict__ feats,
                                                   const uint32_t* __restrict__ newpos,
                                                   const uint32_t* __restrict__ newent,
-                                                  const unsigned* __restrict__ tmin,
+                                                  const unsigned long long* __restrict__ trank,
                                                   const uint64_t* __restrict__ tslot,
                                                   const uint8_t* __restrict__ toc,
                                                   uint64_t* __restrict__ out_slots,
@@ -478,7 +516,7 @@ __global__ void __launch_bounds__(256) k_finalize(BatchCounters* ctr,
         const uint32_t pos = newpos[k];
         const uint32_t e = newent[k];
         uint8_t oc = toc[e];
-        if (feats && feats[pos] != feats[tmin[e]]) oc = oc == kCollision ? kCollision : kFound;
+        if (feats && feats[pos] != feats[rank_of(trank[e])]) oc = oc == kCollision ? kCollision : kFound;
         out_slots[pos] = tslot[e];
         out_oc[pos] = oc;
         ++c[oc];
@@ -491,18 +529,12 @@ __global__ void __launch_bounds__(256) k_finalize(BatchCounters* ctr,
         if (c[2]) atomicAdd(&ctr->evicted, c[2]);
         if (c[3]) atomicAdd(&ctr->collision, c[3]);
     }
-}
-
-// K9: return the id-table entries to EMPTY for the next batch.
-__global__ void __launch_bounds__(256) k_cleanup(BatchCounters* ctr, const uint32_t* __restrict__ elist,
-                                                 uint64_t* tkey, unsigned* tmin, uint8_t* tstate) {
-    const unsigned cnt = ctr->entry_count;
-    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
-        const uint32_t e = elist[k];
-        tkey[e] = kEmpty;
-        tmin[e] = kNone32;
-        tstate[e] = 0;
-    }
+    // distinct new ids of the batch (stats): count primary items
+    unsigned np = 0;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x)
+        np += is_primary(trank, newent[k], newpos[k]);
+    for (int o = 16; o; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
+    if (lane_id() == 0 && np) atomicAdd(&ctr->entry_count, np);
 }
 
 }  // namespace
@@ -520,13 +552,18 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     constexpr int kU = 2;  // positions in flight per probe thread
     const uint64_t n = a.n;
     t.ensure_fast_scratch(n);
+    const uint64_t epoch = ++t.epoch;
     const unsigned B = 256;
     const unsigned gW = grid_for(n, B, 148u * 8u);  // count-driven kernels
     const unsigned gP = grid_for((n + kU - 1) / kU, B, 148u * 16u);
     const bool ttl = a.pol->mode == kModeTtl;
     uint32_t* newpos = t.s_newpos.as<uint32_t>();
+    uint64_t* newid = t.s_newid.as<uint64_t>();
     uint32_t* newa = t.s_newa.as<uint32_t>();
     uint32_t* newm = t.s_newm.as<uint32_t>();
+    uint32_t* newent = t.s_newent.as<uint32_t>();
+    u128* tkey = t.s_tkey.as<u128>();
+    unsigned long long* trank = t.s_tmin.as<unsigned long long>();
     k_init_counters<<<1, 32, 0, st>>>(t.d_ctr);
     k_validate<<<grid_for(n / 2 + 1, B, 148u * 8u), B, 0, st>>>(t.dev, a.ids, n, t.d_ctr);
     t.launches += 2;
@@ -534,23 +571,20 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     if (t.profiling) cudaEventRecord(t.ev[0], st);
     if (ttl)
         k_probe<kModeTtl, kU><<<gP, B, 0, st>>>(t.dev, a.ids, n, a.now, a.uniform_meta, t.d_ctr,
-                                                a.out_slots, a.out_oc, newpos, newa, newm);
+                                                a.out_slots, a.out_oc, newpos, newid, newa, newm);
     else
         k_probe<kModeDisabled, kU><<<gP, B, 0, st>>>(t.dev, a.ids, n, a.now, a.uniform_meta, t.d_ctr,
-                                                     a.out_slots, a.out_oc, newpos, newa, newm);
+                                                     a.out_slots, a.out_oc, newpos, newid, newa, newm);
     ++t.launches;
     if (t.profiling) cudaEventRecord(t.ev[1], st);
-    k_dedup<<<gW, B, 0, st>>>(a.ids, t.d_ctr, t.tcap, newpos, newa, newm, t.s_newent.as<uint32_t>(),
-                              t.s_tkey.as<uint64_t>(), t.s_tmin.as<unsigned>(), t.s_ta.as<uint32_t>(),
-                              t.s_tm.as<uint32_t>(), t.s_theld.as<uint32_t>(),
-                              t.s_elist.as<uint32_t>());
+    k_dedup<<<gW, B, 0, st>>>(t.d_ctr, t.tcap, epoch, newpos, newid, newa, newm, newent, tkey, trank,
+                              t.s_ta.as<uint32_t>(), t.s_tm.as<uint32_t>(), t.s_theld.as<uint32_t>(),
+                              t.s_tstate.as<uint8_t>());
 #define MPZCH_CLAIM_COMMIT(MODE)                                                                   \
-    k_claim<MODE><<<gW, B, 0, st>>>(t.dev, a.now, t.d_ctr, t.s_elist.as<uint32_t>(),              \
-                                    t.s_tkey.as<uint64_t>(), t.s_tmin.as<unsigned>(),              \
+    k_claim<MODE><<<gW, B, 0, st>>>(t.dev, a.now, t.d_ctr, newpos, newent, tkey, trank,            \
                                     t.s_ta.as<uint32_t>(), t.s_tm.as<uint32_t>(),                  \
                                     t.s_theld.as<uint32_t>(), t.s_tstate.as<uint8_t>());           \
-    k_commit<MODE><<<gW, B, 0, st>>>(t.dev, t.d_ctr, t.s_elist.as<uint32_t>(),                    \
-                                     t.s_tkey.as<uint64_t>(), t.s_tmin.as<unsigned>(),             \
+    k_commit<MODE><<<gW, B, 0, st>>>(t.dev, t.d_ctr, newpos, newid, newent, trank,               \
                                      t.s_tm.as<uint32_t>(), t.s_theld.as<uint32_t>(),              \
                                      t.s_tstate.as<uint8_t>(), t.s_tslot.as<uint64_t>(),           \
                                      t.s_toc.as<uint8_t>(), t.gen_clock, a.uniform_meta,           \
@@ -561,8 +595,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
 #undef MPZCH_CLAIM_COMMIT
     t.launches += 3;
     if (t.profiling) cudaEventRecord(t.ev[2], st);
-    k_finalize<<<gW, B, 0, st>>>(t.d_ctr, a.feats, newpos, t.s_newent.as<uint32_t>(),
-                                 t.s_tmin.as<unsigned>(), t.s_tslot.as<uint64_t>(),
+    k_finalize<<<gW, B, 0, st>>>(t.d_ctr, a.feats, newpos, newent, trank, t.s_tslot.as<uint64_t>(),
                                  t.s_toc.as<uint8_t>(), a.out_slots, a.out_oc);
     ++t.launches;
     if (t.dim > 0) launch_reset_rows(t, t.s_reset.as<uint64_t>(), &t.d_ctr->reset_count, st);
@@ -571,9 +604,6 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
         else MPZCH_CUDA(cudaMemsetAsync(a.out_mark, 0, n, st));
     }
     if (ttl) enqueue_compact_evicted(t, n, a.out_ev, a.ev_cap, st);
-    k_cleanup<<<gW, B, 0, st>>>(t.d_ctr, t.s_elist.as<uint32_t>(), t.s_tkey.as<uint64_t>(),
-                                t.s_tmin.as<unsigned>(), t.s_tstate.as<uint8_t>());
-    ++t.launches;
     if (t.profiling) cudaEventRecord(t.ev[3], st);
 }
 

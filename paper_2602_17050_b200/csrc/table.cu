@@ -163,24 +163,24 @@ Table::~Table() {
 
 void Table::ensure_fast_scratch(uint64_t n) {
     s_newpos.reserve(n * 4);
+    s_newid.reserve(n * 8);
     s_newa.reserve(n * 4);
     s_newm.reserve(n * 4);
     s_newent.reserve(n * 4);
     const uint64_t want = pow2_at_least(2 * n);
     if (want > tcap) {
-        s_tkey.reserve(want * 8);
-        s_tmin.reserve(want * 4);
+        s_tkey.reserve(want * 16);  // epoch-tagged keys: epoch 0 = empty
+        s_tmin.reserve(want * 8);   // epoch-tagged rank words
         s_ta.reserve(want * 4);
         s_tm.reserve(want * 4);
         s_theld.reserve(want * 4);
         s_tstate.reserve(want);
         s_tslot.reserve(want * 8);
         s_toc.reserve(want);
-        s_elist.reserve(want * 4);
-        MPZCH_CUDA(cudaMemsetAsync(s_tkey.p, 0xff, want * 8, stream));
-        MPZCH_CUDA(cudaMemsetAsync(s_tmin.p, 0xff, want * 4, stream));
-        MPZCH_CUDA(cudaMemsetAsync(s_tstate.p, 0, want, stream));
+        MPZCH_CUDA(cudaMemsetAsync(s_tkey.p, 0, want * 16, stream));
+        MPZCH_CUDA(cudaMemsetAsync(s_tmin.p, 0, want * 8, stream));
         tcap = want;
+        epoch = 0;
     }
     s_reset.reserve(n * 8);
     const size_t fl = ((n + 15) & ~15ull) + 16;
@@ -190,7 +190,10 @@ void Table::ensure_fast_scratch(uint64_t n) {
     }
     s_evslot.reserve(n * 8);
     s_blk.reserve(((n + kCompactChunk - 1) / kCompactChunk + 1) * 4);
-    MPZCH_CUDA(cudaStreamSynchronize(stream));
+    if (n > fast_ready) {  // first use at this size: the memsets above must land first
+        MPZCH_CUDA(cudaStreamSynchronize(stream));
+        fast_ready = n;
+    }
 }
 
 void Table::ensure_ordered_scratch(uint64_t n) {

@@ -110,9 +110,11 @@ public:
     BatchCounters* d_ctr = nullptr;
 
     // scratch
-    DevBuf s_newpos, s_newa, s_newm, s_newent;      // new-list (fast path)
-    DevBuf s_tkey, s_tmin, s_ta, s_tm, s_theld, s_tstate, s_tslot, s_toc, s_elist;  // id table
+    DevBuf s_newpos, s_newid, s_newa, s_newm, s_newent;  // new-list (fast path)
+    DevBuf s_tkey, s_tmin, s_ta, s_tm, s_theld, s_tstate, s_tslot, s_toc;  // id table
     uint64_t tcap = 0;                               // allocated id-table capacity (pow2)
+    uint64_t epoch = 0;                              // id-table batch epoch (0 = never used)
+    uint64_t fast_ready = 0;                         // largest n the fast scratch is ready for
     DevBuf s_reset;                                  // rows to reset
     DevBuf s_evflag, s_evslot, s_blk;                // evicted-list compaction
     DevBuf s_ids, s_feats, s_oslot, s_ooc, s_oev;    // staging for host-buffer calls
