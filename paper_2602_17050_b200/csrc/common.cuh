@@ -121,6 +121,14 @@ __device__ __forceinline__ void ld_sector(const uint64_t* p, uint64_t& a, uint64
                  : "l"(p));
 }
 
+// L2-coherent (L1-bypassing) sector load, for state other threads mutate in this kernel
+__device__ __forceinline__ void ld_sector_cg(const uint64_t* p, uint64_t& a, uint64_t& b, uint64_t& c,
+                                             uint64_t& d) {
+    asm volatile("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+                 : "l"(p));
+}
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 }  // namespace mpzch_b200

@@ -151,8 +151,6 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
                                                uint32_t* __restrict__ newm) {
     if (batch_failed(&ctr->err)) return;
     constexpr uint8_t kPending = 0, kHit = 1, kEmptyHit = 2, kExhausted = 3, kIdle = 4;
-    __shared__ unsigned s_cnt[32];
-    __shared__ unsigned s_base;
     const unsigned lane = lane_id();
     const uint64_t tile = (uint64_t)blockDim.x * U;
     unsigned long long my_found = 0, my_coll = 0, my_isec = 0, my_msec = 0;
@@ -240,29 +238,21 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
                     if (foc == kFound) ++my_found; else ++my_coll;
                 }
             }
-            // block-aggregated append of the new positions (one global atomic per block-tile)
+            // warp-aggregated append of the new positions (a block barrier here would make
+            // every warp wait for the slowest probe of the tile: measured slower)
             const unsigned mask = __ballot_sync(0xffffffffu, is_new);
-            const unsigned wid = threadIdx.x >> 5;
-            if (lane == 0) s_cnt[wid] = __popc(mask);
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                unsigned tot = 0;
-                for (unsigned w = 0; w < blockDim.x / 32; ++w) {
-                    const unsigned c = s_cnt[w];
-                    s_cnt[w] = tot;
-                    tot += c;
+            if (mask) {
+                unsigned basek = 0;
+                if (lane == 0) basek = atomicAdd(&ctr->new_count, (unsigned)__popc(mask));
+                basek = __shfl_sync(0xffffffffu, basek, 0);
+                if (is_new) {
+                    const unsigned k = basek + __popc(mask & ((1u << lane) - 1));
+                    newpos[k] = (uint32_t)i;
+                    newid[k] = id[u];
+                    newa[k] = a_off;
+                    newm[k] = m_off;
                 }
-                s_base = tot ? atomicAdd(&ctr->new_count, tot) : 0;
             }
-            __syncthreads();
-            if (is_new) {
-                const unsigned k = s_base + s_cnt[wid] + __popc(mask & ((1u << lane) - 1));
-                newpos[k] = (uint32_t)i;
-                newid[k] = id[u];
-                newa[k] = a_off;
-                newm[k] = m_off;
-            }
-            __syncthreads();
         }
     }
     for (int o = 16; o; o >>= 1) {
@@ -383,9 +373,16 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                 off = fresh ? ta[e] : resume;
             }
             if (!held) {
+                // sector-wide scan: one L2 read per 4 slots; a slot is re-read only through
+                // the CAS that tries it
+                uint64_t sec_a4 = ~0ull, w0 = 0, w1 = 0, w2 = 0, w3 = 0;
                 for (; off < t.P; ++off) {
                     const uint64_t g = base + wrap_add(h, off, cap);
-                    uint64_t v = ld_cg(t.ident + g);
+                    if ((g & ~3ull) != sec_a4) {
+                        sec_a4 = g & ~3ull;
+                        ld_sector_cg(t.ident + sec_a4, w0, w1, w2, w3);
+                    }
+                    uint64_t v = pick4((uint32_t)(g - sec_a4), w0, w1, w2, w3);
                     for (;;) {
                         uint64_t nv;
                         if (v == kEmpty) {
