@@ -296,6 +296,9 @@ def main():
 
         def remap(ids, now):
             table.process_batch_device(ids, now, pol, None, out_s, out_o, None, stream)
+
+        def remap_async(ids, now):  # enqueue only; the ticket is waited after the loop
+            return table.process_batch_device_async(ids, now, pol, None, out_s, out_o, None, stream)
     else:
         # C5 row-sharded: the S=8 logical shards of ONE 1B-slot table spread over the ranks;
         # every global batch of BATCH positions is split into rank slices (strong scaling)
@@ -305,6 +308,8 @@ def main():
 
         def remap(ids, now):
             sharded.process_batch(ids, now, pol)
+
+        remap_async = None  # the sharded protocol synchronises on its collectives
 
     def my_slice(lo, hi):
         n = hi - lo
@@ -348,9 +353,17 @@ def main():
         torch.cuda.synchronize(dev)
         w0 = time.time()
         ev0.record(stream)
-        for b in range(args.warmup, nb):
-            remap(batches[b], 2 + b)
-            stats.append(probe_table.last_stats())
+        if remap_async is not None:
+            # pipelined: enqueue every step, then wait each ticket (each wait reports its
+            # batch's errors exactly as the synchronous call would)
+            tickets = [remap_async(batches[b], 2 + b) for b in range(args.warmup, nb)]
+            for tk in tickets:
+                table.wait(tk)
+                stats.append(probe_table.last_stats())
+        else:
+            for b in range(args.warmup, nb):
+                remap(batches[b], 2 + b)
+                stats.append(probe_table.last_stats())
         ev1.record(stream)
         torch.cuda.synchronize(dev)
         ms_total = ev0.elapsed_time(ev1)

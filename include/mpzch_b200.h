@@ -118,6 +118,21 @@ mpzch_status mpzch_process_batch_device(mpzch_table* t, const uint64_t* ids,
                                         uint64_t evicted_cap, uint64_t* out_evicted_n,
                                         void* stream);
 
+/* Asynchronous variant: enqueues the batch on `stream` and returns a ticket without
+ * waiting (host-side argument errors are still returned immediately).  mpzch_batch_wait
+ * blocks until the ticket's batch is done and returns ITS status (invalid id, TTL overflow,
+ * ... exactly as the synchronous call would have) and evicted-list length.  Batches of one
+ * handle run in enqueue order; a batch that fails validation mutates nothing, so later
+ * batches see the table as if the failed call had thrown.  Up to 8 batches may be in flight;
+ * results of the last 64 tickets stay retrievable. */
+mpzch_status mpzch_process_batch_device_async(mpzch_table* t, const uint64_t* ids,
+                                              const uint32_t* features, uint64_t n, uint64_t now,
+                                              const mpzch_policy* policy, uint64_t* out_slots,
+                                              uint8_t* out_outcomes, uint64_t* out_evicted,
+                                              uint64_t evicted_cap, void* stream,
+                                              uint64_t* out_ticket);
+mpzch_status mpzch_batch_wait(mpzch_table* t, uint64_t ticket, uint64_t* out_evicted_n);
+
 /* ---- lookup-only: MpzchTable::lookup(Id) const, table.hpp:65, table.cpp:150-156,
  *      batched (semantics = one lookup per position, no writes). */
 mpzch_status mpzch_lookup(const mpzch_table* t, const uint64_t* ids, uint64_t n,

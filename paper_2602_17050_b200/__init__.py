@@ -131,6 +131,10 @@ _SIGS = {
     "mpzch_process_batch_device": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_uint64, ctypes.c_uint64,
                                                   ctypes.POINTER(_Policy), _vp, _vp, _vp,
                                                   ctypes.c_uint64, _u64p, _vp]),
+    "mpzch_process_batch_device_async": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_uint64,
+                                                        ctypes.c_uint64, ctypes.POINTER(_Policy),
+                                                        _vp, _vp, _vp, ctypes.c_uint64, _vp, _u64p]),
+    "mpzch_batch_wait": (ctypes.c_int, [_vp, ctypes.c_uint64, _u64p]),
     "mpzch_lookup": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _vp, _vp]),
     "mpzch_lookup_device": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _vp, _vp, _vp]),
     "mpzch_lookup_or_insert": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint32,
@@ -413,6 +417,29 @@ class MpzchTable:
             ctypes.c_void_p(mark.data_ptr()) if n else None, ctypes.byref(nev),
             ctypes.c_void_p(st.cuda_stream)))
         return slots, oc, mark
+
+    def process_batch_device_async(self, ids, now: int, policy: EvictionPolicy, features=None,
+                                   out_slots=None, out_outcomes=None, out_evicted=None,
+                                   stream=None) -> int:
+        """Enqueue process_batch on device tensors and return a ticket (see wait)."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        tk = ctypes.c_uint64(0)
+        _check(self._lib.mpzch_process_batch_device_async(
+            self._h, ctypes.c_void_p(ids.data_ptr()),
+            ctypes.c_void_p(features.data_ptr()) if features is not None else None, ids.numel(), now,
+            ctypes.byref(policy._c), ctypes.c_void_p(out_slots.data_ptr()),
+            ctypes.c_void_p(out_outcomes.data_ptr()),
+            ctypes.c_void_p(out_evicted.data_ptr()) if out_evicted is not None else None,
+            out_evicted.numel() if out_evicted is not None else 0, ctypes.c_void_p(st.cuda_stream),
+            ctypes.byref(tk)))
+        return tk.value
+
+    def wait(self, ticket: int) -> int:
+        """Block until the ticket's batch is done; raise its error; return its evicted count."""
+        nev = ctypes.c_uint64(0)
+        _check(self._lib.mpzch_batch_wait(self._h, ticket, ctypes.byref(nev)))
+        return nev.value
 
     def lookup(self, ids) -> Tuple[np.ndarray, np.ndarray]:
         """Batched MpzchTable::lookup (table.cpp:150-156): (slots, outcomes), no writes."""

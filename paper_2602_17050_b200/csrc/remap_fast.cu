@@ -537,11 +537,11 @@ __global__ void __launch_bounds__(256) k_finalize(BatchCounters* ctr,
 }  // namespace
 
 void run_validate(Table& t, const uint64_t* ids, uint64_t n, cudaStream_t st) {
-    k_init_counters<<<1, 32, 0, st>>>(t.d_ctr);
-    k_validate<<<grid_for(n / 2 + 1, 256, 148u * 8u), 256, 0, st>>>(t.dev, ids, n, t.d_ctr);
+    k_init_counters<<<1, 32, 0, st>>>(t.d_aux);
+    k_validate<<<grid_for(n / 2 + 1, 256, 148u * 8u), 256, 0, st>>>(t.dev, ids, n, t.d_aux);
     t.launches += 2;
     MPZCH_CUDA(cudaGetLastError());
-    MPZCH_CUDA(cudaMemcpyAsync(&t.h_ctr->err, &t.d_ctr->err, sizeof(BatchErr), cudaMemcpyDeviceToHost, st));
+    MPZCH_CUDA(cudaMemcpyAsync(&t.h_aux->err, &t.d_aux->err, sizeof(BatchErr), cudaMemcpyDeviceToHost, st));
     MPZCH_CUDA(cudaStreamSynchronize(st));
 }
 

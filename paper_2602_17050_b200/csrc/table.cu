@@ -98,8 +98,13 @@ Table::Table(const uint64_t* cap_in, uint32_t num_shards, uint32_t max_probe, ui
 
     DeviceGuard g(device);
     MPZCH_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-    MPZCH_CUDA(cudaMallocHost((void**)&h_ctr, sizeof(BatchCounters)));
-    MPZCH_CUDA(cudaMalloc((void**)&d_ctr, sizeof(BatchCounters)));
+    MPZCH_CUDA(cudaMallocHost((void**)&h_ring, (kRing + 1) * sizeof(BatchCounters)));
+    MPZCH_CUDA(cudaMalloc((void**)&d_ring, (kRing + 1) * sizeof(BatchCounters)));
+    h_aux = h_ring + kRing;
+    d_aux = d_ring + kRing;
+    h_ctr = h_ring;
+    d_ctr = d_ring;
+    for (auto& sl : slots) MPZCH_CUDA(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
     // identity/metadata start 4-row aligned and are padded so a 32-byte sector load at the
     // first or last held slot stays in bounds
     const uint64_t padded = ((row_hi - row_base + 3) & ~3ull) + 4;
@@ -154,10 +159,13 @@ Table::~Table() {
     cudaFree(momentum);
     cudaFree(trained);
     cudaFree(d_shards);
-    cudaFree(d_ctr);
-    if (h_ctr) cudaFreeHost(h_ctr);
-    for (auto& e : ev)
-        if (e) cudaEventDestroy(e);
+    cudaFree(d_ring);
+    if (h_ring) cudaFreeHost(h_ring);
+    for (auto& sl : slots) {
+        if (sl.done) cudaEventDestroy(sl.done);
+        for (auto& e : sl.ev)
+            if (e) cudaEventDestroy(e);
+    }
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -282,14 +290,100 @@ void require_valid_id(uint64_t id) {  // ids.hpp:25-31
                                           : "id exceeds the 63-bit ID space"};
 }
 
-// The batch core shared by the host- and device-buffer entry points.
-void run_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n, uint64_t now,
-               const Policy& pol, uint64_t* out_slots, uint8_t* out_oc, uint64_t* out_ev,
-               uint64_t ev_cap, uint64_t* out_ev_n, cudaStream_t st, uint8_t* out_mark = nullptr) {
+// Turn a finished slot's counters into its Result (errors in the reference's order).
+void complete_slot(Table& t, int si) {
+    Table::Slot& sl = t.slots[si];
+    if (!sl.busy) return;
+    MPZCH_CUDA(cudaEventSynchronize(sl.done));
+    const BatchCounters& c = t.h_ring[si];
+    Table::Result r;
+    r.ticket = sl.ticket;
+    if (c.err.too_many == 2) {
+        r.status = MPZCH_ECUDA;
+        r.msg = "internal error: claim invariant violated";
+    } else if (c.err.bad_pos != ~0ull) {
+        r.status = MPZCH_EINVAL;
+        r.msg = "invalid id at batch position " + std::to_string(c.err.bad_pos);
+    } else if (c.err.foreign_pos != ~0ull) {
+        r.status = MPZCH_ERANGE;
+        r.msg = "id at batch position " + std::to_string(c.err.foreign_pos) +
+                " routes to a shard this handle does not hold";
+    } else if (sl.overflow_all || c.err.overflow) {
+        r.status = MPZCH_EOVERFLOW;
+        r.msg = "TTL expiry overflows the 64-bit timestamp range";
+    }
+    if (r.status == MPZCH_OK) {
+        r.evicted_n = c.evicted_count;
+        mpzch_batch_stats& s = r.stats;
+        s.positions = sl.n;
+        s.new_positions = sl.fast ? c.new_count : 0;
+        s.new_ids = c.entry_count;
+        s.found = c.found;
+        s.inserted = c.inserted;
+        s.evicted = c.evicted;
+        s.collision = c.collision;
+        s.evicted_rows = c.evicted_count;
+        s.path = sl.fast ? MPZCH_PATH_AUTO : MPZCH_PATH_ORDERED;
+        t.last = s;
+        if (sl.profiled && sl.fast) {
+            float a01 = 0, a12 = 0, a23 = 0, a03 = 0;
+            MPZCH_CUDA(cudaEventElapsedTime(&a01, sl.ev[0], sl.ev[1]));
+            MPZCH_CUDA(cudaEventElapsedTime(&a12, sl.ev[1], sl.ev[2]));
+            MPZCH_CUDA(cudaEventElapsedTime(&a23, sl.ev[2], sl.ev[3]));
+            MPZCH_CUDA(cudaEventElapsedTime(&a03, sl.ev[0], sl.ev[3]));
+            mpzch_profile& p = t.prof;
+            const uint64_t n = sl.n;
+            p.batches += 1;
+            p.probe_launches += 1;
+            p.probe_ms += a01;
+            p.claim_ms += a12;
+            p.tail_ms += a23;
+            p.batch_ms += a03;
+            const uint64_t sectors = c.id_sectors + c.meta_sectors;
+            const uint64_t n_final = n - c.new_count;
+            p.probe_sectors += sectors;
+            // probe kernel: sectors read + 8 B id per position + 9 B result and one metadata
+            // sector written per final position + 12 B new-list record per new position
+            p.probe_bytes += 32 * sectors + 8 * n + (9 + 32) * n_final + 12ull * c.new_count;
+            // whole batch (SURVEY 8d terms, counted per position): probe reads, 8 B id in,
+            // 9 B result out, one metadata sector written per position, one identity sector +
+            // 8 B row_generation per Inserted/Evicted position, 8*dim+1 B per reset row
+            p.batch_bytes += 32 * sectors + 8 * n + 9 * n + 32 * n +
+                             40ull * (c.inserted + c.evicted) +
+                             (uint64_t)c.reset_count * (8ull * t.dim + 1);
+        }
+    }
+    t.results[r.ticket % Table::kResults] = std::move(r);
+    sl.busy = false;
+}
+
+// Enqueue one batch on `st`; returns its ticket.  Host-detectable argument errors throw
+// here; device-detected ones (invalid id, ...) are reported by wait_batch.
+uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n,
+                       uint64_t now, const Policy& pol, uint64_t* out_slots, uint8_t* out_oc,
+                       uint64_t* out_ev, uint64_t ev_cap, cudaStream_t st,
+                       uint8_t* out_mark = nullptr) {
     if (n > 0xffffffffull) throw Error{MPZCH_ELENGTH, "batch exceeds 2^32 - 1 positions"};
-    if (out_ev_n) *out_ev_n = 0;
-    t.last = mpzch_batch_stats{};
-    if (n == 0) return;
+    const uint64_t ticket = t.next_ticket++;
+    const int si = (int)(ticket % Table::kRing);
+    if (n == 0) {
+        Table::Result r;
+        r.ticket = ticket;
+        t.results[ticket % Table::kResults] = r;
+        return ticket;
+    }
+    complete_slot(t, si);  // the ring wrapped: retire the batch that used this block
+    // batches of one handle share scratch: order a new stream after the previous batch
+    if (t.last_ticket && st != t.last_stream) {
+        const Table::Slot& prev = t.slots[t.last_ticket % Table::kRing];
+        if (prev.busy && prev.ticket == t.last_ticket) MPZCH_CUDA(cudaStreamWaitEvent(st, prev.done, 0));
+    }
+    Table::Slot& sl = t.slots[si];
+    t.d_ctr = t.d_ring + si;
+    t.h_ctr = t.h_ring + si;
+    if (t.profiling && !sl.ev[0])
+        for (auto& e : sl.ev) MPZCH_CUDA(cudaEventCreate(&e));
+    t.ev = sl.ev;
     BatchArgs a{};
     a.ids = ids;
     a.feats = feats;
@@ -330,57 +424,44 @@ void run_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n,
     }
     const bool fast = t.path_override == MPZCH_PATH_AUTO && t.hole_free &&
                       pol.mode != kModeLru && a.uniform && n <= (1ull << 29);
+    const bool profiled = t.profiling;
+    if (!fast) t.profiling = false;  // events are recorded by the fast path only
     if (fast) enqueue_fast_batch(t, a, st);
     else enqueue_ordered_batch(t, a, st);
+    t.profiling = profiled;
     MPZCH_CUDA(cudaGetLastError());
     MPZCH_CUDA(cudaMemcpyAsync(t.h_ctr, t.d_ctr, sizeof(BatchCounters), cudaMemcpyDeviceToHost, st));
-    MPZCH_CUDA(cudaStreamSynchronize(st));
-    const BatchCounters& c = *t.h_ctr;
-    if (c.err.too_many == 2) throw Error{MPZCH_ECUDA, "internal error: claim invariant violated"};
-    if (c.err.bad_pos != ~0ull)
-        throw Error{MPZCH_EINVAL, "invalid id at batch position " + std::to_string(c.err.bad_pos)};
-    if (c.err.foreign_pos != ~0ull)
-        throw Error{MPZCH_ERANGE, "id at batch position " + std::to_string(c.err.foreign_pos) +
-                                      " routes to a shard this handle does not hold"};
-    if (a.overflow_all || c.err.overflow)
-        throw Error{MPZCH_EOVERFLOW, "TTL expiry overflows the 64-bit timestamp range"};
-    if (out_ev_n) *out_ev_n = c.evicted_count;
-    mpzch_batch_stats& s = t.last;
-    s.positions = n;
-    s.new_positions = fast ? c.new_count : 0;
-    s.new_ids = c.entry_count;
-    s.found = c.found;
-    s.inserted = c.inserted;
-    s.evicted = c.evicted;
-    s.collision = c.collision;
-    s.evicted_rows = c.evicted_count;
-    s.path = fast ? MPZCH_PATH_AUTO : MPZCH_PATH_ORDERED;
-    if (t.profiling && fast) {
-        float a01 = 0, a12 = 0, a23 = 0, a03 = 0;
-        MPZCH_CUDA(cudaEventElapsedTime(&a01, t.ev[0], t.ev[1]));
-        MPZCH_CUDA(cudaEventElapsedTime(&a12, t.ev[1], t.ev[2]));
-        MPZCH_CUDA(cudaEventElapsedTime(&a23, t.ev[2], t.ev[3]));
-        MPZCH_CUDA(cudaEventElapsedTime(&a03, t.ev[0], t.ev[3]));
-        mpzch_profile& p = t.prof;
-        p.batches += 1;
-        p.probe_launches += 1;
-        p.probe_ms += a01;
-        p.claim_ms += a12;
-        p.tail_ms += a23;
-        p.batch_ms += a03;
-        const uint64_t sectors = c.id_sectors + c.meta_sectors;
-        const uint64_t n_final = n - c.new_count;
-        p.probe_sectors += sectors;
-        // probe kernel: sectors read + 8 B id per position + 9 B result and one metadata
-        // sector written per final position + 12 B new-list record per new position
-        p.probe_bytes += 32 * sectors + 8 * n + (9 + 32) * n_final + 12ull * c.new_count;
-        // whole batch (SURVEY 8d terms, counted per position): probe reads, 8 B id in,
-        // 9 B result out, one metadata sector written per position, one identity sector +
-        // 8 B row_generation per Inserted/Evicted position, 8*dim+1 B per reset row
-        p.batch_bytes += 32 * sectors + 8 * n + 9 * n + 32 * n +
-                         40ull * (c.inserted + c.evicted) +
-                         (uint64_t)c.reset_count * (8ull * t.dim + 1);
-    }
+    MPZCH_CUDA(cudaEventRecord(sl.done, st));
+    sl.busy = true;
+    sl.ticket = ticket;
+    sl.n = n;
+    sl.fast = fast;
+    sl.overflow_all = a.overflow_all;
+    sl.profiled = profiled;
+    t.last_stream = st;
+    t.last_ticket = ticket;
+    return ticket;
+}
+
+// Wait for a ticket; rethrow its error; return its evicted-list length.
+uint64_t wait_batch(Table& t, uint64_t ticket) {
+    const int si = (int)(ticket % Table::kRing);
+    if (t.slots[si].busy && t.slots[si].ticket == ticket) complete_slot(t, si);
+    const Table::Result& r = t.results[ticket % Table::kResults];
+    if (r.ticket != ticket) throw Error{MPZCH_EINVAL, "unknown or expired batch ticket"};
+    if (r.status != MPZCH_OK) throw Error{r.status, r.msg};
+    return r.evicted_n;
+}
+
+void run_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n, uint64_t now,
+               const Policy& pol, uint64_t* out_slots, uint8_t* out_oc, uint64_t* out_ev,
+               uint64_t ev_cap, uint64_t* out_ev_n, cudaStream_t st, uint8_t* out_mark = nullptr) {
+    if (out_ev_n) *out_ev_n = 0;
+    const uint64_t tk = enqueue_batch(t, ids, feats, n, now, pol, out_slots, out_oc, out_ev, ev_cap,
+                                      st, out_mark);
+    const uint64_t nev = wait_batch(t, tk);
+    if (out_ev_n) *out_ev_n = nev;
+    if (n == 0) t.last = mpzch_batch_stats{};
 }
 
 template <class F>
@@ -481,7 +562,7 @@ mpzch_status mpzch_validate_device(const mpzch_table* t, const uint64_t* ids, ui
         *out_bad_pos = ~0ull;
         if (n == 0) return;
         run_validate(T, ids, n, (cudaStream_t)stream);
-        *out_bad_pos = T.h_ctr->err.bad_pos;
+        *out_bad_pos = T.h_aux->err.bad_pos;
     });
 }
 
@@ -546,6 +627,31 @@ mpzch_status mpzch_process_batch_device(mpzch_table* t, const uint64_t* ids, con
     });
 }
 
+mpzch_status mpzch_process_batch_device_async(mpzch_table* t, const uint64_t* ids,
+                                              const uint32_t* feats, uint64_t n, uint64_t now,
+                                              const mpzch_policy* policy, uint64_t* out_slots,
+                                              uint8_t* out_oc, uint64_t* out_ev, uint64_t ev_cap,
+                                              void* stream, uint64_t* out_ticket) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        DeviceGuard g(T.device);
+        const Policy pol = parse_policy(policy);
+        *out_ticket = enqueue_batch(T, ids, feats, n, now, pol, out_slots, out_oc, out_ev, ev_cap,
+                                    (cudaStream_t)stream);
+    });
+}
+
+mpzch_status mpzch_batch_wait(mpzch_table* t, uint64_t ticket, uint64_t* out_ev_n) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        DeviceGuard g(T.device);
+        const uint64_t nev = wait_batch(T, ticket);
+        if (out_ev_n) *out_ev_n = nev;
+    });
+}
+
 mpzch_status mpzch_process_batch(mpzch_table* t, const uint64_t* ids, const uint32_t* feats,
                                  uint64_t n, uint64_t now, const mpzch_policy* policy,
                                  uint64_t* out_slots, uint8_t* out_oc, uint64_t* out_ev,
@@ -599,20 +705,20 @@ mpzch_status mpzch_lookup_device(const mpzch_table* t, const uint64_t* ids, uint
         if (n == 0) return;
         cudaStream_t st = (cudaStream_t)stream;  // 0 = legacy default stream
         BatchErr init{~0ull, 0, 0, ~0ull};
-        MPZCH_CUDA(cudaMemcpyAsync(&T.d_ctr->err, &init, sizeof init, cudaMemcpyHostToDevice, st));
-        run_lookup(T, ids, n, out_slots, out_oc, &T.d_ctr->err, st);
+        MPZCH_CUDA(cudaMemcpyAsync(&T.d_aux->err, &init, sizeof init, cudaMemcpyHostToDevice, st));
+        run_lookup(T, ids, n, out_slots, out_oc, &T.d_aux->err, st);
         ++T.launches;
         MPZCH_CUDA(cudaGetLastError());
-        MPZCH_CUDA(cudaMemcpyAsync(&T.h_ctr->err, &T.d_ctr->err, sizeof(BatchErr),
+        MPZCH_CUDA(cudaMemcpyAsync(&T.h_aux->err, &T.d_aux->err, sizeof(BatchErr),
                                    cudaMemcpyDeviceToHost, st));
         MPZCH_CUDA(cudaStreamSynchronize(st));
-        if (T.h_ctr->err.bad_pos != ~0ull) {
+        if (T.h_aux->err.bad_pos != ~0ull) {
             uint64_t bad = 0;
-            MPZCH_CUDA(cudaMemcpy(&bad, ids + T.h_ctr->err.bad_pos, 8, cudaMemcpyDeviceToHost));
+            MPZCH_CUDA(cudaMemcpy(&bad, ids + T.h_aux->err.bad_pos, 8, cudaMemcpyDeviceToHost));
             require_valid_id(bad);
         }
-        if (T.h_ctr->err.foreign_pos != ~0ull)
-            throw Error{MPZCH_ERANGE, "id at batch position " + std::to_string(T.h_ctr->err.foreign_pos) +
+        if (T.h_aux->err.foreign_pos != ~0ull)
+            throw Error{MPZCH_ERANGE, "id at batch position " + std::to_string(T.h_aux->err.foreign_pos) +
                                           " routes to a shard this handle does not hold"};
     });
 }
@@ -630,19 +736,19 @@ mpzch_status mpzch_lookup(const mpzch_table* t, const uint64_t* ids, uint64_t n,
         T.s_ooc.reserve(n);
         MPZCH_CUDA(cudaMemcpyAsync(T.s_ids.p, ids, n * 8, cudaMemcpyHostToDevice, st));
         BatchErr init{~0ull, 0, 0, ~0ull};
-        MPZCH_CUDA(cudaMemcpyAsync(&T.d_ctr->err, &init, sizeof init, cudaMemcpyHostToDevice, st));
+        MPZCH_CUDA(cudaMemcpyAsync(&T.d_aux->err, &init, sizeof init, cudaMemcpyHostToDevice, st));
         run_lookup(T, T.s_ids.as<uint64_t>(), n, T.s_oslot.as<uint64_t>(), T.s_ooc.as<uint8_t>(),
-                   &T.d_ctr->err, st);
+                   &T.d_aux->err, st);
         ++T.launches;
         MPZCH_CUDA(cudaGetLastError());
-        MPZCH_CUDA(cudaMemcpyAsync(&T.h_ctr->err, &T.d_ctr->err, sizeof(BatchErr),
+        MPZCH_CUDA(cudaMemcpyAsync(&T.h_aux->err, &T.d_aux->err, sizeof(BatchErr),
                                    cudaMemcpyDeviceToHost, st));
         MPZCH_CUDA(cudaMemcpyAsync(out_slots, T.s_oslot.p, n * 8, cudaMemcpyDeviceToHost, st));
         MPZCH_CUDA(cudaMemcpyAsync(out_oc, T.s_ooc.p, n, cudaMemcpyDeviceToHost, st));
         MPZCH_CUDA(cudaStreamSynchronize(st));
-        if (T.h_ctr->err.bad_pos != ~0ull) require_valid_id(ids[T.h_ctr->err.bad_pos]);
-        if (T.h_ctr->err.foreign_pos != ~0ull)
-            throw Error{MPZCH_ERANGE, "id at batch position " + std::to_string(T.h_ctr->err.foreign_pos) +
+        if (T.h_aux->err.bad_pos != ~0ull) require_valid_id(ids[T.h_aux->err.bad_pos]);
+        if (T.h_aux->err.foreign_pos != ~0ull)
+            throw Error{MPZCH_ERANGE, "id at batch position " + std::to_string(T.h_aux->err.foreign_pos) +
                                           " routes to a shard this handle does not hold"};
     });
 }
@@ -830,7 +936,7 @@ mpzch_status mpzch_dirty_rows_since(const mpzch_table* t, uint64_t gen, uint64_t
         k_dirty_flags<<<grid_for(held, 256), 256, 0, st>>>(T.row_gen, held, gen,
                                                             flags.as<uint8_t>());
         ++T.launches;
-        unsigned* d_n = &T.d_ctr->pad;
+        unsigned* d_n = &T.d_aux->pad;
         EmitIndex em{rows.as<uint64_t>(), cap, T.row_lo};
         compact_flags(flags.as<uint8_t>(), held, blk.as<unsigned>(), d_n, false, em, st, T.launches);
         unsigned nn = 0;
@@ -846,8 +952,6 @@ mpzch_status mpzch_set_profiling(mpzch_table* t, int on) {
     return guarded([&] {
         Table& T = *t->t;
         DeviceGuard g(T.device);
-        if (on && !T.ev[0])
-            for (auto& e : T.ev) MPZCH_CUDA(cudaEventCreate(&e));
         T.profiling = on != 0;
         T.prof = mpzch_profile{};
     });

@@ -93,7 +93,33 @@ public:
     uint64_t launches = 0;
     bool profiling = false;
     mpzch_profile prof{};
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t* ev = nullptr;  // the current batch slot's profiling events
+
+    // ---- in-flight batches (mpzch_process_batch_device_async): a ring of counter blocks,
+    // each with its completion event; results of completed batches kept by ticket
+    static constexpr int kRing = 8, kResults = 64;
+    struct Slot {
+        bool busy = false, fast = false, overflow_all = false, profiled = false;
+        uint64_t ticket = 0, n = 0;
+        cudaEvent_t done = nullptr;
+        cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    };
+    struct Result {
+        uint64_t ticket = ~0ull;
+        mpzch_status status = MPZCH_OK;
+        std::string msg;
+        mpzch_batch_stats stats{};
+        uint64_t evicted_n = 0;
+    };
+    Slot slots[kRing];
+    Result results[kResults];
+    uint64_t next_ticket = 1;
+    cudaStream_t last_stream = nullptr;
+    uint64_t last_ticket = 0;
+    BatchCounters* d_ring = nullptr;  // kRing blocks
+    BatchCounters* h_ring = nullptr;  // pinned
+    BatchCounters* d_aux = nullptr;   // synchronous helpers (lookup, validate, dirty rows)
+    BatchCounters* h_aux = nullptr;
 
     // resident arrays
     uint64_t* ident = nullptr;
@@ -106,7 +132,7 @@ public:
     TableDev dev{};
 
     cudaStream_t stream = nullptr;
-    BatchCounters* h_ctr = nullptr;  // pinned
+    BatchCounters* h_ctr = nullptr;  // the current batch's counters (pinned / device)
     BatchCounters* d_ctr = nullptr;
 
     // scratch

@@ -453,3 +453,45 @@ def test_default_stream_ordering(oracle):
         ids = bench.distinct_ids_t(5, torch.arange(b * B, (b + 1) * B, dtype=torch.int64, device="cuda"))
         t.process_batch_device(ids, 1, mz.EvictionPolicy.disabled(), None, out_s, out_o, None, st)
         assert t.last_stats()["found"] == 0  # fresh distinct ids are never found
+
+
+def test_async_tickets_and_deferred_errors(oracle):
+    """mpzch_process_batch_device_async: batches pipeline on one stream; each ticket's wait
+    reports that batch's result or error; a failed batch mutates nothing."""
+    import torch
+    rows = 1 << 14
+    caps = mz.even_capacities(rows, 4)
+    t = mz.MpzchTable(mz.TableConfig(caps, 32, 5, 4, 2))
+    o = oracle.OracleTable(caps, 32, 5, 4, 2)
+    pol = mz.EvictionPolicy.ttl(mz.TtlPolicy(30))
+    uni = oracle.distinct_ids(6, 0, rows)
+    rng = np.random.default_rng(4)
+    host = []
+    outs = []
+    tickets = []
+    for b in range(12):  # more batches than the 8-slot ring
+        ids = uni[rng.integers(0, uni.size, 3000)].copy()
+        if b == 5:
+            ids[17] = np.uint64(1 << 63)
+        host.append(ids)
+        d = torch.from_numpy(ids.view(np.int64)).cuda()
+        so = torch.empty(ids.size, dtype=torch.int64, device="cuda")
+        oo = torch.empty(ids.size, dtype=torch.uint8, device="cuda")
+        eo = torch.empty(ids.size, dtype=torch.int64, device="cuda")
+        outs.append((d, so, oo, eo))
+        tickets.append(t.process_batch_device_async(d, 10 + 20 * b, pol, None, so, oo, eo))
+    for b, tk in enumerate(tickets):
+        if b == 5:
+            with pytest.raises(mz.InvalidArgument, match="invalid id at batch position 17"):
+                t.wait(tk)
+            with pytest.raises(oracle.OracleError):
+                o.process_batch(host[b], 10 + 20 * b, 1, 30)
+            continue
+        nev = t.wait(tk)
+        s, oc, e = o.process_batch(host[b], 10 + 20 * b, 1, 30)
+        _, so, oo, eo = outs[b]
+        assert (so.cpu().numpy().view(np.uint64) == s).all() and (oo.cpu().numpy() == oc).all()
+        assert nev == e.size and (eo[:nev].cpu().numpy().view(np.uint64) == e).all()
+    assert_same_state(gpu_state(t, 4), oracle_state(o, 4))
+    with pytest.raises(mz.InvalidArgument, match="unknown or expired batch ticket"):
+        t.wait(10 ** 9)
