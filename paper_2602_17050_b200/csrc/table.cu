@@ -324,7 +324,6 @@ void complete_slot(Table& t, int si) {
         s.collision = c.collision;
         s.evicted_rows = c.evicted_count;
         s.path = sl.fast ? MPZCH_PATH_AUTO : MPZCH_PATH_ORDERED;
-        t.last = s;
         if (sl.profiled && sl.fast) {
             float a01 = 0, a12 = 0, a23 = 0, a03 = 0;
             MPZCH_CUDA(cudaEventElapsedTime(&a01, sl.ev[0], sl.ev[1]));
@@ -449,6 +448,7 @@ uint64_t wait_batch(Table& t, uint64_t ticket) {
     if (t.slots[si].busy && t.slots[si].ticket == ticket) complete_slot(t, si);
     const Table::Result& r = t.results[ticket % Table::kResults];
     if (r.ticket != ticket) throw Error{MPZCH_EINVAL, "unknown or expired batch ticket"};
+    t.last = r.stats;  // mpzch_last_stats: the batch most recently waited for
     if (r.status != MPZCH_OK) throw Error{r.status, r.msg};
     return r.evicted_n;
 }
