@@ -224,6 +224,21 @@ typedef struct mpzch_profile {
 mpzch_status mpzch_set_profiling(mpzch_table* t, int on);
 mpzch_status mpzch_get_profile(const mpzch_table* t, mpzch_profile* out);
 
+/* ---- SURVEY 8f "next" rows built on the same tables:
+ * fused lookup + gather (frozen-replica read path): MpzchTable::lookup (table.cpp:150-156)
+ * followed by gather of the resolved rows (table.cpp:158-163); out_rows is n x dim fp32
+ * (device).  Misses gather the home row, as a lookup -> gather pipeline would. */
+mpzch_status mpzch_lookup_gather_device(const mpzch_table* t, const uint64_t* ids, uint64_t n,
+                                        uint64_t* out_slots, uint8_t* out_outcomes,
+                                        float* out_rows, void* stream);
+/* delta cut (DeltaSource::cut, publish.cpp:288-305): the rows dirtied since `generation`
+ * (a cursor from mpzch_make_cursor), each with its identity word and weights (host buffers,
+ * row-major), in row order; *out_n is the full count.  When it fits in `cap` a new cursor is
+ * taken and returned in *out_next_generation (the cut's successor cursor). */
+mpzch_status mpzch_delta_cut(mpzch_table* t, uint64_t generation, uint64_t* out_rows,
+                             uint64_t* out_identities, float* out_weights, uint64_t cap,
+                             uint64_t* out_n, uint64_t* out_next_generation);
+
 /* ---- execution control / introspection */
 mpzch_status mpzch_set_path(mpzch_table* t, int path);
 mpzch_status mpzch_last_stats(const mpzch_table* t, mpzch_batch_stats* out);

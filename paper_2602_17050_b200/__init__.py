@@ -164,6 +164,9 @@ _SIGS = {
     "mpzch_process_batch_device_marked": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_uint64,
                                                          ctypes.c_uint64, ctypes.POINTER(_Policy),
                                                          _vp, _vp, _vp, _u64p, _vp]),
+    "mpzch_lookup_gather_device": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _vp, _vp, _vp, _vp]),
+    "mpzch_delta_cut": (ctypes.c_int, [_vp, ctypes.c_uint64, _vp, _vp, _vp, ctypes.c_uint64, _u64p,
+                                       _u64p]),
     "mpzch_set_path": (ctypes.c_int, [_vp, ctypes.c_int]),
     "mpzch_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),
     "mpzch_get_profile": (ctypes.c_int, [_vp, ctypes.POINTER(_Profile)]),
@@ -538,6 +541,34 @@ class MpzchTable:
         w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float32)
         m = None if momentum is None else np.ascontiguousarray(momentum, dtype=np.float32)
         _check(self._lib.mpzch_write_row(self._h, row, _ptr(w), _ptr(m), trained))
+
+    def lookup_gather_device(self, ids, stream=None):
+        """Fused lookup + gather: (slots, outcomes, rows[n, dim]) device tensors."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        n = ids.numel()
+        slots = torch.empty(n, dtype=torch.int64, device=ids.device)
+        oc = torch.empty(n, dtype=torch.uint8, device=ids.device)
+        rows = torch.empty((n, self.dim), dtype=torch.float32, device=ids.device)
+        _check(self._lib.mpzch_lookup_gather_device(
+            self._h, ctypes.c_void_p(ids.data_ptr()), n, ctypes.c_void_p(slots.data_ptr()),
+            ctypes.c_void_p(oc.data_ptr()), ctypes.c_void_p(rows.data_ptr()),
+            ctypes.c_void_p(st.cuda_stream)))
+        return slots, oc, rows
+
+    def delta_cut(self, cursor: int):
+        """DeltaSource::cut (publish.cpp:288-305) on device: (rows, identities, weights[k, dim],
+        next_cursor)."""
+        cap = self.held_rows
+        rows = np.empty(cap, dtype=np.uint64)
+        ids = np.empty(cap, dtype=np.uint64)
+        w = np.empty((cap, max(self.dim, 1)), dtype=np.float32)
+        n = ctypes.c_uint64(0)
+        nxt = ctypes.c_uint64(0)
+        _check(self._lib.mpzch_delta_cut(self._h, cursor, _ptr(rows), _ptr(ids), _ptr(w), cap,
+                                         ctypes.byref(n), ctypes.byref(nxt)))
+        k = n.value
+        return rows[:k].copy(), ids[:k].copy(), w[:k].copy(), nxt.value
 
     def make_cursor(self) -> int:
         g = ctypes.c_uint64(0)

@@ -63,7 +63,78 @@ __global__ void __launch_bounds__(256) k_lookup(TableDev t, const uint64_t* __re
     }
 }
 
+// Fused lookup + gather (the frozen-replica read path, MpzchTable::lookup
+// table.cpp:150-156 then MpzchTable::gather table.cpp:158-163 / EmbeddingTable::gather
+// embedding_store.cpp:95-103): each lane of a warp probes one position, then the warp copies
+// the 32 resolved rows with 16-byte loads/stores (one row per step, dim/4 lanes busy).
+template <bool kHoleFree>
+__global__ void __launch_bounds__(256) k_lookup_gather(TableDev t, const uint64_t* __restrict__ ids,
+                                                       uint64_t n, uint64_t* __restrict__ out_slots,
+                                                       uint8_t* __restrict__ out_oc,
+                                                       float* __restrict__ out_rows, BatchErr* err) {
+    const unsigned lane = lane_id();
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * 32 < n; w += warps) {
+        const uint64_t i = w * 32 + lane;
+        uint64_t slot = kEmpty;
+        if (i < n) {
+            const uint64_t id = ids[i];
+            if (id >> 63) {
+                atomicMin(&err->bad_pos, (unsigned long long)i);
+            } else if (!holds_shard(t, shard_of(id, t))) {
+                atomicMin(&err->foreign_pos, (unsigned long long)i);
+            } else {
+                const ShardDev sd = t.shards[shard_of(id, t)];
+                const uint64_t cap = sd.cap.d, base = sd.offset, end = base + cap;
+                const uint64_t h = home_of(id, sd, t.seed);
+                uint32_t off = 0;
+                uint64_t g = base + h, gf = kEmpty;
+                bool stop = false;
+                while (off < t.P && !stop) {
+                    const uint64_t a4 = g & ~3ull;
+                    uint64_t w0, w1, w2, w3;
+                    ld_sector(t.ident + a4, w0, w1, w2, w3);
+                    do {
+                        const uint64_t v = pick4((uint32_t)(g - a4), w0, w1, w2, w3);
+                        if (v == id) { gf = g; stop = true; break; }
+                        if (kHoleFree && v == kEmpty) { stop = true; break; }
+                        ++off;
+                        if (++g == end) g = base;
+                    } while (off < t.P && (g >> 2) == (a4 >> 2));
+                }
+                slot = gf != kEmpty ? gf : base + h;
+                out_slots[i] = slot;
+                out_oc[i] = gf != kEmpty ? kFound : kCollision;
+            }
+        }
+        // cooperative row copy
+        const uint32_t quads = t.dim / 4;
+        for (int r = 0; r < 32; ++r) {
+            const uint64_t sr = __shfl_sync(0xffffffffu, slot, r);
+            const uint64_t ir = w * 32 + r;
+            if (ir >= n || sr == kEmpty) continue;
+            const float* src = t.weights + sr * t.dim;
+            float* dst = out_rows + ir * t.dim;
+            if ((t.dim & 3u) == 0) {
+                for (uint32_t q = lane; q < quads; q += 32)
+                    reinterpret_cast<float4*>(dst)[q] = __ldg(reinterpret_cast<const float4*>(src) + q);
+            } else {
+                for (uint32_t j = lane; j < t.dim; j += 32) dst[j] = __ldg(src + j);
+            }
+        }
+    }
+}
+
 }  // namespace
+
+void run_lookup_gather(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots,
+                       uint8_t* out_oc, float* out_rows, BatchErr* err, cudaStream_t st) {
+    const unsigned grid = grid_for((n + 31) / 32 * 32, 256, 148u * 16u);
+    if (t.hole_free)
+        k_lookup_gather<true><<<grid, 256, 0, st>>>(t.dev, ids, n, out_slots, out_oc, out_rows, err);
+    else
+        k_lookup_gather<false><<<grid, 256, 0, st>>>(t.dev, ids, n, out_slots, out_oc, out_rows, err);
+}
 
 void run_lookup(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots, uint8_t* out_oc,
                 BatchErr* err, cudaStream_t st) {

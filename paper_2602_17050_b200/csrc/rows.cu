@@ -126,7 +126,35 @@ __global__ void __launch_bounds__(256) k_hole_check(TableDev t, unsigned* bad) {
     }
 }
 
+// Delta cut gather (DeltaSource::cut, proj/src/publish.cpp:288-305): for each dirty row,
+// its identity word and its weights.  One warp per row, 16-byte copies.
+__global__ void __launch_bounds__(256) k_gather_rows(TableDev t, const uint64_t* __restrict__ rows,
+                                                     uint64_t n, uint64_t* __restrict__ out_ids,
+                                                     float* __restrict__ out_w) {
+    const unsigned lane = lane_id();
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+        const uint64_t row = rows[r];
+        if (lane == 0) out_ids[r] = t.ident[row];
+        if (!out_w) continue;
+        const float* src = t.weights + row * t.dim;
+        float* dst = out_w + r * t.dim;
+        if ((t.dim & 3u) == 0) {
+            for (uint32_t q = lane; q < t.dim / 4; q += 32)
+                reinterpret_cast<float4*>(dst)[q] = reinterpret_cast<const float4*>(src)[q];
+        } else {
+            for (uint32_t j = lane; j < t.dim; j += 32) dst[j] = src[j];
+        }
+    }
+}
+
 }  // namespace
+
+void run_gather_rows(const Table& t, const uint64_t* rows, uint64_t n, uint64_t* out_ids, float* out_w,
+                     cudaStream_t st) {
+    if (!n) return;
+    k_gather_rows<<<grid_for(n * 32, 256, 148u * 16u), 256, 0, st>>>(t.dev, rows, n, out_ids, out_w);
+}
 
 void launch_init_table(Table& t) {
     if (t.dim == 0 || t.held_rows() == 0) return;

@@ -963,6 +963,81 @@ mpzch_status mpzch_get_profile(const mpzch_table* t, mpzch_profile* out) {
     return MPZCH_OK;
 }
 
+mpzch_status mpzch_lookup_gather_device(const mpzch_table* t, const uint64_t* ids, uint64_t n,
+                                        uint64_t* out_slots, uint8_t* out_oc, float* out_rows,
+                                        void* stream) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        if (T.dim == 0) throw Error{MPZCH_ELOGIC, "table has no embedding payload (dim = 0)"};
+        DeviceGuard g(T.device);
+        if (n == 0) return;
+        cudaStream_t st = (cudaStream_t)stream;
+        BatchErr init{~0ull, 0, 0, ~0ull};
+        MPZCH_CUDA(cudaMemcpyAsync(&T.d_aux->err, &init, sizeof init, cudaMemcpyHostToDevice, st));
+        run_lookup_gather(T, ids, n, out_slots, out_oc, out_rows, &T.d_aux->err, st);
+        ++T.launches;
+        MPZCH_CUDA(cudaGetLastError());
+        MPZCH_CUDA(cudaMemcpyAsync(&T.h_aux->err, &T.d_aux->err, sizeof(BatchErr),
+                                   cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaStreamSynchronize(st));
+        if (T.h_aux->err.bad_pos != ~0ull) {
+            uint64_t bad = 0;
+            MPZCH_CUDA(cudaMemcpy(&bad, ids + T.h_aux->err.bad_pos, 8, cudaMemcpyDeviceToHost));
+            require_valid_id(bad);
+        }
+        if (T.h_aux->err.foreign_pos != ~0ull)
+            throw Error{MPZCH_ERANGE, "id at batch position " + std::to_string(T.h_aux->err.foreign_pos) +
+                                          " routes to a shard this handle does not hold"};
+    });
+}
+
+mpzch_status mpzch_delta_cut(mpzch_table* t, uint64_t generation, uint64_t* out_rows,
+                             uint64_t* out_identities, float* out_weights, uint64_t cap,
+                             uint64_t* out_n, uint64_t* out_next_generation) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        // DeltaSource::cut (publish.cpp:288-305): rows dirtied since the cursor, then a fresh
+        // cursor; index-only tables cannot be published (publish.cpp:282-286)
+        if (T.dim == 0) throw Error{MPZCH_ELOGIC, "index-only tables (dim = 0) cannot be published"};
+        if (generation == 0 || generation >= T.gen_clock)
+            throw Error{MPZCH_EINVAL, "stale or unknown publication cursor"};
+        DeviceGuard g(T.device);
+        cudaStream_t st = T.stream;
+        const uint64_t held = T.held_rows();
+        DevBuf flags, rows, blk, ids, w;
+        flags.reserve(((held + 15) & ~15ull) + 16);
+        MPZCH_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes, st));
+        rows.reserve(std::max<uint64_t>(held, 1) * 8);
+        blk.reserve(((held + kCompactChunk - 1) / kCompactChunk + 1) * 4);
+        k_dirty_flags<<<grid_for(held, 256), 256, 0, st>>>(T.row_gen, held, generation,
+                                                            flags.as<uint8_t>());
+        unsigned* d_n = &T.d_aux->pad;
+        EmitIndex em{rows.as<uint64_t>(), held, T.row_lo};
+        compact_flags(flags.as<uint8_t>(), held, blk.as<unsigned>(), d_n, false, em, st, T.launches);
+        unsigned nn = 0;
+        MPZCH_CUDA(cudaMemcpyAsync(&nn, d_n, 4, cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaStreamSynchronize(st));
+        const uint64_t k = std::min<uint64_t>(nn, cap);
+        if (k) {
+            ids.reserve(k * 8);
+            w.reserve(k * T.dim * 4);
+            run_gather_rows(T, rows.as<uint64_t>(), k, ids.as<uint64_t>(), w.as<float>(), st);
+            T.launches += 2;
+            MPZCH_CUDA(cudaGetLastError());
+            if (out_rows) MPZCH_CUDA(cudaMemcpyAsync(out_rows, rows.p, k * 8, cudaMemcpyDeviceToHost, st));
+            if (out_identities)
+                MPZCH_CUDA(cudaMemcpyAsync(out_identities, ids.p, k * 8, cudaMemcpyDeviceToHost, st));
+            if (out_weights)
+                MPZCH_CUDA(cudaMemcpyAsync(out_weights, w.p, k * T.dim * 4, cudaMemcpyDeviceToHost, st));
+            MPZCH_CUDA(cudaStreamSynchronize(st));
+        }
+        *out_n = nn;
+        if (nn <= cap && out_next_generation) *out_next_generation = T.gen_clock++;  // new cursor
+    });
+}
+
 mpzch_status mpzch_set_path(mpzch_table* t, int path) {
     CHECK_T(t);
     if (path != MPZCH_PATH_AUTO && path != MPZCH_PATH_ORDERED) {

@@ -161,6 +161,10 @@ void launch_write_slots(Table& t, const uint64_t* gslots, const uint64_t* ids, c
 bool run_hole_check(Table& t);
 void run_lookup(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots,
                 uint8_t* out_oc, BatchErr* err, cudaStream_t st);
+void run_lookup_gather(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots,
+                       uint8_t* out_oc, float* out_rows, BatchErr* err, cudaStream_t st);
+void run_gather_rows(const Table& t, const uint64_t* rows, uint64_t n, uint64_t* out_ids,
+                     float* out_w, cudaStream_t st);
 
 struct BatchArgs {
     const uint64_t* ids;

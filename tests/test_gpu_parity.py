@@ -495,3 +495,52 @@ def test_async_tickets_and_deferred_errors(oracle):
     assert_same_state(gpu_state(t, 4), oracle_state(o, 4))
     with pytest.raises(mz.InvalidArgument, match="unknown or expired batch ticket"):
         t.wait(10 ** 9)
+
+
+def test_lookup_gather_matches_lookup_then_gather(oracle):
+    """SURVEY 8f rank 2: fused lookup + gather == MpzchTable::lookup then gather of the rows."""
+    import torch
+    rows = 1 << 14
+    caps = mz.even_capacities(rows, 4)
+    for dim in (128, 3):
+        t = mz.MpzchTable(mz.TableConfig(caps, 32, 9, dim, 5))
+        o = oracle.OracleTable(caps, 32, 9, dim, 5)
+        ids = oracle.distinct_ids(12, 0, 12000)
+        t.process_batch(ids[:9000], 1, mz.EvictionPolicy.disabled())
+        o.process_batch(ids[:9000], 1, 0)
+        q = ids[::2].copy()
+        s, oc, r = t.lookup_gather_device(torch.from_numpy(q.view(np.int64)).cuda())
+        os_, oo = o.lookup(q)
+        assert (s.cpu().numpy().view(np.uint64) == os_).all() and (oc.cpu().numpy() == oo).all()
+        assert (r.cpu().numpy().view(np.uint32) == o.weights()[os_.astype(np.int64)].view(np.uint32)).all()
+    t0 = mz.MpzchTable(mz.TableConfig(caps, 32, 9))
+    with pytest.raises(mz.LogicError):
+        t0.lookup_gather_device(torch.zeros(4, dtype=torch.int64, device="cuda"))
+
+
+def test_delta_cut_matches_dirty_rows(oracle):
+    """SURVEY 8f rank 1: DeltaSource::cut on device -- rows dirtied since the cursor (inserts,
+    evictions, training writes), with identities and weights, then a fresh cursor."""
+    rows = 1 << 12
+    caps = mz.even_capacities(rows, 4)
+    t = mz.MpzchTable(mz.TableConfig(caps, 16, 3, 8, 4))
+    o = oracle.OracleTable(caps, 16, 3, 8, 4)
+    pol = mz.EvictionPolicy.ttl(mz.TtlPolicy(20))
+    ids = oracle.distinct_ids(13, 0, 6000)
+    c = t.make_cursor()
+    oc_ = o.make_cursor()
+    rng = np.random.default_rng(1)
+    for b in range(3):
+        batch = ids[rng.integers(0, ids.size, 1500)]
+        t.process_batch(batch, 100 + 30 * b, pol)
+        o.process_batch(batch, 100 + 30 * b, 1, 20)
+    r, idn, w, nxt = t.delta_cut(c)
+    want = o.dirty_rows_since(oc_)
+    assert (r == want).all() and r.size > 0
+    assert (idn == o.identities_all()[want.astype(np.int64)]).all()
+    assert (w.view(np.uint32) == o.weights()[want.astype(np.int64)].view(np.uint32)).all()
+    # nothing dirtied since the new cursor
+    r2, _, _, _ = t.delta_cut(nxt)
+    assert r2.size == 0
+    with pytest.raises(mz.InvalidArgument, match="stale or unknown publication cursor"):
+        t.delta_cut(0)
