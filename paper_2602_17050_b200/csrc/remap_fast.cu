@@ -269,6 +269,234 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// K1s: staged probe (Disabled).  Each thread owns kSU positions of a 2048-position tile; the
+// first sector of every position is pulled into shared memory with cp.async (LDGSTS, L1
+// bypass) so all kSU sector loads of a thread are in flight at once without holding
+// registers.  Up to kRounds sector rounds are resolved in shared memory; positions still
+// open after that (long runs) go to a queue that k_probe_long finishes warp-cooperatively.
+constexpr int kSU = 8;
+constexpr int kSTPB = 256;
+constexpr int kSTile = kSU * kSTPB;
+constexpr int kRounds = 3;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+struct __align__(16) StagedSmem {
+    ulonglong4 sec[kSTile];  // the position's current 32-byte identity sector
+    uint64_t id[kSTile];
+    uint64_t g[kSTile];      // global slot the scan resumes at
+    uint32_t off[kSTile];    // probe offset of g
+    uint8_t st[kSTile];      // 0 pending, 1 hit, 2 empty, 3 exhausted, 4 idle, 5 queued long
+};
+
+__global__ void __launch_bounds__(kSTPB, 2) k_probe_staged(TableDev t, const uint64_t* __restrict__ ids,
+                                                           uint64_t n, uint64_t meta_value,
+                                                           BatchCounters* ctr,
+                                                           uint64_t* __restrict__ out_slots,
+                                                           uint8_t* __restrict__ out_oc,
+                                                           uint32_t* __restrict__ newpos,
+                                                           uint64_t* __restrict__ newid,
+                                                           uint32_t* __restrict__ newa,
+                                                           uint32_t* __restrict__ newm,
+                                                           uint32_t* __restrict__ longq) {
+    if (batch_failed(&ctr->err)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    StagedSmem& S = *reinterpret_cast<StagedSmem*>(smem_raw);
+    const unsigned lane = lane_id();
+    unsigned long long my_found = 0, my_coll = 0, my_isec = 0;
+    for (uint64_t t0 = (uint64_t)blockIdx.x * kSTile; t0 < n; t0 += (uint64_t)gridDim.x * kSTile) {
+        // issue: ids -> homes -> first sectors, all kSU positions before any wait
+#pragma unroll
+        for (int u = 0; u < kSU; ++u) {
+            const int x = u * kSTPB + threadIdx.x;
+            const uint64_t i = t0 + x;
+            if (i < n) {
+                const uint64_t id = ids[i];
+                const ShardDev sd = t.shards[shard_of(id, t)];
+                const uint64_t g = sd.offset + home_of(id, sd, t.seed);
+                S.id[x] = id;
+                S.g[x] = g;
+                S.off[x] = 0;
+                S.st[x] = 0;
+                const uint64_t* src = t.ident + (g & ~3ull);
+                cp_async16(&S.sec[x], src);
+                cp_async16(reinterpret_cast<char*>(&S.sec[x]) + 16, src + 2);
+                ++my_isec;
+            } else {
+                S.st[x] = 4;
+            }
+        }
+        cp_async_commit();
+        for (int round = 0;; ++round) {
+            cp_async_wait_all();
+            __syncthreads();
+            bool any = false;
+#pragma unroll
+            for (int u = 0; u < kSU; ++u) {
+                const int x = u * kSTPB + threadIdx.x;
+                if (S.st[x] != 0) continue;
+                const uint64_t id = S.id[x];
+                uint64_t g = S.g[x];
+                uint32_t off = S.off[x];
+                const ulonglong4 w = S.sec[x];
+                const uint64_t a4 = g & ~3ull;
+                // shard bounds for the wrap: the home's shard
+                const ShardDev sd = t.shards[shard_of(id, t)];
+                const uint64_t base = sd.offset, end = base + sd.cap.d;
+                uint8_t st = 0;
+                do {
+                    const uint64_t v = pick4((uint32_t)(g - a4), w.x, w.y, w.z, w.w);
+                    if (v == id) { st = 1; break; }
+                    if (v == kEmpty) { st = 2; break; }
+                    ++off;
+                    if (++g == end) g = base;
+                } while (off < t.P && (g >> 2) == (a4 >> 2));
+                if (st == 0 && off >= t.P) st = 3;
+                S.g[x] = g;
+                S.off[x] = off;
+                if (st == 0) {
+                    if (round + 1 < kRounds) {  // next sector of this position
+                        const uint64_t* src = t.ident + (g & ~3ull);
+                        cp_async16(&S.sec[x], src);
+                        cp_async16(reinterpret_cast<char*>(&S.sec[x]) + 16, src + 2);
+                        ++my_isec;
+                        any = true;
+                    } else {
+                        st = 5;  // long run: finish warp-cooperatively
+                    }
+                }
+                S.st[x] = st;
+            }
+            cp_async_commit();
+            if (!__syncthreads_or(any)) break;
+        }
+        // decisions: final results (+ the metadata word), new list, long queue
+#pragma unroll
+        for (int u = 0; u < kSU; ++u) {
+            const int x = u * kSTPB + threadIdx.x;
+            const uint64_t i = t0 + x;
+            const uint8_t st = S.st[x];
+            if (st == 1 || st == 3) {
+                uint64_t slot = S.g[x];
+                if (st == 3) {  // collision: the home slot (recomputed; rare)
+                    const ShardDev sd = t.shards[shard_of(S.id[x], t)];
+                    slot = sd.offset + home_of(S.id[x], sd, t.seed);
+                }
+                out_slots[i] = slot;
+                out_oc[i] = st == 1 ? kFound : kCollision;
+                t.meta[slot] = meta_value;
+                if (st == 1) ++my_found; else ++my_coll;
+            }
+            const unsigned mnew = __ballot_sync(0xffffffffu, st == 2);
+            if (mnew) {
+                unsigned basek = 0;
+                if (lane == 0) basek = atomicAdd(&ctr->new_count, (unsigned)__popc(mnew));
+                basek = __shfl_sync(0xffffffffu, basek, 0);
+                if (st == 2) {
+                    const unsigned k = basek + __popc(mnew & ((1u << lane) - 1));
+                    newpos[k] = (uint32_t)i;
+                    newid[k] = S.id[x];
+                    newa[k] = S.off[x];
+                    newm[k] = kNone32;
+                }
+            }
+            const unsigned mlong = __ballot_sync(0xffffffffu, st == 5);
+            if (mlong) {
+                unsigned basek = 0;
+                if (lane == 0) basek = atomicAdd(&ctr->long_count, (unsigned)__popc(mlong));
+                basek = __shfl_sync(0xffffffffu, basek, 0);
+                if (st == 5) longq[basek + __popc(mlong & ((1u << lane) - 1))] = (uint32_t)i;
+            }
+        }
+        __syncthreads();  // shared state is reused by the next tile
+    }
+    for (int o = 16; o; o >>= 1) {
+        my_found += __shfl_xor_sync(0xffffffffu, my_found, o);
+        my_coll += __shfl_xor_sync(0xffffffffu, my_coll, o);
+        my_isec += __shfl_xor_sync(0xffffffffu, my_isec, o);
+    }
+    if (lane == 0) {
+        if (my_found) atomicAdd(&ctr->found, my_found);
+        if (my_coll) atomicAdd(&ctr->collision, my_coll);
+        if (my_isec) atomicAdd(&ctr->id_sectors, my_isec);
+    }
+}
+
+// K1b: warp-cooperative probe of the long runs (Disabled): one warp per queued position,
+// one coalesced 256-byte load of 32 consecutive window slots per step, __ballot_sync for
+// match / EMPTY and __ffs for the first of either (probe_core.cpp:89-101 order).
+__global__ void __launch_bounds__(256) k_probe_long(TableDev t, const uint64_t* __restrict__ ids,
+                                                    uint64_t meta_value, BatchCounters* ctr,
+                                                    const uint32_t* __restrict__ longq,
+                                                    uint64_t* __restrict__ out_slots,
+                                                    uint8_t* __restrict__ out_oc,
+                                                    uint32_t* __restrict__ newpos,
+                                                    uint64_t* __restrict__ newid,
+                                                    uint32_t* __restrict__ newa,
+                                                    uint32_t* __restrict__ newm) {
+    if (batch_failed(&ctr->err)) return;
+    const unsigned cnt = ctr->long_count;
+    const unsigned lane = lane_id();
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long my_found = 0, my_coll = 0, my_isec = 0;
+    for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < cnt; w += warps) {
+        const uint32_t i = longq[w];
+        const uint64_t id = ids[i];
+        const ShardDev sd = t.shards[shard_of(id, t)];
+        const uint64_t cap = sd.cap.d, base = sd.offset;
+        const uint64_t h = home_of(id, sd, t.seed);
+        int kind = 0;  // 1 hit, 2 empty, 3 exhausted
+        uint64_t gsel = 0;
+        uint32_t osel = 0;
+        for (uint32_t c = 0; c < t.P; c += 32) {
+            const uint32_t off = c + lane;
+            bool hit = false, emp = false;
+            uint64_t g = 0;
+            if (off < t.P) {
+                g = base + wrap_add(h, off, cap);
+                const uint64_t v = __ldg(t.ident + g);
+                hit = v == id;
+                emp = v == kEmpty;
+            }
+            my_isec += lane == 0;
+            const unsigned m = __ballot_sync(0xffffffffu, hit || emp);
+            if (m) {
+                const int src = __ffs(m) - 1;
+                kind = __shfl_sync(0xffffffffu, hit ? 1 : 2, src);
+                gsel = __shfl_sync(0xffffffffu, g, src);
+                osel = c + src;
+                break;
+            }
+        }
+        if (lane == 0) {
+            if (kind == 1 || kind == 0) {
+                const uint64_t slot = kind == 1 ? gsel : base + h;
+                out_slots[i] = slot;
+                out_oc[i] = kind == 1 ? kFound : kCollision;
+                t.meta[slot] = meta_value;
+                if (kind == 1) ++my_found; else ++my_coll;
+            } else {
+                const unsigned k = atomicAdd(&ctr->new_count, 1u);
+                newpos[k] = i;
+                newid[k] = id;
+                newa[k] = osel;
+                newm[k] = kNone32;
+            }
+        }
+    }
+    if (lane == 0) {
+        if (my_found) atomicAdd(&ctr->found, my_found);
+        if (my_coll) atomicAdd(&ctr->collision, my_coll);
+        if (my_isec) atomicAdd(&ctr->id_sectors, my_isec * 8);  // 256 B = 8 sectors per step
+    }
+}
+
 // K2: distinct-id table over the new positions (128-bit CAS on an epoch-tagged key).
 __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap, uint64_t epoch,
                                                const uint32_t* __restrict__ newpos,
@@ -569,9 +797,22 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     if (ttl)
         k_probe<kModeTtl, kU><<<gP, B, 0, st>>>(t.dev, a.ids, n, a.now, a.uniform_meta, t.d_ctr,
                                                 a.out_slots, a.out_oc, newpos, newid, newa, newm);
-    else
-        k_probe<kModeDisabled, kU><<<gP, B, 0, st>>>(t.dev, a.ids, n, a.now, a.uniform_meta, t.d_ctr,
-                                                     a.out_slots, a.out_oc, newpos, newid, newa, newm);
+    else {
+        static bool attr = false;
+        if (!attr) {
+            MPZCH_CUDA(cudaFuncSetAttribute(k_probe_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)sizeof(StagedSmem)));
+            attr = true;
+        }
+        const unsigned gS = grid_for((n + kSTile - 1) / kSTile, 1, 148u * 2u);
+        k_probe_staged<<<gS, kSTPB, sizeof(StagedSmem), st>>>(t.dev, a.ids, n, a.uniform_meta, t.d_ctr,
+                                                             a.out_slots, a.out_oc, newpos, newid,
+                                                             newa, newm, t.s_longq.as<uint32_t>());
+        k_probe_long<<<grid_for(n / 8 + 32, B, 148u * 4u), B, 0, st>>>(
+            t.dev, a.ids, a.uniform_meta, t.d_ctr, t.s_longq.as<uint32_t>(), a.out_slots, a.out_oc,
+            newpos, newid, newa, newm);
+        ++t.launches;
+    }
     ++t.launches;
     if (t.profiling) cudaEventRecord(t.ev[1], st);
     k_dedup<<<gW, B, 0, st>>>(t.d_ctr, t.tcap, epoch, newpos, newid, newa, newm, newent, tkey, trank,

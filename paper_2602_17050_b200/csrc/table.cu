@@ -175,6 +175,7 @@ void Table::ensure_fast_scratch(uint64_t n) {
     s_newa.reserve(n * 4);
     s_newm.reserve(n * 4);
     s_newent.reserve(n * 4);
+    s_longq.reserve(n * 4);
     const uint64_t want = pow2_at_least(2 * n);
     if (want > tcap) {
         s_tkey.reserve(want * 16);  // epoch-tagged keys: epoch 0 = empty
