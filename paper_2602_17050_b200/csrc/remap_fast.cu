@@ -148,7 +148,8 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
                                                uint32_t* __restrict__ newpos,
                                                uint64_t* __restrict__ newid,
                                                uint32_t* __restrict__ newa,
-                                               uint32_t* __restrict__ newm) {
+                                               uint32_t* __restrict__ newm,
+                                               uint32_t* __restrict__ longq) {
     if (batch_failed(&ctr->err)) return;
     constexpr uint8_t kPending = 0, kHit = 1, kEmptyHit = 2, kExhausted = 3, kIdle = 4;
     const unsigned lane = lane_id();
@@ -173,8 +174,12 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
                 st[u] = kPending;
             }
         }
-        // scan rounds: issue every pending position's next sector, then scan them
-        for (;;) {
+        // scan rounds: issue every pending position's next sector, then scan them.  Under
+        // Disabled, a position still open after kLongAfter sectors is handed to the
+        // warp-cooperative long-run probe instead of keeping its warp waiting.
+        constexpr uint8_t kLong = 5;
+        constexpr int kLongAfter = 4;
+        for (int round = 0;; ++round) {
             uint64_t w[U][4];
             bool any = false;
 #pragma unroll
@@ -196,6 +201,7 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
                 } while (off[u] < t.P && (g[u] >> 2) == (a4 >> 2));
                 if (st[u] == kPending) {
                     if (off[u] >= t.P) st[u] = kExhausted;
+                    else if (MODE == kModeDisabled && round + 1 >= kLongAfter) st[u] = kLong;
                     else any = true;
                 }
             }
@@ -207,7 +213,7 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
             const uint64_t i = t0 + (uint64_t)u * blockDim.x + threadIdx.x;
             bool is_new = false;
             uint32_t a_off = 0, m_off = kNone32;
-            if (st[u] != kIdle) {
+            if (st[u] != kIdle && st[u] != kLong) {
                 uint64_t fslot = kEmpty;
                 uint8_t foc = kFound;
                 if (MODE == kModeDisabled) {
@@ -240,6 +246,15 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
             }
             // warp-aggregated append of the new positions (a block barrier here would make
             // every warp wait for the slowest probe of the tile: measured slower)
+            if (MODE == kModeDisabled) {
+                const unsigned mlong = __ballot_sync(0xffffffffu, st[u] == kLong);
+                if (mlong) {
+                    unsigned bl = 0;
+                    if (lane == 0) bl = atomicAdd(&ctr->long_count, (unsigned)__popc(mlong));
+                    bl = __shfl_sync(0xffffffffu, bl, 0);
+                    if (st[u] == kLong) longq[bl + __popc(mlong & ((1u << lane) - 1))] = (uint32_t)i;
+                }
+            }
             const unsigned mask = __ballot_sync(0xffffffffu, is_new);
             if (mask) {
                 unsigned basek = 0;
@@ -266,165 +281,6 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
         if (my_coll) atomicAdd(&ctr->collision, my_coll);
         if (my_isec) atomicAdd(&ctr->id_sectors, my_isec);
         if (my_msec) atomicAdd(&ctr->meta_sectors, my_msec);
-    }
-}
-
-// ---------------------------------------------------------------------------------------
-// K1s: staged probe (Disabled).  Each thread owns kSU positions of a 2048-position tile; the
-// first sector of every position is pulled into shared memory with cp.async (LDGSTS, L1
-// bypass) so all kSU sector loads of a thread are in flight at once without holding
-// registers.  Up to kRounds sector rounds are resolved in shared memory; positions still
-// open after that (long runs) go to a queue that k_probe_long finishes warp-cooperatively.
-constexpr int kSU = 8;
-constexpr int kSTPB = 256;
-constexpr int kSTile = kSU * kSTPB;
-constexpr int kRounds = 3;
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-struct __align__(16) StagedSmem {
-    ulonglong4 sec[kSTile];  // the position's current 32-byte identity sector
-    uint64_t id[kSTile];
-    uint64_t g[kSTile];      // global slot the scan resumes at
-    uint32_t off[kSTile];    // probe offset of g
-    uint8_t st[kSTile];      // 0 pending, 1 hit, 2 empty, 3 exhausted, 4 idle, 5 queued long
-};
-
-__global__ void __launch_bounds__(kSTPB, 2) k_probe_staged(TableDev t, const uint64_t* __restrict__ ids,
-                                                           uint64_t n, uint64_t meta_value,
-                                                           BatchCounters* ctr,
-                                                           uint64_t* __restrict__ out_slots,
-                                                           uint8_t* __restrict__ out_oc,
-                                                           uint32_t* __restrict__ newpos,
-                                                           uint64_t* __restrict__ newid,
-                                                           uint32_t* __restrict__ newa,
-                                                           uint32_t* __restrict__ newm,
-                                                           uint32_t* __restrict__ longq) {
-    if (batch_failed(&ctr->err)) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    StagedSmem& S = *reinterpret_cast<StagedSmem*>(smem_raw);
-    const unsigned lane = lane_id();
-    unsigned long long my_found = 0, my_coll = 0, my_isec = 0;
-    for (uint64_t t0 = (uint64_t)blockIdx.x * kSTile; t0 < n; t0 += (uint64_t)gridDim.x * kSTile) {
-        // issue: ids -> homes -> first sectors, all kSU positions before any wait
-#pragma unroll
-        for (int u = 0; u < kSU; ++u) {
-            const int x = u * kSTPB + threadIdx.x;
-            const uint64_t i = t0 + x;
-            if (i < n) {
-                const uint64_t id = ids[i];
-                const ShardDev sd = t.shards[shard_of(id, t)];
-                const uint64_t g = sd.offset + home_of(id, sd, t.seed);
-                S.id[x] = id;
-                S.g[x] = g;
-                S.off[x] = 0;
-                S.st[x] = 0;
-                const uint64_t* src = t.ident + (g & ~3ull);
-                cp_async16(&S.sec[x], src);
-                cp_async16(reinterpret_cast<char*>(&S.sec[x]) + 16, src + 2);
-                ++my_isec;
-            } else {
-                S.st[x] = 4;
-            }
-        }
-        cp_async_commit();
-        for (int round = 0;; ++round) {
-            cp_async_wait_all();
-            __syncthreads();
-            bool any = false;
-#pragma unroll
-            for (int u = 0; u < kSU; ++u) {
-                const int x = u * kSTPB + threadIdx.x;
-                if (S.st[x] != 0) continue;
-                const uint64_t id = S.id[x];
-                uint64_t g = S.g[x];
-                uint32_t off = S.off[x];
-                const ulonglong4 w = S.sec[x];
-                const uint64_t a4 = g & ~3ull;
-                // shard bounds for the wrap: the home's shard
-                const ShardDev sd = t.shards[shard_of(id, t)];
-                const uint64_t base = sd.offset, end = base + sd.cap.d;
-                uint8_t st = 0;
-                do {
-                    const uint64_t v = pick4((uint32_t)(g - a4), w.x, w.y, w.z, w.w);
-                    if (v == id) { st = 1; break; }
-                    if (v == kEmpty) { st = 2; break; }
-                    ++off;
-                    if (++g == end) g = base;
-                } while (off < t.P && (g >> 2) == (a4 >> 2));
-                if (st == 0 && off >= t.P) st = 3;
-                S.g[x] = g;
-                S.off[x] = off;
-                if (st == 0) {
-                    if (round + 1 < kRounds) {  // next sector of this position
-                        const uint64_t* src = t.ident + (g & ~3ull);
-                        cp_async16(&S.sec[x], src);
-                        cp_async16(reinterpret_cast<char*>(&S.sec[x]) + 16, src + 2);
-                        ++my_isec;
-                        any = true;
-                    } else {
-                        st = 5;  // long run: finish warp-cooperatively
-                    }
-                }
-                S.st[x] = st;
-            }
-            cp_async_commit();
-            if (!__syncthreads_or(any)) break;
-        }
-        // decisions: final results (+ the metadata word), new list, long queue
-#pragma unroll
-        for (int u = 0; u < kSU; ++u) {
-            const int x = u * kSTPB + threadIdx.x;
-            const uint64_t i = t0 + x;
-            const uint8_t st = S.st[x];
-            if (st == 1 || st == 3) {
-                uint64_t slot = S.g[x];
-                if (st == 3) {  // collision: the home slot (recomputed; rare)
-                    const ShardDev sd = t.shards[shard_of(S.id[x], t)];
-                    slot = sd.offset + home_of(S.id[x], sd, t.seed);
-                }
-                out_slots[i] = slot;
-                out_oc[i] = st == 1 ? kFound : kCollision;
-                t.meta[slot] = meta_value;
-                if (st == 1) ++my_found; else ++my_coll;
-            }
-            const unsigned mnew = __ballot_sync(0xffffffffu, st == 2);
-            if (mnew) {
-                unsigned basek = 0;
-                if (lane == 0) basek = atomicAdd(&ctr->new_count, (unsigned)__popc(mnew));
-                basek = __shfl_sync(0xffffffffu, basek, 0);
-                if (st == 2) {
-                    const unsigned k = basek + __popc(mnew & ((1u << lane) - 1));
-                    newpos[k] = (uint32_t)i;
-                    newid[k] = S.id[x];
-                    newa[k] = S.off[x];
-                    newm[k] = kNone32;
-                }
-            }
-            const unsigned mlong = __ballot_sync(0xffffffffu, st == 5);
-            if (mlong) {
-                unsigned basek = 0;
-                if (lane == 0) basek = atomicAdd(&ctr->long_count, (unsigned)__popc(mlong));
-                basek = __shfl_sync(0xffffffffu, basek, 0);
-                if (st == 5) longq[basek + __popc(mlong & ((1u << lane) - 1))] = (uint32_t)i;
-            }
-        }
-        __syncthreads();  // shared state is reused by the next tile
-    }
-    for (int o = 16; o; o >>= 1) {
-        my_found += __shfl_xor_sync(0xffffffffu, my_found, o);
-        my_coll += __shfl_xor_sync(0xffffffffu, my_coll, o);
-        my_isec += __shfl_xor_sync(0xffffffffu, my_isec, o);
-    }
-    if (lane == 0) {
-        if (my_found) atomicAdd(&ctr->found, my_found);
-        if (my_coll) atomicAdd(&ctr->collision, my_coll);
-        if (my_isec) atomicAdd(&ctr->id_sectors, my_isec);
     }
 }
 
@@ -794,21 +650,15 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     t.launches += 2;
     if (a.overflow_all) return;  // validation only; the host reports the error
     if (t.profiling) cudaEventRecord(t.ev[0], st);
-    if (ttl)
+    if (ttl) {
         k_probe<kModeTtl, kU><<<gP, B, 0, st>>>(t.dev, a.ids, n, a.now, a.uniform_meta, t.d_ctr,
-                                                a.out_slots, a.out_oc, newpos, newid, newa, newm);
-    else {
-        static bool attr = false;
-        if (!attr) {
-            MPZCH_CUDA(cudaFuncSetAttribute(k_probe_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)sizeof(StagedSmem)));
-            attr = true;
-        }
-        const unsigned gS = grid_for((n + kSTile - 1) / kSTile, 1, 148u * 2u);
-        k_probe_staged<<<gS, kSTPB, sizeof(StagedSmem), st>>>(t.dev, a.ids, n, a.uniform_meta, t.d_ctr,
-                                                             a.out_slots, a.out_oc, newpos, newid,
-                                                             newa, newm, t.s_longq.as<uint32_t>());
-        k_probe_long<<<grid_for(n / 8 + 32, B, 148u * 4u), B, 0, st>>>(
+                                                a.out_slots, a.out_oc, newpos, newid, newa, newm,
+                                                t.s_longq.as<uint32_t>());
+    } else {
+        k_probe<kModeDisabled, kU><<<gP, B, 0, st>>>(t.dev, a.ids, n, a.now, a.uniform_meta, t.d_ctr,
+                                                     a.out_slots, a.out_oc, newpos, newid, newa, newm,
+                                                     t.s_longq.as<uint32_t>());
+        k_probe_long<<<grid_for(n / 16 + 32, B, 148u * 8u), B, 0, st>>>(
             t.dev, a.ids, a.uniform_meta, t.d_ctr, t.s_longq.as<uint32_t>(), a.out_slots, a.out_oc,
             newpos, newid, newa, newm);
         ++t.launches;

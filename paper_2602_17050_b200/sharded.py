@@ -104,9 +104,9 @@ class ThreadComm:
     """In-process collectives for G logical ranks driven by G threads (one GPU tests)."""
 
     class _Hub:
-        def __init__(self, world):
+        def __init__(self, world, timeout=600.0):
             self.world = world
-            self.barrier = threading.Barrier(world)
+            self.barrier = threading.Barrier(world, timeout=timeout)
             self.slots = [None] * world
 
     def __init__(self, hub: "_Hub", rank: int):
@@ -118,6 +118,10 @@ class ThreadComm:
     def group(cls, world: int):
         hub = cls._Hub(world)
         return [cls(hub, r) for r in range(world)]
+
+    def abort(self):
+        """Break the barrier so the other ranks fail instead of waiting forever."""
+        self.hub.barrier.abort()
 
     def _exchange(self, obj):
         self.hub.barrier.wait()

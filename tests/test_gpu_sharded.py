@@ -35,8 +35,9 @@ def run_sharded(cfg, world, batches, pol):
                 res.append((s.cpu().numpy().view(np.uint64), o.cpu().numpy(),
                             e.cpu().numpy().view(np.uint64)))
             out[r] = res
-        except Exception as ex:  # surface worker failures
+        except Exception as ex:  # surface worker failures, release the other ranks
             errs.append(repr(ex))
+            comms[r].abort()
             raise
 
     th = [threading.Thread(target=worker, args=(r,)) for r in range(world)]

@@ -71,6 +71,25 @@ def run_batches(t, batches, nows, pol, stream, timed_from=0, feats=None):
                 batch_gbs=(prof["batch_bytes"] / nb) / (prof["batch_ms"] / nb / 1e3) / 1e9 if prof["batch_ms"] else None)
 
 
+def run_batches_async(t, batches, nows, pol, stream, timed_from=0):
+    """Same as run_batches but pipelined: enqueue every batch, then wait every ticket."""
+    n = max(b.numel() for b in batches)
+    out_s = torch.empty(n, dtype=torch.int64, device="cuda")
+    out_o = torch.empty(n, dtype=torch.uint8, device="cuda")
+    out_e = torch.empty(n, dtype=torch.int64, device="cuda")
+    for b in range(timed_from):
+        t.process_batch_device(batches[b], nows[b], pol, None, out_s, out_o, out_e, stream)
+
+    def body():
+        tks = [t.process_batch_device_async(batches[b], nows[b], pol, None, out_s, out_o, out_e, stream)
+               for b in range(timed_from, len(batches))]
+        for tk in tks:
+            t.wait(tk)
+    ms = ev_time(body, stream)
+    pos = sum(b.numel() for b in batches[timed_from:])
+    return dict(ids_per_s=pos / (ms / 1e3), ms_per_batch=ms / max(len(batches) - timed_from, 1))
+
+
 def ref_time(caps, P, batches_np, nows, mode, ttl, dim=0, init_seed=0, warm=0):
     """The reference library on the same host stream (bounded)."""
     import pyoracle
@@ -107,9 +126,12 @@ def c1(shards):
     cold = run_batches(t, batches[:16], nows[:16], pol, st)
     t2 = mz.MpzchTable(mz.TableConfig(caps, 128, 7))
     steady = run_batches(t2, batches, nows, pol, st, timed_from=16)
+    t3 = mz.MpzchTable(mz.TableConfig(caps, 128, 7))
+    steady_async = run_batches_async(t3, batches, nows, pol, st, timed_from=16)
     bn = [b.cpu().numpy().view(np.uint64) for b in batches]
     ref = ref_time(caps, 128, bn, nows, 0, 0, warm=16)
-    return dict(config=f"C1 S={shards}", cold_fill=cold, steady=steady, reference=ref)
+    return dict(config=f"C1 S={shards}", cold_fill=cold, steady=steady, steady_pipelined=steady_async,
+                reference=ref)
 
 
 def zipf_ranks(n, s, universe, seed):
