@@ -55,6 +55,22 @@ __device__ __forceinline__ uint64_t key_id(u128 k) { return (uint64_t)k; }
 __device__ __forceinline__ uint64_t key_epoch(u128 k) { return (uint64_t)(k >> 64); }
 __device__ __forceinline__ uint32_t rank_of(uint64_t tr) { return ~(uint32_t)tr; }
 
+// One id-table entry in one 64-byte record, so every kernel's accesses to an entry
+// (insert, rank, claim bookkeeping, result) land in the same DRAM burst.
+struct __align__(64) IdEntry {
+    u128 key;                 // epoch << 64 | id
+    unsigned long long rank;  // epoch << 32 | ~first position   (atomicMax)
+    uint32_t a;               // first available offset (taker start)
+    uint32_t m;               // owner: offset of the expired own slot, else kNone32
+    uint32_t held;            // last taker claim offset          (atomicMax)
+    uint8_t state;            // kStateCollided when the window is exhausted
+    uint8_t oc;               // committed outcome
+    uint8_t pad0[2];
+    uint64_t slot;            // committed global slot
+    uint64_t pad1[2];
+};
+static_assert(sizeof(IdEntry) == 64, "IdEntry must be one 64-byte record");
+
 __device__ __forceinline__ bool is_claim(uint64_t v) { return (v >> 63) != 0 && v != kEmpty; }
 __device__ __forceinline__ uint32_t claim_rank(uint64_t v) { return (uint32_t)(v >> 31); }
 __device__ __forceinline__ uint32_t claim_entry(uint64_t v) { return (uint32_t)(v & kEntryMask); }
@@ -148,8 +164,7 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
                                                uint32_t* __restrict__ newpos,
                                                uint64_t* __restrict__ newid,
                                                uint32_t* __restrict__ newa,
-                                               uint32_t* __restrict__ newm,
-                                               uint32_t* __restrict__ longq) {
+                                               uint32_t* __restrict__ newm) {
     if (batch_failed(&ctr->err)) return;
     constexpr uint8_t kPending = 0, kHit = 1, kEmptyHit = 2, kExhausted = 3, kIdle = 4;
     const unsigned lane = lane_id();
@@ -174,12 +189,10 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
                 st[u] = kPending;
             }
         }
-        // scan rounds: issue every pending position's next sector, then scan them.  Under
-        // Disabled, a position still open after kLongAfter sectors is handed to the
-        // warp-cooperative long-run probe instead of keeping its warp waiting.
-        constexpr uint8_t kLong = 5;
-        constexpr int kLongAfter = 4;
-        for (int round = 0;; ++round) {
+        // scan rounds: issue every pending position's next sector, then scan them.  (Handing
+        // long runs to a warp-cooperative kernel, or staging sectors in shared memory with
+        // cp.async behind block barriers, both measured slower on C5 and C3.)
+        for (;;) {
             uint64_t w[U][4];
             bool any = false;
 #pragma unroll
@@ -201,7 +214,6 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
                 } while (off[u] < t.P && (g[u] >> 2) == (a4 >> 2));
                 if (st[u] == kPending) {
                     if (off[u] >= t.P) st[u] = kExhausted;
-                    else if (MODE == kModeDisabled && round + 1 >= kLongAfter) st[u] = kLong;
                     else any = true;
                 }
             }
@@ -213,7 +225,7 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
             const uint64_t i = t0 + (uint64_t)u * blockDim.x + threadIdx.x;
             bool is_new = false;
             uint32_t a_off = 0, m_off = kNone32;
-            if (st[u] != kIdle && st[u] != kLong) {
+            if (st[u] != kIdle) {
                 uint64_t fslot = kEmpty;
                 uint8_t foc = kFound;
                 if (MODE == kModeDisabled) {
@@ -246,15 +258,6 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
             }
             // warp-aggregated append of the new positions (a block barrier here would make
             // every warp wait for the slowest probe of the tile: measured slower)
-            if (MODE == kModeDisabled) {
-                const unsigned mlong = __ballot_sync(0xffffffffu, st[u] == kLong);
-                if (mlong) {
-                    unsigned bl = 0;
-                    if (lane == 0) bl = atomicAdd(&ctr->long_count, (unsigned)__popc(mlong));
-                    bl = __shfl_sync(0xffffffffu, bl, 0);
-                    if (st[u] == kLong) longq[bl + __popc(mlong & ((1u << lane) - 1))] = (uint32_t)i;
-                }
-            }
             const unsigned mask = __ballot_sync(0xffffffffu, is_new);
             if (mask) {
                 unsigned basek = 0;
@@ -284,84 +287,13 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
     }
 }
 
-// K1b: warp-cooperative probe of the long runs (Disabled): one warp per queued position,
-// one coalesced 256-byte load of 32 consecutive window slots per step, __ballot_sync for
-// match / EMPTY and __ffs for the first of either (probe_core.cpp:89-101 order).
-__global__ void __launch_bounds__(256) k_probe_long(TableDev t, const uint64_t* __restrict__ ids,
-                                                    uint64_t meta_value, BatchCounters* ctr,
-                                                    const uint32_t* __restrict__ longq,
-                                                    uint64_t* __restrict__ out_slots,
-                                                    uint8_t* __restrict__ out_oc,
-                                                    uint32_t* __restrict__ newpos,
-                                                    uint64_t* __restrict__ newid,
-                                                    uint32_t* __restrict__ newa,
-                                                    uint32_t* __restrict__ newm) {
-    if (batch_failed(&ctr->err)) return;
-    const unsigned cnt = ctr->long_count;
-    const unsigned lane = lane_id();
-    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    unsigned long long my_found = 0, my_coll = 0, my_isec = 0;
-    for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < cnt; w += warps) {
-        const uint32_t i = longq[w];
-        const uint64_t id = ids[i];
-        const ShardDev sd = t.shards[shard_of(id, t)];
-        const uint64_t cap = sd.cap.d, base = sd.offset;
-        const uint64_t h = home_of(id, sd, t.seed);
-        int kind = 0;  // 1 hit, 2 empty, 3 exhausted
-        uint64_t gsel = 0;
-        uint32_t osel = 0;
-        for (uint32_t c = 0; c < t.P; c += 32) {
-            const uint32_t off = c + lane;
-            bool hit = false, emp = false;
-            uint64_t g = 0;
-            if (off < t.P) {
-                g = base + wrap_add(h, off, cap);
-                const uint64_t v = __ldg(t.ident + g);
-                hit = v == id;
-                emp = v == kEmpty;
-            }
-            my_isec += lane == 0;
-            const unsigned m = __ballot_sync(0xffffffffu, hit || emp);
-            if (m) {
-                const int src = __ffs(m) - 1;
-                kind = __shfl_sync(0xffffffffu, hit ? 1 : 2, src);
-                gsel = __shfl_sync(0xffffffffu, g, src);
-                osel = c + src;
-                break;
-            }
-        }
-        if (lane == 0) {
-            if (kind == 1 || kind == 0) {
-                const uint64_t slot = kind == 1 ? gsel : base + h;
-                out_slots[i] = slot;
-                out_oc[i] = kind == 1 ? kFound : kCollision;
-                t.meta[slot] = meta_value;
-                if (kind == 1) ++my_found; else ++my_coll;
-            } else {
-                const unsigned k = atomicAdd(&ctr->new_count, 1u);
-                newpos[k] = i;
-                newid[k] = id;
-                newa[k] = osel;
-                newm[k] = kNone32;
-            }
-        }
-    }
-    if (lane == 0) {
-        if (my_found) atomicAdd(&ctr->found, my_found);
-        if (my_coll) atomicAdd(&ctr->collision, my_coll);
-        if (my_isec) atomicAdd(&ctr->id_sectors, my_isec * 8);  // 256 B = 8 sectors per step
-    }
-}
-
 // K2: distinct-id table over the new positions (128-bit CAS on an epoch-tagged key).
 __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap, uint64_t epoch,
                                                const uint32_t* __restrict__ newpos,
                                                const uint64_t* __restrict__ newid,
                                                const uint32_t* __restrict__ newa,
                                                const uint32_t* __restrict__ newm,
-                                               uint32_t* __restrict__ newent, u128* tkey,
-                                               unsigned long long* trank, uint32_t* ta,
-                                               uint32_t* tm, uint32_t* theld, uint8_t* tstate) {
+                                               uint32_t* __restrict__ newent, IdEntry* te) {
     if (batch_failed(&ctr->err)) return;
     const unsigned cnt = ctr->new_count;
     const uint64_t mask = table_mask(cnt, tcap);
@@ -373,15 +305,15 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
         for (;;) {
             // atomic 128-bit read (a CAS that can only write back the value it found):
             // a plain 16-byte load is not guaranteed single-copy atomic
-            u128 cur = atomicCAS(tkey + h, (u128)0, (u128)0);
+            u128 cur = atomicCAS(&te[h].key, (u128)0, (u128)0);
             if (key_epoch(cur) != epoch) {  // empty for this batch: try to take it
-                const u128 old = atomicCAS(tkey + h, cur, mine);
+                const u128 old = atomicCAS(&te[h].key, cur, mine);
                 if (old == cur) {  // inserted: publish the entry's probe facts
                     e = (uint32_t)h;
-                    ta[e] = newa[k];
-                    tm[e] = newm[k];
-                    theld[e] = 0;
-                    tstate[e] = 0;
+                    te[e].a = newa[k];
+                    te[e].m = newm[k];
+                    te[e].held = 0;
+                    te[e].state = 0;
                     break;
                 }
                 cur = old;
@@ -393,15 +325,15 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
             }
             h = (h + 1) & mask;
         }
-        atomicMax(trank + e, (unsigned long long)((epoch << 32) | (uint32_t)~newpos[k]));
+        atomicMax(&te[e].rank, (unsigned long long)((epoch << 32) | (uint32_t)~newpos[k]));
         newent[k] = e;
     }
 }
 
 // The primary item of an entry (the new-list item at the id's first position) does the
 // entry's work in K3/K4; every other item of the same id only reads the result in K5.
-__device__ __forceinline__ bool is_primary(const unsigned long long* trank, uint32_t e, uint32_t pos) {
-    return rank_of(trank[e]) == pos;
+__device__ __forceinline__ bool is_primary(const IdEntry* te, uint32_t e, uint32_t pos) {
+    return rank_of(te[e].rank) == pos;
 }
 
 // K3: rank-priority claims with takeover.
@@ -409,21 +341,17 @@ template <int MODE>
 __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCounters* ctr,
                                                const uint32_t* __restrict__ newpos,
                                                const uint32_t* __restrict__ newent,
-                                               const u128* __restrict__ tkey,
-                                               const unsigned long long* __restrict__ trank,
-                                               const uint32_t* __restrict__ ta,
-                                               const uint32_t* __restrict__ tm,
-                                               uint32_t* theld, uint8_t* tstate) {
+                                               IdEntry* te) {
     if (batch_failed(&ctr->err)) return;
     const unsigned cnt = ctr->new_count;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
         uint32_t e = newent[k];
-        if (!is_primary(trank, e, newpos[k])) continue;
+        if (!is_primary(te, e, newpos[k])) continue;
         bool fresh = true;
         uint32_t resume = 0;
         for (;;) {
-            const uint64_t id = key_id(tkey[e]);
-            const uint32_t rank = rank_of(trank[e]);
+            const uint64_t id = key_id(te[e].key);
+            const uint32_t rank = rank_of(te[e].rank);
             const uint32_t s = shard_of(id, t);
             const ShardDev sd = t.shards[s];
             const uint64_t cap = sd.cap.d, base = sd.offset;
@@ -433,9 +361,9 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
             uint64_t gnext = 0;
             bool held = false;
             uint32_t off;
-            if (MODE == kModeTtl && fresh && tm[e] != kNone32) {
+            if (MODE == kModeTtl && fresh && te[e].m != kNone32) {
                 // owner: try to keep (refresh) the expired slot holding our own id
-                const uint32_t m = tm[e];
+                const uint32_t m = te[e].m;
                 const uint64_t gm = base + wrap_add(h, m, cap);
                 uint64_t v = ld_cg(t.ident + gm);
                 for (;;) {
@@ -452,9 +380,9 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                     }
                     v = old;
                 }
-                off = ta[e];
+                off = te[e].a;
             } else {
-                off = fresh ? ta[e] : resume;
+                off = fresh ? te[e].a : resume;
             }
             if (!held) {
                 // sector-wide scan: one L2 read per 4 slots; a slot is re-read only through
@@ -485,7 +413,7 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                         if (old == v) {
                             // taker claims of one entry move strictly forward, so the max is the
                             // slot it holds last (a late max from a displaced claim is harmless)
-                            atomicMax(theld + e, off);
+                            atomicMax(&te[e].held, off);
                             held = true;
                             if (is_claim(v)) { next = claim_entry(v); gnext = g; }
                             break;
@@ -494,19 +422,19 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                     }
                     if (held) break;
                 }
-                if (!held) tstate[e] = kStateCollided;
+                if (!held) te[e].state = kStateCollided;
             }
             if (next == kNone32) break;
             // take over the displaced entry: it resumes right after the slot it lost,
             // or -- if it was an owner losing its own id's slot -- as a taker from its
             // first available offset.
             {
-                const uint64_t id2 = key_id(tkey[next]);
+                const uint64_t id2 = key_id(te[next].key);
                 const uint64_t h2 = home_of(id2, sd, t.seed);  // same shard as the slot
                 const uint64_t loc = gnext - base;
                 const uint32_t off2 = (uint32_t)(loc >= h2 ? loc - h2 : loc + cap - h2);
-                if (MODE == kModeTtl && tm[next] != kNone32 && off2 == tm[next])
-                    resume = ta[next];
+                if (MODE == kModeTtl && te[next].m != kNone32 && off2 == te[next].m)
+                    resume = te[next].a;
                 else
                     resume = off2 + 1;
                 e = next;
@@ -524,12 +452,7 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
                                                 const uint32_t* __restrict__ newpos,
                                                 const uint64_t* __restrict__ newid,
                                                 const uint32_t* __restrict__ newent,
-                                                const unsigned long long* __restrict__ trank,
-                                                const uint32_t* __restrict__ tm,
-                                                const uint32_t* __restrict__ theld,
-                                                const uint8_t* __restrict__ tstate,
-                                                uint64_t* __restrict__ tslot,
-                                                uint8_t* __restrict__ toc, uint64_t gen_clock,
+                                                IdEntry* te, uint64_t gen_clock,
                                                 uint64_t meta_value,
                                                 uint64_t* __restrict__ reset_rows,
                                                 uint8_t* __restrict__ evflag,
@@ -539,7 +462,7 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
         const uint32_t e = newent[k];
         const uint32_t rank = newpos[k];
-        if (!is_primary(trank, e, rank)) continue;
+        if (!is_primary(te, e, rank)) continue;
         const uint64_t id = newid[k];
         const uint32_t s = shard_of(id, t);
         const ShardDev sd = t.shards[s];
@@ -550,12 +473,12 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
         uint64_t g = base + h;
         uint64_t v = 0;
         bool ok = true;
-        if (MODE == kModeTtl && tm[e] != kNone32 &&
-            ((v = t.ident[base + wrap_add(h, tm[e], cap)]) & ~kFlagEmpty) == mine) {
-            g = base + wrap_add(h, tm[e], cap);  // the owner kept (refreshed) its own slot
+        if (MODE == kModeTtl && te[e].m != kNone32 &&
+            ((v = t.ident[base + wrap_add(h, te[e].m, cap)]) & ~kFlagEmpty) == mine) {
+            g = base + wrap_add(h, te[e].m, cap);  // the owner kept (refreshed) its own slot
             oc = kFound;
-        } else if (tstate[e] != kStateCollided) {
-            g = base + wrap_add(h, theld[e], cap);
+        } else if (te[e].state != kStateCollided) {
+            g = base + wrap_add(h, te[e].held, cap);
             v = t.ident[g];
             ok = (v & ~kFlagEmpty) == mine;
             oc = (v & kFlagEmpty) ? kInserted : kEvicted;
@@ -574,8 +497,8 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
             evslot[rank] = g;
             atomicAdd(&ctr->evicted_count, 1u);
         }
-        tslot[e] = g;
-        toc[e] = oc;
+        te[e].slot = g;
+        te[e].oc = oc;
     }
 }
 
@@ -585,9 +508,7 @@ __global__ void __launch_bounds__(256) k_finalize(BatchCounters* ctr,
                                                   const uint32_t* __restrict__ feats,
                                                   const uint32_t* __restrict__ newpos,
                                                   const uint32_t* __restrict__ newent,
-                                                  const unsigned long long* __restrict__ trank,
-                                                  const uint64_t* __restrict__ tslot,
-                                                  const uint8_t* __restrict__ toc,
+                                                  const IdEntry* te,
                                                   uint64_t* __restrict__ out_slots,
                                                   uint8_t* __restrict__ out_oc) {
     if (batch_failed(&ctr->err)) return;
@@ -596,9 +517,9 @@ __global__ void __launch_bounds__(256) k_finalize(BatchCounters* ctr,
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
         const uint32_t pos = newpos[k];
         const uint32_t e = newent[k];
-        uint8_t oc = toc[e];
-        if (feats && feats[pos] != feats[rank_of(trank[e])]) oc = oc == kCollision ? kCollision : kFound;
-        out_slots[pos] = tslot[e];
+        uint8_t oc = te[e].oc;
+        if (feats && feats[pos] != feats[rank_of(te[e].rank)]) oc = oc == kCollision ? kCollision : kFound;
+        out_slots[pos] = te[e].slot;
         out_oc[pos] = oc;
         ++c[oc];
     }
@@ -613,7 +534,7 @@ __global__ void __launch_bounds__(256) k_finalize(BatchCounters* ctr,
     // distinct new ids of the batch (stats): count primary items
     unsigned np = 0;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x)
-        np += is_primary(trank, newent[k], newpos[k]);
+        np += is_primary(te, newent[k], newpos[k]);
     for (int o = 16; o; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
     if (lane_id() == 0 && np) atomicAdd(&ctr->entry_count, np);
 }
@@ -643,48 +564,32 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     uint32_t* newa = t.s_newa.as<uint32_t>();
     uint32_t* newm = t.s_newm.as<uint32_t>();
     uint32_t* newent = t.s_newent.as<uint32_t>();
-    u128* tkey = t.s_tkey.as<u128>();
-    unsigned long long* trank = t.s_tmin.as<unsigned long long>();
     k_init_counters<<<1, 32, 0, st>>>(t.d_ctr);
     k_validate<<<grid_for(n / 2 + 1, B, 148u * 8u), B, 0, st>>>(t.dev, a.ids, n, t.d_ctr);
     t.launches += 2;
     if (a.overflow_all) return;  // validation only; the host reports the error
     if (t.profiling) cudaEventRecord(t.ev[0], st);
-    if (ttl) {
+    if (ttl)
         k_probe<kModeTtl, kU><<<gP, B, 0, st>>>(t.dev, a.ids, n, a.now, a.uniform_meta, t.d_ctr,
-                                                a.out_slots, a.out_oc, newpos, newid, newa, newm,
-                                                t.s_longq.as<uint32_t>());
-    } else {
+                                                a.out_slots, a.out_oc, newpos, newid, newa, newm);
+    else
         k_probe<kModeDisabled, kU><<<gP, B, 0, st>>>(t.dev, a.ids, n, a.now, a.uniform_meta, t.d_ctr,
-                                                     a.out_slots, a.out_oc, newpos, newid, newa, newm,
-                                                     t.s_longq.as<uint32_t>());
-        k_probe_long<<<grid_for(n / 16 + 32, B, 148u * 8u), B, 0, st>>>(
-            t.dev, a.ids, a.uniform_meta, t.d_ctr, t.s_longq.as<uint32_t>(), a.out_slots, a.out_oc,
-            newpos, newid, newa, newm);
-        ++t.launches;
-    }
+                                                     a.out_slots, a.out_oc, newpos, newid, newa, newm);
     ++t.launches;
     if (t.profiling) cudaEventRecord(t.ev[1], st);
-    k_dedup<<<gW, B, 0, st>>>(t.d_ctr, t.tcap, epoch, newpos, newid, newa, newm, newent, tkey, trank,
-                              t.s_ta.as<uint32_t>(), t.s_tm.as<uint32_t>(), t.s_theld.as<uint32_t>(),
-                              t.s_tstate.as<uint8_t>());
+    IdEntry* te = t.s_tent.as<IdEntry>();
+    k_dedup<<<gW, B, 0, st>>>(t.d_ctr, t.tcap, epoch, newpos, newid, newa, newm, newent, te);
 #define MPZCH_CLAIM_COMMIT(MODE)                                                                   \
-    k_claim<MODE><<<gW, B, 0, st>>>(t.dev, a.now, t.d_ctr, newpos, newent, tkey, trank,            \
-                                    t.s_ta.as<uint32_t>(), t.s_tm.as<uint32_t>(),                  \
-                                    t.s_theld.as<uint32_t>(), t.s_tstate.as<uint8_t>());           \
-    k_commit<MODE><<<gW, B, 0, st>>>(t.dev, t.d_ctr, newpos, newid, newent, trank,               \
-                                     t.s_tm.as<uint32_t>(), t.s_theld.as<uint32_t>(),              \
-                                     t.s_tstate.as<uint8_t>(), t.s_tslot.as<uint64_t>(),           \
-                                     t.s_toc.as<uint8_t>(), t.gen_clock, a.uniform_meta,           \
-                                     t.s_reset.as<uint64_t>(), t.s_evflag.as<uint8_t>(),           \
-                                     t.s_evslot.as<uint64_t>())
+    k_claim<MODE><<<gW, B, 0, st>>>(t.dev, a.now, t.d_ctr, newpos, newent, te);                   \
+    k_commit<MODE><<<gW, B, 0, st>>>(t.dev, t.d_ctr, newpos, newid, newent, te, t.gen_clock,      \
+                                     a.uniform_meta, t.s_reset.as<uint64_t>(),                     \
+                                     t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>())
     if (ttl) { MPZCH_CLAIM_COMMIT(kModeTtl); }
     else { MPZCH_CLAIM_COMMIT(kModeDisabled); }
 #undef MPZCH_CLAIM_COMMIT
     t.launches += 3;
     if (t.profiling) cudaEventRecord(t.ev[2], st);
-    k_finalize<<<gW, B, 0, st>>>(t.d_ctr, a.feats, newpos, newent, trank, t.s_tslot.as<uint64_t>(),
-                                 t.s_toc.as<uint8_t>(), a.out_slots, a.out_oc);
+    k_finalize<<<gW, B, 0, st>>>(t.d_ctr, a.feats, newpos, newent, te, a.out_slots, a.out_oc);
     ++t.launches;
     if (t.dim > 0) launch_reset_rows(t, t.s_reset.as<uint64_t>(), &t.d_ctr->reset_count, st);
     if (a.out_mark) {  // first positions of Evicted uniques (row-sharded evicted list)

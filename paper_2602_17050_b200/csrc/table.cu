@@ -175,19 +175,10 @@ void Table::ensure_fast_scratch(uint64_t n) {
     s_newa.reserve(n * 4);
     s_newm.reserve(n * 4);
     s_newent.reserve(n * 4);
-    s_longq.reserve(n * 4);
     const uint64_t want = pow2_at_least(2 * n);
     if (want > tcap) {
-        s_tkey.reserve(want * 16);  // epoch-tagged keys: epoch 0 = empty
-        s_tmin.reserve(want * 8);   // epoch-tagged rank words
-        s_ta.reserve(want * 4);
-        s_tm.reserve(want * 4);
-        s_theld.reserve(want * 4);
-        s_tstate.reserve(want);
-        s_tslot.reserve(want * 8);
-        s_toc.reserve(want);
-        MPZCH_CUDA(cudaMemsetAsync(s_tkey.p, 0, want * 16, stream));
-        MPZCH_CUDA(cudaMemsetAsync(s_tmin.p, 0, want * 8, stream));
+        s_tent.reserve(want * 64);  // epoch-tagged 64-byte entries: epoch 0 = empty
+        MPZCH_CUDA(cudaMemsetAsync(s_tent.p, 0, want * 64, stream));
         tcap = want;
         epoch = 0;
     }

@@ -53,8 +53,6 @@ struct BatchCounters {
     unsigned int overflow_list;  // claim-log overflow (defensive)
     unsigned int pad;
     unsigned long long id_sectors, meta_sectors;  // sectors the probe kernel read
-    unsigned int long_count;  // positions handed to the warp-cooperative long-run probe
-    unsigned int pad2;
 };
 
 struct Policy {
@@ -139,8 +137,7 @@ public:
 
     // scratch
     DevBuf s_newpos, s_newid, s_newa, s_newm, s_newent;  // new-list (fast path)
-    DevBuf s_longq;                                      // long-run probe queue
-    DevBuf s_tkey, s_tmin, s_ta, s_tm, s_theld, s_tstate, s_tslot, s_toc;  // id table
+    DevBuf s_tent;                                   // id table: 64-byte entries
     uint64_t tcap = 0;                               // allocated id-table capacity (pow2)
     uint64_t epoch = 0;                              // id-table batch epoch (0 = never used)
     uint64_t fast_ready = 0;                         // largest n the fast scratch is ready for
