@@ -275,11 +275,21 @@ def main():
 
     import torch
     import paper_2602_17050_b200 as mz
+    # MPZCH_DIST_BACKEND=gloo (+ MPZCH_SHARE_GPU=1) runs the multi-rank path with every rank
+    # on cuda:0 and collectives staged through the host: a functional check of the N>1 code
+    # on a single-GPU box, never a scaling number
+    backend = os.environ.get("MPZCH_DIST_BACKEND", "nccl")
+    share = os.environ.get("MPZCH_SHARE_GPU", "0") == "1"
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = local if world > 1 else 0
+        dev_i = 0 if share else local
+        torch.cuda.set_device(dev_i)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_i))
+        else:
+            dist.init_process_group(backend)
+    dev = (0 if share else local) if world > 1 else 0
+    red_dev = "cpu" if (world > 1 and backend == "gloo") else dev  # device of reduction tensors
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -376,7 +386,7 @@ def main():
         while k < 2000:
             more = len([t for t, _ in clk.rows if t >= w0]) < 4
             if world > 1:
-                more = bool(_allreduce_max_int(torch, int(more), dev))
+                more = bool(_allreduce_max_int(torch, int(more), red_dev))
             if not more:
                 break
             remap(batches[args.warmup + k % args.steps], 2 + nb)
@@ -384,7 +394,7 @@ def main():
         torch.cuda.synchronize(dev)
         clk.windows.append((w0, time.time()))
     if world > 1:
-        tt = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+        tt = torch.tensor([ms_total], device=red_dev, dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         ms_total = float(tt.item())
     ms_step = ms_total / args.steps
@@ -465,7 +475,7 @@ def main():
         e2e_api = "ShardedMpzchTable.process_batch (pinned host slices, H2D/D2H timed)"
         e2e_sync_value = None
     if world > 1:
-        tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        tt = torch.tensor([e2e_s], device=red_dev, dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(tt.item())
     e2e_value = BATCH * e2e_steps / e2e_s

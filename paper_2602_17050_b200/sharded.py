@@ -55,7 +55,9 @@ def held_shards(rank: int, num_shards: int, parts: int) -> Tuple[int, int]:
 # ------------------------------------------------------------------------------ comms
 
 class TorchComm:
-    """Collectives over torch.distributed (NCCL for CUDA tensors, gloo for CPU tensors)."""
+    """Collectives over torch.distributed: NCCL moves CUDA tensors directly (NVLink); with a
+    gloo group, CUDA tensors are staged through host memory (used to exercise the
+    multi-rank path on a single-GPU box)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -63,9 +65,13 @@ class TorchComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self.stage = dist.get_backend(group) == "gloo"
 
     def _dev(self, like):
-        return like.device
+        return "cpu" if self.stage else like.device
+
+    def _to(self, t):
+        return t.cpu() if self.stage and t.is_cuda else t
 
     def all_gather_int(self, x: int, like) -> List[int]:
         import torch
@@ -84,20 +90,22 @@ class TorchComm:
 
     def all_to_all(self, send, send_counts: Sequence[int], recv_counts: Sequence[int]):
         import torch
+        src = self._to(send.contiguous())
         out = torch.empty((sum(recv_counts),) + tuple(send.shape[1:]), dtype=send.dtype,
-                          device=send.device)
-        self.dist.all_to_all_single(out, send.contiguous(), list(recv_counts), list(send_counts),
+                          device=src.device)
+        self.dist.all_to_all_single(out, src, list(recv_counts), list(send_counts),
                                     group=self.group)
-        return out
+        return out.to(send.device)
 
     def all_gather_v(self, t, counts: Sequence[int]):
         import torch
         m = max(counts) if counts else 0
-        pad = torch.zeros(max(m, 1), dtype=t.dtype, device=t.device)
-        pad[:t.numel()] = t
+        src = self._to(t)
+        pad = torch.zeros(max(m, 1), dtype=t.dtype, device=src.device)
+        pad[:src.numel()] = src
         outs = [torch.empty_like(pad) for _ in range(self.world)]
         self.dist.all_gather(outs, pad, group=self.group)
-        return torch.cat([o[:c] for o, c in zip(outs, counts)])
+        return torch.cat([o[:c] for o, c in zip(outs, counts)]).to(t.device)
 
 
 class ThreadComm:
