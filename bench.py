@@ -504,11 +504,12 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (DistinctIdStream ids, SplitMix64 sampler)",
-            "config": {"workload": "C5: 1B-slot (2^30-row) table, S=8 logical shards, "
+            "config": {"workload": ("C5: 1B-slot (2^30-row) table" if rows == ROWS else
+                                    f"C5-shaped {rows}-row table") + ", S=8 logical shards, "
                                    "max_probe=128, load 0.8 prefilled via the API, 4M-position "
                                    "batches 90% hit / 10% fresh, eviction Disabled"
                                    + ("" if world == 1 else f"; row-sharded over {world} GPUs, "
-                                      "NCCL all-to-all id routing"),
+                                      f"{backend} all-to-all id routing"),
                        "rows": rows, "num_shards": SHARDS, "max_probe": MAX_PROBE,
                        "batch_positions": BATCH, "global_batch": BATCH,
                        "parallelism": "single GPU" if world == 1 else f"row-sharded x{world}",
