@@ -7,31 +7,30 @@
 // window not taken by a lower-rank unique.  The kernels below reach exactly that
 // assignment without any ordering pass:
 //
-//   K1 probe      one thread per POSITION, sector (32 B) loads from the home slot up to
-//                 the first match or EMPTY (hole-free early exit).  Hits on
-//                 live slots and full windows are final here; everything else goes to
-//                 the new list.  Read-only, so id validation is fused in.
-//   K2 dedup      new positions -> one entry per distinct id (64-bit atomicCAS key),
-//                 rank = first position (atomicMin).  (id, feature) secondaries are
-//                 resolved from the id's first position in K5.
+//   K0 validate   streaming pass over the ids: first invalid position (and, on a
+//                 row-sharded handle, ids of shards it does not hold).  Nothing below
+//                 mutates a batch that failed here.
+//   K1 probe      one thread per POSITION (2 in flight per thread), 32-byte sector loads
+//                 from the home slot up to the first match or EMPTY (hole-free early
+//                 exit).  Hits on live slots and full windows are final here
+//                 and write their metadata word; everything else goes to the new list.
+//   K2 dedup      new positions -> one 64-byte entry per distinct id (128-bit atomicCAS on
+//                 an epoch-tagged key), rank = first position (atomicMax of ~position).
+//                 (id, feature) secondaries are resolved from the id's first position in K5.
 //   K3 claim      every entry claims slots in its window by 64-bit atomicCAS of a
 //                 rank-stamped claim word into the identity array itself.  A claim
 //                 with a lower rank replaces a higher one; the thread that displaces a
 //                 claim continues the displaced entry's scan ("takeover"), so the
 //                 fixpoint -- each entry on the first slot no lower rank holds -- is
 //                 reached in one launch with no grid barrier.
-//   K4 commit     claim words -> ids, outcomes (Inserted/Evicted/Found-owner), touch_row,
-//                 reset list, evicted flags by rank.
+//   K4 commit     claim words -> ids, outcomes (Inserted/Evicted/Found-owner), the entry's
+//                 metadata word, touch_row, reset list, evicted flags by rank.
 //   K5 finalize   per new position result (+ secondary (id, f') rule).
-//   K6 meta       M[slot] = meta for every position (one value per batch => order-free).
+// One metadata value per batch makes every metadata write order-free.
 #include <cuda_runtime.h>
-
-#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "table.hpp"
-
-namespace cg = cooperative_groups;
 
 namespace mpzch_b200 {
 
