@@ -1,5 +1,13 @@
+"""Scale check on one B200: prefill a C5-sized table (default 2^30 rows, S=8, P=128) through the
+API in 4M-id batches and, every 20 batches, verify with the read-only lookup that every id of
+the batch is found at the slot the remap returned (or collided).  Catches memory-ordering bugs
+that only appear at full size (it found the stream-0 ordering bug in round 1).
+
+    python tools/scale_check.py [rows]
+"""
+import os
 import sys, time, os
-sys.path.insert(0, '.'); sys.path.insert(0, 'oracle')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__)))); sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), 'oracle'))
 import numpy as np, torch
 import paper_2602_17050_b200 as mz, bench
 rows = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 30
