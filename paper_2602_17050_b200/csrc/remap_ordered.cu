@@ -233,6 +233,161 @@ __global__ void __launch_bounds__(256) k_ordered(TableDev t, BatchCounters* ctr,
     }
 }
 
+// G4' (hole-free tables): the same per-shard rank-order walk, but one pass per unique that
+// stops at the first match or EMPTY.  With no hole in any window "exists"
+// (pass 1, probe_core.cpp:78-86) is "a match before the first EMPTY", so pass 2's decision
+// (probe_core.cpp:89-133) can be taken on the fly: match -> Found; EMPTY -> the first expired
+// slot before it (TTL) else Inserted; neither in the window -> first expired (TTL), the first
+// strict LRU minimum (LRU), else Collision.  The first 32-slot chunk of the NEXT unique of
+// the shard is loaded while the current one is decided and patched with the current one's
+// writes, so consecutive uniques overlap their latency.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_ordered_hf(TableDev t, BatchCounters* ctr,
+                                                    const uint64_t* __restrict__ ids,
+                                                    const uint32_t* __restrict__ upos,
+                                                    const uint32_t* __restrict__ ushard,
+                                                    const uint64_t* __restrict__ umeta, uint64_t now,
+                                                    uint64_t gen_clock, uint64_t* __restrict__ uslot,
+                                                    uint8_t* __restrict__ uoc,
+                                                    uint64_t* __restrict__ reset_rows,
+                                                    uint8_t* __restrict__ evflag,
+                                                    uint64_t* __restrict__ evslot) {
+    if (batch_failed(&ctr->err)) return;
+    const uint32_t shard = t.shard_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (shard >= t.shard_hi) return;
+    const unsigned lane = lane_id();
+    const unsigned u = ctr->entry_count;
+    const ShardDev sd = t.shards[shard];
+    const uint64_t cap = sd.cap.d, base = sd.offset;
+    const uint32_t P = t.P;
+    auto slot_at = [&](uint64_t h, uint32_t off) {
+        uint64_t x = h + off;
+        return base + (x >= cap ? x - cap : x);
+    };
+    // prefetched first chunk of the next unique of this shard
+    unsigned pf_k = kNone32;
+    uint64_t pf_v = 0, pf_m = 0;
+    for (unsigned k0 = 0; k0 < u; k0 += 32) {
+        const unsigned kk = k0 + lane;
+        unsigned mine = __ballot_sync(0xffffffffu, kk < u && ushard[kk] == shard);
+        while (mine) {
+            const unsigned k = k0 + __ffs(mine) - 1;
+            mine &= mine - 1;
+            const uint64_t id = ids[upos[k]];
+            const uint64_t meta_in = umeta[k];
+            const uint64_t h = home_of(id, sd, t.seed);
+            // issue the next unique's first chunk now
+            const unsigned nk = mine ? k0 + __ffs(mine) - 1 : kNone32;
+            uint64_t n_v = 0, n_m = 0, n_g = kEmpty;
+            if (nk != kNone32 && lane < P) {
+                const uint64_t nid = ids[upos[nk]];
+                n_g = slot_at(home_of(nid, sd, t.seed), lane);
+                n_v = ld_cg(t.ident + n_g);
+                if (MODE != kModeDisabled) n_m = ld_cg(t.meta + n_g);
+            }
+            uint8_t oc = kCollision;
+            uint64_t gslot = base + h;
+            bool decided = false;
+            uint32_t exp_off = kNone32;
+            uint64_t exp_g = 0, best_m = 0, best_g = 0;
+            uint32_t best_off = kNone32;
+            for (uint32_t c = 0; c < P; c += 32) {
+                const uint32_t off = c + lane;
+                const bool valid = off < P;
+                uint64_t g = 0, v = 0, m = 0;
+                if (valid) {
+                    g = slot_at(h, off);
+                    if (c == 0 && pf_k == k) {
+                        v = pf_v;
+                        m = pf_m;
+                    } else {
+                        v = ld_cg(t.ident + g);
+                        if (MODE != kModeDisabled) m = ld_cg(t.meta + g);
+                    }
+                }
+                const bool is_match = valid && v == id;
+                const bool is_empty = valid && v == kEmpty;
+                const unsigned stop = __ballot_sync(0xffffffffu, is_match || is_empty);
+                const int sl = stop ? __ffs(stop) - 1 : 32;
+                const unsigned before = sl == 32 ? 0xffffffffu : ((1u << sl) - 1);
+                if (MODE == kModeTtl && exp_off == kNone32) {
+                    const unsigned em = __ballot_sync(0xffffffffu, valid && !is_match && !is_empty &&
+                                                                       m < now) & before;
+                    if (em) {
+                        const int src = __ffs(em) - 1;
+                        exp_off = c + src;
+                        exp_g = __shfl_sync(0xffffffffu, g, src);
+                    }
+                }
+                if (MODE == kModeLru && !stop) {
+                    // first strict minimum over the window, ties -> lowest offset
+                    uint64_t bm = valid ? m : ~0ull;
+                    uint32_t bo = valid ? off : kNone32;
+                    uint64_t bg = g;
+                    for (int o = 16; o; o >>= 1) {
+                        const uint64_t om = __shfl_xor_sync(0xffffffffu, bm, o);
+                        const uint32_t oo = __shfl_xor_sync(0xffffffffu, bo, o);
+                        const uint64_t og = __shfl_xor_sync(0xffffffffu, bg, o);
+                        if (om < bm || (om == bm && oo < bo)) { bm = om; bo = oo; bg = og; }
+                    }
+                    if (bo != kNone32 && (best_off == kNone32 || bm < best_m)) {
+                        best_m = bm;
+                        best_off = bo;
+                        best_g = bg;
+                    }
+                }
+                if (stop) {
+                    const bool match = __shfl_sync(0xffffffffu, is_match, sl);
+                    const uint64_t gs = __shfl_sync(0xffffffffu, g, sl);
+                    if (match) {
+                        gslot = gs;
+                        oc = kFound;
+                    } else if (MODE == kModeTtl && exp_off != kNone32) {
+                        gslot = exp_g;
+                        oc = kEvicted;
+                    } else {
+                        gslot = gs;
+                        oc = kInserted;
+                    }
+                    decided = true;
+                    break;
+                }
+            }
+            if (!decided) {
+                if (MODE == kModeTtl && exp_off != kNone32) {
+                    gslot = exp_g;
+                    oc = kEvicted;
+                } else if (MODE == kModeLru && best_off != kNone32) {
+                    gslot = best_g;
+                    oc = kEvicted;  // LRU fallback, probe_core.cpp:125-129
+                }
+            }
+            if (lane == 0) {
+                if (oc == kInserted || oc == kEvicted) t.ident[gslot] = id;
+                t.meta[gslot] = meta_in;
+                if (oc == kInserted || oc == kEvicted) t.row_gen[gslot] = gen_clock;
+                if (oc == kEvicted) {
+                    if (t.dim) reset_rows[atomicAdd(&ctr->reset_count, 1u)] = gslot;
+                    evflag[k] = 1;
+                    evslot[k] = gslot;
+                    atomicAdd(&ctr->evicted_count, 1u);
+                }
+                uslot[k] = gslot;
+                uoc[k] = oc;
+            }
+            // patch the prefetched chunk with this unique's writes
+            if (n_g == gslot) {
+                if (oc == kInserted || oc == kEvicted) n_v = id;
+                n_m = meta_in;
+            }
+            pf_k = nk;
+            pf_v = n_v;
+            pf_m = n_m;
+            __syncwarp();
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) k_scatter(BatchCounters* ctr, uint64_t n,
                                                  const uint32_t* __restrict__ posent,
                                                  const uint32_t* __restrict__ entu,
@@ -309,7 +464,7 @@ void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
                              t.o_umeta.as<uint64_t>());
     const unsigned gS = (unsigned)(((uint64_t)(t.shard_hi - t.shard_lo) * 32 + B - 1) / B);
 #define MPZCH_ORDERED(MODE)                                                                       \
-    k_ordered<MODE><<<gS, B, 0, st>>>(t.dev, t.d_ctr, a.ids, t.o_upos.as<uint32_t>(),             \
+    (t.hole_free ? k_ordered_hf<MODE> : k_ordered<MODE>)<<<gS, B, 0, st>>>(t.dev, t.d_ctr, a.ids, t.o_upos.as<uint32_t>(),             \
                                       t.o_ushard.as<uint32_t>(), t.o_umeta.as<uint64_t>(), a.now, \
                                       t.gen_clock, t.o_uslot.as<uint64_t>(), t.o_uoc.as<uint8_t>(), \
                                       t.s_reset.as<uint64_t>(), t.s_evflag.as<uint8_t>(),           \

@@ -235,6 +235,29 @@ def c4():
     return dict(config="C4", init_draw_s=init_s, steady=r)
 
 
+def lru():
+    """Not a BASELINE config: C1-shaped LRU and per-feature-TTL batches, which take the ordered
+    per-shard path (exact for any policy), next to the reference on the same stream."""
+    rows = 1 << 20
+    pool = int(1.2 * rows)  # more ids than slots: full windows, LRU victims, double evictions
+    ids_pool = bench.distinct_ids_t(9, torch.arange(pool, dtype=torch.int64, device="cuda"))
+    B, nb = 65536, 24
+    g = torch.Generator(device="cuda").manual_seed(9)
+    batches = [ids_pool[torch.randint(0, pool, (B,), generator=g, device="cuda")].contiguous()
+               for _ in range(nb)]
+    nows = [10 + b for b in range(nb)]
+    st = torch.cuda.current_stream()
+    out = {}
+    bn = [b.cpu().numpy().view(np.uint64) for b in batches]
+    for shards in (8, 64):
+        caps = mz.even_capacities(rows, shards)
+        t = mz.MpzchTable(mz.TableConfig(caps, 128, 7))
+        r = run_batches(t, batches, nows, mz.EvictionPolicy.lru(), st, timed_from=8)
+        ref = ref_time(caps, 128, bn, nows, 2, 0, warm=8)
+        out[f"lru_S{shards}"] = dict(gpu=r, reference=ref)
+    return dict(config="LRU (ordered path)", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["c1", "c2", "c3", "c4"]
     out = []
