@@ -526,7 +526,10 @@ def main():
                          "batch_algorithmic_bytes": batch_bytes,
                          "batch_gbs": batch_bytes / (batch_ms / 1e3) / 1e9 if batch_ms else 0.0,
                          "claim_ms": prof["claim_ms"] / max(prof["batches"], 1),
-                         "tail_ms": prof["tail_ms"] / max(prof["batches"], 1)},
+                         "tail_ms": prof["tail_ms"] / max(prof["batches"], 1),
+                         "kernel_ms": {k: prof[k] / max(prof["batches"], 1) for k in
+                                       ("validate_ms", "dedup_ms", "claimk_ms", "commit_ms",
+                                        "finalize_ms")}},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "IDs/s", "h2d_bytes_per_step": BATCH * 8,
                     "d2h_bytes_per_step": BATCH * 9, "steps": e2e_steps, "api": e2e_api,

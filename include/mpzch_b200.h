@@ -220,6 +220,8 @@ typedef struct mpzch_profile {
     uint64_t probe_sectors; /* 32-byte identity/metadata sectors the probe read */
     uint64_t probe_bytes;   /* algorithmic bytes of the probe kernel (sectors + position I/O) */
     uint64_t batch_bytes;   /* algorithmic bytes of the whole batch (SURVEY 8d terms) */
+    double validate_ms;     /* per-kernel split of the fast path */
+    double dedup_ms, claimk_ms, commit_ms, finalize_ms;
 } mpzch_profile;
 mpzch_status mpzch_set_profiling(mpzch_table* t, int on);
 mpzch_status mpzch_get_profile(const mpzch_table* t, mpzch_profile* out);

@@ -103,7 +103,9 @@ class _Profile(ctypes.Structure):
                 ("probe_ms", ctypes.c_double), ("claim_ms", ctypes.c_double),
                 ("tail_ms", ctypes.c_double), ("batch_ms", ctypes.c_double),
                 ("probe_sectors", ctypes.c_uint64), ("probe_bytes", ctypes.c_uint64),
-                ("batch_bytes", ctypes.c_uint64)]
+                ("batch_bytes", ctypes.c_uint64), ("validate_ms", ctypes.c_double),
+                ("dedup_ms", ctypes.c_double), ("claimk_ms", ctypes.c_double),
+                ("commit_ms", ctypes.c_double), ("finalize_ms", ctypes.c_double)]
 
 
 _LIB = None

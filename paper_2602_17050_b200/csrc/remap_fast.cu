@@ -563,6 +563,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     uint32_t* newa = t.s_newa.as<uint32_t>();
     uint32_t* newm = t.s_newm.as<uint32_t>();
     uint32_t* newent = t.s_newent.as<uint32_t>();
+    if (t.profiling) cudaEventRecord(t.ev[7], st);
     k_init_counters<<<1, 32, 0, st>>>(t.d_ctr);
     k_validate<<<grid_for(n / 2 + 1, B, 148u * 8u), B, 0, st>>>(t.dev, a.ids, n, t.d_ctr);
     t.launches += 2;
@@ -578,8 +579,10 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     if (t.profiling) cudaEventRecord(t.ev[1], st);
     IdEntry* te = t.s_tent.as<IdEntry>();
     k_dedup<<<gW, B, 0, st>>>(t.d_ctr, t.tcap, epoch, newpos, newid, newa, newm, newent, te);
+    if (t.profiling) cudaEventRecord(t.ev[4], st);
 #define MPZCH_CLAIM_COMMIT(MODE)                                                                   \
     k_claim<MODE><<<gW, B, 0, st>>>(t.dev, a.now, t.d_ctr, newpos, newent, te);                   \
+    if (t.profiling) cudaEventRecord(t.ev[5], st);                                               \
     k_commit<MODE><<<gW, B, 0, st>>>(t.dev, t.d_ctr, newpos, newid, newent, te, t.gen_clock,      \
                                      a.uniform_meta, t.s_reset.as<uint64_t>(),                     \
                                      t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>())
@@ -589,6 +592,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     t.launches += 3;
     if (t.profiling) cudaEventRecord(t.ev[2], st);
     k_finalize<<<gW, B, 0, st>>>(t.d_ctr, a.feats, newpos, newent, te, a.out_slots, a.out_oc);
+    if (t.profiling) cudaEventRecord(t.ev[6], st);
     ++t.launches;
     if (t.dim > 0) launch_reset_rows(t, t.s_reset.as<uint64_t>(), &t.d_ctr->reset_count, st);
     if (a.out_mark) {  // first positions of Evicted uniques (row-sharded evicted list)

@@ -317,12 +317,22 @@ void complete_slot(Table& t, int si) {
         s.evicted_rows = c.evicted_count;
         s.path = sl.fast ? MPZCH_PATH_AUTO : MPZCH_PATH_ORDERED;
         if (sl.profiled && sl.fast) {
-            float a01 = 0, a12 = 0, a23 = 0, a03 = 0;
+            float a01 = 0, a12 = 0, a23 = 0, a03 = 0, k70 = 0, k14 = 0, k45 = 0, k52 = 0, k26 = 0;
             MPZCH_CUDA(cudaEventElapsedTime(&a01, sl.ev[0], sl.ev[1]));
             MPZCH_CUDA(cudaEventElapsedTime(&a12, sl.ev[1], sl.ev[2]));
             MPZCH_CUDA(cudaEventElapsedTime(&a23, sl.ev[2], sl.ev[3]));
             MPZCH_CUDA(cudaEventElapsedTime(&a03, sl.ev[0], sl.ev[3]));
+            MPZCH_CUDA(cudaEventElapsedTime(&k70, sl.ev[7], sl.ev[0]));
+            MPZCH_CUDA(cudaEventElapsedTime(&k14, sl.ev[1], sl.ev[4]));
+            MPZCH_CUDA(cudaEventElapsedTime(&k45, sl.ev[4], sl.ev[5]));
+            MPZCH_CUDA(cudaEventElapsedTime(&k52, sl.ev[5], sl.ev[2]));
+            MPZCH_CUDA(cudaEventElapsedTime(&k26, sl.ev[2], sl.ev[6]));
             mpzch_profile& p = t.prof;
+            p.validate_ms += k70;
+            p.dedup_ms += k14;
+            p.claimk_ms += k45;
+            p.commit_ms += k52;
+            p.finalize_ms += k26;
             const uint64_t n = sl.n;
             p.batches += 1;
             p.probe_launches += 1;

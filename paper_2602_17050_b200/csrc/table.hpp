@@ -102,7 +102,7 @@ public:
         bool busy = false, fast = false, overflow_all = false, profiled = false;
         uint64_t ticket = 0, n = 0;
         cudaEvent_t done = nullptr;
-        cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+        cudaEvent_t ev[8] = {};
     };
     struct Result {
         uint64_t ticket = ~0ull;
