@@ -45,9 +45,11 @@ enum { MPZCH_MODE_DISABLED = 0, MPZCH_MODE_TTL = 1, MPZCH_MODE_LRU = 2 };
 /* Outcome, proj/include/mpzch/probe_core.hpp:56 (same order, u8) */
 enum { MPZCH_FOUND = 0, MPZCH_INSERTED = 1, MPZCH_EVICTED = 2, MPZCH_COLLISION = 3 };
 
-/* Execution-path override (default AUTO: the fast claim path whenever it is
- * exact for the batch, the per-shard ordered kernel otherwise). */
-enum { MPZCH_PATH_AUTO = 0, MPZCH_PATH_ORDERED = 1 };
+/* Execution path (default AUTO): the claim path for Disabled / single-TTL batches on
+ * hole-free tables, the A.4 rounds path for LRU and per-feature-TTL batches on hole-free
+ * tables, the per-shard ordered kernel for tables with raw-imported holes.  ORDERED and
+ * ROUNDS force those paths (all three are exact for every batch). */
+enum { MPZCH_PATH_AUTO = 0, MPZCH_PATH_ORDERED = 1, MPZCH_PATH_ROUNDS = 2 };
 
 /* EvictionPolicy / TtlPolicy, proj/include/mpzch/eviction.hpp:13-46.
  * per-feature TTLs are given as parallel arrays (feat_keys[i] -> feat_ttls[i]). */
@@ -67,7 +69,7 @@ typedef struct mpzch_batch_stats {
     uint64_t found, inserted, evicted, collision; /* per position */
     uint64_t evicted_rows;   /* canonical evicted-list length */
     uint32_t path;           /* MPZCH_PATH_* actually taken */
-    uint32_t reserved;
+    uint32_t rounds;         /* rounds run by the rounds path */
 } mpzch_batch_stats;
 
 typedef struct mpzch_table mpzch_table;

@@ -95,7 +95,7 @@ class _Stats(ctypes.Structure):
                 ("new_ids", ctypes.c_uint64), ("found", ctypes.c_uint64),
                 ("inserted", ctypes.c_uint64), ("evicted", ctypes.c_uint64),
                 ("collision", ctypes.c_uint64), ("evicted_rows", ctypes.c_uint64),
-                ("path", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("path", ctypes.c_uint32), ("rounds", ctypes.c_uint32)]
 
 
 class _Profile(ctypes.Structure):
@@ -584,13 +584,13 @@ class MpzchTable:
         return out[:n.value].copy()
 
     def set_path(self, path: str):
-        _check(self._lib.mpzch_set_path(self._h, {"auto": 0, "ordered": 1}[path]))
+        _check(self._lib.mpzch_set_path(self._h, {"auto": 0, "ordered": 1, "rounds": 2}[path]))
 
     def last_stats(self) -> dict:
         s = _Stats()
         _check(self._lib.mpzch_last_stats(self._h, ctypes.byref(s)))
         d = {k: getattr(s, k) for k, _ in _Stats._fields_}
-        d["path"] = "fast" if s.path == 0 else "ordered"
+        d["path"] = {0: "fast", 1: "ordered", 2: "rounds"}[s.path]
         return d
 
     def set_profiling(self, on: bool = True):

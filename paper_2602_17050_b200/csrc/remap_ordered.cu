@@ -135,7 +135,8 @@ __global__ void __launch_bounds__(256) k_ordered(TableDev t, BatchCounters* ctr,
                                                  uint8_t* __restrict__ uoc,
                                                  uint64_t* __restrict__ reset_rows,
                                                  uint8_t* __restrict__ evflag,
-                                                 uint64_t* __restrict__ evslot) {
+                                                 uint64_t* __restrict__ evslot,
+                                                 const uint8_t* __restrict__ todo) {
     if (batch_failed(&ctr->err)) return;
     const uint32_t shard = t.shard_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (shard >= t.shard_hi) return;
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(256) k_ordered(TableDev t, BatchCounters* ctr,
     const uint32_t P = t.P;
     for (unsigned k0 = 0; k0 < u; k0 += 32) {
         const unsigned kk = k0 + lane;
-        unsigned mine = __ballot_sync(0xffffffffu, kk < u && ushard[kk] == shard);
+        unsigned mine = __ballot_sync(0xffffffffu, kk < u && ushard[kk] == shard && (!todo || todo[kk]));
         while (mine) {
             const unsigned k = k0 + __ffs(mine) - 1;
             mine &= mine - 1;
@@ -251,7 +252,8 @@ __global__ void __launch_bounds__(256) k_ordered_hf(TableDev t, BatchCounters* c
                                                     uint8_t* __restrict__ uoc,
                                                     uint64_t* __restrict__ reset_rows,
                                                     uint8_t* __restrict__ evflag,
-                                                    uint64_t* __restrict__ evslot) {
+                                                    uint64_t* __restrict__ evslot,
+                                                    const uint8_t* __restrict__ todo) {
     if (batch_failed(&ctr->err)) return;
     const uint32_t shard = t.shard_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (shard >= t.shard_hi) return;
@@ -269,7 +271,7 @@ __global__ void __launch_bounds__(256) k_ordered_hf(TableDev t, BatchCounters* c
     uint64_t pf_v = 0, pf_m = 0;
     for (unsigned k0 = 0; k0 < u; k0 += 32) {
         const unsigned kk = k0 + lane;
-        unsigned mine = __ballot_sync(0xffffffffu, kk < u && ushard[kk] == shard);
+        unsigned mine = __ballot_sync(0xffffffffu, kk < u && ushard[kk] == shard && (!todo || todo[kk]));
         while (mine) {
             const unsigned k = k0 + __ffs(mine) - 1;
             mine &= mine - 1;
@@ -438,7 +440,7 @@ __global__ void __launch_bounds__(256) k_cleanup_o(uint64_t n, const uint32_t* _
 
 }  // namespace
 
-void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
+void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st, bool rounds) {
     const uint64_t n = a.n;
     t.ensure_ordered_scratch(n);
     const unsigned B = 256;
@@ -463,19 +465,31 @@ void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
                              p.default_ttl, a.d_featk, a.d_featv, nk, t.o_ushard.as<uint32_t>(),
                              t.o_umeta.as<uint64_t>());
     const unsigned gS = (unsigned)(((uint64_t)(t.shard_hi - t.shard_lo) * 32 + B - 1) / B);
+    // rounds path (hole-free tables): parallel A.4 rounds, then the remainder (if any) in order
+    const uint8_t* todo = nullptr;
+    bool run_ordered = true;
+    if (rounds) {
+        t.o_todo.reserve(n);
+        const unsigned rem = run_rounds(t, a, st, t.o_todo.as<uint8_t>());
+        run_ordered = rem > 0;
+        todo = t.o_todo.as<uint8_t>();
+    }
 #define MPZCH_ORDERED(MODE)                                                                       \
-    (t.hole_free ? k_ordered_hf<MODE> : k_ordered<MODE>)<<<gS, B, 0, st>>>(t.dev, t.d_ctr, a.ids, t.o_upos.as<uint32_t>(),             \
-                                      t.o_ushard.as<uint32_t>(), t.o_umeta.as<uint64_t>(), a.now, \
-                                      t.gen_clock, t.o_uslot.as<uint64_t>(), t.o_uoc.as<uint8_t>(), \
-                                      t.s_reset.as<uint64_t>(), t.s_evflag.as<uint8_t>(),           \
-                                      t.s_evslot.as<uint64_t>())
-    if (p.mode == kModeTtl) MPZCH_ORDERED(kModeTtl);
-    else if (p.mode == kModeLru) MPZCH_ORDERED(kModeLru);
-    else MPZCH_ORDERED(kModeDisabled);
+    (t.hole_free ? k_ordered_hf<MODE> : k_ordered<MODE>)<<<gS, B, 0, st>>>(                      \
+        t.dev, t.d_ctr, a.ids, t.o_upos.as<uint32_t>(), t.o_ushard.as<uint32_t>(),                \
+        t.o_umeta.as<uint64_t>(), a.now, t.gen_clock, t.o_uslot.as<uint64_t>(),                   \
+        t.o_uoc.as<uint8_t>(), t.s_reset.as<uint64_t>(), t.s_evflag.as<uint8_t>(),                 \
+        t.s_evslot.as<uint64_t>(), todo)
+    if (run_ordered) {
+        if (p.mode == kModeTtl) MPZCH_ORDERED(kModeTtl);
+        else if (p.mode == kModeLru) MPZCH_ORDERED(kModeLru);
+        else MPZCH_ORDERED(kModeDisabled);
+        ++t.launches;
+    }
 #undef MPZCH_ORDERED
     k_scatter<<<gN, B, 0, st>>>(t.d_ctr, n, posent, t.o_entu.as<uint32_t>(), t.o_uslot.as<uint64_t>(),
                                 t.o_uoc.as<uint8_t>(), a.out_slots, a.out_oc);
-    t.launches += 3;
+    t.launches += 2;
     if (t.dim > 0) launch_reset_rows(t, t.s_reset.as<uint64_t>(), &t.d_ctr->reset_count, st);
     if (a.out_mark) {  // unique k's first position is upos[k]
         MPZCH_CUDA(cudaMemsetAsync(a.out_mark, 0, n, st));

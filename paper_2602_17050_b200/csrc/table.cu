@@ -315,7 +315,8 @@ void complete_slot(Table& t, int si) {
         s.evicted = c.evicted;
         s.collision = c.collision;
         s.evicted_rows = c.evicted_count;
-        s.path = sl.fast ? MPZCH_PATH_AUTO : MPZCH_PATH_ORDERED;
+        s.path = sl.path;
+        s.rounds = sl.rounds;
         if (sl.profiled && sl.fast) {
             float a01 = 0, a12 = 0, a23 = 0, a03 = 0, k70 = 0, k14 = 0, k45 = 0, k52 = 0, k26 = 0;
             MPZCH_CUDA(cudaEventElapsedTime(&a01, sl.ev[0], sl.ev[1]));
@@ -425,10 +426,12 @@ uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uin
     }
     const bool fast = t.path_override == MPZCH_PATH_AUTO && t.hole_free &&
                       pol.mode != kModeLru && a.uniform && n <= (1ull << 29);
+    const bool rounds = !fast && t.hole_free && t.path_override != MPZCH_PATH_ORDERED;
     const bool profiled = t.profiling;
     if (!fast) t.profiling = false;  // events are recorded by the fast path only
+    t.last_rounds = 0;
     if (fast) enqueue_fast_batch(t, a, st);
-    else enqueue_ordered_batch(t, a, st);
+    else enqueue_ordered_batch(t, a, st, rounds);
     t.profiling = profiled;
     MPZCH_CUDA(cudaGetLastError());
     MPZCH_CUDA(cudaMemcpyAsync(t.h_ctr, t.d_ctr, sizeof(BatchCounters), cudaMemcpyDeviceToHost, st));
@@ -437,6 +440,8 @@ uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uin
     sl.ticket = ticket;
     sl.n = n;
     sl.fast = fast;
+    sl.path = fast ? MPZCH_PATH_AUTO : (rounds ? MPZCH_PATH_ROUNDS : MPZCH_PATH_ORDERED);
+    sl.rounds = (uint32_t)t.last_rounds;
     sl.overflow_all = a.overflow_all;
     sl.profiled = profiled;
     t.last_stream = st;
@@ -1042,7 +1047,7 @@ mpzch_status mpzch_delta_cut(mpzch_table* t, uint64_t generation, uint64_t* out_
 
 mpzch_status mpzch_set_path(mpzch_table* t, int path) {
     CHECK_T(t);
-    if (path != MPZCH_PATH_AUTO && path != MPZCH_PATH_ORDERED) {
+    if (path != MPZCH_PATH_AUTO && path != MPZCH_PATH_ORDERED && path != MPZCH_PATH_ROUNDS) {
         g_last_error = "unknown execution path";
         return MPZCH_EINVAL;
     }

@@ -53,6 +53,7 @@ struct BatchCounters {
     unsigned int overflow_list;  // claim-log overflow (defensive)
     unsigned int pad;
     unsigned long long id_sectors, meta_sectors;  // sectors the probe kernel read
+    unsigned int r_new, r_next;  // rounds path: new suspects / next pending
 };
 
 struct Policy {
@@ -100,6 +101,7 @@ public:
     static constexpr int kRing = 8, kResults = 64;
     struct Slot {
         bool busy = false, fast = false, overflow_all = false, profiled = false;
+        uint32_t path = 0, rounds = 0;
         uint64_t ticket = 0, n = 0;
         cudaEvent_t done = nullptr;
         cudaEvent_t ev[8] = {};
@@ -146,8 +148,12 @@ public:
     DevBuf s_ids, s_feats, s_oslot, s_ooc, s_oev;    // staging for host-buffer calls
     DevBuf s_featk, s_featv;                         // per-feature TTL map
     // ordered path
-    DevBuf o_key, o_min, o_posent, o_flag, o_upos, o_entu, o_ushard, o_umeta, o_uslot, o_uoc;
+    DevBuf o_key, o_min, o_posent, o_flag, o_upos, o_entu, o_ushard, o_umeta, o_uslot, o_uoc, o_todo;
     uint64_t ocap = 0;
+    // rounds path: epoch-keyed reservation marks (one word per held row)
+    DevBuf r_mark, r_pend, r_next, r_new, r_slot, r_oc, r_d, r_susp;
+    uint32_t mark_epoch = 0;
+    uint64_t last_rounds = 0;  // rounds run by the last rounds-path batch
 
     void ensure_fast_scratch(uint64_t n);
     void ensure_ordered_scratch(uint64_t n);
@@ -186,7 +192,8 @@ struct BatchArgs {
 
 // enqueue the whole batch; counters land in t.h_ctr after the stream syncs
 void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st);
-void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st);
+void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st, bool rounds = false);
+unsigned run_rounds(Table& t, const BatchArgs& a, cudaStream_t st, uint8_t* todo);
 void enqueue_compact_evicted(Table& t, uint64_t n, uint64_t* out_ev, uint64_t ev_cap, cudaStream_t st);
 void run_route(Table& t, const uint64_t* ids, uint64_t n, const uint32_t* shard_to_part,
                uint32_t parts, uint32_t* perm, uint64_t* counts, cudaStream_t st);

@@ -45,7 +45,7 @@ def assert_same_state(a, b, tag=""):
 
 # ---------------------------------------------------------------- reference fixtures
 
-@pytest.mark.parametrize("path", ["auto", "ordered"])
+@pytest.mark.parametrize("path", ["auto", "ordered", "rounds"])
 def test_replay_reference_fixtures(path):
     z, man = _fixture()
     paths_seen = set()
@@ -70,7 +70,9 @@ def test_replay_reference_fixtures(path):
     n = replay_fixture(make, run, state, z, man)
     assert n == len(z["batches"])
     if path == "auto":
-        assert "fast" in paths_seen  # the claim path really ran
+        assert {"fast", "rounds"} <= paths_seen  # the claim and rounds paths really ran
+    if path == "rounds":
+        assert "rounds" in paths_seen
 
 
 # ---------------------------------------------------------------- probe-core scenarios
@@ -544,3 +546,24 @@ def test_delta_cut_matches_dirty_rows(oracle):
     assert r2.size == 0
     with pytest.raises(mz.InvalidArgument, match="stale or unknown publication cursor"):
         t.delta_cut(0)
+
+
+
+@pytest.mark.parametrize("path", ["auto", "ordered", "rounds"])
+@pytest.mark.parametrize("shards", [1, 8])
+def test_lru_and_feature_ttl_streams_all_paths(oracle, path, shards):
+    """LRU (full windows, double evictions) and per-feature TTL batches at a dense load:
+    the A.4 rounds path (auto), the ordered path and forced rounds agree with the oracle."""
+    rows = 1 << 13
+    caps = mz.even_capacities(rows, shards)
+    uni = oracle.distinct_ids(21, 0, int(rows * 1.3))
+    rng = np.random.default_rng(shards)
+    for mode, dttl, pf in ((2, 0, None), (1, 40, {1: 7, 2: 90})):
+        batches = []
+        for b in range(12):
+            n = 3000
+            f = rng.integers(0, 3, n).astype(np.uint32) if mode == 1 or b % 2 else None
+            batches.append((uni[rng.integers(0, uni.size, n)], f, 100 + 9 * b))
+        t = run_stream(oracle, caps, 16, 5, 4, 3, batches, mode, dttl, pf, path, check_state_every=4)
+        if path == "auto":
+            assert t.last_stats()["path"] == "rounds"
