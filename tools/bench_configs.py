@@ -61,7 +61,7 @@ def run_batches(t, batches, nows, pol, stream, timed_from=0, feats=None):
     prof = t.profile()
     t.set_profiling(False)
     pos = sum(b.numel() for b in batches[timed_from:])
-    agg = {k: int(sum(s[k] for s in stats)) for k in ("found", "inserted", "evicted", "collision", "new_ids", "evicted_rows")}
+    agg = {k: int(sum(s[k] for s in stats)) for k in ("found", "inserted", "evicted", "collision", "new_ids", "evicted_rows", "rounds")}
     nb = max(prof["batches"], 1)
     return dict(ids_per_s=pos / (ms / 1e3), ms_per_batch=ms / max(len(stats), 1), positions=pos,
                 outcomes=agg, path=stats[-1]["path"] if stats else None,
@@ -235,11 +235,12 @@ def c4():
     return dict(config="C4", init_draw_s=init_s, steady=r)
 
 
-def lru():
-    """Not a BASELINE config: C1-shaped LRU and per-feature-TTL batches, which take the ordered
-    per-shard path (exact for any policy), next to the reference on the same stream."""
+def lru(pool_factor=1.2):
+    """Not a BASELINE config: C1-shaped LRU batches (the A.4 rounds path), next to the
+    reference on the same stream.  pool_factor 1.2: more ids than slots (full windows, LRU
+    victims, double evictions); 0.8: the C1 pool."""
     rows = 1 << 20
-    pool = int(1.2 * rows)  # more ids than slots: full windows, LRU victims, double evictions
+    pool = int(pool_factor * rows)
     ids_pool = bench.distinct_ids_t(9, torch.arange(pool, dtype=torch.int64, device="cuda"))
     B, nb = 65536, 24
     g = torch.Generator(device="cuda").manual_seed(9)
@@ -255,7 +256,11 @@ def lru():
         r = run_batches(t, batches, nows, mz.EvictionPolicy.lru(), st, timed_from=8)
         ref = ref_time(caps, 128, bn, nows, 2, 0, warm=8)
         out[f"lru_S{shards}"] = dict(gpu=r, reference=ref)
-    return dict(config="LRU (ordered path)", **out)
+    return dict(config=f"LRU pool {pool_factor} x rows", **out)
+
+
+def lru08():
+    return lru(0.8)
 
 
 if __name__ == "__main__":
