@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256) k_ordered(TableDev t, BatchCounters* ctr,
                                                  uint8_t* __restrict__ evflag,
                                                  uint64_t* __restrict__ evslot,
                                                  const uint8_t* __restrict__ todo) {
-    if (batch_failed(&ctr->err)) return;
+    if (batch_failed(&ctr->err) || (todo && !ctr->r_left)) return;  // rounds left nothing
     const uint32_t shard = t.shard_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (shard >= t.shard_hi) return;
     const unsigned lane = lane_id();
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(256) k_ordered_hf(TableDev t, BatchCounters* c
                                                     uint8_t* __restrict__ evflag,
                                                     uint64_t* __restrict__ evslot,
                                                     const uint8_t* __restrict__ todo) {
-    if (batch_failed(&ctr->err)) return;
+    if (batch_failed(&ctr->err) || (todo && !ctr->r_left)) return;  // rounds left nothing
     const uint32_t shard = t.shard_lo + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (shard >= t.shard_hi) return;
     const unsigned lane = lane_id();
@@ -467,11 +467,9 @@ void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st, bool r
     const unsigned gS = (unsigned)(((uint64_t)(t.shard_hi - t.shard_lo) * 32 + B - 1) / B);
     // rounds path (hole-free tables): parallel A.4 rounds, then the remainder (if any) in order
     const uint8_t* todo = nullptr;
-    bool run_ordered = true;
     if (rounds) {
         t.o_todo.reserve(n);
-        const unsigned rem = run_rounds(t, a, st, t.o_todo.as<uint8_t>());
-        run_ordered = rem > 0;
+        enqueue_rounds(t, a, st, t.o_todo.as<uint8_t>());
         todo = t.o_todo.as<uint8_t>();
     }
 #define MPZCH_ORDERED(MODE)                                                                       \
@@ -480,12 +478,10 @@ void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st, bool r
         t.o_umeta.as<uint64_t>(), a.now, t.gen_clock, t.o_uslot.as<uint64_t>(),                   \
         t.o_uoc.as<uint8_t>(), t.s_reset.as<uint64_t>(), t.s_evflag.as<uint8_t>(),                 \
         t.s_evslot.as<uint64_t>(), todo)
-    if (run_ordered) {
-        if (p.mode == kModeTtl) MPZCH_ORDERED(kModeTtl);
-        else if (p.mode == kModeLru) MPZCH_ORDERED(kModeLru);
-        else MPZCH_ORDERED(kModeDisabled);
-        ++t.launches;
-    }
+    if (p.mode == kModeTtl) MPZCH_ORDERED(kModeTtl);
+    else if (p.mode == kModeLru) MPZCH_ORDERED(kModeLru);
+    else MPZCH_ORDERED(kModeDisabled);
+    ++t.launches;
 #undef MPZCH_ORDERED
     k_scatter<<<gN, B, 0, st>>>(t.d_ctr, n, posent, t.o_entu.as<uint32_t>(), t.o_uslot.as<uint64_t>(),
                                 t.o_uoc.as<uint8_t>(), a.out_slots, a.out_oc);

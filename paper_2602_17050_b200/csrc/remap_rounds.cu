@@ -4,100 +4,64 @@
 // path's dedup produced (rank = unique index, first-occurrence order).
 //
 // One round, over the pending uniques, against the committed state C:
-//   R1 k_tentative  each unique decides against C exactly as probe_core.cpp:69-134 would
-//                   (single pass to the first match/EMPTY: hole-free), recording
-//                   its read range [h, h+d] (identity and metadata words it looked at) and
-//                   its write slot, and marks the write slot with its rank (64-bit atomicMin
-//                   of an epoch-keyed word, so marks never need clearing).
-//   R2 k_check      a unique is SUSPECT if a lower-rank pending unique marked a slot inside
-//                   its read range (first order) ...
-//   R3 k_mark_win   ... or a lower-rank suspect's whole window overlaps it (transitive):
-//                   new suspects mark their windows and R2 runs again until no new suspect.
-//   R4 k_commit     non-suspects are final (by induction on rank, A.4) and have pairwise
-//                   disjoint write slots (every write slot lies in its writer's read range),
-//                   so they commit in any order; the suspects are the next round's pending set.
-// The lowest-rank pending unique is never suspect, so every round commits at least one; after
-// kMaxRounds the remaining uniques go to the per-shard ordered kernel (always exact).
+//   R1 k_tentative  each unique k decides against C exactly as probe_core.cpp:69-134 would
+//                   (single pass to the first match/EMPTY: hole-free), recording its
+//                   read range R_k = [h, h+d] and its write slot w_k in R_k, and marks w_k with
+//                   its rank: ident-changing writes (Inserted/Evicted) in mark_id, metadata-only
+//                   writes (Found refresh, Collision's home touch) in mark_any (64-bit atomicMin
+//                   of epoch-keyed words, so marks never need clearing).
+//   R2 k_check      k is SUSPECT if a lower rank left a mark_id mark anywhere in R_k, or any
+//                   lower-rank mark on w_k, or (LRU full window: the victim depends on every
+//                   metadata word of R_k) any lower-rank mark in R_k.  A metadata-only write at
+//                   x != w_k changes no other decision: Found and Inserted-at-EMPTY read no
+//                   metadata, and under TTL a refresh (now + ttl >= now) only un-expires x, which
+//                   matters only if x was k's victim, i.e. x == w_k.
+//   R3 mark_window  a suspect may end up writing anywhere in its window: a new suspect marks its
+//                   whole window in mark_id at once (so cascades spread inside a pass) and R2
+//                   repeats until a pass finds no new suspect (the fixpoint).  After kClosureMax
+//                   passes the last pass's suspects are left unmarked; with m = the lowest of
+//                   their ranks, every non-suspect of rank < m is final (every suspect below it
+//                   was marked before that pass).
+//   R4 k_commit     non-suspects of rank < m are final (induction on rank, A.4) and have pairwise
+//                   distinct write slots (own-slot rule), so they commit in any order; the rest
+//                   is the next round's pending set.  A committed k never lies in the window of a
+//                   lower-rank unique that stays pending (those are marked suspects), so later
+//                   rounds never read what k wrote out of order.
+// The lowest-rank pending unique is never suspect, so every round commits at least one.
+//
+// All rounds run in ONE persistent cooperative kernel (grid-wide barriers between the phases,
+// the closure iterated to its fixpoint), so the path needs no host round trip: after kMaxRounds
+// the remaining uniques are flagged for the per-shard ordered kernel (always exact), which the
+// host enqueues unconditionally and which returns at once when nothing is left.  Data other
+// blocks wrote inside the kernel is read through L2 (ld.cg), never the .nc/L1 path.  The mark
+// arrays alias slots modulo their size: an alias only adds suspicion.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
-#include <vector>
+#include <algorithm>
 
 #include "common.cuh"
 #include "table.hpp"
 
 namespace mpzch_b200 {
 
+namespace cg = cooperative_groups;
+
 namespace {
 
-constexpr int kMaxRounds = 24;
+constexpr int kMaxRounds = 32;
+constexpr int kClosureMax = 16;  // R2/R3 passes before the closure falls back to the rank bound
 
 __device__ __forceinline__ uint64_t mark_key(uint32_t epoch, uint32_t rank) {
     return ((uint64_t)(0xffffffffu - epoch) << 32) | rank;
 }
-__device__ __forceinline__ bool mark_is(uint64_t mk, uint32_t epoch) {
-    return (uint32_t)(mk >> 32) == 0xffffffffu - epoch;
+// rank of this epoch's mark, or ~0 when the word holds an older epoch's mark
+__device__ __forceinline__ uint32_t mark_rank(uint64_t mk, uint32_t epoch) {
+    return (uint32_t)(mk >> 32) == 0xffffffffu - epoch ? (uint32_t)mk : kNone32;
 }
 
 __device__ __forceinline__ uint64_t pick4r(uint32_t j, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
     return j == 0 ? a : (j == 1 ? b : (j == 2 ? c : d));
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(256) k_tentative(TableDev t, const BatchCounters* ctr,
-                                                   const uint64_t* __restrict__ ids,
-                                                   const uint32_t* __restrict__ upos,
-                                                   const uint32_t* __restrict__ ushard,
-                                                   const uint32_t* __restrict__ pend, unsigned npend,
-                                                   uint64_t now, uint32_t epoch,
-                                                   uint64_t* __restrict__ td_slot,
-                                                   uint8_t* __restrict__ td_oc,
-                                                   uint32_t* __restrict__ td_d,
-                                                   unsigned long long* mark, uint64_t mark_base) {
-    if (batch_failed(&ctr->err)) return;
-    for (unsigned x = blockIdx.x * blockDim.x + threadIdx.x; x < npend; x += gridDim.x * blockDim.x) {
-        const uint32_t k = pend[x];
-        const uint64_t id = ids[upos[k]];
-        const ShardDev sd = t.shards[ushard[k]];
-        const uint64_t cap = sd.cap.d, base = sd.offset, end = base + cap;
-        const uint64_t h = home_of(id, sd, t.seed);
-        uint64_t g = base + h;
-        uint32_t off = 0;
-        int kind = 0;  // 1 match, 2 empty
-        uint32_t exp_off = kNone32;
-        uint64_t exp_g = 0, best_m = 0, best_g = 0;
-        bool have_best = false;
-        while (off < t.P && !kind) {
-            const uint64_t a4 = g & ~3ull;
-            uint64_t i0, i1, i2, i3, m0 = 0, m1 = 0, m2 = 0, m3 = 0;
-            ld_sector(t.ident + a4, i0, i1, i2, i3);
-            if (MODE != kModeDisabled) ld_sector(t.meta + a4, m0, m1, m2, m3);
-            do {
-                const uint32_t j = (uint32_t)(g - a4);
-                const uint64_t v = pick4r(j, i0, i1, i2, i3);
-                if (v == id) { kind = 1; break; }
-                if (v == kEmpty) { kind = 2; break; }
-                if (MODE != kModeDisabled) {
-                    const uint64_t m = pick4r(j, m0, m1, m2, m3);
-                    if (MODE == kModeTtl && exp_off == kNone32 && m < now) { exp_off = off; exp_g = g; }
-                    if (MODE == kModeLru && (!have_best || m < best_m)) { have_best = true; best_m = m; best_g = g; }
-                }
-                ++off;
-                if (++g == end) g = base;
-            } while (off < t.P && (g >> 2) == (a4 >> 2));
-        }
-        uint8_t oc = kCollision;
-        uint64_t ws = base + h;
-        if (kind == 1) { oc = kFound; ws = g; }
-        else if (kind == 2) {
-            if (MODE == kModeTtl && exp_off != kNone32) { oc = kEvicted; ws = exp_g; }
-            else { oc = kInserted; ws = g; }
-        } else if (MODE == kModeTtl && exp_off != kNone32) { oc = kEvicted; ws = exp_g; }
-        else if (MODE == kModeLru && have_best) { oc = kEvicted; ws = best_g; }
-        td_slot[k] = ws;
-        td_oc[k] = oc;
-        td_d[k] = kind ? off : t.P - 1;  // read range [h, h + d]
-        atomicMin(mark + (ws - mark_base), (unsigned long long)mark_key(epoch, k));
-    }
 }
 
 __device__ __forceinline__ uint64_t slot_of(const ShardDev& sd, uint64_t h, uint32_t off) {
@@ -106,189 +70,283 @@ __device__ __forceinline__ uint64_t slot_of(const ShardDev& sd, uint64_t h, uint
     return sd.offset + x;
 }
 
-// R2: first-order and transitive suspicion (marks of lower ranks inside my read range)
-__global__ void __launch_bounds__(256) k_check(TableDev t, BatchCounters* ctr,
-                                               const uint64_t* __restrict__ ids,
-                                               const uint32_t* __restrict__ upos,
-                                               const uint32_t* __restrict__ ushard,
-                                               const uint32_t* __restrict__ pend, unsigned npend,
-                                               uint32_t epoch, const uint32_t* __restrict__ td_d,
-                                               uint8_t* susp, const unsigned long long* mark,
-                                               uint64_t mark_base, uint32_t* newsusp) {
-    if (batch_failed(&ctr->err)) return;
-    for (unsigned x = blockIdx.x * blockDim.x + threadIdx.x; x < npend; x += gridDim.x * blockDim.x) {
-        const uint32_t k = pend[x];
-        if (susp[k]) continue;
-        const uint64_t id = ids[upos[k]];
-        const ShardDev sd = t.shards[ushard[k]];
-        const uint64_t h = home_of(id, sd, t.seed);
-        const uint32_t d = td_d[k];
-        bool s = false;
-        for (uint32_t off = 0; off <= d && !s; ++off) {
-            const uint64_t mk = __ldcg(mark + (slot_of(sd, h, off) - mark_base));
-            s = mark_is(mk, epoch) && (uint32_t)mk < k;
-        }
-        if (s) {
-            susp[k] = 1;
-            newsusp[atomicAdd(&ctr->r_new, 1u)] = k;
-        }
-    }
+__device__ __forceinline__ unsigned ldcg_u32(const unsigned* p) { return __ldcg(p); }
+__device__ __forceinline__ uint8_t ldcg_u8(const uint8_t* p) {
+    return (uint8_t)__ldcg(reinterpret_cast<const unsigned char*>(p));
+}
+__device__ __forceinline__ void stcg_u8(uint8_t* p, uint8_t v) {
+    __stcg(reinterpret_cast<unsigned char*>(p), (unsigned char)v);
 }
 
-// R3: a suspect may end up writing anywhere in its window
-__global__ void __launch_bounds__(256) k_mark_windows(TableDev t, const BatchCounters* ctr,
-                                                      const uint64_t* __restrict__ ids,
-                                                      const uint32_t* __restrict__ upos,
-                                                      const uint32_t* __restrict__ ushard,
-                                                      const uint32_t* __restrict__ list, unsigned cnt,
-                                                      uint32_t epoch, unsigned long long* mark,
-                                                      uint64_t mark_base) {
-    for (unsigned x = blockIdx.x * blockDim.x + threadIdx.x; x < cnt; x += gridDim.x * blockDim.x) {
-        const uint32_t k = list[x];
-        const uint64_t id = ids[upos[k]];
-        const ShardDev sd = t.shards[ushard[k]];
-        const uint64_t h = home_of(id, sd, t.seed);
-        for (uint32_t off = 0; off < t.P; ++off)
-            atomicMin(mark + (slot_of(sd, h, off) - mark_base), (unsigned long long)mark_key(epoch, k));
+struct RoundsArgs {
+    TableDev t;
+    BatchCounters* ctr;
+    const uint64_t* ids;
+    const uint32_t* upos;
+    const uint32_t* ushard;
+    const uint64_t* umeta;
+    uint64_t now, gen_clock;
+    uint32_t epoch0;
+    uint32_t* pend[2];
+    uint64_t* td_slot;
+    uint8_t* td_oc;
+    uint32_t* td_d;
+    uint8_t* susp;  // 0 clear, 1 suspect
+    uint8_t* todo;
+    unsigned long long* mark_any;  // metadata-only writes
+    unsigned long long* mark_id;   // ident-changing writes and suspect windows
+    uint64_t mark_base, mark_mask;
+    uint64_t* uslot;
+    uint8_t* uoc;
+    uint64_t* reset_rows;
+    uint8_t* evflag;
+    uint64_t* evslot;
+    __device__ __forceinline__ uint64_t mi(uint64_t g) const { return (g - mark_base) & mark_mask; }
+};
+
+// R1
+template <int MODE>
+__device__ __forceinline__ void tentative(const RoundsArgs& r, uint32_t k, uint32_t epoch) {
+    const TableDev& t = r.t;
+    const uint64_t id = r.ids[r.upos[k]];
+    const ShardDev sd = t.shards[r.ushard[k]];
+    const uint64_t cap = sd.cap.d, base = sd.offset, end = base + cap;
+    const uint64_t h = home_of(id, sd, t.seed);
+    uint64_t g = base + h;
+    uint32_t off = 0;
+    int kind = 0;  // 1 match, 2 empty
+    uint32_t exp_off = kNone32;
+    uint64_t exp_g = 0, best_m = 0, best_g = 0;
+    bool have_best = false;
+    while (off < t.P && !kind) {
+        const uint64_t a4 = g & ~3ull;
+        uint64_t i0, i1, i2, i3, m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+        ld_sector_cg(t.ident + a4, i0, i1, i2, i3);
+        if (MODE != kModeDisabled) ld_sector_cg(t.meta + a4, m0, m1, m2, m3);
+        do {
+            const uint32_t j = (uint32_t)(g - a4);
+            const uint64_t v = pick4r(j, i0, i1, i2, i3);
+            if (v == id) { kind = 1; break; }
+            if (v == kEmpty) { kind = 2; break; }
+            if (MODE != kModeDisabled) {
+                const uint64_t m = pick4r(j, m0, m1, m2, m3);
+                if (MODE == kModeTtl && exp_off == kNone32 && m < r.now) { exp_off = off; exp_g = g; }
+                if (MODE == kModeLru && (!have_best || m < best_m)) { have_best = true; best_m = m; best_g = g; }
+            }
+            ++off;
+            if (++g == end) g = base;
+        } while (off < t.P && (g >> 2) == (a4 >> 2));
     }
+    uint8_t oc = kCollision;
+    uint64_t ws = base + h;
+    if (kind == 1) { oc = kFound; ws = g; }
+    else if (kind == 2) {
+        if (MODE == kModeTtl && exp_off != kNone32) { oc = kEvicted; ws = exp_g; }
+        else { oc = kInserted; ws = g; }
+    } else if (MODE == kModeTtl && exp_off != kNone32) { oc = kEvicted; ws = exp_g; }
+    else if (MODE == kModeLru && have_best) { oc = kEvicted; ws = best_g; }
+    __stcg(r.td_slot + k, ws);
+    stcg_u8(r.td_oc + k, oc);
+    __stcg(r.td_d + k, kind ? off : t.P - 1);  // read range [h, h + d]
+    const bool ident_write = oc == kInserted || oc == kEvicted;
+    atomicMin((ident_write ? r.mark_id : r.mark_any) + r.mi(ws), (unsigned long long)mark_key(epoch, k));
 }
 
-// R4: commit the non-suspects; collect the suspects as the next pending set
-__global__ void __launch_bounds__(256) k_commit_round(TableDev t, BatchCounters* ctr,
-                                                      const uint64_t* __restrict__ ids,
-                                                      const uint32_t* __restrict__ upos,
-                                                      const uint64_t* __restrict__ umeta,
-                                                      const uint32_t* __restrict__ pend, unsigned npend,
-                                                      uint8_t* susp, const uint64_t* __restrict__ td_slot,
-                                                      const uint8_t* __restrict__ td_oc,
-                                                      uint64_t gen_clock, uint64_t* __restrict__ uslot,
-                                                      uint8_t* __restrict__ uoc,
-                                                      uint64_t* __restrict__ reset_rows,
-                                                      uint8_t* __restrict__ evflag,
-                                                      uint64_t* __restrict__ evslot, uint32_t* next) {
-    if (batch_failed(&ctr->err)) return;
-    for (unsigned x = blockIdx.x * blockDim.x + threadIdx.x; x < npend; x += gridDim.x * blockDim.x) {
-        const uint32_t k = pend[x];
-        if (susp[k]) {
-            susp[k] = 0;
-            next[atomicAdd(&ctr->r_next, 1u)] = k;
-            continue;
-        }
-        const uint64_t g = td_slot[k];
-        const uint8_t oc = td_oc[k];
-        if (oc == kInserted || oc == kEvicted) {
-            t.ident[g] = ids[upos[k]];
-            t.row_gen[g] = gen_clock;
-        }
-        t.meta[g] = umeta[k];
-        if (oc == kEvicted) {
-            if (t.dim) reset_rows[atomicAdd(&ctr->reset_count, 1u)] = g;
-            evflag[k] = 1;
-            evslot[k] = g;
-            atomicAdd(&ctr->evicted_count, 1u);
-        }
-        uslot[k] = g;
-        uoc[k] = oc;
+// R2 (rule in the header)
+template <int MODE>
+__device__ __forceinline__ bool suspect(const RoundsArgs& r, uint32_t k, uint32_t epoch) {
+    const uint64_t id = r.ids[r.upos[k]];
+    const ShardDev sd = r.t.shards[r.ushard[k]];
+    const uint64_t h = home_of(id, sd, r.t.seed);
+    const uint32_t d = __ldcg(r.td_d + k);
+    const uint64_t w = __ldcg(r.td_slot + k);
+    const bool meta_dep = MODE == kModeLru && ldcg_u8(r.td_oc + k) == kEvicted;  // full window
+    for (uint32_t off = 0; off <= d; ++off) {
+        const uint64_t g = slot_of(sd, h, off);
+        const uint64_t i = r.mi(g);
+        if (mark_rank(__ldcg(r.mark_id + i), epoch) < k) return true;
+        if ((meta_dep || g == w) && mark_rank(__ldcg(r.mark_any + i), epoch) < k) return true;
     }
+    return false;
 }
 
-__global__ void k_iota(uint32_t* p, const BatchCounters* ctr) {
+// R3
+__device__ __forceinline__ void mark_window(const RoundsArgs& r, uint32_t k, uint32_t epoch) {
+    const uint64_t id = r.ids[r.upos[k]];
+    const ShardDev sd = r.t.shards[r.ushard[k]];
+    const uint64_t h = home_of(id, sd, r.t.seed);
+    for (uint32_t off = 0; off < r.t.P; ++off)
+        atomicMin(r.mark_id + r.mi(slot_of(sd, h, off)), (unsigned long long)mark_key(epoch, k));
+}
+
+// R4
+__device__ __forceinline__ void commit(const RoundsArgs& r, uint32_t k) {
+    const TableDev& t = r.t;
+    const uint64_t g = __ldcg(r.td_slot + k);
+    const uint8_t oc = ldcg_u8(r.td_oc + k);
+    if (oc == kInserted || oc == kEvicted) {
+        __stcg(t.ident + g, r.ids[r.upos[k]]);
+        t.row_gen[g] = r.gen_clock;
+    }
+    __stcg(t.meta + g, r.umeta[k]);
+    if (oc == kEvicted) {
+        if (t.dim) r.reset_rows[atomicAdd(&r.ctr->reset_count, 1u)] = g;
+        r.evflag[k] = 1;
+        r.evslot[k] = g;
+        atomicAdd(&r.ctr->evicted_count, 1u);
+    }
+    r.uslot[k] = g;
+    r.uoc[k] = oc;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_rounds(RoundsArgs r) {
+    cg::grid_group grid = cg::this_grid();
+    BatchCounters* ctr = r.ctr;
+    if (batch_failed(&ctr->err)) return;  // uniform: the error words are final before this kernel
+    const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     const unsigned u = ctr->entry_count;
-    for (unsigned x = blockIdx.x * blockDim.x + threadIdx.x; x < u; x += gridDim.x * blockDim.x) p[x] = x;
+    for (unsigned x = tid; x < u; x += nth) {
+        __stcg(r.pend[0] + x, x);
+        stcg_u8(r.susp + x, 0);
+        r.todo[x] = 0;
+    }
+    if (tid == 0) {
+        ctr->r_cnt[0] = u;
+        ctr->r_cnt[1] = 0;
+    }
+    grid.sync();
+    int round = 0;
+    unsigned npend = u;
+    for (; round < kMaxRounds; ++round) {
+        const int par = round & 1;
+        npend = ldcg_u32(&ctr->r_cnt[par]);
+        if (!npend) break;
+        const uint32_t epoch = r.epoch0 + round;
+        const uint32_t* pend = r.pend[par];
+        if (tid == 0) {
+            ctr->r_newc[0] = 0;
+            ctr->r_minrank = kNone32;
+        }
+        for (unsigned x = tid; x < npend; x += nth) tentative<MODE>(r, __ldcg(pend + x), epoch);
+        grid.sync();
+        if (tid == 0) ctr->r_cnt[par ^ 1] = 0;
+        for (int c = 0;; ++c) {  // suspicion closure: check and mark in one pass
+            const bool last = c == kClosureMax;
+            for (unsigned x = tid; x < npend; x += nth) {
+                const uint32_t k = __ldcg(pend + x);
+                if (ldcg_u8(r.susp + k) || !suspect<MODE>(r, k, epoch)) continue;
+                stcg_u8(r.susp + k, 1);
+                if (last) {
+                    atomicMin(&ctr->r_minrank, k);
+                } else {
+                    mark_window(r, k, epoch);
+                    atomicAdd(&ctr->r_newc[c & 1], 1u);
+                    atomicAdd(&ctr->r_marked, 1u);
+                }
+            }
+            grid.sync();
+            if (tid == 0) ++ctr->r_iters;
+            if (last || !ldcg_u32(&ctr->r_newc[c & 1])) break;
+            if (tid == 0) ctr->r_newc[(c + 1) & 1] = 0;
+        }
+        const uint32_t bound = ldcg_u32(&ctr->r_minrank);
+        uint32_t* next = r.pend[par ^ 1];
+        for (unsigned x = tid; x < npend; x += nth) {
+            const uint32_t k = __ldcg(pend + x);
+            if (ldcg_u8(r.susp + k) || k > bound) {
+                stcg_u8(r.susp + k, 0);
+                __stcg(next + atomicAdd(&ctr->r_cnt[par ^ 1], 1u), k);
+            } else {
+                commit(r, k);
+            }
+        }
+        grid.sync();
+    }
+    if (round == kMaxRounds) npend = ldcg_u32(&ctr->r_cnt[round & 1]);
+    else npend = 0;
+    const uint32_t* left = r.pend[round & 1];
+    for (unsigned x = tid; x < npend; x += nth) r.todo[__ldcg(left + x)] = 1;
+    if (tid == 0) {
+        ctr->r_left = npend;
+        ctr->r_rounds = round + (npend ? 1 : 0);
+    }
 }
 
-__global__ void k_flag_list(const uint32_t* list, unsigned cnt, uint8_t* flag) {
-    for (unsigned x = blockIdx.x * blockDim.x + threadIdx.x; x < cnt; x += gridDim.x * blockDim.x)
-        flag[list[x]] = 1;
-}
-
-__global__ void k_reset_round_ctr(BatchCounters* c) {
-    c->r_new = 0;
-    c->r_next = 0;
+template <int MODE>
+int rounds_grid(uint64_t n) {
+    static int max_blocks = 0;
+    if (!max_blocks) {
+        int dev = 0, sms = 0, per = 0;
+        MPZCH_CUDA(cudaGetDevice(&dev));
+        MPZCH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        MPZCH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_rounds<MODE>, 256, 0));
+        max_blocks = sms * std::max(per, 1);
+    }
+    const uint64_t want = std::max<uint64_t>(148, (n + 255) / 256);
+    return (int)std::min<uint64_t>(want, (uint64_t)max_blocks);
 }
 
 }  // namespace
 
-// Runs the rounds for the uniques prepared by enqueue_ordered_batch (host-synchronous: the
-// pending counts steer the loop).  Returns the number of uniques left for the ordered kernel,
-// flagged in `todo`.
-unsigned run_rounds(Table& t, const BatchArgs& a, cudaStream_t st, uint8_t* todo) {
+// Enqueues the rounds kernel for the uniques prepared by enqueue_ordered_batch (no host sync).
+// The uniques it leaves (if any) are flagged in `todo` and counted in BatchCounters::r_left.
+void enqueue_rounds(Table& t, const BatchArgs& a, cudaStream_t st, uint8_t* todo) {
     const Policy& p = *a.pol;
-    MPZCH_CUDA(cudaMemcpyAsync(t.h_ctr, t.d_ctr, sizeof(BatchCounters), cudaMemcpyDeviceToHost, st));
-    MPZCH_CUDA(cudaStreamSynchronize(st));
-    if (t.h_ctr->err.bad_pos != ~0ull || t.h_ctr->err.overflow || t.h_ctr->err.foreign_pos != ~0ull)
-        return 0;  // invalid batch: nothing runs, the host reports the error
-    const unsigned u = t.h_ctr->entry_count;
-    if (!u) return 0;
+    const uint64_t n = a.n;
     const uint64_t held = t.held_rows();
-    if (t.r_mark.bytes < held * 8) {
-        t.r_mark.reserve(held * 8);
-        MPZCH_CUDA(cudaMemsetAsync(t.r_mark.p, 0xff, held * 8, st));
+    uint64_t msize = 1024;
+    while (msize < held && msize < (1ull << 27)) msize <<= 1;
+    if (t.r_mark_mask != msize - 1 || t.mark_epoch > 0xffff0000u) {
+        t.r_mark_any.reserve(msize * 8);
+        t.r_mark_id.reserve(msize * 8);
+        MPZCH_CUDA(cudaMemsetAsync(t.r_mark_any.p, 0xff, msize * 8, st));
+        MPZCH_CUDA(cudaMemsetAsync(t.r_mark_id.p, 0xff, msize * 8, st));
+        t.r_mark_mask = msize - 1;
+        t.mark_epoch = 0;
     }
-    t.r_pend.reserve(u * 4ull);
-    t.r_next.reserve(u * 4ull);
-    t.r_new.reserve(u * 4ull);
-    t.r_slot.reserve(u * 8ull);
-    t.r_oc.reserve(u);
-    t.r_d.reserve(u * 4ull);
-    t.r_susp.reserve(u);
-    MPZCH_CUDA(cudaMemsetAsync(t.r_susp.p, 0, u, st));
-    unsigned long long* mark = t.r_mark.as<unsigned long long>();
-    const uint64_t mb = t.row_lo;
-    uint32_t* pend = t.r_pend.as<uint32_t>();
-    uint32_t* next = t.r_next.as<uint32_t>();
-    const unsigned B = 256;
-    k_iota<<<grid_for(u, B), B, 0, st>>>(pend, t.d_ctr);
+    t.r_pend.reserve(n * 4);
+    t.r_next.reserve(n * 4);
+    t.r_slot.reserve(n * 8);
+    t.r_oc.reserve(n);
+    t.r_d.reserve(n * 4);
+    t.r_susp.reserve(n);
+    RoundsArgs r;
+    r.t = t.dev;
+    r.ctr = t.d_ctr;
+    r.ids = a.ids;
+    r.upos = t.o_upos.as<uint32_t>();
+    r.ushard = t.o_ushard.as<uint32_t>();
+    r.umeta = t.o_umeta.as<uint64_t>();
+    r.now = a.now;
+    r.gen_clock = t.gen_clock;
+    r.epoch0 = t.mark_epoch + 1;
+    t.mark_epoch += kMaxRounds;
+    r.pend[0] = t.r_pend.as<uint32_t>();
+    r.pend[1] = t.r_next.as<uint32_t>();
+    r.td_slot = t.r_slot.as<uint64_t>();
+    r.td_oc = t.r_oc.as<uint8_t>();
+    r.td_d = t.r_d.as<uint32_t>();
+    r.susp = t.r_susp.as<uint8_t>();
+    r.todo = todo;
+    r.mark_any = t.r_mark_any.as<unsigned long long>();
+    r.mark_id = t.r_mark_id.as<unsigned long long>();
+    r.mark_base = t.row_lo;
+    r.mark_mask = t.r_mark_mask;
+    r.uslot = t.o_uslot.as<uint64_t>();
+    r.uoc = t.o_uoc.as<uint8_t>();
+    r.reset_rows = t.s_reset.as<uint64_t>();
+    r.evflag = t.s_evflag.as<uint8_t>();
+    r.evslot = t.s_evslot.as<uint64_t>();
+    void* args[] = {&r};
+    const dim3 block(256);
+#define MPZCH_ROUNDS(MODE) \
+    MPZCH_CUDA(cudaLaunchCooperativeKernel((void*)k_rounds<MODE>, dim3(rounds_grid<MODE>(n)), block, args, 0, st))
+    if (p.mode == kModeTtl) MPZCH_ROUNDS(kModeTtl);
+    else if (p.mode == kModeLru) MPZCH_ROUNDS(kModeLru);
+    else MPZCH_ROUNDS(kModeDisabled);
+#undef MPZCH_ROUNDS
     ++t.launches;
-    unsigned npend = u;
-    const uint64_t* ids = a.ids;
-    const uint32_t* upos = t.o_upos.as<uint32_t>();
-    const uint32_t* ushard = t.o_ushard.as<uint32_t>();
-    const uint64_t* umeta = t.o_umeta.as<uint64_t>();
-    for (int round = 0; round < kMaxRounds && npend; ++round) {
-        const uint32_t epoch = ++t.mark_epoch;
-        const unsigned g = grid_for(npend, B);
-        k_reset_round_ctr<<<1, 1, 0, st>>>(t.d_ctr);
-#define MPZCH_TENT(MODE)                                                                           \
-    k_tentative<MODE><<<g, B, 0, st>>>(t.dev, t.d_ctr, ids, upos, ushard, pend, npend, a.now, epoch, \
-                                       t.r_slot.as<uint64_t>(), t.r_oc.as<uint8_t>(),              \
-                                       t.r_d.as<uint32_t>(), mark, mb)
-        if (p.mode == kModeTtl) MPZCH_TENT(kModeTtl);
-        else if (p.mode == kModeLru) MPZCH_TENT(kModeLru);
-        else MPZCH_TENT(kModeDisabled);
-#undef MPZCH_TENT
-        t.launches += 2;
-        for (;;) {  // suspicion closure
-            MPZCH_CUDA(cudaMemsetAsync(&t.d_ctr->r_new, 0, sizeof(unsigned), st));
-            k_check<<<g, B, 0, st>>>(t.dev, t.d_ctr, ids, upos, ushard, pend, npend, epoch,
-                                     t.r_d.as<uint32_t>(), t.r_susp.as<uint8_t>(), mark, mb,
-                                     t.r_new.as<uint32_t>());
-            ++t.launches;
-            unsigned nn = 0;
-            MPZCH_CUDA(cudaMemcpyAsync(&nn, &t.d_ctr->r_new, 4, cudaMemcpyDeviceToHost, st));
-            MPZCH_CUDA(cudaStreamSynchronize(st));
-            if (!nn) break;
-            k_mark_windows<<<grid_for(nn, B), B, 0, st>>>(t.dev, t.d_ctr, ids, upos, ushard,
-                                                          t.r_new.as<uint32_t>(), nn, epoch, mark, mb);
-            ++t.launches;
-        }
-        k_commit_round<<<g, B, 0, st>>>(t.dev, t.d_ctr, ids, upos, umeta, pend, npend,
-                                        t.r_susp.as<uint8_t>(), t.r_slot.as<uint64_t>(),
-                                        t.r_oc.as<uint8_t>(), t.gen_clock, t.o_uslot.as<uint64_t>(),
-                                        t.o_uoc.as<uint8_t>(), t.s_reset.as<uint64_t>(),
-                                        t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>(), next);
-        ++t.launches;
-        MPZCH_CUDA(cudaMemcpyAsync(&npend, &t.d_ctr->r_next, 4, cudaMemcpyDeviceToHost, st));
-        MPZCH_CUDA(cudaStreamSynchronize(st));
-        std::swap(pend, next);
-        ++t.last_rounds;
-    }
-    if (npend) {  // the remainder goes to the per-shard ordered kernel
-        MPZCH_CUDA(cudaMemsetAsync(todo, 0, u, st));
-        k_flag_list<<<grid_for(npend, B), B, 0, st>>>(pend, npend, todo);
-        ++t.launches;
-    }
-    return npend;
 }
 
 }  // namespace mpzch_b200

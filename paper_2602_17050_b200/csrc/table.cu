@@ -316,7 +316,10 @@ void complete_slot(Table& t, int si) {
         s.collision = c.collision;
         s.evicted_rows = c.evicted_count;
         s.path = sl.path;
-        s.rounds = sl.rounds;
+        s.rounds = sl.path == MPZCH_PATH_ROUNDS ? c.r_rounds : 0;
+        if (sl.path == MPZCH_PATH_ROUNDS && getenv("MPZCH_DEBUG_ROUNDS"))
+            fprintf(stderr, "rounds u=%u rounds=%u iters=%u marked=%u left=%u\n", c.entry_count,
+                    c.r_rounds, c.r_iters, c.r_marked, c.r_left);
         if (sl.profiled && sl.fast) {
             float a01 = 0, a12 = 0, a23 = 0, a03 = 0, k70 = 0, k14 = 0, k45 = 0, k52 = 0, k26 = 0;
             MPZCH_CUDA(cudaEventElapsedTime(&a01, sl.ev[0], sl.ev[1]));
@@ -429,7 +432,6 @@ uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uin
     const bool rounds = !fast && t.hole_free && t.path_override != MPZCH_PATH_ORDERED;
     const bool profiled = t.profiling;
     if (!fast) t.profiling = false;  // events are recorded by the fast path only
-    t.last_rounds = 0;
     if (fast) enqueue_fast_batch(t, a, st);
     else enqueue_ordered_batch(t, a, st, rounds);
     t.profiling = profiled;
@@ -441,7 +443,6 @@ uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uin
     sl.n = n;
     sl.fast = fast;
     sl.path = fast ? MPZCH_PATH_AUTO : (rounds ? MPZCH_PATH_ROUNDS : MPZCH_PATH_ORDERED);
-    sl.rounds = (uint32_t)t.last_rounds;
     sl.overflow_all = a.overflow_all;
     sl.profiled = profiled;
     t.last_stream = st;

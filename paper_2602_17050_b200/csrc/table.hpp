@@ -53,7 +53,11 @@ struct BatchCounters {
     unsigned int overflow_list;  // claim-log overflow (defensive)
     unsigned int pad;
     unsigned long long id_sectors, meta_sectors;  // sectors the probe kernel read
-    unsigned int r_new, r_next;  // rounds path: new suspects / next pending
+    // rounds path (device-driven): pending count per round parity, new suspects per closure
+    // step parity, lowest rank among the unmarked last-step suspects, rounds run, uniques left
+    // for the ordered kernel
+    unsigned int r_cnt[2], r_newc[2], r_minrank, r_rounds, r_left, r_iters;
+    unsigned int r_marked, r_checked;  // closure steps / windows marked / range checks (diagnostics)
 };
 
 struct Policy {
@@ -150,10 +154,10 @@ public:
     // ordered path
     DevBuf o_key, o_min, o_posent, o_flag, o_upos, o_entu, o_ushard, o_umeta, o_uslot, o_uoc, o_todo;
     uint64_t ocap = 0;
-    // rounds path: epoch-keyed reservation marks (one word per held row)
-    DevBuf r_mark, r_pend, r_next, r_new, r_slot, r_oc, r_d, r_susp;
+    // rounds path: epoch-keyed reservation marks (<= 2^27 words each, aliased)
+    DevBuf r_mark_any, r_mark_id, r_pend, r_next, r_slot, r_oc, r_d, r_susp;
+    uint64_t r_mark_mask = 0;  // mark arrays alias slots modulo their size (sound: more suspects)
     uint32_t mark_epoch = 0;
-    uint64_t last_rounds = 0;  // rounds run by the last rounds-path batch
 
     void ensure_fast_scratch(uint64_t n);
     void ensure_ordered_scratch(uint64_t n);
@@ -193,7 +197,7 @@ struct BatchArgs {
 // enqueue the whole batch; counters land in t.h_ctr after the stream syncs
 void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st);
 void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st, bool rounds = false);
-unsigned run_rounds(Table& t, const BatchArgs& a, cudaStream_t st, uint8_t* todo);
+void enqueue_rounds(Table& t, const BatchArgs& a, cudaStream_t st, uint8_t* todo);
 void enqueue_compact_evicted(Table& t, uint64_t n, uint64_t* out_ev, uint64_t ev_cap, cudaStream_t st);
 void run_route(Table& t, const uint64_t* ids, uint64_t n, const uint32_t* shard_to_part,
                uint32_t parts, uint32_t* perm, uint64_t* counts, cudaStream_t st);
