@@ -243,6 +243,21 @@ mpzch_status mpzch_delta_cut(mpzch_table* t, uint64_t generation, uint64_t* out_
                              uint64_t* out_identities, float* out_weights, uint64_t cap,
                              uint64_t* out_n, uint64_t* out_next_generation);
 
+/* sgd_step: MpzchTable::sgd_step (proj/src/table.cpp:174-179) over
+ * EmbeddingTable::sgd_step (proj/src/embedding_store.cpp:70-93).  For i = 0..n-1 in order:
+ * momentum[rows[i]] := beta*momentum + grads[i]; weights[rows[i]] -= lr*momentum (fp32,
+ * separately rounded), trained := 1; then every row is stamped dirty.  grads is n x dim,
+ * row-major; n_grads = its element count.  Errors in the reference's order: dim 0 ->
+ * MPZCH_ELOGIC; n_grads != n*dim, !(lr > 0), beta outside [0, 1) -> MPZCH_EINVAL; a row out of
+ * range -> MPZCH_ERANGE after the rows before it were updated (none stamped).  Repeated rows
+ * compound in position order.  _device: rows/grads in device memory, enqueued on `stream`
+ * (0 = legacy default stream) after this handle's pending batches; returns when done. */
+mpzch_status mpzch_sgd_step(mpzch_table* t, const uint64_t* rows, uint64_t n, const float* grads,
+                            uint64_t n_grads, float lr, float beta);
+mpzch_status mpzch_sgd_step_device(mpzch_table* t, const uint64_t* rows, uint64_t n,
+                                   const float* grads, uint64_t n_grads, float lr, float beta,
+                                   void* stream);
+
 /* ---- execution control / introspection */
 mpzch_status mpzch_set_path(mpzch_table* t, int path);
 mpzch_status mpzch_last_stats(const mpzch_table* t, mpzch_batch_stats* out);

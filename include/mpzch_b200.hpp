@@ -22,6 +22,7 @@
 #include <string>
 #include <unordered_map>
 #include <utility>
+#include <span>
 #include <vector>
 
 #include "mpzch_b200.h"
@@ -233,6 +234,15 @@ public:
         return w;
     }
 
+    // MpzchTable::gather (proj/src/table.cpp:158-163): row-major copy of the requested rows
+    std::vector<float> gather(std::span<const std::uint64_t> rows) const {
+        if (dim_ == 0) throw std::logic_error("table has no embedding payload (dim = 0)");
+        std::vector<float> out(rows.size() * dim_);
+        for (std::size_t i = 0; i < rows.size(); ++i)
+            check(mpzch_copy_weights(t_, rows[i], 1, out.data() + i * dim_));
+        return out;
+    }
+
     std::vector<float> momentum_row(std::uint64_t r) const {
         std::vector<float> m(dim_);
         check(mpzch_copy_momentum(t_, r, 1, m.data()));
@@ -245,6 +255,12 @@ public:
         check(mpzch_copy_trained(t_, t.data()));
         if (r >= t.size()) throw std::out_of_range("embedding row out of range");
         return t[r] != 0;
+    }
+
+    // MpzchTable::sgd_step (proj/src/table.cpp:174-179)
+    void sgd_step(std::span<const std::uint64_t> rows, std::span<const float> grads, float lr,
+                  float beta) {
+        check(mpzch_sgd_step(t_, rows.data(), rows.size(), grads.data(), grads.size(), lr, beta));
     }
 
     PublishCursor make_cursor() {

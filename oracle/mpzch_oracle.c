@@ -186,6 +186,34 @@ uint64_t* orc_row_generation(orc_table* t) { return t->row_gen; }
 /* MpzchTable::make_cursor proj/src/table.cpp:209-214 */
 uint64_t orc_make_cursor(orc_table* t) { return t->gen_clock++; }
 
+/* MpzchTable::sgd_step, proj/src/table.cpp:174-179 -> embedding_store.cpp:70-93 */
+int orc_sgd_step(orc_table* t, const uint64_t* rows, uint64_t n, const float* grads,
+                 uint64_t n_grads, float lr, float beta) {
+    /* check_embeddings, table.cpp:94-96 (check_mutable: no frozen replicas here) */
+    if (t->dim == 0) return fail(ORC_ELOGIC, "table has no embedding payload (dim = 0)");
+    /* embedding_store.cpp:72-81 */
+    if (n_grads != n * t->dim)
+        return fail(ORC_EINVAL, "gradient shape does not match rows * dim");
+    if (!(lr > 0.0f)) return fail(ORC_EINVAL, "learning rate must be positive");
+    if (beta < 0.0f || beta >= 1.0f)
+        return fail(ORC_EINVAL, "momentum coefficient must lie in [0, 1)");
+    for (uint64_t i = 0; i < n; ++i) { /* embedding_store.cpp:82-92 */
+        if (rows[i] >= t->total) return fail(ORC_ERANGE, "embedding row out of range");
+        float* w = t->weights + rows[i] * t->dim;
+        float* m = t->momentum + rows[i] * t->dim;
+        const float* g = grads + i * t->dim;
+        for (uint32_t j = 0; j < t->dim; ++j) {
+            volatile float bm = beta * m[j]; /* x86-64 baseline: no FMA contraction */
+            m[j] = bm + g[j];
+            volatile float lm = lr * m[j];
+            w[j] = w[j] - lm;
+        }
+        t->trained[rows[i]] = 1;
+    }
+    for (uint64_t i = 0; i < n; ++i) t->row_gen[rows[i]] = t->gen_clock; /* table.cpp:179 */
+    return ORC_OK;
+}
+
 void orc_copy_identities(const orc_table* t, uint64_t* out) {
     memcpy(out, t->ident, sizeof(uint64_t) * t->total);
 }

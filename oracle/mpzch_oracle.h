@@ -104,6 +104,13 @@ float* orc_momentum(orc_table* t);
 uint8_t* orc_trained(orc_table* t);
 uint64_t* orc_row_generation(orc_table* t);
 uint64_t orc_make_cursor(orc_table* t);
+/* MpzchTable::sgd_step (proj/src/table.cpp:174-179) over EmbeddingTable::sgd_step
+ * (proj/src/embedding_store.cpp:70-93): momentum := beta*momentum + grad,
+ * weights := weights - lr*momentum (fp32, separately rounded), trained := 1, in position
+ * order; then touch_row for every row.  A row out of range throws after the rows before it
+ * were updated (and before any touch). */
+int orc_sgd_step(orc_table* t, const uint64_t* rows, uint64_t n, const float* grads,
+                 uint64_t n_grads, float lr, float beta);
 
 /* copies of the state (same entry points exist in oracle/_ref, prefix ref_) */
 void orc_copy_identities(const orc_table* t, uint64_t* out);

@@ -85,6 +85,8 @@ def lib(kind: str = "port"):
         "copy_momentum": (None, [_vp, _vp]),
         "copy_trained": (None, [_vp, _vp]),
         "make_cursor": (ctypes.c_uint64, [_vp]),
+        "sgd_step": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _vp, ctypes.c_uint64, ctypes.c_float,
+                                    ctypes.c_float]),
         "dirty_rows_since": (ctypes.c_int, [_vp, ctypes.c_uint64, _vp, ctypes.c_uint64, _u64p]),
         "last_error": (ctypes.c_char_p, []),
     }
@@ -210,6 +212,11 @@ class OracleTable:
 
     def make_cursor(self):
         return int(self.L["make_cursor"](self.h))
+
+    def sgd_step(self, rows, grads, lr, beta):
+        rows = np.ascontiguousarray(rows, dtype=np.uint64)
+        g = np.ascontiguousarray(grads, dtype=np.float32).reshape(-1)
+        _raise(self.L, self.L["sgd_step"](self.h, _ptr(rows), rows.size, _ptr(g), g.size, lr, beta))
 
     def dirty_rows_since(self, cursor):
         out = np.empty(self.total_rows, dtype=np.uint64)

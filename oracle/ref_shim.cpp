@@ -15,6 +15,7 @@
 #include <cstring>
 #include <memory>
 #include <new>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -292,6 +293,17 @@ std::uint64_t ref_make_cursor(RefTable* t) {
     if (t->cursors.size() <= c.generation) t->cursors.resize(c.generation + 1);
     t->cursors[c.generation] = c;
     return c.generation;
+}
+
+int ref_sgd_step(RefTable* t, const std::uint64_t* rows, std::uint64_t n, const float* grads,
+                 std::uint64_t n_grads, float lr, float beta) {
+    try {
+        t->table.sgd_step(std::span<const std::uint64_t>(rows, n),
+                          std::span<const float>(grads, n_grads), lr, beta);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
 }
 
 int ref_dirty_rows_since(const RefTable* t, std::uint64_t cursor, std::uint64_t* out,

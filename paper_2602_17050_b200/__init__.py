@@ -169,6 +169,10 @@ _SIGS = {
     "mpzch_lookup_gather_device": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _vp, _vp, _vp, _vp]),
     "mpzch_delta_cut": (ctypes.c_int, [_vp, ctypes.c_uint64, _vp, _vp, _vp, ctypes.c_uint64, _u64p,
                                        _u64p]),
+    "mpzch_sgd_step": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _vp, ctypes.c_uint64, ctypes.c_float,
+                                      ctypes.c_float]),
+    "mpzch_sgd_step_device": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _vp, ctypes.c_uint64,
+                                             ctypes.c_float, ctypes.c_float, _vp]),
     "mpzch_set_path": (ctypes.c_int, [_vp, ctypes.c_int]),
     "mpzch_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),
     "mpzch_get_profile": (ctypes.c_int, [_vp, ctypes.POINTER(_Profile)]),
@@ -543,6 +547,21 @@ class MpzchTable:
         w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float32)
         m = None if momentum is None else np.ascontiguousarray(momentum, dtype=np.float32)
         _check(self._lib.mpzch_write_row(self._h, row, _ptr(w), _ptr(m), trained))
+
+    def sgd_step(self, rows, grads, lr: float, beta: float):
+        """MpzchTable::sgd_step (table.cpp:174-179) with host arrays: rows[n], grads[n, dim]."""
+        r = np.ascontiguousarray(rows, dtype=np.uint64)
+        g = np.ascontiguousarray(grads, dtype=np.float32).reshape(-1)
+        _check(self._lib.mpzch_sgd_step(self._h, _ptr(r), r.size, _ptr(g), g.size, lr, beta))
+
+    def sgd_step_device(self, rows, grads, lr: float, beta: float, stream=None):
+        """sgd_step on device tensors (rows int64 [n], grads float32 [n, dim]), stream-ordered."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        g = grads.contiguous()
+        _check(self._lib.mpzch_sgd_step_device(
+            self._h, ctypes.c_void_p(rows.data_ptr()), rows.numel(), ctypes.c_void_p(g.data_ptr()),
+            g.numel(), lr, beta, ctypes.c_void_p(st.cuda_stream)))
 
     def lookup_gather_device(self, ids, stream=None):
         """Fused lookup + gather: (slots, outcomes, rows[n, dim]) device tensors."""

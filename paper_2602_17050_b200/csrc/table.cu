@@ -919,6 +919,63 @@ mpzch_status mpzch_write_row(mpzch_table* t, uint64_t row, const float* w, const
     });
 }
 
+// EmbeddingTable::sgd_step argument checks in the reference's order (table.cpp:174-178,
+// embedding_store.cpp:70-81); the per-row range check happens on the device
+static void check_sgd_args(const Table& T, uint64_t n, uint64_t n_grads, float lr, float beta) {
+    if (T.dim == 0) throw Error{MPZCH_ELOGIC, "table has no embedding payload (dim = 0)"};
+    if (n_grads != n * T.dim) throw Error{MPZCH_EINVAL, "gradient shape does not match rows * dim"};
+    if (!(lr > 0.0f)) throw Error{MPZCH_EINVAL, "learning rate must be positive"};
+    if (beta < 0.0f || beta >= 1.0f)
+        throw Error{MPZCH_EINVAL, "momentum coefficient must lie in [0, 1)"};
+}
+
+// a stream that is not the one the handle's last batch ran on waits for that batch
+static void order_after_last_batch(Table& T, cudaStream_t st) {
+    if (T.last_ticket && st != T.last_stream) {
+        const Table::Slot& prev = T.slots[T.last_ticket % Table::kRing];
+        if (prev.busy && prev.ticket == T.last_ticket) MPZCH_CUDA(cudaStreamWaitEvent(st, prev.done, 0));
+    }
+}
+
+static void sgd_common(Table& T, const uint64_t* d_rows, uint64_t n, const float* d_grads, float lr,
+                       float beta, cudaStream_t st) {
+    const uint64_t bad = run_sgd_step(T, d_rows, n, d_grads, lr, beta, st);
+    if (bad != ~0ull) throw Error{MPZCH_ERANGE, "embedding row out of range"};
+}
+
+mpzch_status mpzch_sgd_step(mpzch_table* t, const uint64_t* rows, uint64_t n, const float* grads,
+                            uint64_t n_grads, float lr, float beta) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        check_sgd_args(T, n, n_grads, lr, beta);
+        if (n == 0) return;
+        DeviceGuard g(T.device);
+        cudaStream_t st = T.stream;
+        order_after_last_batch(T, st);
+        T.s_ids.reserve(n * 8);
+        T.s_grads.reserve(n_grads * 4);
+        MPZCH_CUDA(cudaMemcpyAsync(T.s_ids.p, rows, n * 8, cudaMemcpyHostToDevice, st));
+        MPZCH_CUDA(cudaMemcpyAsync(T.s_grads.p, grads, n_grads * 4, cudaMemcpyHostToDevice, st));
+        sgd_common(T, T.s_ids.as<uint64_t>(), n, T.s_grads.as<float>(), lr, beta, st);
+    });
+}
+
+mpzch_status mpzch_sgd_step_device(mpzch_table* t, const uint64_t* rows, uint64_t n,
+                                   const float* grads, uint64_t n_grads, float lr, float beta,
+                                   void* stream) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        check_sgd_args(T, n, n_grads, lr, beta);
+        if (n == 0) return;
+        DeviceGuard g(T.device);
+        cudaStream_t st = (cudaStream_t)stream;
+        order_after_last_batch(T, st);
+        sgd_common(T, rows, n, grads, lr, beta, st);
+    });
+}
+
 mpzch_status mpzch_make_cursor(mpzch_table* t, uint64_t* out_generation) {
     CHECK_T(t);
     *out_generation = t->t->gen_clock++;  // MpzchTable::make_cursor, table.cpp:209-214

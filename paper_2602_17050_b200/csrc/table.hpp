@@ -60,6 +60,12 @@ struct BatchCounters {
     unsigned int r_marked, r_checked;  // closure steps / windows marked / range checks (diagnostics)
 };
 
+// sgd_step scratch counters (train.cu)
+struct SgdCounters {
+    unsigned long long bad;  // first out-of-range position (~0: none)
+    unsigned dup, dup_total, dup_entries, pad;
+};
+
 struct Policy {
     int mode = 0;
     uint64_t default_ttl = 0;
@@ -151,6 +157,7 @@ public:
     DevBuf s_evflag, s_evslot, s_blk;                // evicted-list compaction
     DevBuf s_ids, s_feats, s_oslot, s_ooc, s_oev;    // staging for host-buffer calls
     DevBuf s_featk, s_featv;                         // per-feature TTL map
+    DevBuf s_grads;                                  // staging for host-buffer sgd_step
     // ordered path
     DevBuf o_key, o_min, o_posent, o_flag, o_upos, o_entu, o_ushard, o_umeta, o_uslot, o_uoc, o_todo;
     uint64_t ocap = 0;
@@ -158,6 +165,9 @@ public:
     DevBuf r_mark_any, r_mark_id, r_pend, r_next, r_slot, r_oc, r_d, r_susp;
     uint64_t r_mark_mask = 0;  // mark arrays alias slots modulo their size (sound: more suspects)
     uint32_t mark_epoch = 0;
+    // sgd_step (train.cu): row hash, occurrence lists
+    DevBuf g_key, g_cnt, g_base, g_pe, g_pr, g_list, g_dupent, g_ctr;
+    uint64_t g_cap = 0;
 
     void ensure_fast_scratch(uint64_t n);
     void ensure_ordered_scratch(uint64_t n);
@@ -173,6 +183,9 @@ void run_lookup(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_s
                 uint8_t* out_oc, BatchErr* err, cudaStream_t st);
 void run_lookup_gather(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots,
                        uint8_t* out_oc, float* out_rows, BatchErr* err, cudaStream_t st);
+// returns the first out-of-range position (~0 if none); synchronous on st
+uint64_t run_sgd_step(Table& t, const uint64_t* rows, uint64_t n, const float* grads, float lr,
+                      float beta, cudaStream_t st);
 void run_gather_rows(const Table& t, const uint64_t* rows, uint64_t n, uint64_t* out_ids,
                      float* out_w, cudaStream_t st);
 

@@ -6,6 +6,7 @@
 // and tests/test_gpu_cpp.py runs it.
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -65,6 +66,7 @@ Trace run(std::uint64_t seed, int mode) {
                                                 : NS::Policy::ttl(ttl);
     mpzch::DistinctIdStream ids(rng.next());
     std::uint64_t now = 1;
+    std::vector<std::uint64_t> last_rows;
     for (int b = 0; b < 25; ++b) {
         now += rng.next_below(5);
         typename NS::Batch batch;
@@ -73,7 +75,9 @@ Trace run(std::uint64_t seed, int mode) {
         for (std::uint64_t k = 0; k < len; ++k)
             batch.ids.push_back({ids.at(rng.next_below(1500)), static_cast<std::uint32_t>(rng.next_below(3))});
         try {
+            last_rows.clear();
             for (const auto& r : NS::pb(table, batch, pol)) {
+                last_rows.push_back(r.slot);
                 tr.out.push_back(r.slot);
                 tr.out.push_back(r.evicted);
                 tr.out.push_back(static_cast<std::uint64_t>(r.outcome));
@@ -83,6 +87,30 @@ Trace run(std::uint64_t seed, int mode) {
             return tr;
         }
     }
+    // a training step on the last batch's rows (repeated rows compound in order), its dirty
+    // set, and a step that fails on its second row after updating the first
+    auto bits = [&tr](float f) {
+        std::uint32_t u;
+        std::memcpy(&u, &f, 4);
+        tr.out.push_back(u);
+    };
+    std::vector<float> grads(last_rows.size() * table.dim());
+    for (float& g : grads) g = static_cast<float>(rng.next_unit() - 0.5);
+    const auto cursor = table.make_cursor();
+    table.sgd_step(last_rows, grads, 0.05f, 0.9f);
+    for (float v : table.gather(last_rows)) bits(v);
+    for (std::uint64_t r : last_rows) {
+        for (float v : table.momentum_row(r)) bits(v);
+        tr.out.push_back(table.row_trained(r));
+    }
+    for (auto r : table.dirty_rows_since(cursor)) tr.out.push_back(r);
+    const std::vector<std::uint64_t> bad_rows = {last_rows[0], table.total_rows()};
+    try {
+        table.sgd_step(bad_rows, std::vector<float>(2 * table.dim(), 0.25f), 0.1f, 0.5f);
+    } catch (const std::out_of_range& e) {
+        tr.out.push_back(0xE77);
+    }
+    for (float v : table.gather(std::vector<std::uint64_t>{last_rows[0]})) bits(v);
     for (std::uint32_t s = 0; s < table.num_shards(); ++s) {
         for (auto v : NS::ident(table, s)) tr.out.push_back(v);
         for (auto v : NS::meta(table, s)) tr.out.push_back(v);

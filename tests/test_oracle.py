@@ -165,3 +165,72 @@ def test_port_error_order(oracle):
         t.process_batch(np.array([1], dtype=np.uint64), (1 << 64) - 6, 1, 1000)
     assert e.value.code == 2
     assert (t.identities_all() == np.uint64((1 << 64) - 1)).all()
+
+
+# ------------------------------------------------------------------ sgd_step
+
+def test_sgd_known_answers(oracle):
+    """proj/tests/test_embedding.cpp:55-99 and :122-134 on MpzchTable (same row draws)."""
+    for kind in _kinds(oracle):
+        t = oracle.OracleTable([4], 1, 0, dim=2, init_seed=1, kind=kind)
+        w0 = t.weights()[2].copy()
+        t.sgd_step(np.array([2], np.uint64), np.array([[1.0, -2.0]], np.float32), 0.5, 0.5)
+        assert t.momentum()[2].tolist() == [1.0, -2.0]
+        assert np.allclose(t.weights()[2], w0 - np.array([0.5, -1.0], np.float32))
+        assert t.trained().tolist() == [0, 0, 1, 0]
+        t.sgd_step(np.array([2], np.uint64), np.array([[2.0, 2.0]], np.float32), 0.5, 0.5)
+        assert t.momentum()[2].tolist() == [2.5, 1.0]
+        assert np.allclose(t.weights()[2], w0 - np.array([0.5 + 1.25, -1.0 + 0.5], np.float32))
+        good = np.zeros((1, 2), np.float32)
+        one = np.array([0], np.uint64)
+        for args, code in [((one, np.zeros((1, 3), np.float32), 0.1, 0.0), 1),
+                           ((one, good, 0.0, 0.0), 1), ((one, good, -1.0, 0.0), 1),
+                           ((one, good, float("nan"), 0.0), 1),
+                           ((one, good, 0.1, 1.0), 1), ((one, good, 0.1, -0.1), 1),
+                           ((np.array([4], np.uint64), good, 0.1, 0.0), 5)]:
+            with pytest.raises(oracle.OracleError) as e:
+                t.sgd_step(*args)
+            assert e.value.code == code
+        nodim = oracle.OracleTable([4], 1, 0, kind=kind)
+        with pytest.raises(oracle.OracleError) as e:
+            nodim.sgd_step(one, np.zeros((1, 0), np.float32), 0.1, 0.0)
+        assert e.value.code == 4
+
+
+def test_sgd_port_vs_reference_live(oracle):
+    """Training steps interleaved with TTL batches (resets), repeated rows, and steps that fail
+    part-way: port and reference agree bit for bit, dirty sets included."""
+    if not oracle.available("reference"):
+        pytest.skip("oracle/_ref not built (no /root/reference here)")
+    rng = np.random.default_rng(11)
+    for trial in range(12):
+        caps = list(rng.integers(8, 60, size=int(rng.integers(1, 4))))
+        dim = int(rng.choice([1, 3, 4, 8]))
+        seed = int(rng.integers(0, 2**63))
+        T = [oracle.OracleTable(caps, 4, seed, dim, 5, kind=k) for k in ("port", "reference")]
+        total = sum(caps)
+        now = 1
+        for step in range(10):
+            now += 3
+            ids = rng.integers(0, total * 2, size=int(rng.integers(1, 50))).astype(np.uint64)
+            res = [t.process_batch(ids, now, 1, 4) for t in T]
+            assert all((x == y).all() for x, y in zip(res[0], res[1]))
+            rows = res[0][0].copy()
+            if step % 4 == 3:
+                rows[rng.integers(0, rows.size)] = total + 1  # fails part-way
+            g = (rng.random((rows.size, dim)) - 0.5).astype(np.float32)
+            lr, beta = float(rng.choice([0.01, 0.5])), float(rng.choice([0.0, 0.9]))
+            cur = [t.make_cursor() for t in T]
+            errs = []
+            for t in T:
+                try:
+                    t.sgd_step(rows, g, lr, beta)
+                    errs.append(0)
+                except oracle.OracleError as e:
+                    errs.append(e.code)
+            assert errs[0] == errs[1]
+            a, b = T
+            assert (a.weights().view(np.uint32) == b.weights().view(np.uint32)).all()
+            assert (a.momentum().view(np.uint32) == b.momentum().view(np.uint32)).all()
+            assert (a.trained() == b.trained()).all()
+            assert (a.dirty_rows_since(cur[0]) == b.dirty_rows_since(cur[1])).all()
