@@ -120,13 +120,21 @@ void run_route(Table& t, const uint64_t* ids, uint64_t n, const uint32_t* shard_
     for (uint32_t s = 0; s < t.S; ++s)
         if (shard_to_part[s] >= parts) throw Error{MPZCH_EINVAL, "route: shard mapped to no part"};
     const uint64_t nchunks = (n + kChunk - 1) / kChunk;
-    DevBuf s2p, cnt, tot;
+    // per-handle scratch (a temporary allocation would cudaFree -- a device sync -- per call);
+    // the shard->part map is uploaded only when it changes
+    DevBuf& s2p = t.rt_s2p;
+    DevBuf& cnt = t.rt_cnt;
+    DevBuf& tot = t.rt_tot;
     s2p.reserve(t.S);
     cnt.reserve(std::max<uint64_t>(1, nchunks * parts) * 4);
     tot.reserve(parts * 4);
     std::vector<uint8_t> h(t.S);
     for (uint32_t s = 0; s < t.S; ++s) h[s] = (uint8_t)shard_to_part[s];
-    MPZCH_CUDA(cudaMemcpyAsync(s2p.p, h.data(), t.S, cudaMemcpyHostToDevice, st));
+    if (h != t.rt_map) {
+        MPZCH_CUDA(cudaMemcpyAsync(s2p.p, h.data(), t.S, cudaMemcpyHostToDevice, st));
+        MPZCH_CUDA(cudaStreamSynchronize(st));  // h is pageable and about to go out of scope
+        t.rt_map = h;
+    }
     std::vector<unsigned> ht(parts, 0);
     if (n) {
         const unsigned blocks = (unsigned)((nchunks * 32 + 255) / 256);

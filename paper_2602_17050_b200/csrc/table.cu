@@ -49,13 +49,25 @@ struct DeviceGuard {
     }
 };
 
+// Resets the synchronous helpers' error block on the device: a pageable host->device copy
+// would first wait for everything already queued on the stream.
+__global__ void k_init_err(BatchErr* e) { *e = BatchErr{~0ull, 0, 0, ~0ull}; }
+static void init_aux_err(Table& T, cudaStream_t st) {
+    k_init_err<<<1, 1, 0, st>>>(&T.d_aux->err);
+    ++T.launches;
+}
+
+// Grows geometrically (x1.5, 1 MiB granules): scratch sized by batch length must not be
+// reallocated -- cudaFree synchronises the device -- every time the length creeps up.
 void DevBuf::reserve(size_t want) {
     if (want <= bytes) return;
+    size_t grow = std::max(want, bytes + bytes / 2);
+    if (grow > (1u << 20)) grow = (grow + (1u << 20) - 1) & ~((size_t)(1u << 20) - 1);
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
-    MPZCH_CUDA(cudaMalloc(&p, want));
-    bytes = want;
+    MPZCH_CUDA(cudaMalloc(&p, grow));
+    bytes = grow;
 }
 
 DevBuf::~DevBuf() {
@@ -184,9 +196,9 @@ void Table::ensure_fast_scratch(uint64_t n) {
     }
     s_reset.reserve(n * 8);
     const size_t fl = ((n + 15) & ~15ull) + 16;
-    if (s_evflag.bytes < fl) {
+    if (s_evflag.bytes < fl) {  // zero the whole allocation: it may exceed fl
         s_evflag.reserve(fl);
-        MPZCH_CUDA(cudaMemsetAsync(s_evflag.p, 0, fl, stream));
+        MPZCH_CUDA(cudaMemsetAsync(s_evflag.p, 0, s_evflag.bytes, stream));
     }
     s_evslot.reserve(n * 8);
     s_blk.reserve(((n + kCompactChunk - 1) / kCompactChunk + 1) * 4);
@@ -210,7 +222,7 @@ void Table::ensure_ordered_scratch(uint64_t n) {
     const size_t fl = ((n + 15) & ~15ull) + 16;
     if (o_flag.bytes < fl) {
         o_flag.reserve(fl);
-        MPZCH_CUDA(cudaMemsetAsync(o_flag.p, 0, fl, stream));
+        MPZCH_CUDA(cudaMemsetAsync(o_flag.p, 0, o_flag.bytes, stream));
     }
     o_upos.reserve(n * 4);
     o_ushard.reserve(n * 4);
@@ -218,9 +230,9 @@ void Table::ensure_ordered_scratch(uint64_t n) {
     o_uslot.reserve(n * 8);
     o_uoc.reserve(n);
     s_reset.reserve(n * 8);
-    if (s_evflag.bytes < fl) {
+    if (s_evflag.bytes < fl) {  // zero the whole allocation: it may exceed fl
         s_evflag.reserve(fl);
-        MPZCH_CUDA(cudaMemsetAsync(s_evflag.p, 0, fl, stream));
+        MPZCH_CUDA(cudaMemsetAsync(s_evflag.p, 0, s_evflag.bytes, stream));
     }
     s_evslot.reserve(n * 8);
     s_blk.reserve(((n + kCompactChunk - 1) / kCompactChunk + 1) * 4);
@@ -712,8 +724,7 @@ mpzch_status mpzch_lookup_device(const mpzch_table* t, const uint64_t* ids, uint
         DeviceGuard g(T.device);
         if (n == 0) return;
         cudaStream_t st = (cudaStream_t)stream;  // 0 = legacy default stream
-        BatchErr init{~0ull, 0, 0, ~0ull};
-        MPZCH_CUDA(cudaMemcpyAsync(&T.d_aux->err, &init, sizeof init, cudaMemcpyHostToDevice, st));
+        init_aux_err(T, st);
         run_lookup(T, ids, n, out_slots, out_oc, &T.d_aux->err, st);
         ++T.launches;
         MPZCH_CUDA(cudaGetLastError());
@@ -743,8 +754,7 @@ mpzch_status mpzch_lookup(const mpzch_table* t, const uint64_t* ids, uint64_t n,
         T.s_oslot.reserve(n * 8);
         T.s_ooc.reserve(n);
         MPZCH_CUDA(cudaMemcpyAsync(T.s_ids.p, ids, n * 8, cudaMemcpyHostToDevice, st));
-        BatchErr init{~0ull, 0, 0, ~0ull};
-        MPZCH_CUDA(cudaMemcpyAsync(&T.d_aux->err, &init, sizeof init, cudaMemcpyHostToDevice, st));
+        init_aux_err(T, st);
         run_lookup(T, T.s_ids.as<uint64_t>(), n, T.s_oslot.as<uint64_t>(), T.s_ooc.as<uint8_t>(),
                    &T.d_aux->err, st);
         ++T.launches;
@@ -1038,8 +1048,7 @@ mpzch_status mpzch_lookup_gather_device(const mpzch_table* t, const uint64_t* id
         DeviceGuard g(T.device);
         if (n == 0) return;
         cudaStream_t st = (cudaStream_t)stream;
-        BatchErr init{~0ull, 0, 0, ~0ull};
-        MPZCH_CUDA(cudaMemcpyAsync(&T.d_aux->err, &init, sizeof init, cudaMemcpyHostToDevice, st));
+        init_aux_err(T, st);
         run_lookup_gather(T, ids, n, out_slots, out_oc, out_rows, &T.d_aux->err, st);
         ++T.launches;
         MPZCH_CUDA(cudaGetLastError());

@@ -168,6 +168,9 @@ public:
     // sgd_step (train.cu): row hash, occurrence lists
     DevBuf g_key, g_cnt, g_base, g_pe, g_pr, g_list, g_dupent, g_ctr;
     uint64_t g_cap = 0;
+    // route (route.cu)
+    DevBuf rt_s2p, rt_cnt, rt_tot;
+    std::vector<uint8_t> rt_map;
 
     void ensure_fast_scratch(uint64_t n);
     void ensure_ordered_scratch(uint64_t n);

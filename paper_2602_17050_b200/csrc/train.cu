@@ -66,6 +66,10 @@ __device__ __forceinline__ void apply_row(const TableDev& t, uint64_t row, const
     }
 }
 
+__global__ void k_sgd_init(SgdCounters* c) {
+    *c = SgdCounters{~0ull, 0, 0, 0, 0};
+}
+
 __global__ void __launch_bounds__(256) k_sgd_prep(TableDev t, const uint64_t* __restrict__ rows,
                                                   uint64_t n, unsigned long long* key,
                                                   unsigned* cnt, uint32_t* pe, uint32_t* pr,
@@ -217,8 +221,7 @@ uint64_t run_sgd_step(Table& t, const uint64_t* rows, uint64_t n, const float* g
     t.g_dupent.reserve(n * 4);
     t.g_ctr.reserve(sizeof(SgdCounters));
     SgdCounters* c = t.g_ctr.as<SgdCounters>();
-    const SgdCounters init{~0ull, 0, 0, 0, 0};
-    MPZCH_CUDA(cudaMemcpyAsync(c, &init, sizeof init, cudaMemcpyHostToDevice, st));
+    k_sgd_init<<<1, 1, 0, st>>>(c);  // (a pageable H2D copy would stall the host on the stream)
     unsigned long long* key = t.g_key.as<unsigned long long>();
     unsigned* cnt = t.g_cnt.as<unsigned>();
     unsigned* base = t.g_base.as<unsigned>();
@@ -239,7 +242,7 @@ uint64_t run_sgd_step(Table& t, const uint64_t* rows, uint64_t n, const float* g
                                                   t.g_dupent.as<uint32_t>(), t.g_list.as<uint32_t>(),
                                                   lr, beta, vec, t.gen_clock, c);
     k_sgd_clean<<<gN, B, 0, st>>>(pe, n, key, cnt);
-    t.launches += 6;
+    t.launches += 7;
     MPZCH_CUDA(cudaGetLastError());
     uint64_t bad = ~0ull;
     MPZCH_CUDA(cudaMemcpyAsync(&bad, &c->bad, 8, cudaMemcpyDeviceToHost, st));

@@ -263,6 +263,81 @@ def lru08():
     return lru(0.8)
 
 
+def train():
+    """Not a BASELINE config: the reference's churn training loop (proj/src/experiments.cpp:86-125)
+    at scale -- remap a batch (TTL evictions reset rows), then sgd_step over the distinct
+    remapped rows -- on a 2^24-row dim-128 table (weights + momentum 16 GiB).  The reference
+    runs the same loop (process_batch + sgd_step) on a 2^20-row sample."""
+    rows, dim, B = 1 << 24, 128, 1 << 20
+    caps = mz.even_capacities(rows, 8)
+    t = mz.MpzchTable(mz.TableConfig(caps, 128, 7, dim, 11))
+    pol = mz.EvictionPolicy.ttl(mz.TtlPolicy(3600))
+    st = torch.cuda.current_stream()
+    npre = int(0.8 * rows)
+    out_s = torch.empty(B, dtype=torch.int64, device="cuda")
+    out_o = torch.empty(B, dtype=torch.uint8, device="cuda")
+    for a in range(0, npre, B):
+        ids = bench.distinct_ids_t(4, torch.arange(a, min(a + B, npre), dtype=torch.int64, device="cuda"))
+        t.process_batch_device(ids, 1, pol, None, out_s, out_o, None, st)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    nb = 12
+    batches = [bench.distinct_ids_t(4, torch.randint(0, int(npre * 1.25), (B,), generator=g, device="cuda"))
+               for _ in range(nb)]
+    nows = [4000 + 400 * i for i in range(nb)]
+    grads = (torch.rand((B, dim), generator=g, device="cuda") - 0.5).contiguous()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    tm = {"remap": 0.0, "unique": 0.0, "sgd": 0.0}
+    urows = 0
+    evicted = 0
+    for b in range(nb):
+        ev[0].record(st)
+        t.process_batch_device(batches[b], nows[b], pol, None, out_s, out_o, None, st)
+        evicted += t.last_stats()["evicted_rows"]
+        ev[1].record(st)
+        rows_u = torch.unique(out_s)
+        ev[2].record(st)
+        t.sgd_step_device(rows_u, grads[:rows_u.numel()], 0.05, 0.9, st)
+        ev[3].record(st)
+        torch.cuda.synchronize()
+        if b >= 2:
+            tm["remap"] += ev[0].elapsed_time(ev[1])
+            tm["unique"] += ev[1].elapsed_time(ev[2])
+            tm["sgd"] += ev[2].elapsed_time(ev[3])
+            urows += rows_u.numel()
+    steps = nb - 2
+    step_ms = sum(tm.values()) / steps
+    sgd_bytes = urows / steps * dim * 4 * 5  # grad read + weights/momentum read and write
+    out = dict(config="train (churn loop, 2^24 rows, dim 128, 1M-position batches)",
+               ids_per_s=B / (step_ms / 1e3), step_ms=step_ms,
+               split_ms={k: v / steps for k, v in tm.items()}, distinct_rows=urows / steps,
+               evicted_rows=evicted / nb,
+               sgd_gbs=sgd_bytes / (tm["sgd"] / steps / 1e3) / 1e9)
+    # reference: the same loop on a 2^20-row sample, 64K-position batches
+    import pyoracle
+    if pyoracle.available("reference"):
+        pyoracle.lib("reference")["set_threads"](os.cpu_count() or 1)
+        rrows, rB = 1 << 20, 1 << 16
+        ref = pyoracle.OracleTable(mz.even_capacities(rrows, 8), 128, 7, dim, 11, kind="reference")
+        pre = pyoracle.distinct_ids(4, 0, int(0.8 * rrows))
+        for a in range(0, pre.size, 1 << 18):
+            ref.process_batch(pre[a:a + (1 << 18)], 1, 1, 3600)
+        rng = np.random.default_rng(5)
+        gref = (rng.random((rB, dim), dtype=np.float32) - 0.5)
+        tot, pos = 0.0, 0
+        for b in range(6):
+            ids = pyoracle.distinct_ids(4, 0, int(pre.size * 1.25))[rng.integers(0, int(pre.size * 1.25), rB)]
+            s0 = time.perf_counter()
+            sl, _, _ = ref.process_batch(ids, 4000 + 400 * b, 1, 3600)
+            ur = np.unique(sl)
+            ref.sgd_step(ur, gref[:ur.size], 0.05, 0.9)
+            if b >= 1:
+                tot += time.perf_counter() - s0
+                pos += rB
+        out["reference"] = dict(ids_per_s=pos / tot, cores=os.cpu_count(), kind="reference",
+                                sample="2^20 rows, dim 128, 64K-position batches")
+    return out
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["c1", "c2", "c3", "c4"]
     out = []
