@@ -258,6 +258,24 @@ mpzch_status mpzch_sgd_step_device(mpzch_table* t, const uint64_t* rows, uint64_
                                    const float* grads, uint64_t n_grads, float lr, float beta,
                                    void* stream);
 
+/* ---- publish: .mpzc / .mpzd images (proj/README.md:129-145) built from HBM,
+ * CRC-32 computed on the device.
+ * crc32 (publish.cpp:110-124) of n bytes of DEVICE memory, enqueued on `stream`; returns when done. */
+mpzch_status mpzch_crc32_device(const void* bytes, uint64_t n, uint32_t* out_crc, void* stream);
+/* serialize_snapshot (publish.cpp:126-155) into a host buffer.  *out_len = image size; out NULL:
+ * size query.  cap too small: MPZCH_ELENGTH.  dim 0: MPZCH_ELOGIC.  Row-sharded handles:
+ * MPZCH_EINVAL (a snapshot covers every shard).  The trailer CRC is the lineage checksum
+ * (snapshot_checksum, publish.cpp:157-162). */
+mpzch_status mpzch_serialize_snapshot(const mpzch_table* t, uint8_t* out, uint64_t cap,
+                                      uint64_t* out_len);
+/* DeltaSource::cut (publish.cpp:288-305) + serialize_delta (publish.cpp:212-230) in one pass:
+ * the rows dirtied since `generation`, ascending, each record (row u64, identity u64, dim f32)
+ * packed on the device, CRC on the device.  out NULL: size query (cursor unchanged); otherwise
+ * a fresh cursor is returned in *out_next_generation. */
+mpzch_status mpzch_serialize_delta(mpzch_table* t, uint64_t generation, uint32_t base_checksum,
+                                   uint64_t sequence, uint8_t* out, uint64_t cap,
+                                   uint64_t* out_len, uint64_t* out_next_generation);
+
 /* ---- execution control / introspection */
 mpzch_status mpzch_set_path(mpzch_table* t, int path);
 mpzch_status mpzch_last_stats(const mpzch_table* t, mpzch_batch_stats* out);

@@ -246,6 +246,94 @@ int orc_dirty_rows_since(const orc_table* t, uint64_t cursor, uint64_t* out, uin
     return ORC_OK;
 }
 
+/* --------------------------------------------------------------- publish */
+
+uint32_t orc_crc32(const uint8_t* bytes, uint64_t n) { /* publish.cpp:110-124 */
+    static uint32_t table[256];
+    static int ready = 0;
+    if (!ready) {
+        for (uint32_t i = 0; i < 256; ++i) {
+            uint32_t c = i;
+            for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+            table[i] = c;
+        }
+        ready = 1;
+    }
+    uint32_t crc = 0xFFFFFFFFu;
+    for (uint64_t i = 0; i < n; ++i) crc = table[(crc ^ bytes[i]) & 0xFFu] ^ (crc >> 8);
+    return crc ^ 0xFFFFFFFFu;
+}
+
+/* ByteWriter, publish.cpp:17-38: little-endian appends */
+typedef struct {
+    uint8_t* p;
+    uint64_t n;
+} bw;
+static void bw_u32(bw* w, uint32_t v) {
+    for (int i = 0; i < 4; ++i) w->p[w->n++] = (uint8_t)(v >> (8 * i));
+}
+static void bw_u64(bw* w, uint64_t v) {
+    for (int i = 0; i < 8; ++i) w->p[w->n++] = (uint8_t)(v >> (8 * i));
+}
+static void bw_f32(bw* w, float v) {
+    uint32_t u;
+    memcpy(&u, &v, 4);
+    bw_u32(w, u);
+}
+static void bw_magic(bw* w, const char* m) {
+    for (int i = 0; i < 4; ++i) w->p[w->n++] = (uint8_t)m[i];
+}
+
+int orc_serialize_snapshot(const orc_table* t, uint8_t* out, uint64_t cap, uint64_t* out_len) {
+    if (t->dim == 0) return fail(ORC_ELOGIC, "index-only tables (dim = 0) cannot be published");
+    const uint64_t need = 48 + 8ull * t->num_shards + 8 * t->total + 4ull * t->dim * t->total;
+    *out_len = need;
+    if (!out || cap < need) return fail(ORC_ELENGTH, "output buffer too small");
+    bw w = {out, 0};
+    bw_magic(&w, "MPZC");
+    bw_u32(&w, 1); /* kFormatVersion */
+    bw_u64(&w, t->seed);
+    bw_u32(&w, t->max_probe);
+    bw_u32(&w, t->dim);
+    bw_u32(&w, t->num_shards);
+    for (uint32_t s = 0; s < t->num_shards; ++s) bw_u64(&w, t->caps[s]);
+    bw_u64(&w, t->total);
+    for (uint64_t r = 0; r < t->total; ++r) bw_u64(&w, t->ident[r]); /* shards in order */
+    bw_u64(&w, t->total * t->dim);
+    for (uint64_t i = 0; i < t->total * t->dim; ++i) bw_f32(&w, t->weights[i]);
+    bw_u32(&w, orc_crc32(out, w.n)); /* trailer */
+    return ORC_OK;
+}
+
+int orc_serialize_delta(orc_table* t, uint64_t cursor, uint32_t base_checksum, uint64_t sequence,
+                        uint8_t* out, uint64_t cap, uint64_t* out_len, uint64_t* out_next_cursor) {
+    if (t->dim == 0) return fail(ORC_ELOGIC, "index-only tables (dim = 0) cannot be published");
+    if (cursor == 0 || cursor >= t->gen_clock)
+        return fail(ORC_EINVAL, "stale or unknown publication cursor");
+    uint64_t k = 0;
+    for (uint64_t r = 0; r < t->total; ++r) k += t->row_gen[r] > cursor;
+    const uint64_t rec = 16 + 4ull * t->dim;
+    const uint64_t need = 32 + k * rec + 4;
+    *out_len = need;
+    if (!out || cap < need) return fail(ORC_ELENGTH, "output buffer too small");
+    *out_next_cursor = orc_make_cursor(t); /* cut: cursor_ = make_cursor() */
+    bw w = {out, 0};
+    bw_magic(&w, "MPZD");
+    bw_u32(&w, 1);
+    bw_u32(&w, base_checksum);
+    bw_u64(&w, sequence);
+    bw_u32(&w, t->dim);
+    bw_u64(&w, k);
+    for (uint64_t r = 0; r < t->total; ++r) { /* dirty rows ascending, publish.cpp:297-303 */
+        if (t->row_gen[r] <= cursor) continue;
+        bw_u64(&w, r);
+        bw_u64(&w, t->ident[r]);
+        for (uint32_t j = 0; j < t->dim; ++j) bw_f32(&w, t->weights[r * t->dim + j]);
+    }
+    bw_u32(&w, orc_crc32(out, w.n));
+    return ORC_OK;
+}
+
 /* --------------------------------------------------------------- probe core */
 
 /* lookup_readonly, proj/src/probe_core.cpp:32-43 (full window, no early exit) */

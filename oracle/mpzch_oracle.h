@@ -123,6 +123,17 @@ int orc_dirty_rows_since(const orc_table* t, uint64_t cursor, uint64_t* out, uin
                          uint64_t* out_n);
 
 /* last error text (thread-local) */
+/* ---- publish, proj/src/publish.cpp */
+/* crc32, publish.cpp:110-124: reflected, polynomial 0xEDB88320, init/final ~0 */
+uint32_t orc_crc32(const uint8_t* bytes, uint64_t n);
+/* serialize_snapshot, publish.cpp:126-155 (.mpzc).  *out_len = full size even when it
+ * exceeds cap (then nothing is written and ORC_ELENGTH is returned). */
+int orc_serialize_snapshot(const orc_table* t, uint8_t* out, uint64_t cap, uint64_t* out_len);
+/* DeltaSource::cut (publish.cpp:288-305) + serialize_delta (publish.cpp:212-230): the rows
+ * dirtied since `cursor`, then a fresh cursor in *out_next_cursor. */
+int orc_serialize_delta(orc_table* t, uint64_t cursor, uint32_t base_checksum, uint64_t sequence,
+                        uint8_t* out, uint64_t cap, uint64_t* out_len, uint64_t* out_next_cursor);
+
 const char* orc_last_error(void);
 
 #ifdef __cplusplus

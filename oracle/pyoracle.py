@@ -89,11 +89,17 @@ def lib(kind: str = "port"):
                                     ctypes.c_float]),
         "dirty_rows_since": (ctypes.c_int, [_vp, ctypes.c_uint64, _vp, ctypes.c_uint64, _u64p]),
         "last_error": (ctypes.c_char_p, []),
+        "crc32": (ctypes.c_uint32, [_vp, ctypes.c_uint64]),
+        "serialize_snapshot": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _u64p]),
     }
     if kind == "port":
+        sig["serialize_delta"] = (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint32,
+                                                 ctypes.c_uint64, _vp, ctypes.c_uint64, _u64p, _u64p])
         sig["draw_row"] = (None, [_vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64])
         sig["splitmix_next"] = (ctypes.c_uint64, [_u64p])
     else:
+        sig["delta_source_create"] = (ctypes.c_int, [_vp, ctypes.c_uint32])
+        sig["delta_source_cut"] = (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _u64p])
         sig["set_threads"] = (None, [ctypes.c_int])
         sig["max_threads"] = (ctypes.c_int, [])
     fns = {}
@@ -213,6 +219,44 @@ class OracleTable:
     def make_cursor(self):
         return int(self.L["make_cursor"](self.h))
 
+    def serialize_snapshot(self) -> bytes:
+        n = ctypes.c_uint64(0)
+        self.L["serialize_snapshot"](self.h, None, 0, ctypes.byref(n))
+        if n.value == 0:
+            _raise(self.L, self.L["serialize_snapshot"](self.h, None, 0, ctypes.byref(n)))
+        out = np.empty(n.value, np.uint8)
+        _raise(self.L, self.L["serialize_snapshot"](self.h, _ptr(out), out.size, ctypes.byref(n)))
+        return out.tobytes()
+
+    def delta_source(self, base_checksum: int):
+        """DeltaSource(table, base) (publish.hpp:69-82): returns a cut() -> bytes callable
+        (cut + serialize_delta)."""
+        if self.kind == "reference":
+            _raise(self.L, self.L["delta_source_create"](self.h, base_checksum))
+
+            def cut():
+                n = ctypes.c_uint64(0)
+                cap = 64 + self.total_rows * (16 + 4 * self.dim)
+                out = np.empty(cap, np.uint8)
+                _raise(self.L, self.L["delta_source_cut"](self.h, _ptr(out), cap, ctypes.byref(n)))
+                return out[:n.value].tobytes()
+            return cut
+        if self.dim == 0:
+            raise OracleError(4, "index-only tables (dim = 0) cannot be published")
+        state = {"cursor": self.make_cursor(), "seq": 0}
+
+        def cut():
+            n, nxt = ctypes.c_uint64(0), ctypes.c_uint64(0)
+            cap = 64 + self.total_rows * (16 + 4 * self.dim)
+            out = np.empty(cap, np.uint8)
+            _raise(self.L, self.L["serialize_delta"](self.h, state["cursor"], base_checksum,
+                                                     state["seq"], _ptr(out), cap,
+                                                     ctypes.byref(n), ctypes.byref(nxt)))
+            state["cursor"] = nxt.value
+            state["seq"] += 1
+            return out[:n.value].tobytes()
+        return cut
+
     def sgd_step(self, rows, grads, lr, beta):
         rows = np.ascontiguousarray(rows, dtype=np.uint64)
         g = np.ascontiguousarray(grads, dtype=np.float32).reshape(-1)
@@ -223,6 +267,11 @@ class OracleTable:
         n = ctypes.c_uint64(0)
         _raise(self.L, self.L["dirty_rows_since"](self.h, cursor, _ptr(out), out.size, ctypes.byref(n)))
         return out[:n.value].copy()
+
+
+def crc32(data: bytes, kind="port") -> int:
+    a = np.frombuffer(data, np.uint8)
+    return int(lib(kind)["crc32"](_ptr(a), a.size))
 
 
 def probe(id, meta_in, now, identities, metadata, capacity, max_probe, seed, mode, kind="port"):

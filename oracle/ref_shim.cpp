@@ -23,6 +23,7 @@
 #include "mpzch/batch_engine.hpp"
 #include "mpzch/eviction.hpp"
 #include "mpzch/probe_core.hpp"
+#include "mpzch/publish.hpp"
 #include "mpzch/rng.hpp"
 #include "mpzch/shard_router.hpp"
 #include "mpzch/table.hpp"
@@ -34,6 +35,7 @@ thread_local std::string g_err;
 struct RefTable {
     mpzch::MpzchTable table;
     std::vector<mpzch::PublishCursor> cursors;  // index = generation
+    std::unique_ptr<mpzch::DeltaSource> source;   // publish.hpp:69-82
     explicit RefTable(mpzch::TableConfig cfg) : table(std::move(cfg)) {}
 };
 
@@ -293,6 +295,52 @@ std::uint64_t ref_make_cursor(RefTable* t) {
     if (t->cursors.size() <= c.generation) t->cursors.resize(c.generation + 1);
     t->cursors[c.generation] = c;
     return c.generation;
+}
+
+std::uint32_t ref_crc32(const std::uint8_t* bytes, std::uint64_t n) {
+    return mpzch::crc32(std::span<const std::uint8_t>(bytes, n));
+}
+
+int ref_serialize_snapshot(const RefTable* t, std::uint8_t* out, std::uint64_t cap,
+                           std::uint64_t* out_len) {
+    try {
+        const std::vector<std::uint8_t> b = mpzch::serialize_snapshot(t->table);
+        *out_len = b.size();
+        if (!out || cap < b.size()) {
+            g_err = "output buffer too small";
+            return 3;
+        }
+        std::memcpy(out, b.data(), b.size());
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// DeltaSource(table, base) -- takes its cursor now, like the reference constructor
+int ref_delta_source_create(RefTable* t, std::uint32_t base_checksum) {
+    try {
+        t->source = std::make_unique<mpzch::DeltaSource>(t->table, base_checksum);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// DeltaSource::cut + serialize_delta
+int ref_delta_source_cut(RefTable* t, std::uint8_t* out, std::uint64_t cap, std::uint64_t* out_len) {
+    try {
+        const std::vector<std::uint8_t> b = mpzch::serialize_delta(t->source->cut());
+        *out_len = b.size();
+        if (!out || cap < b.size()) {
+            g_err = "output buffer too small";
+            return 3;
+        }
+        std::memcpy(out, b.data(), b.size());
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
 }
 
 int ref_sgd_step(RefTable* t, const std::uint64_t* rows, std::uint64_t n, const float* grads,

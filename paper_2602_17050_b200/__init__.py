@@ -173,6 +173,10 @@ _SIGS = {
                                       ctypes.c_float]),
     "mpzch_sgd_step_device": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _vp, ctypes.c_uint64,
                                              ctypes.c_float, ctypes.c_float, _vp]),
+    "mpzch_crc32_device": (ctypes.c_int, [_vp, ctypes.c_uint64, _u32p, _vp]),
+    "mpzch_serialize_snapshot": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _u64p]),
+    "mpzch_serialize_delta": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
+                                             _vp, ctypes.c_uint64, _u64p, _u64p]),
     "mpzch_set_path": (ctypes.c_int, [_vp, ctypes.c_int]),
     "mpzch_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),
     "mpzch_get_profile": (ctypes.c_int, [_vp, ctypes.POINTER(_Profile)]),
@@ -623,6 +627,78 @@ class MpzchTable:
 
     def kernel_launches(self) -> int:
         return int(self._lib.mpzch_kernel_launches(self._h))
+
+    def serialize_snapshot(self) -> bytes:
+        """serialize_snapshot (publish.cpp:126-155): the .mpzc image, CRC-32 on the device."""
+        n = ctypes.c_uint64(0)
+        _check(self._lib.mpzch_serialize_snapshot(self._h, None, 0, ctypes.byref(n)))
+        out = np.empty(n.value, np.uint8)
+        _check(self._lib.mpzch_serialize_snapshot(self._h, _ptr(out), out.size, ctypes.byref(n)))
+        return out.tobytes()
+
+
+class DeltaSource:
+    """DeltaSource (proj/include/mpzch/publish.hpp:69-82): takes a cursor now; each cut()
+    returns the serialized .mpzd log of the rows dirtied since the previous cut (records packed
+    and checksummed on the device)."""
+
+    def __init__(self, table: MpzchTable, base_checksum: int):
+        if table.dim == 0:
+            raise LogicError("index-only tables (dim = 0) cannot be published")
+        self.table = table
+        self.base_checksum = base_checksum
+        self.sequence = 0
+        self.cursor = table.make_cursor()
+
+    def cut(self) -> bytes:
+        t = self.table
+        n, nxt = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        _check(t._lib.mpzch_serialize_delta(t._h, self.cursor, self.base_checksum, self.sequence,
+                                            None, 0, ctypes.byref(n), ctypes.byref(nxt)))
+        out = np.empty(n.value, np.uint8)
+        _check(t._lib.mpzch_serialize_delta(t._h, self.cursor, self.base_checksum, self.sequence,
+                                            _ptr(out), out.size, ctypes.byref(n), ctypes.byref(nxt)))
+        self.cursor = nxt.value
+        self.sequence += 1
+        return out.tobytes()
+
+
+def snapshot_checksum(image: bytes) -> int:
+    """snapshot_checksum (publish.cpp:157-162): the trailer CRC, the lineage id."""
+    if len(image) < 4:
+        raise ValueError("truncated file")
+    return int.from_bytes(image[-4:], "little")
+
+
+def crc32_device(t) -> int:
+    """crc32 (publish.cpp:110-124) of a CUDA tensor's bytes, computed on the device."""
+    import torch
+    c = ctypes.c_uint32(0)
+    st = torch.cuda.current_stream(t.device)
+    _check(load_library().mpzch_crc32_device(ctypes.c_void_p(t.data_ptr()),
+                                             t.numel() * t.element_size(), ctypes.byref(c),
+                                             ctypes.c_void_p(st.cuda_stream)))
+    return c.value
+
+
+def parse_delta(image: bytes) -> dict:
+    """parse_delta (publish.cpp:232-252) on the host: header fields and records
+    (rows, identities, weights[k, dim]); raises ValueError on a malformed image."""
+    import struct
+    import zlib
+    if len(image) < 36 or image[:4] != b"MPZD":
+        raise ValueError("bad magic; not a delta file")
+    ver, base, seq, dim, count = struct.unpack_from("<IIQIQ", image, 4)
+    rec = 16 + 4 * dim
+    if ver != 1 or dim == 0 or len(image) != 36 + count * rec:
+        raise ValueError("malformed delta")
+    if int.from_bytes(image[-4:], "little") != zlib.crc32(image[:-4]):
+        raise ValueError("checksum failure")
+    body = np.frombuffer(image, np.uint8, count * rec, 32).reshape(count, rec)
+    return dict(base_checksum=base, sequence=seq, dim=dim,
+                rows=body[:, :8].copy().view(np.uint64).reshape(-1),
+                identities=body[:, 8:16].copy().view(np.uint64).reshape(-1),
+                weights=body[:, 16:].copy().view(np.float32).reshape(count, dim))
 
 
 def process_batch(table: MpzchTable, ids, now: int, policy: EvictionPolicy, features=None):

@@ -266,6 +266,28 @@ struct EmitIndex {
     }
 };
 
+// Rows of this handle dirtied since `gen` (row_generation > gen), ascending, into T.p_rows;
+// returns the count.  Persistent scratch: k_dirty_flags writes every held flag, the padding
+// past `held` is zeroed once at allocation.
+unsigned run_dirty_compact(Table& T, uint64_t gen, cudaStream_t st) {
+    const uint64_t held = T.held_rows();
+    const size_t fl = ((held + 15) & ~15ull) + 16;
+    if (T.p_flags.bytes < fl) {
+        T.p_flags.reserve(fl);
+        MPZCH_CUDA(cudaMemsetAsync(T.p_flags.p, 0, T.p_flags.bytes, st));
+    }
+    T.p_rows.reserve(std::max<uint64_t>(held, 1) * 8);
+    T.p_blk.reserve(((held + kCompactChunk - 1) / kCompactChunk + 1) * 4);
+    k_dirty_flags<<<grid_for(held, 256), 256, 0, st>>>(T.row_gen, held, gen, T.p_flags.as<uint8_t>());
+    ++T.launches;
+    unsigned* d_n = &T.d_aux->pad;
+    EmitIndex em{T.p_rows.as<uint64_t>(), held, T.row_lo};
+    compact_flags(T.p_flags.as<uint8_t>(), held, T.p_blk.as<unsigned>(), d_n, false, em, st, T.launches);
+    MPZCH_CUDA(cudaMemcpyAsync(&T.h_aux->pad, d_n, 4, cudaMemcpyDeviceToHost, st));
+    MPZCH_CUDA(cudaStreamSynchronize(st));
+    return T.h_aux->pad;
+}
+
 Policy parse_policy(const mpzch_policy* p) {
     Policy pol;
     if (!p) return pol;  // Disabled
@@ -1002,22 +1024,10 @@ mpzch_status mpzch_dirty_rows_since(const mpzch_table* t, uint64_t gen, uint64_t
             throw Error{MPZCH_EINVAL, "stale or unknown publication cursor"};
         DeviceGuard g(T.device);
         cudaStream_t st = T.stream;
-        DevBuf flags, rows, blk;
-        const uint64_t held = T.held_rows();
-        flags.reserve(((held + 15) & ~15ull) + 16);
-        MPZCH_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes, st));
-        rows.reserve(std::max<uint64_t>(cap, 1) * 8);
-        blk.reserve(((held + kCompactChunk - 1) / kCompactChunk + 1) * 4);
-        k_dirty_flags<<<grid_for(held, 256), 256, 0, st>>>(T.row_gen, held, gen,
-                                                            flags.as<uint8_t>());
-        ++T.launches;
-        unsigned* d_n = &T.d_aux->pad;
-        EmitIndex em{rows.as<uint64_t>(), cap, T.row_lo};
-        compact_flags(flags.as<uint8_t>(), held, blk.as<unsigned>(), d_n, false, em, st, T.launches);
-        unsigned nn = 0;
-        MPZCH_CUDA(cudaMemcpyAsync(&nn, d_n, 4, cudaMemcpyDeviceToHost, st));
-        MPZCH_CUDA(cudaStreamSynchronize(st));
-        if (cap && out) MPZCH_CUDA(cudaMemcpy(out, rows.p, std::min<uint64_t>(nn, cap) * 8, cudaMemcpyDeviceToHost));
+        order_after_last_batch(T, st);
+        const unsigned nn = run_dirty_compact(T, gen, st);
+        if (cap && out && nn)
+            MPZCH_CUDA(cudaMemcpy(out, T.p_rows.p, std::min<uint64_t>(nn, cap) * 8, cudaMemcpyDeviceToHost));
         *out_n = nn;
     });
 }
@@ -1079,36 +1089,134 @@ mpzch_status mpzch_delta_cut(mpzch_table* t, uint64_t generation, uint64_t* out_
             throw Error{MPZCH_EINVAL, "stale or unknown publication cursor"};
         DeviceGuard g(T.device);
         cudaStream_t st = T.stream;
-        const uint64_t held = T.held_rows();
-        DevBuf flags, rows, blk, ids, w;
-        flags.reserve(((held + 15) & ~15ull) + 16);
-        MPZCH_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes, st));
-        rows.reserve(std::max<uint64_t>(held, 1) * 8);
-        blk.reserve(((held + kCompactChunk - 1) / kCompactChunk + 1) * 4);
-        k_dirty_flags<<<grid_for(held, 256), 256, 0, st>>>(T.row_gen, held, generation,
-                                                            flags.as<uint8_t>());
-        unsigned* d_n = &T.d_aux->pad;
-        EmitIndex em{rows.as<uint64_t>(), held, T.row_lo};
-        compact_flags(flags.as<uint8_t>(), held, blk.as<unsigned>(), d_n, false, em, st, T.launches);
-        unsigned nn = 0;
-        MPZCH_CUDA(cudaMemcpyAsync(&nn, d_n, 4, cudaMemcpyDeviceToHost, st));
-        MPZCH_CUDA(cudaStreamSynchronize(st));
+        order_after_last_batch(T, st);
+        const unsigned nn = run_dirty_compact(T, generation, st);
         const uint64_t k = std::min<uint64_t>(nn, cap);
         if (k) {
-            ids.reserve(k * 8);
-            w.reserve(k * T.dim * 4);
-            run_gather_rows(T, rows.as<uint64_t>(), k, ids.as<uint64_t>(), w.as<float>(), st);
+            T.p_ids.reserve(k * 8);
+            T.p_w.reserve(k * T.dim * 4);
+            run_gather_rows(T, T.p_rows.as<uint64_t>(), k, T.p_ids.as<uint64_t>(), T.p_w.as<float>(), st);
             T.launches += 2;
             MPZCH_CUDA(cudaGetLastError());
-            if (out_rows) MPZCH_CUDA(cudaMemcpyAsync(out_rows, rows.p, k * 8, cudaMemcpyDeviceToHost, st));
+            if (out_rows) MPZCH_CUDA(cudaMemcpyAsync(out_rows, T.p_rows.p, k * 8, cudaMemcpyDeviceToHost, st));
             if (out_identities)
-                MPZCH_CUDA(cudaMemcpyAsync(out_identities, ids.p, k * 8, cudaMemcpyDeviceToHost, st));
+                MPZCH_CUDA(cudaMemcpyAsync(out_identities, T.p_ids.p, k * 8, cudaMemcpyDeviceToHost, st));
             if (out_weights)
-                MPZCH_CUDA(cudaMemcpyAsync(out_weights, w.p, k * T.dim * 4, cudaMemcpyDeviceToHost, st));
+                MPZCH_CUDA(cudaMemcpyAsync(out_weights, T.p_w.p, k * T.dim * 4, cudaMemcpyDeviceToHost, st));
             MPZCH_CUDA(cudaStreamSynchronize(st));
         }
         *out_n = nn;
         if (nn <= cap && out_next_generation) *out_next_generation = T.gen_clock++;  // new cursor
+    });
+}
+
+// ---- publish: .mpzc / .mpzd images (proj/src/publish.cpp; csrc/publish.cu)
+
+namespace {
+void put_u32(std::vector<uint8_t>& b, uint32_t v) {
+    for (int i = 0; i < 4; ++i) b.push_back((uint8_t)(v >> (8 * i)));
+}
+void put_u64(std::vector<uint8_t>& b, uint64_t v) {
+    for (int i = 0; i < 8; ++i) b.push_back((uint8_t)(v >> (8 * i)));
+}
+void put_magic(std::vector<uint8_t>& b, const char* m) { b.insert(b.end(), m, m + 4); }
+}  // namespace
+
+mpzch_status mpzch_crc32_device(const void* bytes, uint64_t n, uint32_t* out_crc, void* stream) {
+    return guarded([&] {
+        int dev = 0;
+        MPZCH_CUDA(cudaGetDevice(&dev));
+        const uint32_t raw = crc32_raw_device((const uint8_t*)bytes, n, (cudaStream_t)stream, dev);
+        *out_crc = crc32_finish(raw, n);
+    });
+}
+
+mpzch_status mpzch_serialize_snapshot(const mpzch_table* t, uint8_t* out, uint64_t cap,
+                                      uint64_t* out_len) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        // serialize_snapshot, publish.cpp:126-155
+        if (T.dim == 0) throw Error{MPZCH_ELOGIC, "index-only tables (dim = 0) cannot be published"};
+        if (T.row_lo != 0 || T.row_hi != T.total)
+            throw Error{MPZCH_EINVAL, "a snapshot needs every shard (this handle is row-sharded)"};
+        const uint64_t id_bytes = T.total * 8, w_bytes = T.total * T.dim * 4ull;
+        const uint64_t need = 48 + 8ull * T.S + id_bytes + w_bytes;
+        *out_len = need;
+        if (!out) return;  // size query
+        if (cap < need) throw Error{MPZCH_ELENGTH, "output buffer too small"};
+        std::vector<uint8_t> h;
+        put_magic(h, "MPZC");
+        put_u32(h, 1);  // kFormatVersion
+        put_u64(h, T.seed);
+        put_u32(h, T.P);
+        put_u32(h, T.dim);
+        put_u32(h, T.S);
+        for (uint64_t c : T.caps) put_u64(h, c);
+        put_u64(h, T.total);
+        std::vector<uint8_t> cnt;
+        put_u64(cnt, T.total * T.dim);
+        DeviceGuard g(T.device);
+        cudaStream_t st = T.stream;
+        order_after_last_batch(T, st);
+        // CRC over header | identities | weight count | weights (device sections on the GPU)
+        uint32_t raw = crc32_raw_host(0, h.data(), h.size());
+        raw = crc32_shift(raw, id_bytes) ^ crc32_raw_device((const uint8_t*)T.dev.ident, id_bytes, st, T.device);
+        raw = crc32_raw_host(raw, cnt.data(), 8);
+        raw = crc32_shift(raw, w_bytes) ^ crc32_raw_device((const uint8_t*)T.dev.weights, w_bytes, st, T.device);
+        const uint32_t crc = crc32_finish(raw, need - 4);
+        uint8_t* o = out;
+        std::memcpy(o, h.data(), h.size());
+        o += h.size();
+        MPZCH_CUDA(cudaMemcpyAsync(o, T.dev.ident, id_bytes, cudaMemcpyDeviceToHost, st));
+        o += id_bytes;
+        std::memcpy(o, cnt.data(), 8);
+        o += 8;
+        MPZCH_CUDA(cudaMemcpyAsync(o, T.dev.weights, w_bytes, cudaMemcpyDeviceToHost, st));
+        o += w_bytes;
+        for (int i = 0; i < 4; ++i) o[i] = (uint8_t)(crc >> (8 * i));
+        MPZCH_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+mpzch_status mpzch_serialize_delta(mpzch_table* t, uint64_t generation, uint32_t base_checksum,
+                                   uint64_t sequence, uint8_t* out, uint64_t cap, uint64_t* out_len,
+                                   uint64_t* out_next_generation) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        if (T.dim == 0) throw Error{MPZCH_ELOGIC, "index-only tables (dim = 0) cannot be published"};
+        if (generation == 0 || generation >= T.gen_clock)
+            throw Error{MPZCH_EINVAL, "stale or unknown publication cursor"};
+        DeviceGuard g(T.device);
+        cudaStream_t st = T.stream;
+        order_after_last_batch(T, st);
+        const unsigned k = run_dirty_compact(T, generation, st);
+        const uint64_t rec = 16 + 4ull * T.dim, body = k * rec;
+        const uint64_t need = 32 + body + 4;
+        *out_len = need;
+        if (!out) return;  // size query: the cursor does not move
+        if (cap < need) throw Error{MPZCH_ELENGTH, "output buffer too small"};
+        std::vector<uint8_t> h;  // serialize_delta, publish.cpp:212-230
+        put_magic(h, "MPZD");
+        put_u32(h, 1);
+        put_u32(h, base_checksum);
+        put_u64(h, sequence);
+        put_u32(h, T.dim);
+        put_u64(h, k);
+        uint32_t raw = crc32_raw_host(0, h.data(), h.size());
+        if (k) {
+            T.p_rec.reserve(body);
+            launch_pack_delta(T, T.p_rows.as<uint64_t>(), &T.d_aux->pad, k, T.p_rec.as<uint8_t>(), st);
+            MPZCH_CUDA(cudaGetLastError());
+            raw = crc32_shift(raw, body) ^ crc32_raw_device(T.p_rec.as<uint8_t>(), body, st, T.device);
+            MPZCH_CUDA(cudaMemcpyAsync(out + 32, T.p_rec.p, body, cudaMemcpyDeviceToHost, st));
+        }
+        const uint32_t crc = crc32_finish(raw, 32 + body);
+        std::memcpy(out, h.data(), 32);
+        for (int i = 0; i < 4; ++i) out[32 + body + i] = (uint8_t)(crc >> (8 * i));
+        MPZCH_CUDA(cudaStreamSynchronize(st));
+        *out_next_generation = T.gen_clock++;  // DeltaSource::cut: cursor_ = make_cursor()
     });
 }
 

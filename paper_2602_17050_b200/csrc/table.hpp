@@ -168,6 +168,8 @@ public:
     // sgd_step (train.cu): row hash, occurrence lists
     DevBuf g_key, g_cnt, g_base, g_pe, g_pr, g_list, g_dupent, g_ctr;
     uint64_t g_cap = 0;
+    // publish / dirty rows (table.cu, publish.cu)
+    DevBuf p_flags, p_rows, p_blk, p_ids, p_w, p_rec;
     // route (route.cu)
     DevBuf rt_s2p, rt_cnt, rt_tot;
     std::vector<uint8_t> rt_map;
@@ -186,6 +188,14 @@ void run_lookup(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_s
                 uint8_t* out_oc, BatchErr* err, cudaStream_t st);
 void run_lookup_gather(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots,
                        uint8_t* out_oc, float* out_rows, BatchErr* err, cudaStream_t st);
+// publish.cu: CRC-32 (raw register from 0; finish() applies the reference's init/final xor)
+uint32_t crc32_raw_device(const uint8_t* data, uint64_t n, cudaStream_t st, int device);
+uint32_t crc32_raw_host(uint32_t raw, const uint8_t* p, uint64_t n);
+uint32_t crc32_shift(uint32_t raw, uint64_t n);
+uint32_t crc32_finish(uint32_t raw, uint64_t n);
+void launch_pack_delta(Table& t, const uint64_t* rows, const unsigned* count, uint64_t max_n,
+                       uint8_t* out, cudaStream_t st);
+
 // returns the first out-of-range position (~0 if none); synchronous on st
 uint64_t run_sgd_step(Table& t, const uint64_t* rows, uint64_t n, const float* grads, float lr,
                       float beta, cudaStream_t st);

@@ -234,3 +234,62 @@ def test_sgd_port_vs_reference_live(oracle):
             assert (a.momentum().view(np.uint32) == b.momentum().view(np.uint32)).all()
             assert (a.trained() == b.trained()).all()
             assert (a.dirty_rows_since(cur[0]) == b.dirty_rows_since(cur[1])).all()
+
+
+# ------------------------------------------------------------------ publish
+
+def test_crc32_known_answers(oracle):
+    """proj/tests/test_publish.cpp:49-56; zlib's CRC-32 is the same code."""
+    import zlib
+    for kind in _kinds(oracle):
+        assert oracle.crc32(b"123456789", kind) == 0xCBF43926
+        assert oracle.crc32(b"", kind) == 0
+        assert oracle.crc32(b"hello world", kind) != oracle.crc32(b"helmo world", kind)
+    rng = np.random.default_rng(3)
+    for n in (1, 7, 4096, 100003):
+        b = rng.integers(0, 256, n, dtype=np.uint8).tobytes()
+        assert oracle.crc32(b) == zlib.crc32(b)
+
+
+def _busy(oracle, kind, seed, caps=(6, 5, 5), P=3, dim=4):
+    """make_busy_table, proj/tests/test_publish.cpp:26-45."""
+    t = oracle.OracleTable(list(caps), P, seed, dim, seed + 1, kind=kind)
+    ids = oracle.distinct_ids(seed, 0, 64)
+    touched = []
+    for i, x in enumerate(ids):
+        s, o = t.lookup_or_insert(int(x), 0, i + 2, mode=2)
+        if o != 3:
+            touched.append(s)
+    t.sgd_step(np.array(touched, np.uint64), np.full((len(touched), dim), 0.125, np.float32),
+               0.05, 0.9)
+    return t
+
+
+def test_snapshot_and_delta_port_vs_reference(oracle):
+    import struct
+    import zlib
+    if not oracle.available("reference"):
+        pytest.skip("oracle/_ref not built (no /root/reference here)")
+    for seed in (500, 77, 9):
+        a, b = (_busy(oracle, k, seed) for k in ("port", "reference"))
+        sa, sb = a.serialize_snapshot(), b.serialize_snapshot()
+        assert sa == sb
+        assert len(sa) == 48 + 8 * 3 + 8 * 16 + 4 * 4 * 16  # test_publish.cpp:58-66
+        assert struct.unpack("<I", sa[-4:])[0] == zlib.crc32(sa[:-4])
+        base = struct.unpack("<I", sa[-4:])[0]
+        ca, cb = a.delta_source(base), b.delta_source(base)
+        rng = np.random.default_rng(seed)
+        for step in range(6):
+            da, db = ca(), cb()
+            assert da == db, step
+            assert da[:4] == b"MPZD" and struct.unpack("<Q", da[12:20])[0] == step
+            ids = rng.integers(0, 1 << 40, 12).astype(np.uint64)
+            for t in (a, b):
+                s, o, e = t.process_batch(ids, 100 + step, 1, 1)  # TTL 1: evictions
+                if step % 2:
+                    t.sgd_step(s[:3], np.ones((3, 4), np.float32), 0.1, 0.0)
+    for kind in _kinds(oracle):
+        nodim = oracle.OracleTable([4, 4], 2, 1, kind=kind)
+        with pytest.raises(oracle.OracleError) as e:
+            nodim.serialize_snapshot()
+        assert e.value.code == 4
