@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "line_scan.cuh"
 #include "table.hpp"
 
 namespace mpzch_b200 {
@@ -59,6 +60,91 @@ __global__ void __launch_bounds__(256) k_lookup(TableDev t, const uint64_t* __re
         } else {
             out_slots[i] = base + h;
             out_oc[i] = kCollision;
+        }
+    }
+}
+
+// Quad line walk (line_scan.cuh): one quad per position, U positions in flight per quad,
+// 16 slots per round.  Used when windows run long (max_probe >= 256 or a full-window scan).
+template <bool kHoleFree, int U>
+__global__ void __launch_bounds__(256, 4) k_lookup_line(TableDev t, const uint64_t* __restrict__ ids,
+                                                        uint64_t n, uint64_t* __restrict__ out_slots,
+                                                        uint8_t* __restrict__ out_oc, BatchErr* err) {
+    constexpr uint8_t kPending = 0, kHit = 1, kStop = 2, kIdle = 3;
+    const unsigned j = quad_lane(), qm = quad_mask();
+    const uint64_t qpb = blockDim.x >> 2, qib = threadIdx.x >> 2, tile = qpb * U;
+    for (uint64_t t0 = (uint64_t)blockIdx.x * tile; t0 < n; t0 += (uint64_t)gridDim.x * tile) {
+        uint64_t id[U], g[U], home[U];
+        uint32_t off[U], sh[U];
+        uint8_t st[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = t0 + (uint64_t)u * qpb + qib;
+            st[u] = kIdle;
+            off[u] = 0;
+            if (i < n) {
+                id[u] = ids[i];
+                if (id[u] >> 63) {
+                    if (j == 0) atomicMin(&err->bad_pos, (unsigned long long)i);
+                    continue;
+                }
+                sh[u] = shard_of(id[u], t);
+                if (!holds_shard(t, sh[u])) {
+                    if (j == 0) atomicMin(&err->foreign_pos, (unsigned long long)i);
+                    continue;
+                }
+                const ShardDev sd = t.shards[sh[u]];
+                home[u] = sd.offset + home_of(id[u], sd, t.seed);
+                g[u] = home[u];
+                st[u] = kPending;
+            }
+        }
+        for (;;) {
+            uint64_t w[U][4];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (st[u] == kPending) ld_line_part(t.ident, g[u], j, w[u]);
+            bool any = false;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (st[u] != kPending) continue;
+                unsigned m = 0, e = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    m |= (unsigned)(w[u][k] == id[u]) << k;
+                    e |= (unsigned)(w[u][k] == kEmpty) << k;
+                }
+                const unsigned x = quad_gather(m, kHoleFree ? e : 0u, j, qm);
+                const ShardDev sd = t.shards[sh[u]];
+                const uint64_t base = sd.offset, end = base + sd.cap.d;
+                const LineSpan sp = line_span(g[u], end, off[u], t.P);
+                const unsigned hit = (x | (x >> 16)) & sp.range();
+                if (hit) {
+                    const unsigned p = __ffs(hit) - 1;
+                    st[u] = (x >> p) & 1u ? kHit : kStop;
+                    g[u] += p - sp.s;
+                } else {
+                    off[u] += sp.c;
+                    g[u] += sp.c;
+                    if (g[u] == end) g[u] = base;
+                    if (off[u] >= t.P) st[u] = kStop;
+                    else any = true;
+                }
+            }
+            if (!any) break;
+        }
+        if (j == 0) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t i = t0 + (uint64_t)u * qpb + qib;
+                if (st[u] == kHit) {
+                    out_slots[i] = g[u];
+                    out_oc[i] = kFound;
+                } else if (st[u] == kStop) {
+                    out_slots[i] = home[u];
+                    out_oc[i] = kCollision;
+                }
+            }
         }
     }
 }
@@ -138,10 +224,19 @@ void run_lookup_gather(const Table& t, const uint64_t* ids, uint64_t n, uint64_t
 
 void run_lookup(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots, uint8_t* out_oc,
                 BatchErr* err, cudaStream_t st) {
-    if (t.hole_free)
+    // long windows (max_probe >= 256, or the full-window scan of a table with holes): quad
+    // line walk; else the per-thread sector walk (remap_fast.cu has the same rule)
+    if (t.P >= 256 || !t.hole_free) {
+        const unsigned gl = grid_for(4 * ((n + 1) / 2), 256, 148u * 16u);
+        if (t.hole_free)
+            k_lookup_line<true, 2><<<gl, 256, 0, st>>>(t.dev, ids, n, out_slots, out_oc, err);
+        else
+            k_lookup_line<false, 2><<<gl, 256, 0, st>>>(t.dev, ids, n, out_slots, out_oc, err);
+    } else if (t.hole_free) {
         k_lookup<true><<<grid_for(n, 256), 256, 0, st>>>(t.dev, ids, n, out_slots, out_oc, err);
-    else
+    } else {
         k_lookup<false><<<grid_for(n, 256), 256, 0, st>>>(t.dev, ids, n, out_slots, out_oc, err);
+    }
 }
 
 }  // namespace mpzch_b200

@@ -30,7 +30,11 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "line_scan.cuh"
 #include "table.hpp"
+
+#include <cstdlib>
+#include <string>
 
 namespace mpzch_b200 {
 
@@ -272,6 +276,153 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
             }
         }
     }
+    for (int o = 16; o; o >>= 1) {
+        my_found += __shfl_xor_sync(0xffffffffu, my_found, o);
+        my_coll += __shfl_xor_sync(0xffffffffu, my_coll, o);
+        my_isec += __shfl_xor_sync(0xffffffffu, my_isec, o);
+        my_msec += __shfl_xor_sync(0xffffffffu, my_msec, o);
+    }
+    if (lane == 0) {
+        if (my_found) atomicAdd(&ctr->found, my_found);
+        if (my_coll) atomicAdd(&ctr->collision, my_coll);
+        if (my_isec) atomicAdd(&ctr->id_sectors, my_isec);
+        if (my_msec) atomicAdd(&ctr->meta_sectors, my_msec);
+    }
+}
+
+// K1 (line variant): one QUAD of lanes per position, U positions in flight per quad.  Each
+// scan round reads the whole 128-byte identity line of every pending position with one warp
+// instruction (lane j: sector j) -- the same cost per access as a single sector on B200
+// (line_scan.cuh) -- and finds the first match / EMPTY of the window part in that line with
+// one 16-bit mask.  Decisions, writes and the new-list append are made by lane 0 of the quad.
+template <int MODE, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint64_t* __restrict__ ids,
+                                                          uint64_t n, uint64_t now, uint64_t meta_value,
+                                                          BatchCounters* ctr,
+                                                          uint64_t* __restrict__ out_slots,
+                                                          uint8_t* __restrict__ out_oc,
+                                                          uint32_t* __restrict__ newpos,
+                                                          uint64_t* __restrict__ newid,
+                                                          uint32_t* __restrict__ newa,
+                                                          uint32_t* __restrict__ newm) {
+    if (batch_failed(&ctr->err)) return;
+    constexpr uint8_t kPending = 0, kHit = 1, kEmptyHit = 2, kExhausted = 3, kIdle = 4;
+    const unsigned lane = lane_id();
+    const unsigned j = quad_lane(), qm = quad_mask();
+    const uint64_t qpb = blockDim.x >> 2;  // quads per block
+    const uint64_t qib = threadIdx.x >> 2;
+    const uint64_t tile = qpb * U;
+    unsigned long long my_found = 0, my_coll = 0, my_isec = 0, my_msec = 0;
+    for (uint64_t t0 = (uint64_t)blockIdx.x * tile; t0 < n; t0 += (uint64_t)gridDim.x * tile) {
+        uint64_t id[U], g[U];
+        uint32_t off[U], sh[U];
+        uint8_t st[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = t0 + (uint64_t)u * qpb + qib;
+            st[u] = kIdle;
+            off[u] = 0;
+            if (i < n) {
+                id[u] = ids[i];
+                sh[u] = shard_of(id[u], t);
+                const ShardDev sd = t.shards[sh[u]];
+                g[u] = sd.offset + home_of(id[u], sd, t.seed);
+                st[u] = kPending;
+            }
+        }
+        for (;;) {
+            uint64_t w[U][4];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (st[u] == kPending) ld_line_part(t.ident, g[u], j, w[u]);
+            bool any = false;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (st[u] != kPending) continue;
+                unsigned m = 0, e = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    m |= (unsigned)(w[u][k] == id[u]) << k;
+                    e |= (unsigned)(w[u][k] == kEmpty) << k;
+                }
+                const unsigned x = quad_gather(m, e, j, qm);
+                const ShardDev sd = t.shards[sh[u]];
+                const uint64_t base = sd.offset, end = base + sd.cap.d;
+                const LineSpan sp = line_span(g[u], end, off[u], t.P);
+                const unsigned hit = (x | (x >> 16)) & sp.range();
+                if (hit) {
+                    const unsigned p = __ffs(hit) - 1;
+                    st[u] = (x >> p) & 1u ? kHit : kEmptyHit;
+                    off[u] += p - sp.s;
+                    g[u] += p - sp.s;
+                    my_isec += sp.sectors_to(p);
+                } else {
+                    my_isec += sp.sectors_to(sp.s + sp.c - 1);
+                    off[u] += sp.c;
+                    g[u] += sp.c;
+                    if (g[u] == end) g[u] = base;
+                    if (off[u] >= t.P) st[u] = kExhausted;
+                    else any = true;
+                }
+            }
+            if (!any) break;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = t0 + (uint64_t)u * qpb + qib;
+            bool is_new = false;
+            uint32_t a_off = 0, m_off = kNone32;
+            if (st[u] != kIdle) {
+                const ShardDev sd = t.shards[sh[u]];
+                const uint64_t base = sd.offset, cap = sd.cap.d;
+                const uint64_t h = home_of(id[u], sd, t.seed);
+                uint64_t fslot = kEmpty;
+                uint8_t foc = kFound;
+                if (MODE == kModeDisabled) {
+                    if (st[u] == kHit) fslot = g[u];
+                    else if (st[u] == kEmptyHit) { is_new = true; a_off = off[u]; }
+                    else { fslot = base + h; foc = kCollision; }
+                } else {  // TTL with one metadata value per batch
+                    if (st[u] == kHit) {
+                        ++my_msec;
+                        if (__ldg(t.meta + g[u]) >= now) {
+                            fslot = g[u];  // live: nobody can take it in this batch
+                        } else {           // expired own slot: lower-rank new ids contest it
+                            is_new = true;
+                            m_off = off[u];
+                            a_off = quad_first_expired(t.meta, base, h, cap, off[u], now, j, qm, my_msec);
+                        }
+                    } else {
+                        const uint32_t lim = st[u] == kEmptyHit ? off[u] : t.P;
+                        const uint32_t xo = quad_first_expired(t.meta, base, h, cap, lim, now, j, qm, my_msec);
+                        if (xo < lim || st[u] == kEmptyHit) { is_new = true; a_off = xo; }
+                        else { fslot = base + h; foc = kCollision; }
+                    }
+                }
+                if (fslot != kEmpty && j == 0) {
+                    out_slots[i] = fslot;
+                    out_oc[i] = foc;
+                    t.meta[fslot] = meta_value;  // Found refresh / Collision at home
+                    if (foc == kFound) ++my_found; else ++my_coll;
+                }
+            }
+            is_new = is_new && j == 0;
+            const unsigned mask = __ballot_sync(0xffffffffu, is_new);
+            if (mask) {
+                unsigned basek = 0;
+                if (lane == 0) basek = atomicAdd(&ctr->new_count, (unsigned)__popc(mask));
+                basek = __shfl_sync(0xffffffffu, basek, 0);
+                if (is_new) {
+                    const unsigned k = basek + __popc(mask & ((1u << lane) - 1));
+                    newpos[k] = (uint32_t)i;
+                    newid[k] = id[u];
+                    newa[k] = a_off;
+                    newm[k] = m_off;
+                }
+            }
+        }
+    }
+    if (j != 0) my_isec = my_msec = 0;  // every lane of a quad counted the same sectors
     for (int o = 16; o; o >>= 1) {
         my_found += __shfl_xor_sync(0xffffffffu, my_found, o);
         my_coll += __shfl_xor_sync(0xffffffffu, my_coll, o);
@@ -569,12 +720,25 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     t.launches += 2;
     if (a.overflow_all) return;  // validation only; the host reports the error
     if (t.profiling) cudaEventRecord(t.ev[0], st);
-    if (ttl)
-        k_probe<kModeTtl, kU><<<gP, B, 0, st>>>(t.dev, a.ids, n, a.now, a.uniform_meta, t.d_ctr,
-                                                a.out_slots, a.out_oc, newpos, newid, newa, newm);
-    else
-        k_probe<kModeDisabled, kU><<<gP, B, 0, st>>>(t.dev, a.ids, n, a.now, a.uniform_meta, t.d_ctr,
-                                                     a.out_slots, a.out_oc, newpos, newid, newa, newm);
+    // probe kernel: the quad line walk when windows run long (max_probe >= 256: at 0.95 load
+    // 16% of misses walk all 256 slots), else the per-thread sector walk (DESIGN.md section 4
+    // has the measurements behind the rule); MPZCH_PROBE=sector|line overrides it
+    static const int forced = [] {
+        const char* e = std::getenv("MPZCH_PROBE");
+        return !e ? -1 : (std::string(e) == "line" ? 1 : 0);
+    }();
+    const bool line = forced >= 0 ? forced == 1 : t.P >= 256;
+#define MPZCH_PROBE_ARGS t.dev, a.ids, n, a.now, a.uniform_meta, t.d_ctr, a.out_slots, a.out_oc, newpos, newid, newa, newm
+    if (line) {
+        constexpr int kUL = 2;
+        const unsigned gl = grid_for(4 * ((n + kUL - 1) / kUL), B, 148u * 16u);
+        if (ttl) k_probe_line<kModeTtl, kUL, 4><<<gl, B, 0, st>>>(MPZCH_PROBE_ARGS);
+        else k_probe_line<kModeDisabled, kUL, 4><<<gl, B, 0, st>>>(MPZCH_PROBE_ARGS);
+    } else {
+        if (ttl) k_probe<kModeTtl, kU><<<gP, B, 0, st>>>(MPZCH_PROBE_ARGS);
+        else k_probe<kModeDisabled, kU><<<gP, B, 0, st>>>(MPZCH_PROBE_ARGS);
+    }
+#undef MPZCH_PROBE_ARGS
     ++t.launches;
     if (t.profiling) cudaEventRecord(t.ev[1], st);
     IdEntry* te = t.s_tent.as<IdEntry>();

@@ -105,7 +105,7 @@ Table::Table(const uint64_t* cap_in, uint32_t num_shards, uint32_t max_probe, ui
     shard_hi = hi;
     row_lo = offsets[lo];
     row_hi = offsets[hi];
-    row_base = row_lo & ~3ull;
+    row_base = row_lo & ~15ull;  // identity/metadata lines are 128-byte aligned in global rows
     const uint64_t held = row_hi - row_lo;
 
     DeviceGuard g(device);
@@ -117,9 +117,9 @@ Table::Table(const uint64_t* cap_in, uint32_t num_shards, uint32_t max_probe, ui
     h_ctr = h_ring;
     d_ctr = d_ring;
     for (auto& sl : slots) MPZCH_CUDA(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
-    // identity/metadata start 4-row aligned and are padded so a 32-byte sector load at the
-    // first or last held slot stays in bounds
-    const uint64_t padded = ((row_hi - row_base + 3) & ~3ull) + 4;
+    // identity/metadata start 16-row (128-byte line) aligned and are padded to whole lines, so
+    // a line read (line_scan.cuh) at the first or last held slot stays in bounds
+    const uint64_t padded = ((row_hi - row_base + 15) & ~15ull) + 16;
     MPZCH_CUDA(cudaMalloc((void**)&ident, padded * sizeof(uint64_t)));
     MPZCH_CUDA(cudaMalloc((void**)&meta, padded * sizeof(uint64_t)));
     MPZCH_CUDA(cudaMalloc((void**)&row_gen, held * sizeof(uint64_t)));
