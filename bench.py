@@ -401,7 +401,7 @@ def main():
     value = BATCH * args.steps / (ms_total / 1e3)
 
     # e2e: host buffers in, host buffers out, through the public API (pinned memory)
-    e2e_steps = args.e2e_steps or max(3, args.steps // 2)
+    e2e_steps = args.e2e_steps or max(8, args.steps)
     e2e_batches = []
     for i in range(e2e_steps):
         idx, nf = batch_indices(torch, dev, npre, BATCH, nb + i, fresh_base, SAMPLER_SEED)
@@ -416,30 +416,39 @@ def main():
     torch.cuda.synchronize(dev)
     e2e_api = None
     if world == 1:
-        # pipelined service loop through the public API: H2D of step i+1, the remap of step i
-        # (mpzch_process_batch_device_async) and the D2H of step i-1 on three streams
-        # (PCIe is full duplex); every step's result is waited for (its ticket) and read back
+        # pipelined service loop through the public API: the H2D of step i, the remap of
+        # step i-1 (mpzch_process_batch_device_async) and the D2H of step i-2 overlap on three
+        # streams (PCIe is full duplex); D buffer sets, so the host only blocks on step i-D
+        # (its ticket -- errors reported exactly as the synchronous call would -- and its
+        # slots/outcomes on the host) before reusing that step's buffers
+        D = 4
         s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        d_ids = [torch.empty(nloc, dtype=torch.int64, device=dev) for _ in range(2)]
-        d_s = [torch.empty(nloc, dtype=torch.int64, device=dev) for _ in range(2)]
-        d_o = [torch.empty(nloc, dtype=torch.uint8, device=dev) for _ in range(2)]
-        h_s = [torch.empty(nloc, dtype=torch.int64).pin_memory() for _ in range(2)]
-        h_o = [torch.empty(nloc, dtype=torch.uint8).pin_memory() for _ in range(2)]
+        d_ids = [torch.empty(nloc, dtype=torch.int64, device=dev) for _ in range(D)]
+        d_s = [torch.empty(nloc, dtype=torch.int64, device=dev) for _ in range(D)]
+        d_o = [torch.empty(nloc, dtype=torch.uint8, device=dev) for _ in range(D)]
+        h_s = [torch.empty(nloc, dtype=torch.int64).pin_memory() for _ in range(D)]
+        h_o = [torch.empty(nloc, dtype=torch.uint8).pin_memory() for _ in range(D)]
         ev_in = [torch.cuda.Event() for _ in range(e2e_steps)]
         ev_cmp = [torch.cuda.Event() for _ in range(e2e_steps)]
         ev_out = [torch.cuda.Event() for _ in range(e2e_steps)]
         t0 = time.perf_counter()
         tickets = []
+        done_slots = 0
+
+        def retire(k):  # step k: its ticket waited and its results on the host
+            table.wait(tickets[k])
+            ev_out[k].synchronize()
+            return int(h_o[k % D][0])  # touch the host copy
+
         for i in range(e2e_steps):
-            j = i % 2
+            j = i % D
+            if i >= D:
+                retire(i - D)
+                done_slots += 1
             with torch.cuda.stream(s_in):
-                if i >= 2:
-                    s_in.wait_event(ev_cmp[i - 2])       # buffer j no longer read by step i-2
                 d_ids[j].copy_(e2e_batches[i], non_blocking=True)
                 ev_in[i].record(s_in)
             stream.wait_event(ev_in[i])
-            if i >= 2:
-                stream.wait_event(ev_out[i - 2])         # result buffers j drained
             tickets.append(table.process_batch_device_async(d_ids[j], 100 + i, pol, None,
                                                             d_s[j], d_o[j], None, stream))
             ev_cmp[i].record(stream)
@@ -448,15 +457,35 @@ def main():
                 h_s[j].copy_(d_s[j], non_blocking=True)
                 h_o[j].copy_(d_o[j], non_blocking=True)
                 ev_out[i].record(s_out)
-            if i >= 1:
-                table.wait(tickets[i - 1])
-                ev_out[i - 1].synchronize()            # step i-1's results are on the host
-        table.wait(tickets[-1])
-        ev_out[-1].synchronize()
+        for k in range(done_slots, e2e_steps):
+            retire(k)
         e2e_s = time.perf_counter() - t0
+        # the link's own ceiling for this traffic: the same H2D and D2H bytes per step copied
+        # concurrently with no remap in between (what the e2e number is bound by)
+        ev_a, ev_b, ev_c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        torch.cuda.synchronize(dev)
+        reps = 6
+        ev_a.record(stream)
+        s_in.wait_event(ev_a)
+        s_out.wait_event(ev_a)
+        for r in range(reps):
+            with torch.cuda.stream(s_in):
+                d_ids[r % D].copy_(e2e_batches[r % e2e_steps], non_blocking=True)
+            with torch.cuda.stream(s_out):
+                h_s[r % D].copy_(d_s[r % D], non_blocking=True)
+                h_o[r % D].copy_(d_o[r % D], non_blocking=True)
+        ev_b.record(s_in)
+        ev_c.record(s_out)
+        torch.cuda.synchronize(dev)
+        link_ms = max(ev_a.elapsed_time(ev_b), ev_a.elapsed_time(ev_c)) / reps
+        pcie_bound = BATCH / (link_ms / 1e3)
         e2e_api = ("mpzch_process_batch_device_async + pinned H2D/D2H on separate streams "
                    "(each step's ticket waited and its slots/outcomes read back)")
-        # the plain synchronous host-buffer call, for reference
+        # the plain synchronous host-buffer call, for reference (one untimed call first: it
+        # sizes the handle's host-path staging buffers)
+        table.process_batch(e2e_batches[0].numpy().view(np.uint64), 199, pol,
+                            out_slots=pin_s.numpy().view(np.uint64), out_outcomes=pin_o.numpy(),
+                            out_evicted=pin_ev)
         t1 = time.perf_counter()
         for i in range(min(3, e2e_steps)):
             table.process_batch(e2e_batches[i].numpy().view(np.uint64), 200 + i, pol,
@@ -474,6 +503,7 @@ def main():
         e2e_s = time.perf_counter() - t0
         e2e_api = "ShardedMpzchTable.process_batch (pinned host slices, H2D/D2H timed)"
         e2e_sync_value = None
+        pcie_bound = None
     if world > 1:
         tt = torch.tensor([e2e_s], device=red_dev, dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -533,7 +563,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "IDs/s", "h2d_bytes_per_step": BATCH * 8,
                     "d2h_bytes_per_step": BATCH * 9, "steps": e2e_steps, "api": e2e_api,
-                    "synchronous_host_call_value": e2e_sync_value},
+                    "synchronous_host_call_value": e2e_sync_value,
+                    "pcie_copy_only_ids_per_s": pcie_bound},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }

@@ -24,8 +24,10 @@
 //                 fixpoint -- each entry on the first slot no lower rank holds -- is
 //                 reached in one launch with no grid barrier.
 //   K4 commit     claim words -> ids, outcomes (Inserted/Evicted/Found-owner), the entry's
-//                 metadata word, touch_row, reset list, evicted flags by rank.
-//   K5 finalize   per new position result (+ secondary (id, f') rule).
+//                 metadata word, touch_row, reset list, evicted flags by rank, and the
+//                 result of the entry's own (first) position.
+//   K5 finalize   results of the later positions of repeated new ids (+ secondary (id, f')
+//                 rule); a no-op when the dedup saw no repeated id.
 // One metadata value per batch makes every metadata write order-free.
 #include <cuda_runtime.h>
 
@@ -83,16 +85,28 @@ __device__ __forceinline__ uint64_t wrap_add(uint64_t h, uint64_t off, uint64_t 
     return x >= cap ? x - cap : x;
 }
 
-__device__ __forceinline__ uint64_t pick4(uint32_t j, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
-    return j == 0 ? a : (j == 1 ? b : (j == 2 ? c : d));
-}
-
 // Id-table sizing: power of two >= 2 * count, at least 1024, at most the allocation.
+// (Sizing by positions instead, so the probe could prefetch records, measured slower.)
 __device__ __forceinline__ uint64_t table_mask(unsigned count, uint64_t cap_alloc) {
     uint64_t c = 1024;
     while (c < 2ull * count && c < cap_alloc) c <<= 1;
     return c - 1;
 }
+
+__device__ __forceinline__ uint64_t te_home(uint64_t id, uint64_t mask) {
+    return mix64(id, 0x2545F4914F6CDD1Dull) & mask;
+}
+
+__device__ __forceinline__ u128 ld_cg_u128(const u128* p) {
+    uint64_t lo, hi;
+    asm volatile("ld.global.cg.v2.u64 {%0,%1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(p));
+    return ((u128)hi << 64) | lo;
+}
+
+__device__ __forceinline__ uint64_t pick4(uint32_t j, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+    return j == 0 ? a : (j == 1 ? b : (j == 2 ? c : d));
+}
+
 
 __global__ void k_init_counters(BatchCounters* c) {
     if (threadIdx.x == 0) {
@@ -135,7 +149,19 @@ __global__ void __launch_bounds__(256) k_validate(TableDev t, const uint64_t* __
     if ((reinterpret_cast<uintptr_t>(ids) & 15) == 0) {
         const uint64_t n2 = n / 2;
         const ulonglong2* v2 = reinterpret_cast<const ulonglong2*>(ids);
-        for (uint64_t q = tid; q < n2; q += stride) {
+        uint64_t q = tid;
+        for (; q + 3 * stride < n2; q += 4 * stride) {  // four 16-byte loads in flight
+            ulonglong2 v[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) v[r] = __ldcs(v2 + q + r * stride);
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                if ((v[r].x | v[r].y) >> 63) {
+                    const uint64_t qq = q + r * stride;
+                    bad = min(bad, (unsigned long long)(v[r].x >> 63 ? 2 * qq : 2 * qq + 1));
+                }
+        }
+        for (; q < n2; q += stride) {
             const ulonglong2 v = __ldcs(v2 + q);
             if ((v.x | v.y) >> 63) bad = min(bad, (unsigned long long)(v.x >> 63 ? 2 * q : 2 * q + 1));
         }
@@ -447,15 +473,19 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
     if (batch_failed(&ctr->err)) return;
     const unsigned cnt = ctr->new_count;
     const uint64_t mask = table_mask(cnt, tcap);
+    unsigned dups = 0;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
         const uint64_t id = newid[k];
         const u128 mine = make_key(epoch, id);
-        uint64_t h = mix64(id, 0x2545F4914F6CDD1Dull) & mask;
+        uint64_t h = te_home(id, mask);
         uint32_t e;
         for (;;) {
-            // atomic 128-bit read (a CAS that can only write back the value it found):
-            // a plain 16-byte load is not guaranteed single-copy atomic
-            u128 cur = atomicCAS(&te[h].key, (u128)0, (u128)0);
+            // a plain 16-byte L2 load first (one round trip less than an atomic read on the
+            // common path, a stale entry of an older epoch).  It is not single-copy atomic: a
+            // torn value can only fail the CAS below, or -- if it shows the current epoch --
+            // is re-read atomically before it is trusted.
+            u128 cur = ld_cg_u128(&te[h].key);
+            if (key_epoch(cur) == epoch) cur = atomicCAS(&te[h].key, (u128)0, (u128)0);
             if (key_epoch(cur) != epoch) {  // empty for this batch: try to take it
                 const u128 old = atomicCAS(&te[h].key, cur, mine);
                 if (old == cur) {  // inserted: publish the entry's probe facts
@@ -471,6 +501,7 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
             }
             if (key_id(cur) == id) {
                 e = (uint32_t)h;
+                ++dups;
                 break;
             }
             h = (h + 1) & mask;
@@ -478,6 +509,8 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
         atomicMax(&te[e].rank, (unsigned long long)((epoch << 32) | (uint32_t)~newpos[k]));
         newent[k] = e;
     }
+    for (int o = 16; o; o >>= 1) dups += __shfl_xor_sync(0xffffffffu, dups, o);
+    if (lane_id() == 0 && dups) atomicAdd(&ctr->dup_items, dups);
 }
 
 // The primary item of an entry (the new-list item at the id's first position) does the
@@ -606,9 +639,13 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
                                                 uint64_t meta_value,
                                                 uint64_t* __restrict__ reset_rows,
                                                 uint8_t* __restrict__ evflag,
-                                                uint64_t* __restrict__ evslot) {
+                                                uint64_t* __restrict__ evslot,
+                                                uint64_t* __restrict__ out_slots,
+                                                uint8_t* __restrict__ out_oc) {
     if (batch_failed(&ctr->err)) return;
     const unsigned cnt = ctr->new_count;
+    unsigned long long c[4] = {0, 0, 0, 0};
+    unsigned np = 0;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
         const uint32_t e = newent[k];
         const uint32_t rank = newpos[k];
@@ -649,11 +686,29 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
         }
         te[e].slot = g;
         te[e].oc = oc;
+        // the primary item's own position (its feature is the entry's): result written
+        // here, so K5 only has items of repeated ids left
+        out_slots[rank] = g;
+        out_oc[rank] = oc;
+        ++c[oc];
+        ++np;
+    }
+    for (int j = 0; j < 4; ++j)
+        for (int o = 16; o; o >>= 1) c[j] += __shfl_xor_sync(0xffffffffu, c[j], o);
+    for (int o = 16; o; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
+    if (lane_id() == 0) {
+        if (c[0]) atomicAdd(&ctr->found, c[0]);
+        if (c[1]) atomicAdd(&ctr->inserted, c[1]);
+        if (c[2]) atomicAdd(&ctr->evicted, c[2]);
+        if (c[3]) atomicAdd(&ctr->collision, c[3]);
+        if (np) atomicAdd(&ctr->entry_count, np);
     }
 }
 
-// K5: results of the new positions (+ (id, f') secondaries: same id, other feature, later
-// first position -> Found on the primary's slot, or Collision if the primary collided).
+// K5: results of the non-primary items -- later positions of a repeated new id: the
+// primary's slot and outcome, or, for an (id, f') secondary (same id, other feature, later
+// first position), Found on the primary's slot / Collision if the primary collided.  Primary
+// items got their result in K4; without repeated ids (dup_items == 0) this is a no-op.
 __global__ void __launch_bounds__(256) k_finalize(BatchCounters* ctr,
                                                   const uint32_t* __restrict__ feats,
                                                   const uint32_t* __restrict__ newpos,
@@ -661,14 +716,16 @@ __global__ void __launch_bounds__(256) k_finalize(BatchCounters* ctr,
                                                   const IdEntry* te,
                                                   uint64_t* __restrict__ out_slots,
                                                   uint8_t* __restrict__ out_oc) {
-    if (batch_failed(&ctr->err)) return;
+    if (batch_failed(&ctr->err) || ctr->dup_items == 0) return;
     const unsigned cnt = ctr->new_count;
     unsigned long long c[4] = {0, 0, 0, 0};
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
         const uint32_t pos = newpos[k];
         const uint32_t e = newent[k];
+        const uint32_t first = rank_of(te[e].rank);
+        if (first == pos) continue;  // primary: done in K4
         uint8_t oc = te[e].oc;
-        if (feats && feats[pos] != feats[rank_of(te[e].rank)]) oc = oc == kCollision ? kCollision : kFound;
+        if (feats && feats[pos] != feats[first]) oc = oc == kCollision ? kCollision : kFound;
         out_slots[pos] = te[e].slot;
         out_oc[pos] = oc;
         ++c[oc];
@@ -681,12 +738,6 @@ __global__ void __launch_bounds__(256) k_finalize(BatchCounters* ctr,
         if (c[2]) atomicAdd(&ctr->evicted, c[2]);
         if (c[3]) atomicAdd(&ctr->collision, c[3]);
     }
-    // distinct new ids of the batch (stats): count primary items
-    unsigned np = 0;
-    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x)
-        np += is_primary(te, newent[k], newpos[k]);
-    for (int o = 16; o; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
-    if (lane_id() == 0 && np) atomicAdd(&ctr->entry_count, np);
 }
 
 }  // namespace
@@ -749,7 +800,8 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     if (t.profiling) cudaEventRecord(t.ev[5], st);                                               \
     k_commit<MODE><<<gW, B, 0, st>>>(t.dev, t.d_ctr, newpos, newid, newent, te, t.gen_clock,      \
                                      a.uniform_meta, t.s_reset.as<uint64_t>(),                     \
-                                     t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>())
+                                     t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>(),         \
+                                     a.out_slots, a.out_oc)
     if (ttl) { MPZCH_CLAIM_COMMIT(kModeTtl); }
     else { MPZCH_CLAIM_COMMIT(kModeDisabled); }
 #undef MPZCH_CLAIM_COMMIT

@@ -52,6 +52,8 @@ struct BatchCounters {
     unsigned long long found, inserted, evicted, collision;  // per position
     unsigned int overflow_list;  // claim-log overflow (defensive)
     unsigned int pad;
+    unsigned int dup_items;      // fast path: new-list items whose id was already in the id table
+    unsigned int pad2;
     unsigned long long id_sectors, meta_sectors;  // sectors the probe kernel read
     // rounds path (device-driven): pending count per round parity, new suspects per closure
     // step parity, lowest rank among the unmarked last-step suspects, rounds run, uniques left
