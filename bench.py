@@ -173,6 +173,20 @@ def random_sector_ceiling():
         return None
 
 
+def random_access_ceiling():
+    """Measured random DRAM access rate (tools/sector_probe.cu): G accesses/s over a 16 GiB
+    array for 32-byte reads -- the same rate holds for 128-byte line reads -- and for 8-byte
+    writes (profiles/line_ceiling_r01.json)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "line_ceiling_r01.json")))
+        t = [r for r in d["timings"] if r.get("gib") == 16]
+        rd = max(r.get("G_sectors_s", r.get("G_accesses_s", 0)) for r in t if r["kernel"].startswith("cg_"))
+        w8 = max(r["G_sectors_s"] for r in t if r["kernel"] == "write8")
+        return {"read_g_per_s": rd, "write8_g_per_s": w8}
+    except Exception:
+        return None
+
+
 def ncu_traffic():
     """dram bytes per probe launch from the committed ncu --set full summary, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_probe_summary.json")
@@ -552,6 +566,7 @@ def main():
                          "probe_sectors_per_launch": prof["probe_sectors"] / max(prof["probe_launches"], 1),
                          "launch_ms": probe_ms, "peak_source": peak_src,
                          "random_sector_ceiling_gbs": random_sector_ceiling(),
+                         "random_access_ceiling": random_access_ceiling(),
                          "share_of_step": probe_ms / ms_step,
                          "batch_algorithmic_bytes": batch_bytes,
                          "batch_gbs": batch_bytes / (batch_ms / 1e3) / 1e9 if batch_ms else 0.0,
