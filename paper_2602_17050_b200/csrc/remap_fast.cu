@@ -257,9 +257,10 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
             if (st[u] != kIdle) {
                 uint64_t fslot = kEmpty;
                 uint8_t foc = kFound;
-                if (MODE == kModeDisabled) {
+                if (MODE != kModeTtl) {
                     if (st[u] == kHit) fslot = g[u];
                     else if (st[u] == kEmptyHit) { is_new = true; a_off = off[u]; }
+                    else if (MODE == kModeLru) atomicExch(&ctr->lru_abort, 1u);  // would evict
                     else { fslot = base[u] + h[u]; foc = kCollision; }
                 } else {  // TTL with one metadata value per batch
                     if (st[u] == kHit) {
@@ -281,7 +282,9 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
                 if (fslot != kEmpty) {
                     out_slots[i] = fslot;
                     out_oc[i] = foc;
-                    t.meta[fslot] = meta_value;  // Found refresh / Collision at home
+                    // Found refresh / Collision at home (LRU: deferred to k_lru_meta, the
+                    // batch may still turn out to need an eviction)
+                    if (MODE != kModeLru) t.meta[fslot] = meta_value;
                     if (foc == kFound) ++my_found; else ++my_coll;
                 }
             }
@@ -404,9 +407,10 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
                 const uint64_t h = home_of(id[u], sd, t.seed);
                 uint64_t fslot = kEmpty;
                 uint8_t foc = kFound;
-                if (MODE == kModeDisabled) {
+                if (MODE != kModeTtl) {
                     if (st[u] == kHit) fslot = g[u];
                     else if (st[u] == kEmptyHit) { is_new = true; a_off = off[u]; }
+                    else if (MODE == kModeLru) { if (j == 0) atomicExch(&ctr->lru_abort, 1u); }
                     else { fslot = base + h; foc = kCollision; }
                 } else {  // TTL with one metadata value per batch
                     if (st[u] == kHit) {
@@ -428,7 +432,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
                 if (fslot != kEmpty && j == 0) {
                     out_slots[i] = fslot;
                     out_oc[i] = foc;
-                    t.meta[fslot] = meta_value;  // Found refresh / Collision at home
+                    if (MODE != kModeLru) t.meta[fslot] = meta_value;  // (LRU: k_lru_meta)
                     if (foc == kFound) ++my_found; else ++my_coll;
                 }
             }
@@ -525,7 +529,7 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                                                const uint32_t* __restrict__ newpos,
                                                const uint32_t* __restrict__ newent,
                                                IdEntry* te) {
-    if (batch_failed(&ctr->err)) return;
+    if (batch_failed(&ctr->err) || (MODE == kModeLru && ctr->lru_abort)) return;
     const unsigned cnt = ctr->new_count;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
         uint32_t e = newent[k];
@@ -605,7 +609,12 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                     }
                     if (held) break;
                 }
-                if (!held) te[e].state = kStateCollided;
+                if (!held) {
+                    te[e].state = kStateCollided;
+                    // LRU: a full window evicts its least recently used slot -- order-dependent
+                    // on in-batch refreshes, so the batch goes to the rounds path instead
+                    if (MODE == kModeLru) atomicExch(&ctr->lru_abort, 1u);
+                }
             }
             if (next == kNone32) break;
             // take over the displaced entry: it resumes right after the slot it lost,
@@ -642,7 +651,7 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
                                                 uint64_t* __restrict__ evslot,
                                                 uint64_t* __restrict__ out_slots,
                                                 uint8_t* __restrict__ out_oc) {
-    if (batch_failed(&ctr->err)) return;
+    if (batch_failed(&ctr->err) || (MODE == kModeLru && ctr->lru_abort)) return;
     const unsigned cnt = ctr->new_count;
     unsigned long long c[4] = {0, 0, 0, 0};
     unsigned np = 0;
@@ -705,6 +714,37 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
     }
 }
 
+// LRU attempt aborted after K3: put every claimed slot back to EMPTY (only EMPTY slots are
+// claimable outside TTL, and every claimed slot ends held by exactly one entry -- the one
+// whose last claim offset points at it), so the rounds path starts from the pre-batch state.
+__global__ void __launch_bounds__(256) k_lru_revert(TableDev t, BatchCounters* ctr,
+                                                    const uint32_t* __restrict__ newpos,
+                                                    const uint32_t* __restrict__ newent,
+                                                    const IdEntry* te) {
+    if (batch_failed(&ctr->err) || !ctr->lru_abort) return;
+    const unsigned cnt = ctr->new_count;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
+        const uint32_t e = newent[k];
+        if (!is_primary(te, e, newpos[k]) || te[e].state == kStateCollided) continue;
+        const uint64_t id = key_id(te[e].key);
+        const ShardDev sd = t.shards[shard_of(id, t)];
+        const uint64_t g = sd.offset + wrap_add(home_of(id, sd, t.seed), te[e].held, sd.cap.d);
+        const uint64_t v = t.ident[g];
+        if (is_claim(v) && claim_entry(v) == e) t.ident[g] = kEmpty;
+    }
+}
+
+// LRU batch that needed no eviction: it is a Disabled batch whose metadata writes were held
+// back; every position's final slot gets the batch's metadata value (Found refresh; new ids'
+// slots were written in K4 already -- the same word).
+__global__ void __launch_bounds__(256) k_lru_meta(TableDev t, const BatchCounters* ctr, uint64_t n,
+                                                  const uint64_t* __restrict__ out_slots,
+                                                  uint64_t meta_value) {
+    if (batch_failed(&ctr->err) || ctr->lru_abort) return;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        t.meta[out_slots[i]] = meta_value;
+}
+
 // K5: results of the non-primary items -- later positions of a repeated new id: the
 // primary's slot and outcome, or, for an (id, f') secondary (same id, other feature, later
 // first position), Found on the primary's slot / Collision if the primary collided.  Primary
@@ -716,7 +756,7 @@ __global__ void __launch_bounds__(256) k_finalize(BatchCounters* ctr,
                                                   const IdEntry* te,
                                                   uint64_t* __restrict__ out_slots,
                                                   uint8_t* __restrict__ out_oc) {
-    if (batch_failed(&ctr->err) || ctr->dup_items == 0) return;
+    if (batch_failed(&ctr->err) || ctr->dup_items == 0 || ctr->lru_abort) return;
     const unsigned cnt = ctr->new_count;
     unsigned long long c[4] = {0, 0, 0, 0};
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
@@ -760,6 +800,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     const unsigned gW = grid_for(n, B, 148u * 8u);  // count-driven kernels
     const unsigned gP = grid_for((n + kU - 1) / kU, B, 148u * 16u);
     const bool ttl = a.pol->mode == kModeTtl;
+    const bool lru = a.pol->mode == kModeLru;
     uint32_t* newpos = t.s_newpos.as<uint32_t>();
     uint64_t* newid = t.s_newid.as<uint64_t>();
     uint32_t* newa = t.s_newa.as<uint32_t>();
@@ -784,9 +825,11 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
         constexpr int kUL = 2;
         const unsigned gl = grid_for(4 * ((n + kUL - 1) / kUL), B, 148u * 16u);
         if (ttl) k_probe_line<kModeTtl, kUL, 4><<<gl, B, 0, st>>>(MPZCH_PROBE_ARGS);
+        else if (lru) k_probe_line<kModeLru, kUL, 4><<<gl, B, 0, st>>>(MPZCH_PROBE_ARGS);
         else k_probe_line<kModeDisabled, kUL, 4><<<gl, B, 0, st>>>(MPZCH_PROBE_ARGS);
     } else {
         if (ttl) k_probe<kModeTtl, kU><<<gP, B, 0, st>>>(MPZCH_PROBE_ARGS);
+        else if (lru) k_probe<kModeLru, kU><<<gP, B, 0, st>>>(MPZCH_PROBE_ARGS);
         else k_probe<kModeDisabled, kU><<<gP, B, 0, st>>>(MPZCH_PROBE_ARGS);
     }
 #undef MPZCH_PROBE_ARGS
@@ -803,6 +846,16 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
                                      t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>(),         \
                                      a.out_slots, a.out_oc)
     if (ttl) { MPZCH_CLAIM_COMMIT(kModeTtl); }
+    else if (lru) {
+        k_claim<kModeLru><<<gW, B, 0, st>>>(t.dev, a.now, t.d_ctr, newpos, newent, te);
+        if (t.profiling) cudaEventRecord(t.ev[5], st);
+        k_lru_revert<<<gW, B, 0, st>>>(t.dev, t.d_ctr, newpos, newent, te);
+        k_commit<kModeLru><<<gW, B, 0, st>>>(t.dev, t.d_ctr, newpos, newid, newent, te, t.gen_clock,
+                                             a.uniform_meta, t.s_reset.as<uint64_t>(),
+                                             t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>(),
+                                             a.out_slots, a.out_oc);
+        t.launches += 1;
+    }
     else { MPZCH_CLAIM_COMMIT(kModeDisabled); }
 #undef MPZCH_CLAIM_COMMIT
     t.launches += 3;
@@ -810,6 +863,10 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     k_finalize<<<gW, B, 0, st>>>(t.d_ctr, a.feats, newpos, newent, te, a.out_slots, a.out_oc);
     if (t.profiling) cudaEventRecord(t.ev[6], st);
     ++t.launches;
+    if (lru) {
+        k_lru_meta<<<grid_for(n, B, 148u * 8u), B, 0, st>>>(t.dev, t.d_ctr, n, a.out_slots, a.uniform_meta);
+        ++t.launches;
+    }
     if (t.dim > 0) launch_reset_rows(t, t.s_reset.as<uint64_t>(), &t.d_ctr->reset_count, st);
     if (a.out_mark) {  // first positions of Evicted uniques (row-sharded evicted list)
         if (ttl) MPZCH_CUDA(cudaMemcpyAsync(a.out_mark, t.s_evflag.p, n, cudaMemcpyDeviceToDevice, st));

@@ -461,13 +461,30 @@ uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uin
         a.d_featk = t.s_featk.as<uint32_t>();
         a.d_featv = t.s_featv.as<uint64_t>();
     }
-    const bool fast = t.path_override == MPZCH_PATH_AUTO && t.hole_free &&
-                      pol.mode != kModeLru && a.uniform && n <= (1ull << 29);
-    const bool rounds = !fast && t.hole_free && t.path_override != MPZCH_PATH_ORDERED;
+    bool fast = t.path_override == MPZCH_PATH_AUTO && t.hole_free && a.uniform && n <= (1ull << 29);
     const bool profiled = t.profiling;
-    if (!fast) t.profiling = false;  // events are recorded by the fast path only
-    if (fast) enqueue_fast_batch(t, a, st);
-    else enqueue_ordered_batch(t, a, st, rounds);
+    const bool lru_try = fast && pol.mode == kModeLru;
+    if (lru_try) {
+        // LRU differs from Disabled only when a new id finds its window full (it evicts the
+        // least recently used slot, which depends on the batch's own refreshes).  Try the
+        // claim path with metadata writes held back; if any window is full it reverts its
+        // claims on the device and the batch goes to the rounds path (one host round trip).
+        t.profiling = false;
+        enqueue_fast_batch(t, a, st);
+        MPZCH_CUDA(cudaMemcpyAsync(t.h_ctr, t.d_ctr, sizeof(BatchCounters), cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaStreamSynchronize(st));
+        const BatchErr& e = t.h_ctr->err;
+        const bool failed = e.bad_pos != ~0ull || e.overflow || e.too_many || e.foreign_pos != ~0ull;
+        fast = failed || !t.h_ctr->lru_abort;
+        if (!fast) ++t.lru_fallbacks;
+    } else if (fast) {
+        enqueue_fast_batch(t, a, st);
+    }
+    const bool rounds = !fast && t.hole_free && t.path_override != MPZCH_PATH_ORDERED;
+    if (!fast) {
+        t.profiling = false;  // events are recorded by the fast path only
+        enqueue_ordered_batch(t, a, st, rounds);
+    }
     t.profiling = profiled;
     MPZCH_CUDA(cudaGetLastError());
     MPZCH_CUDA(cudaMemcpyAsync(t.h_ctr, t.d_ctr, sizeof(BatchCounters), cudaMemcpyDeviceToHost, st));
@@ -478,7 +495,7 @@ uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uin
     sl.fast = fast;
     sl.path = fast ? MPZCH_PATH_AUTO : (rounds ? MPZCH_PATH_ROUNDS : MPZCH_PATH_ORDERED);
     sl.overflow_all = a.overflow_all;
-    sl.profiled = profiled;
+    sl.profiled = profiled && fast && !lru_try;  // per-kernel events: plain fast batches only
     t.last_stream = st;
     t.last_ticket = ticket;
     return ticket;

@@ -53,7 +53,7 @@ struct BatchCounters {
     unsigned int overflow_list;  // claim-log overflow (defensive)
     unsigned int pad;
     unsigned int dup_items;      // fast path: new-list items whose id was already in the id table
-    unsigned int pad2;
+    unsigned int lru_abort;      // LRU on the fast path: an eviction is needed -> rounds path
     unsigned long long id_sectors, meta_sectors;  // sectors the probe kernel read
     // rounds path (device-driven): pending count per round parity, new suspects per closure
     // step parity, lowest rank among the unmarked last-step suspects, rounds run, uniques left
@@ -102,6 +102,7 @@ public:
     uint64_t gen_clock = 1;  // MpzchTable::generation_clock_
     bool hole_free = true;   // SURVEY A.2 invariant; false after raw imports
     int path_override = MPZCH_PATH_AUTO;
+    uint64_t lru_fallbacks = 0;  // LRU batches that needed an eviction (claim attempt reverted)
     mpzch_batch_stats last{};
     uint64_t launches = 0;
     bool profiling = false;

@@ -567,3 +567,34 @@ def test_lru_and_feature_ttl_streams_all_paths(oracle, path, shards):
         t = run_stream(oracle, caps, 16, 5, 4, 3, batches, mode, dttl, pf, path, check_state_every=4)
         if path == "auto":
             assert t.last_stats()["path"] == "rounds"
+
+
+@pytest.mark.parametrize("line", [False, True])
+def test_lru_claim_path_and_fallback(oracle, line):
+    """LRU batches go to the claim path while no new id meets a full window (metadata writes
+    held back, then applied); a batch that needs an eviction -- found by the probe (pre-batch
+    full window) or by the claims (window filled by lower ranks in the batch) -- reverts its
+    claims on the device and runs the rounds path.  Both kinds of batch, with features, against
+    the oracle, state compared after every batch."""
+    rows = 1 << 12
+    caps = mz.even_capacities(rows, 4)
+    uni = oracle.distinct_ids(31, 0, int(rows * 1.25))
+    rng = np.random.default_rng(7)
+    batches, fill = [], 0
+    for b in range(16):
+        n = 600
+        lo = 0 if b < 6 else fill // 2   # early batches: a sparse table, no full window
+        fill = min(uni.size, fill + 350)
+        f = rng.integers(0, 2, n).astype(np.uint32) if b % 3 == 0 else None
+        batches.append((uni[rng.integers(lo, max(fill, 1), n)], f, 50 + 3 * b))
+    paths = []
+    t = mz.MpzchTable(mz.TableConfig(caps, 8 if not line else 256, 5, 4, 9))
+    o = oracle.OracleTable(caps, 8 if not line else 256, 5, 4, 9)
+    p = mz.EvictionPolicy.lru()
+    for bi, (ids, f, now) in enumerate(batches):
+        gs, go, ge = t.process_batch(ids, now, p, f)
+        os_, oo, oe = o.process_batch(ids, now, 2, 0, None, f)
+        assert (gs == os_).all() and (go == oo).all() and (ge == oe).all(), f"batch {bi}"
+        assert_same_state(gpu_state(t, 4), oracle_state(o, 4), f"batch {bi}")
+        paths.append(t.last_stats()["path"])
+    assert "fast" in paths and "rounds" in paths, paths
