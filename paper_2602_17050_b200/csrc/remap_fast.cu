@@ -494,10 +494,10 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
                 const u128 old = atomicCAS(&te[h].key, cur, mine);
                 if (old == cur) {  // inserted: publish the entry's probe facts
                     e = (uint32_t)h;
-                    te[e].a = newa[k];
-                    te[e].m = newm[k];
-                    te[e].held = 0;
-                    te[e].state = 0;
+                    // a | m << 32, then held = state = oc = 0: two 8-byte stores
+                    uint64_t* w = reinterpret_cast<uint64_t*>(&te[e].a);
+                    w[0] = (uint64_t)newa[k] | ((uint64_t)newm[k] << 32);
+                    w[1] = 0;
                     break;
                 }
                 cur = old;
@@ -517,6 +517,25 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
     if (lane_id() == 0 && dups) atomicAdd(&ctr->dup_items, dups);
 }
 
+// The entry's bookkeeping words in two 16-byte loads: (rank, a | m << 32) and
+// (held | state << 32 | oc << 40, slot).
+struct EntryView {
+    unsigned long long rank;
+    uint32_t a, m, held;
+    uint8_t state;
+};
+__device__ __forceinline__ EntryView load_entry(const IdEntry* te, uint32_t e) {
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(&te[e].rank);
+    const ulonglong2 w1 = p[0], w2 = p[1];
+    EntryView v;
+    v.rank = w1.x;
+    v.a = (uint32_t)w1.y;
+    v.m = (uint32_t)(w1.y >> 32);
+    v.held = (uint32_t)w2.x;
+    v.state = (uint8_t)(w2.x >> 32);
+    return v;
+}
+
 // The primary item of an entry (the new-list item at the id's first position) does the
 // entry's work in K3/K4; every other item of the same id only reads the result in K5.
 __device__ __forceinline__ bool is_primary(const IdEntry* te, uint32_t e, uint32_t pos) {
@@ -533,12 +552,14 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
     const unsigned cnt = ctr->new_count;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
         uint32_t e = newent[k];
-        if (!is_primary(te, e, newpos[k])) continue;
+        EntryView ev = load_entry(te, e);
+        if (rank_of(ev.rank) != newpos[k]) continue;  // not the primary item
         bool fresh = true;
         uint32_t resume = 0;
         for (;;) {
-            const uint64_t id = key_id(te[e].key);
-            const uint32_t rank = rank_of(te[e].rank);
+            if (!fresh) ev = load_entry(te, e);  // a taken-over entry
+            const uint64_t id = *reinterpret_cast<const uint64_t*>(&te[e].key);
+            const uint32_t rank = rank_of(ev.rank);
             const uint32_t s = shard_of(id, t);
             const ShardDev sd = t.shards[s];
             const uint64_t cap = sd.cap.d, base = sd.offset;
@@ -548,9 +569,9 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
             uint64_t gnext = 0;
             bool held = false;
             uint32_t off;
-            if (MODE == kModeTtl && fresh && te[e].m != kNone32) {
+            if (MODE == kModeTtl && fresh && ev.m != kNone32) {
                 // owner: try to keep (refresh) the expired slot holding our own id
-                const uint32_t m = te[e].m;
+                const uint32_t m = ev.m;
                 const uint64_t gm = base + wrap_add(h, m, cap);
                 uint64_t v = ld_cg(t.ident + gm);
                 for (;;) {
@@ -567,9 +588,9 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                     }
                     v = old;
                 }
-                off = te[e].a;
+                off = ev.a;
             } else {
-                off = fresh ? te[e].a : resume;
+                off = fresh ? ev.a : resume;
             }
             if (!held) {
                 // sector-wide scan: one L2 read per 4 slots; a slot is re-read only through
@@ -653,12 +674,14 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
                                                 uint8_t* __restrict__ out_oc) {
     if (batch_failed(&ctr->err) || (MODE == kModeLru && ctr->lru_abort)) return;
     const unsigned cnt = ctr->new_count;
+    const bool dups = ctr->dup_items != 0;
     unsigned long long c[4] = {0, 0, 0, 0};
     unsigned np = 0;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
         const uint32_t e = newent[k];
         const uint32_t rank = newpos[k];
-        if (!is_primary(te, e, rank)) continue;
+        const EntryView ev = load_entry(te, e);
+        if (rank_of(ev.rank) != rank) continue;  // not the primary item
         const uint64_t id = newid[k];
         const uint32_t s = shard_of(id, t);
         const ShardDev sd = t.shards[s];
@@ -669,12 +692,12 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
         uint64_t g = base + h;
         uint64_t v = 0;
         bool ok = true;
-        if (MODE == kModeTtl && te[e].m != kNone32 &&
-            ((v = t.ident[base + wrap_add(h, te[e].m, cap)]) & ~kFlagEmpty) == mine) {
-            g = base + wrap_add(h, te[e].m, cap);  // the owner kept (refreshed) its own slot
+        if (MODE == kModeTtl && ev.m != kNone32 &&
+            ((v = t.ident[base + wrap_add(h, ev.m, cap)]) & ~kFlagEmpty) == mine) {
+            g = base + wrap_add(h, ev.m, cap);  // the owner kept (refreshed) its own slot
             oc = kFound;
-        } else if (te[e].state != kStateCollided) {
-            g = base + wrap_add(h, te[e].held, cap);
+        } else if (ev.state != kStateCollided) {
+            g = base + wrap_add(h, ev.held, cap);
             v = t.ident[g];
             ok = (v & ~kFlagEmpty) == mine;
             oc = (v & kFlagEmpty) ? kInserted : kEvicted;
@@ -686,15 +709,26 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
         if (oc != kCollision) t.ident[g] = id;
         t.meta[g] = meta_value;
         if (oc == kInserted || oc == kEvicted) t.row_gen[g] = gen_clock;
-        if (oc == kEvicted) {
-            const unsigned r = atomicAdd(&ctr->reset_count, 1u);
-            reset_rows[r] = g;
-            evflag[rank] = 1;
-            evslot[rank] = g;
-            atomicAdd(&ctr->evicted_count, 1u);
+        {   // reset list: one warp-aggregated append (a per-row atomic on one counter word
+            // serialises at the L2 -- C4 evicts ~0.8 M rows per 1 M-position batch); the
+            // evicted-list length is the rank-ordered compaction's count (TTL; no evictions
+            // otherwise on this path)
+            const unsigned am = __activemask();
+            const unsigned em = __ballot_sync(am, oc == kEvicted);
+            if (oc == kEvicted) {
+                const unsigned leader = __ffs(em) - 1;
+                unsigned r0 = 0;
+                if (lane_id() == leader) r0 = atomicAdd(&ctr->reset_count, (unsigned)__popc(em));
+                r0 = __shfl_sync(em, r0, leader);
+                reset_rows[r0 + __popc(em & ((1u << lane_id()) - 1))] = g;
+                evflag[rank] = 1;
+                evslot[rank] = g;
+            }
         }
-        te[e].slot = g;
-        te[e].oc = oc;
+        if (dups) {  // K5 reads the entry's result for the later positions of its id
+            te[e].slot = g;
+            te[e].oc = oc;
+        }
         // the primary item's own position (its feature is the entry's): result written
         // here, so K5 only has items of repeated ids left
         out_slots[rank] = g;

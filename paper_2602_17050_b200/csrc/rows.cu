@@ -54,40 +54,45 @@ __global__ void __launch_bounds__(256) k_draw_all(TableDev t) {
     }
 }
 
-// reset: one warp per listed row; rows may repeat (LRU double eviction), the
-// operation is idempotent.
+// reset: a warp takes 32 listed rows at a time (one coalesced load of their indices, so no
+// row waits on its own index load) and resets them one after another, a row's dim floats
+// spread over the lanes; rows may repeat (LRU double eviction), the operation is idempotent.
 __global__ void __launch_bounds__(256) k_reset_rows(TableDev t, const uint64_t* __restrict__ rows,
                                                     const unsigned* __restrict__ count) {
     const unsigned n = *count;
     const unsigned lane = lane_id();
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t r = warp; r < n; r += nwarps) {
-        const uint64_t row = rows[r];
-        const uint64_t s0 = mix64(row, t.init_seed);
-        float* w = t.weights + row * t.dim;
-        float* m = t.momentum + row * t.dim;
-        if ((t.dim & 3u) == 0) {
-            float4* w4 = reinterpret_cast<float4*>(w);
-            float4* m4 = reinterpret_cast<float4*>(m);
-            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (uint32_t q = lane; q < t.dim / 4; q += 32) {
-                const uint64_t j = (uint64_t)q * 4;
-                float4 v;
-                v.x = draw_elem(s0, j, t.bound);
-                v.y = draw_elem(s0, j + 1, t.bound);
-                v.z = draw_elem(s0, j + 2, t.bound);
-                v.w = draw_elem(s0, j + 3, t.bound);
-                w4[q] = v;
-                m4[q] = z;
+    for (uint64_t r0 = warp * 32; r0 < n; r0 += nwarps * 32) {
+        const uint64_t mine = r0 + lane < n ? rows[r0 + lane] : 0;
+        const unsigned cnt = n - r0 < 32 ? (unsigned)(n - r0) : 32u;
+        for (unsigned k = 0; k < cnt; ++k) {
+            const uint64_t row = __shfl_sync(0xffffffffu, mine, k);
+            const uint64_t s0 = mix64(row, t.init_seed);
+            float* w = t.weights + row * t.dim;
+            float* m = t.momentum + row * t.dim;
+            if ((t.dim & 3u) == 0) {
+                float4* w4 = reinterpret_cast<float4*>(w);
+                float4* m4 = reinterpret_cast<float4*>(m);
+                const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (uint32_t q = lane; q < t.dim / 4; q += 32) {
+                    const uint64_t j = (uint64_t)q * 4;
+                    float4 v;
+                    v.x = draw_elem(s0, j, t.bound);
+                    v.y = draw_elem(s0, j + 1, t.bound);
+                    v.z = draw_elem(s0, j + 2, t.bound);
+                    v.w = draw_elem(s0, j + 3, t.bound);
+                    w4[q] = v;
+                    m4[q] = z;
+                }
+            } else {
+                for (uint32_t j = lane; j < t.dim; j += 32) {
+                    w[j] = draw_elem(s0, j, t.bound);
+                    m[j] = 0.f;
+                }
             }
-        } else {
-            for (uint32_t j = lane; j < t.dim; j += 32) {
-                w[j] = draw_elem(s0, j, t.bound);
-                m[j] = 0.f;
-            }
+            if (lane == 0) t.trained[row] = 0;
         }
-        if (lane == 0) t.trained[row] = 0;
     }
 }
 
