@@ -847,13 +847,15 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     if (a.overflow_all) return;  // validation only; the host reports the error
     if (t.profiling) cudaEventRecord(t.ev[0], st);
     // probe kernel: the quad line walk when windows run long (max_probe >= 256: at 0.95 load
-    // 16% of misses walk all 256 slots), else the per-thread sector walk (DESIGN.md section 4
+    // 16% of misses walk all 256 slots) or the batch is small, else the per-thread sector walk (DESIGN.md section 4
     // has the measurements behind the rule); MPZCH_PROBE=sector|line overrides it
     static const int forced = [] {
         const char* e = std::getenv("MPZCH_PROBE");
         return !e ? -1 : (std::string(e) == "line" ? 1 : 0);
     }();
-    const bool line = forced >= 0 ? forced == 1 : t.P >= 256;
+    // small batches (C1: 64K positions) cannot fill the GPU with one thread per position: the
+    // quad kernel runs 4x the threads and a quarter of the rounds per walk
+    const bool line = forced >= 0 ? forced == 1 : (t.P >= 256 || n <= (1ull << 18));
 #define MPZCH_PROBE_ARGS t.dev, a.ids, n, a.now, a.uniform_meta, t.d_ctr, a.out_slots, a.out_oc, newpos, newid, newa, newm
     if (line) {
         constexpr int kUL = 2;
