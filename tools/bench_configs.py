@@ -236,9 +236,10 @@ def c4():
 
 
 def lru(pool_factor=1.2):
-    """Not a BASELINE config: C1-shaped LRU batches (the A.4 rounds path), next to the
-    reference on the same stream.  pool_factor 1.2: more ids than slots (full windows, LRU
-    victims, double evictions); 0.8: the C1 pool."""
+    """Not a BASELINE config: C1-shaped LRU batches next to the reference on the same stream.
+    pool_factor 0.8 (the C1 pool): no window fills, every batch runs the claim path;
+    1.2: more ids than slots (full windows, LRU victims, double evictions) -- the claim
+    attempt reverts and the A.4 rounds path runs."""
     rows = 1 << 20
     pool = int(pool_factor * rows)
     ids_pool = bench.distinct_ids_t(9, torch.arange(pool, dtype=torch.int64, device="cuda"))
