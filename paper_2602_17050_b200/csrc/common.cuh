@@ -131,4 +131,9 @@ __device__ __forceinline__ void ld_sector_cg(const uint64_t* p, uint64_t& a, uin
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+// Programmatic dependent launch: a kernel launched with the PDL attribute may start while its
+// predecessor in the stream drains; it waits here (before touching anything the predecessor
+// wrote) for the predecessor's completion and memory flush.  A no-op without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 }  // namespace mpzch_b200

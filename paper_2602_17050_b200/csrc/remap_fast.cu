@@ -143,6 +143,7 @@ __device__ __forceinline__ uint32_t first_expired(const uint64_t* __restrict__ m
 // Runs before anything mutates, so the probe can write metadata for final positions.
 __global__ void __launch_bounds__(256) k_validate(TableDev t, const uint64_t* __restrict__ ids,
                                                   uint64_t n, BatchCounters* ctr) {
+    pdl_wait();
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long bad = ~0ull;
@@ -194,6 +195,7 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
                                                uint64_t* __restrict__ newid,
                                                uint32_t* __restrict__ newa,
                                                uint32_t* __restrict__ newm) {
+    pdl_wait();
     if (batch_failed(&ctr->err)) return;
     constexpr uint8_t kPending = 0, kHit = 1, kEmptyHit = 2, kExhausted = 3, kIdle = 4;
     const unsigned lane = lane_id();
@@ -334,6 +336,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
                                                           uint64_t* __restrict__ newid,
                                                           uint32_t* __restrict__ newa,
                                                           uint32_t* __restrict__ newm) {
+    pdl_wait();
     if (batch_failed(&ctr->err)) return;
     constexpr uint8_t kPending = 0, kHit = 1, kEmptyHit = 2, kExhausted = 3, kIdle = 4;
     const unsigned lane = lane_id();
@@ -474,6 +477,7 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
                                                const uint32_t* __restrict__ newa,
                                                const uint32_t* __restrict__ newm,
                                                uint32_t* __restrict__ newent, IdEntry* te) {
+    pdl_wait();
     if (batch_failed(&ctr->err)) return;
     const unsigned cnt = ctr->new_count;
     const uint64_t mask = table_mask(cnt, tcap);
@@ -548,6 +552,7 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                                                const uint32_t* __restrict__ newpos,
                                                const uint32_t* __restrict__ newent,
                                                IdEntry* te) {
+    pdl_wait();
     if (batch_failed(&ctr->err) || (MODE == kModeLru && ctr->lru_abort)) return;
     const unsigned cnt = ctr->new_count;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
@@ -672,6 +677,7 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
                                                 uint64_t* __restrict__ evslot,
                                                 uint64_t* __restrict__ out_slots,
                                                 uint8_t* __restrict__ out_oc) {
+    pdl_wait();
     if (batch_failed(&ctr->err) || (MODE == kModeLru && ctr->lru_abort)) return;
     const unsigned cnt = ctr->new_count;
     const bool dups = ctr->dup_items != 0;
@@ -755,6 +761,7 @@ __global__ void __launch_bounds__(256) k_lru_revert(TableDev t, BatchCounters* c
                                                     const uint32_t* __restrict__ newpos,
                                                     const uint32_t* __restrict__ newent,
                                                     const IdEntry* te) {
+    pdl_wait();
     if (batch_failed(&ctr->err) || !ctr->lru_abort) return;
     const unsigned cnt = ctr->new_count;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
@@ -774,6 +781,7 @@ __global__ void __launch_bounds__(256) k_lru_revert(TableDev t, BatchCounters* c
 __global__ void __launch_bounds__(256) k_lru_meta(TableDev t, const BatchCounters* ctr, uint64_t n,
                                                   const uint64_t* __restrict__ out_slots,
                                                   uint64_t meta_value) {
+    pdl_wait();
     if (batch_failed(&ctr->err) || ctr->lru_abort) return;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         t.meta[out_slots[i]] = meta_value;
@@ -790,6 +798,7 @@ __global__ void __launch_bounds__(256) k_finalize(BatchCounters* ctr,
                                                   const IdEntry* te,
                                                   uint64_t* __restrict__ out_slots,
                                                   uint8_t* __restrict__ out_oc) {
+    pdl_wait();
     if (batch_failed(&ctr->err) || ctr->dup_items == 0 || ctr->lru_abort) return;
     const unsigned cnt = ctr->new_count;
     unsigned long long c[4] = {0, 0, 0, 0};
@@ -825,6 +834,31 @@ void run_validate(Table& t, const uint64_t* ids, uint64_t n, cudaStream_t st) {
     MPZCH_CUDA(cudaStreamSynchronize(st));
 }
 
+template <class T>
+struct same_type { using type = T; };
+
+// Launch `k` as a programmatic dependent of the previous kernel in `st` (it starts while that
+// kernel drains and waits in pdl_wait()): the batch's kernel chain pays one launch latency,
+// not one per kernel.
+template <typename... KArgs>
+void launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t st,
+                typename same_type<KArgs>::type... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = st;
+    static const bool enabled = [] {
+        const char* e = std::getenv("MPZCH_PDL");
+        return !(e && std::string(e) == "0");
+    }();
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = enabled ? 1 : 0;
+    MPZCH_CUDA(cudaLaunchKernelEx(&cfg, k, args...));
+}
+
 void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     constexpr int kU = 2;  // positions in flight per probe thread
     const uint64_t n = a.n;
@@ -842,7 +876,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     uint32_t* newent = t.s_newent.as<uint32_t>();
     if (t.profiling) cudaEventRecord(t.ev[7], st);
     k_init_counters<<<1, 32, 0, st>>>(t.d_ctr);
-    k_validate<<<grid_for(n / 2 + 1, B, 148u * 8u), B, 0, st>>>(t.dev, a.ids, n, t.d_ctr);
+    launch_pdl(k_validate, grid_for(n / 2 + 1, B, 148u * 8u), B, st, t.dev, a.ids, n, t.d_ctr);
     t.launches += 2;
     if (a.overflow_all) return;  // validation only; the host reports the error
     if (t.profiling) cudaEventRecord(t.ev[0], st);
@@ -860,33 +894,33 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     if (line) {
         constexpr int kUL = 2;
         const unsigned gl = grid_for(4 * ((n + kUL - 1) / kUL), B, 148u * 16u);
-        if (ttl) k_probe_line<kModeTtl, kUL, 4><<<gl, B, 0, st>>>(MPZCH_PROBE_ARGS);
-        else if (lru) k_probe_line<kModeLru, kUL, 4><<<gl, B, 0, st>>>(MPZCH_PROBE_ARGS);
-        else k_probe_line<kModeDisabled, kUL, 4><<<gl, B, 0, st>>>(MPZCH_PROBE_ARGS);
+        if (ttl) launch_pdl(k_probe_line<kModeTtl, kUL, 4>, gl, B, st, MPZCH_PROBE_ARGS);
+        else if (lru) launch_pdl(k_probe_line<kModeLru, kUL, 4>, gl, B, st, MPZCH_PROBE_ARGS);
+        else launch_pdl(k_probe_line<kModeDisabled, kUL, 4>, gl, B, st, MPZCH_PROBE_ARGS);
     } else {
-        if (ttl) k_probe<kModeTtl, kU><<<gP, B, 0, st>>>(MPZCH_PROBE_ARGS);
-        else if (lru) k_probe<kModeLru, kU><<<gP, B, 0, st>>>(MPZCH_PROBE_ARGS);
-        else k_probe<kModeDisabled, kU><<<gP, B, 0, st>>>(MPZCH_PROBE_ARGS);
+        if (ttl) launch_pdl(k_probe<kModeTtl, kU>, gP, B, st, MPZCH_PROBE_ARGS);
+        else if (lru) launch_pdl(k_probe<kModeLru, kU>, gP, B, st, MPZCH_PROBE_ARGS);
+        else launch_pdl(k_probe<kModeDisabled, kU>, gP, B, st, MPZCH_PROBE_ARGS);
     }
 #undef MPZCH_PROBE_ARGS
     ++t.launches;
     if (t.profiling) cudaEventRecord(t.ev[1], st);
     IdEntry* te = t.s_tent.as<IdEntry>();
-    k_dedup<<<gW, B, 0, st>>>(t.d_ctr, t.tcap, epoch, newpos, newid, newa, newm, newent, te);
+    launch_pdl(k_dedup, gW, B, st, t.d_ctr, t.tcap, epoch, newpos, newid, newa, newm, newent, te);
     if (t.profiling) cudaEventRecord(t.ev[4], st);
 #define MPZCH_CLAIM_COMMIT(MODE)                                                                   \
-    k_claim<MODE><<<gW, B, 0, st>>>(t.dev, a.now, t.d_ctr, newpos, newent, te);                   \
+    launch_pdl(k_claim<MODE>, gW, B, st, t.dev, a.now, t.d_ctr, newpos, newent, te);              \
     if (t.profiling) cudaEventRecord(t.ev[5], st);                                               \
-    k_commit<MODE><<<gW, B, 0, st>>>(t.dev, t.d_ctr, newpos, newid, newent, te, t.gen_clock,      \
+    launch_pdl(k_commit<MODE>, gW, B, st, t.dev, t.d_ctr, newpos, newid, newent, te, t.gen_clock, \
                                      a.uniform_meta, t.s_reset.as<uint64_t>(),                     \
                                      t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>(),         \
                                      a.out_slots, a.out_oc)
     if (ttl) { MPZCH_CLAIM_COMMIT(kModeTtl); }
     else if (lru) {
-        k_claim<kModeLru><<<gW, B, 0, st>>>(t.dev, a.now, t.d_ctr, newpos, newent, te);
+        launch_pdl(k_claim<kModeLru>, gW, B, st, t.dev, a.now, t.d_ctr, newpos, newent, te);
         if (t.profiling) cudaEventRecord(t.ev[5], st);
-        k_lru_revert<<<gW, B, 0, st>>>(t.dev, t.d_ctr, newpos, newent, te);
-        k_commit<kModeLru><<<gW, B, 0, st>>>(t.dev, t.d_ctr, newpos, newid, newent, te, t.gen_clock,
+        launch_pdl(k_lru_revert, gW, B, st, t.dev, t.d_ctr, newpos, newent, te);
+        launch_pdl(k_commit<kModeLru>, gW, B, st, t.dev, t.d_ctr, newpos, newid, newent, te, t.gen_clock,
                                              a.uniform_meta, t.s_reset.as<uint64_t>(),
                                              t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>(),
                                              a.out_slots, a.out_oc);
@@ -896,11 +930,11 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
 #undef MPZCH_CLAIM_COMMIT
     t.launches += 3;
     if (t.profiling) cudaEventRecord(t.ev[2], st);
-    k_finalize<<<gW, B, 0, st>>>(t.d_ctr, a.feats, newpos, newent, te, a.out_slots, a.out_oc);
+    launch_pdl(k_finalize, gW, B, st, t.d_ctr, a.feats, newpos, newent, te, a.out_slots, a.out_oc);
     if (t.profiling) cudaEventRecord(t.ev[6], st);
     ++t.launches;
     if (lru) {
-        k_lru_meta<<<grid_for(n, B, 148u * 8u), B, 0, st>>>(t.dev, t.d_ctr, n, a.out_slots, a.uniform_meta);
+        launch_pdl(k_lru_meta, grid_for(n, B, 148u * 8u), B, st, t.dev, t.d_ctr, n, a.out_slots, a.uniform_meta);
         ++t.launches;
     }
     if (t.dim > 0) launch_reset_rows(t, t.s_reset.as<uint64_t>(), &t.d_ctr->reset_count, st);
