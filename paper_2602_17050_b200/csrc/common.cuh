@@ -11,6 +11,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+#include <cstring>
+
 namespace mpzch_b200 {
 
 constexpr uint64_t kEmpty = ~0ull;
@@ -135,5 +138,30 @@ __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 // predecessor in the stream drains; it waits here (before touching anything the predecessor
 // wrote) for the predecessor's completion and memory flush.  A no-op without the attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <class T>
+struct same_type { using type = T; };
+
+// Launch `k` as a programmatic dependent of the previous kernel in `st` (it starts while that
+// kernel drains and waits in pdl_wait()): a chain of kernels pays one launch latency, not one
+// per kernel.  MPZCH_PDL=0 launches plainly.  Launch errors surface through cudaGetLastError.
+template <typename... KArgs>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t st,
+                              typename same_type<KArgs>::type... args) {
+    static const bool enabled = [] {
+        const char* e = std::getenv("MPZCH_PDL");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = enabled ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
 
 }  // namespace mpzch_b200

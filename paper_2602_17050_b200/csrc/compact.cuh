@@ -30,6 +30,7 @@ __device__ __forceinline__ unsigned count16(const uint8_t* f, uint64_t i0, uint6
 static __global__ void __launch_bounds__(kCompactThreads) k_compact_count(const uint8_t* __restrict__ flags,
                                                                    uint64_t n,
                                                                    unsigned* __restrict__ blk) {
+    pdl_wait();
     __shared__ unsigned red[kCompactThreads / 32];
     const uint64_t i0 = (uint64_t)blockIdx.x * kCompactChunk + threadIdx.x * kCompactPerThread;
     unsigned c = i0 < n ? count16(flags, i0, n) : 0;
@@ -45,6 +46,7 @@ static __global__ void __launch_bounds__(kCompactThreads) k_compact_count(const 
 
 // exclusive scan in place; total -> *total
 static __global__ void __launch_bounds__(1024) k_compact_scan(unsigned* blk, unsigned nblk, unsigned* total) {
+    pdl_wait();
     __shared__ unsigned carry;
     __shared__ unsigned wsum[32];
     if (threadIdx.x == 0) carry = 0;
@@ -82,6 +84,7 @@ template <class Emit>
 __global__ void __launch_bounds__(kCompactThreads) k_compact_write(uint8_t* __restrict__ flags, uint64_t n,
                                                                    const unsigned* __restrict__ blk,
                                                                    bool clear, Emit emit) {
+    pdl_wait();
     __shared__ unsigned wsum[kCompactThreads / 32];
     const uint64_t i0 = (uint64_t)blockIdx.x * kCompactChunk + threadIdx.x * kCompactPerThread;
     const unsigned c = i0 < n ? count16(flags, i0, n) : 0;
@@ -119,9 +122,9 @@ inline void compact_flags(uint8_t* flags, uint64_t n, unsigned* blk, unsigned* t
                           Emit emit, cudaStream_t st, uint64_t& launches) {
     const unsigned nblk = (unsigned)((n + kCompactChunk - 1) / kCompactChunk);
     if (nblk == 0) return;
-    k_compact_count<<<nblk, kCompactThreads, 0, st>>>(flags, n, blk);
-    k_compact_scan<<<1, 1024, 0, st>>>(blk, nblk, total);
-    k_compact_write<<<nblk, kCompactThreads, 0, st>>>(flags, n, blk, clear, emit);
+    launch_pdl(k_compact_count, nblk, kCompactThreads, st, flags, n, blk);
+    launch_pdl(k_compact_scan, 1, 1024, st, blk, nblk, total);
+    launch_pdl(k_compact_write<Emit>, nblk, kCompactThreads, st, flags, n, (const unsigned*)blk, clear, emit);
     launches += 3;
 }
 

@@ -834,31 +834,6 @@ void run_validate(Table& t, const uint64_t* ids, uint64_t n, cudaStream_t st) {
     MPZCH_CUDA(cudaStreamSynchronize(st));
 }
 
-template <class T>
-struct same_type { using type = T; };
-
-// Launch `k` as a programmatic dependent of the previous kernel in `st` (it starts while that
-// kernel drains and waits in pdl_wait()): the batch's kernel chain pays one launch latency,
-// not one per kernel.
-template <typename... KArgs>
-void launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t st,
-                typename same_type<KArgs>::type... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(block);
-    cfg.stream = st;
-    static const bool enabled = [] {
-        const char* e = std::getenv("MPZCH_PDL");
-        return !(e && std::string(e) == "0");
-    }();
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = enabled ? 1 : 0;
-    MPZCH_CUDA(cudaLaunchKernelEx(&cfg, k, args...));
-}
-
 void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     constexpr int kU = 2;  // positions in flight per probe thread
     const uint64_t n = a.n;

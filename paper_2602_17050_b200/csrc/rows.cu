@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(256) k_draw_all(TableDev t) {
 // spread over the lanes; rows may repeat (LRU double eviction), the operation is idempotent.
 __global__ void __launch_bounds__(256) k_reset_rows(TableDev t, const uint64_t* __restrict__ rows,
                                                     const unsigned* __restrict__ count) {
+    pdl_wait();
     const unsigned n = *count;
     const unsigned lane = lane_id();
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -169,7 +170,7 @@ void launch_init_table(Table& t) {
 }
 
 void launch_reset_rows(Table& t, const uint64_t* rows, const unsigned* count, cudaStream_t st) {
-    k_reset_rows<<<148 * 8, 256, 0, st>>>(t.dev, rows, count);
+    launch_pdl(k_reset_rows, 148 * 8, 256, st, t.dev, rows, count);
     ++t.launches;
 }
 
