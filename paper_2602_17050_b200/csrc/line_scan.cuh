@@ -57,35 +57,4 @@ __device__ __forceinline__ LineSpan line_span(uint64_t g, uint64_t end, uint32_t
     return sp;
 }
 
-// First offset in [0, limit) of the window starting at home h whose metadata word is expired
-// (stored < now, eviction.hpp:53), or limit.  Quad-cooperative line reads.
-__device__ __forceinline__ uint32_t quad_first_expired(const uint64_t* __restrict__ meta, uint64_t base,
-                                                       uint64_t h, uint64_t cap, uint32_t limit,
-                                                       uint64_t now, unsigned j, unsigned qm,
-                                                       unsigned long long& nsec) {
-    uint32_t off = 0;
-    uint64_t g = base + h;
-    const uint64_t end = base + cap;
-    while (off < limit) {
-        uint64_t w[4];
-        ld_line_part(meta, g, j, w);
-        unsigned e = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) e |= (unsigned)(w[k] < now) << k;
-        const unsigned x = quad_gather(e, 0, j, qm) & 0xFFFFu;
-        const LineSpan sp = line_span(g, end, off, limit);
-        const unsigned hit = x & sp.range();
-        if (hit) {
-            const unsigned p = __ffs(hit) - 1;
-            nsec += sp.sectors_to(p);
-            return off + (p - sp.s);
-        }
-        nsec += sp.sectors_to(sp.s + sp.c - 1);
-        off += sp.c;
-        g += sp.c;
-        if (g == end) g = base;
-    }
-    return limit;
-}
-
 }  // namespace mpzch_b200

@@ -117,28 +117,6 @@ __global__ void k_init_counters(BatchCounters* c) {
     }
 }
 
-// First offset in [0, limit) whose metadata is expired (stored < now), or limit.
-// Only called under TTL; reads one sector per 4 slots.
-__device__ __forceinline__ uint32_t first_expired(const uint64_t* __restrict__ meta, uint64_t base,
-                                                  uint64_t h, uint64_t cap, uint32_t limit,
-                                                  uint64_t now, unsigned long long& nsec) {
-    uint32_t off = 0;
-    uint64_t g = base + h;
-    const uint64_t end = base + cap;
-    while (off < limit) {
-        const uint64_t a4 = g & ~3ull;
-        uint64_t w0, w1, w2, w3;
-        ld_sector(meta + a4, w0, w1, w2, w3);
-        ++nsec;
-        do {
-            if (pick4((uint32_t)(g - a4), w0, w1, w2, w3) < now) return off;
-            ++off;
-            if (++g == end) g = base;
-        } while (off < limit && (g >> 2) == (a4 >> 2));
-    }
-    return limit;
-}
-
 // K0: streaming validation of the batch (batch_engine.cpp:90-94): min invalid position.
 // Runs before anything mutates, so the probe can write metadata for final positions.
 __global__ void __launch_bounds__(256) k_validate(TableDev t, const uint64_t* __restrict__ ids,
@@ -186,7 +164,7 @@ __global__ void __launch_bounds__(256) k_validate(TableDev t, const uint64_t* __
 // K1: probe; each thread keeps U positions in flight (independent sector loads), all
 // positions of a round are issued before any is scanned.
 template <int MODE, int U>
-__global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __restrict__ ids,
+__global__ void __launch_bounds__(256, MODE == kModeTtl ? 3 : 4) k_probe(TableDev t, const uint64_t* __restrict__ ids,
                                                uint64_t n, uint64_t now, uint64_t meta_value,
                                                BatchCounters* ctr,
                                                uint64_t* __restrict__ out_slots,
@@ -204,12 +182,18 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
     for (uint64_t t0 = (uint64_t)blockIdx.x * tile; t0 < n; t0 += (uint64_t)gridDim.x * tile) {
         uint64_t id[U], g[U], base[U], cap[U], h[U];
         uint32_t off[U];
+        uint32_t fe[U];  // TTL: offset of the first expired slot walked before the stop
+        bool hexp[U];    // TTL: the matched slot itself is expired
+        bool mld[U];     // TTL: this round's metadata sector was loaded
         uint8_t st[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint64_t i = t0 + (uint64_t)u * blockDim.x + threadIdx.x;
             st[u] = kIdle;
             off[u] = 0;
+            fe[u] = kNone32;
+            hexp[u] = false;
+            mld[u] = false;
             if (i < n) {
                 id[u] = ids[i];
                 const ShardDev sd = t.shards[shard_of(id[u], t)];
@@ -225,21 +209,41 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
         // cp.async behind block barriers, both measured slower on C5 and C3.)
         for (;;) {
             uint64_t w[U][4];
+            uint64_t mw[MODE == kModeTtl ? U : 1][4];  // TTL: the metadata sector, same round
             bool any = false;
 #pragma unroll
             for (int u = 0; u < U; ++u)
                 if (st[u] == kPending) {
                     ld_sector(t.ident + (g[u] & ~3ull), w[u][0], w[u][1], w[u][2], w[u][3]);
                     ++my_isec;
+                    // TTL: the metadata sector comes in the same round until the walk has
+                    // seen an expired slot (after that only a hit's own word is needed)
+                    if (MODE == kModeTtl) {
+                        mld[u] = fe[u] == kNone32;
+                        if (mld[u]) {
+                            ld_sector(t.meta + (g[u] & ~3ull), mw[u][0], mw[u][1], mw[u][2], mw[u][3]);
+                            ++my_msec;
+                        }
+                    }
                 }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (st[u] != kPending) continue;
                 const uint64_t a4 = g[u] & ~3ull, end = base[u] + cap[u];
                 do {
-                    const uint64_t v = pick4((uint32_t)(g[u] - a4), w[u][0], w[u][1], w[u][2], w[u][3]);
-                    if (v == id[u]) { st[u] = kHit; break; }
+                    const uint32_t jj = (uint32_t)(g[u] - a4);
+                    const uint64_t v = pick4(jj, w[u][0], w[u][1], w[u][2], w[u][3]);
+                    if (v == id[u]) {
+                        st[u] = kHit;
+                        if (MODE == kModeTtl)
+                            hexp[u] = mld[u] ? pick4(jj, mw[u][0], mw[u][1], mw[u][2], mw[u][3]) < now
+                                             : __ldg(t.meta + g[u]) < now;
+                        break;
+                    }
                     if (v == kEmpty) { st[u] = kEmptyHit; break; }
+                    if (MODE == kModeTtl && mld[u] && fe[u] == kNone32 &&
+                        pick4(jj, mw[u][0], mw[u][1], mw[u][2], mw[u][3]) < now)
+                        fe[u] = off[u];
                     ++off[u];
                     if (++g[u] == end) g[u] = base[u];
                 } while (off[u] < t.P && (g[u] >> 2) == (a4 >> 2));
@@ -264,19 +268,18 @@ __global__ void __launch_bounds__(256, 4) k_probe(TableDev t, const uint64_t* __
                     else if (st[u] == kEmptyHit) { is_new = true; a_off = off[u]; }
                     else if (MODE == kModeLru) atomicExch(&ctr->lru_abort, 1u);  // would evict
                     else { fslot = base[u] + h[u]; foc = kCollision; }
-                } else {  // TTL with one metadata value per batch
+                } else {  // TTL with one metadata value per batch (expiry read with the walk)
                     if (st[u] == kHit) {
-                        ++my_msec;
-                        if (__ldg(t.meta + g[u]) >= now) {
+                        if (!hexp[u]) {
                             fslot = g[u];  // live: nobody can take it in this batch
                         } else {           // expired own slot: lower-rank new ids contest it
                             is_new = true;
                             m_off = off[u];
-                            a_off = first_expired(t.meta, base[u], h[u], cap[u], off[u], now, my_msec);
+                            a_off = fe[u] != kNone32 ? fe[u] : off[u];
                         }
                     } else {
                         const uint32_t lim = st[u] == kEmptyHit ? off[u] : t.P;
-                        const uint32_t x = first_expired(t.meta, base[u], h[u], cap[u], lim, now, my_msec);
+                        const uint32_t x = fe[u] != kNone32 ? fe[u] : lim;
                         if (x < lim || st[u] == kEmptyHit) { is_new = true; a_off = x; }
                         else { fslot = base[u] + h[u]; foc = kCollision; }
                     }
@@ -348,12 +351,18 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
     for (uint64_t t0 = (uint64_t)blockIdx.x * tile; t0 < n; t0 += (uint64_t)gridDim.x * tile) {
         uint64_t id[U], g[U];
         uint32_t off[U], sh[U];
+        uint32_t fe[U];  // TTL: offset of the first expired slot walked before the stop
+        bool hexp[U];    // TTL: the matched slot itself is expired
+        bool mld[U];     // TTL: this round's metadata line was loaded
         uint8_t st[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint64_t i = t0 + (uint64_t)u * qpb + qib;
             st[u] = kIdle;
             off[u] = 0;
+            fe[u] = kNone32;
+            hexp[u] = false;
+            mld[u] = false;
             if (i < n) {
                 id[u] = ids[i];
                 sh[u] = shard_of(id[u], t);
@@ -364,9 +373,16 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
         }
         for (;;) {
             uint64_t w[U][4];
+            uint64_t mw[MODE == kModeTtl ? U : 1][4];  // TTL: the metadata line, same round
 #pragma unroll
             for (int u = 0; u < U; ++u)
-                if (st[u] == kPending) ld_line_part(t.ident, g[u], j, w[u]);
+                if (st[u] == kPending) {
+                    ld_line_part(t.ident, g[u], j, w[u]);
+                    if (MODE == kModeTtl) {  // until the walk has seen an expired slot
+                        mld[u] = fe[u] == kNone32;
+                        if (mld[u]) ld_line_part(t.meta, g[u], j, mw[u]);
+                    }
+                }
             bool any = false;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -378,6 +394,13 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
                     e |= (unsigned)(w[u][k] == kEmpty) << k;
                 }
                 const unsigned x = quad_gather(m, e, j, qm);
+                unsigned xe = 0;
+                if (MODE == kModeTtl && mld[u]) {
+                    unsigned x4 = 0;
+#pragma unroll
+                    for (int k2 = 0; k2 < 4; ++k2) x4 |= (unsigned)(mw[u][k2] < now) << k2;
+                    xe = quad_gather(x4, 0, j, qm) & 0xFFFFu;
+                }
                 const ShardDev sd = t.shards[sh[u]];
                 const uint64_t base = sd.offset, end = base + sd.cap.d;
                 const LineSpan sp = line_span(g[u], end, off[u], t.P);
@@ -385,10 +408,21 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
                 if (hit) {
                     const unsigned p = __ffs(hit) - 1;
                     st[u] = (x >> p) & 1u ? kHit : kEmptyHit;
+                    if (MODE == kModeTtl) {
+                        const unsigned before = xe & sp.range() & ((1u << p) - 1u);
+                        if (fe[u] == kNone32 && before) fe[u] = off[u] + (__ffs(before) - 1 - sp.s);
+                        hexp[u] = mld[u] ? (xe >> p) & 1u : __ldg(t.meta + g[u] + (p - sp.s)) < now;
+                        if (mld[u]) my_msec += sp.sectors_to(p);
+                    }
                     off[u] += p - sp.s;
                     g[u] += p - sp.s;
                     my_isec += sp.sectors_to(p);
                 } else {
+                    if (MODE == kModeTtl && mld[u]) {
+                        const unsigned ex = xe & sp.range();
+                        if (fe[u] == kNone32 && ex) fe[u] = off[u] + (__ffs(ex) - 1 - sp.s);
+                        my_msec += sp.sectors_to(sp.s + sp.c - 1);
+                    }
                     my_isec += sp.sectors_to(sp.s + sp.c - 1);
                     off[u] += sp.c;
                     g[u] += sp.c;
@@ -415,19 +449,18 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
                     else if (st[u] == kEmptyHit) { is_new = true; a_off = off[u]; }
                     else if (MODE == kModeLru) { if (j == 0) atomicExch(&ctr->lru_abort, 1u); }
                     else { fslot = base + h; foc = kCollision; }
-                } else {  // TTL with one metadata value per batch
+                } else {  // TTL with one metadata value per batch (expiry read with the walk)
                     if (st[u] == kHit) {
-                        ++my_msec;
-                        if (__ldg(t.meta + g[u]) >= now) {
+                        if (!hexp[u]) {
                             fslot = g[u];  // live: nobody can take it in this batch
                         } else {           // expired own slot: lower-rank new ids contest it
                             is_new = true;
                             m_off = off[u];
-                            a_off = quad_first_expired(t.meta, base, h, cap, off[u], now, j, qm, my_msec);
+                            a_off = fe[u] != kNone32 ? fe[u] : off[u];
                         }
                     } else {
                         const uint32_t lim = st[u] == kEmptyHit ? off[u] : t.P;
-                        const uint32_t xo = quad_first_expired(t.meta, base, h, cap, lim, now, j, qm, my_msec);
+                        const uint32_t xo = fe[u] != kNone32 ? fe[u] : lim;
                         if (xo < lim || st[u] == kEmptyHit) { is_new = true; a_off = xo; }
                         else { fslot = base + h; foc = kCollision; }
                     }
@@ -869,7 +902,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     if (line) {
         constexpr int kUL = 2;
         const unsigned gl = grid_for(4 * ((n + kUL - 1) / kUL), B, 148u * 16u);
-        if (ttl) launch_pdl(k_probe_line<kModeTtl, kUL, 4>, gl, B, st, MPZCH_PROBE_ARGS);
+        if (ttl) launch_pdl(k_probe_line<kModeTtl, kUL, 3>, gl, B, st, MPZCH_PROBE_ARGS);
         else if (lru) launch_pdl(k_probe_line<kModeLru, kUL, 4>, gl, B, st, MPZCH_PROBE_ARGS);
         else launch_pdl(k_probe_line<kModeDisabled, kUL, 4>, gl, B, st, MPZCH_PROBE_ARGS);
     } else {
