@@ -187,6 +187,16 @@ def random_access_ceiling():
         return None
 
 
+def probe_dram_accesses():
+    """Random DRAM accesses per k_probe launch from the committed ncu capture: 128-byte line
+    fetches (read sectors / 4: the L2 fetches whole lines for random reads) + written sectors."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_probe_summary.json")))
+        return d["dram_read_bytes"] / 128.0 + d["dram_write_bytes"] / 32.0
+    except Exception:
+        return None
+
+
 def ncu_traffic():
     """dram bytes per probe launch from the committed ncu --set full summary, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_probe_summary.json")
@@ -575,6 +585,7 @@ def main():
                          "launch_ms": probe_ms, "peak_source": peak_src,
                          "random_sector_ceiling_gbs": random_sector_ceiling(),
                          "random_access_ceiling": random_access_ceiling(),
+                         "random_access_frac": _access_frac(probe_ms),
                          "share_of_step": probe_ms / ms_step,
                          "batch_algorithmic_bytes": batch_bytes,
                          "batch_gbs": batch_bytes / (batch_ms / 1e3) / 1e9 if batch_ms else 0.0,
@@ -594,6 +605,15 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def _access_frac(probe_ms):
+    """k_probe's DRAM accesses per second (ncu count per launch / live launch time) against the
+    measured random-access read ceiling: the roofline that binds this kernel."""
+    acc, ceil = probe_dram_accesses(), random_access_ceiling()
+    if not acc or not ceil or not probe_ms:
+        return None
+    return acc / (probe_ms / 1e3) / (ceil["read_g_per_s"] * 1e9)
 
 
 def _allreduce_max_int(torch, x, dev):

@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
             uint32_t a_off = 0, m_off = kNone32;
             if (st[u] != kIdle) {
                 const ShardDev sd = t.shards[sh[u]];
-                const uint64_t base = sd.offset, cap = sd.cap.d;
+                const uint64_t base = sd.offset;
                 const uint64_t h = home_of(id[u], sd, t.seed);
                 uint64_t fslot = kEmpty;
                 uint8_t foc = kFound;

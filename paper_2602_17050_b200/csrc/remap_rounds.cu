@@ -104,7 +104,10 @@ struct RoundsArgs {
     __device__ __forceinline__ uint64_t mi(uint64_t g) const { return (g - mark_base) & mark_mask; }
 };
 
-// R1
+// R1.  The walk reads a whole 128-byte line (16 slots) of identities -- and of metadata
+// words outside Disabled -- per round trip: four independent 32-byte loads issued together.
+// LRU windows are full by the time this path runs, so a miss walks all P slots: 8 round trips
+// at P = 128 instead of 32 sector by sector.
 template <int MODE>
 __device__ __forceinline__ void tentative(const RoundsArgs& r, uint32_t k, uint32_t epoch) {
     const TableDev& t = r.t;
@@ -119,23 +122,39 @@ __device__ __forceinline__ void tentative(const RoundsArgs& r, uint32_t k, uint3
     uint64_t exp_g = 0, best_m = 0, best_g = 0;
     bool have_best = false;
     while (off < t.P && !kind) {
-        const uint64_t a4 = g & ~3ull;
-        uint64_t i0, i1, i2, i3, m0 = 0, m1 = 0, m2 = 0, m3 = 0;
-        ld_sector_cg(t.ident + a4, i0, i1, i2, i3);
-        if (MODE != kModeDisabled) ld_sector_cg(t.meta + a4, m0, m1, m2, m3);
-        do {
-            const uint32_t j = (uint32_t)(g - a4);
-            const uint64_t v = pick4r(j, i0, i1, i2, i3);
-            if (v == id) { kind = 1; break; }
-            if (v == kEmpty) { kind = 2; break; }
+        const uint64_t L = g & ~15ull;
+        const unsigned s0 = (unsigned)(g - L);
+        uint64_t c = 16 - s0;
+        if (end - g < c) c = end - g;
+        if (t.P - off < c) c = t.P - off;
+        uint64_t iw[16], mw[MODE != kModeDisabled ? 16 : 1];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ld_sector_cg(t.ident + L + 4 * q, iw[4 * q], iw[4 * q + 1], iw[4 * q + 2], iw[4 * q + 3]);
+        if (MODE != kModeDisabled) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) ld_sector_cg(t.meta + L + 4 * q, mw[4 * q], mw[4 * q + 1], mw[4 * q + 2], mw[4 * q + 3]);
+        }
+        unsigned stop = 16;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            if (stop != 16 || q < (int)s0 || q >= (int)(s0 + c)) continue;
+            const uint64_t v = iw[q];
+            if (v == id) { kind = 1; stop = q; continue; }
+            if (v == kEmpty) { kind = 2; stop = q; continue; }
             if (MODE != kModeDisabled) {
-                const uint64_t m = pick4r(j, m0, m1, m2, m3);
-                if (MODE == kModeTtl && exp_off == kNone32 && m < r.now) { exp_off = off; exp_g = g; }
-                if (MODE == kModeLru && (!have_best || m < best_m)) { have_best = true; best_m = m; best_g = g; }
+                const uint64_t m = mw[q];
+                if (MODE == kModeTtl && exp_off == kNone32 && m < r.now) { exp_off = off + (q - s0); exp_g = L + q; }
+                if (MODE == kModeLru && (!have_best || m < best_m)) { have_best = true; best_m = m; best_g = L + q; }
             }
-            ++off;
-            if (++g == end) g = base;
-        } while (off < t.P && (g >> 2) == (a4 >> 2));
+        }
+        if (stop != 16) {
+            off += stop - s0;
+            g = L + stop;
+        } else {
+            off += (uint32_t)c;
+            g += c;
+            if (g == end) g = base;
+        }
     }
     uint8_t oc = kCollision;
     uint64_t ws = base + h;
@@ -152,7 +171,8 @@ __device__ __forceinline__ void tentative(const RoundsArgs& r, uint32_t k, uint3
     atomicMin((ident_write ? r.mark_id : r.mark_any) + r.mi(ws), (unsigned long long)mark_key(epoch, k));
 }
 
-// R2 (rule in the header)
+// R2 (rule in the header).  The read range's mark words are read 16 at a time (four
+// 32-byte loads of one 128-byte block of the mark array per round trip).
 template <int MODE>
 __device__ __forceinline__ bool suspect(const RoundsArgs& r, uint32_t k, uint32_t epoch) {
     const uint64_t id = r.ids[r.upos[k]];
@@ -161,11 +181,34 @@ __device__ __forceinline__ bool suspect(const RoundsArgs& r, uint32_t k, uint32_
     const uint32_t d = __ldcg(r.td_d + k);
     const uint64_t w = __ldcg(r.td_slot + k);
     const bool meta_dep = MODE == kModeLru && ldcg_u8(r.td_oc + k) == kEvicted;  // full window
-    for (uint32_t off = 0; off <= d; ++off) {
-        const uint64_t g = slot_of(sd, h, off);
-        const uint64_t i = r.mi(g);
-        if (mark_rank(__ldcg(r.mark_id + i), epoch) < k) return true;
-        if ((meta_dep || g == w) && mark_rank(__ldcg(r.mark_any + i), epoch) < k) return true;
+    const uint64_t end = sd.offset + sd.cap.d;
+    uint64_t g = slot_of(sd, h, 0);
+    uint32_t off = 0;
+    while (off <= d) {
+        const uint64_t i = r.mi(g), I = i & ~15ull;
+        const unsigned s0 = (unsigned)(i - I);
+        uint64_t c = 16 - s0;
+        if (end - g < c) c = end - g;
+        if ((uint64_t)(d + 1 - off) < c) c = d + 1 - off;
+        uint64_t mid[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ld_sector_cg((const uint64_t*)(r.mark_id + I + 4 * q), mid[4 * q], mid[4 * q + 1], mid[4 * q + 2], mid[4 * q + 3]);
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+            if (q >= (int)s0 && q < (int)(s0 + c) && mark_rank(mid[q], epoch) < k) return true;
+        if (meta_dep) {
+            uint64_t man[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) ld_sector_cg((const uint64_t*)(r.mark_any + I + 4 * q), man[4 * q], man[4 * q + 1], man[4 * q + 2], man[4 * q + 3]);
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                if (q >= (int)s0 && q < (int)(s0 + c) && mark_rank(man[q], epoch) < k) return true;
+        } else if (w >= g && w < g + c) {  // the write slot lies in this block
+            if (mark_rank(__ldcg(r.mark_any + i + (w - g)), epoch) < k) return true;
+        }
+        off += (uint32_t)c;
+        g += c;
+        if (g == end) g = sd.offset;
     }
     return false;
 }

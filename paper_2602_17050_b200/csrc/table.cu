@@ -463,7 +463,15 @@ uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uin
     }
     bool fast = t.path_override == MPZCH_PATH_AUTO && t.hole_free && a.uniform && n <= (1ull << 29);
     const bool profiled = t.profiling;
-    const bool lru_try = fast && pol.mode == kModeLru;
+    // LRU: after attempts that needed an eviction, skip the claim attempt for a growing number
+    // of batches (1, 3, 7, 15 ... at most 15), so a stream whose windows are full pays for
+    // the rounds path only
+    bool lru_try = fast && pol.mode == kModeLru;
+    if (lru_try && t.lru_skip_left > 0) {
+        --t.lru_skip_left;
+        lru_try = false;
+        fast = false;
+    }
     if (lru_try) {
         // LRU differs from Disabled only when a new id finds its window full (it evicts the
         // least recently used slot, which depends on the batch's own refreshes).  Try the
@@ -476,7 +484,13 @@ uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uin
         const BatchErr& e = t.h_ctr->err;
         const bool failed = e.bad_pos != ~0ull || e.overflow || e.too_many || e.foreign_pos != ~0ull;
         fast = failed || !t.h_ctr->lru_abort;
-        if (!fast) ++t.lru_fallbacks;
+        if (!fast) {
+            ++t.lru_fallbacks;
+            t.lru_backoff = std::min<uint32_t>(2 * t.lru_backoff + 1, 15);
+            t.lru_skip_left = t.lru_backoff;
+        } else {
+            t.lru_backoff = 0;
+        }
     } else if (fast) {
         enqueue_fast_batch(t, a, st);
     }

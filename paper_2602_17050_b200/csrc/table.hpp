@@ -103,6 +103,7 @@ public:
     bool hole_free = true;   // SURVEY A.2 invariant; false after raw imports
     int path_override = MPZCH_PATH_AUTO;
     uint64_t lru_fallbacks = 0;  // LRU batches that needed an eviction (claim attempt reverted)
+    uint32_t lru_backoff = 0, lru_skip_left = 0;  // claim-attempt backoff after evictions
     mpzch_batch_stats last{};
     uint64_t launches = 0;
     bool profiling = false;

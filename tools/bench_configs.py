@@ -43,7 +43,7 @@ def ev_time(fn, stream):
     return e0.elapsed_time(e1)
 
 
-def run_batches(t, batches, nows, pol, stream, timed_from=0, feats=None):
+def run_batches(t, batches, nows, pol, stream, timed_from=0, feats=None, split=True):
     """Synchronous batches after `timed_from` warm-up batches.  The first half of the timed
     batches runs with the in-library per-kernel event profiler (the split: probe / claim /
     tail), the second half without it (ids_per_s, ms_per_batch: no events between the
@@ -54,7 +54,8 @@ def run_batches(t, batches, nows, pol, stream, timed_from=0, feats=None):
     out_e = torch.empty(n, dtype=torch.int64, device="cuda")
     for b in range(timed_from):
         t.process_batch_device(batches[b], nows[b], pol, None, out_s, out_o, out_e, stream)
-    mid = timed_from + max((len(batches) - timed_from) // 2, 1)
+    # split=False (non-stationary streams, e.g. LRU filling up): every timed batch unprofiled
+    mid = timed_from + max((len(batches) - timed_from) // 2, 1) if split else timed_from
     stats = []
 
     def run(lo, hi):
@@ -263,7 +264,7 @@ def lru(pool_factor=1.2):
     for shards in (8, 64):
         caps = mz.even_capacities(rows, shards)
         t = mz.MpzchTable(mz.TableConfig(caps, 128, 7))
-        r = run_batches(t, batches, nows, mz.EvictionPolicy.lru(), st, timed_from=8)
+        r = run_batches(t, batches, nows, mz.EvictionPolicy.lru(), st, timed_from=8, split=False)
         ref = ref_time(caps, 128, bn, nows, 2, 0, warm=8)
         out[f"lru_S{shards}"] = dict(gpu=r, reference=ref)
     return dict(config=f"LRU pool {pool_factor} x rows", **out)
