@@ -585,7 +585,8 @@ def main():
                          "launch_ms": probe_ms, "peak_source": peak_src,
                          "random_sector_ceiling_gbs": random_sector_ceiling(),
                          "random_access_ceiling": random_access_ceiling(),
-                         "random_access_frac": _access_frac(probe_ms),
+                         # (the ncu access count is for the single-GPU C5 launch)
+                         "random_access_frac": _access_frac(probe_ms) if (world == 1 and rows == ROWS) else None,
                          "share_of_step": probe_ms / ms_step,
                          "batch_algorithmic_bytes": batch_bytes,
                          "batch_gbs": batch_bytes / (batch_ms / 1e3) / 1e9 if batch_ms else 0.0,
