@@ -567,14 +567,18 @@ class MpzchTable:
             self._h, ctypes.c_void_p(rows.data_ptr()), rows.numel(), ctypes.c_void_p(g.data_ptr()),
             g.numel(), lr, beta, ctypes.c_void_p(st.cuda_stream)))
 
-    def lookup_gather_device(self, ids, stream=None):
-        """Fused lookup + gather: (slots, outcomes, rows[n, dim]) device tensors."""
+    def lookup_gather_device(self, ids, stream=None, out=None):
+        """Fused lookup + gather: (slots, outcomes, rows[n, dim]) device tensors (out: a
+        preallocated (slots, outcomes, rows) triple to fill instead)."""
         import torch
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         n = ids.numel()
-        slots = torch.empty(n, dtype=torch.int64, device=ids.device)
-        oc = torch.empty(n, dtype=torch.uint8, device=ids.device)
-        rows = torch.empty((n, self.dim), dtype=torch.float32, device=ids.device)
+        if out is not None:
+            slots, oc, rows = out
+        else:
+            slots = torch.empty(n, dtype=torch.int64, device=ids.device)
+            oc = torch.empty(n, dtype=torch.uint8, device=ids.device)
+            rows = torch.empty((n, self.dim), dtype=torch.float32, device=ids.device)
         _check(self._lib.mpzch_lookup_gather_device(
             self._h, ctypes.c_void_p(ids.data_ptr()), n, ctypes.c_void_p(slots.data_ptr()),
             ctypes.c_void_p(oc.data_ptr()), ctypes.c_void_p(rows.data_ptr()),
@@ -627,6 +631,18 @@ class MpzchTable:
 
     def kernel_launches(self) -> int:
         return int(self._lib.mpzch_kernel_launches(self._h))
+
+    def serialize_snapshot_into(self, out) -> int:
+        """serialize_snapshot into a caller buffer (e.g. page-locked uint8 numpy); returns the
+        image length.  The buffer must hold snapshot_size() bytes."""
+        n = ctypes.c_uint64(0)
+        _check(self._lib.mpzch_serialize_snapshot(self._h, _ptr(out), out.size, ctypes.byref(n)))
+        return n.value
+
+    def snapshot_size(self) -> int:
+        n = ctypes.c_uint64(0)
+        _check(self._lib.mpzch_serialize_snapshot(self._h, None, 0, ctypes.byref(n)))
+        return n.value
 
     def serialize_snapshot(self) -> bytes:
         """serialize_snapshot (publish.cpp:126-155): the .mpzc image, CRC-32 on the device."""

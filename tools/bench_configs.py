@@ -274,6 +274,80 @@ def lru08():
     return lru(0.8)
 
 
+def serve():
+    """Not a BASELINE config: the frozen-replica read path -- batched lookup
+    and fused lookup + row gather on a 2^24-row dim-128 table prefilled to 0.8, 1M-position
+    batches (90% present ids, 10% absent)."""
+    rows, dim, B = 1 << 24, 128, 1 << 20
+    caps = mz.even_capacities(rows, 8)
+    t = mz.MpzchTable(mz.TableConfig(caps, 128, 7, dim, 11))
+    pol = mz.EvictionPolicy.disabled()
+    st = torch.cuda.current_stream()
+    npre = int(0.8 * rows)
+    out_s = torch.empty(B, dtype=torch.int64, device="cuda")
+    out_o = torch.empty(B, dtype=torch.uint8, device="cuda")
+    for a in range(0, npre, B):
+        ids = bench.distinct_ids_t(6, torch.arange(a, min(a + B, npre), dtype=torch.int64, device="cuda"))
+        t.process_batch_device(ids, 1, pol, None, out_s, out_o, None, st)
+    g = torch.Generator(device="cuda").manual_seed(6)
+    nb = 10
+    batches = [bench.distinct_ids_t(6, torch.randint(0, int(npre / 0.9), (B,), generator=g, device="cuda"))
+               for _ in range(nb + 2)]
+    torch.cuda.synchronize()
+    rows_out = torch.empty((B, dim), dtype=torch.float32, device="cuda")
+    trip = (out_s, out_o, rows_out)
+    for b in range(2):
+        t.lookup_device(batches[b], out_s, out_o, st)
+        t.lookup_gather_device(batches[b], st, out=trip)
+    ms_l = ev_time(lambda: [t.lookup_device(batches[2 + b], out_s, out_o, st) for b in range(nb)], st)
+    ms_g = ev_time(lambda: [t.lookup_gather_device(batches[2 + b], st, out=trip) for b in range(nb)], st)
+    found = int((out_o == 0).sum().item())
+    return dict(config="serve (2^24 rows, dim 128, 1M-position lookups)", lookup_ids_per_s=nb * B / (ms_l / 1e3),
+                lookup_gather_ids_per_s=nb * B / (ms_g / 1e3),
+                gather_gbs=nb * B * dim * 4 * 2 / (ms_g / 1e3) / 1e9, found_fraction=found / B)
+
+
+def publish():
+    """Not a BASELINE config: publication images from HBM -- the .mpzc
+    snapshot of a 2^22-row dim-128 table (2.1 GB image, CRC-32 on the device) and the .mpzd
+    delta of the rows one 1M-position TTL batch dirtied."""
+    rows, dim, B = 1 << 22, 128, 1 << 20
+    caps = mz.even_capacities(rows, 8)
+    t = mz.MpzchTable(mz.TableConfig(caps, 128, 7, dim, 11))
+    pol = mz.EvictionPolicy.ttl(mz.TtlPolicy(3600))
+    st = torch.cuda.current_stream()
+    npre = int(0.8 * rows)
+    out_s = torch.empty(B, dtype=torch.int64, device="cuda")
+    out_o = torch.empty(B, dtype=torch.uint8, device="cuda")
+    for a in range(0, npre, B):
+        ids = bench.distinct_ids_t(7, torch.arange(a, min(a + B, npre), dtype=torch.int64, device="cuda"))
+        t.process_batch_device(ids, 1, pol, None, out_s, out_o, None, st)
+    torch.cuda.synchronize()
+    size = t.snapshot_size()
+    buf = torch.empty(size, dtype=torch.uint8).pin_memory().numpy()  # page-locked image buffer
+    t.serialize_snapshot_into(buf)  # warm (staging buffers)
+    t0 = time.perf_counter()
+    t.serialize_snapshot_into(buf)
+    snap_s = time.perf_counter() - t0
+    img = buf.tobytes()
+    wts = torch.empty(rows * dim, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    mz.crc32_device(wts)
+    crc_s = time.perf_counter() - t0
+    src = mz.DeltaSource(t, mz.snapshot_checksum(img))
+    g = torch.Generator(device="cuda").manual_seed(7)
+    ids = bench.distinct_ids_t(7, torch.randint(0, 2 * npre, (B,), generator=g, device="cuda"))
+    t.process_batch_device(ids, 10000, pol, None, out_s, out_o, None, st)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    delta = src.cut()
+    delta_s = time.perf_counter() - t0
+    return dict(config="publish (2^22 rows, dim 128)", snapshot_bytes=len(img), snapshot_s=snap_s,
+                snapshot_gbs=len(img) / snap_s / 1e9, delta_bytes=len(delta), delta_s=delta_s,
+                delta_gbs=len(delta) / delta_s / 1e9, crc32_device_gbs=rows * dim * 4 / crc_s / 1e9)
+
+
 def train():
     """Not a BASELINE config: the reference's churn training loop (proj/src/experiments.cpp:86-125)
     at scale -- remap a batch (TTL evictions reset rows), then sgd_step over the distinct
