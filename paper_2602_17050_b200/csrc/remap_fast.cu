@@ -163,8 +163,8 @@ __global__ void __launch_bounds__(256) k_validate(TableDev t, const uint64_t* __
 
 // K1: probe; each thread keeps U positions in flight (independent sector loads), all
 // positions of a round are issued before any is scanned.
-template <int MODE, int U>
-__global__ void __launch_bounds__(256, MODE == kModeTtl ? 3 : 4) k_probe(TableDev t, const uint64_t* __restrict__ ids,
+template <int MODE, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t* __restrict__ ids,
                                                uint64_t n, uint64_t now, uint64_t meta_value,
                                                BatchCounters* ctr,
                                                uint64_t* __restrict__ out_slots,
@@ -868,13 +868,14 @@ void run_validate(Table& t, const uint64_t* ids, uint64_t n, cudaStream_t st) {
 }
 
 void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
-    constexpr int kU = 2;  // positions in flight per probe thread
+    constexpr int kU = 1;  // positions per probe thread (more threads beat more positions per
+                           // thread: C5 probe 0.46 -> 0.39 ms going from 2 x 4 blocks/SM to 1 x 6)
     const uint64_t n = a.n;
     t.ensure_fast_scratch(n);
     const uint64_t epoch = ++t.epoch;
     const unsigned B = 256;
     const unsigned gW = grid_for(n, B, 148u * 8u);  // count-driven kernels
-    const unsigned gP = grid_for((n + kU - 1) / kU, B, 148u * 16u);
+    const unsigned gP = grid_for((n + kU - 1) / kU, B, 148u * 24u);
     const bool ttl = a.pol->mode == kModeTtl;
     const bool lru = a.pol->mode == kModeLru;
     uint32_t* newpos = t.s_newpos.as<uint32_t>();
@@ -904,11 +905,17 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
         const unsigned gl = grid_for(4 * ((n + kUL - 1) / kUL), B, 148u * 16u);
         if (ttl) launch_pdl(k_probe_line<kModeTtl, kUL, 3>, gl, B, st, MPZCH_PROBE_ARGS);
         else if (lru) launch_pdl(k_probe_line<kModeLru, kUL, 4>, gl, B, st, MPZCH_PROBE_ARGS);
+        // long windows: one position per quad at 8 blocks/SM (C3 insert-heavy 1.88 -> 2.07 G/s);
+        // small batches keep 2 per quad (C1 1.10 vs 1.04 G/s pipelined)
+        else if (t.P >= 256)
+            launch_pdl(k_probe_line<kModeDisabled, 1, 8>, grid_for(4 * n, B, 148u * 32u), B, st, MPZCH_PROBE_ARGS);
         else launch_pdl(k_probe_line<kModeDisabled, kUL, 4>, gl, B, st, MPZCH_PROBE_ARGS);
     } else {
-        if (ttl) launch_pdl(k_probe<kModeTtl, kU>, gP, B, st, MPZCH_PROBE_ARGS);
-        else if (lru) launch_pdl(k_probe<kModeLru, kU>, gP, B, st, MPZCH_PROBE_ARGS);
-        else launch_pdl(k_probe<kModeDisabled, kU>, gP, B, st, MPZCH_PROBE_ARGS);
+        // TTL walks carry a metadata sector per round too: 2 positions per thread at 3 blocks/SM
+        // (C2: 2.78 vs 2.40 G/s for 1 x 4; C4 1.04 vs 1.09)
+        if (ttl) launch_pdl(k_probe<kModeTtl, 2, 3>, grid_for((n + 1) / 2, B, 148u * 16u), B, st, MPZCH_PROBE_ARGS);
+        else if (lru) launch_pdl(k_probe<kModeLru, 1, 6>, gP, B, st, MPZCH_PROBE_ARGS);
+        else launch_pdl(k_probe<kModeDisabled, 1, 6>, gP, B, st, MPZCH_PROBE_ARGS);
     }
 #undef MPZCH_PROBE_ARGS
     ++t.launches;
