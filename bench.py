@@ -579,7 +579,7 @@ def main():
                        "outcomes_per_step_rank0_owner": {k: v / args.steps for k, v in agg.items()}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic() if world == 1 else None,
-                         "kernel": "k_probe<Disabled,2> (probe of every position; rank 0)",
+                         "kernel": "k_probe<Disabled, 1 position per thread> (probe of every position; rank 0)",
                          "algorithmic_bytes_per_launch": probe_bytes,
                          "probe_sectors_per_launch": prof["probe_sectors"] / max(prof["probe_launches"], 1),
                          "launch_ms": probe_ms, "peak_source": peak_src,
