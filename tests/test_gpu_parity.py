@@ -598,3 +598,29 @@ def test_lru_claim_path_and_fallback(oracle, line):
         assert_same_state(gpu_state(t, 4), oracle_state(o, 4), f"batch {bi}")
         paths.append(t.last_stats()["path"])
     assert "fast" in paths and "rounds" in paths, paths
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_large_batches_sector_probe(oracle, mode):
+    """Batches above 256K positions take the per-thread sector probe (the C5 kernel; smaller
+    batches and max_probe >= 256 take the quad line walk): Disabled, uniform TTL (expired
+    owners, evictions) and eviction-free LRU against the oracle, state after every batch."""
+    rows = 1 << 20
+    caps = mz.even_capacities(rows, 4)
+    uni = oracle.distinct_ids(51 + mode, 0, int(rows * 0.75))
+    rng = np.random.default_rng(mode)
+    n = 300_000
+    t = mz.MpzchTable(mz.TableConfig(caps, 64, 7, 4 if mode == 1 else 0, 3))
+    o = oracle.OracleTable(caps, 64, 7, 4 if mode == 1 else 0, 3)
+    p = pol(mode, 30, None)
+    hi = 250_000
+    for b in range(4):
+        hi = min(uni.size, hi + 120_000)
+        ids = uni[rng.integers(0, hi, n)]
+        now = 100 + 20 * b
+        gs, go, ge = t.process_batch(ids, now, p)
+        os_, oo, oe = o.process_batch(ids, now, mode, 30, None, None)
+        assert (gs == os_).all() and (go == oo).all() and (ge == oe).all(), f"batch {b}"
+        assert t.last_stats()["path"] == "fast"
+        dim = 4 if mode == 1 else 0
+        assert_same_state(gpu_state(t, dim), oracle_state(o, dim), f"batch {b}")
