@@ -17,11 +17,17 @@ namespace mpzch_b200 {
 
 namespace {
 
-__device__ __forceinline__ float draw_elem(uint64_t s0, uint64_t j, double bound) {
-    const uint64_t z = splitmix_out(s0 + (j + 1) * kGolden);
-    const double u = (double)(z >> 11) * 0x1.0p-53;
-    const double t = __dadd_rn(__dmul_rn(2.0, u), -1.0);
+// element with SplitMix64 state `state` (= s0 + (j+1) * golden for element j)
+__device__ __forceinline__ float draw_at(uint64_t state, double bound) {
+    const uint64_t z = splitmix_out(state);
+    // 2u - 1 with u = (z >> 11) * 2^-53 is exactly ((z >> 11) - 2^52) * 2^-52: one exact
+    // integer -> double conversion instead of a multiply and an add (both exact as well)
+    const double t = (double)((int64_t)(z >> 11) - (1ll << 52)) * 0x1.0p-52;
     return __double2float_rn(__dmul_rn(t, bound));
+}
+
+__device__ __forceinline__ float draw_elem(uint64_t s0, uint64_t j, double bound) {
+    return draw_at(s0 + (j + 1) * kGolden, bound);
 }
 
 // init: grid-stride over (row, quad) for dim % 4 == 0, else over elements
@@ -77,12 +83,13 @@ __global__ void __launch_bounds__(256) k_reset_rows(TableDev t, const uint64_t* 
                 float4* m4 = reinterpret_cast<float4*>(m);
                 const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
                 for (uint32_t q = lane; q < t.dim / 4; q += 32) {
-                    const uint64_t j = (uint64_t)q * 4;
+                    // states of elements 4q .. 4q+3: one multiply, then golden increments
+                    const uint64_t s1 = s0 + ((uint64_t)q * 4 + 1) * kGolden;
                     float4 v;
-                    v.x = draw_elem(s0, j, t.bound);
-                    v.y = draw_elem(s0, j + 1, t.bound);
-                    v.z = draw_elem(s0, j + 2, t.bound);
-                    v.w = draw_elem(s0, j + 3, t.bound);
+                    v.x = draw_at(s1, t.bound);
+                    v.y = draw_at(s1 + kGolden, t.bound);
+                    v.z = draw_at(s1 + 2 * kGolden, t.bound);
+                    v.w = draw_at(s1 + 3 * kGolden, t.bound);
                     w4[q] = v;
                     m4[q] = z;
                 }
