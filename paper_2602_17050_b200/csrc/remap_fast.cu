@@ -10,9 +10,9 @@
 //   K0 validate   streaming pass over the ids: first invalid position (and, on a
 //                 row-sharded handle, ids of shards it does not hold).  Nothing below
 //                 mutates a batch that failed here.
-//   K1 probe      one thread per POSITION (2 in flight per thread), 32-byte sector loads
-//                 from the home slot up to the first match or EMPTY (hole-free early
-//                 exit).  Hits on live slots and full windows are final here
+//   K1 probe      one thread per POSITION, 32-byte sector loads from the home slot up to
+//                 the first match or EMPTY (hole-free early exit); long
+//                 windows and small batches: one quad per position, 128-byte lines.  Hits on live slots and full windows are final here
 //                 and write their metadata word; everything else goes to the new list.
 //   K2 dedup      new positions -> one 64-byte entry per distinct id (128-bit atomicCAS on
 //                 an epoch-tagged key), rank = first position (atomicMax of ~position).
