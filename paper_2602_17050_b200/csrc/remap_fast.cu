@@ -12,8 +12,9 @@
 //                 mutates a batch that failed here.
 //   K1 probe      one thread per POSITION, 32-byte sector loads from the home slot up to
 //                 the first match or EMPTY (hole-free early exit); long
-//                 windows and small batches: one quad per position, 128-byte lines.  Hits on live slots and full windows are final here
-//                 and write their metadata word; everything else goes to the new list.
+//                 windows and small batches: one quad per position, 128-byte lines.
+//                 Hits on live slots and full windows are final here and write their
+//                 metadata word; everything else goes to the new list.
 //   K2 dedup      new positions -> one 64-byte entry per distinct id (128-bit atomicCAS on
 //                 an epoch-tagged key), rank = first position (atomicMax of ~position).
 //                 (id, feature) secondaries are resolved from the id's first position in K5.
