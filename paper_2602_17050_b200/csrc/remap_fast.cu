@@ -876,6 +876,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     const uint64_t epoch = ++t.epoch;
     const unsigned B = 256;
     const unsigned gW = grid_for(n, B, 148u * 8u);  // count-driven kernels (4/16/32 x 148: same)
+    // 24 blocks per SM of grid (4 waves at 6 resident): 18 / 30 / 36 / 48 measured slower
     const unsigned gP = grid_for((n + kU - 1) / kU, B, 148u * 24u);
     const bool ttl = a.pol->mode == kModeTtl;
     const bool lru = a.pol->mode == kModeLru;
