@@ -291,6 +291,96 @@ private:
     std::vector<std::uint64_t> caps_, offsets_;
 };
 
+// ---- publish (proj/include/mpzch/publish.hpp): the images are built from HBM, CRC on the device
+
+// crc32 (publish.hpp:20-22) of host bytes, with the reference's polynomial and conditioning
+inline std::uint32_t crc32(std::span<const std::uint8_t> bytes) {
+    std::uint32_t c = ~0u;
+    for (std::uint8_t b : bytes) {
+        c ^= b;
+        for (int k = 0; k < 8; ++k) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
+    }
+    return ~c;
+}
+
+// serialize_snapshot (publish.hpp:39): the byte-identical .mpzc image
+inline std::vector<std::uint8_t> serialize_snapshot(const MpzchTable& table) {
+    std::uint64_t n = 0;
+    check(mpzch_serialize_snapshot(table.handle(), nullptr, 0, &n));
+    std::vector<std::uint8_t> out(n);
+    check(mpzch_serialize_snapshot(table.handle(), out.data(), out.size(), &n));
+    return out;
+}
+
+// snapshot_checksum (publish.hpp:42-44): the trailer CRC, the lineage id deltas carry
+inline std::uint32_t snapshot_checksum(std::span<const std::uint8_t> bytes) {
+    if (bytes.size() < 4) throw std::invalid_argument("truncated snapshot");
+    const std::size_t k = bytes.size() - 4;
+    return std::uint32_t(bytes[k]) | std::uint32_t(bytes[k + 1]) << 8 | std::uint32_t(bytes[k + 2]) << 16 |
+           std::uint32_t(bytes[k + 3]) << 24;
+}
+
+struct DeltaRecord {
+    std::uint64_t global_row = 0;
+    Id identity = kEmptySlot;
+    std::vector<float> weights;
+};
+
+struct DeltaLog {
+    std::uint32_t base_checksum = 0;
+    std::uint64_t sequence = 0;
+    std::uint32_t dim = 0;
+    std::vector<DeltaRecord> records;
+};
+
+// DeltaSource (publish.hpp:66-80): each cut() captures exactly the rows dirtied since the
+// previous one.  cut_image() is the fused device path (cut + serialize_delta in one call, the
+// .mpzd image byte-identical to serialize_delta(cut())).
+class DeltaSource {
+public:
+    DeltaSource(MpzchTable& table, std::uint32_t base_checksum) : table_(&table), base_(base_checksum) {
+        if (table.dim() == 0) throw std::logic_error("index-only tables (dim = 0) cannot be published");
+        check(mpzch_make_cursor(table.handle(), &cursor_));
+    }
+
+    DeltaLog cut() {
+        const std::uint32_t dim = table_->dim();
+        std::uint64_t n = 0, next = 0;
+        check(mpzch_delta_cut(table_->handle(), cursor_, nullptr, nullptr, nullptr, 0, &n, &next));
+        std::vector<std::uint64_t> rows(n), ids(n);
+        std::vector<float> w(n * dim);
+        check(mpzch_delta_cut(table_->handle(), cursor_, rows.data(), ids.data(), w.data(), n, &n, &next));
+        DeltaLog log;
+        log.base_checksum = base_;
+        log.sequence = seq_++;
+        log.dim = dim;
+        log.records.resize(n);
+        for (std::uint64_t i = 0; i < n; ++i) {
+            log.records[i].global_row = rows[i];
+            log.records[i].identity = ids[i];
+            log.records[i].weights.assign(w.begin() + i * dim, w.begin() + (i + 1) * dim);
+        }
+        cursor_ = next;
+        return log;
+    }
+
+    std::vector<std::uint8_t> cut_image() {
+        std::uint64_t n = 0, next = 0;
+        check(mpzch_serialize_delta(table_->handle(), cursor_, base_, seq_, nullptr, 0, &n, &next));
+        std::vector<std::uint8_t> out(n);
+        check(mpzch_serialize_delta(table_->handle(), cursor_, base_, seq_, out.data(), out.size(), &n, &next));
+        cursor_ = next;
+        ++seq_;
+        return out;
+    }
+
+private:
+    MpzchTable* table_;
+    std::uint32_t base_;
+    std::uint64_t seq_ = 0;
+    std::uint64_t cursor_ = 0;
+};
+
 // process_batch (batch_engine.hpp:44-46): same signature, same results.
 inline std::vector<ProbeResult> process_batch_with_evicted(MpzchTable& table, const IdBatch& batch,
                                                            const EvictionPolicy& policy,

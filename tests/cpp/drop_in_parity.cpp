@@ -6,12 +6,14 @@
 // and tests/test_gpu_cpp.py runs it.
 #include <cstdint>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "mpzch/batch_engine.hpp"
+#include "mpzch/publish.hpp"
 #include "mpzch/rng.hpp"
 #include "mpzch_b200.hpp"
 
@@ -32,6 +34,9 @@ struct Ref {
         return v;
     }
     static auto pb(Table& t, const Batch& b, const Policy& p) { return mpzch::process_batch(t, b, p); }
+    using Delta = mpzch::DeltaSource;
+    static std::vector<std::uint8_t> snap(const Table& t) { return mpzch::serialize_snapshot(t); }
+    static std::uint32_t cks(const std::vector<std::uint8_t>& b) { return mpzch::snapshot_checksum(b); }
 };
 
 struct Gpu {
@@ -43,6 +48,9 @@ struct Gpu {
     static std::vector<std::uint64_t> ident(const Table& t, std::uint32_t s) { return t.identities(s); }
     static std::vector<std::uint64_t> meta(const Table& t, std::uint32_t s) { return t.metadata(s); }
     static auto pb(Table& t, const Batch& b, const Policy& p) { return mpzch_b200::process_batch(t, b, p); }
+    using Delta = mpzch_b200::DeltaSource;
+    static std::vector<std::uint8_t> snap(const Table& t) { return mpzch_b200::serialize_snapshot(t); }
+    static std::uint32_t cks(const std::vector<std::uint8_t>& b) { return mpzch_b200::snapshot_checksum(b); }
 };
 
 struct Trace {
@@ -96,8 +104,29 @@ Trace run(std::uint64_t seed, int mode) {
     };
     std::vector<float> grads(last_rows.size() * table.dim());
     for (float& g : grads) g = static_cast<float>(rng.next_unit() - 0.5);
+    // publication: the .mpzc image byte for byte, then a delta source cut after the training
+    // step (rows, identities, weights of every dirtied row)
+    const std::vector<std::uint8_t> img = NS::snap(table);
+    tr.out.push_back(img.size());
+    for (std::size_t i = 0; i < img.size(); i += 8) {
+        std::uint64_t w = 0;
+        std::memcpy(&w, img.data() + i, std::min<std::size_t>(8, img.size() - i));
+        tr.out.push_back(w);
+    }
+    typename NS::Delta src(table, NS::cks(img));
     const auto cursor = table.make_cursor();
     table.sgd_step(last_rows, grads, 0.05f, 0.9f);
+    {
+        const auto log = src.cut();
+        tr.out.push_back(log.base_checksum);
+        tr.out.push_back(log.sequence);
+        tr.out.push_back(log.records.size());
+        for (const auto& r : log.records) {
+            tr.out.push_back(r.global_row);
+            tr.out.push_back(r.identity);
+            for (float v : r.weights) bits(v);
+        }
+    }
     for (float v : table.gather(last_rows)) bits(v);
     for (std::uint64_t r : last_rows) {
         for (float v : table.momentum_row(r)) bits(v);
