@@ -915,6 +915,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     } else {
         // TTL walks carry a metadata sector per round too: 2 positions per thread at 3 blocks/SM
         // (C2: 2.78 vs 2.40 G/s for 1 x 4; C4 1.04 vs 1.09)
+        // (C2 swept: 1 or 4 positions per thread, 3-32 blocks/SM of grid: all slower)
         if (ttl) launch_pdl(k_probe<kModeTtl, 2, 3>, grid_for((n + 1) / 2, B, 148u * 16u), B, st, MPZCH_PROBE_ARGS);
         else if (lru) launch_pdl(k_probe<kModeLru, 1, 6>, gP, B, st, MPZCH_PROBE_ARGS);
         else launch_pdl(k_probe<kModeDisabled, 1, 6>, gP, B, st, MPZCH_PROBE_ARGS);
