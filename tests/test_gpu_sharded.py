@@ -49,13 +49,14 @@ def run_sharded(cfg, world, batches, pol):
     return out, tables
 
 
-@pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("mode", [0, 1, 2])
 def test_sharded_equals_single_table(oracle, world, mode):
     rows = 1 << 16
     caps = mz.even_capacities(rows, 8)
     cfg = mz.TableConfig(caps, 32, 7, 8 if mode == 1 else 0, 3)
-    pol = mz.EvictionPolicy.ttl(mz.TtlPolicy(50)) if mode == 1 else mz.EvictionPolicy.disabled()
+    pol = (mz.EvictionPolicy.ttl(mz.TtlPolicy(50)) if mode == 1 else
+           mz.EvictionPolicy.lru() if mode == 2 else mz.EvictionPolicy.disabled())
     uni = oracle.distinct_ids(9, 0, rows)
     rng = np.random.default_rng(world + 10 * mode)
     batches = [(uni[rng.integers(0, uni.size, 20000)],
