@@ -134,6 +134,14 @@ mpzch_status mpzch_process_batch_device_async(mpzch_table* t, const uint64_t* id
                                               uint64_t evicted_cap, void* stream,
                                               uint64_t* out_ticket);
 mpzch_status mpzch_batch_wait(mpzch_table* t, uint64_t ticket, uint64_t* out_evicted_n);
+/* Batched read-only lookup (MpzchTable::lookup per position) enqueued on `stream` without
+ * waiting; the ticket shares the batch ring, and mpzch_batch_wait reports the status the
+ * synchronous mpzch_lookup_device would have returned (invalid id: the reference's
+ * require_valid_id text; id of a shard this handle does not hold: MPZCH_ERANGE).  Ordered after
+ * this handle's pending batches. */
+mpzch_status mpzch_lookup_device_async(mpzch_table* t, const uint64_t* ids, uint64_t n,
+                                       uint64_t* out_slots, uint8_t* out_outcomes, void* stream,
+                                       uint64_t* out_ticket);
 
 /* ---- lookup-only: MpzchTable::lookup(Id) const, table.hpp:65, table.cpp:150-156,
  *      batched (semantics = one lookup per position, no writes). */

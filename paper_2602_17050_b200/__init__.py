@@ -181,6 +181,7 @@ _SIGS = {
     "mpzch_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),
     "mpzch_get_profile": (ctypes.c_int, [_vp, ctypes.POINTER(_Profile)]),
     "mpzch_last_stats": (ctypes.c_int, [_vp, ctypes.POINTER(_Stats)]),
+    "mpzch_lookup_device_async": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _vp, _vp, _vp, _u64p]),
     "mpzch_kernel_launches": (ctypes.c_uint64, [_vp]),
     "mpzch_last_error": (ctypes.c_char_p, []),
     "mpzch_build_info": (ctypes.c_char_p, []),
@@ -469,6 +470,17 @@ class MpzchTable:
                                              ctypes.c_void_p(out_slots.data_ptr()),
                                              ctypes.c_void_p(out_outcomes.data_ptr()),
                                              ctypes.c_void_p(st.cuda_stream)))
+
+    def lookup_device_async(self, ids, out_slots, out_outcomes, stream=None) -> int:
+        """Enqueue a batched lookup on device tensors; returns a ticket (see wait)."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        tk = ctypes.c_uint64(0)
+        _check(self._lib.mpzch_lookup_device_async(self._h, ctypes.c_void_p(ids.data_ptr()), ids.numel(),
+                                                   ctypes.c_void_p(out_slots.data_ptr()),
+                                                   ctypes.c_void_p(out_outcomes.data_ptr()),
+                                                   ctypes.c_void_p(st.cuda_stream), ctypes.byref(tk)))
+        return tk.value
 
     def lookup_or_insert(self, id: int, feature: int, now: int, policy: EvictionPolicy):
         """MpzchTable::lookup_or_insert (table.cpp:98-110): (global slot, outcome)."""

@@ -211,7 +211,30 @@ __global__ void __launch_bounds__(256) k_lookup_gather(TableDev t, const uint64_
     }
 }
 
+__global__ void k_lookup_init(BatchCounters* c) {
+    if (threadIdx.x == 0) {
+        BatchCounters z{};
+        z.err.bad_pos = ~0ull;
+        z.err.foreign_pos = ~0ull;
+        *c = z;
+    }
+}
+
+// the id at the first invalid position (the exception text distinguishes EMPTY from > 2^63)
+__global__ void k_lookup_bad_id(const uint64_t* __restrict__ ids, BatchCounters* c) {
+    pdl_wait();
+    if (threadIdx.x == 0 && c->err.bad_pos != ~0ull) c->bad_id = ids[c->err.bad_pos];
+}
+
 }  // namespace
+
+void launch_lookup_async(Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots, uint8_t* out_oc,
+                         BatchCounters* c, cudaStream_t st) {
+    k_lookup_init<<<1, 32, 0, st>>>(c);
+    run_lookup(t, ids, n, out_slots, out_oc, &c->err, st);
+    launch_pdl(k_lookup_bad_id, 1, 32, st, ids, c);
+    t.launches += 3;
+}
 
 void run_lookup_gather(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots,
                        uint8_t* out_oc, float* out_rows, BatchErr* err, cudaStream_t st) {

@@ -324,7 +324,10 @@ void complete_slot(Table& t, int si) {
     const BatchCounters& c = t.h_ring[si];
     Table::Result r;
     r.ticket = sl.ticket;
-    if (c.err.too_many == 2) {
+    if (sl.lookup && c.err.bad_pos != ~0ull) {  // MpzchTable::lookup -> require_valid_id (ids.hpp:25-31)
+        r.status = MPZCH_EINVAL;
+        r.msg = c.bad_id == ~0ull ? "id is the empty-slot sentinel" : "id exceeds the 63-bit ID space";
+    } else if (c.err.too_many == 2) {
         r.status = MPZCH_ECUDA;
         r.msg = "internal error: claim invariant violated";
     } else if (c.err.bad_pos != ~0ull) {
@@ -510,6 +513,7 @@ uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uin
     sl.path = fast ? MPZCH_PATH_AUTO : (rounds ? MPZCH_PATH_ROUNDS : MPZCH_PATH_ORDERED);
     sl.overflow_all = a.overflow_all;
     sl.profiled = profiled && fast && !lru_try;  // per-kernel events: plain fast batches only
+    sl.lookup = false;
     t.last_stream = st;
     t.last_ticket = ticket;
     return ticket;
@@ -792,6 +796,47 @@ mpzch_status mpzch_lookup_device(const mpzch_table* t, const uint64_t* ids, uint
         if (T.h_aux->err.foreign_pos != ~0ull)
             throw Error{MPZCH_ERANGE, "id at batch position " + std::to_string(T.h_aux->err.foreign_pos) +
                                           " routes to a shard this handle does not hold"};
+    });
+}
+
+mpzch_status mpzch_lookup_device_async(mpzch_table* t, const uint64_t* ids, uint64_t n,
+                                       uint64_t* out_slots, uint8_t* out_oc, void* stream,
+                                       uint64_t* out_ticket) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        DeviceGuard g(T.device);
+        cudaStream_t st = (cudaStream_t)stream;
+        const uint64_t ticket = T.next_ticket++;
+        const int si = (int)(ticket % Table::kRing);
+        *out_ticket = ticket;
+        if (n == 0) {
+            Table::Result r;
+            r.ticket = ticket;
+            T.results[ticket % Table::kResults] = r;
+            return;
+        }
+        complete_slot(T, si);
+        if (T.last_ticket && st != T.last_stream) {  // after the handle's pending batches
+            const Table::Slot& prev = T.slots[T.last_ticket % Table::kRing];
+            if (prev.busy && prev.ticket == T.last_ticket) MPZCH_CUDA(cudaStreamWaitEvent(st, prev.done, 0));
+        }
+        Table::Slot& sl = T.slots[si];
+        BatchCounters* dc = T.d_ring + si;
+        launch_lookup_async(T, ids, n, out_slots, out_oc, dc, st);
+        MPZCH_CUDA(cudaGetLastError());
+        MPZCH_CUDA(cudaMemcpyAsync(T.h_ring + si, dc, sizeof(BatchCounters), cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaEventRecord(sl.done, st));
+        sl.busy = true;
+        sl.ticket = ticket;
+        sl.n = n;
+        sl.fast = false;
+        sl.path = MPZCH_PATH_AUTO;
+        sl.overflow_all = false;
+        sl.profiled = false;
+        sl.lookup = true;
+        T.last_stream = st;
+        T.last_ticket = ticket;
     });
 }
 

@@ -54,6 +54,8 @@ struct BatchCounters {
     unsigned int pad;
     unsigned int dup_items;      // fast path: new-list items whose id was already in the id table
     unsigned int lru_abort;      // LRU on the fast path: an eviction is needed -> rounds path
+    unsigned int pad3;
+    unsigned long long bad_id;   // lookups: the id at err.bad_pos (the exception text needs it)
     unsigned long long id_sectors, meta_sectors;  // sectors the probe kernel read
     // rounds path (device-driven): pending count per round parity, new suspects per closure
     // step parity, lowest rank among the unmarked last-step suspects, rounds run, uniques left
@@ -118,6 +120,7 @@ public:
         uint32_t path = 0, rounds = 0;
         uint64_t ticket = 0, n = 0;
         cudaEvent_t done = nullptr;
+        bool lookup = false;  // a batched read-only lookup (mpzch_lookup_device_async)
         cudaEvent_t ev[8] = {};
     };
     struct Result {
@@ -188,6 +191,9 @@ void launch_reset_rows(Table& t, const uint64_t* rows, const unsigned int* count
 void launch_write_slots(Table& t, const uint64_t* gslots, const uint64_t* ids, const uint64_t* metas,
                         uint64_t n, cudaStream_t st);
 bool run_hole_check(Table& t);
+// lookup into a ring counter block (error word + the first bad id), all enqueued on st
+void launch_lookup_async(Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots, uint8_t* out_oc,
+                         BatchCounters* c, cudaStream_t st);
 void run_lookup(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots,
                 uint8_t* out_oc, BatchErr* err, cudaStream_t st);
 void run_lookup_gather(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots,

@@ -624,3 +624,43 @@ def test_large_batches_sector_probe(oracle, mode):
         assert t.last_stats()["path"] == "fast"
         dim = 4 if mode == 1 else 0
         assert_same_state(gpu_state(t, dim), oracle_state(o, dim), f"batch {b}")
+
+
+def test_lookup_async_tickets(oracle):
+    """mpzch_lookup_device_async: results equal the oracle's lookup, tickets interleave with
+    remap batches in enqueue order, and an invalid id is reported at wait with the reference's
+    require_valid_id text."""
+    import torch
+    caps = mz.even_capacities(1 << 14, 4)
+    t = mz.MpzchTable(mz.TableConfig(caps, 32, 7))
+    o = oracle.OracleTable(caps, 32, 7, 0, 0)
+    ids = oracle.distinct_ids(3, 0, 12000)
+    rng = np.random.default_rng(5)
+    p = mz.EvictionPolicy.disabled()
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.Stream(dev)
+    checks = []
+    for b in range(6):
+        ins = ids[rng.integers(0, 9000, 4000)]
+        q = ids[rng.integers(0, 12000, 5000)]
+        di = torch.from_numpy(ins.view(np.int64)).to(dev)
+        dq = torch.from_numpy(q.view(np.int64)).to(dev)
+        os_ = torch.empty(4000, dtype=torch.int64, device=dev)
+        oo = torch.empty(4000, dtype=torch.uint8, device=dev)
+        ls = torch.empty(5000, dtype=torch.int64, device=dev)
+        lo = torch.empty(5000, dtype=torch.uint8, device=dev)
+        torch.cuda.synchronize()
+        t1 = t.process_batch_device_async(di, 10 + b, p, None, os_, oo, None, st)
+        t2 = t.lookup_device_async(dq, ls, lo, st)
+        o.process_batch(ins, 10 + b, 0, 0, None, None)
+        ws, wo = o.lookup(q)
+        checks.append((t1, t2, ls, lo, ws, wo))
+    for t1, t2, ls, lo, ws, wo in checks:
+        t.wait(t1)
+        t.wait(t2)
+        assert (ls.cpu().numpy().view(np.uint64) == ws).all() and (lo.cpu().numpy() == wo).all()
+    bad = torch.tensor([5, -1, 7], dtype=torch.int64, device=dev)
+    tk = t.lookup_device_async(bad, torch.empty(3, dtype=torch.int64, device=dev),
+                               torch.empty(3, dtype=torch.uint8, device=dev), st)
+    with pytest.raises(mz.InvalidArgument, match="empty-slot sentinel"):
+        t.wait(tk)
