@@ -204,10 +204,17 @@ def c3():
     hits = bench.distinct_ids_t(3, hit_idx)
     half = torch.cat([hits[:B // 2], bench.distinct_ids_t(3, torch.arange(npre, npre + B // 2, device="cuda"))])
 
-    def look(q):
+    def look(q):  # pipelined: 8 lookups enqueued, then every ticket waited
+        def body():
+            for tk in [t.lookup_device_async(q, out_s, out_o, st) for _ in range(8)]:
+                t.wait(tk)
+        return ev_time(body, st) / 8
+
+    def look_sync(q):
         return ev_time(lambda: [t.lookup_device(q, out_s, out_o, st) for _ in range(8)], st) / 8
     lk = look(hits)
     lk_half = look(half)
+    lk_sync = look_sync(hits)
     fresh = bench.distinct_ids_t(3, torch.arange(npre + B, npre + B + B // 2, device="cuda"))
     ins = [torch.cat([hits[:B // 2], fresh]).contiguous()]
     for i in range(1, 5):
@@ -215,7 +222,8 @@ def c3():
         ins.append(torch.cat([hits[B // 2:], f2]).contiguous())
     r = run_batches(t, ins, [2 + i for i in range(5)], pol, st, timed_from=1)
     return dict(config="C3", prefill_s=prefill_s, lookup_ids_per_s=B / (lk / 1e3),
-                lookup_50pct_absent_ids_per_s=B / (lk_half / 1e3), insert_heavy=r)
+                lookup_50pct_absent_ids_per_s=B / (lk_half / 1e3),
+                lookup_sync_call_ids_per_s=B / (lk_sync / 1e3), insert_heavy=r)
 
 
 def c4():
@@ -299,7 +307,10 @@ def serve():
     for b in range(2):
         t.lookup_device(batches[b], out_s, out_o, st)
         t.lookup_gather_device(batches[b], st, out=trip)
-    ms_l = ev_time(lambda: [t.lookup_device(batches[2 + b], out_s, out_o, st) for b in range(nb)], st)
+    def lookups():
+        for tk in [t.lookup_device_async(batches[2 + b], out_s, out_o, st) for b in range(nb)]:
+            t.wait(tk)
+    ms_l = ev_time(lookups, st)
     ms_g = ev_time(lambda: [t.lookup_gather_device(batches[2 + b], st, out=trip) for b in range(nb)], st)
     found = int((out_o == 0).sum().item())
     return dict(config="serve (2^24 rows, dim 128, 1M-position lookups)", lookup_ids_per_s=nb * B / (ms_l / 1e3),
