@@ -183,6 +183,42 @@ def c2():
     return dict(config="C2", ttl=ttl, live_occupancy=live / rows, steady=res)
 
 
+def c2f():
+    """Not a BASELINE config: C2 with three features carrying different TTLs (per-feature
+    TTL: metadata values differ per feature, so batches take the A.4 rounds path)."""
+    rows = 1 << 26
+    universe = 1 << 27
+    w = torch.arange(1, universe + 1, dtype=torch.float64, device="cuda").pow_(-1.05)
+    zipf_ranks.cdf = torch.cumsum(w, 0) / w.sum()
+    del w
+    B = 1 << 20
+    pol = mz.EvictionPolicy.ttl(mz.TtlPolicy(42000, {1: 21000, 2: 84000}))
+    st = torch.cuda.current_stream()
+    caps = mz.even_capacities(rows, 8)
+    t = mz.MpzchTable(mz.TableConfig(caps, 128, 7))
+    g = torch.Generator(device="cuda").manual_seed(77)
+    warm, timed = 300, 16
+    out_s = torch.empty(B, dtype=torch.int64, device="cuda")
+    out_o = torch.empty(B, dtype=torch.uint8, device="cuda")
+    for b in range(warm):
+        r = zipf_ranks(B, 1.05, universe, 2000 + b)
+        f = torch.randint(0, 3, (B,), generator=g, device="cuda", dtype=torch.int32)
+        t.process_batch_device(bench.distinct_ids_t(2, r), 10**6 + 60 * b, pol, f, out_s, out_o, None, st)
+    batches, feats, nows = [], [], []
+    for b in range(warm, warm + timed):
+        batches.append(bench.distinct_ids_t(2, zipf_ranks(B, 1.05, universe, 2000 + b)).contiguous())
+        feats.append(torch.randint(0, 3, (B,), generator=g, device="cuda", dtype=torch.int32))
+        nows.append(10**6 + 60 * b)
+    torch.cuda.synchronize()
+
+    def body():
+        for b in range(timed):
+            t.process_batch_device(batches[b], nows[b], pol, feats[b], out_s, out_o, None, st)
+    ms = ev_time(body, st)
+    return dict(config="C2 with per-feature TTL", ids_per_s=timed * B / (ms / 1e3),
+                path=t.last_stats()["path"], rounds=t.last_stats()["rounds"])
+
+
 def c3():
     rows = 1 << 28
     caps = mz.even_capacities(rows, 8)
