@@ -91,3 +91,30 @@ def test_foreign_id_is_rejected():
     with pytest.raises(mz.OutOfRange, match="routes to a shard this handle does not hold"):
         t.process_batch(ids, 1, mz.EvictionPolicy.disabled())
     assert (t.identities_all() == np.uint64((1 << 64) - 1)).all()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_uneven_shards(oracle, world):
+    """Shard capacities that are not multiples of the 16-row line: every rank's held range
+    starts and ends inside a line (line-aligned allocation base, masked line walks), with
+    small batches (quad line walk) and one >256K-position batch (sector walk)."""
+    caps = [1003, 2050, 777, 4093, 1500, 3001, 999, 2577]
+    cfg = mz.TableConfig(caps, 24, 7, 4, 5)
+    pol = mz.EvictionPolicy.ttl(mz.TtlPolicy(30))
+    uni = oracle.distinct_ids(17, 0, sum(caps))
+    rng = np.random.default_rng(world)
+    batches = [(uni[rng.integers(0, uni.size, 5000 if b < 5 else 300_000)], None, 1 + 20 * b)
+               for b in range(6)]
+    out, tables = run_sharded(cfg, world, batches, pol)
+    o = oracle.OracleTable(caps, 24, 7, 4, 5)
+    for b, (ids, f, now) in enumerate(batches):
+        os_, oo, oe = o.process_batch(ids, now, 1, 30, {}, f)
+        gs = np.concatenate([out[r][b][0] for r in range(world)])
+        go = np.concatenate([out[r][b][1] for r in range(world)])
+        assert (gs == os_).all() and (go == oo).all(), f"batch {b}"
+        for r in range(world):
+            assert (out[r][b][2] == oe).all()
+    ident = o.identities_all()
+    for r in range(world):
+        t = tables[r].engine.table
+        assert (t.identities_all() == ident[t.row_lo:t.row_hi]).all()
