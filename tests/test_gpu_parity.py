@@ -664,3 +664,37 @@ def test_lookup_async_tickets(oracle):
                                torch.empty(3, dtype=torch.uint8, device=dev), st)
     with pytest.raises(mz.InvalidArgument, match="empty-slot sentinel"):
         t.wait(tk)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_configurations(oracle, seed):
+    """Randomised configurations against the oracle: shard count and uneven capacities (not
+    multiples of the 16-row line), max_probe from 1 up to the smallest capacity (whole-shard
+    wrapping windows), all three policies incl. per-feature TTL, batch sizes on both sides of
+    the line/sector probe switch, features on some batches; results and the full state after
+    every batch."""
+    rng = np.random.default_rng(1000 + seed)
+    S = int(rng.integers(1, 9))
+    caps = [int(c) for c in rng.integers(60, 20000, S)]
+    P = int(min(min(caps), rng.choice([1, 3, 8, 16, 48, 128, 256])))
+    mode = int(rng.integers(0, 3))
+    pf = {1: int(rng.integers(1, 40)), 2: int(rng.integers(1, 40))} if (mode == 1 and seed % 2) else None
+    dttl = int(rng.integers(1, 60))
+    dim = int(rng.choice([0, 0, 4]))
+    seed_tab = int(rng.integers(0, 1 << 32))
+    t = mz.MpzchTable(mz.TableConfig(caps, P, seed_tab, dim, 9))
+    o = oracle.OracleTable(caps, P, seed_tab, dim, 9)
+    pool = oracle.distinct_ids(seed, 0, int(sum(caps) * float(rng.choice([0.5, 0.9, 1.3]))))
+    p = pol(mode, dttl, pf)
+    now = 1
+    for b in range(5):
+        n = int(rng.choice([1, 17, 5000, 70000, 300000]))
+        ids = pool[rng.integers(0, pool.size, n)]
+        f = rng.integers(0, 3, n).astype(np.uint32) if (b % 2 or pf) else None
+        now += int(rng.integers(0, 25))
+        gs, go, ge = t.process_batch(ids, now, p, f)
+        os_, oo, oe = o.process_batch(ids, now, mode, dttl, pf, f)
+        assert (gs == os_).all(), f"slots differ: batch {b}, S={S}, P={P}, mode={mode}"
+        assert (go == oo).all(), f"outcomes differ: batch {b}"
+        assert (ge == oe).all(), f"evicted list differs: batch {b}"
+        assert_same_state(gpu_state(t, dim), oracle_state(o, dim), f"batch {b}")
