@@ -118,3 +118,39 @@ def test_sharded_uneven_shards(oracle, world):
     for r in range(world):
         t = tables[r].engine.table
         assert (t.identities_all() == ident[t.row_lo:t.row_hi]).all()
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_sharded_random_configurations(oracle, seed):
+    """Randomised row-sharded runs: S logical shards (uneven capacities) over G ranks, all
+    policies, features on some batches; every rank's slice and the evicted list against the
+    oracle, and each rank's held rows against the oracle state."""
+    rng = np.random.default_rng(500 + seed)
+    S = int(rng.choice([2, 4, 8]))
+    world = int(rng.choice([w for w in (2, 4, 8) if w <= S]))
+    caps = [int(c) for c in rng.integers(300, 5000, S)]
+    P = int(min(min(caps), rng.choice([4, 16, 64])))
+    mode = int(rng.integers(0, 3))
+    dim = 4 if mode == 1 else 0
+    cfg = mz.TableConfig(caps, P, 11, dim, 3)
+    pol = (mz.EvictionPolicy.ttl(mz.TtlPolicy(35)) if mode == 1 else
+           mz.EvictionPolicy.lru() if mode == 2 else mz.EvictionPolicy.disabled())
+    uni = oracle.distinct_ids(60 + seed, 0, int(sum(caps) * 1.1))
+    batches = []
+    for b in range(5):
+        n = int(rng.choice([3000, 20000]))
+        f = rng.integers(0, 3, n).astype(np.uint32) if b % 2 else None
+        batches.append((uni[rng.integers(0, uni.size, n)], f, 1 + 15 * b))
+    out, tables = run_sharded(cfg, world, batches, pol)
+    o = oracle.OracleTable(caps, P, 11, dim, 3)
+    for b, (ids, f, now) in enumerate(batches):
+        os_, oo, oe = o.process_batch(ids, now, mode, 35 if mode == 1 else 0, {}, f)
+        gs = np.concatenate([out[r][b][0] for r in range(world)])
+        go = np.concatenate([out[r][b][1] for r in range(world)])
+        assert (gs == os_).all() and (go == oo).all(), f"batch {b} S={S} G={world} mode={mode}"
+        for r in range(world):
+            assert (out[r][b][2] == oe).all()
+    ident = o.identities_all()
+    for r in range(world):
+        t = tables[r].engine.table
+        assert (t.identities_all() == ident[t.row_lo:t.row_hi]).all()
