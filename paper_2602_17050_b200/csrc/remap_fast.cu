@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(256) k_validate(TableDev t, const uint64_t* __
 
 // K1: probe; each thread keeps U positions in flight (independent sector loads), all
 // positions of a round are issued before any is scanned.
-template <int MODE, int U, int MINB>
+template <int MODE, int U, int MINB, bool PF = false>
 __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t* __restrict__ ids,
                                                uint64_t n, uint64_t now, uint64_t meta_value,
                                                BatchCounters* ctr,
@@ -290,7 +290,8 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
                     out_oc[i] = foc;
                     // Found refresh / Collision at home (LRU: deferred to k_lru_meta, the
                     // batch may still turn out to need an eviction)
-                    if (MODE != kModeLru) t.meta[fslot] = meta_value;
+                    // (per-feature TTL: the last-writer pass after K5 writes it)
+                    if (MODE != kModeLru && !PF) t.meta[fslot] = meta_value;
                     if (foc == kFound) ++my_found; else ++my_coll;
                 }
             }
@@ -330,7 +331,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
 // instruction (lane j: sector j) -- the same cost per access as a single sector on B200
 // (line_scan.cuh) -- and finds the first match / EMPTY of the window part in that line with
 // one 16-bit mask.  Decisions, writes and the new-list append are made by lane 0 of the quad.
-template <int MODE, int U, int MINB>
+template <int MODE, int U, int MINB, bool PF = false>
 __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint64_t* __restrict__ ids,
                                                           uint64_t n, uint64_t now, uint64_t meta_value,
                                                           BatchCounters* ctr,
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
                 if (fslot != kEmpty && j == 0) {
                     out_slots[i] = fslot;
                     out_oc[i] = foc;
-                    if (MODE != kModeLru) t.meta[fslot] = meta_value;  // (LRU: k_lru_meta)
+                    if (MODE != kModeLru && !PF) t.meta[fslot] = meta_value;  // (LRU: k_lru_meta)
                     if (foc == kFound) ++my_found; else ++my_coll;
                 }
             }
@@ -699,7 +700,7 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
 // K4: commit claims: claim word -> id, outcome, the entry's metadata word (one value per
 // batch, so duplicates / (id, f') secondaries of the entry need no write of their own),
 // touch_row, reset list and rank-indexed evicted flags.
-template <int MODE>
+template <int MODE, bool PF = false>
 __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
                                                 const uint32_t* __restrict__ newpos,
                                                 const uint64_t* __restrict__ newid,
@@ -747,7 +748,7 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
             continue;
         }
         if (oc != kCollision) t.ident[g] = id;
-        t.meta[g] = meta_value;
+        if (!PF) t.meta[g] = meta_value;  // per-feature TTL: the last-writer pass
         if (oc == kInserted || oc == kEvicted) t.row_gen[g] = gen_clock;
         {   // reset list: one warp-aggregated append (a per-row atomic on one counter word
             // serialises at the L2 -- C4 evicts ~0.8 M rows per 1 M-position batch); the
@@ -785,6 +786,94 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
         if (c[2]) atomicAdd(&ctr->evicted, c[2]);
         if (c[3]) atomicAdd(&ctr->collision, c[3]);
         if (np) atomicAdd(&ctr->entry_count, np);
+    }
+}
+
+// ---- per-feature TTL on the fast path.  With differing per-feature TTLs the uniques of one
+// batch write different metadata values, so a slot's final word is the value of the LAST
+// unique writing it in the reference's order (batch_engine.cpp:160-221: uniques in first-
+// occurrence order), i.e. of the (id, feature) unique with the largest first position among
+// those whose result slot it is.  Every decision is the same as with one value per batch (each
+// value is now + ttl > now: expiry does not change inside the batch), so K1..K5 run unchanged
+// with their metadata writes held back, then:
+//   M1 k_pf_group  every position -> its (id, feature) group, first position by atomicMax of
+//                  epoch << 32 | ~position (the dedup trick);
+//   M2 k_pf_slot   every group's first position -> its result slot's record, the largest first
+//                  position by atomicMax of epoch << 32 | position;
+//   M3 k_pf_write  the winning group writes now + ttl(feature) (eviction.cpp:20-30).
+struct __align__(32) PfEntry {
+    u128 key;                 // (id | feature << 64 | epoch << 96) or (slot | epoch << 96)
+    unsigned long long rank;  // epoch << 32 | ~first position (groups) / | position (slots)
+    unsigned long long pad;
+};
+
+__device__ __forceinline__ uint64_t pf_ttl(uint32_t f, uint64_t def, const uint32_t* keys,
+                                           const uint64_t* vals, uint32_t nk) {
+    for (uint32_t i = 0; i < nk; ++i)
+        if (keys[i] == f) return vals[i];
+    return def;
+}
+
+// insert-or-find an epoch-tagged 128-bit key (epoch in the top 32 bits); returns the record
+__device__ __forceinline__ uint32_t pf_find(PfEntry* tab, uint64_t mask, u128 mine, uint64_t h) {
+    const uint32_t ep = (uint32_t)(mine >> 96);
+    for (;;) {
+        u128 cur = atomicCAS(&tab[h].key, (u128)0, (u128)0);
+        if ((uint32_t)(cur >> 96) != ep) {
+            const u128 old = atomicCAS(&tab[h].key, cur, mine);
+            if (old == cur) return (uint32_t)h;
+            cur = old;
+            if ((uint32_t)(cur >> 96) != ep) continue;
+        }
+        if (cur == mine) return (uint32_t)h;
+        h = (h + 1) & mask;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_pf_group(const BatchCounters* ctr, const uint64_t* __restrict__ ids,
+                                                  const uint32_t* __restrict__ feats, uint64_t n, uint32_t ep,
+                                                  PfEntry* tab, uint64_t mask, uint32_t* __restrict__ ent) {
+    pdl_wait();
+    if (batch_failed(&ctr->err)) return;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t id = ids[i];
+        const uint32_t f = feats[i];
+        const u128 mine = (u128)id | ((u128)f << 64) | ((u128)ep << 96);
+        const uint32_t e = pf_find(tab, mask, mine, mix64(id ^ ((uint64_t)f * 0x9E3779B97F4A7C15ull), 0x51ED27ull) & mask);
+        atomicMax(&tab[e].rank, ((unsigned long long)ep << 32) | (uint32_t)~(uint32_t)i);
+        ent[i] = e;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_pf_slot(const BatchCounters* ctr, uint64_t n, uint32_t ep,
+                                                 const PfEntry* gtab, const uint32_t* __restrict__ gent,
+                                                 const uint64_t* __restrict__ out_slots, PfEntry* stab,
+                                                 uint64_t mask, uint32_t* __restrict__ sent) {
+    pdl_wait();
+    if (batch_failed(&ctr->err)) return;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (~(uint32_t)__ldcg(&gtab[gent[i]].rank) != (uint32_t)i) continue;  // not its group's first
+        const uint64_t g = out_slots[i];
+        const u128 mine = (u128)g | ((u128)ep << 96);
+        const uint32_t e = pf_find(stab, mask, mine, mix64(g, 0x5107ull) & mask);
+        atomicMax(&stab[e].rank, ((unsigned long long)ep << 32) | (uint32_t)i);
+        sent[i] = e;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_pf_write(TableDev t, const BatchCounters* ctr,
+                                                  const uint32_t* __restrict__ feats, uint64_t n,
+                                                  const PfEntry* gtab, const uint32_t* __restrict__ gent,
+                                                  const PfEntry* stab, const uint32_t* __restrict__ sent,
+                                                  const uint64_t* __restrict__ out_slots, uint64_t now,
+                                                  uint64_t def_ttl, const uint32_t* keys, const uint64_t* vals,
+                                                  uint32_t nk) {
+    pdl_wait();
+    if (batch_failed(&ctr->err)) return;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (~(uint32_t)__ldcg(&gtab[gent[i]].rank) != (uint32_t)i) continue;
+        if ((uint32_t)__ldcg(&stab[sent[i]].rank) != (uint32_t)i) continue;  // a later group wrote last
+        t.meta[out_slots[i]] = now + pf_ttl(feats[i], def_ttl, keys, vals, nk);
     }
 }
 
@@ -905,7 +994,8 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     if (line) {
         constexpr int kUL = 2;
         const unsigned gl = grid_for(4 * ((n + kUL - 1) / kUL), B, 148u * 16u);
-        if (ttl) launch_pdl(k_probe_line<kModeTtl, kUL, 3>, gl, B, st, MPZCH_PROBE_ARGS);
+        if (ttl && a.per_feature) launch_pdl(k_probe_line<kModeTtl, kUL, 3, true>, gl, B, st, MPZCH_PROBE_ARGS);
+        else if (ttl) launch_pdl(k_probe_line<kModeTtl, kUL, 3>, gl, B, st, MPZCH_PROBE_ARGS);
         else if (lru) launch_pdl(k_probe_line<kModeLru, kUL, 4>, gl, B, st, MPZCH_PROBE_ARGS);
         // long windows: one position per quad at 8 blocks/SM (C3 insert-heavy 1.88 -> 2.07 G/s);
         // small batches keep 2 per quad (C1 1.10 vs 1.04 G/s pipelined)
@@ -916,7 +1006,9 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
         // TTL walks carry a metadata sector per round too: 2 positions per thread at 3 blocks/SM
         // (C2: 2.78 vs 2.40 G/s for 1 x 4; C4 1.04 vs 1.09)
         // (C2 swept: 1 or 4 positions per thread, 3-32 blocks/SM of grid: all slower)
-        if (ttl) launch_pdl(k_probe<kModeTtl, 2, 3>, grid_for((n + 1) / 2, B, 148u * 16u), B, st, MPZCH_PROBE_ARGS);
+        if (ttl && a.per_feature)
+            launch_pdl(k_probe<kModeTtl, 2, 3, true>, grid_for((n + 1) / 2, B, 148u * 16u), B, st, MPZCH_PROBE_ARGS);
+        else if (ttl) launch_pdl(k_probe<kModeTtl, 2, 3>, grid_for((n + 1) / 2, B, 148u * 16u), B, st, MPZCH_PROBE_ARGS);
         else if (lru) launch_pdl(k_probe<kModeLru, 1, 6>, gP, B, st, MPZCH_PROBE_ARGS);
         else launch_pdl(k_probe<kModeDisabled, 1, 6>, gP, B, st, MPZCH_PROBE_ARGS);
     }
@@ -933,7 +1025,14 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
                                      a.uniform_meta, t.s_reset.as<uint64_t>(),                     \
                                      t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>(),         \
                                      a.out_slots, a.out_oc)
-    if (ttl) { MPZCH_CLAIM_COMMIT(kModeTtl); }
+    if (ttl && a.per_feature) {
+        launch_pdl(k_claim<kModeTtl>, gW, B, st, t.dev, a.now, t.d_ctr, newpos, newent, te);
+        if (t.profiling) cudaEventRecord(t.ev[5], st);
+        launch_pdl(k_commit<kModeTtl, true>, gW, B, st, t.dev, t.d_ctr, newpos, newid, newent, te, t.gen_clock,
+                   a.uniform_meta, t.s_reset.as<uint64_t>(), t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>(),
+                   a.out_slots, a.out_oc);
+    }
+    else if (ttl) { MPZCH_CLAIM_COMMIT(kModeTtl); }
     else if (lru) {
         launch_pdl(k_claim<kModeLru>, gW, B, st, t.dev, a.now, t.d_ctr, newpos, newent, te);
         if (t.profiling) cudaEventRecord(t.ev[5], st);
@@ -954,6 +1053,25 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     if (lru) {
         launch_pdl(k_lru_meta, grid_for(n, B, 148u * 8u), B, st, t.dev, t.d_ctr, n, a.out_slots, a.uniform_meta);
         ++t.launches;
+    }
+    if (ttl && a.per_feature) {  // the metadata words, by last writer (M1..M3 above)
+        t.ensure_pf_scratch(n);
+        uint64_t cap = 1024;
+        while (cap < 2 * n) cap <<= 1;
+        const uint32_t ep = (uint32_t)t.epoch;
+        const unsigned gN = grid_for(n, B, 148u * 8u);
+        PfEntry* gtab = t.mf_tab.as<PfEntry>();
+        PfEntry* stab = t.sl_tab.as<PfEntry>();
+        launch_pdl(k_pf_group, gN, B, st, (const BatchCounters*)t.d_ctr, a.ids, a.feats, n, ep, gtab, cap - 1,
+                   t.mf_ent.as<uint32_t>());
+        launch_pdl(k_pf_slot, gN, B, st, (const BatchCounters*)t.d_ctr, n, ep, (const PfEntry*)gtab,
+                   (const uint32_t*)t.mf_ent.as<uint32_t>(), (const uint64_t*)a.out_slots, stab, cap - 1,
+                   t.sl_ent.as<uint32_t>());
+        launch_pdl(k_pf_write, gN, B, st, t.dev, (const BatchCounters*)t.d_ctr, a.feats, n, (const PfEntry*)gtab,
+                   (const uint32_t*)t.mf_ent.as<uint32_t>(), (const PfEntry*)stab,
+                   (const uint32_t*)t.sl_ent.as<uint32_t>(), (const uint64_t*)a.out_slots, a.now,
+                   a.pol->default_ttl, a.d_featk, a.d_featv, a.nk);
+        t.launches += 3;
     }
     if (t.dim > 0) launch_reset_rows(t, t.s_reset.as<uint64_t>(), &t.d_ctr->reset_count, st);
     if (a.out_mark) {  // first positions of Evicted uniques (row-sharded evicted list)

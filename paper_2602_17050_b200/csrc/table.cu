@@ -208,6 +208,20 @@ void Table::ensure_fast_scratch(uint64_t n) {
     }
 }
 
+void Table::ensure_pf_scratch(uint64_t n) {
+    mf_ent.reserve(n * 4);
+    sl_ent.reserve(n * 4);
+    const uint64_t want = pow2_at_least(2 * n);
+    if (want > mf_cap) {  // 32-byte epoch-keyed records; epoch 0 = empty (t.epoch starts at 1)
+        mf_tab.reserve(want * 32);
+        sl_tab.reserve(want * 32);
+        MPZCH_CUDA(cudaMemsetAsync(mf_tab.p, 0, mf_tab.bytes, stream));
+        MPZCH_CUDA(cudaMemsetAsync(sl_tab.p, 0, sl_tab.bytes, stream));
+        MPZCH_CUDA(cudaStreamSynchronize(stream));
+        mf_cap = want;
+    }
+}
+
 void Table::ensure_ordered_scratch(uint64_t n) {
     const uint64_t want = pow2_at_least(2 * n);
     if (want > ocap) {
@@ -464,7 +478,23 @@ uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uin
         a.d_featk = t.s_featk.as<uint32_t>();
         a.d_featv = t.s_featv.as<uint64_t>();
     }
-    bool fast = t.path_override == MPZCH_PATH_AUTO && t.hole_free && a.uniform && n <= (1ull << 29);
+    // per-feature TTL (differing values) takes the fast path too -- its metadata goes through the
+    // last-writer pass -- unless some TTL of the map could overflow at this `now` (the ordered
+    // path then reports exactly which position does, eviction.cpp:26-28); MPZCH_PF_FAST=0 keeps
+    // such batches on the rounds path
+    static const bool pf_env = [] {
+        const char* e = getenv("MPZCH_PF_FAST");
+        return !(e && std::string(e) == "0");
+    }();
+    a.nk = nk;
+    if (pol.mode == kModeTtl && !a.uniform && pf_env) {
+        bool ovf = pol.default_ttl > ~0ull - now;
+        for (uint64_t v : pol.ttls) ovf = ovf || v > ~0ull - now;
+        a.per_feature = !ovf;
+        a.uniform_meta = 0;
+    }
+    bool fast = t.path_override == MPZCH_PATH_AUTO && t.hole_free && (a.uniform || a.per_feature) &&
+                n <= (1ull << 29);
     const bool profiled = t.profiling;
     // LRU: after attempts that needed an eviction, skip the claim attempt for a growing number
     // of batches (1, 3, 7, 15 ... at most 15), so a stream whose windows are full pays for

@@ -177,11 +177,15 @@ public:
     uint64_t g_cap = 0;
     // publish / dirty rows (table.cu, publish.cu)
     DevBuf p_flags, p_rows, p_blk, p_ids, p_w, p_rec;
+    // per-feature TTL on the fast path: (id, feature) groups and per-slot last writers
+    DevBuf mf_tab, mf_ent, sl_tab, sl_ent;
+    uint64_t mf_cap = 0;
     // route (route.cu)
     DevBuf rt_s2p, rt_cnt, rt_tot;
     std::vector<uint8_t> rt_map;
 
     void ensure_fast_scratch(uint64_t n);
+    void ensure_pf_scratch(uint64_t n);  // per-feature TTL last-writer tables
     void ensure_ordered_scratch(uint64_t n);
 };
 
@@ -228,6 +232,9 @@ struct BatchArgs {
     uint64_t* out_ev;
     uint64_t ev_cap;
     uint8_t* out_mark = nullptr;  // optional: 1 at the first position of every Evicted unique
+    bool per_feature = false;     // TTL with differing per-feature values on the fast path:
+                                  // metadata written by the last-writer pass (remap_fast.cu)
+    uint32_t nk = 0;              // per-feature map size
 };
 
 // enqueue the whole batch; counters land in t.h_ctr after the stream syncs
