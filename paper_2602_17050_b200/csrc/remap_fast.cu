@@ -47,6 +47,8 @@ constexpr uint64_t kClaimBit = 1ull << 63;
 constexpr uint64_t kFlagEmpty = 1ull << 30;  // the claimed slot was EMPTY before the batch
 constexpr uint64_t kEntryMask = (1ull << 30) - 1;
 constexpr uint8_t kStateCollided = 1;
+constexpr uint8_t kStateEvict = 2;     // LRU: the entry evicts the slot at offset `held` (K3b)
+constexpr uint8_t kPendingOc = 0xFF;   // LRU: out_oc of a position on the new list until K4/K5
 
 // Id table (one entry per distinct new id): an epoch-tagged 128-bit key (epoch << 64 | id)
 // -- any entry whose epoch is not the current batch's is empty, so no cleanup pass is
@@ -267,7 +269,9 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
                 if (MODE != kModeTtl) {
                     if (st[u] == kHit) fslot = g[u];
                     else if (st[u] == kEmptyHit) { is_new = true; a_off = off[u]; }
-                    else if (MODE == kModeLru) atomicExch(&ctr->lru_abort, 1u);  // would evict
+                    // LRU full window: an evictor -- its claim finds nothing (a = P) and K3b
+                    // picks the least recently used slot
+                    else if (MODE == kModeLru) { is_new = true; a_off = t.P; }
                     else { fslot = base[u] + h[u]; foc = kCollision; }
                 } else {  // TTL with one metadata value per batch (expiry read with the walk)
                     if (st[u] == kHit) {
@@ -293,6 +297,8 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
                     // (per-feature TTL: the last-writer pass after K5 writes it)
                     if (MODE != kModeLru && !PF) t.meta[fslot] = meta_value;
                     if (foc == kFound) ++my_found; else ++my_coll;
+                } else if (MODE == kModeLru) {
+                    out_oc[i] = kPendingOc;  // K3c tells Found positions apart by this byte
                 }
             }
             // warp-aggregated append of the new positions (a block barrier here would make
@@ -449,7 +455,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
                 if (MODE != kModeTtl) {
                     if (st[u] == kHit) fslot = g[u];
                     else if (st[u] == kEmptyHit) { is_new = true; a_off = off[u]; }
-                    else if (MODE == kModeLru) { if (j == 0) atomicExch(&ctr->lru_abort, 1u); }
+                    else if (MODE == kModeLru) { is_new = true; a_off = t.P; }  // evictor (K3b)
                     else { fslot = base + h; foc = kCollision; }
                 } else {  // TTL with one metadata value per batch (expiry read with the walk)
                     if (st[u] == kHit) {
@@ -472,6 +478,8 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
                     out_oc[i] = foc;
                     if (MODE != kModeLru && !PF) t.meta[fslot] = meta_value;  // (LRU: k_lru_meta)
                     if (foc == kFound) ++my_found; else ++my_coll;
+                } else if (MODE == kModeLru && st[u] != kIdle && j == 0) {
+                    out_oc[i] = kPendingOc;
                 }
             }
             is_new = is_new && j == 0;
@@ -586,9 +594,9 @@ template <int MODE>
 __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCounters* ctr,
                                                const uint32_t* __restrict__ newpos,
                                                const uint32_t* __restrict__ newent,
-                                               IdEntry* te) {
+                                               IdEntry* te, uint32_t* __restrict__ evl) {
     pdl_wait();
-    if (batch_failed(&ctr->err) || (MODE == kModeLru && ctr->lru_abort)) return;
+    if (batch_failed(&ctr->err)) return;
     const unsigned cnt = ctr->new_count;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
         uint32_t e = newent[k];
@@ -672,9 +680,9 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                 }
                 if (!held) {
                     te[e].state = kStateCollided;
-                    // LRU: a full window evicts its least recently used slot -- order-dependent
-                    // on in-batch refreshes, so the batch goes to the rounds path instead
-                    if (MODE == kModeLru) atomicExch(&ctr->lru_abort, 1u);
+                    // LRU: a full window evicts its least recently used slot: K3b picks it
+                    // (a collided entry holds nothing, so it is never taken over again)
+                    if (MODE == kModeLru) evl[atomicAdd(&ctr->lru_evict, 1u)] = e;
                 }
             }
             if (next == kNone32) break;
@@ -737,6 +745,9 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
             ((v = t.ident[base + wrap_add(h, ev.m, cap)]) & ~kFlagEmpty) == mine) {
             g = base + wrap_add(h, ev.m, cap);  // the owner kept (refreshed) its own slot
             oc = kFound;
+        } else if (MODE == kModeLru && ev.state == kStateEvict) {
+            g = base + wrap_add(h, ev.held, cap);  // K3b's victim (still its pre-batch id)
+            oc = kEvicted;
         } else if (ev.state != kStateCollided) {
             g = base + wrap_add(h, ev.held, cap);
             v = t.ident[g];
@@ -877,6 +888,91 @@ __global__ void __launch_bounds__(256) k_pf_write(TableDev t, const BatchCounter
     }
 }
 
+// ---- LRU evictions on the claim path.  A new id whose window is full evicts the window's least
+// recently used slot: the first slot of smallest metadata (strict <, probe_core.cpp:97-101 and
+// 125-129) in the table as the sequential reference has it at that id's turn.  At that turn
+// every slot touched earlier in the batch (Found refresh, insert, eviction) holds metadata
+// `now`; every other slot its pre-batch value.  K3b decides every evictor in parallel on K3's end
+// state with claimed slots counted as `now`; its pick v is the reference's whenever
+//   * v holds a pre-batch id whose metadata is older than `now` -- then no slot touched before
+//     the evictor's turn (metadata `now`) can beat or tie it, and a slot touched only after it
+//     still had its pre-batch value, which K3b compared;
+//   * no other evictor picked v -- an earlier eviction elsewhere in the window only raises
+//     that slot to `now` (the first point again);
+//   * no position of the batch Found v's id (K3c) -- else the eviction would change what a
+//     later position finds, or the victim was refreshed before the evictor's turn.
+// Any other case sets lru_abort: the claims revert and the batch takes the rounds path.
+__global__ void __launch_bounds__(256) k_lru_victim(TableDev t, uint64_t now, BatchCounters* ctr,
+                                                    const uint32_t* __restrict__ evl, IdEntry* te,
+                                                    PfEntry* vtab, uint64_t cap_alloc, uint32_t ep) {
+    pdl_wait();
+    if (batch_failed(&ctr->err)) return;
+    const unsigned cnt = ctr->lru_evict;
+    if (cnt == 0) return;
+    const uint64_t mask = table_mask(cnt, cap_alloc);
+    const unsigned lane = lane_id();
+    const unsigned warps = gridDim.x * (blockDim.x >> 5);
+    for (unsigned k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < cnt; k += warps) {
+        const uint32_t e = evl[k];
+        const uint64_t id = key_id(te[e].key);
+        const ShardDev sd = t.shards[shard_of(id, t)];
+        const uint64_t cap = sd.cap.d, base = sd.offset, h = home_of(id, sd, t.seed);
+        // lane j scans offsets j, j + 32, ...: first smallest per lane, then across the warp
+        uint64_t best = ~0ull;
+        uint32_t boff = kNone32;
+        for (uint32_t off = lane; off < t.P; off += 32) {
+            const uint64_t g = base + wrap_add(h, off, cap);
+            const uint64_t v = t.ident[g];
+            const uint64_t m = (v >> 63) ? now : t.meta[g];  // claimed in this batch: `now`
+            if (m < best) { best = m; boff = off; }
+        }
+        uint64_t wb = best;
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t x = __shfl_xor_sync(0xffffffffu, wb, o);
+            wb = x < wb ? x : wb;
+        }
+        uint32_t wo = best == wb ? boff : kNone32;
+        for (int o = 16; o; o >>= 1) wo = min(wo, __shfl_xor_sync(0xffffffffu, wo, o));
+        if (lane == 0) {
+            bool ok = wb < now && wo != kNone32;  // < now: a pre-batch id, untouched by claims
+            if (ok) {
+                const uint64_t g = base + wrap_add(h, wo, cap);
+                const uint32_t r = pf_find(vtab, mask, (u128)g | ((u128)ep << 96), mix64(g, 0x5107ull) & mask);
+                const unsigned long long tag = ((unsigned long long)ep << 32) | 1ull;
+                ok = atomicExch(&vtab[r].rank, tag) != tag;  // else two evictors picked one slot
+            }
+            if (ok) {
+                te[e].held = wo;
+                te[e].state = kStateEvict;
+            } else {
+                atomicExch(&ctr->lru_abort, 1u);
+            }
+        }
+    }
+}
+
+// K3c (LRU, evictors only): a victim whose id some position Found aborts the attempt.
+__global__ void __launch_bounds__(256) k_lru_touch(BatchCounters* ctr, uint64_t n,
+                                                   const uint64_t* __restrict__ out_slots,
+                                                   const uint8_t* __restrict__ out_oc,
+                                                   const PfEntry* vtab, uint64_t cap_alloc, uint32_t ep) {
+    pdl_wait();
+    if (batch_failed(&ctr->err) || ctr->lru_evict == 0 || ctr->lru_abort) return;
+    const uint64_t mask = table_mask(ctr->lru_evict, cap_alloc);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (out_oc[i] != kFound) continue;
+        const uint64_t g = out_slots[i];
+        for (uint64_t h = mix64(g, 0x5107ull) & mask;; h = (h + 1) & mask) {
+            const u128 key = ld_cg_u128(&vtab[h].key);
+            if ((uint32_t)(key >> 96) != ep) break;  // not a victim
+            if ((uint64_t)key == g) {
+                atomicExch(&ctr->lru_abort, 1u);
+                break;
+            }
+        }
+    }
+}
+
 // LRU attempt aborted after K3: put every claimed slot back to EMPTY (only EMPTY slots are
 // claimable outside TTL, and every claimed slot ends held by exactly one entry -- the one
 // whose last claim offset points at it), so the rounds path starts from the pre-batch state.
@@ -962,6 +1058,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
                            // thread: C5 probe 0.46 -> 0.39 ms going from 2 x 4 blocks/SM to 1 x 6)
     const uint64_t n = a.n;
     t.ensure_fast_scratch(n);
+    if (a.pol->mode == kModeLru) t.ensure_pf_scratch(n);  // the victim set (K3b/K3c)
     const uint64_t epoch = ++t.epoch;
     const unsigned B = 256;
     const unsigned gW = grid_for(n, B, 148u * 8u);  // count-driven kernels (4/16/32 x 148: same)
@@ -1019,14 +1116,14 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     launch_pdl(k_dedup, gW, B, st, t.d_ctr, t.tcap, epoch, newpos, newid, newa, newm, newent, te);
     if (t.profiling) cudaEventRecord(t.ev[4], st);
 #define MPZCH_CLAIM_COMMIT(MODE)                                                                   \
-    launch_pdl(k_claim<MODE>, gW, B, st, t.dev, a.now, t.d_ctr, newpos, newent, te);              \
+    launch_pdl(k_claim<MODE>, gW, B, st, t.dev, a.now, t.d_ctr, newpos, newent, te, nullptr);     \
     if (t.profiling) cudaEventRecord(t.ev[5], st);                                               \
     launch_pdl(k_commit<MODE>, gW, B, st, t.dev, t.d_ctr, newpos, newid, newent, te, t.gen_clock, \
                                      a.uniform_meta, t.s_reset.as<uint64_t>(),                     \
                                      t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>(),         \
                                      a.out_slots, a.out_oc)
     if (ttl && a.per_feature) {
-        launch_pdl(k_claim<kModeTtl>, gW, B, st, t.dev, a.now, t.d_ctr, newpos, newent, te);
+        launch_pdl(k_claim<kModeTtl>, gW, B, st, t.dev, a.now, t.d_ctr, newpos, newent, te, nullptr);
         if (t.profiling) cudaEventRecord(t.ev[5], st);
         launch_pdl(k_commit<kModeTtl, true>, gW, B, st, t.dev, t.d_ctr, newpos, newid, newent, te, t.gen_clock,
                    a.uniform_meta, t.s_reset.as<uint64_t>(), t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>(),
@@ -1034,14 +1131,21 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     }
     else if (ttl) { MPZCH_CLAIM_COMMIT(kModeTtl); }
     else if (lru) {
-        launch_pdl(k_claim<kModeLru>, gW, B, st, t.dev, a.now, t.d_ctr, newpos, newent, te);
+        // evictors listed in newa's storage (dead after K2)
+        launch_pdl(k_claim<kModeLru>, gW, B, st, t.dev, a.now, t.d_ctr, newpos, newent, te, newa);
         if (t.profiling) cudaEventRecord(t.ev[5], st);
+        PfEntry* vtab = t.sl_tab.as<PfEntry>();
+        const uint32_t ep = (uint32_t)epoch;
+        launch_pdl(k_lru_victim, 148u * 4u, B, st, t.dev, a.now, t.d_ctr, (const uint32_t*)newa, te, vtab,
+                   t.mf_cap, ep);
+        launch_pdl(k_lru_touch, grid_for(n, B, 148u * 8u), B, st, t.d_ctr, n, (const uint64_t*)a.out_slots,
+                   (const uint8_t*)a.out_oc, (const PfEntry*)vtab, t.mf_cap, ep);
         launch_pdl(k_lru_revert, gW, B, st, t.dev, t.d_ctr, newpos, newent, te);
         launch_pdl(k_commit<kModeLru>, gW, B, st, t.dev, t.d_ctr, newpos, newid, newent, te, t.gen_clock,
                                              a.uniform_meta, t.s_reset.as<uint64_t>(),
                                              t.s_evflag.as<uint8_t>(), t.s_evslot.as<uint64_t>(),
                                              a.out_slots, a.out_oc);
-        t.launches += 1;
+        t.launches += 3;
     }
     else { MPZCH_CLAIM_COMMIT(kModeDisabled); }
 #undef MPZCH_CLAIM_COMMIT
@@ -1075,10 +1179,10 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     }
     if (t.dim > 0) launch_reset_rows(t, t.s_reset.as<uint64_t>(), &t.d_ctr->reset_count, st);
     if (a.out_mark) {  // first positions of Evicted uniques (row-sharded evicted list)
-        if (ttl) MPZCH_CUDA(cudaMemcpyAsync(a.out_mark, t.s_evflag.p, n, cudaMemcpyDeviceToDevice, st));
+        if (ttl || lru) MPZCH_CUDA(cudaMemcpyAsync(a.out_mark, t.s_evflag.p, n, cudaMemcpyDeviceToDevice, st));
         else MPZCH_CUDA(cudaMemsetAsync(a.out_mark, 0, n, st));
     }
-    if (ttl) enqueue_compact_evicted(t, n, a.out_ev, a.ev_cap, st);
+    if (ttl || lru) enqueue_compact_evicted(t, n, a.out_ev, a.ev_cap, st);
     if (t.profiling) cudaEventRecord(t.ev[3], st);
 }
 

@@ -53,8 +53,9 @@ struct BatchCounters {
     unsigned int overflow_list;  // claim-log overflow (defensive)
     unsigned int pad;
     unsigned int dup_items;      // fast path: new-list items whose id was already in the id table
-    unsigned int lru_abort;      // LRU on the fast path: an eviction is needed -> rounds path
-    unsigned int pad3;
+    unsigned int lru_abort;      // LRU on the fast path: an eviction the claim path cannot place
+                                 // exactly -> the batch reverts and takes the rounds path
+    unsigned int lru_evict;      // LRU on the fast path: entries whose window is full (evictors)
     unsigned long long bad_id;   // lookups: the id at err.bad_pos (the exception text needs it)
     unsigned long long id_sectors, meta_sectors;  // sectors the probe kernel read
     // rounds path (device-driven): pending count per round parity, new suspects per closure

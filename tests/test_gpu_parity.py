@@ -553,8 +553,9 @@ def test_delta_cut_matches_dirty_rows(oracle):
 @pytest.mark.parametrize("shards", [1, 8])
 def test_lru_and_feature_ttl_streams_all_paths(oracle, path, shards):
     """LRU (full windows, double evictions) and per-feature TTL batches at a dense load: auto
-    (LRU: the rounds path once windows fill; per-feature TTL: the claim path with the
-    last-writer metadata pass), the ordered path and forced rounds agree with the oracle."""
+    (LRU: the claim path with K3b evictions, or the rounds path when an eviction cannot be
+    placed there; per-feature TTL: the claim path with the last-writer metadata pass), the
+    ordered path and forced rounds agree with the oracle."""
     rows = 1 << 13
     caps = mz.even_capacities(rows, shards)
     uni = oracle.distinct_ids(21, 0, int(rows * 1.3))
@@ -567,16 +568,16 @@ def test_lru_and_feature_ttl_streams_all_paths(oracle, path, shards):
             batches.append((uni[rng.integers(0, uni.size, n)], f, 100 + 9 * b))
         t = run_stream(oracle, caps, 16, 5, 4, 3, batches, mode, dttl, pf, path, check_state_every=4)
         if path == "auto":
-            assert t.last_stats()["path"] == ("rounds" if mode == 2 else "fast")
+            assert t.last_stats()["path"] in (("fast", "rounds") if mode == 2 else ("fast",))
 
 
 @pytest.mark.parametrize("line", [False, True])
 def test_lru_claim_path_and_fallback(oracle, line):
-    """LRU batches go to the claim path while no new id meets a full window (metadata writes
-    held back, then applied); a batch that needs an eviction -- found by the probe (pre-batch
-    full window) or by the claims (window filled by lower ranks in the batch) -- reverts its
-    claims on the device and runs the rounds path.  Both kinds of batch, with features, against
-    the oracle, state compared after every batch."""
+    """LRU batches go to the claim path (metadata writes held back, then applied); a new id
+    whose window is full -- before the batch (probe) or filled by lower ranks (claims) -- evicts
+    there too when K3b can place the eviction exactly, else the batch reverts its claims on the
+    device and runs the rounds path.  With features, against the oracle, state compared after
+    every batch."""
     rows = 1 << 12
     caps = mz.even_capacities(rows, 4)
     uni = oracle.distinct_ids(31, 0, int(rows * 1.25))
@@ -597,8 +598,74 @@ def test_lru_claim_path_and_fallback(oracle, line):
         os_, oo, oe = o.process_batch(ids, now, 2, 0, None, f)
         assert (gs == os_).all() and (go == oo).all() and (ge == oe).all(), f"batch {bi}"
         assert_same_state(gpu_state(t, 4), oracle_state(o, 4), f"batch {bi}")
-        paths.append(t.last_stats()["path"])
-    assert "fast" in paths and "rounds" in paths, paths
+        st = t.last_stats()
+        paths.append((st["path"], st["evicted"] > 0))
+    assert ("fast", False) in paths and any(e for _, e in paths), paths
+    if not line:  # max_probe 8: evicting batches on the claim path
+        assert ("fast", True) in paths, paths
+
+
+def _lru_case(oracle, caps, P, batches, want_paths):
+    t = mz.MpzchTable(mz.TableConfig(caps, P, 5, 4, 9))
+    o = oracle.OracleTable(caps, P, 5, 4, 9)
+    p = mz.EvictionPolicy.lru()
+    got = []
+    for bi, (ids, now) in enumerate(batches):
+        ids = np.asarray(ids, dtype=np.uint64)
+        gs, go, ge = t.process_batch(ids, now, p)
+        os_, oo, oe = o.process_batch(ids, now, 2, 0, None, None)
+        assert (gs == os_).all() and (go == oo).all() and (ge == oe).all(), f"batch {bi}"
+        assert_same_state(gpu_state(t, 4), oracle_state(o, 4), f"batch {bi}")
+        got.append(t.last_stats()["path"])
+    assert got[-1] == want_paths, got
+
+
+@pytest.mark.parametrize("case", ["untouched", "found_before", "found_after", "same_victim",
+                                  "tied_now", "repeated_evictor"])
+def test_lru_eviction_cases(oracle, case):
+    """The K3b exactness conditions one by one, on a single 8-slot shard with max_probe 8 (every
+    window is the whole shard): one evictor on an untouched victim stays on the claim path; a
+    victim whose id the batch also Finds (before or after the evictor), two evictors on one
+    victim, and metadata tied with `now` revert to the rounds path.  Results, evicted lists,
+    metadata and reset rows equal the oracle's in every case."""
+    ids = [1000 + 17 * k for k in range(8)]
+    fill = [([x], 1 + k) for k, x in enumerate(ids)]  # metadata 1..8: ids[0] is the LRU slot
+    new1, new2 = 5_000_001, 5_000_003
+    last = {
+        "untouched": ([ids[3], new1, ids[5]], 20, "fast"),
+        "found_before": ([ids[0], new1], 20, "rounds"),
+        "found_after": ([new1, ids[0]], 20, "rounds"),
+        "same_victim": ([new1, new2], 20, "rounds"),
+        "tied_now": ([new1], 5, "rounds"),
+        "repeated_evictor": ([new1, ids[2], new1, ids[6]], 21, "fast"),
+    }[case]
+    if case == "tied_now":
+        fill = [(ids, 5)]  # every slot's metadata equals the evicting batch's `now`
+    _lru_case(oracle, [8], 8, fill + [(last[0], last[1])], last[2])
+
+
+def test_lru_evictions_sector_probe(oracle):
+    """Batches above 256K positions (per-thread sector probe) over a pool 1.25x the table under
+    LRU: evictions on the claim path and, where K3b cannot place one, the rounds path; results
+    and state against the oracle after every batch."""
+    rows = 1 << 17
+    caps = mz.even_capacities(rows, 4)
+    uni = oracle.distinct_ids(61, 0, int(rows * 1.25))
+    rng = np.random.default_rng(9)
+    t = mz.MpzchTable(mz.TableConfig(caps, 16, 7, 0, 3))
+    o = oracle.OracleTable(caps, 16, 7, 0, 3)
+    p = mz.EvictionPolicy.lru()
+    seen = set()
+    for b in range(5):
+        ids = uni[rng.integers(0, uni.size, 300_000)]
+        now = 100 + 20 * b
+        gs, go, ge = t.process_batch(ids, now, p)
+        os_, oo, oe = o.process_batch(ids, now, 2, 0, None, None)
+        assert (gs == os_).all() and (go == oo).all() and (ge == oe).all(), f"batch {b}"
+        st = t.last_stats()
+        seen.add((st["path"], st["evicted"] > 0))
+        assert_same_state(gpu_state(t, 0), oracle_state(o, 0), f"batch {b}")
+    assert any(e for _, e in seen), seen
 
 
 @pytest.mark.parametrize("mode", [0, 1, 2])

@@ -75,6 +75,7 @@ def run_batches(t, batches, nows, pol, stream, timed_from=0, feats=None, split=T
     return dict(ids_per_s=pos / (ms / 1e3), ms_per_batch=ms / max(len(batches) - mid, 1),
                 positions=sum(b.numel() for b in batches[timed_from:]),
                 outcomes=agg, path=stats[-1]["path"] if stats else None,
+                paths={p: sum(s["path"] == p for s in stats) for p in sorted({s["path"] for s in stats})},
                 probe_ms=prof["probe_ms"] / nb, claim_ms=prof["claim_ms"] / nb,
                 tail_ms=prof["tail_ms"] / nb,
                 probe_gbs=(prof["probe_bytes"] / nb) / (prof["probe_ms"] / nb / 1e3) / 1e9 if prof["probe_ms"] else None,
@@ -316,6 +317,34 @@ def lru(pool_factor=1.2):
 
 def lru08():
     return lru(0.8)
+
+
+def lru_zipf():
+    """Not a BASELINE config: LRU under C2's Zipf(1.05) traffic over 2^27 ids on a 2^22-row table
+    (8 shards, P=128, 1M-position batches): windows are full, so every batch evicts; the victims
+    are cold tail ids, which the claim path places (K3b).  Beside it the same stream forced onto
+    the rounds path."""
+    rows, universe, B = 1 << 22, 1 << 27, 1 << 20
+    w = torch.arange(1, universe + 1, dtype=torch.float64, device="cuda").pow_(-1.05)
+    zipf_ranks.cdf = torch.cumsum(w, 0) / w.sum()
+    del w
+    st = torch.cuda.current_stream()
+    caps = mz.even_capacities(rows, 8)
+    pol = mz.EvictionPolicy.lru()
+    warm, timed = 48, 16
+    batches = [bench.distinct_ids_t(2, zipf_ranks(B, 1.05, universe, 3000 + b)).contiguous()
+               for b in range(warm + timed)]
+    nows = [10**6 + 60 * b for b in range(warm + timed)]
+    out = dict(config="LRU Zipf(1.05), 2^22 rows, 1M batches")
+    for path in ("auto", "rounds"):
+        t = mz.MpzchTable(mz.TableConfig(caps, 128, 7))
+        t.set_path(path)
+        run_batches(t, batches[:warm], nows[:warm], pol, st, split=False)
+        r = run_batches(t, batches[warm:], nows[warm:], pol, st, split=False)
+        out[path] = r
+    bn = [b.cpu().numpy().view(np.uint64) for b in batches]
+    out["reference"] = ref_time(caps, 128, bn, nows, 2, 0, warm=warm)
+    return out
 
 
 def serve():
