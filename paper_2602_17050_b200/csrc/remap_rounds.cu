@@ -10,12 +10,17 @@
 //                   its rank: ident-changing writes (Inserted/Evicted) in mark_id, metadata-only
 //                   writes (Found refresh, Collision's home touch) in mark_any (64-bit atomicMin
 //                   of epoch-keyed words, so marks never need clearing).
-//   R2 k_check      k is SUSPECT if a lower rank left a mark_id mark anywhere in R_k, or any
-//                   lower-rank mark on w_k, or (LRU full window: the victim depends on every
-//                   metadata word of R_k) any lower-rank mark in R_k.  A metadata-only write at
-//                   x != w_k changes no other decision: Found and Inserted-at-EMPTY read no
-//                   metadata, and under TTL a refresh (now + ttl >= now) only un-expires x, which
-//                   matters only if x was k's victim, i.e. x == w_k.
+//   R2 k_check      k is SUSPECT if a lower rank left a mark (either array) on w_k, or -- LRU
+//                   victim whose metadata is not older than `now` -- any lower-rank mark in R_k.
+//                   A lower-rank write at x != w_k changes no decision of k against C:
+//                   * a unique with k's own id decides exactly as k does against the same C, so
+//                     it writes w_k (or, as a suspect, marks a window holding w_k);
+//                   * any other id written at x is not k's, so k's discovery pass is unchanged,
+//                     and no write empties a slot;
+//                   * Found and Inserted-at-EMPTY read no metadata; under TTL a write only makes
+//                     x live (refresh, or an expired x replaced -- then x lies past k's first
+//                     expired slot w_k, or k found its id first); an LRU victim with metadata
+//                     older than `now` is not beaten or tied by x raised to `now`.
 //   R3 mark_window  a suspect may end up writing anywhere in its window: a new suspect marks its
 //                   whole window in mark_id at once (so cascades spread inside a pass) and R2
 //                   repeats until a pass finds no new suspect (the fixpoint).  After kClosureMax
@@ -166,7 +171,11 @@ __device__ __forceinline__ void tentative(const RoundsArgs& r, uint32_t k, uint3
     else if (MODE == kModeLru && have_best) { oc = kEvicted; ws = best_g; }
     __stcg(r.td_slot + k, ws);
     stcg_u8(r.td_oc + k, oc);
-    __stcg(r.td_d + k, kind ? off : t.P - 1);  // read range [h, h + d]
+    // read range [h, h + d]; bit 31: the decision reads every metadata word of the range (an
+    // LRU victim whose metadata is not older than `now` -- slots raised to `now` by lower ranks
+    // would tie it)
+    const bool wide = MODE == kModeLru && oc == kEvicted && best_m >= r.now;
+    __stcg(r.td_d + k, (kind ? off : t.P - 1) | (wide ? 1u << 31 : 0u));
     const bool ident_write = oc == kInserted || oc == kEvicted;
     atomicMin((ident_write ? r.mark_id : r.mark_any) + r.mi(ws), (unsigned long long)mark_key(epoch, k));
 }
@@ -175,12 +184,17 @@ __device__ __forceinline__ void tentative(const RoundsArgs& r, uint32_t k, uint3
 // 32-byte loads of one 128-byte block of the mark array per round trip).
 template <int MODE>
 __device__ __forceinline__ bool suspect(const RoundsArgs& r, uint32_t k, uint32_t epoch) {
+    const uint32_t dw = __ldcg(r.td_d + k);
+    const uint64_t w = __ldcg(r.td_slot + k);
+    if (!(dw >> 31)) {  // the write slot decides (header): one word in each mark array
+        const uint64_t i = r.mi(w);
+        return mark_rank(__ldcg(r.mark_id + i), epoch) < k || mark_rank(__ldcg(r.mark_any + i), epoch) < k;
+    }
     const uint64_t id = r.ids[r.upos[k]];
     const ShardDev sd = r.t.shards[r.ushard[k]];
     const uint64_t h = home_of(id, sd, r.t.seed);
-    const uint32_t d = __ldcg(r.td_d + k);
-    const uint64_t w = __ldcg(r.td_slot + k);
-    const bool meta_dep = MODE == kModeLru && ldcg_u8(r.td_oc + k) == kEvicted;  // full window
+    const uint32_t d = dw & 0x7fffffffu;
+    const bool meta_dep = true;  // LRU victim tied with `now`: any mark in the range
     const uint64_t end = sd.offset + sd.cap.d;
     uint64_t g = slot_of(sd, h, 0);
     uint32_t off = 0;
