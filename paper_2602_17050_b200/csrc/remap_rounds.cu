@@ -22,7 +22,8 @@
 //                     expired slot w_k, or k found its id first); an LRU victim with metadata
 //                     older than `now` is not beaten or tied by x raised to `now`.
 //   R3 mark_window  a suspect may end up writing anywhere in its window: a new suspect marks its
-//                   whole window in mark_id at once (so cascades spread inside a pass) and R2
+//                   whole window at once (so cascades spread inside a pass) in mark_win, one
+//                   word per 16-slot block (9 atomics for a 128-slot window, not 128), and R2
 //                   repeats until a pass finds no new suspect (the fixpoint).  After kClosureMax
 //                   passes the last pass's suspects are left unmarked; with m = the lowest of
 //                   their ranks, every non-suspect of rank < m is final (every suspect below it
@@ -99,7 +100,8 @@ struct RoundsArgs {
     uint8_t* susp;  // 0 clear, 1 suspect
     uint8_t* todo;
     unsigned long long* mark_any;  // metadata-only writes
-    unsigned long long* mark_id;   // ident-changing writes and suspect windows
+    unsigned long long* mark_id;   // ident-changing writes
+    unsigned long long* mark_win;  // suspect windows, one word per 16-slot block of mark_id
     uint64_t mark_base, mark_mask;
     uint64_t* uslot;
     uint8_t* uoc;
@@ -188,7 +190,8 @@ __device__ __forceinline__ bool suspect(const RoundsArgs& r, uint32_t k, uint32_
     const uint64_t w = __ldcg(r.td_slot + k);
     if (!(dw >> 31)) {  // the write slot decides (header): one word in each mark array
         const uint64_t i = r.mi(w);
-        return mark_rank(__ldcg(r.mark_id + i), epoch) < k || mark_rank(__ldcg(r.mark_any + i), epoch) < k;
+        return mark_rank(__ldcg(r.mark_id + i), epoch) < k || mark_rank(__ldcg(r.mark_any + i), epoch) < k ||
+               mark_rank(__ldcg(r.mark_win + (i >> 4)), epoch) < k;
     }
     const uint64_t id = r.ids[r.upos[k]];
     const ShardDev sd = r.t.shards[r.ushard[k]];
@@ -204,6 +207,7 @@ __device__ __forceinline__ bool suspect(const RoundsArgs& r, uint32_t k, uint32_
         uint64_t c = 16 - s0;
         if (end - g < c) c = end - g;
         if ((uint64_t)(d + 1 - off) < c) c = d + 1 - off;
+        if (mark_rank(__ldcg(r.mark_win + (I >> 4)), epoch) < k) return true;  // a suspect's window
         uint64_t mid[16];
 #pragma unroll
         for (int q = 0; q < 4; ++q) ld_sector_cg((const uint64_t*)(r.mark_id + I + 4 * q), mid[4 * q], mid[4 * q + 1], mid[4 * q + 2], mid[4 * q + 3]);
@@ -232,8 +236,15 @@ __device__ __forceinline__ void mark_window(const RoundsArgs& r, uint32_t k, uin
     const uint64_t id = r.ids[r.upos[k]];
     const ShardDev sd = r.t.shards[r.ushard[k]];
     const uint64_t h = home_of(id, sd, r.t.seed);
-    for (uint32_t off = 0; off < r.t.P; ++off)
-        atomicMin(r.mark_id + r.mi(slot_of(sd, h, off)), (unsigned long long)mark_key(epoch, k));
+    const uint64_t end = sd.offset + sd.cap.d;
+    for (uint32_t off = 0; off < r.t.P;) {  // one atomic per 16-slot block the window touches
+        const uint64_t g = slot_of(sd, h, off);
+        const uint64_t i = r.mi(g);
+        atomicMin(r.mark_win + (i >> 4), (unsigned long long)mark_key(epoch, k));
+        uint64_t step = 16 - (i & 15);
+        if (end - g < step) step = end - g;  // the window wraps inside the shard
+        off += (uint32_t)step;
+    }
 }
 
 // R4
@@ -357,6 +368,8 @@ void enqueue_rounds(Table& t, const BatchArgs& a, cudaStream_t st, uint8_t* todo
     if (t.r_mark_mask != msize - 1 || t.mark_epoch > 0xffff0000u) {
         t.r_mark_any.reserve(msize * 8);
         t.r_mark_id.reserve(msize * 8);
+        t.r_mark_win.reserve(msize / 2);
+        MPZCH_CUDA(cudaMemsetAsync(t.r_mark_win.p, 0xff, msize / 2, st));
         MPZCH_CUDA(cudaMemsetAsync(t.r_mark_any.p, 0xff, msize * 8, st));
         MPZCH_CUDA(cudaMemsetAsync(t.r_mark_id.p, 0xff, msize * 8, st));
         t.r_mark_mask = msize - 1;
@@ -388,6 +401,7 @@ void enqueue_rounds(Table& t, const BatchArgs& a, cudaStream_t st, uint8_t* todo
     r.todo = todo;
     r.mark_any = t.r_mark_any.as<unsigned long long>();
     r.mark_id = t.r_mark_id.as<unsigned long long>();
+    r.mark_win = t.r_mark_win.as<unsigned long long>();
     r.mark_base = t.row_lo;
     r.mark_mask = t.r_mark_mask;
     r.uslot = t.o_uslot.as<uint64_t>();

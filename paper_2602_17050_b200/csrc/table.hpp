@@ -170,7 +170,7 @@ public:
     DevBuf o_key, o_min, o_posent, o_flag, o_upos, o_entu, o_ushard, o_umeta, o_uslot, o_uoc, o_todo;
     uint64_t ocap = 0;
     // rounds path: epoch-keyed reservation marks (<= 2^27 words each, aliased)
-    DevBuf r_mark_any, r_mark_id, r_pend, r_next, r_slot, r_oc, r_d, r_susp;
+    DevBuf r_mark_any, r_mark_id, r_mark_win, r_pend, r_next, r_slot, r_oc, r_d, r_susp;
     uint64_t r_mark_mask = 0;  // mark arrays alias slots modulo their size (sound: more suspects)
     uint32_t mark_epoch = 0;
     // sgd_step (train.cu): row hash, occurrence lists
