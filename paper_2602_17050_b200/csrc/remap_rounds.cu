@@ -45,6 +45,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "table.hpp"
@@ -103,6 +104,7 @@ struct RoundsArgs {
     unsigned long long* mark_id;   // ident-changing writes
     unsigned long long* mark_win;  // suspect windows, one word per 16-slot block of mark_id
     uint64_t mark_base, mark_mask;
+    int closure_max;
     uint64_t* uslot;
     uint8_t* uoc;
     uint64_t* reset_rows;
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(256) k_rounds(RoundsArgs r) {
         grid.sync();
         if (tid == 0) ctr->r_cnt[par ^ 1] = 0;
         for (int c = 0;; ++c) {  // suspicion closure: check and mark in one pass
-            const bool last = c == kClosureMax;
+            const bool last = c == r.closure_max;
             for (unsigned x = tid; x < npend; x += nth) {
                 const uint32_t k = __ldcg(pend + x);
                 if (ldcg_u8(r.susp + k) || !suspect<MODE>(r, k, epoch)) continue;
@@ -402,6 +404,11 @@ void enqueue_rounds(Table& t, const BatchArgs& a, cudaStream_t st, uint8_t* todo
     r.mark_any = t.r_mark_any.as<unsigned long long>();
     r.mark_id = t.r_mark_id.as<unsigned long long>();
     r.mark_win = t.r_mark_win.as<unsigned long long>();
+    static const int closure_max = [] {
+        const char* e = getenv("MPZCH_CLOSURE_MAX");
+        return e ? atoi(e) : kClosureMax;
+    }();
+    r.closure_max = closure_max;
     r.mark_base = t.row_lo;
     r.mark_mask = t.r_mark_mask;
     r.uslot = t.o_uslot.as<uint64_t>();
