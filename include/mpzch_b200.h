@@ -209,6 +209,41 @@ mpzch_status mpzch_validate_device(const mpzch_table* t, const uint64_t* ids, ui
 mpzch_status mpzch_route_device(const mpzch_table* t, const uint64_t* ids, uint64_t n,
                                 const uint32_t* shard_to_part, uint32_t parts, uint32_t* perm,
                                 uint64_t* counts, void* stream);
+/* ---- peer-memory transport of the row-sharded mode (replaces the NCCL all-to-all pair; the
+ *      reference has no counterpart -- its shards live in one process, batch_engine.cpp:141-221).
+ *      Addresses are device addresses valid in the calling process: local buffers, buffers of
+ *      another GPU reachable by P2P, or another process's buffers mapped by mpzch_ipc_import.
+ *   1. mpzch_route_count_device: per-part counts[parts] (host) of this rank's positions (the
+ *      count and scan phases of mpzch_route_device; arms step 2 for the same ids/n/parts);
+ *   2. mpzch_route_scatter_device: every position i of part q stores ids[i], features[i] and
+ *      i into part q's receive buffers ids_to[q] (u64), features_to[q] (u32), src_to[q] (u32)
+ *      at offset[q] + (its rank among this rank's part-q positions): stable, so an owner that
+ *      gives each source rank the offset sum of the lower ranks' counts receives the global
+ *      batch's part-q positions in global order.  One kernel: partition + NVLink stores;
+ *   3. (owners remap their received positions with mpzch_process_batch_device_marked)
+ *   4. mpzch_return_scatter_device: received position j (source rank r: recv_offset[r] <= j <
+ *      recv_offset[r+1]) stores slots[j], outcomes[j], marks[j] into slots_to[r][src[j]],
+ *      outcomes_to[r][src[j]], marks_to[r][src[j]] (marks_to / marks nullable).
+ * The caller orders the phases across ranks (stream sync + a barrier). */
+mpzch_status mpzch_route_count_device(const mpzch_table* t, const uint64_t* ids, uint64_t n,
+                                      const uint32_t* shard_to_part, uint32_t parts, uint64_t* counts,
+                                      void* stream);
+mpzch_status mpzch_route_scatter_device(const mpzch_table* t, const uint64_t* ids,
+                                        const uint32_t* features, uint64_t n, uint32_t parts,
+                                        const uint64_t* ids_to, const uint64_t* features_to,
+                                        const uint64_t* src_to, const uint64_t* offset, void* stream);
+mpzch_status mpzch_return_scatter_device(int device, uint64_t n_recv, const uint64_t* slots,
+                                         const uint8_t* outcomes, const uint8_t* marks,
+                                         const uint32_t* src, uint32_t parts, const uint64_t* recv_offset,
+                                         const uint64_t* slots_to, const uint64_t* outcomes_to,
+                                         const uint64_t* marks_to, void* stream);
+/* CUDA IPC for the transport: a 72-byte record (allocation handle + offset, so buffers inside a
+ * caching allocator's block work); imports are reference counted per allocation. */
+#define MPZCH_IPC_RECORD_BYTES 72
+mpzch_status mpzch_ipc_export(const void* device_ptr, uint8_t* out_record);
+mpzch_status mpzch_ipc_import(int device, const uint8_t* record, uint64_t* out_addr);
+mpzch_status mpzch_ipc_close(uint64_t addr);
+
 /* process_batch on device buffers; out_first_evicted[n] (device, nullable) gets 1 at the first
  * position of every Evicted (id, feature) unique (how the sharded evicted list is assembled) */
 mpzch_status mpzch_process_batch_device_marked(mpzch_table* t, const uint64_t* ids,

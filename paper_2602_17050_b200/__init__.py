@@ -163,6 +163,15 @@ _SIGS = {
     "mpzch_validate_device": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _u64p, _vp]),
     "mpzch_route_device": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _u32p, ctypes.c_uint32, _vp,
                                           _u64p, _vp]),
+    "mpzch_route_count_device": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _u32p, ctypes.c_uint32,
+                                                _u64p, _vp]),
+    "mpzch_route_scatter_device": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_uint64, ctypes.c_uint32,
+                                                  _u64p, _u64p, _u64p, _u64p, _vp]),
+    "mpzch_return_scatter_device": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, _vp, _vp, _vp, _vp,
+                                                   ctypes.c_uint32, _u64p, _u64p, _u64p, _u64p, _vp]),
+    "mpzch_ipc_export": (ctypes.c_int, [_vp, _vp]),
+    "mpzch_ipc_import": (ctypes.c_int, [ctypes.c_int, _vp, _u64p]),
+    "mpzch_ipc_close": (ctypes.c_int, [ctypes.c_uint64]),
     "mpzch_process_batch_device_marked": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_uint64,
                                                          ctypes.c_uint64, ctypes.POINTER(_Policy),
                                                          _vp, _vp, _vp, _u64p, _vp]),
@@ -209,6 +218,45 @@ def _check(rc: int):
     if rc != 0:
         msg = _LIB.mpzch_last_error().decode()
         raise _STATUS.get(rc, MpzchError)(msg)
+
+
+def return_scatter_device(device: int, slots, outcomes, marks, src, recv_offset, slots_to,
+                          outcomes_to, marks_to=None, stream=None):
+    """Store received results into the source ranks' buffers (mpzch_return_scatter_device)."""
+    import torch
+    lib = load_library()
+    st = stream if stream is not None else torch.cuda.current_stream(device)
+    parts = len(recv_offset) - 1
+    a = [np.ascontiguousarray(x, dtype=np.uint64) for x in (recv_offset, slots_to, outcomes_to)]
+    mt = np.ascontiguousarray(marks_to, dtype=np.uint64) if marks_to is not None else None
+    _check(lib.mpzch_return_scatter_device(
+        device, slots.numel(), ctypes.c_void_p(slots.data_ptr()), ctypes.c_void_p(outcomes.data_ptr()),
+        ctypes.c_void_p(marks.data_ptr()) if marks is not None else None, ctypes.c_void_p(src.data_ptr()),
+        parts, *[x.ctypes.data_as(_u64p) for x in a], mt.ctypes.data_as(_u64p) if mt is not None else None,
+        ctypes.c_void_p(st.cuda_stream)))
+
+
+IPC_RECORD_BYTES = 72
+
+
+def ipc_export(tensor) -> bytes:
+    """CUDA IPC record of a device tensor's storage (allocation handle + offset)."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(IPC_RECORD_BYTES)
+    _check(lib.mpzch_ipc_export(ctypes.c_void_p(tensor.data_ptr()), buf))
+    return buf.raw
+
+
+def ipc_import(device: int, record: bytes) -> int:
+    """Map another process's buffer; returns its device address in this process."""
+    lib = load_library()
+    out = ctypes.c_uint64(0)
+    _check(lib.mpzch_ipc_import(device, ctypes.create_string_buffer(record, IPC_RECORD_BYTES), ctypes.byref(out)))
+    return out.value
+
+
+def ipc_close(addr: int):
+    _check(load_library().mpzch_ipc_close(addr))
 
 
 def _ptr(a: np.ndarray):
@@ -413,6 +461,29 @@ class MpzchTable:
                                             counts.ctypes.data_as(_u64p),
                                             ctypes.c_void_p(st.cuda_stream)))
         return perm, [int(c) for c in counts]
+
+    def route_count_device(self, ids, shard_to_part, parts: int, stream=None):
+        """Per-part counts of this rank's positions (count + scan of route_device); arms
+        route_scatter_device for the same ids."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        s2p = np.ascontiguousarray(shard_to_part, dtype=np.uint32)
+        counts = np.zeros(parts, dtype=np.uint64)
+        _check(self._lib.mpzch_route_count_device(self._h, ctypes.c_void_p(ids.data_ptr()), ids.numel(),
+                                                  s2p.ctypes.data_as(_u32p), parts,
+                                                  counts.ctypes.data_as(_u64p), ctypes.c_void_p(st.cuda_stream)))
+        return [int(c) for c in counts]
+
+    def route_scatter_device(self, ids, features, parts: int, ids_to, features_to, src_to, offset,
+                             stream=None):
+        """Partition + store into the owners' receive buffers (device addresses per part)."""
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        a = [np.ascontiguousarray(x, dtype=np.uint64) for x in (ids_to, features_to or [0] * parts, src_to, offset)]
+        _check(self._lib.mpzch_route_scatter_device(
+            self._h, ctypes.c_void_p(ids.data_ptr()),
+            ctypes.c_void_p(features.data_ptr()) if features is not None else None, ids.numel(), parts,
+            *[x.ctypes.data_as(_u64p) for x in a], ctypes.c_void_p(st.cuda_stream)))
 
     def process_batch_device_marked(self, ids, now: int, policy: EvictionPolicy, features=None,
                                     stream=None):

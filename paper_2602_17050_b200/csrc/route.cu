@@ -8,6 +8,15 @@
 //   k_route_count  one warp per 1024-position chunk: per-part counts (ballot + popc)
 //   k_route_scan   one block: part-major exclusive scan of the chunk counts
 //   k_route_write  one warp per chunk: ballot ranks -> perm[offset + rank] = position
+//
+// Peer-memory transport (replaces the NCCL all-to-all pair of the row-sharded mode):
+//   k_route_scatter  the write phase of the same partition, but every position's id, feature
+//                    and source index are stored straight into the OWNER's receive buffer
+//                    (P2P / IPC-mapped peer memory over NVLink) at this rank's offset there --
+//                    partition and transfer in one kernel, no staging copy, no collective;
+//   k_return_scatter the owner stores every received position's (slot, outcome, first-evicted
+//                    mark) straight into the SOURCE rank's result buffers at the source
+//                    position -- the reverse transfer and the inverse permutation in one kernel.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -64,6 +73,67 @@ __global__ void __launch_bounds__(256) k_route_write(TableDev t, const uint64_t*
             if (p == q) perm[b + __popc(m & ((1u << lane) - 1))] = (uint32_t)i;
             if (lane == (q & 31)) (q < 32 ? base : base2) += __popc(m);
         }
+    }
+}
+
+// Destinations by value (kernel parameters): one entry per part.
+struct PeerDst {
+    uint64_t ids[kMaxParts], feats[kMaxParts], src[kMaxParts], off[kMaxParts];
+};
+
+__global__ void __launch_bounds__(256) k_route_scatter(TableDev t, const uint64_t* __restrict__ ids,
+                                                       const uint32_t* __restrict__ feats, uint64_t n,
+                                                       const uint8_t* __restrict__ s2p, uint32_t parts,
+                                                       const unsigned* __restrict__ off, uint64_t nchunks,
+                                                       const PeerDst d) {
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned lane = lane_id();
+    if (warp >= nchunks) return;
+    // index inside the owner's buffer: this rank's offset there + the position's rank among
+    // this rank's positions of that part (the part-major scan minus the part's start)
+    uint64_t base = 0, base2 = 0;
+    if (lane < parts) base = d.off[lane] + off[(uint64_t)lane * nchunks + warp] - off[(uint64_t)lane * nchunks];
+    if (lane + 32 < parts)
+        base2 = d.off[lane + 32] + off[(uint64_t)(lane + 32) * nchunks + warp] - off[(uint64_t)(lane + 32) * nchunks];
+    for (uint64_t i0 = warp * kChunk; i0 < (warp + 1) * kChunk && i0 < n; i0 += 32) {
+        const uint64_t i = i0 + lane;
+        const uint64_t id = i < n ? ids[i] : 0;
+        const uint32_t p = i < n ? part_of(id, t, s2p) : kNone32;
+        for (uint32_t q = 0; q < parts; ++q) {
+            const unsigned m = __ballot_sync(0xffffffffu, p == q);
+            if (!m) continue;
+            const uint64_t b = __shfl_sync(0xffffffffu, q < 32 ? base : base2, q & 31);
+            if (p == q) {
+                const uint64_t k = b + __popc(m & ((1u << lane) - 1));
+                reinterpret_cast<uint64_t*>(d.ids[q])[k] = id;
+                if (d.feats[q]) reinterpret_cast<uint32_t*>(d.feats[q])[k] = feats[i];
+                reinterpret_cast<uint32_t*>(d.src[q])[k] = (uint32_t)i;
+            }
+            if (lane == (q & 31)) (q < 32 ? base : base2) += __popc(m);
+        }
+    }
+}
+
+struct PeerBack {
+    uint64_t slots[kMaxParts], oc[kMaxParts], mark[kMaxParts], roff[kMaxParts + 1];
+};
+
+__global__ void __launch_bounds__(256) k_return_scatter(uint64_t n_recv, const uint64_t* __restrict__ slots,
+                                                        const uint8_t* __restrict__ oc,
+                                                        const uint8_t* __restrict__ mark,
+                                                        const uint32_t* __restrict__ src, uint32_t parts,
+                                                        const PeerBack b) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_recv; j += (uint64_t)gridDim.x * blockDim.x) {
+        // source rank: the part whose received range holds j (sources arrive rank-ordered)
+        uint32_t lo = 0, hi = parts;  // roff[lo] <= j < roff[hi]
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (b.roff[mid] <= j) lo = mid; else hi = mid;
+        }
+        const uint32_t p = src[j];
+        reinterpret_cast<uint64_t*>(b.slots[lo])[p] = slots[j];
+        reinterpret_cast<uint8_t*>(b.oc[lo])[p] = oc[j];
+        if (b.mark[lo]) reinterpret_cast<uint8_t*>(b.mark[lo])[p] = mark ? mark[j] : 0;
     }
 }
 
@@ -142,14 +212,66 @@ void run_route(Table& t, const uint64_t* ids, uint64_t n, const uint32_t* shard_
                                               cnt.as<unsigned>(), nchunks);
         k_route_scan<<<1, 1024, 0, st>>>(cnt.as<unsigned>(), nchunks * parts, tot.as<unsigned>(), parts,
                                          nchunks);
-        k_route_write<<<blocks, 256, 0, st>>>(t.dev, ids, n, s2p.as<uint8_t>(), parts,
-                                              cnt.as<unsigned>(), nchunks, perm);
-        t.launches += 3;
+        if (perm) {
+            k_route_write<<<blocks, 256, 0, st>>>(t.dev, ids, n, s2p.as<uint8_t>(), parts,
+                                                  cnt.as<unsigned>(), nchunks, perm);
+            ++t.launches;
+        }
+        t.launches += 2;
         MPZCH_CUDA(cudaGetLastError());
         MPZCH_CUDA(cudaMemcpyAsync(ht.data(), tot.p, parts * 4, cudaMemcpyDeviceToHost, st));
     }
     MPZCH_CUDA(cudaStreamSynchronize(st));
     for (uint32_t p = 0; p < parts; ++p) counts[p] = ht[p];
+    t.rt_ids = perm ? nullptr : ids;  // a count-only route arms run_route_scatter
+    t.rt_n = n;
+    t.rt_nchunks = nchunks;
+    t.rt_parts = parts;
+}
+
+void run_route_scatter(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n,
+                       uint32_t parts, const PeerScatter& d, cudaStream_t st) {
+    if (!t.rt_ids || t.rt_ids != ids || t.rt_n != n || t.rt_parts != parts)
+        throw Error{MPZCH_EINVAL, "route scatter: call mpzch_route_count_device on the same ids first"};
+    PeerDst pd{};
+    for (uint32_t q = 0; q < parts; ++q) {
+        if (!d.ids_to[q] || !d.src_to[q]) throw Error{MPZCH_EINVAL, "route scatter: null destination"};
+        if (feats && !d.feats_to[q]) throw Error{MPZCH_EINVAL, "route scatter: null feature destination"};
+        pd.ids[q] = d.ids_to[q];
+        pd.feats[q] = feats ? d.feats_to[q] : 0;
+        pd.src[q] = d.src_to[q];
+        pd.off[q] = d.offset[q];
+    }
+    t.rt_ids = nullptr;
+    if (n == 0) return;
+    const uint64_t nchunks = t.rt_nchunks;
+    const unsigned blocks = (unsigned)((nchunks * 32 + 255) / 256);
+    k_route_scatter<<<blocks, 256, 0, st>>>(t.dev, ids, feats, n, t.rt_s2p.as<uint8_t>(), parts,
+                                            t.rt_cnt.as<unsigned>(), nchunks, pd);
+    ++t.launches;
+    MPZCH_CUDA(cudaGetLastError());
+}
+
+void run_return_scatter(uint64_t n_recv, const uint64_t* slots, const uint8_t* oc, const uint8_t* mark,
+                        const uint32_t* src, uint32_t parts, const uint64_t* recv_offset,
+                        const uint64_t* slots_to, const uint64_t* oc_to, const uint64_t* mark_to,
+                        cudaStream_t st) {
+    if (parts == 0 || parts > kMaxParts) throw Error{MPZCH_EINVAL, "return scatter: 1..64 parts"};
+    PeerBack b{};
+    for (uint32_t r = 0; r <= parts; ++r) b.roff[r] = recv_offset[r];
+    if (b.roff[0] != 0 || b.roff[parts] != n_recv)
+        throw Error{MPZCH_EINVAL, "return scatter: received offsets must run from 0 to n_recv"};
+    for (uint32_t r = 0; r < parts; ++r) {
+        if (b.roff[r + 1] < b.roff[r]) throw Error{MPZCH_EINVAL, "return scatter: offsets decrease"};
+        if (b.roff[r + 1] > b.roff[r] && (!slots_to[r] || !oc_to[r]))
+            throw Error{MPZCH_EINVAL, "return scatter: null destination"};
+        b.slots[r] = slots_to[r];
+        b.oc[r] = oc_to[r];
+        b.mark[r] = mark_to ? mark_to[r] : 0;
+    }
+    if (n_recv == 0) return;
+    k_return_scatter<<<grid_for(n_recv, 256, 148u * 8u), 256, 0, st>>>(n_recv, slots, oc, mark, src, parts, b);
+    MPZCH_CUDA(cudaGetLastError());
 }
 
 }  // namespace mpzch_b200

@@ -8,11 +8,14 @@
 //   make_cursor / dirty_rows_since proj/src/table.cpp:209-225
 // Every error is detected before the first mutation and reported with the
 // reference's exception category and what() text.
+#include <cuda.h>  // CUresult / CUdeviceptr types only (driver entry point, no -lcuda)
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -681,6 +684,129 @@ mpzch_status mpzch_route_device(const mpzch_table* t, const uint64_t* ids, uint6
         Table& T = *t->t;
         DeviceGuard g(T.device);
         run_route(T, ids, n, shard_to_part, parts, perm, counts, (cudaStream_t)stream);
+    });
+}
+
+mpzch_status mpzch_route_count_device(const mpzch_table* t, const uint64_t* ids, uint64_t n,
+                                      const uint32_t* shard_to_part, uint32_t parts, uint64_t* counts,
+                                      void* stream) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        DeviceGuard g(T.device);
+        run_route(T, ids, n, shard_to_part, parts, nullptr, counts, (cudaStream_t)stream);
+    });
+}
+
+mpzch_status mpzch_route_scatter_device(const mpzch_table* t, const uint64_t* ids,
+                                        const uint32_t* features, uint64_t n, uint32_t parts,
+                                        const uint64_t* ids_to, const uint64_t* features_to,
+                                        const uint64_t* src_to, const uint64_t* offset, void* stream) {
+    CHECK_T(t);
+    return guarded([&] {
+        if (!ids_to || !src_to || !offset || (features && !features_to))
+            throw Error{MPZCH_EINVAL, "route scatter: null destination table"};
+        Table& T = *t->t;
+        DeviceGuard g(T.device);
+        PeerScatter d{ids_to, features_to, src_to, offset};
+        run_route_scatter(T, ids, features, n, parts, d, (cudaStream_t)stream);
+    });
+}
+
+mpzch_status mpzch_return_scatter_device(int device, uint64_t n_recv, const uint64_t* slots,
+                                         const uint8_t* outcomes, const uint8_t* marks,
+                                         const uint32_t* src, uint32_t parts, const uint64_t* recv_offset,
+                                         const uint64_t* slots_to, const uint64_t* outcomes_to,
+                                         const uint64_t* marks_to, void* stream) {
+    return guarded([&] {
+        if (!recv_offset || !slots_to || !outcomes_to)
+            throw Error{MPZCH_EINVAL, "return scatter: null destination table"};
+        DeviceGuard g(device);
+        run_return_scatter(n_recv, slots, outcomes, marks, src, parts, recv_offset, slots_to, outcomes_to,
+                           marks_to, (cudaStream_t)stream);
+    });
+}
+
+namespace {
+// CUDA IPC of buffers that may sit inside a larger allocation (PyTorch's caching allocator):
+// the handle names the allocation, the record carries the offset.  Imports are reference
+// counted per handle (a process maps an allocation once).
+struct IpcRecord {
+    cudaIpcMemHandle_t h;
+    uint64_t offset;
+};
+static_assert(sizeof(IpcRecord) == MPZCH_IPC_RECORD_BYTES, "IPC record size");
+std::mutex g_ipc_mu;
+struct IpcMap {
+    void* base;
+    int refs;
+};
+std::map<std::string, IpcMap> g_ipc_open;        // handle bytes -> mapping
+std::map<uint64_t, std::string> g_ipc_addr;      // imported address -> handle bytes
+
+CUresult (*get_range_fn())(CUdeviceptr*, size_t*, CUdeviceptr) {
+    static CUresult (*fn)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        MPZCH_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) throw Error{MPZCH_ECUDA, "cuMemGetAddressRange unavailable"};
+        fn = reinterpret_cast<CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr)>(p);
+    }
+    return fn;
+}
+}  // namespace
+
+mpzch_status mpzch_ipc_export(const void* device_ptr, uint8_t* out) {
+    return guarded([&] {
+        if (!device_ptr || !out) throw Error{MPZCH_EINVAL, "ipc export: null pointer"};
+        CUdeviceptr base = 0;
+        size_t size = 0;
+        if (get_range_fn()(&base, &size, (CUdeviceptr)device_ptr) != CUDA_SUCCESS)
+            throw Error{MPZCH_EINVAL, "ipc export: not a device allocation"};
+        IpcRecord r{};
+        MPZCH_CUDA(cudaIpcGetMemHandle(&r.h, (void*)base));
+        r.offset = (uint64_t)device_ptr - (uint64_t)base;
+        std::memcpy(out, &r, sizeof r);
+    });
+}
+
+mpzch_status mpzch_ipc_import(int device, const uint8_t* in, uint64_t* out_addr) {
+    return guarded([&] {
+        if (!in || !out_addr) throw Error{MPZCH_EINVAL, "ipc import: null pointer"};
+        IpcRecord r;
+        std::memcpy(&r, in, sizeof r);
+        const std::string key(reinterpret_cast<const char*>(&r.h), sizeof r.h);
+        DeviceGuard g(device);
+        std::lock_guard<std::mutex> lk(g_ipc_mu);
+        auto it = g_ipc_open.find(key);
+        if (it == g_ipc_open.end()) {
+            void* base = nullptr;
+            MPZCH_CUDA(cudaIpcOpenMemHandle(&base, r.h, cudaIpcMemLazyEnablePeerAccess));
+            it = g_ipc_open.emplace(key, IpcMap{base, 0}).first;
+        }
+        ++it->second.refs;
+        const uint64_t addr = (uint64_t)it->second.base + r.offset;
+        g_ipc_addr[addr] = key;  // (same address imported twice: one entry, refs counts both)
+        *out_addr = addr;
+    });
+}
+
+mpzch_status mpzch_ipc_close(uint64_t addr) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> lk(g_ipc_mu);
+        auto a = g_ipc_addr.find(addr);
+        if (a == g_ipc_addr.end()) throw Error{MPZCH_EINVAL, "ipc close: address was not imported"};
+        const std::string key = a->second;
+        auto it = g_ipc_open.find(key);
+        if (--it->second.refs == 0) {
+            void* base = it->second.base;
+            g_ipc_open.erase(it);
+            // forget every address of this mapping
+            for (auto i = g_ipc_addr.begin(); i != g_ipc_addr.end();)
+                i = i->second == key ? g_ipc_addr.erase(i) : std::next(i);
+            MPZCH_CUDA(cudaIpcCloseMemHandle(base));
+        }
     });
 }
 

@@ -184,6 +184,10 @@ public:
     // route (route.cu)
     DevBuf rt_s2p, rt_cnt, rt_tot;
     std::vector<uint8_t> rt_map;
+    // the last count-only route (mpzch_route_count_device), which a scatter must match
+    const uint64_t* rt_ids = nullptr;
+    uint64_t rt_n = 0, rt_nchunks = 0;
+    uint32_t rt_parts = 0;
 
     void ensure_fast_scratch(uint64_t n);
     void ensure_pf_scratch(uint64_t n);  // per-feature TTL last-writer tables
@@ -246,6 +250,20 @@ void enqueue_compact_evicted(Table& t, uint64_t n, uint64_t* out_ev, uint64_t ev
 void run_route(Table& t, const uint64_t* ids, uint64_t n, const uint32_t* shard_to_part,
                uint32_t parts, uint32_t* perm, uint64_t* counts, cudaStream_t st);
 void run_validate(Table& t, const uint64_t* ids, uint64_t n, cudaStream_t st);
+// peer-memory routing (route.cu): addresses are device addresses valid in this process (local,
+// P2P or IPC-mapped peer memory)
+struct PeerScatter {
+    const uint64_t* ids_to;     // [parts] u64 id arrays of the owners' receive buffers
+    const uint64_t* feats_to;   // [parts] u32 feature arrays (0: no features)
+    const uint64_t* src_to;     // [parts] u32 source-position arrays
+    const uint64_t* offset;     // [parts] this rank's first index in each owner's buffers
+};
+void run_route_scatter(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n,
+                       uint32_t parts, const PeerScatter& d, cudaStream_t st);
+void run_return_scatter(uint64_t n_recv, const uint64_t* slots, const uint8_t* oc, const uint8_t* mark,
+                        const uint32_t* src, uint32_t parts, const uint64_t* recv_offset,
+                        const uint64_t* slots_to, const uint64_t* oc_to, const uint64_t* mark_to,
+                        cudaStream_t st);
 
 inline unsigned grid_for(uint64_t n, unsigned block, unsigned max_blocks = 148u * 32u) {
     uint64_t g = (n + block - 1) / block;

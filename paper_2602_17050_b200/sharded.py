@@ -25,6 +25,14 @@ positions [base_r, base_r + n_r)); one process_batch is:
 The communication and the per-rank engine are parameters, so the same protocol runs
 with torch.distributed (NCCL on GPUs, gloo on CPU in the tests), with in-process
 threads on one GPU (tests), and with any engine exposing validate/route/remap.
+
+transport="peer" replaces both all-to-alls with stores into peer memory (PeerTransport):
+step 2 becomes one kernel (mpzch_route_scatter_device) that partitions the slice and writes
+every (id, feature, source position) straight into its owner's receive buffers over NVLink
+(P2P / CUDA IPC mappings), at an offset the ranks agree on from an all-gather of the per-part
+counts; step 4 becomes one kernel (mpzch_return_scatter_device) in which the owner writes
+every result straight into the source rank's result buffers at the source position, so the
+inverse permutation disappears too.  Phases are ordered by a stream sync + barrier.
 """
 from __future__ import annotations
 
@@ -97,6 +105,16 @@ class TorchComm:
                                     group=self.group)
         return out.to(send.device)
 
+    in_process = False
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+    def all_gather_object(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
     def all_gather_v(self, t, counts: Sequence[int]):
         import torch
         m = max(counts) if counts else 0
@@ -139,6 +157,14 @@ class ThreadComm:
         self.hub.barrier.wait()
         return got
 
+    in_process = True  # every rank's buffers are addressable directly
+
+    def barrier(self):
+        self.hub.barrier.wait()
+
+    def all_gather_object(self, obj):
+        return self._exchange(obj)
+
     def all_gather_int(self, x, like):
         return [int(v) for v in self._exchange(int(x))]
 
@@ -157,6 +183,73 @@ class ThreadComm:
         return torch.cat(self._exchange(t))
 
 
+# ------------------------------------------------------------------------------ peer memory
+
+class PeerTransport:
+    """This rank's receive / result buffers and the device addresses of every rank's.
+
+    Receive side (an owner's): ids u64, features u32, source positions u32 -- written by the
+    sources' route-scatter kernels.  Result side (a source's): slots u64, outcomes u8, marks u8
+    -- written by the owners' return-scatter kernels.  Buffers grow collectively (every rank
+    reallocates and re-exchanges addresses when any rank needs more room)."""
+
+    KEYS = (("ids", "int64"), ("feats", "int32"), ("src", "int32"), ("slots", "int64"),
+            ("oc", "uint8"), ("mark", "uint8"))
+
+    def __init__(self, comm, device: int):
+        self.comm, self.device = comm, device
+        self.cap = 0
+        self.local = {}
+        self.peers: List[dict] = []
+        self._imported: List[int] = []
+
+    def close(self):
+        from . import ipc_close
+        for a in self._imported:
+            ipc_close(a)
+        self._imported = []
+
+    def ensure(self, need: int, like):
+        import torch
+        from . import ipc_export, ipc_import
+        want = max(self.comm.all_gather_int(need, like))
+        if want <= self.cap:
+            return
+        cap = 1024
+        while cap < want:
+            cap <<= 1
+        self.close()
+        self.local = {k: torch.empty(cap, dtype=getattr(torch, dt), device=f"cuda:{self.device}")
+                      for k, dt in self.KEYS}
+        if self.comm.in_process:
+            self.peers = self.comm.all_gather_object({k: v.data_ptr() for k, v in self.local.items()})
+        else:
+            torch.cuda.synchronize(self.device)
+            recs = self.comm.all_gather_object({k: ipc_export(v) for k, v in self.local.items()})
+            self.peers = []
+            for r, rec in enumerate(recs):
+                if r == self.comm.rank:
+                    self.peers.append({k: v.data_ptr() for k, v in self.local.items()})
+                else:
+                    addrs = {k: ipc_import(self.device, rec[k]) for k in rec}
+                    self._imported += list(addrs.values())
+                    self.peers.append(addrs)
+        self.cap = cap
+
+    def addrs(self, key: str) -> List[int]:
+        return [p[key] for p in self.peers]
+
+
+def peer_offsets(all_counts: Sequence[Sequence[int]], rank: int) -> Tuple[List[int], List[int]]:
+    """(offsets of this rank's positions in every owner's receive buffer, received counts):
+    sources are laid out in rank order, so owner q's buffer holds the global batch's part-q
+    positions in global order."""
+    world = len(all_counts)
+    offset = [sum(int(all_counts[r][q]) for r in range(rank)) for q in range(world)]
+    recv = [int(all_counts[r][rank]) for r in range(world)]
+    return offset, recv
+
+
 # ------------------------------------------------------------------------------ engines
 
 class GpuEngine:
@@ -173,6 +266,12 @@ class GpuEngine:
     def route(self, ids, shard_to_part, parts):
         return self.table.route_device(ids, shard_to_part, parts)
 
+    def route_count(self, ids, shard_to_part, parts):
+        return self.table.route_count_device(ids, shard_to_part, parts)
+
+    def route_scatter(self, ids, features, parts, ids_to, features_to, src_to, offset):
+        self.table.route_scatter_device(ids, features, parts, ids_to, features_to, src_to, offset)
+
     def remap(self, ids, features, now, policy):
         return self.table.process_batch_device_marked(ids, now, policy, features)
 
@@ -182,9 +281,14 @@ class GpuEngine:
 class ShardedMpzchTable:
     """One rank's view of a row-sharded MpzchTable (proj/include/mpzch/table.hpp:41-131)."""
 
-    def __init__(self, cfg: TableConfig, comm, engine=None, device: int = 0):
+    def __init__(self, cfg: TableConfig, comm, engine=None, device: int = 0, transport: str = "collective"):
+        if transport not in ("collective", "peer"):
+            raise InvalidArgument("transport must be 'collective' or 'peer'")
         self.cfg = cfg
         self.comm = comm
+        self.transport = transport
+        self.device = device
+        self.peer = PeerTransport(comm, device) if transport == "peer" else None
         self.rank, self.world = comm.rank, comm.world
         self.num_shards = len(cfg.shard_capacities)
         self.shard_to_part = np.array([shard_owner(s, self.num_shards, self.world)
@@ -214,6 +318,11 @@ class ShardedMpzchTable:
             over = any(policy.ttl.ttl_for(f) > limit for f in present) if n else False
             if comm.all_reduce_min(0 if over else 1, ids) == 0:
                 raise OverflowError_("TTL expiry overflows the 64-bit timestamp range")
+        if self.peer is not None:
+            slots, oc, mark = self._route_remap_peer(ids, features, now, policy)
+            mine = slots[mark.bool()]
+            counts = comm.all_gather_int(mine.numel(), ids)
+            return slots, oc, comm.all_gather_v(mine, counts)
         perm, send_counts = self.engine.route(ids, self.shard_to_part, self.world)
         recv_counts = self._exchange_counts(send_counts, ids)
         permi = perm.long()
@@ -235,6 +344,31 @@ class ShardedMpzchTable:
         counts = comm.all_gather_int(mine.numel(), ids)
         evicted = comm.all_gather_v(mine, counts)
         return slots, oc, evicted
+
+    def _route_remap_peer(self, ids, features, now, policy):
+        """Steps 2-4 over peer memory (module docstring)."""
+        import torch
+        from . import return_scatter_device
+        comm, tp, G = self.comm, self.peer, self.world
+        n = ids.numel()
+        send_counts = self.engine.route_count(ids, self.shard_to_part, G)
+        offset, recv = peer_offsets(comm.all_gather_object(send_counts), self.rank)
+        R = sum(recv)
+        tp.ensure(max(n, R), ids)
+        self.engine.route_scatter(ids, features, G, tp.addrs("ids"),
+                                  tp.addrs("feats") if features is not None else None,
+                                  tp.addrs("src"), offset)
+        torch.cuda.current_stream(self.device).synchronize()
+        comm.barrier()  # every source's stores have landed in this owner's buffers
+        rid = tp.local["ids"][:R]
+        rfeat = tp.local["feats"][:R] if features is not None else None
+        rs, ro, rm = self.engine.remap(rid, rfeat, now, policy)
+        roff = np.concatenate([[0], np.cumsum(recv)]).astype(np.uint64)
+        return_scatter_device(self.device, rs, ro, rm, tp.local["src"][:R], roff, tp.addrs("slots"),
+                              tp.addrs("oc"), tp.addrs("mark"))
+        torch.cuda.current_stream(self.device).synchronize()
+        comm.barrier()  # every owner's results have landed in this source's buffers
+        return (tp.local["slots"][:n].clone(), tp.local["oc"][:n].clone(), tp.local["mark"][:n].clone())
 
     def _exchange_counts(self, send_counts, like):
         import torch

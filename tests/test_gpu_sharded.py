@@ -14,7 +14,7 @@ from paper_2602_17050_b200.sharded import ShardedMpzchTable, ThreadComm, held_sh
 pytestmark = pytest.mark.gpu
 
 
-def run_sharded(cfg, world, batches, pol):
+def run_sharded(cfg, world, batches, pol, transport="collective"):
     comms = ThreadComm.group(world)
     out = [None] * world
     tables = [None] * world
@@ -23,7 +23,7 @@ def run_sharded(cfg, world, batches, pol):
     def worker(r):
         try:
             torch.cuda.set_device(0)
-            st = ShardedMpzchTable(cfg, comms[r], device=0)
+            st = ShardedMpzchTable(cfg, comms[r], device=0, transport=transport)
             tables[r] = st
             res = []
             for ids, f, now in batches:
@@ -49,9 +49,10 @@ def run_sharded(cfg, world, batches, pol):
     return out, tables
 
 
+@pytest.mark.parametrize("transport", ["collective", "peer"])
 @pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("mode", [0, 1, 2])
-def test_sharded_equals_single_table(oracle, world, mode):
+def test_sharded_equals_single_table(oracle, world, mode, transport):
     rows = 1 << 16
     caps = mz.even_capacities(rows, 8)
     cfg = mz.TableConfig(caps, 32, 7, 8 if mode == 1 else 0, 3)
@@ -62,7 +63,7 @@ def test_sharded_equals_single_table(oracle, world, mode):
     batches = [(uni[rng.integers(0, uni.size, 20000)],
                 rng.integers(0, 3, 20000).astype(np.uint32) if b % 3 == 2 else None, 1 + 40 * b)
                for b in range(8)]
-    out, tables = run_sharded(cfg, world, batches, pol)
+    out, tables = run_sharded(cfg, world, batches, pol, transport)
     single = mz.MpzchTable(cfg)
     o = oracle.OracleTable(caps, 32, 7, cfg.dim, 3)
     for b, (ids, f, now) in enumerate(batches):
@@ -93,8 +94,9 @@ def test_foreign_id_is_rejected():
     assert (t.identities_all() == np.uint64((1 << 64) - 1)).all()
 
 
+@pytest.mark.parametrize("transport", ["collective", "peer"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_sharded_uneven_shards(oracle, world):
+def test_sharded_uneven_shards(oracle, world, transport):
     """Shard capacities that are not multiples of the 16-row line: every rank's held range
     starts and ends inside a line (line-aligned allocation base, masked line walks), with
     small batches (quad line walk) and one >256K-position batch (sector walk)."""
@@ -105,7 +107,7 @@ def test_sharded_uneven_shards(oracle, world):
     rng = np.random.default_rng(world)
     batches = [(uni[rng.integers(0, uni.size, 5000 if b < 5 else 300_000)], None, 1 + 20 * b)
                for b in range(6)]
-    out, tables = run_sharded(cfg, world, batches, pol)
+    out, tables = run_sharded(cfg, world, batches, pol, transport)
     o = oracle.OracleTable(caps, 24, 7, 4, 5)
     for b, (ids, f, now) in enumerate(batches):
         os_, oo, oe = o.process_batch(ids, now, 1, 30, {}, f)
@@ -141,7 +143,7 @@ def test_sharded_random_configurations(oracle, seed):
         n = int(rng.choice([3000, 20000]))
         f = rng.integers(0, 3, n).astype(np.uint32) if b % 2 else None
         batches.append((uni[rng.integers(0, uni.size, n)], f, 1 + 15 * b))
-    out, tables = run_sharded(cfg, world, batches, pol)
+    out, tables = run_sharded(cfg, world, batches, pol, "peer" if seed % 2 else "collective")
     o = oracle.OracleTable(caps, P, 11, dim, 3)
     for b, (ids, f, now) in enumerate(batches):
         os_, oo, oe = o.process_batch(ids, now, mode, 35 if mode == 1 else 0, {}, f)
@@ -154,3 +156,31 @@ def test_sharded_random_configurations(oracle, seed):
     for r in range(world):
         t = tables[r].engine.table
         assert (t.identities_all() == ident[t.row_lo:t.row_hi]).all()
+
+
+def test_peer_transport_two_processes(oracle, tmp_path):
+    """The peer transport across PROCESSES: two ranks (torchrun, gloo for the host barrier and
+    the address exchange) share the one B200 and map each other's receive / result buffers
+    with CUDA IPC (mpzch_ipc_export / mpzch_ipc_import) -- the same code path as one process
+    per GPU on an NVLink box.  Every rank's slice and the evicted list against the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29533",
+           os.path.join(root, "tests", "peer_ipc_worker.py"), str(tmp_path)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    import peer_ipc_worker as w
+    caps, P, batches = w.workload(oracle)
+    o = oracle.OracleTable(caps, P, 7, 4, 3)
+    for b, (ids, f, now) in enumerate(batches):
+        os_, oo, oe = o.process_batch(ids, now, 1, 40, {}, f)
+        got = [np.load(tmp_path / f"r{r}_b{b}.npz") for r in range(2)]
+        gs = np.concatenate([g["s"] for g in got])
+        go = np.concatenate([g["o"] for g in got])
+        assert (gs == os_).all() and (go == oo).all(), f"batch {b}"
+        for g in got:
+            assert (g["e"] == oe).all()

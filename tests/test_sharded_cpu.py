@@ -121,3 +121,20 @@ def test_sharded_protocol_matches_single_table(world, mode):
         a, b_ = int(offs[s_]), int(offs[s_ + 1])
         assert (got[r][4][0][a:b_] == ident[a:b_]).all()
         assert (got[r][4][1][a:b_] == meta[a:b_]).all()
+
+
+def test_peer_offsets_lay_sources_out_in_rank_order():
+    """peer_offsets: rank r's part-q positions start after every lower rank's part-q positions
+    in owner q's receive buffer, and owner r receives column r of the count matrix."""
+    from paper_2602_17050_b200.sharded import peer_offsets
+    counts = [[3, 0, 5], [1, 4, 2], [0, 7, 6]]  # counts[source][owner]
+    assert peer_offsets(counts, 0) == ([0, 0, 0], [3, 1, 0])
+    assert peer_offsets(counts, 1) == ([3, 0, 5], [0, 4, 7])
+    assert peer_offsets(counts, 2) == ([4, 4, 7], [5, 2, 6])
+    for q in range(3):  # the sources tile each owner's buffer exactly
+        spans = sorted((peer_offsets(counts, r)[0][q], counts[r][q]) for r in range(3))
+        pos = 0
+        for off, c in spans:
+            assert off == pos
+            pos += c
+        assert pos == sum(counts[r][q] for r in range(3))
