@@ -20,8 +20,10 @@ run_latency_bench does, proj/src/experiments.cpp:325,347).
 
 Multi-GPU (torchrun, N>1): the same 1B-slot table row-sharded over the N ranks (each holds
 8/N logical shards), every 4M-position batch split into N slices, ids routed to owners and
-results routed back by NCCL all-to-all (paper_2602_17050_b200/sharded.py) -- strong
-scaling of the fixed C5 workload.
+results routed back over peer memory (route-scatter / return-scatter kernels storing into the
+other ranks' CUDA-IPC-mapped buffers over NVLink; MPZCH_TRANSPORT=collective uses the NCCL
+all-to-all instead, paper_2602_17050_b200/sharded.py) -- strong scaling of the fixed C5
+workload.
 """
 import argparse
 import json
@@ -303,6 +305,7 @@ def main():
     # on cuda:0 and collectives staged through the host: a functional check of the N>1 code
     # on a single-GPU box, never a scaling number
     backend = os.environ.get("MPZCH_DIST_BACKEND", "nccl")
+    transport = os.environ.get("MPZCH_TRANSPORT", "peer")
     share = os.environ.get("MPZCH_SHARE_GPU", "0") == "1"
     if world > 1:
         import torch.distributed as dist
@@ -337,7 +340,7 @@ def main():
         # C5 row-sharded: the S=8 logical shards of ONE 1B-slot table spread over the ranks;
         # every global batch of BATCH positions is split into rank slices (strong scaling)
         from paper_2602_17050_b200.sharded import ShardedMpzchTable, TorchComm
-        sharded = ShardedMpzchTable(cfg, TorchComm(), device=dev)
+        sharded = ShardedMpzchTable(cfg, TorchComm(), device=dev, transport=transport)
         probe_table = sharded.engine.table
 
         def remap(ids, now):
@@ -573,7 +576,9 @@ def main():
                                    "max_probe=128, load 0.8 prefilled via the API, 4M-position "
                                    "batches 90% hit / 10% fresh, eviction Disabled"
                                    + ("" if world == 1 else f"; row-sharded over {world} GPUs, "
-                                      f"{backend} all-to-all id routing"),
+                                      + ("peer-memory id routing (IPC stores, "
+                                         f"{backend} barrier)" if transport == "peer" else
+                                         f"{backend} all-to-all id routing")),
                        "rows": rows, "num_shards": SHARDS, "max_probe": MAX_PROBE,
                        "batch_positions": BATCH, "global_batch": BATCH,
                        "parallelism": "single GPU" if world == 1 else f"row-sharded x{world}",

@@ -192,7 +192,7 @@ mpzch_status mpzch_dirty_rows_since(const mpzch_table* t, uint64_t generation, u
 /* ---- row-sharded mode: one handle per rank holds the logical shards
  *      [shard_lo, shard_hi) of the layout (global row numbering unchanged, so results are
  *      identical for every number of ranks).  A rank routes its positions to owners with
- *      mpzch_route_device + an all-to-all (NCCL), owners remap with
+ *      mpzch_route_device + an all-to-all (NCCL) or over peer memory (below), owners remap with
  *      mpzch_process_batch_device_marked, results travel back; see
  *      paper_2602_17050_b200/sharded.py.  Copies (mpzch_copy_*) return the held rows only. */
 mpzch_status mpzch_table_create_sharded(const uint64_t* shard_capacities, uint32_t num_shards,

@@ -115,6 +115,14 @@ class TorchComm:
         self.dist.all_gather_object(out, obj, group=self.group)
         return out
 
+    def all_gather_ints(self, xs: Sequence[int], like) -> List[List[int]]:
+        """One small tensor all-gather (no pickling): every rank's int list."""
+        import torch
+        t = torch.tensor([int(x) for x in xs], dtype=torch.int64, device=self._dev(like))
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return torch.stack(out).cpu().tolist()
+
     def all_gather_v(self, t, counts: Sequence[int]):
         import torch
         m = max(counts) if counts else 0
@@ -165,6 +173,9 @@ class ThreadComm:
     def all_gather_object(self, obj):
         return self._exchange(obj)
 
+    def all_gather_ints(self, xs, like):
+        return [[int(v) for v in x] for x in self._exchange(list(xs))]
+
     def all_gather_int(self, x, like):
         return [int(v) for v in self._exchange(int(x))]
 
@@ -209,10 +220,10 @@ class PeerTransport:
             ipc_close(a)
         self._imported = []
 
-    def ensure(self, need: int, like):
+    def ensure(self, want: int):
+        """Collective when it grows: `want` must be the same on every rank."""
         import torch
         from . import ipc_export, ipc_import
-        want = max(self.comm.all_gather_int(need, like))
         if want <= self.cap:
             return
         cap = 1024
@@ -300,6 +311,8 @@ class ShardedMpzchTable:
         evicted) where evicted is the GLOBAL canonical evicted list (identical on every
         rank)."""
         import torch
+        if self.peer is not None:
+            return self._process_peer(ids, features, now, policy)
         comm = self.comm
         n = ids.numel()
         sizes = comm.all_gather_int(n, ids)
@@ -318,11 +331,6 @@ class ShardedMpzchTable:
             over = any(policy.ttl.ttl_for(f) > limit for f in present) if n else False
             if comm.all_reduce_min(0 if over else 1, ids) == 0:
                 raise OverflowError_("TTL expiry overflows the 64-bit timestamp range")
-        if self.peer is not None:
-            slots, oc, mark = self._route_remap_peer(ids, features, now, policy)
-            mine = slots[mark.bool()]
-            counts = comm.all_gather_int(mine.numel(), ids)
-            return slots, oc, comm.all_gather_v(mine, counts)
         perm, send_counts = self.engine.route(ids, self.shard_to_part, self.world)
         recv_counts = self._exchange_counts(send_counts, ids)
         permi = perm.long()
@@ -345,20 +353,43 @@ class ShardedMpzchTable:
         evicted = comm.all_gather_v(mine, counts)
         return slots, oc, evicted
 
-    def _route_remap_peer(self, ids, features, now, policy):
-        """Steps 2-4 over peer memory (module docstring)."""
+    def _process_peer(self, ids, features, now, policy):
+        """process_batch over peer memory in four host collectives: (1) one small all-gather
+        carries every rank's slice size, first invalid position, TTL-overflow flag and
+        per-part counts -- the errors are raised on every rank before anything moves; (2) a
+        barrier after the route-scatter kernel; (3) after the owners' return-scatter, an
+        all-gather of each owner's per-source count of first-evicted marks (it doubles as the
+        barrier); (4) the all-gather of the marked slots (the canonical evicted list)."""
         import torch
         from . import return_scatter_device
         comm, tp, G = self.comm, self.peer, self.world
         n = ids.numel()
+        bad = self.engine.validate(ids) if n else None
+        over = 0
+        if policy.mode == EvictionPolicy.TTL and n:  # make_metadata, eviction.cpp:20-30
+            limit = (1 << 64) - 1 - now
+            present = [0] if features is None else [int(f) for f in torch.unique(features).tolist()]
+            over = int(any(policy.ttl.ttl_for(f) > limit for f in present))
         send_counts = self.engine.route_count(ids, self.shard_to_part, G)
-        offset, recv = peer_offsets(comm.all_gather_object(send_counts), self.rank)
+        allv = comm.all_gather_ints([n, -1 if bad is None else bad, over] + send_counts, ids)
+        sizes = [v[0] for v in allv]
+        if sum(sizes) > 0xFFFFFFFF:  # batch_engine.cpp:82-83
+            raise LengthError("batch exceeds 2^32 - 1 positions")
+        bads = [sum(sizes[:r]) + v[1] for r, v in enumerate(allv) if v[1] >= 0]
+        if bads:  # batch_engine.cpp:90-94: the first invalid GLOBAL position, on every rank
+            raise InvalidArgument(f"invalid id at batch position {min(bads)}")
+        if any(v[2] for v in allv):
+            raise OverflowError_("TTL expiry overflows the 64-bit timestamp range")
+        allc = [v[3:] for v in allv]
+        offset, recv = peer_offsets(allc, self.rank)
         R = sum(recv)
-        tp.ensure(max(n, R), ids)
+        # room for the largest slice and the largest received set of any rank (same on all)
+        tp.ensure(max(max(sizes), max(sum(col) for col in zip(*allc))))
         self.engine.route_scatter(ids, features, G, tp.addrs("ids"),
                                   tp.addrs("feats") if features is not None else None,
                                   tp.addrs("src"), offset)
-        torch.cuda.current_stream(self.device).synchronize()
+        stream = torch.cuda.current_stream(self.device)
+        stream.synchronize()
         comm.barrier()  # every source's stores have landed in this owner's buffers
         rid = tp.local["ids"][:R]
         rfeat = tp.local["feats"][:R] if features is not None else None
@@ -366,9 +397,19 @@ class ShardedMpzchTable:
         roff = np.concatenate([[0], np.cumsum(recv)]).astype(np.uint64)
         return_scatter_device(self.device, rs, ro, rm, tp.local["src"][:R], roff, tp.addrs("slots"),
                               tp.addrs("oc"), tp.addrs("mark"))
-        torch.cuda.current_stream(self.device).synchronize()
-        comm.barrier()  # every owner's results have landed in this source's buffers
-        return (tp.local["slots"][:n].clone(), tp.local["oc"][:n].clone(), tp.local["mark"][:n].clone())
+        if R:
+            src_rank = torch.repeat_interleave(torch.arange(G, device=rm.device),
+                                               torch.tensor(recv, device=rm.device))
+            per_src = torch.bincount(src_rank[rm.bool()], minlength=G).tolist()
+        else:
+            per_src = [0] * G
+        stream.synchronize()
+        marks = comm.all_gather_ints(per_src, ids)  # also: every owner's results have landed
+        ev_counts = [sum(marks[o][r] for o in range(G)) for r in range(G)]
+        slots = tp.local["slots"][:n].clone()
+        oc = tp.local["oc"][:n].clone()
+        mine = slots[tp.local["mark"][:n].bool()]
+        return slots, oc, comm.all_gather_v(mine, ev_counts)
 
     def _exchange_counts(self, send_counts, like):
         import torch

@@ -184,3 +184,36 @@ def test_peer_transport_two_processes(oracle, tmp_path):
         assert (gs == os_).all() and (go == oo).all(), f"batch {b}"
         for g in got:
             assert (g["e"] == oe).all()
+
+
+@pytest.mark.parametrize("transport", ["collective", "peer"])
+def test_sharded_invalid_id_raises_everywhere(transport):
+    """An invalid id in one rank's slice: every rank raises the reference's message with the
+    GLOBAL position (batch_engine.cpp:90-94) and no rank's table changes."""
+    world = 2
+    caps = mz.even_capacities(1 << 12, 4)
+    cfg = mz.TableConfig(caps, 16, 7)
+    comms = ThreadComm.group(world)
+    msgs = [None] * world
+    tables = [None] * world
+
+    def worker(r):
+        torch.cuda.set_device(0)
+        st = ShardedMpzchTable(cfg, comms[r], device=0, transport=transport)
+        tables[r] = st
+        ids = np.arange(1 + 1000 * r, 301 + 1000 * r, dtype=np.uint64)
+        if r == 1:
+            ids[17] = np.uint64((1 << 64) - 1)  # the EMPTY sentinel
+        try:
+            st.process_batch(torch.from_numpy(ids.view(np.int64)).cuda(), 5, mz.EvictionPolicy.disabled())
+        except mz.InvalidArgument as e:
+            msgs[r] = str(e)
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert msgs == ["invalid id at batch position 317"] * world, msgs
+    for r in range(world):
+        assert (tables[r].engine.table.identities_all() == np.uint64((1 << 64) - 1)).all()
