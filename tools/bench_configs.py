@@ -78,6 +78,8 @@ def run_batches(t, batches, nows, pol, stream, timed_from=0, feats=None, split=T
                 paths={p: sum(s["path"] == p for s in stats) for p in sorted({s["path"] for s in stats})},
                 probe_ms=prof["probe_ms"] / nb, claim_ms=prof["claim_ms"] / nb,
                 tail_ms=prof["tail_ms"] / nb,
+                kernel_ms={k: prof[k] / nb for k in ("validate_ms", "dedup_ms", "claimk_ms", "commit_ms",
+                                                     "finalize_ms")},
                 probe_gbs=(prof["probe_bytes"] / nb) / (prof["probe_ms"] / nb / 1e3) / 1e9 if prof["probe_ms"] else None,
                 batch_gbs=(prof["batch_bytes"] / nb) / (prof["batch_ms"] / nb / 1e3) / 1e9 if prof["batch_ms"] else None)
 
