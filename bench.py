@@ -226,6 +226,19 @@ def prefill_count(rows):
     return int(0.8 * rows)
 
 
+def host_cpu() -> str:
+    """nproc and the CPU model (SURVEY 8d asks for both beside the CPU number)."""
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return f"{os.cpu_count()} logical CPUs, {model}"
+
+
 def run_reference_sample(steps: int, warmup: int, rows: int = CPU_ROWS, log=print):
     """The reference library (oracle/_ref, OpenMP process_batch) on the bounded sample."""
     import torch
@@ -293,7 +306,7 @@ def main():
                 "config": {"workload": "C5 sample (reference CPU path)", "rows": CPU_ROWS,
                            "num_shards": SHARDS, "max_probe": MAX_PROBE, "batch_positions": BATCH},
                 "cpu_baseline": {"value": r["value"], "unit": "IDs/s", "cores": r["cores"],
-                                 "kind": r["kind"], "sample": r["sample"]},
+                                 "kind": r["kind"], "sample": r["sample"], "host": host_cpu()},
                 "e2e": {"value": r["value"], "unit": "IDs/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -559,10 +572,15 @@ def main():
         try:
             r = run_reference_sample(3, 1, log=log)
             cpu = {"value": r["value"], "unit": "IDs/s", "cores": r["cores"], "kind": r["kind"],
-                   "sample": r["sample"]}
+                   "sample": r["sample"], "host": host_cpu()}
         except Exception as e:  # the baseline must not take the GPU number down with it
             cpu = {"value": None, "unit": "IDs/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {e}"}
+
+    # distinct (id, feature) uniques per step (uniques/s beside positions/s), counted
+    # on the timed batches outside the timed region
+    uniq = statistics.mean(int(torch.unique(batches[b]).numel())
+                           for b in range(args.warmup, args.warmup + args.steps)) * world
 
     if rank == 0:
         agg = {k: sum(s[k] for s in stats) for k in ("found", "inserted", "collision", "new_ids")}
@@ -586,6 +604,10 @@ def main():
                        "outcomes_per_step_rank0_owner": {k: v / args.steps for k, v in agg.items()}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic() if world == 1 else None,
+                         "frac_vs_nominal_8tbs": achieved / 8000.0,
+                         # DRAM bytes (ncu, the C5 launch) per algorithmic byte
+                         "overfetch": (ncu_traffic() / probe_bytes) if (world == 1 and rows == ROWS and
+                                                                        ncu_traffic() and probe_bytes) else None,
                          "kernel": "k_probe<Disabled, 1 position per thread> (probe of every position; rank 0)",
                          "algorithmic_bytes_per_launch": probe_bytes,
                          "probe_sectors_per_launch": prof["probe_sectors"] / max(prof["probe_launches"], 1),
@@ -602,6 +624,7 @@ def main():
                          "kernel_ms": {k: prof[k] / max(prof["batches"], 1) for k in
                                        ("validate_ms", "dedup_ms", "claimk_ms", "commit_ms",
                                         "finalize_ms")}},
+            "uniques_per_s": uniq / (ms_step / 1e3),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "IDs/s", "h2d_bytes_per_step": BATCH * 8,
                     "d2h_bytes_per_step": BATCH * 9, "steps": e2e_steps, "api": e2e_api,
