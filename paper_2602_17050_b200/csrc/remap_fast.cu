@@ -166,7 +166,13 @@ __global__ void __launch_bounds__(256) k_validate(TableDev t, const uint64_t* __
 
 // K1: probe; each thread keeps U positions in flight (independent sector loads), all
 // positions of a round are issued before any is scanned.
-template <int MODE, int U, int MINB, bool PF = false>
+// TTL walks of new ids run to the first EMPTY through windows full of live and expired ids (C2:
+// a few % of the positions, but most warps hold one, and the warp waits for it).  With
+// defer > 0 a walk still pending after `defer` rounds is handed over -- (position, offset, first
+// expired offset) -- to a RESUME launch of the same kernel, whose warps hold long walks only.
+// Exact: K1 writes no identity and only refreshes live slots (they stay live), so a resumed
+// walk reads what it would have read.
+template <int MODE, int U, int MINB, bool PF = false, bool RESUME = false>
 __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t* __restrict__ ids,
                                                uint64_t n, uint64_t now, uint64_t meta_value,
                                                BatchCounters* ctr,
@@ -175,15 +181,18 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
                                                uint32_t* __restrict__ newpos,
                                                uint64_t* __restrict__ newid,
                                                uint32_t* __restrict__ newa,
-                                               uint32_t* __restrict__ newm) {
+                                               uint32_t* __restrict__ newm,
+                                               uint32_t* __restrict__ dlist = nullptr,
+                                               unsigned defer = 0) {
     pdl_wait();
     if (batch_failed(&ctr->err)) return;
-    constexpr uint8_t kPending = 0, kHit = 1, kEmptyHit = 2, kExhausted = 3, kIdle = 4;
+    constexpr uint8_t kPending = 0, kHit = 1, kEmptyHit = 2, kExhausted = 3, kIdle = 4, kDeferred = 5;
     const unsigned lane = lane_id();
     const uint64_t tile = (uint64_t)blockDim.x * U;
     unsigned long long my_found = 0, my_coll = 0, my_isec = 0, my_msec = 0;
-    for (uint64_t t0 = (uint64_t)blockIdx.x * tile; t0 < n; t0 += (uint64_t)gridDim.x * tile) {
-        uint64_t id[U], g[U], base[U], cap[U], h[U];
+    const uint64_t total = RESUME ? (uint64_t)*(volatile unsigned*)&ctr->deferred : n;
+    for (uint64_t t0 = (uint64_t)blockIdx.x * tile; t0 < total; t0 += (uint64_t)gridDim.x * tile) {
+        uint64_t id[U], g[U], base[U], cap[U], h[U], pos[U];
         uint32_t off[U];
         uint32_t fe[U];  // TTL: offset of the first expired slot walked before the stop
         bool hexp[U];    // TTL: the matched slot itself is expired
@@ -197,16 +206,23 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
             fe[u] = kNone32;
             hexp[u] = false;
             mld[u] = false;
-            if (i < n) {
-                id[u] = ids[i];
+            pos[u] = i;
+            if (i < total) {
+                if (RESUME) {
+                    pos[u] = dlist[3 * i];
+                    off[u] = dlist[3 * i + 1];
+                    fe[u] = dlist[3 * i + 2];
+                }
+                id[u] = ids[pos[u]];
                 const ShardDev sd = t.shards[shard_of(id[u], t)];
                 cap[u] = sd.cap.d;
                 base[u] = sd.offset;
                 h[u] = home_of(id[u], sd, t.seed);
-                g[u] = base[u] + h[u];
+                g[u] = base[u] + (RESUME ? wrap_add(h[u], off[u], cap[u]) : h[u]);
                 st[u] = kPending;
             }
         }
+        unsigned rounds = 0;
         // scan rounds: issue every pending position's next sector, then scan them.  (Handing
         // long runs to a warp-cooperative kernel, or staging sectors in shared memory with
         // cp.async behind block barriers, both measured slower on C5 and C3.)
@@ -255,15 +271,32 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
                     else any = true;
                 }
             }
+            if (!RESUME && defer && any && ++rounds >= defer) {  // hand the long walks over (below)
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (st[u] == kPending) st[u] = kDeferred;
+                any = false;
+            }
             if (!any) break;
+        }
+        if (!RESUME && defer) {  // append the handed-over walks (the new-list ballot below
+                                 // carries the warp's other appends)
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (st[u] != kDeferred) continue;
+                const unsigned k = atomicAdd(&ctr->deferred, 1u);
+                dlist[3 * k] = (uint32_t)pos[u];
+                dlist[3 * k + 1] = off[u];
+                dlist[3 * k + 2] = fe[u];
+            }
         }
         // decisions, final writes (result + metadata word) and the new list
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint64_t i = t0 + (uint64_t)u * blockDim.x + threadIdx.x;
+            const uint64_t i = pos[u];
             bool is_new = false;
             uint32_t a_off = 0, m_off = kNone32;
-            if (st[u] != kIdle) {
+            if (st[u] != kIdle && st[u] != kDeferred) {
                 uint64_t fslot = kEmpty;
                 uint8_t foc = kFound;
                 if (MODE != kModeTtl) {
@@ -1103,11 +1136,26 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
         // TTL walks carry a metadata sector per round too: 2 positions per thread at 3 blocks/SM
         // (C2: 2.78 vs 2.40 G/s for 1 x 4; C4 1.04 vs 1.09)
         // (C2 swept: 1 or 4 positions per thread, 3-32 blocks/SM of grid: all slower)
-        if (ttl && a.per_feature)
-            launch_pdl(k_probe<kModeTtl, 2, 3, true>, grid_for((n + 1) / 2, B, 148u * 16u), B, st, MPZCH_PROBE_ARGS);
-        else if (ttl) launch_pdl(k_probe<kModeTtl, 2, 3>, grid_for((n + 1) / 2, B, 148u * 16u), B, st, MPZCH_PROBE_ARGS);
-        else if (lru) launch_pdl(k_probe<kModeLru, 1, 6>, gP, B, st, MPZCH_PROBE_ARGS);
-        else launch_pdl(k_probe<kModeDisabled, 1, 6>, gP, B, st, MPZCH_PROBE_ARGS);
+        // TTL: walks still pending after `defer` sector rounds finish in a resume launch whose
+        // warps hold long walks only (MPZCH_DEFER=0 disables)
+        static const unsigned defer = [] {
+            const char* e = std::getenv("MPZCH_DEFER");
+            return e ? (unsigned)std::atoi(e) : 8u;  // C4 1.03 -> 1.07 G/s; C2 unchanged (2: -11%, 4: -5%)
+        }();
+        uint32_t* dl = t.s_defer.as<uint32_t>();
+        const unsigned gT = grid_for((n + 1) / 2, B, 148u * 16u), gR = 148u * 3u;
+        if (ttl && a.per_feature) {
+            launch_pdl(k_probe<kModeTtl, 2, 3, true>, gT, B, st, MPZCH_PROBE_ARGS, dl, defer);
+            if (defer) launch_pdl(k_probe<kModeTtl, 2, 3, true, true>, gR, B, st, MPZCH_PROBE_ARGS, dl, 0u);
+        } else if (ttl) {
+            launch_pdl(k_probe<kModeTtl, 2, 3>, gT, B, st, MPZCH_PROBE_ARGS, dl, defer);
+            if (defer) launch_pdl(k_probe<kModeTtl, 2, 3, false, true>, gR, B, st, MPZCH_PROBE_ARGS, dl, 0u);
+        } else if (lru) {
+            launch_pdl(k_probe<kModeLru, 1, 6>, gP, B, st, MPZCH_PROBE_ARGS, (uint32_t*)nullptr, 0u);
+        } else {
+            launch_pdl(k_probe<kModeDisabled, 1, 6>, gP, B, st, MPZCH_PROBE_ARGS, (uint32_t*)nullptr, 0u);
+        }
+        if (ttl && defer) ++t.launches;
     }
 #undef MPZCH_PROBE_ARGS
     ++t.launches;

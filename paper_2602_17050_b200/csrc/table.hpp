@@ -63,6 +63,7 @@ struct BatchCounters {
     // for the ordered kernel
     unsigned int r_cnt[2], r_newc[2], r_minrank, r_rounds, r_left, r_iters;
     unsigned int r_marked, r_checked;  // closure steps / windows marked / range checks (diagnostics)
+    unsigned int deferred, pad4;       // TTL probe: walks handed to the resume pass
 };
 
 // sgd_step scratch counters (train.cu)
@@ -157,6 +158,7 @@ public:
 
     // scratch
     DevBuf s_newpos, s_newid, s_newa, s_newm, s_newent;  // new-list (fast path)
+    DevBuf s_defer;  // TTL probe: (position, offset, first expired) of walks handed to the resume pass
     DevBuf s_tent;                                   // id table: 64-byte entries
     uint64_t tcap = 0;                               // allocated id-table capacity (pow2)
     uint64_t epoch = 0;                              // id-table batch epoch (0 = never used)
