@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256) k_validate(TableDev t, const uint64_t* __
 // expired offset) -- to a RESUME launch of the same kernel, whose warps hold long walks only.
 // Exact: K1 writes no identity and only refreshes live slots (they stay live), so a resumed
 // walk reads what it would have read.
-template <int MODE, int U, int MINB, bool PF = false, bool RESUME = false>
+template <int MODE, int U, int MINB, bool PF = false, bool RESUME = false, bool DEFER = false>
 __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t* __restrict__ ids,
                                                uint64_t n, uint64_t now, uint64_t meta_value,
                                                BatchCounters* ctr,
@@ -192,7 +192,8 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
     unsigned long long my_found = 0, my_coll = 0, my_isec = 0, my_msec = 0;
     const uint64_t total = RESUME ? (uint64_t)*(volatile unsigned*)&ctr->deferred : n;
     for (uint64_t t0 = (uint64_t)blockIdx.x * tile; t0 < total; t0 += (uint64_t)gridDim.x * tile) {
-        uint64_t id[U], g[U], base[U], cap[U], h[U], pos[U];
+        uint64_t id[U], g[U], base[U], cap[U], h[U];
+        uint32_t pos[RESUME ? U : 1];  // RESUME: the handed-over positions
         uint32_t off[U];
         uint32_t fe[U];  // TTL: offset of the first expired slot walked before the stop
         bool hexp[U];    // TTL: the matched slot itself is expired
@@ -206,14 +207,15 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
             fe[u] = kNone32;
             hexp[u] = false;
             mld[u] = false;
-            pos[u] = i;
             if (i < total) {
+                uint64_t p = i;
                 if (RESUME) {
                     pos[u] = dlist[3 * i];
                     off[u] = dlist[3 * i + 1];
                     fe[u] = dlist[3 * i + 2];
+                    p = pos[u];
                 }
-                id[u] = ids[pos[u]];
+                id[u] = ids[p];
                 const ShardDev sd = t.shards[shard_of(id[u], t)];
                 cap[u] = sd.cap.d;
                 base[u] = sd.offset;
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
                 st[u] = kPending;
             }
         }
-        unsigned rounds = 0;
+        unsigned rounds = 0;  // (DEFER)
         // scan rounds: issue every pending position's next sector, then scan them.  (Handing
         // long runs to a warp-cooperative kernel, or staging sectors in shared memory with
         // cp.async behind block barriers, both measured slower on C5 and C3.)
@@ -271,7 +273,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
                     else any = true;
                 }
             }
-            if (!RESUME && defer && any && ++rounds >= defer) {  // hand the long walks over (below)
+            if (DEFER && any && ++rounds >= defer) {  // hand the long walks over (below)
 #pragma unroll
                 for (int u = 0; u < U; ++u)
                     if (st[u] == kPending) st[u] = kDeferred;
@@ -279,13 +281,13 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
             }
             if (!any) break;
         }
-        if (!RESUME && defer) {  // append the handed-over walks (the new-list ballot below
+        if (DEFER) {  // append the handed-over walks (the new-list ballot below
                                  // carries the warp's other appends)
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (st[u] != kDeferred) continue;
                 const unsigned k = atomicAdd(&ctr->deferred, 1u);
-                dlist[3 * k] = (uint32_t)pos[u];
+                dlist[3 * k] = (uint32_t)(t0 + (uint64_t)u * blockDim.x + threadIdx.x);
                 dlist[3 * k + 1] = off[u];
                 dlist[3 * k + 2] = fe[u];
             }
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
         // decisions, final writes (result + metadata word) and the new list
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint64_t i = pos[u];
+            const uint64_t i = RESUME ? (uint64_t)pos[RESUME ? u : 0] : t0 + (uint64_t)u * blockDim.x + threadIdx.x;
             bool is_new = false;
             uint32_t a_off = 0, m_off = kNone32;
             if (st[u] != kIdle && st[u] != kDeferred) {
@@ -1145,11 +1147,19 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
         uint32_t* dl = t.s_defer.as<uint32_t>();
         const unsigned gT = grid_for((n + 1) / 2, B, 148u * 16u), gR = 148u * 3u;
         if (ttl && a.per_feature) {
-            launch_pdl(k_probe<kModeTtl, 2, 3, true>, gT, B, st, MPZCH_PROBE_ARGS, dl, defer);
-            if (defer) launch_pdl(k_probe<kModeTtl, 2, 3, true, true>, gR, B, st, MPZCH_PROBE_ARGS, dl, 0u);
+            if (defer) {
+                launch_pdl(k_probe<kModeTtl, 2, 3, true, false, true>, gT, B, st, MPZCH_PROBE_ARGS, dl, defer);
+                launch_pdl(k_probe<kModeTtl, 2, 3, true, true>, gR, B, st, MPZCH_PROBE_ARGS, dl, 0u);
+            } else {
+                launch_pdl(k_probe<kModeTtl, 2, 3, true>, gT, B, st, MPZCH_PROBE_ARGS, dl, 0u);
+            }
         } else if (ttl) {
-            launch_pdl(k_probe<kModeTtl, 2, 3>, gT, B, st, MPZCH_PROBE_ARGS, dl, defer);
-            if (defer) launch_pdl(k_probe<kModeTtl, 2, 3, false, true>, gR, B, st, MPZCH_PROBE_ARGS, dl, 0u);
+            if (defer) {
+                launch_pdl(k_probe<kModeTtl, 2, 3, false, false, true>, gT, B, st, MPZCH_PROBE_ARGS, dl, defer);
+                launch_pdl(k_probe<kModeTtl, 2, 3, false, true>, gR, B, st, MPZCH_PROBE_ARGS, dl, 0u);
+            } else {
+                launch_pdl(k_probe<kModeTtl, 2, 3>, gT, B, st, MPZCH_PROBE_ARGS, dl, 0u);
+            }
         } else if (lru) {
             launch_pdl(k_probe<kModeLru, 1, 6>, gP, B, st, MPZCH_PROBE_ARGS, (uint32_t*)nullptr, 0u);
         } else {
