@@ -372,7 +372,9 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
 // instruction (lane j: sector j) -- the same cost per access as a single sector on B200
 // (line_scan.cuh) -- and finds the first match / EMPTY of the window part in that line with
 // one 16-bit mask.  Decisions, writes and the new-list append are made by lane 0 of the quad.
-template <int MODE, int U, int MINB, bool PF = false>
+// RESUME: the walks k_probe<..., DEFER> handed over, continued a 128-byte line per round trip
+// (a long walk is a chain of dependent loads: 4x fewer round trips than sector by sector).
+template <int MODE, int U, int MINB, bool PF = false, bool RESUME = false>
 __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint64_t* __restrict__ ids,
                                                           uint64_t n, uint64_t now, uint64_t meta_value,
                                                           BatchCounters* ctr,
@@ -381,7 +383,8 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
                                                           uint32_t* __restrict__ newpos,
                                                           uint64_t* __restrict__ newid,
                                                           uint32_t* __restrict__ newa,
-                                                          uint32_t* __restrict__ newm) {
+                                                          uint32_t* __restrict__ newm,
+                                                          const uint32_t* __restrict__ dlist = nullptr) {
     pdl_wait();
     if (batch_failed(&ctr->err)) return;
     constexpr uint8_t kPending = 0, kHit = 1, kEmptyHit = 2, kExhausted = 3, kIdle = 4;
@@ -391,8 +394,10 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
     const uint64_t qib = threadIdx.x >> 2;
     const uint64_t tile = qpb * U;
     unsigned long long my_found = 0, my_coll = 0, my_isec = 0, my_msec = 0;
-    for (uint64_t t0 = (uint64_t)blockIdx.x * tile; t0 < n; t0 += (uint64_t)gridDim.x * tile) {
+    const uint64_t total = RESUME ? (uint64_t)*(volatile unsigned*)&ctr->deferred : n;
+    for (uint64_t t0 = (uint64_t)blockIdx.x * tile; t0 < total; t0 += (uint64_t)gridDim.x * tile) {
         uint64_t id[U], g[U];
+        uint32_t pos[RESUME ? U : 1];
         uint32_t off[U], sh[U];
         uint32_t fe[U];  // TTL: offset of the first expired slot walked before the stop
         bool hexp[U];    // TTL: the matched slot itself is expired
@@ -406,11 +411,19 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
             fe[u] = kNone32;
             hexp[u] = false;
             mld[u] = false;
-            if (i < n) {
-                id[u] = ids[i];
+            if (i < total) {
+                uint64_t p = i;
+                if (RESUME) {
+                    pos[u] = dlist[3 * i];
+                    off[u] = dlist[3 * i + 1];
+                    fe[u] = dlist[3 * i + 2];
+                    p = pos[u];
+                }
+                id[u] = ids[p];
                 sh[u] = shard_of(id[u], t);
                 const ShardDev sd = t.shards[sh[u]];
-                g[u] = sd.offset + home_of(id[u], sd, t.seed);
+                const uint64_t hh = home_of(id[u], sd, t.seed);
+                g[u] = sd.offset + (RESUME ? wrap_add(hh, off[u], sd.cap.d) : hh);
                 st[u] = kPending;
             }
         }
@@ -478,7 +491,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint64_t i = t0 + (uint64_t)u * qpb + qib;
+            const uint64_t i = RESUME ? (uint64_t)pos[RESUME ? u : 0] : t0 + (uint64_t)u * qpb + qib;
             bool is_new = false;
             uint32_t a_off = 0, m_off = kNone32;
             if (st[u] != kIdle) {
@@ -1126,37 +1139,40 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     if (line) {
         constexpr int kUL = 2;
         const unsigned gl = grid_for(4 * ((n + kUL - 1) / kUL), B, 148u * 16u);
-        if (ttl && a.per_feature) launch_pdl(k_probe_line<kModeTtl, kUL, 3, true>, gl, B, st, MPZCH_PROBE_ARGS);
-        else if (ttl) launch_pdl(k_probe_line<kModeTtl, kUL, 3>, gl, B, st, MPZCH_PROBE_ARGS);
-        else if (lru) launch_pdl(k_probe_line<kModeLru, kUL, 4>, gl, B, st, MPZCH_PROBE_ARGS);
+        const uint32_t* nol = nullptr;
+        if (ttl && a.per_feature) launch_pdl(k_probe_line<kModeTtl, kUL, 3, true>, gl, B, st, MPZCH_PROBE_ARGS, nol);
+        else if (ttl) launch_pdl(k_probe_line<kModeTtl, kUL, 3>, gl, B, st, MPZCH_PROBE_ARGS, nol);
+        else if (lru) launch_pdl(k_probe_line<kModeLru, kUL, 4>, gl, B, st, MPZCH_PROBE_ARGS, nol);
         // long windows: one position per quad at 8 blocks/SM (C3 insert-heavy 1.88 -> 2.07 G/s);
         // small batches keep 2 per quad (C1 1.10 vs 1.04 G/s pipelined)
         else if (t.P >= 256)
-            launch_pdl(k_probe_line<kModeDisabled, 1, 8>, grid_for(4 * n, B, 148u * 32u), B, st, MPZCH_PROBE_ARGS);
-        else launch_pdl(k_probe_line<kModeDisabled, kUL, 4>, gl, B, st, MPZCH_PROBE_ARGS);
+            launch_pdl(k_probe_line<kModeDisabled, 1, 8>, grid_for(4 * n, B, 148u * 32u), B, st, MPZCH_PROBE_ARGS, nol);
+        else launch_pdl(k_probe_line<kModeDisabled, kUL, 4>, gl, B, st, MPZCH_PROBE_ARGS, nol);
     } else {
         // TTL walks carry a metadata sector per round too: 2 positions per thread at 3 blocks/SM
         // (C2: 2.78 vs 2.40 G/s for 1 x 4; C4 1.04 vs 1.09)
         // (C2 swept: 1 or 4 positions per thread, 3-32 blocks/SM of grid: all slower)
-        // TTL: walks still pending after `defer` sector rounds finish in a resume launch whose
-        // warps hold long walks only (MPZCH_DEFER=0 disables)
+        // TTL: walks still pending after `defer` sector rounds finish in a resume launch of the
+        // quad line walk, whose warps hold long walks only (MPZCH_DEFER=0 disables)
         static const unsigned defer = [] {
             const char* e = std::getenv("MPZCH_DEFER");
-            return e ? (unsigned)std::atoi(e) : 8u;  // C4 1.03 -> 1.07 G/s; C2 unchanged (2: -11%, 4: -5%)
+            return e ? (unsigned)std::atoi(e) : 8u;  // C2 2.75 -> 3.05-3.09, C4 1.03 -> 1.09 G/s
         }();
         uint32_t* dl = t.s_defer.as<uint32_t>();
-        const unsigned gT = grid_for((n + 1) / 2, B, 148u * 16u), gR = 148u * 3u;
+        const unsigned gT = grid_for((n + 1) / 2, B, 148u * 16u), gR = 148u * 4u;
         if (ttl && a.per_feature) {
             if (defer) {
                 launch_pdl(k_probe<kModeTtl, 2, 3, true, false, true>, gT, B, st, MPZCH_PROBE_ARGS, dl, defer);
-                launch_pdl(k_probe<kModeTtl, 2, 3, true, true>, gR, B, st, MPZCH_PROBE_ARGS, dl, 0u);
+                launch_pdl(k_probe_line<kModeTtl, 1, 4, true, true>, gR, B, st, MPZCH_PROBE_ARGS,
+                           (const uint32_t*)dl);
             } else {
                 launch_pdl(k_probe<kModeTtl, 2, 3, true>, gT, B, st, MPZCH_PROBE_ARGS, dl, 0u);
             }
         } else if (ttl) {
             if (defer) {
                 launch_pdl(k_probe<kModeTtl, 2, 3, false, false, true>, gT, B, st, MPZCH_PROBE_ARGS, dl, defer);
-                launch_pdl(k_probe<kModeTtl, 2, 3, false, true>, gR, B, st, MPZCH_PROBE_ARGS, dl, 0u);
+                launch_pdl(k_probe_line<kModeTtl, 1, 4, false, true>, gR, B, st, MPZCH_PROBE_ARGS,
+                           (const uint32_t*)dl);
             } else {
                 launch_pdl(k_probe<kModeTtl, 2, 3>, gT, B, st, MPZCH_PROBE_ARGS, dl, 0u);
             }
