@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
                     if (MODE != kModeLru && !PF) t.meta[fslot] = meta_value;
                     if (foc == kFound) ++my_found; else ++my_coll;
                 } else if (MODE == kModeLru) {
-                    out_oc[i] = kPendingOc;  // K3c tells Found positions apart by this byte
+                    out_oc[i] = kPendingOc;  // K3a tells Found positions apart by this byte
                 }
             }
             // warp-aggregated append of the new positions (a block barrier here would make
@@ -940,19 +940,45 @@ __global__ void __launch_bounds__(256) k_pf_write(TableDev t, const BatchCounter
 // recently used slot: the first slot of smallest metadata (strict <, probe_core.cpp:97-101 and
 // 125-129) in the table as the sequential reference has it at that id's turn.  At that turn
 // every slot touched earlier in the batch (Found refresh, insert, eviction) holds metadata
-// `now`; every other slot its pre-batch value.  K3b decides every evictor in parallel on K3's end
-// state with claimed slots counted as `now`; its pick v is the reference's whenever
+// `now`; every other slot its pre-batch value.  K3a maps every Found slot to its first Found
+// position; K3b decides every evictor in parallel on K3's end state, counting claimed slots and
+// slots Found before the evictor's position as `now`.  Its pick v is the reference's whenever
 //   * v holds a pre-batch id whose metadata is older than `now` -- then no slot touched before
 //     the evictor's turn (metadata `now`) can beat or tie it, and a slot touched only after it
 //     still had its pre-batch value, which K3b compared;
 //   * no other evictor picked v -- an earlier eviction elsewhere in the window only raises
 //     that slot to `now` (the first point again);
-//   * no position of the batch Found v's id (K3c) -- else the eviction would change what a
-//     later position finds, or the victim was refreshed before the evictor's turn.
+//   * no position Found v's id (after the evictor's turn, since one before would have made v
+//     `now`) -- else that position would miss the evicted id: a cascade.
 // Any other case sets lru_abort: the claims revert and the batch takes the rounds path.
+__device__ __forceinline__ uint32_t found_first(const PfEntry* tab, uint64_t mask, uint64_t g, uint32_t ep) {
+    for (uint64_t h = mix64(g, 0xF0D5ull) & mask;; h = (h + 1) & mask) {
+        const u128 key = ld_cg_u128(&tab[h].key);
+        if ((uint32_t)(key >> 96) != ep) return kNone32;  // no position Found this slot
+        if ((uint64_t)key == g) return ~(uint32_t)__ldcg(&tab[h].rank);
+    }
+}
+
+// K3a (LRU, evictors only): Found slot -> its first Found position
+__global__ void __launch_bounds__(256) k_lru_found(BatchCounters* ctr, uint64_t n,
+                                                   const uint64_t* __restrict__ out_slots,
+                                                   const uint8_t* __restrict__ out_oc,
+                                                   PfEntry* ftab, uint64_t mask, uint32_t ep) {
+    pdl_wait();
+    if (batch_failed(&ctr->err) || ctr->lru_evict == 0) return;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (out_oc[i] != kFound) continue;
+        const uint64_t g = out_slots[i];
+        const uint32_t r = pf_find(ftab, mask, (u128)g | ((u128)ep << 96), mix64(g, 0xF0D5ull) & mask);
+        atomicMax(&ftab[r].rank, ((unsigned long long)ep << 32) | (uint32_t)~(uint32_t)i);
+    }
+}
+
+// K3b
 __global__ void __launch_bounds__(256) k_lru_victim(TableDev t, uint64_t now, BatchCounters* ctr,
                                                     const uint32_t* __restrict__ evl, IdEntry* te,
-                                                    PfEntry* vtab, uint64_t cap_alloc, uint32_t ep) {
+                                                    PfEntry* vtab, uint64_t cap_alloc, const PfEntry* ftab,
+                                                    uint64_t fmask, uint32_t ep) {
     pdl_wait();
     if (batch_failed(&ctr->err)) return;
     const unsigned cnt = ctr->lru_evict;
@@ -963,6 +989,7 @@ __global__ void __launch_bounds__(256) k_lru_victim(TableDev t, uint64_t now, Ba
     for (unsigned k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < cnt; k += warps) {
         const uint32_t e = evl[k];
         const uint64_t id = key_id(te[e].key);
+        const uint32_t rank = rank_of(te[e].rank);
         const ShardDev sd = t.shards[shard_of(id, t)];
         const uint64_t cap = sd.cap.d, base = sd.offset, h = home_of(id, sd, t.seed);
         // lane j scans offsets j, j + 32, ...: first smallest per lane, then across the warp
@@ -971,7 +998,11 @@ __global__ void __launch_bounds__(256) k_lru_victim(TableDev t, uint64_t now, Ba
         for (uint32_t off = lane; off < t.P; off += 32) {
             const uint64_t g = base + wrap_add(h, off, cap);
             const uint64_t v = t.ident[g];
-            const uint64_t m = (v >> 63) ? now : t.meta[g];  // claimed in this batch: `now`
+            uint64_t m = now;  // claimed in this batch
+            if (!(v >> 63)) {
+                m = t.meta[g];
+                if (m < now && found_first(ftab, fmask, g, ep) < rank) m = now;  // refreshed before
+            }
             if (m < best) { best = m; boff = off; }
         }
         uint64_t wb = best;
@@ -982,9 +1013,10 @@ __global__ void __launch_bounds__(256) k_lru_victim(TableDev t, uint64_t now, Ba
         uint32_t wo = best == wb ? boff : kNone32;
         for (int o = 16; o; o >>= 1) wo = min(wo, __shfl_xor_sync(0xffffffffu, wo, o));
         if (lane == 0) {
-            bool ok = wb < now && wo != kNone32;  // < now: a pre-batch id, untouched by claims
+            bool ok = wb < now && wo != kNone32;  // < now: a pre-batch id, untouched before the turn
+            const uint64_t g = base + wrap_add(h, ok ? wo : 0, cap);
+            if (ok) ok = found_first(ftab, fmask, g, ep) == kNone32;  // else a later position Found it
             if (ok) {
-                const uint64_t g = base + wrap_add(h, wo, cap);
                 const uint32_t r = pf_find(vtab, mask, (u128)g | ((u128)ep << 96), mix64(g, 0x5107ull) & mask);
                 const unsigned long long tag = ((unsigned long long)ep << 32) | 1ull;
                 ok = atomicExch(&vtab[r].rank, tag) != tag;  // else two evictors picked one slot
@@ -994,28 +1026,6 @@ __global__ void __launch_bounds__(256) k_lru_victim(TableDev t, uint64_t now, Ba
                 te[e].state = kStateEvict;
             } else {
                 atomicExch(&ctr->lru_abort, 1u);
-            }
-        }
-    }
-}
-
-// K3c (LRU, evictors only): a victim whose id some position Found aborts the attempt.
-__global__ void __launch_bounds__(256) k_lru_touch(BatchCounters* ctr, uint64_t n,
-                                                   const uint64_t* __restrict__ out_slots,
-                                                   const uint8_t* __restrict__ out_oc,
-                                                   const PfEntry* vtab, uint64_t cap_alloc, uint32_t ep) {
-    pdl_wait();
-    if (batch_failed(&ctr->err) || ctr->lru_evict == 0 || ctr->lru_abort) return;
-    const uint64_t mask = table_mask(ctr->lru_evict, cap_alloc);
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        if (out_oc[i] != kFound) continue;
-        const uint64_t g = out_slots[i];
-        for (uint64_t h = mix64(g, 0x5107ull) & mask;; h = (h + 1) & mask) {
-            const u128 key = ld_cg_u128(&vtab[h].key);
-            if ((uint32_t)(key >> 96) != ep) break;  // not a victim
-            if ((uint64_t)key == g) {
-                atomicExch(&ctr->lru_abort, 1u);
-                break;
             }
         }
     }
@@ -1106,7 +1116,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
                            // thread: C5 probe 0.46 -> 0.39 ms going from 2 x 4 blocks/SM to 1 x 6)
     const uint64_t n = a.n;
     t.ensure_fast_scratch(n);
-    if (a.pol->mode == kModeLru) t.ensure_pf_scratch(n);  // the victim set (K3b/K3c)
+    if (a.pol->mode == kModeLru) t.ensure_pf_scratch(n);  // the found map and victim set (K3a/K3b)
     const uint64_t epoch = ++t.epoch;
     const unsigned B = 256;
     const unsigned gW = grid_for(n, B, 148u * 8u);  // count-driven kernels (4/16/32 x 148: same)
@@ -1210,10 +1220,11 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
         if (t.profiling) cudaEventRecord(t.ev[5], st);
         PfEntry* vtab = t.sl_tab.as<PfEntry>();
         const uint32_t ep = (uint32_t)epoch;
+        PfEntry* ftab = t.mf_tab.as<PfEntry>();
+        launch_pdl(k_lru_found, grid_for(n, B, 148u * 8u), B, st, t.d_ctr, n, (const uint64_t*)a.out_slots,
+                   (const uint8_t*)a.out_oc, ftab, t.mf_cap - 1, ep);
         launch_pdl(k_lru_victim, 148u * 4u, B, st, t.dev, a.now, t.d_ctr, (const uint32_t*)newa, te, vtab,
-                   t.mf_cap, ep);
-        launch_pdl(k_lru_touch, grid_for(n, B, 148u * 8u), B, st, t.d_ctr, n, (const uint64_t*)a.out_slots,
-                   (const uint8_t*)a.out_oc, (const PfEntry*)vtab, t.mf_cap, ep);
+                   t.mf_cap, (const PfEntry*)ftab, t.mf_cap - 1, ep);
         launch_pdl(k_lru_revert, gW, B, st, t.dev, t.d_ctr, newpos, newent, te);
         launch_pdl(k_commit<kModeLru>, gW, B, st, t.dev, t.d_ctr, newpos, newid, newent, te, t.gen_clock,
                                              a.uniform_meta, t.s_reset.as<uint64_t>(),

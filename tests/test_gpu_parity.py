@@ -620,20 +620,22 @@ def _lru_case(oracle, caps, P, batches, want_paths):
     assert got[-1] == want_paths, got
 
 
-@pytest.mark.parametrize("case", ["untouched", "found_before", "found_after", "same_victim",
-                                  "tied_now", "repeated_evictor"])
+@pytest.mark.parametrize("case", ["untouched", "found_before", "found_after", "found_before_next_after",
+                                  "same_victim", "tied_now", "repeated_evictor"])
 def test_lru_eviction_cases(oracle, case):
     """The K3b exactness conditions one by one, on a single 8-slot shard with max_probe 8 (every
-    window is the whole shard): one evictor on an untouched victim stays on the claim path; a
-    victim whose id the batch also Finds (before or after the evictor), two evictors on one
-    victim, and metadata tied with `now` revert to the rounds path.  Results, evicted lists,
-    metadata and reset rows equal the oracle's in every case."""
+    window is the whole shard): one evictor on an untouched victim stays on the claim path, and
+    so does one whose least recently used slot was Found earlier in the batch (it is `now` at the
+    evictor's turn, the next oldest is evicted); a victim Found after the evictor (a cascade),
+    two evictors on one victim, and metadata tied with `now` revert to the rounds path.
+    Results, evicted lists, metadata and reset rows equal the oracle's in every case."""
     ids = [1000 + 17 * k for k in range(8)]
     fill = [([x], 1 + k) for k, x in enumerate(ids)]  # metadata 1..8: ids[0] is the LRU slot
     new1, new2 = 5_000_001, 5_000_003
     last = {
         "untouched": ([ids[3], new1, ids[5]], 20, "fast"),
-        "found_before": ([ids[0], new1], 20, "rounds"),
+        "found_before": ([ids[0], new1], 20, "fast"),
+        "found_before_next_after": ([ids[0], new1, ids[1]], 20, "rounds"),
         "found_after": ([new1, ids[0]], 20, "rounds"),
         "same_victim": ([new1, new2], 20, "rounds"),
         "tied_now": ([new1], 5, "rounds"),
