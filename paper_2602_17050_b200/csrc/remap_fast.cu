@@ -699,12 +699,14 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                         ld_sector_cg(t.ident + sec_a4, w0, w1, w2, w3);
                     }
                     uint64_t v = pick4((uint32_t)(g - sec_a4), w0, w1, w2, w3);
-                    if (MODE != kModeTtl) {
-                        // only EMPTY slots are claimable and every claim word carries kFlagEmpty,
-                        // so the lowest rank wins with one atomicMin -- no CAS retry loop under
-                        // contention (EMPTY = ~0 and ids < 2^63 order correctly around claims)
+                    if (MODE != kModeTtl || (v >> 63)) {
+                        // an EMPTY slot or a claim word: the lowest rank wins with one atomicMin --
+                        // no CAS retry loop under contention (EMPTY = ~0 and ids < 2^63 order
+                        // correctly around claim words, which order by rank; a slot's claim words
+                        // all carry its was-EMPTY flag).  Outside TTL only EMPTY slots are
+                        // claimable; under TTL an expired id is claimed by the CAS below.
                         if (!(v >> 63) || (v != kEmpty && claim_rank(v) < rank)) continue;
-                        const uint64_t nv = cv | kFlagEmpty;
+                        const uint64_t nv = cv | (v == kEmpty ? kFlagEmpty : (v & kFlagEmpty));
                         const uint64_t old = atomicMin((unsigned long long*)(t.ident + g), (unsigned long long)nv);
                         if (old < nv) continue;  // an id, or a lower rank got here first
                         atomicMax(&te[e].held, off);
