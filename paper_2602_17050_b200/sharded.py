@@ -353,6 +353,12 @@ class ShardedMpzchTable:
         evicted = comm.all_gather_v(mine, counts)
         return slots, oc, evicted
 
+    def close(self):
+        """Unmap the other ranks' buffers (peer transport); call on every rank before the
+        process group goes away.  (Process exit unmaps them too.)"""
+        if self.peer is not None:
+            self.peer.close()
+
     def _process_peer(self, ids, features, now, policy):
         """process_batch over peer memory in four host collectives: (1) one small all-gather
         carries every rank's slice size, first invalid position, TTL-overflow flag and

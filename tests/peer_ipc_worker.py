@@ -44,7 +44,7 @@ def main():
         s, o, e = st.process_batch(ti, now, pol, tf)
         np.savez(os.path.join(out, f"r{rank}_b{b}.npz"), s=s.cpu().numpy().view(np.uint64),
                  o=o.cpu().numpy(), e=e.cpu().numpy().view(np.uint64))
-    st.peer.close()
+    st.close()
     dist.barrier()
     dist.destroy_process_group()
 
