@@ -635,6 +635,8 @@ def main():
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        torch.distributed.barrier()
+        sharded.close()  # unmap the peers' IPC buffers before the group goes away
         torch.distributed.destroy_process_group()
 
 
