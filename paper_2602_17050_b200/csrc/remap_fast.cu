@@ -1,5 +1,7 @@
 // remap_fast.cu -- the B200 fast path of process_batch (proj/src/batch_engine.cpp:141-221)
-// for hole-free tables under Disabled, or TTL with one metadata value per batch.
+// for hole-free tables under Disabled, TTL (one metadata value per batch, or per-feature values
+// through the last-writer pass M1-M3 below) and LRU (evictions placed by K3a/K3b below, or the
+// batch reverts to the rounds path).
 //
 // Exactness argument: within a batch the set of slots a new id may
 // take only shrinks (EMPTY -> id, expired -> live), every unique probes its own window,
@@ -12,14 +14,16 @@
 //                 mutates a batch that failed here.
 //   K1 probe      one thread per POSITION, 32-byte sector loads from the home slot up to
 //                 the first match or EMPTY (hole-free early exit); long
-//                 windows and small batches: one quad per position, 128-byte lines.
+//                 windows and small batches: one quad per position, 128-byte lines.  TTL:
+//                 walks still pending after 8 sector rounds resume in a quad-line launch.
 //                 Hits on live slots and full windows are final here and write their
 //                 metadata word; everything else goes to the new list.
 //   K2 dedup      new positions -> one 64-byte entry per distinct id (128-bit atomicCAS on
 //                 an epoch-tagged key), rank = first position (atomicMax of ~position).
 //                 (id, feature) secondaries are resolved from the id's first position in K5.
-//   K3 claim      every entry claims slots in its window by 64-bit atomicCAS of a
-//                 rank-stamped claim word into the identity array itself.  A claim
+//   K3 claim      every entry claims slots in its window by a 64-bit atomicMin (EMPTY slots,
+//                 claim words) or atomicCAS (TTL: expired ids) of a rank-stamped claim word
+//                 into the identity array itself.  A claim
 //                 with a lower rank replaces a higher one; the thread that displaces a
 //                 claim continues the displaced entry's scan ("takeover"), so the
 //                 fixpoint -- each entry on the first slot no lower rank holds -- is
