@@ -27,10 +27,14 @@ __device__ __forceinline__ unsigned count16(const uint8_t* f, uint64_t i0, uint6
 }
 
 // flags must be 0/1 bytes; the flag array is padded to a multiple of 16 bytes.
+// gate (nullable): a device word that is 0 when no flag can be set (the three kernels then only
+// write a zero total)
 static __global__ void __launch_bounds__(kCompactThreads) k_compact_count(const uint8_t* __restrict__ flags,
                                                                    uint64_t n,
-                                                                   unsigned* __restrict__ blk) {
+                                                                   unsigned* __restrict__ blk,
+                                                                   const unsigned* gate) {
     pdl_wait();
+    if (gate && *gate == 0) return;
     __shared__ unsigned red[kCompactThreads / 32];
     const uint64_t i0 = (uint64_t)blockIdx.x * kCompactChunk + threadIdx.x * kCompactPerThread;
     unsigned c = i0 < n ? count16(flags, i0, n) : 0;
@@ -45,8 +49,13 @@ static __global__ void __launch_bounds__(kCompactThreads) k_compact_count(const 
 }
 
 // exclusive scan in place; total -> *total
-static __global__ void __launch_bounds__(1024) k_compact_scan(unsigned* blk, unsigned nblk, unsigned* total) {
+static __global__ void __launch_bounds__(1024) k_compact_scan(unsigned* blk, unsigned nblk, unsigned* total,
+                                                             const unsigned* gate) {
     pdl_wait();
+    if (gate && *gate == 0) {
+        if (threadIdx.x == 0 && total) *total = 0;
+        return;
+    }
     __shared__ unsigned carry;
     __shared__ unsigned wsum[32];
     if (threadIdx.x == 0) carry = 0;
@@ -83,8 +92,9 @@ static __global__ void __launch_bounds__(1024) k_compact_scan(unsigned* blk, uns
 template <class Emit>
 __global__ void __launch_bounds__(kCompactThreads) k_compact_write(uint8_t* __restrict__ flags, uint64_t n,
                                                                    const unsigned* __restrict__ blk,
-                                                                   bool clear, Emit emit) {
+                                                                   bool clear, Emit emit, const unsigned* gate) {
     pdl_wait();
+    if (gate && *gate == 0) return;
     __shared__ unsigned wsum[kCompactThreads / 32];
     const uint64_t i0 = (uint64_t)blockIdx.x * kCompactChunk + threadIdx.x * kCompactPerThread;
     const unsigned c = i0 < n ? count16(flags, i0, n) : 0;
@@ -119,12 +129,12 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_write(uint8_t* __re
 
 template <class Emit>
 inline void compact_flags(uint8_t* flags, uint64_t n, unsigned* blk, unsigned* total, bool clear,
-                          Emit emit, cudaStream_t st, uint64_t& launches) {
+                          Emit emit, cudaStream_t st, uint64_t& launches, const unsigned* gate = nullptr) {
     const unsigned nblk = (unsigned)((n + kCompactChunk - 1) / kCompactChunk);
     if (nblk == 0) return;
-    launch_pdl(k_compact_count, nblk, kCompactThreads, st, flags, n, blk);
-    launch_pdl(k_compact_scan, 1, 1024, st, blk, nblk, total);
-    launch_pdl(k_compact_write<Emit>, nblk, kCompactThreads, st, flags, n, (const unsigned*)blk, clear, emit);
+    launch_pdl(k_compact_count, nblk, kCompactThreads, st, (const uint8_t*)flags, n, blk, gate);
+    launch_pdl(k_compact_scan, 1, 1024, st, blk, nblk, total, gate);
+    launch_pdl(k_compact_write<Emit>, nblk, kCompactThreads, st, flags, n, (const unsigned*)blk, clear, emit, gate);
     launches += 3;
 }
 

@@ -1286,7 +1286,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
         if (ttl || lru) MPZCH_CUDA(cudaMemcpyAsync(a.out_mark, t.s_evflag.p, n, cudaMemcpyDeviceToDevice, st));
         else MPZCH_CUDA(cudaMemsetAsync(a.out_mark, 0, n, st));
     }
-    if (ttl || lru) enqueue_compact_evicted(t, n, a.out_ev, a.ev_cap, st);
+    if (ttl || lru) enqueue_compact_evicted(t, n, a.out_ev, a.ev_cap, st, lru ? &t.d_ctr->lru_evict : nullptr);
     if (t.profiling) cudaEventRecord(t.ev[3], st);
 }
 
