@@ -8,6 +8,8 @@
 // keep the full-window scan.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "line_scan.cuh"
 #include "table.hpp"
@@ -66,23 +68,44 @@ __global__ void __launch_bounds__(256) k_lookup(TableDev t, const uint64_t* __re
 
 // Quad line walk (line_scan.cuh): one quad per position, U positions in flight per quad,
 // 16 slots per round.  Used when windows run long (max_probe >= 256 or a full-window scan).
-template <bool kHoleFree, int U>
+// DEFER: walks still pending after `defer` line rounds are handed over -- (position, offset) in
+// dlist, counted in *dcount -- to a RESUME launch whose warps hold long walks only (a warp
+// otherwise waits for its longest walk; the table is read-only here, so a resumed walk reads
+// what it would have read).
+template <bool kHoleFree, int U, bool RESUME = false, bool DEFER = false>
 __global__ void __launch_bounds__(256, U == 1 ? 6 : 4) k_lookup_line(TableDev t, const uint64_t* __restrict__ ids,
                                                         uint64_t n, uint64_t* __restrict__ out_slots,
-                                                        uint8_t* __restrict__ out_oc, BatchErr* err) {
-    constexpr uint8_t kPending = 0, kHit = 1, kStop = 2, kIdle = 3;
+                                                        uint8_t* __restrict__ out_oc, BatchErr* err,
+                                                        uint32_t* __restrict__ dlist = nullptr,
+                                                        unsigned* dcount = nullptr, unsigned defer = 0) {
+    constexpr uint8_t kPending = 0, kHit = 1, kStop = 2, kIdle = 3, kDeferred = 4;
+    if (RESUME) pdl_wait();
     const unsigned j = quad_lane(), qm = quad_mask();
     const uint64_t qpb = blockDim.x >> 2, qib = threadIdx.x >> 2, tile = qpb * U;
-    for (uint64_t t0 = (uint64_t)blockIdx.x * tile; t0 < n; t0 += (uint64_t)gridDim.x * tile) {
+    const uint64_t total = RESUME ? (uint64_t)*(volatile unsigned*)dcount : n;
+    for (uint64_t t0 = (uint64_t)blockIdx.x * tile; t0 < total; t0 += (uint64_t)gridDim.x * tile) {
         uint64_t id[U], g[U], home[U];
         uint32_t off[U], sh[U];
+        uint32_t pos[RESUME ? U : 1];
         uint8_t st[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint64_t i = t0 + (uint64_t)u * qpb + qib;
             st[u] = kIdle;
             off[u] = 0;
-            if (i < n) {
+            if (RESUME && i < total) {
+                pos[u] = dlist[2 * i];
+                off[u] = dlist[2 * i + 1];
+                id[u] = ids[pos[u]];
+                sh[u] = shard_of(id[u], t);
+                const ShardDev sd = t.shards[sh[u]];
+                const uint64_t hh = home_of(id[u], sd, t.seed);
+                home[u] = sd.offset + hh;
+                uint64_t x = hh + off[u];
+                if (x >= sd.cap.d) x -= sd.cap.d;
+                g[u] = sd.offset + x;
+                st[u] = kPending;
+            } else if (!RESUME && i < n) {
                 id[u] = ids[i];
                 if (id[u] >> 63) {
                     if (j == 0) atomicMin(&err->bad_pos, (unsigned long long)i);
@@ -99,6 +122,7 @@ __global__ void __launch_bounds__(256, U == 1 ? 6 : 4) k_lookup_line(TableDev t,
                 st[u] = kPending;
             }
         }
+        unsigned rounds = 0;  // (DEFER)
         for (;;) {
             uint64_t w[U][4];
 #pragma unroll
@@ -131,13 +155,23 @@ __global__ void __launch_bounds__(256, U == 1 ? 6 : 4) k_lookup_line(TableDev t,
                     else any = true;
                 }
             }
+            if (DEFER && any && ++rounds >= defer) {
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (st[u] == kPending) st[u] = kDeferred;
+                any = false;
+            }
             if (!any) break;
         }
         if (j == 0) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const uint64_t i = t0 + (uint64_t)u * qpb + qib;
-                if (st[u] == kHit) {
+                const uint64_t i = RESUME ? (uint64_t)pos[RESUME ? u : 0] : t0 + (uint64_t)u * qpb + qib;
+                if (DEFER && st[u] == kDeferred) {
+                    const unsigned k = atomicAdd(dcount, 1u);
+                    dlist[2 * k] = (uint32_t)i;
+                    dlist[2 * k + 1] = off[u];
+                } else if (st[u] == kHit) {
                     out_slots[i] = g[u];
                     out_oc[i] = kFound;
                 } else if (st[u] == kStop) {
@@ -246,13 +280,23 @@ void run_lookup_gather(const Table& t, const uint64_t* ids, uint64_t n, uint64_t
 }
 
 void run_lookup(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots, uint8_t* out_oc,
-                BatchErr* err, cudaStream_t st) {
+                BatchErr* err, cudaStream_t st, uint32_t* dlist, unsigned* dcount) {
     // long windows (max_probe >= 256, or the full-window scan of a table with holes): quad
     // line walk; else the per-thread sector walk (remap_fast.cu has the same rule)
     if (t.P >= 256 || !t.hole_free) {
         const unsigned gl = grid_for(4 * ((n + 1) / 2), 256, 148u * 16u);
         // one position per quad, 6 blocks/SM (C3 lookups 7.15 -> 8.68 G/s vs 2 per quad)
-        if (t.hole_free)
+        static const unsigned defer = [] {
+            const char* e = getenv("MPZCH_LOOKUP_DEFER");
+            return e ? (unsigned)atoi(e) : 4u;  // C3 synchronous lookups 9.7 -> 10.4 G/s (2: slower)
+        }();
+        if (t.hole_free && dlist && defer && n >= (1ull << 18)) {  // hand the long walks over
+            MPZCH_CUDA(cudaMemsetAsync(dcount, 0, sizeof(unsigned), st));
+            k_lookup_line<true, 1, false, true><<<grid_for(4 * n, 256, 148u * 24u), 256, 0, st>>>(
+                t.dev, ids, n, out_slots, out_oc, err, dlist, dcount, defer);
+            launch_pdl(k_lookup_line<true, 1, true, false>, 148u * 12u, 256u, st, t.dev, ids, n, out_slots, out_oc,
+                       err, dlist, dcount, 0u);
+        } else if (t.hole_free)
             k_lookup_line<true, 1><<<grid_for(4 * n, 256, 148u * 24u), 256, 0, st>>>(t.dev, ids, n, out_slots, out_oc, err);
         else
             k_lookup_line<false, 2><<<gl, 256, 0, st>>>(t.dev, ids, n, out_slots, out_oc, err);

@@ -940,7 +940,8 @@ mpzch_status mpzch_lookup_device(const mpzch_table* t, const uint64_t* ids, uint
         if (n == 0) return;
         cudaStream_t st = (cudaStream_t)stream;  // 0 = legacy default stream
         init_aux_err(T, st);
-        run_lookup(T, ids, n, out_slots, out_oc, &T.d_aux->err, st);
+        T.s_defer.reserve(n * 12);
+        run_lookup(T, ids, n, out_slots, out_oc, &T.d_aux->err, st, T.s_defer.as<uint32_t>(), &T.d_aux->deferred);
         ++T.launches;
         MPZCH_CUDA(cudaGetLastError());
         MPZCH_CUDA(cudaMemcpyAsync(&T.h_aux->err, &T.d_aux->err, sizeof(BatchErr),
@@ -1011,8 +1012,9 @@ mpzch_status mpzch_lookup(const mpzch_table* t, const uint64_t* ids, uint64_t n,
         T.s_ooc.reserve(n);
         MPZCH_CUDA(cudaMemcpyAsync(T.s_ids.p, ids, n * 8, cudaMemcpyHostToDevice, st));
         init_aux_err(T, st);
+        T.s_defer.reserve(n * 12);
         run_lookup(T, T.s_ids.as<uint64_t>(), n, T.s_oslot.as<uint64_t>(), T.s_ooc.as<uint8_t>(),
-                   &T.d_aux->err, st);
+                   &T.d_aux->err, st, T.s_defer.as<uint32_t>(), &T.d_aux->deferred);
         ++T.launches;
         MPZCH_CUDA(cudaGetLastError());
         MPZCH_CUDA(cudaMemcpyAsync(&T.h_aux->err, &T.d_aux->err, sizeof(BatchErr),

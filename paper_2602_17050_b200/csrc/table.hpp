@@ -206,7 +206,7 @@ bool run_hole_check(Table& t);
 void launch_lookup_async(Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots, uint8_t* out_oc,
                          BatchCounters* c, cudaStream_t st);
 void run_lookup(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots,
-                uint8_t* out_oc, BatchErr* err, cudaStream_t st);
+                uint8_t* out_oc, BatchErr* err, cudaStream_t st, uint32_t* dlist = nullptr, unsigned* dcount = nullptr);
 void run_lookup_gather(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots,
                        uint8_t* out_oc, float* out_rows, BatchErr* err, cudaStream_t st);
 // publish.cu: CRC-32 (raw register from 0; finish() applies the reference's init/final xor)
