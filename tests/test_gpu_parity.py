@@ -404,6 +404,35 @@ def test_lookup_matches_oracle(oracle):
     assert (t.identities_all() == o.identities_all()).all()
 
 
+def test_lookup_long_walk_hand_over(oracle):
+    """Synchronous lookups of >= 256K positions at max_probe 256 hand their long walks (after 4
+    line rounds) to a resume launch: host-buffer and device-buffer calls, hits and misses at
+    0.95 load, against the oracle; the ticketed call (no hand-over) agrees too."""
+    import torch
+    rows = 1 << 20
+    caps = mz.even_capacities(rows, 8)
+    t = mz.MpzchTable(mz.TableConfig(caps, 256, 9))
+    o = oracle.OracleTable(caps, 256, 9)
+    ids = oracle.distinct_ids(13, 0, int(0.95 * rows))
+    for i in range(0, ids.size, 1 << 18):
+        t.process_batch(ids[i:i + (1 << 18)], 1, mz.EvictionPolicy.disabled())
+        o.process_batch(ids[i:i + (1 << 18)], 1, 0)
+    q = np.concatenate([ids[::2], oracle.distinct_ids(13, ids.size, 150_000)])
+    assert q.size >= 1 << 18
+    os_, oo = o.lookup(q)
+    gs, go = t.lookup(q)
+    assert (gs == os_).all() and (go == oo).all()
+    qd = torch.from_numpy(q.view(np.int64)).cuda()
+    ds = torch.empty(q.size, dtype=torch.int64, device="cuda")
+    do = torch.empty(q.size, dtype=torch.uint8, device="cuda")
+    t.lookup_device(qd, ds, do)
+    torch.cuda.synchronize()
+    assert (ds.cpu().numpy().view(np.uint64) == os_).all() and (do.cpu().numpy() == oo).all()
+    ds.zero_()
+    t.wait(t.lookup_device_async(qd, ds, do))
+    assert (ds.cpu().numpy().view(np.uint64) == os_).all() and (do.cpu().numpy() == oo).all()
+
+
 def test_hole_import_uses_exact_path(oracle):
     """After a raw import with a hole, remaps follow the full two-pass semantics
     (pass 2 inserts at the EMPTY in front of an existing copy, probe_core.cpp:89-101)."""
