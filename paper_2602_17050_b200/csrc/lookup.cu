@@ -169,8 +169,8 @@ __global__ void __launch_bounds__(256, U == 1 ? 6 : 4) k_lookup_line(TableDev t,
                 const uint64_t i = RESUME ? (uint64_t)pos[RESUME ? u : 0] : t0 + (uint64_t)u * qpb + qib;
                 if (DEFER && st[u] == kDeferred) {
                     const unsigned k = atomicAdd(dcount, 1u);
-                    dlist[2 * k] = (uint32_t)i;
-                    dlist[2 * k + 1] = off[u];
+                    dlist[2 * (uint64_t)k] = (uint32_t)i;
+                    dlist[2 * (uint64_t)k + 1] = off[u];
                 } else if (st[u] == kHit) {
                     out_slots[i] = g[u];
                     out_oc[i] = kFound;
@@ -280,7 +280,7 @@ void run_lookup_gather(const Table& t, const uint64_t* ids, uint64_t n, uint64_t
 }
 
 void run_lookup(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots, uint8_t* out_oc,
-                BatchErr* err, cudaStream_t st, uint32_t* dlist, unsigned* dcount) {
+                BatchErr* err, cudaStream_t st, DevBuf* ldefer, unsigned* dcount) {
     // long windows (max_probe >= 256, or the full-window scan of a table with holes): quad
     // line walk; else the per-thread sector walk (remap_fast.cu has the same rule)
     if (t.P >= 256 || !t.hole_free) {
@@ -290,7 +290,10 @@ void run_lookup(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_s
             const char* e = getenv("MPZCH_LOOKUP_DEFER");
             return e ? (unsigned)atoi(e) : 4u;  // C3 synchronous lookups 9.7 -> 10.4 G/s (2: slower)
         }();
-        if (t.hole_free && dlist && defer && n >= (1ull << 18)) {  // hand the long walks over
+        // the list stores 32-bit positions: batches beyond 2^32 - 1 positions walk in one pass
+        if (t.hole_free && ldefer && defer && n >= (1ull << 18) && n <= 0xffffffffull) {
+            ldefer->reserve(n * 8);  // (position, offset) per handed-over walk
+            uint32_t* dlist = ldefer->as<uint32_t>();
             MPZCH_CUDA(cudaMemsetAsync(dcount, 0, sizeof(unsigned), st));
             k_lookup_line<true, 1, false, true><<<grid_for(4 * n, 256, 148u * 24u), 256, 0, st>>>(
                 t.dev, ids, n, out_slots, out_oc, err, dlist, dcount, defer);

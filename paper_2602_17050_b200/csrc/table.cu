@@ -619,6 +619,8 @@ struct mpzch_table {
 
 extern "C" {
 
+static void order_after_last_batch(Table& T, cudaStream_t st);
+
 const char* mpzch_last_error(void) { return g_last_error.c_str(); }
 
 const char* mpzch_build_info(void) { return MPZCH_BUILD_INFO; }
@@ -939,9 +941,10 @@ mpzch_status mpzch_lookup_device(const mpzch_table* t, const uint64_t* ids, uint
         DeviceGuard g(T.device);
         if (n == 0) return;
         cudaStream_t st = (cudaStream_t)stream;  // 0 = legacy default stream
+        std::lock_guard<std::mutex> lk(T.lookup_mu);
+        order_after_last_batch(T, st);
         init_aux_err(T, st);
-        T.s_defer.reserve(n * 12);
-        run_lookup(T, ids, n, out_slots, out_oc, &T.d_aux->err, st, T.s_defer.as<uint32_t>(), &T.d_aux->deferred);
+        run_lookup(T, ids, n, out_slots, out_oc, &T.d_aux->err, st, &T.s_ldefer, &T.d_aux->ldeferred);
         ++T.launches;
         MPZCH_CUDA(cudaGetLastError());
         MPZCH_CUDA(cudaMemcpyAsync(&T.h_aux->err, &T.d_aux->err, sizeof(BatchErr),
@@ -1007,20 +1010,22 @@ mpzch_status mpzch_lookup(const mpzch_table* t, const uint64_t* ids, uint64_t n,
         DeviceGuard g(T.device);
         if (n == 0) return;
         cudaStream_t st = T.stream;
-        T.s_ids.reserve(n * 8);
-        T.s_oslot.reserve(n * 8);
-        T.s_ooc.reserve(n);
-        MPZCH_CUDA(cudaMemcpyAsync(T.s_ids.p, ids, n * 8, cudaMemcpyHostToDevice, st));
+        std::lock_guard<std::mutex> lk(T.lookup_mu);
+        order_after_last_batch(T, st);
+        DevBuf &ids_d = T.l_ids, &oslot_d = T.l_oslot, &ooc_d = T.l_ooc;  // lookup-owned staging
+        ids_d.reserve(n * 8);
+        oslot_d.reserve(n * 8);
+        ooc_d.reserve(n);
+        MPZCH_CUDA(cudaMemcpyAsync(ids_d.p, ids, n * 8, cudaMemcpyHostToDevice, st));
         init_aux_err(T, st);
-        T.s_defer.reserve(n * 12);
-        run_lookup(T, T.s_ids.as<uint64_t>(), n, T.s_oslot.as<uint64_t>(), T.s_ooc.as<uint8_t>(),
-                   &T.d_aux->err, st, T.s_defer.as<uint32_t>(), &T.d_aux->deferred);
+        run_lookup(T, ids_d.as<uint64_t>(), n, oslot_d.as<uint64_t>(), ooc_d.as<uint8_t>(),
+                   &T.d_aux->err, st, &T.s_ldefer, &T.d_aux->ldeferred);
         ++T.launches;
         MPZCH_CUDA(cudaGetLastError());
         MPZCH_CUDA(cudaMemcpyAsync(&T.h_aux->err, &T.d_aux->err, sizeof(BatchErr),
                                    cudaMemcpyDeviceToHost, st));
-        MPZCH_CUDA(cudaMemcpyAsync(out_slots, T.s_oslot.p, n * 8, cudaMemcpyDeviceToHost, st));
-        MPZCH_CUDA(cudaMemcpyAsync(out_oc, T.s_ooc.p, n, cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaMemcpyAsync(out_slots, oslot_d.p, n * 8, cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaMemcpyAsync(out_oc, ooc_d.p, n, cudaMemcpyDeviceToHost, st));
         MPZCH_CUDA(cudaStreamSynchronize(st));
         if (T.h_aux->err.bad_pos != ~0ull) require_valid_id(ids[T.h_aux->err.bad_pos]);
         if (T.h_aux->err.foreign_pos != ~0ull)
@@ -1294,6 +1299,8 @@ mpzch_status mpzch_lookup_gather_device(const mpzch_table* t, const uint64_t* id
         DeviceGuard g(T.device);
         if (n == 0) return;
         cudaStream_t st = (cudaStream_t)stream;
+        std::lock_guard<std::mutex> lk(T.lookup_mu);
+        order_after_last_batch(T, st);
         init_aux_err(T, st);
         run_lookup_gather(T, ids, n, out_slots, out_oc, out_rows, &T.d_aux->err, st);
         ++T.launches;

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -63,7 +64,8 @@ struct BatchCounters {
     // for the ordered kernel
     unsigned int r_cnt[2], r_newc[2], r_minrank, r_rounds, r_left, r_iters;
     unsigned int r_marked, r_checked;  // closure steps / windows marked / range checks (diagnostics)
-    unsigned int deferred, pad4;       // TTL probe: walks handed to the resume pass
+    unsigned int deferred;             // TTL probe: walks handed to the resume pass
+    unsigned int ldeferred;            // synchronous lookups: walks handed to the resume pass
 };
 
 // sgd_step scratch counters (train.cu)
@@ -159,6 +161,10 @@ public:
     // scratch
     DevBuf s_newpos, s_newid, s_newa, s_newm, s_newent;  // new-list (fast path)
     DevBuf s_defer;  // TTL probe: (position, offset, first expired) of walks handed to the resume pass
+    // synchronous lookups (mpzch_lookup[_device], lookup_gather): their own hand-over list and
+    // a lock, so concurrent const lookups on one handle never share scratch or the error word
+    DevBuf s_ldefer, l_ids, l_oslot, l_ooc;
+    std::mutex lookup_mu;
     DevBuf s_tent;                                   // id table: 64-byte entries
     uint64_t tcap = 0;                               // allocated id-table capacity (pow2)
     uint64_t epoch = 0;                              // id-table batch epoch (0 = never used)
@@ -205,8 +211,10 @@ bool run_hole_check(Table& t);
 // lookup into a ring counter block (error word + the first bad id), all enqueued on st
 void launch_lookup_async(Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots, uint8_t* out_oc,
                          BatchCounters* c, cudaStream_t st);
+// ldefer (nullable): scratch for the walk hand-over, reserved only when the hand-over runs
 void run_lookup(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots,
-                uint8_t* out_oc, BatchErr* err, cudaStream_t st, uint32_t* dlist = nullptr, unsigned* dcount = nullptr);
+                uint8_t* out_oc, BatchErr* err, cudaStream_t st, DevBuf* ldefer = nullptr,
+                unsigned* dcount = nullptr);
 void run_lookup_gather(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_slots,
                        uint8_t* out_oc, float* out_rows, BatchErr* err, cudaStream_t st);
 // publish.cu: CRC-32 (raw register from 0; finish() applies the reference's init/final xor)
