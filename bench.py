@@ -15,8 +15,10 @@ run_latency_bench does, proj/src/experiments.cpp:325,347).
             + per-position I/O) / its CUDA-event launch time, vs MEASURED_PEAKS hbm_gbs
   cpu_baseline / --impl reference
             the REFERENCE library (oracle/_ref, /root/reference/proj/src compiled by
-            oracle/Makefile, OpenMP over all host cores) on a bounded sample of the same
-            workload (2^25 rows, same S/P/load/mix/batch size).
+            oracle/Makefile, OpenMP over all host cores) on the SAME workload: the 2^30-row
+            layout, the same prefill and the same batch stream, each batch timed with
+            steady_clock around process_batch alone (proj/src/experiments.cpp:339-347);
+            cpu_baseline times 3 of those batches, --impl reference K of them.
 
 Multi-GPU (torchrun, N>1): the same 1B-slot table row-sharded over the N ranks (each holds
 8/N logical shards), every 4M-position batch split into N slices, ids routed to owners and
@@ -219,7 +221,6 @@ TABLE_SEED = 7
 ID_SEED = 5
 BATCH = 4 * 1024 * 1024
 SAMPLER_SEED = 0x5CA1AB1E
-CPU_ROWS = 1 << 25
 
 
 def prefill_count(rows):
@@ -239,8 +240,15 @@ def host_cpu() -> str:
     return f"{os.cpu_count()} logical CPUs, {model}"
 
 
-def run_reference_sample(steps: int, warmup: int, rows: int = CPU_ROWS, log=print):
-    """The reference library (oracle/_ref, OpenMP process_batch) on the bounded sample."""
+def run_reference(steps: int, warmup: int, rows: int = ROWS, log=print):
+    """The reference library (oracle/_ref, OpenMP process_batch) on the SAME workload as the GPU
+    arm: the same TableLayout (2^30 rows, S=8, P=128, seed 7), the same prefill
+    (DistinctIdStream(5).at([0, 0.8 * rows)) at now = 1) and the same batch stream (batch b of the
+    GPU arm's list, now = 2 + b).  Each batch is timed the reference's way
+    (proj/src/experiments.cpp:339-347): steady_clock around mpzch::process_batch alone, inside
+    the shim (the IdBatch is packed before the clock starts).  The prefill goes through the
+    reference's per-shard entry process_shard_batch, shards in parallel (the same state
+    process_batch builds from distinct ids; untimed)."""
     import torch
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
@@ -256,26 +264,52 @@ def run_reference_sample(steps: int, warmup: int, rows: int = CPU_ROWS, log=prin
     t = pyoracle.OracleTable(caps, MAX_PROBE, TABLE_SEED, kind=kind)
     npre = prefill_count(rows)
     t0 = time.perf_counter()
-    for a in range(0, npre, BATCH):
-        ids = distinct_ids_t(ID_SEED, torch.arange(a, min(a + BATCH, npre), dtype=torch.int64))
-        t.process_batch(ids.numpy().view(np.uint64), 1, 0)
-    log(f"[ref] prefill {npre} ids in {time.perf_counter() - t0:.1f}s ({kind}, {cores} threads)")
+    if kind == "reference":
+        t.prefill_distinct(ID_SEED, 0, npre, 1)
+    else:
+        for a in range(0, npre, BATCH):
+            ids = distinct_ids_t(ID_SEED, torch.arange(a, min(a + BATCH, npre), dtype=torch.int64))
+            t.process_batch(ids.numpy().view(np.uint64), 1, 0)
+    log(f"[ref] prefill {npre} ids into {rows} rows in {time.perf_counter() - t0:.1f}s "
+        f"({kind}, {cores} threads)")
     fresh_base = npre
     times = []
     for b in range(warmup + steps):
         idx, nf = batch_indices(torch, "cpu", npre, BATCH, b, fresh_base, SAMPLER_SEED)
         fresh_base += nf
         ids = distinct_ids_t(ID_SEED, idx).numpy().view(np.uint64)
-        s = time.perf_counter()
-        t.process_batch(ids, 2 + b, 0)
-        e = time.perf_counter() - s
+        if kind == "reference":
+            e, _, _ = t.process_batch_timed(ids, 2 + b)
+        else:
+            s = time.perf_counter()
+            t.process_batch(ids, 2 + b, 0)
+            e = time.perf_counter() - s
         if b >= warmup:
             times.append(e)
     tot = sum(times)
+    del t
     return dict(value=BATCH * len(times) / tot, kind=kind, cores=cores, ms=1e3 * tot / len(times),
-                sample=f"C5-shaped {rows}-row table (S={SHARDS}, P={MAX_PROBE}, load 0.8 prefilled "
-                       f"untimed), {len(times)} timed batches of {BATCH} positions 90% hit/10% fresh, "
-                       f"process_batch(ExecMode::Parallel)")
+                sample=f"the GPU arm's workload: {rows}-row table (S={SHARDS}, P={MAX_PROBE}, load 0.8 "
+                       f"prefilled untimed), batches {warmup}..{warmup + steps - 1} of the same stream "
+                       f"({BATCH} positions, 90% hit / 10% fresh), each timed with steady_clock around "
+                       f"process_batch(ExecMode::Parallel) alone",
+                threads_effective=min(cores, SHARDS) if kind == "reference" else 1)
+
+
+def c5_config(rows, world, backend="nccl", transport="peer"):
+    """The workload dict both arms print (same_config)."""
+    return {"workload": ("C5: 1B-slot (2^30-row) table" if rows == ROWS else
+                         f"C5-shaped {rows}-row table") + ", S=8 logical shards, "
+                        "max_probe=128, load 0.8 prefilled via the API, 4M-position "
+                        "batches 90% hit / 10% fresh, eviction Disabled"
+                        + ("" if world == 1 else f"; row-sharded over {world} GPUs, "
+                           + ("peer-memory id routing (IPC stores, "
+                              f"{backend} barrier)" if transport == "peer" else
+                              f"{backend} all-to-all id routing")),
+            "rows": rows, "num_shards": SHARDS, "max_probe": MAX_PROBE,
+            "batch_positions": BATCH, "global_batch": BATCH,
+            "parallelism": "single GPU" if world == 1 else f"row-sharded x{world}",
+            "l2": "inputs larger than L2 (16 GiB identity+metadata, random probes)"}
 
 
 def main():
@@ -298,14 +332,16 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        r = run_reference_sample(args.steps, max(args.warmup, 1), log=log)
+        r = run_reference(args.steps, max(args.warmup, 1), rows=args.rows, log=log)
         line = {"metric": metric, "value": r["value"], "unit": "IDs/s", "impl": "reference",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-                "config": {"workload": "C5 sample (reference CPU path)", "rows": CPU_ROWS,
-                           "num_shards": SHARDS, "max_probe": MAX_PROBE, "batch_positions": BATCH},
+                "vs_baseline": None, "dtype": "u64",
+                "data": "synthetic (DistinctIdStream ids, SplitMix64 sampler)",
+                "config": c5_config(args.rows, world, os.environ.get("MPZCH_DIST_BACKEND", "nccl"),
+                                    os.environ.get("MPZCH_TRANSPORT", "peer")),
                 "cpu_baseline": {"value": r["value"], "unit": "IDs/s", "cores": r["cores"],
+                                 "threads_effective": r["threads_effective"],
                                  "kind": r["kind"], "sample": r["sample"], "host": host_cpu()},
                 "e2e": {"value": r["value"], "unit": "IDs/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
@@ -570,9 +606,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            r = run_reference_sample(3, 1, log=log)
+            r = run_reference(3, 1, rows=rows, log=log)
             cpu = {"value": r["value"], "unit": "IDs/s", "cores": r["cores"], "kind": r["kind"],
-                   "sample": r["sample"], "host": host_cpu()}
+                   "threads_effective": r["threads_effective"], "sample": r["sample"],
+                   "host": host_cpu()}
         except Exception as e:  # the baseline must not take the GPU number down with it
             cpu = {"value": None, "unit": "IDs/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {e}"}
@@ -589,19 +626,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (DistinctIdStream ids, SplitMix64 sampler)",
-            "config": {"workload": ("C5: 1B-slot (2^30-row) table" if rows == ROWS else
-                                    f"C5-shaped {rows}-row table") + ", S=8 logical shards, "
-                                   "max_probe=128, load 0.8 prefilled via the API, 4M-position "
-                                   "batches 90% hit / 10% fresh, eviction Disabled"
-                                   + ("" if world == 1 else f"; row-sharded over {world} GPUs, "
-                                      + ("peer-memory id routing (IPC stores, "
-                                         f"{backend} barrier)" if transport == "peer" else
-                                         f"{backend} all-to-all id routing")),
-                       "rows": rows, "num_shards": SHARDS, "max_probe": MAX_PROBE,
-                       "batch_positions": BATCH, "global_batch": BATCH,
-                       "parallelism": "single GPU" if world == 1 else f"row-sharded x{world}",
-                       "l2": "inputs larger than L2 (16 GiB identity+metadata, random probes)",
-                       "outcomes_per_step_rank0_owner": {k: v / args.steps for k, v in agg.items()}},
+            "config": c5_config(rows, world, backend, transport),
+            "outcomes_per_step_rank0_owner": {k: v / args.steps for k, v in agg.items()},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic() if world == 1 else None,
                          "frac_vs_nominal_8tbs": achieved / 8000.0,

@@ -319,6 +319,59 @@ mpzch_status mpzch_serialize_delta(mpzch_table* t, uint64_t generation, uint32_t
                                    uint64_t sequence, uint8_t* out, uint64_t cap,
                                    uint64_t* out_len, uint64_t* out_next_generation);
 
+
+/* ---- the rest of the kept surface, csrc/surface.cu ---------------------------
+ * MpzchTable::process_shard_batch(shard, span<const Id> ids, span<const u64> metas, now,
+ * policy, span<ProbeResult> out), proj/include/mpzch/table.hpp:71-73, proj/src/table.cpp:112-148:
+ * the serialized probe of one shard, positions in order (no dedup: a repeated id probes again
+ * and refreshes with its own metadata word), each with the caller's metadata word.  ids must
+ * route to `shard` (the reference's precondition; not checked).  Errors: shard >= S ->
+ * MPZCH_ERANGE "shard index out of range" before anything runs; an invalid id or a metadata
+ * word that make_metadata could not have produced -> MPZCH_EINVAL with the reference's text
+ * (probe_core.cpp:49-58, 76-77) AFTER the positions before it took effect (their results are
+ * in out_slots / out_outcomes), exactly like the exception thrown inside the reference's loop.
+ * Host buffers; returns when done. */
+mpzch_status mpzch_process_shard_batch(mpzch_table* t, uint32_t shard, const uint64_t* ids,
+                                       const uint64_t* metas, uint64_t n, uint64_t now,
+                                       const mpzch_policy* policy, uint64_t* out_slots,
+                                       uint8_t* out_outcomes);
+/* dedup(span<const BatchEntry>) -> DedupResult{uniques, inverse}, proj/include/mpzch/
+ * batch_engine.hpp:35, proj/src/batch_engine.cpp:79-108, 133-139: first-occurrence uniques keyed
+ * on (id, feature) (features NULL = 0) and inverse[n] (u32 index into the uniques).  Errors:
+ * n > 2^32 - 1 -> MPZCH_ELENGTH "batch exceeds 2^32 - 1 positions"; an invalid id ->
+ * MPZCH_EINVAL "invalid id at batch position <first bad position>".  mpzch_dedup: host buffers
+ * (unique arrays sized n), runs on `device`; _device: device buffers on `stream`, returns when
+ * done. */
+mpzch_status mpzch_dedup(int device, const uint64_t* ids, const uint32_t* features, uint64_t n,
+                         uint64_t* out_unique_ids, uint32_t* out_unique_features, uint32_t* out_inverse,
+                         uint64_t* out_u);
+mpzch_status mpzch_dedup_device(int device, const uint64_t* ids, const uint32_t* features, uint64_t n,
+                                uint64_t* unique_ids, uint32_t* unique_features, uint32_t* inverse,
+                                uint64_t* out_u, void* stream);
+/* MpzchTable::reset_row(global_row), table.hpp:83, table.cpp:181-186: draw_row weights,
+ * momentum 0, trained 0, row stamped dirty.  dim 0 -> MPZCH_ELOGIC; row out of range ->
+ * MPZCH_ERANGE "embedding row out of range". */
+mpzch_status mpzch_reset_row(mpzch_table* t, uint64_t row);
+/* MpzchTable::state_equals(other), table.hpp:106, table.cpp:249-260: capacities and dim equal,
+ * identities of every shard and the weights bit-equal (compared on the device). */
+mpzch_status mpzch_state_equals(const mpzch_table* a, const mpzch_table* b, int* out_equal);
+/* single-word / range reads for the C++ accessors: row_identity (table.hpp:85, one 8-byte copy),
+ * identities(s) / metadata(s) (table.hpp:89-90, only shard s's rows), row_trained (table.hpp:86),
+ * gather (table.hpp:77, table.cpp:158-163: one kernel + one copy; a row out of range ->
+ * MPZCH_ERANGE "embedding row out of range" before anything is copied). */
+mpzch_status mpzch_read_identity(const mpzch_table* t, uint64_t row, uint64_t* out);
+mpzch_status mpzch_copy_identities_range(const mpzch_table* t, uint64_t row0, uint64_t nrows,
+                                         uint64_t* host_out);
+mpzch_status mpzch_copy_metadata_range(const mpzch_table* t, uint64_t row0, uint64_t nrows,
+                                       uint64_t* host_out);
+mpzch_status mpzch_copy_trained_range(const mpzch_table* t, uint64_t row0, uint64_t nrows,
+                                      uint8_t* host_out);
+mpzch_status mpzch_gather(const mpzch_table* t, const uint64_t* rows, uint64_t n, float* host_out);
+/* MpzchTable::shard_config(s) (table.hpp:91, ShardConfig probe_core.hpp:11-18): capacity,
+ * max_probe, seed (shard_id = s); shard >= S -> MPZCH_ERANGE "shard index out of range". */
+mpzch_status mpzch_shard_config(const mpzch_table* t, uint32_t shard, uint64_t* capacity,
+                                uint32_t* max_probe, uint64_t* seed);
+
 /* ---- execution control / introspection */
 mpzch_status mpzch_set_path(mpzch_table* t, int path);
 mpzch_status mpzch_last_stats(const mpzch_table* t, mpzch_batch_stats* out);

@@ -9,6 +9,10 @@
 //   mpzch::MpzchTable (table.hpp:41-131)          mpzch_b200::MpzchTable  (HBM-resident)
 //   mpzch::process_batch (batch_engine.hpp:44)    mpzch_b200::process_batch
 //   mpzch::ProbeResult / Outcome (probe_core.hpp) mpzch_b200::ProbeResult / Outcome
+//   mpzch::dedup (batch_engine.hpp:35)             mpzch_b200::dedup  (on the device)
+//   mpzch::TableLayout / ShardConfig               mpzch_b200::TableLayout / ShardConfig
+//   mpzch::EmbeddingTable (embeddings())           mpzch_b200::EmbeddingsView (read view of HBM rows)
+//   mpzch::shard_of / make_metadata / mix64        same names (host arithmetic)
 //
 // Errors surface as the same std exception types with the same what() text.
 // The extra evicted-slot output of the batched remap is available through
@@ -58,6 +62,39 @@ struct IdBatch {
 
 enum class ExecMode { Serial, Parallel };  // accepted for signature parity; both are exact
 
+struct DedupResult {
+    std::vector<BatchEntry> uniques;     // first-occurrence order
+    std::vector<std::uint32_t> inverse;  // inverse[i] indexes uniques
+};
+
+// ShardConfig, proj/include/mpzch/probe_core.hpp:11-18
+struct ShardConfig {
+    std::uint64_t capacity = 0;
+    std::uint32_t max_probe = 0;
+    std::uint32_t shard_id = 0;
+    std::uint64_t seed = 0;
+};
+
+// TableLayout, proj/include/mpzch/shard_router.hpp:13-29
+struct TableLayout {
+    std::vector<std::uint64_t> shard_capacities;
+    std::vector<std::uint64_t> shard_offsets;  // exclusive prefix sums, num_shards + 1 entries
+    std::uint64_t seed = 0;
+    std::uint32_t num_shards() const { return static_cast<std::uint32_t>(shard_capacities.size()); }
+    std::uint64_t total_rows() const { return shard_offsets.back(); }
+};
+
+// mix64 (ids.hpp:35-43) and shard_of (shard_router.cpp:42-46), bit-identical host arithmetic
+inline constexpr std::uint64_t mix64(std::uint64_t id, std::uint64_t seed) {
+    std::uint64_t x = id ^ seed;
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ull;
+    x ^= x >> 33;
+    return x;
+}
+
 [[noreturn]] inline void rethrow(mpzch_status rc) {
     const std::string msg = mpzch_last_error();
     switch (rc) {
@@ -73,6 +110,35 @@ enum class ExecMode { Serial, Parallel };  // accepted for signature parity; bot
 
 inline void check(mpzch_status rc) {
     if (rc != MPZCH_OK) rethrow(rc);
+}
+
+inline void require_valid_id(Id id) {  // ids.hpp:25-31
+    if (id >> 63)
+        throw std::invalid_argument(id == kEmptySlot ? "id is the empty-slot sentinel"
+                                                     : "id exceeds the 63-bit ID space");
+}
+
+inline std::uint32_t shard_of(Id id, const TableLayout& layout) {
+    require_valid_id(id);
+    return static_cast<std::uint32_t>(mix64(id ^ 0xD1B54A32D192ED03ull, layout.seed) % layout.num_shards());
+}
+
+// dedup (batch_engine.hpp:35, batch_engine.cpp:133-139), run on `device`
+inline DedupResult dedup(std::span<const BatchEntry> entries, int device = 0) {
+    const std::size_t n = entries.size();
+    std::vector<std::uint64_t> ids(n), uids(n);
+    std::vector<std::uint32_t> feats(n), ufeats(n);
+    DedupResult r;
+    r.inverse.resize(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        ids[i] = entries[i].id;
+        feats[i] = entries[i].feature;
+    }
+    std::uint64_t u = 0;
+    check(mpzch_dedup(device, ids.data(), feats.data(), n, uids.data(), ufeats.data(), r.inverse.data(), &u));
+    r.uniques.resize(u);
+    for (std::uint64_t k = 0; k < u; ++k) r.uniques[k] = {uids[k], ufeats[k]};
+    return r;
 }
 
 struct TtlPolicy {
@@ -128,6 +194,62 @@ private:
     mpzch_policy c_{};
 };
 
+// make_metadata (eviction.cpp:20-30): TTL -> now + ttl(feature) (overflow_error), else now
+inline std::uint64_t make_metadata(const EvictionPolicy& policy, Timestamp now, FeatureOrdinal feature) {
+    if (policy.mode() != EvictionMode::Ttl) return now;
+    const std::uint64_t ttl = policy.ttl_config().ttl_for(feature);
+    if (ttl > ~std::uint64_t{0} - now) throw std::overflow_error("TTL expiry overflows the 64-bit timestamp range");
+    return now + ttl;
+}
+
+class MpzchTable;
+
+// Read view of a table's embedding rows (EmbeddingTable, proj/include/mpzch/embedding_store.hpp:
+// 21-64, as returned by MpzchTable::embeddings()): the rows stay in HBM; each call copies
+// what it returns.
+class EmbeddingsView {
+public:
+    EmbeddingsView(const mpzch_table* t, std::uint64_t rows, std::uint32_t dim) : t_(t), rows_(rows), dim_(dim) {}
+    std::uint64_t rows() const { return rows_; }
+    std::uint32_t dim() const { return dim_; }
+    bool trainable() const { return true; }
+    std::uint64_t weights_count() const { return rows_ * dim_; }
+    std::vector<float> gather(std::span<const std::uint64_t> rows) const {
+        std::vector<float> out(rows.size() * dim_);
+        check(mpzch_gather(t_, rows.data(), rows.size(), out.data()));
+        return out;
+    }
+    std::vector<float> row(std::uint64_t r) const {
+        if (r >= rows_) throw std::out_of_range("embedding row out of range");
+        std::vector<float> w(dim_);
+        check(mpzch_copy_weights(t_, r, 1, w.data()));
+        return w;
+    }
+    std::vector<float> momentum_row(std::uint64_t r) const {
+        if (r >= rows_) throw std::out_of_range("embedding row out of range");
+        std::vector<float> m(dim_);
+        check(mpzch_copy_momentum(t_, r, 1, m.data()));
+        return m;
+    }
+    bool trained(std::uint64_t r) const {
+        if (r >= rows_) throw std::out_of_range("embedding row out of range");
+        std::uint8_t v = 0;
+        check(mpzch_copy_trained_range(t_, r, 1, &v));
+        return v != 0;
+    }
+    // the whole weights array (weights_data() of the reference is a host pointer; here a copy)
+    std::vector<float> weights() const {
+        std::vector<float> w(weights_count());
+        if (!w.empty()) check(mpzch_copy_weights(t_, 0, rows_, w.data()));
+        return w;
+    }
+
+private:
+    const mpzch_table* t_;
+    std::uint64_t rows_;
+    std::uint32_t dim_;
+};
+
 struct TableConfig {
     std::vector<std::uint64_t> shard_capacities;
     std::uint32_t max_probe = 1;
@@ -164,6 +286,15 @@ public:
         caps_ = cfg.shard_capacities;
         offsets_.resize(caps_.size() + 1);
         check(mpzch_shard_layout(t_, nullptr, offsets_.data()));
+        layout_.shard_capacities = caps_;
+        layout_.shard_offsets = offsets_;
+        layout_.seed = cfg.seed;
+        for (std::uint32_t s = 0; s < caps_.size(); ++s) {
+            ShardConfig sc;
+            sc.shard_id = s;
+            check(mpzch_shard_config(t_, s, &sc.capacity, &sc.max_probe, &sc.seed));
+            shard_configs_.push_back(sc);
+        }
     }
     MpzchTable(const MpzchTable&) = delete;
     MpzchTable& operator=(const MpzchTable&) = delete;
@@ -207,25 +338,59 @@ public:
         return r;
     }
 
+    const TableLayout& layout() const { return layout_; }
+
+    const ShardConfig& shard_config(std::uint32_t shard) const {
+        if (shard >= shard_configs_.size()) throw std::out_of_range("shard index out of range");
+        return shard_configs_[shard];
+    }
+
+    // MpzchTable::process_shard_batch (table.hpp:71-73): the shard's serialized probe loop
+    void process_shard_batch(std::uint32_t shard, std::span<const Id> ids, std::span<const std::uint64_t> metas,
+                             Timestamp now, const EvictionPolicy& policy, std::span<ProbeResult> out) {
+        if (shard >= caps_.size()) throw std::out_of_range("shard index out of range");
+        if (out.size() != ids.size() || metas.size() != ids.size())
+            throw std::invalid_argument("batch spans disagree on length");
+        std::vector<std::uint64_t> s(ids.size());
+        std::vector<std::uint8_t> o(ids.size(), 0xff);
+        const mpzch_status rc = mpzch_process_shard_batch(t_, shard, ids.data(), metas.data(), ids.size(), now,
+                                                          policy.c_policy(), s.data(), o.data());
+        for (std::size_t i = 0; i < ids.size() && o[i] != 0xff; ++i)  // positions that took effect
+            out[i] = {s[i], o[i] == MPZCH_EVICTED, static_cast<Outcome>(o[i])};
+        check(rc);
+    }
+
+    // MpzchTable::reset_row (table.cpp:181-186)
+    void reset_row(std::uint64_t global_row) { check(mpzch_reset_row(t_, global_row)); }
+
+    // MpzchTable::state_equals (table.cpp:249-260), compared on the device
+    bool state_equals(const MpzchTable& other) const {
+        int eq = 0;
+        check(mpzch_state_equals(t_, other.t_, &eq));
+        return eq != 0;
+    }
+
+    EmbeddingsView embeddings() const { return EmbeddingsView(t_, dim_ ? total_rows() : 0, dim_); }
+
+    // identities(s) / metadata(s) (table.hpp:89-90): a copy of shard s's rows only
     std::vector<Id> identities(std::uint32_t shard) const {
         if (shard >= caps_.size()) throw std::out_of_range("shard index out of range");
-        std::vector<Id> all(total_rows());
-        check(mpzch_copy_identities(t_, all.data()));
-        return {all.begin() + offsets_[shard], all.begin() + offsets_[shard + 1]};
+        std::vector<Id> v(caps_[shard]);
+        check(mpzch_copy_identities_range(t_, offsets_[shard], caps_[shard], v.data()));
+        return v;
     }
 
     std::vector<std::uint64_t> metadata(std::uint32_t shard) const {
         if (shard >= caps_.size()) throw std::out_of_range("shard index out of range");
-        std::vector<std::uint64_t> all(total_rows());
-        check(mpzch_copy_metadata(t_, all.data()));
-        return {all.begin() + offsets_[shard], all.begin() + offsets_[shard + 1]};
+        std::vector<std::uint64_t> v(caps_[shard]);
+        check(mpzch_copy_metadata_range(t_, offsets_[shard], caps_[shard], v.data()));
+        return v;
     }
 
-    Id row_identity(std::uint64_t row) const {
-        if (row >= total_rows()) throw std::out_of_range("global row out of range");
-        std::vector<Id> all(total_rows());
-        check(mpzch_copy_identities(t_, all.data()));
-        return all[row];
+    Id row_identity(std::uint64_t row) const {  // one 8-byte copy
+        Id v = 0;
+        check(mpzch_read_identity(t_, row, &v));
+        return v;
     }
 
     std::vector<float> row(std::uint64_t r) const {
@@ -234,12 +399,10 @@ public:
         return w;
     }
 
-    // MpzchTable::gather (proj/src/table.cpp:158-163): row-major copy of the requested rows
+    // MpzchTable::gather (proj/src/table.cpp:158-163): one gather kernel + one copy
     std::vector<float> gather(std::span<const std::uint64_t> rows) const {
-        if (dim_ == 0) throw std::logic_error("table has no embedding payload (dim = 0)");
         std::vector<float> out(rows.size() * dim_);
-        for (std::size_t i = 0; i < rows.size(); ++i)
-            check(mpzch_copy_weights(t_, rows[i], 1, out.data() + i * dim_));
+        check(mpzch_gather(t_, rows.data(), rows.size(), out.data()));
         return out;
     }
 
@@ -250,11 +413,9 @@ public:
     }
 
     bool row_trained(std::uint64_t r) const {
-        if (dim_ == 0) throw std::logic_error("table has no embedding payload (dim = 0)");
-        std::vector<std::uint8_t> t(total_rows());
-        check(mpzch_copy_trained(t_, t.data()));
-        if (r >= t.size()) throw std::out_of_range("embedding row out of range");
-        return t[r] != 0;
+        std::uint8_t v = 0;
+        check(mpzch_copy_trained_range(t_, r, 1, &v));
+        return v != 0;
     }
 
     // MpzchTable::sgd_step (proj/src/table.cpp:174-179)
@@ -285,10 +446,14 @@ private:
         std::swap(dim_, o.dim_);
         std::swap(caps_, o.caps_);
         std::swap(offsets_, o.offsets_);
+        std::swap(layout_, o.layout_);
+        std::swap(shard_configs_, o.shard_configs_);
     }
     mpzch_table* t_ = nullptr;
     std::uint32_t dim_ = 0;
     std::vector<std::uint64_t> caps_, offsets_;
+    TableLayout layout_;
+    std::vector<ShardConfig> shard_configs_;
 };
 
 // ---- publish (proj/include/mpzch/publish.hpp): the images are built from HBM, CRC on the device

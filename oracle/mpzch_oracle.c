@@ -90,6 +90,11 @@ void orc_draw_row(float* dst, uint32_t dim, uint64_t row, uint64_t init_seed) {
     }
 }
 
+/* draw_row for n rows: dst[k * dim ...] = draw_row(rows[k]) */
+void orc_draw_rows(float* dst, uint32_t dim, const uint64_t* rows, uint64_t n, uint64_t init_seed) {
+    for (uint64_t k = 0; k < n; ++k) orc_draw_row(dst + k * dim, dim, rows[k], init_seed);
+}
+
 /* ---------------------------------------------------------------- table */
 
 struct orc_table {

@@ -63,6 +63,7 @@ void orc_distinct_ids(uint64_t seed, uint64_t start, uint64_t count, uint64_t* o
 uint64_t orc_home_slot(uint64_t id, uint64_t capacity, uint64_t seed);
 uint32_t orc_shard_of(uint64_t id, uint32_t num_shards, uint64_t seed);
 void orc_draw_row(float* dst, uint32_t dim, uint64_t row, uint64_t init_seed);
+void orc_draw_rows(float* dst, uint32_t dim, const uint64_t* rows, uint64_t n, uint64_t init_seed);
 
 /* table */
 int orc_table_create(const uint64_t* capacities, uint32_t num_shards, uint32_t max_probe,

@@ -96,12 +96,18 @@ def lib(kind: str = "port"):
         sig["serialize_delta"] = (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint32,
                                                  ctypes.c_uint64, _vp, ctypes.c_uint64, _u64p, _u64p])
         sig["draw_row"] = (None, [_vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64])
+        sig["draw_rows"] = (None, [_vp, ctypes.c_uint32, _vp, ctypes.c_uint64, ctypes.c_uint64])
         sig["splitmix_next"] = (ctypes.c_uint64, [_u64p])
     else:
         sig["delta_source_create"] = (ctypes.c_int, [_vp, ctypes.c_uint32])
         sig["delta_source_cut"] = (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _u64p])
         sig["set_threads"] = (None, [ctypes.c_int])
         sig["max_threads"] = (ctypes.c_int, [])
+        sig["process_batch_timed"] = (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, ctypes.c_uint64, _vp,
+                                                     _vp, ctypes.POINTER(ctypes.c_double)])
+        sig["prefill_distinct"] = (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64,
+                                                  ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                                  ctypes.c_int, ctypes.c_uint64])
     fns = {}
     for name, (res, args) in sig.items():
         f = getattr(L, p + name)
@@ -171,6 +177,24 @@ class OracleTable:
                                                keys.size, _ptr(keys), _ptr(vals), _ptr(slots),
                                                _ptr(oc), _ptr(ev), n, ctypes.byref(nev)))
         return slots, oc, ev[:nev.value].copy()
+
+    def process_batch_timed(self, ids, now, want_results=False):
+        """Disabled process_batch with steady_clock around the call alone (reference only,
+        proj/src/experiments.cpp:339-347).  Returns (seconds, slots, outcomes)."""
+        ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        slots = np.empty(ids.size, dtype=np.uint64) if want_results else None
+        oc = np.empty(ids.size, dtype=np.uint8) if want_results else None
+        sec = ctypes.c_double(0)
+        _raise(self.L, self.L["process_batch_timed"](self.h, _ptr(ids), ids.size, now, _ptr(slots),
+                                                     _ptr(oc), ctypes.byref(sec)))
+        return sec.value, slots, oc
+
+    def prefill_distinct(self, id_seed, start, count, now, chunk=1 << 24, mode=0, default_ttl=0):
+        """DistinctIdStream(id_seed).at([start, start+count)) at `now` under the policy (mode 0
+        Disabled, 1 TTL with default_ttl, 2 LRU; feature 0), through process_shard_batch with the
+        shards in parallel (reference only)."""
+        _raise(self.L, self.L["prefill_distinct"](self.h, id_seed, start, count, now, chunk, mode,
+                                                  default_ttl))
 
     def lookup(self, ids):
         ids = np.ascontiguousarray(ids, dtype=np.uint64)
@@ -293,6 +317,14 @@ def probe_readonly(id, identities, capacity, max_probe, seed, kind="port"):
     _raise(L, L["probe_readonly"](id, _ptr(I), capacity, max_probe, seed, ctypes.byref(s),
                                   ctypes.byref(o)))
     return s.value, o.value
+
+
+def draw_rows(dim, rows, init_seed):
+    """draw_row for every row of `rows` (closed form, embedding_store.cpp:12-18): [n, dim]."""
+    r = np.ascontiguousarray(rows, dtype=np.uint64)
+    out = np.empty((r.size, dim), dtype=np.float32)
+    lib("port")["draw_rows"](_ptr(out), dim, _ptr(r), r.size, init_seed)
+    return out
 
 
 def draw_row(dim, row, init_seed):

@@ -10,6 +10,7 @@
 // straight into the reference's code.
 #include <omp.h>
 
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -362,6 +363,85 @@ int ref_dirty_rows_since(const RefTable* t, std::uint64_t cursor, std::uint64_t*
         const std::vector<std::uint64_t> rows = t->table.dirty_rows_since(c);
         for (std::size_t i = 0; i < rows.size() && i < cap; ++i) out[i] = rows[i];
         *out_n = rows.size();
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+
+// Same-config CPU baseline (proj/src/experiments.cpp:335-347): process_batch is
+// timed with steady_clock around the call alone -- the IdBatch is packed before the clock
+// starts and the ProbeResults are unpacked after it stops; no evicted-list pass.
+int ref_process_batch_timed(RefTable* t, const std::uint64_t* ids, std::uint64_t n, std::uint64_t now,
+                            std::uint64_t* out_slots, std::uint8_t* out_outcomes, double* out_seconds) {
+    try {
+        const mpzch::EvictionPolicy policy = mpzch::EvictionPolicy::disabled();
+        mpzch::IdBatch batch;
+        batch.now = now;
+        batch.ids.resize(n);
+        for (std::uint64_t i = 0; i < n; ++i) batch.ids[i] = {ids[i], 0u};
+        const auto start = std::chrono::steady_clock::now();
+        const std::vector<mpzch::ProbeResult> r =
+            mpzch::process_batch(t->table, batch, policy, mpzch::ExecMode::Parallel);
+        const auto stop = std::chrono::steady_clock::now();
+        *out_seconds = std::chrono::duration<double>(stop - start).count();
+        if (out_slots)
+            for (std::uint64_t i = 0; i < n; ++i) out_slots[i] = r[i].slot;
+        if (out_outcomes)
+            for (std::uint64_t i = 0; i < n; ++i) out_outcomes[i] = static_cast<std::uint8_t>(r[i].outcome);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// Prefill with the distinct ids DistinctIdStream(id_seed).at([start, start + count)) under
+// the policy (mode 0 Disabled / 1 TTL default_ttl / 2 LRU, feature 0) at `now`, through the reference's per-shard entry MpzchTable::process_shard_batch
+// (table.cpp:112-148) with the shards in parallel.  For distinct ids this is exactly what
+// process_batch does (batch_engine.cpp:141-221: dedup keeps every id, the stable partition keeps
+// each shard's ids in batch order, then process_shard_batch per shard) without its serial
+// dedup / partition / scatter, so a 2^30-row table fills in a fraction of the time.
+int ref_prefill_distinct(RefTable* t, std::uint64_t id_seed, std::uint64_t start, std::uint64_t count,
+                         std::uint64_t now, std::uint64_t chunk, int mode, std::uint64_t default_ttl) {
+    try {
+        const mpzch::EvictionPolicy policy = make_policy(mode, default_ttl, 0, nullptr, nullptr);
+        const std::uint64_t meta = mpzch::make_metadata(policy, now, 0);  // eviction.cpp:20-30
+        const std::uint32_t S = t->table.num_shards();
+        const mpzch::TableLayout& layout = t->table.layout();
+        const mpzch::DistinctIdStream stream(id_seed);
+        if (chunk == 0) chunk = 1ull << 24;
+        if (S > 256) throw std::invalid_argument("prefill_distinct supports at most 256 shards");
+        std::vector<mpzch::Id> all(chunk);
+        std::vector<std::uint8_t> owner(chunk);
+        std::vector<std::vector<mpzch::Id>> ids(S);
+        std::vector<std::vector<std::uint64_t>> metas(S);
+        std::vector<std::vector<mpzch::ProbeResult>> out(S);
+        for (std::uint64_t a = start; a < start + count; a += chunk) {
+            const std::uint64_t m = std::min(start + count, a + chunk) - a;
+#pragma omp parallel for schedule(static)
+            for (std::int64_t i = 0; i < static_cast<std::int64_t>(m); ++i) {
+                all[i] = stream.at(a + i);
+                owner[i] = static_cast<std::uint8_t>(mpzch::shard_of(all[i], layout));
+            }
+            int failed = 0;
+#pragma omp parallel for schedule(dynamic) reduction(| : failed)
+            for (std::int64_t s = 0; s < static_cast<std::int64_t>(S); ++s) {
+                try {
+                    auto& v = ids[s];
+                    v.clear();
+                    for (std::uint64_t i = 0; i < m; ++i)
+                        if (owner[i] == static_cast<std::uint8_t>(s)) v.push_back(all[i]);
+                    metas[s].assign(v.size(), meta);
+                    out[s].resize(v.size());
+                    t->table.process_shard_batch(static_cast<std::uint32_t>(s), v, metas[s], now, policy,
+                                                 out[s]);
+                } catch (...) {
+                    failed = 1;
+                }
+            }
+            if (failed) throw std::runtime_error("prefill failed");
+        }
         return 0;
     } catch (...) {
         return map_exception();

@@ -192,6 +192,19 @@ _SIGS = {
     "mpzch_last_stats": (ctypes.c_int, [_vp, ctypes.POINTER(_Stats)]),
     "mpzch_lookup_device_async": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _vp, _vp, _vp, _u64p]),
     "mpzch_kernel_launches": (ctypes.c_uint64, [_vp]),
+    "mpzch_process_shard_batch": (ctypes.c_int, [_vp, ctypes.c_uint32, _vp, _vp, ctypes.c_uint64,
+                                                 ctypes.c_uint64, ctypes.POINTER(_Policy), _vp, _vp]),
+    "mpzch_dedup": (ctypes.c_int, [ctypes.c_int, _vp, _vp, ctypes.c_uint64, _vp, _vp, _vp, _u64p]),
+    "mpzch_dedup_device": (ctypes.c_int, [ctypes.c_int, _vp, _vp, ctypes.c_uint64, _vp, _vp, _vp,
+                                          _u64p, _vp]),
+    "mpzch_reset_row": (ctypes.c_int, [_vp, ctypes.c_uint64]),
+    "mpzch_state_equals": (ctypes.c_int, [_vp, _vp, ctypes.POINTER(ctypes.c_int)]),
+    "mpzch_read_identity": (ctypes.c_int, [_vp, ctypes.c_uint64, _u64p]),
+    "mpzch_copy_identities_range": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, _vp]),
+    "mpzch_copy_metadata_range": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, _vp]),
+    "mpzch_copy_trained_range": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint64, _vp]),
+    "mpzch_gather": (ctypes.c_int, [_vp, _vp, ctypes.c_uint64, _vp]),
+    "mpzch_shard_config": (ctypes.c_int, [_vp, ctypes.c_uint32, _u64p, _u32p, _u64p]),
     "mpzch_last_error": (ctypes.c_char_p, []),
     "mpzch_build_info": (ctypes.c_char_p, []),
 }
@@ -562,6 +575,55 @@ class MpzchTable:
         return slot.value, oc.value
 
     # ---- state (parity) ------------------------------------------------------------------
+    def process_shard_batch(self, shard: int, ids, metas, now: int, policy: EvictionPolicy):
+        """MpzchTable::process_shard_batch (table.cpp:112-148): shard's positions in order, each
+        with its own metadata word.  Returns (slots, outcomes); on an invalid id / metadata word
+        the exception carries .partial = the results of the positions before it."""
+        ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        metas = np.ascontiguousarray(metas, dtype=np.uint64)
+        if metas.size != ids.size:
+            raise InvalidArgument("batch spans disagree on length")
+        slots = np.zeros(ids.size, dtype=np.uint64)
+        oc = np.full(ids.size, 0xff, dtype=np.uint8)
+        rc = self._lib.mpzch_process_shard_batch(self._h, shard, _ptr(ids), _ptr(metas), ids.size,
+                                                 now, ctypes.byref(policy._c), _ptr(slots), _ptr(oc))
+        if rc:
+            k = int(np.argmax(oc == 0xff)) if (oc == 0xff).any() else ids.size
+            try:
+                _check(rc)
+            except MpzchError as e:
+                e.partial = (slots[:k], oc[:k])
+                raise
+        return slots, oc
+
+    def reset_row(self, row: int):
+        """MpzchTable::reset_row (table.cpp:181-186)."""
+        _check(self._lib.mpzch_reset_row(self._h, row))
+
+    def state_equals(self, other: "MpzchTable") -> bool:
+        """MpzchTable::state_equals (table.cpp:249-260), compared on the device."""
+        v = ctypes.c_int(0)
+        _check(self._lib.mpzch_state_equals(self._h, other._h, ctypes.byref(v)))
+        return bool(v.value)
+
+    def row_identity(self, row: int) -> int:
+        v = ctypes.c_uint64(0)
+        _check(self._lib.mpzch_read_identity(self._h, row, ctypes.byref(v)))
+        return v.value
+
+    def gather(self, rows) -> np.ndarray:
+        """MpzchTable::gather (table.cpp:158-163): one gather kernel, one copy."""
+        r = np.ascontiguousarray(rows, dtype=np.uint64)
+        out = np.empty((r.size, max(self.dim, 1)), dtype=np.float32)
+        _check(self._lib.mpzch_gather(self._h, _ptr(r), r.size, _ptr(out)))
+        return out
+
+    def shard_config(self, shard: int) -> dict:
+        cap, P, seed = ctypes.c_uint64(0), ctypes.c_uint32(0), ctypes.c_uint64(0)
+        _check(self._lib.mpzch_shard_config(self._h, shard, ctypes.byref(cap), ctypes.byref(P),
+                                            ctypes.byref(seed)))
+        return {"capacity": cap.value, "max_probe": P.value, "shard_id": shard, "seed": seed.value}
+
     def identities_all(self) -> np.ndarray:
         """identity words of the held rows [row_lo, row_hi) (all rows unless sharded)."""
         out = np.empty(self.held_rows, dtype=np.uint64)
@@ -798,6 +860,21 @@ def parse_delta(image: bytes) -> dict:
                 rows=body[:, :8].copy().view(np.uint64).reshape(-1),
                 identities=body[:, 8:16].copy().view(np.uint64).reshape(-1),
                 weights=body[:, 16:].copy().view(np.float32).reshape(count, dim))
+
+
+def dedup(ids, features=None, device: int = 0):
+    """dedup (batch_engine.cpp:79-108, 133-139) on `device`: (unique ids, unique features,
+    inverse u32[n]) in first-occurrence order of (id, feature)."""
+    lib = load_library()
+    ids = np.ascontiguousarray(ids, dtype=np.uint64)
+    n = ids.size
+    f = None if features is None else np.ascontiguousarray(features, dtype=np.uint32)
+    uids = np.empty(max(n, 1), dtype=np.uint64)
+    uf = np.empty(max(n, 1), dtype=np.uint32)
+    inv = np.empty(max(n, 1), dtype=np.uint32)
+    u = ctypes.c_uint64(0)
+    _check(lib.mpzch_dedup(device, _ptr(ids), _ptr(f), n, _ptr(uids), _ptr(uf), _ptr(inv), ctypes.byref(u)))
+    return uids[:u.value].copy(), uf[:u.value].copy(), inv[:n].copy()
 
 
 def process_batch(table: MpzchTable, ids, now: int, policy: EvictionPolicy, features=None):

@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "compact.cuh"
+#include "ordered_probe.cuh"
 #include "table.hpp"
 
 namespace mpzch_b200 {
@@ -144,7 +145,6 @@ __global__ void __launch_bounds__(256) k_ordered(TableDev t, BatchCounters* ctr,
     const unsigned u = ctr->entry_count;
     const ShardDev sd = t.shards[shard];
     const uint64_t cap = sd.cap.d, base = sd.offset;
-    const uint32_t P = t.P;
     for (unsigned k0 = 0; k0 < u; k0 += 32) {
         const unsigned kk = k0 + lane;
         unsigned mine = __ballot_sync(0xffffffffu, kk < u && ushard[kk] == shard && (!todo || todo[kk]));
@@ -154,68 +154,9 @@ __global__ void __launch_bounds__(256) k_ordered(TableDev t, BatchCounters* ctr,
             const uint64_t id = ids[upos[k]];
             const uint64_t meta_in = umeta[k];
             const uint64_t h = home_of(id, sd, t.seed);
-            // Pass 1: discovery (probe_core.cpp:78-86)
-            bool exists = false;
-            for (uint32_t c = 0; c < P; c += 32) {
-                const uint32_t off = c + lane;
-                bool hit = false;
-                if (off < P) {
-                    uint64_t x = h + off;
-                    x = x >= cap ? x - cap : x;
-                    hit = ld_cg(t.ident + base + x) == id;
-                }
-                if (__ballot_sync(0xffffffffu, hit)) { exists = true; break; }
-            }
-            // Pass 2: update / insert / evict (probe_core.cpp:89-121)
-            uint8_t oc = kCollision;
-            uint64_t gslot = base + h;
-            bool decided = false;
-            uint64_t best_m = 0;
-            uint32_t best_off = kNone32;
-            for (uint32_t c = 0; c < P && !decided; c += 32) {
-                const uint32_t off = c + lane;
-                const bool valid = off < P;
-                uint64_t g = 0, v = 0, m = 0;
-                if (valid) {
-                    uint64_t x = h + off;
-                    x = x >= cap ? x - cap : x;
-                    g = base + x;
-                    v = ld_cg(t.ident + g);
-                    if (MODE != kModeDisabled) m = ld_cg(t.meta + g);
-                }
-                const bool is_match = valid && v == id;
-                const bool is_empty = valid && v == kEmpty;
-                const bool is_exp = valid && MODE == kModeTtl && !exists && !is_match && !is_empty &&
-                                    m < now;
-                const unsigned stop = __ballot_sync(0xffffffffu, is_match || is_empty || is_exp);
-                if (stop) {
-                    const int src = __ffs(stop) - 1;
-                    const uint64_t gs = __shfl_sync(0xffffffffu, g, src);
-                    const int kind = __shfl_sync(0xffffffffu, is_match ? 0 : (is_empty ? 1 : 2), src);
-                    gslot = gs;
-                    oc = kind == 0 ? kFound : (kind == 1 ? kInserted : kEvicted);
-                    decided = true;
-                } else if (MODE == kModeLru && !exists) {
-                    // first strict minimum over the window, ties -> lowest offset
-                    uint64_t bm = valid ? m : ~0ull;
-                    uint32_t bo = valid ? off : kNone32;
-                    for (int o = 16; o; o >>= 1) {
-                        const uint64_t om = __shfl_xor_sync(0xffffffffu, bm, o);
-                        const uint32_t oo = __shfl_xor_sync(0xffffffffu, bo, o);
-                        if (om < bm || (om == bm && oo < bo)) { bm = om; bo = oo; }
-                    }
-                    if (bo != kNone32 && (best_off == kNone32 || bm < best_m)) {
-                        best_m = bm;
-                        best_off = bo;
-                    }
-                }
-            }
-            if (!decided && MODE == kModeLru && best_off != kNone32) {
-                uint64_t x = h + best_off;
-                x = x >= cap ? x - cap : x;
-                gslot = base + x;
-                oc = kEvicted;  // LRU fallback, probe_core.cpp:125-129
-            }
+            uint64_t gslot;
+            uint8_t oc;
+            two_pass_probe<MODE>(t, base, cap, h, id, now, lane, gslot, oc);
             if (lane == 0) {
                 if (oc == kInserted || oc == kEvicted) t.ident[gslot] = id;
                 t.meta[gslot] = meta_in;  // Found refresh / insert / evict / Collision at home

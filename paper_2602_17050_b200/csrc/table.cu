@@ -1481,4 +1481,258 @@ mpzch_status mpzch_last_stats(const mpzch_table* t, mpzch_batch_stats* out) {
 
 uint64_t mpzch_kernel_launches(const mpzch_table* t) { return t && t->t ? t->t->launches : 0; }
 
+
+// ---- the rest of the kept MpzchTable / batch_engine surface (csrc/surface.cu)
+
+mpzch_status mpzch_process_shard_batch(mpzch_table* t, uint32_t shard, const uint64_t* ids,
+                                       const uint64_t* metas, uint64_t n, uint64_t now,
+                                       const mpzch_policy* policy, uint64_t* out_slots, uint8_t* out_oc) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        const Policy pol = parse_policy(policy);
+        // table.cpp:116-119
+        if (shard >= T.S) throw Error{MPZCH_ERANGE, "shard index out of range"};
+        if (shard < T.shard_lo || shard >= T.shard_hi)
+            throw Error{MPZCH_ERANGE, "shard is not held by this handle"};
+        if (n == 0) return;
+        DeviceGuard g(T.device);
+        cudaStream_t st = T.stream;
+        order_after_last_batch(T, st);
+        T.sb_buf.reserve(n * 33 + 64);
+        uint8_t* b = T.sb_buf.as<uint8_t>();
+        uint64_t* d_ids = (uint64_t*)b;
+        uint64_t* d_metas = d_ids + n;
+        uint64_t* d_slots = d_metas + n;
+        uint64_t* d_reset = d_slots + n;
+        unsigned long long* d_st = (unsigned long long*)(d_reset + n);
+        unsigned* d_rc = (unsigned*)(d_st + 3);
+        uint8_t* d_oc = (uint8_t*)(d_st + 4);
+        MPZCH_CUDA(cudaMemcpyAsync(d_ids, ids, n * 8, cudaMemcpyHostToDevice, st));
+        MPZCH_CUDA(cudaMemcpyAsync(d_metas, metas, n * 8, cudaMemcpyHostToDevice, st));
+        MPZCH_CUDA(cudaMemsetAsync(d_st, 0xff, 8, st));
+        launch_shard_batch(T, shard, pol.mode, d_ids, d_metas, n, now, d_slots, d_oc, d_reset, d_rc, d_st, st);
+        if (T.dim) launch_reset_rows(T, d_reset, d_rc, st);
+        MPZCH_CUDA(cudaGetLastError());
+        unsigned long long h_st[3] = {0, 0, 0};
+        MPZCH_CUDA(cudaMemcpyAsync(h_st, d_st, 24, cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaStreamSynchronize(st));
+        // the positions before a failing one took effect and have their results (out[k] is
+        // written inside the reference's loop before the next lookup_or_insert can throw)
+        const uint64_t done = h_st[0] == ~0ull ? n : h_st[0];
+        if (done) {
+            MPZCH_CUDA(cudaMemcpyAsync(out_slots, d_slots, done * 8, cudaMemcpyDeviceToHost, st));
+            MPZCH_CUDA(cudaMemcpyAsync(out_oc, d_oc, done, cudaMemcpyDeviceToHost, st));
+            MPZCH_CUDA(cudaStreamSynchronize(st));
+        }
+        if (h_st[0] != ~0ull) {
+            if (h_st[1] == 1) require_valid_id(h_st[2]);
+            throw Error{MPZCH_EINVAL, pol.mode == kModeTtl ? "TTL metadata must be an expiry in the future"
+                                                           : "non-TTL metadata must equal the current timestamp"};
+        }
+    });
+}
+
+static void dedup_common(const uint64_t* d_ids, const uint32_t* d_feats, uint64_t n, uint64_t* d_uids,
+                         uint32_t* d_ufeats, uint32_t* d_inverse, uint64_t* out_u, cudaStream_t st) {
+    uint64_t bad = ~0ull;
+    const uint64_t u = run_dedup(d_ids, d_feats, n, d_uids, d_ufeats, d_inverse, &bad, st);
+    if (bad != ~0ull) throw Error{MPZCH_EINVAL, "invalid id at batch position " + std::to_string(bad)};
+    *out_u = u;
+}
+
+mpzch_status mpzch_dedup(int device, const uint64_t* ids, const uint32_t* features, uint64_t n,
+                         uint64_t* out_unique_ids, uint32_t* out_unique_features, uint32_t* out_inverse,
+                         uint64_t* out_u) {
+    return guarded([&] {
+        if (n > 0xffffffffull) throw Error{MPZCH_ELENGTH, "batch exceeds 2^32 - 1 positions"};
+        *out_u = 0;
+        if (n == 0) return;
+        DeviceGuard g(device);
+        cudaStream_t st = nullptr;
+        MPZCH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        struct StreamGuard {
+            cudaStream_t s;
+            ~StreamGuard() { cudaStreamDestroy(s); }
+        } sg{st};
+        uint8_t* b = nullptr;
+        MPZCH_CUDA(cudaMallocAsync((void**)&b, n * 28, st));
+        struct FreeGuard {
+            uint8_t* p;
+            cudaStream_t s;
+            ~FreeGuard() { cudaFreeAsync(p, s); cudaStreamSynchronize(s); }
+        } fg{b, st};
+        uint64_t* d_ids = (uint64_t*)b;
+        uint64_t* d_uids = d_ids + n;
+        uint32_t* d_feats = (uint32_t*)(d_uids + n);
+        uint32_t* d_ufeats = d_feats + n;
+        uint32_t* d_inv = d_ufeats + n;
+        MPZCH_CUDA(cudaMemcpyAsync(d_ids, ids, n * 8, cudaMemcpyHostToDevice, st));
+        if (features) MPZCH_CUDA(cudaMemcpyAsync(d_feats, features, n * 4, cudaMemcpyHostToDevice, st));
+        uint64_t u = 0;
+        dedup_common(d_ids, features ? d_feats : nullptr, n, d_uids, d_ufeats, d_inv, &u, st);
+        MPZCH_CUDA(cudaMemcpyAsync(out_unique_ids, d_uids, u * 8, cudaMemcpyDeviceToHost, st));
+        if (out_unique_features)
+            MPZCH_CUDA(cudaMemcpyAsync(out_unique_features, d_ufeats, u * 4, cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaMemcpyAsync(out_inverse, d_inv, n * 4, cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaStreamSynchronize(st));
+        *out_u = u;
+    });
+}
+
+mpzch_status mpzch_dedup_device(int device, const uint64_t* ids, const uint32_t* features, uint64_t n,
+                                uint64_t* unique_ids, uint32_t* unique_features, uint32_t* inverse,
+                                uint64_t* out_u, void* stream) {
+    return guarded([&] {
+        if (n > 0xffffffffull) throw Error{MPZCH_ELENGTH, "batch exceeds 2^32 - 1 positions"};
+        *out_u = 0;
+        if (n == 0) return;
+        DeviceGuard g(device);
+        dedup_common(ids, features, n, unique_ids, unique_features, inverse, out_u, (cudaStream_t)stream);
+    });
+}
+
+mpzch_status mpzch_reset_row(mpzch_table* t, uint64_t row) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        check_rows(T, row, 1);  // check_embeddings, then check_row (table.cpp:181-186)
+        DeviceGuard g(T.device);
+        cudaStream_t st = T.stream;
+        order_after_last_batch(T, st);
+        T.sb_buf.reserve(64);
+        uint64_t* d = T.sb_buf.as<uint64_t>();
+        const uint64_t h[2] = {row, 1};  // the row, then the list length (as a u32 in word 1)
+        MPZCH_CUDA(cudaMemcpyAsync(d, h, 16, cudaMemcpyHostToDevice, st));
+        launch_reset_rows(T, d, (const unsigned*)(d + 1), st);
+        MPZCH_CUDA(cudaMemcpyAsync(T.dev.row_gen + row, &T.gen_clock, 8, cudaMemcpyHostToDevice, st));  // touch_row
+        MPZCH_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+mpzch_status mpzch_state_equals(const mpzch_table* a, const mpzch_table* b, int* out_equal) {
+    if (!a || !a->t || !b || !b->t) {
+        g_last_error = "null table handle";
+        return MPZCH_EINVAL;
+    }
+    return guarded([&] {
+        const Table& A = *a->t;
+        const Table& B = *b->t;
+        *out_equal = 0;
+        // table.cpp:249-260: capacities, dim, identities of every shard, weights (bitwise)
+        if (A.caps != B.caps || A.dim != B.dim) return;
+        if (A.held_rows() != A.total || B.held_rows() != B.total)
+            throw Error{MPZCH_EINVAL, "state_equals needs handles that hold every shard"};
+        auto same = [&](const void* pa, const void* pb, uint64_t bytes) {
+            if (!bytes) return true;
+            DeviceGuard g(A.device);
+            MPZCH_CUDA(cudaStreamSynchronize(A.stream));
+            if (A.device == B.device) return run_words_equal(pa, pb, bytes, A.stream);
+            {
+                DeviceGuard gb(B.device);
+                MPZCH_CUDA(cudaStreamSynchronize(B.stream));
+            }
+            const uint64_t chunk = 256ull << 20;  // B's bytes staged on A's device
+            void* tmp = nullptr;
+            MPZCH_CUDA(cudaMalloc(&tmp, std::min(chunk, bytes)));
+            bool eq = true;
+            for (uint64_t o = 0; o < bytes && eq; o += chunk) {
+                const uint64_t c = std::min(chunk, bytes - o);
+                MPZCH_CUDA(cudaMemcpyPeer(tmp, A.device, (const uint8_t*)pb + o, B.device, c));
+                eq = run_words_equal((const uint8_t*)pa + o, tmp, c, A.stream);
+            }
+            cudaFree(tmp);
+            return eq;
+        };
+        if (!same(A.ident + (A.row_lo - A.row_base), B.ident + (B.row_lo - B.row_base), A.total * 8)) return;
+        if (A.dim && !same(A.dev.weights, B.dev.weights, A.total * A.dim * 4)) return;
+        *out_equal = 1;
+    });
+}
+
+mpzch_status mpzch_read_identity(const mpzch_table* t, uint64_t row, uint64_t* out) {
+    CHECK_T(t);
+    return guarded([&] {
+        const Table& T = *t->t;
+        if (row >= T.total) throw Error{MPZCH_ERANGE, "global row out of range"};  // from_global
+        if (row < T.row_lo || row >= T.row_hi) throw Error{MPZCH_ERANGE, "row is not held by this handle"};
+        DeviceGuard g(T.device);
+        MPZCH_CUDA(cudaStreamSynchronize(T.stream));
+        MPZCH_CUDA(cudaMemcpy(out, T.dev.ident + row, 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+static void check_held_range(const Table& T, uint64_t row0, uint64_t nrows) {
+    if (row0 < T.row_lo || row0 > T.row_hi || nrows > T.row_hi - row0)
+        throw Error{MPZCH_ERANGE, "row range is not held by this handle"};
+}
+
+mpzch_status mpzch_copy_identities_range(const mpzch_table* t, uint64_t row0, uint64_t nrows, uint64_t* out) {
+    CHECK_T(t);
+    return guarded([&] {
+        const Table& T = *t->t;
+        check_held_range(T, row0, nrows);
+        DeviceGuard g(T.device);
+        MPZCH_CUDA(cudaStreamSynchronize(T.stream));
+        if (nrows) MPZCH_CUDA(cudaMemcpy(out, T.dev.ident + row0, nrows * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+mpzch_status mpzch_copy_metadata_range(const mpzch_table* t, uint64_t row0, uint64_t nrows, uint64_t* out) {
+    CHECK_T(t);
+    return guarded([&] {
+        const Table& T = *t->t;
+        check_held_range(T, row0, nrows);
+        DeviceGuard g(T.device);
+        MPZCH_CUDA(cudaStreamSynchronize(T.stream));
+        if (nrows) MPZCH_CUDA(cudaMemcpy(out, T.dev.meta + row0, nrows * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+mpzch_status mpzch_copy_trained_range(const mpzch_table* t, uint64_t row0, uint64_t nrows, uint8_t* out) {
+    CHECK_T(t);
+    return guarded([&] {
+        const Table& T = *t->t;
+        check_rows(T, row0, nrows);
+        DeviceGuard g(T.device);
+        MPZCH_CUDA(cudaStreamSynchronize(T.stream));
+        if (nrows) MPZCH_CUDA(cudaMemcpy(out, T.dev.trained + row0, nrows, cudaMemcpyDeviceToHost));
+    });
+}
+
+mpzch_status mpzch_gather(const mpzch_table* t, const uint64_t* rows, uint64_t n, float* out) {
+    CHECK_T(t);
+    return guarded([&] {
+        Table& T = *t->t;
+        check_rows(T, T.row_lo, 0);
+        for (uint64_t i = 0; i < n; ++i)  // embedding_store.cpp:97-98, first bad row
+            if (rows[i] < T.row_lo || rows[i] >= T.row_hi) throw Error{MPZCH_ERANGE, "embedding row out of range"};
+        if (n == 0) return;
+        DeviceGuard g(T.device);
+        cudaStream_t st = T.stream;
+        order_after_last_batch(T, st);
+        T.sb_buf.reserve(n * 8 + n * T.dim * 4);
+        uint64_t* d_rows = T.sb_buf.as<uint64_t>();
+        float* d_out = (float*)(d_rows + n);
+        MPZCH_CUDA(cudaMemcpyAsync(d_rows, rows, n * 8, cudaMemcpyHostToDevice, st));
+        run_gather_weights(T, d_rows, n, d_out, st);
+        ++T.launches;
+        MPZCH_CUDA(cudaGetLastError());
+        MPZCH_CUDA(cudaMemcpyAsync(out, d_out, n * T.dim * 4, cudaMemcpyDeviceToHost, st));
+        MPZCH_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+mpzch_status mpzch_shard_config(const mpzch_table* t, uint32_t shard, uint64_t* capacity, uint32_t* max_probe,
+                                uint64_t* seed) {
+    CHECK_T(t);
+    return guarded([&] {
+        const Table& T = *t->t;
+        if (shard >= T.S) throw Error{MPZCH_ERANGE, "shard index out of range"};  // table.cpp:241-244
+        if (capacity) *capacity = T.caps[shard];
+        if (max_probe) *max_probe = T.P;
+        if (seed) *seed = T.seed;
+    });
+}
+
 }  // extern "C"

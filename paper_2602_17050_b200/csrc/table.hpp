@@ -164,6 +164,7 @@ public:
     // synchronous lookups (mpzch_lookup[_device], lookup_gather): their own hand-over list and
     // a lock, so concurrent const lookups on one handle never share scratch or the error word
     DevBuf s_ldefer, l_ids, l_oslot, l_ooc;
+    DevBuf sb_buf;  // process_shard_batch / reset_row / gather staging
     std::mutex lookup_mu;
     DevBuf s_tent;                                   // id table: 64-byte entries
     uint64_t tcap = 0;                               // allocated id-table capacity (pow2)
@@ -276,6 +277,17 @@ void run_return_scatter(uint64_t n_recv, const uint64_t* slots, const uint8_t* o
                         const uint32_t* src, uint32_t parts, const uint64_t* recv_offset,
                         const uint64_t* slots_to, const uint64_t* oc_to, const uint64_t* mark_to,
                         cudaStream_t st);
+
+// surface.cu: process_shard_batch (one warp, positions in order; st = {first failing position,
+// kind 1 id / 2 metadata, id}), dedup (returns the unique count; *bad_pos = first invalid
+// position or ~0; synchronous), state_equals word compare (synchronous), row gather
+void launch_shard_batch(Table& t, uint32_t shard, int mode, const uint64_t* ids, const uint64_t* metas,
+                        uint64_t n, uint64_t now, uint64_t* out_slots, uint8_t* out_oc, uint64_t* reset_rows,
+                        unsigned* reset_count, unsigned long long* st, cudaStream_t s);
+uint64_t run_dedup(const uint64_t* ids, const uint32_t* feats, uint64_t n, uint64_t* uids, uint32_t* ufeats,
+                   uint32_t* inverse, uint64_t* bad_pos, cudaStream_t st);
+bool run_words_equal(const void* a, const void* b, uint64_t bytes, cudaStream_t st);
+void run_gather_weights(const Table& t, const uint64_t* rows, uint64_t n, float* out, cudaStream_t st);
 
 inline unsigned grid_for(uint64_t n, unsigned block, unsigned max_blocks = 148u * 32u) {
     uint64_t g = (n + block - 1) / block;

@@ -37,6 +37,13 @@ struct Ref {
     using Delta = mpzch::DeltaSource;
     static std::vector<std::uint8_t> snap(const Table& t) { return mpzch::serialize_snapshot(t); }
     static std::uint32_t cks(const std::vector<std::uint8_t>& b) { return mpzch::snapshot_checksum(b); }
+    static std::uint32_t shard(std::uint64_t id, const mpzch::TableLayout& l) { return mpzch::shard_of(id, l); }
+    static std::uint64_t meta(const Policy& p, std::uint64_t now, std::uint32_t f) {
+        return mpzch::make_metadata(p, now, f);
+    }
+    static auto dd(const std::vector<mpzch::BatchEntry>& e) { return mpzch::dedup(e); }
+    using Result = mpzch::ProbeResult;
+    using Entry = mpzch::BatchEntry;
 };
 
 struct Gpu {
@@ -51,6 +58,15 @@ struct Gpu {
     using Delta = mpzch_b200::DeltaSource;
     static std::vector<std::uint8_t> snap(const Table& t) { return mpzch_b200::serialize_snapshot(t); }
     static std::uint32_t cks(const std::vector<std::uint8_t>& b) { return mpzch_b200::snapshot_checksum(b); }
+    static std::uint32_t shard(std::uint64_t id, const mpzch_b200::TableLayout& l) {
+        return mpzch_b200::shard_of(id, l);
+    }
+    static std::uint64_t meta(const Policy& p, std::uint64_t now, std::uint32_t f) {
+        return mpzch_b200::make_metadata(p, now, f);
+    }
+    static auto dd(const std::vector<mpzch_b200::BatchEntry>& e) { return mpzch_b200::dedup(e); }
+    using Result = mpzch_b200::ProbeResult;
+    using Entry = mpzch_b200::BatchEntry;
 };
 
 struct Trace {
@@ -156,6 +172,163 @@ Trace run(std::uint64_t seed, int mode) {
     return tr;
 }
 
+// The rest of the kept surface: layout() / shard_config(s), dedup, the per-shard
+// entry process_shard_batch (repeated ids probe again; a bad metadata word stops the loop after
+// the earlier positions took effect), reset_row, embeddings(), state_equals.
+template <class NS>
+Trace run_surface(std::uint64_t seed, int mode) {
+    Trace tr;
+    mpzch::SplitMix64 rng(seed);
+    typename NS::Config cfg = NS::Config::even(300 + rng.next_below(700), 1 + rng.next_below(5),
+                                               2 + rng.next_below(12), rng.next(), 8, rng.next());
+    typename NS::Table table(cfg), twin(cfg);
+    typename NS::Ttl ttl;
+    ttl.default_ttl_seconds = 9;
+    ttl.per_feature_ttl = {{2, 3}};
+    const typename NS::Policy pol = mode == 0   ? NS::Policy::disabled()
+                                    : mode == 1 ? NS::Policy::lru()
+                                                : NS::Policy::ttl(ttl);
+    const auto& L = table.layout();
+    tr.out.push_back(L.num_shards());
+    tr.out.push_back(L.total_rows());
+    tr.out.push_back(L.seed);
+    for (auto v : L.shard_offsets) tr.out.push_back(v);
+    for (std::uint32_t s = 0; s < table.num_shards(); ++s) {
+        const auto& sc = table.shard_config(s);
+        tr.out.push_back(sc.capacity);
+        tr.out.push_back(sc.max_probe);
+        tr.out.push_back(sc.shard_id);
+        tr.out.push_back(sc.seed);
+    }
+    try {
+        (void)table.shard_config(table.num_shards());
+    } catch (const std::out_of_range& e) {
+        tr.error += std::string(e.what()) + "|";
+    }
+    mpzch::DistinctIdStream ids(rng.next());
+    // dedup on (id, feature) with its inverse, then its first-bad-position error
+    std::vector<typename NS::Entry> entries;
+    for (int k = 0; k < 300; ++k)
+        entries.push_back({ids.at(rng.next_below(120)), static_cast<std::uint32_t>(rng.next_below(3))});
+    const auto d = NS::dd(entries);
+    tr.out.push_back(d.uniques.size());
+    for (const auto& u : d.uniques) {
+        tr.out.push_back(u.id);
+        tr.out.push_back(u.feature);
+    }
+    for (auto i : d.inverse) tr.out.push_back(i);
+    entries[17].id = ~0ull;
+    entries[41].id = 1ull << 63;
+    try {
+        (void)NS::dd(entries);
+    } catch (const std::invalid_argument& e) {
+        tr.error += std::string(e.what()) + "|";
+    }
+    // per-shard batches in several rounds (ids routed with shard_of, repeats included)
+    std::uint64_t now = 1;
+    std::vector<std::uint64_t> rows;
+    for (int round = 0; round < 6; ++round) {
+        now += 1 + rng.next_below(4);
+        for (std::uint32_t s = 0; s < table.num_shards(); ++s) {
+            std::vector<std::uint64_t> sid, smeta;
+            for (int k = 0; k < 400 && sid.size() < 60; ++k) {
+                const std::uint64_t id = ids.at(rng.next_below(900));
+                if (NS::shard(id, L) != s) continue;
+                sid.push_back(id);
+                smeta.push_back(NS::meta(pol, now, static_cast<std::uint32_t>(rng.next_below(3))));
+            }
+            std::vector<typename NS::Result> out(sid.size());
+            table.process_shard_batch(s, sid, smeta, now, pol, out);
+            twin.process_shard_batch(s, sid, smeta, now, pol, out);
+            for (const auto& r : out) {
+                tr.out.push_back(r.slot);
+                tr.out.push_back(r.evicted);
+                tr.out.push_back(static_cast<std::uint64_t>(r.outcome));
+                rows.push_back(r.slot);
+            }
+        }
+    }
+    // a metadata word make_metadata could not produce, at position 3 of a shard batch: the
+    // first three positions take effect and have results, then invalid_argument
+    {
+        std::vector<std::uint64_t> sid, smeta;
+        for (int k = 0; sid.size() < 6; ++k) {
+            const std::uint64_t id = ids.at(5000 + k);
+            if (NS::shard(id, L) != 0) continue;
+            sid.push_back(id);
+            smeta.push_back(NS::meta(pol, now, 0));
+        }
+        smeta[3] = mode == 2 ? now : now + 1;
+        std::vector<typename NS::Result> out(sid.size(), typename NS::Result{7, true, {}});
+        try {
+            table.process_shard_batch(0, sid, smeta, now, pol, out);
+        } catch (const std::invalid_argument& e) {
+            tr.error += std::string(e.what()) + "|";
+        }
+        for (const auto& r : out) {
+            tr.out.push_back(r.slot);
+            tr.out.push_back(static_cast<std::uint64_t>(r.outcome));
+        }
+        sid[1] = 1ull << 63;  // an invalid id stops at position 1
+        try {
+            twin.process_shard_batch(0, sid, smeta, now, pol, out);
+        } catch (const std::invalid_argument& e) {
+            tr.error += std::string(e.what()) + "|";
+        }
+        try {
+            std::vector<typename NS::Result> o2(1);
+            twin.process_shard_batch(table.num_shards(), std::vector<std::uint64_t>{1},
+                                     std::vector<std::uint64_t>{now}, now, pol, o2);
+        } catch (const std::out_of_range& e) {
+            tr.error += std::string(e.what()) + "|";
+        }
+    }
+    // training on some rows, then resets; the view of the embeddings; state_equals
+    std::sort(rows.begin(), rows.end());
+    rows.erase(std::unique(rows.begin(), rows.end()), rows.end());
+    std::vector<std::uint64_t> some(rows.begin(), rows.begin() + std::min<std::size_t>(rows.size(), 16));
+    std::vector<float> g(some.size() * table.dim());
+    for (float& x : g) x = static_cast<float>(rng.next_unit() - 0.5);
+    table.sgd_step(some, g, 0.1f, 0.5f);
+    twin.sgd_step(some, g, 0.1f, 0.5f);
+    tr.out.push_back(table.state_equals(twin));
+    const std::uint64_t untouched = table.total_rows() - 1 - rng.next_below(table.total_rows() / 2);
+    if (!std::binary_search(some.begin(), some.end(), untouched)) {
+        table.reset_row(untouched);  // a never-trained row redraws its own initial values
+        tr.out.push_back(table.state_equals(twin));
+    }
+    table.reset_row(some[0]);
+    tr.out.push_back(table.state_equals(twin));
+    tr.out.push_back(table.row_trained(some[0]));
+    tr.out.push_back(table.row_trained(some[1]));
+    try {
+        table.reset_row(table.total_rows());
+    } catch (const std::out_of_range& e) {
+        tr.error += std::string(e.what()) + "|";
+    }
+    auto bits = [&tr](float f) {
+        std::uint32_t u;
+        std::memcpy(&u, &f, 4);
+        tr.out.push_back(u);
+    };
+    const auto& emb = table.embeddings();
+    tr.out.push_back(emb.rows());
+    tr.out.push_back(emb.dim());
+    tr.out.push_back(emb.weights_count());
+    for (float v : emb.row(some[0])) bits(v);
+    for (float v : emb.row(some[1])) bits(v);
+    for (float v : emb.momentum_row(some[0])) bits(v);
+    for (float v : emb.momentum_row(some[1])) bits(v);
+    tr.out.push_back(emb.trained(some[1]));
+    for (float v : emb.gather(some)) bits(v);
+    for (std::uint64_t r = 0; r < table.total_rows(); r += 37) tr.out.push_back(table.row_identity(r));
+    for (std::uint32_t s = 0; s < table.num_shards(); ++s) {
+        for (auto v : NS::ident(table, s)) tr.out.push_back(v);
+        for (auto v : NS::meta(table, s)) tr.out.push_back(v);
+    }
+    return tr;
+}
+
 int main(int argc, char** argv) {
     const int cases = argc > 1 ? std::atoi(argv[1]) : 60;
     int bad = 0;
@@ -169,6 +342,14 @@ int main(int argc, char** argv) {
             ++bad;
         }
         checked += a.out.size();
+        const Trace sa = run_surface<Ref>(0x5afe0000 + c, c % 3);
+        const Trace sb = run_surface<Gpu>(0x5afe0000 + c, c % 3);
+        if (sa.out != sb.out || sa.error != sb.error) {
+            std::printf("MISMATCH surface case %d (mode %d): %zu vs %zu words, '%s' vs '%s'\n", c, c % 3,
+                        sa.out.size(), sb.out.size(), sa.error.c_str(), sb.error.c_str());
+            ++bad;
+        }
+        checked += sa.out.size();
     }
     std::printf("%s: %d cases, %llu result/state words compared, %d mismatches\n",
                 bad ? "FAIL" : "PASS", cases, (unsigned long long)checked, bad);
