@@ -326,10 +326,13 @@ mpzch_status mpzch_serialize_delta(mpzch_table* t, uint64_t generation, uint32_t
  * the serialized probe of one shard, positions in order (no dedup: a repeated id probes again
  * and refreshes with its own metadata word), each with the caller's metadata word.  ids must
  * route to `shard` (the reference's precondition; not checked).  Errors: shard >= S ->
- * MPZCH_ERANGE "shard index out of range" before anything runs; an invalid id or a metadata
- * word that make_metadata could not have produced -> MPZCH_EINVAL with the reference's text
+ * MPZCH_ERANGE "shard index out of range" before anything runs; a metadata word that
+ * make_metadata could not have produced -> MPZCH_EINVAL with the reference's text
  * (probe_core.cpp:49-58, 76-77) AFTER the positions before it took effect (their results are
- * in out_slots / out_outcomes), exactly like the exception thrown inside the reference's loop.
+ * in out_slots / out_outcomes), exactly like the exception thrown inside the reference's loop;
+ * an invalid id -> MPZCH_EINVAL at the START of its 256-position chunk (the reference hoists
+ * home_slot, which validates, over each chunk before probing it: table.cpp:129-133,
+ * probe_core.cpp:27-30), so only the chunks before it took effect.
  * Host buffers; returns when done. */
 mpzch_status mpzch_process_shard_batch(mpzch_table* t, uint32_t shard, const uint64_t* ids,
                                        const uint64_t* metas, uint64_t n, uint64_t now,

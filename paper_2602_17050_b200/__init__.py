@@ -577,8 +577,10 @@ class MpzchTable:
     # ---- state (parity) ------------------------------------------------------------------
     def process_shard_batch(self, shard: int, ids, metas, now: int, policy: EvictionPolicy):
         """MpzchTable::process_shard_batch (table.cpp:112-148): shard's positions in order, each
-        with its own metadata word.  Returns (slots, outcomes); on an invalid id / metadata word
-        the exception carries .partial = the results of the positions before it."""
+        with its own metadata word.  Returns (slots, outcomes); on a bad metadata word the
+        exception carries .partial = the results of the positions before it; on an invalid id,
+        the results of the 256-position chunks before its chunk (the reference hoists the
+        validating home_slot over each chunk, table.cpp:129-133)."""
         ids = np.ascontiguousarray(ids, dtype=np.uint64)
         metas = np.ascontiguousarray(metas, dtype=np.uint64)
         if metas.size != ids.size:

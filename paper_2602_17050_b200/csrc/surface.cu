@@ -21,10 +21,15 @@ typedef unsigned __int128 u128;
 constexpr u128 kKeyEmpty = ~(u128)0;
 
 // ---- process_shard_batch: one warp runs the reference's per-shard loop (table.cpp:126-147) in
-// position order -- no dedup, each position probes with its own metadata word, and a bad id or
-// metadata word stops the loop at that position after the earlier ones took effect
-// (lookup_or_insert throws from inside the loop, probe_core.cpp:76-77).  st[0] = first failing
-// position (~0: none), st[1] = 1 invalid id / 2 metadata word, st[2] = the id.
+// position order -- no dedup, each position probes with its own metadata word.  Errors stop the
+// loop where the reference's would: the reference hoists home_slot (which runs require_valid_id,
+// probe_core.cpp:27-30) over each 256-position chunk before probing it (table.cpp:129-133), so an
+// invalid id stops the batch at the START of its chunk; a bad metadata word stops it at its own
+// position (check_metadata_input inside lookup_or_insert, probe_core.cpp:76-77), after the
+// earlier positions took effect.  st[0] = positions that took effect (~0: all), st[1] = 1 invalid
+// id / 2 metadata word, st[2] = the offending id.
+constexpr uint64_t kShardChunk = 256;  // table.cpp:129
+
 template <int MODE>
 __global__ void __launch_bounds__(32) k_shard_batch(TableDev t, uint32_t shard, const uint64_t* __restrict__ ids,
                                                     const uint64_t* __restrict__ metas, uint64_t n,
@@ -37,19 +42,26 @@ __global__ void __launch_bounds__(32) k_shard_batch(TableDev t, uint32_t shard, 
     const unsigned lane = lane_id();
     const ShardDev sd = t.shards[shard];
     const uint64_t cap = sd.cap.d, base = sd.offset;
+    // first invalid id (warp scan) -> the chunk the reference's home hoisting throws in
+    uint64_t kb = n;
+    for (uint64_t c = 0; c < n && kb == n; c += 32) {
+        const bool bad_id = c + lane < n && (ids[c + lane] >> 63);
+        const unsigned m = __ballot_sync(0xffffffffu, bad_id);
+        if (m) kb = c + (uint64_t)(__ffs(m) - 1);
+    }
+    const uint64_t stop = kb == n ? n : kb / kShardChunk * kShardChunk;
     unsigned nreset = 0;
-    for (uint64_t k = 0; k < n; ++k) {
+    bool failed = false;
+    for (uint64_t k = 0; k < stop; ++k) {
         const uint64_t id = ids[k];
         const uint64_t meta_in = metas[k];
-        // require_valid_id, then check_metadata_input (probe_core.cpp:49-58, 76-77)
-        const int bad = (id >> 63) ? 1
-                        : (MODE == kModeTtl ? meta_in <= now : meta_in != now) ? 2 : 0;
-        if (bad) {
+        if (MODE == kModeTtl ? meta_in <= now : meta_in != now) {  // check_metadata_input
             if (lane == 0) {
                 st[0] = k;
-                st[1] = (unsigned long long)bad;
+                st[1] = 2ull;
                 st[2] = id;
             }
+            failed = true;
             break;
         }
         uint64_t gslot;
@@ -68,7 +80,14 @@ __global__ void __launch_bounds__(32) k_shard_batch(TableDev t, uint32_t shard, 
         nreset += (oc == kEvicted && t.dim) ? 1u : 0u;
         __syncwarp();
     }
-    if (lane == 0) *reset_count = nreset;
+    if (lane == 0) {
+        if (!failed && kb < n) {
+            st[0] = stop;
+            st[1] = 1ull;
+            st[2] = ids[kb];
+        }
+        *reset_count = nreset;
+    }
 }
 
 // ---- dedup (batch_engine.cpp:79-108): first-occurrence uniques keyed on (id, feature) and the

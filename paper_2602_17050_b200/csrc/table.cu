@@ -1711,9 +1711,10 @@ mpzch_status mpzch_gather(const mpzch_table* t, const uint64_t* rows, uint64_t n
         DeviceGuard g(T.device);
         cudaStream_t st = T.stream;
         order_after_last_batch(T, st);
-        T.sb_buf.reserve(n * 8 + n * T.dim * 4);
+        const uint64_t rows_bytes = (n * 8 + 255) & ~255ull;  // the rows stay 16-byte aligned (float4 stores)
+        T.sb_buf.reserve(rows_bytes + n * T.dim * 4);
         uint64_t* d_rows = T.sb_buf.as<uint64_t>();
-        float* d_out = (float*)(d_rows + n);
+        float* d_out = (float*)(T.sb_buf.as<char>() + rows_bytes);
         MPZCH_CUDA(cudaMemcpyAsync(d_rows, rows, n * 8, cudaMemcpyHostToDevice, st));
         run_gather_weights(T, d_rows, n, d_out, st);
         ++T.launches;

@@ -72,7 +72,30 @@ struct Gpu {
 struct Trace {
     std::vector<std::uint64_t> out;  // slot, evicted, outcome per position, then state
     std::string error;
+    std::vector<std::pair<std::size_t, const char*>> marks;  // section starts, for the report
+    void mark(const char* what) { marks.emplace_back(out.size(), what); }
 };
+
+// first differing word and the section it falls in (sections are marked on the GPU side)
+static void report_diff(const Trace& a, const Trace& b, int shown = 0) {
+  for (std::size_t i = 0; i < a.out.size() && i < b.out.size(); ++i) {
+    if (a.out[i] == b.out[i]) continue;
+    if (++shown > 6) return;
+    const char* sec = "start";
+    std::size_t sec0 = 0;
+    for (const auto& m : b.marks)
+        if (m.first <= i) {
+            sec = m.second;
+            sec0 = m.first;
+        }
+    std::printf("  first difference at word %zu (section '%s' + %zu): %llu vs %llu\n", i, sec, i - sec0,
+                (unsigned long long)(i < a.out.size() ? a.out[i] : 0),
+                (unsigned long long)(i < b.out.size() ? b.out[i] : 0));
+  }
+  for (const auto& m : b.marks)
+    if (std::string(m.second) == "failing batch ids")
+      for (int k = 0; k < 6; ++k) std::printf("    sid[%d] = %llu\n", k, (unsigned long long)b.out[m.first + k]);
+}
 
 // One workload in the style of proj/tests/test_table_batch.cpp:291-328.
 template <class NS>
@@ -206,6 +229,7 @@ Trace run_surface(std::uint64_t seed, int mode) {
         tr.error += std::string(e.what()) + "|";
     }
     mpzch::DistinctIdStream ids(rng.next());
+    tr.mark("dedup");
     // dedup on (id, feature) with its inverse, then its first-bad-position error
     std::vector<typename NS::Entry> entries;
     for (int k = 0; k < 300; ++k)
@@ -227,6 +251,7 @@ Trace run_surface(std::uint64_t seed, int mode) {
     // per-shard batches in several rounds (ids routed with shard_of, repeats included)
     std::uint64_t now = 1;
     std::vector<std::uint64_t> rows;
+    tr.mark("shard batches");
     for (int round = 0; round < 6; ++round) {
         now += 1 + rng.next_below(4);
         for (std::uint32_t s = 0; s < table.num_shards(); ++s) {
@@ -250,6 +275,7 @@ Trace run_surface(std::uint64_t seed, int mode) {
     }
     // a metadata word make_metadata could not produce, at position 3 of a shard batch: the
     // first three positions take effect and have results, then invalid_argument
+    tr.mark("bad metadata shard batch");
     {
         std::vector<std::uint64_t> sid, smeta;
         for (int k = 0; sid.size() < 6; ++k) {
@@ -259,6 +285,8 @@ Trace run_surface(std::uint64_t seed, int mode) {
             smeta.push_back(NS::meta(pol, now, 0));
         }
         smeta[3] = mode == 2 ? now : now + 1;
+        tr.mark("failing batch ids");
+        for (auto v : sid) tr.out.push_back(v);
         std::vector<typename NS::Result> out(sid.size(), typename NS::Result{7, true, {}});
         try {
             table.process_shard_batch(0, sid, smeta, now, pol, out);
@@ -275,6 +303,36 @@ Trace run_surface(std::uint64_t seed, int mode) {
         } catch (const std::invalid_argument& e) {
             tr.error += std::string(e.what()) + "|";
         }
+        // an invalid id at position 300 of a 600-position batch: the reference validates each
+        // 256-position chunk before probing it, so positions 0..255 take effect, 256.. do not
+        {
+            std::vector<std::uint64_t> lid, lmeta;
+            for (int k = 0; lid.size() < 600; ++k) {
+                const std::uint64_t id = ids.at(20000 + rng.next_below(2000));
+                if (NS::shard(id, L) != 0) continue;
+                lid.push_back(id);
+                lmeta.push_back(NS::meta(pol, now, 0));
+            }
+            lid[300] = ~0ull;
+            std::vector<typename NS::Result> lo(lid.size(), typename NS::Result{7, true, {}});
+            try {
+                twin.process_shard_batch(0, lid, lmeta, now, pol, lo);
+            } catch (const std::invalid_argument& e) {
+                tr.error += std::string(e.what()) + "|";
+            }
+            for (const auto& r : lo) {
+                tr.out.push_back(r.slot);
+                tr.out.push_back(static_cast<std::uint64_t>(r.outcome));
+            }
+            lid[300] = ids.at(1);
+            lmeta[290] = mode == 2 ? now : now + 1;  // a bad metadata word stops at its position
+            try {
+                twin.process_shard_batch(0, lid, lmeta, now, pol, lo);
+            } catch (const std::invalid_argument& e) {
+                tr.error += std::string(e.what()) + "|";
+            }
+            for (const auto& r : lo) tr.out.push_back(r.slot);
+        }
         try {
             std::vector<typename NS::Result> o2(1);
             twin.process_shard_batch(table.num_shards(), std::vector<std::uint64_t>{1},
@@ -284,6 +342,13 @@ Trace run_surface(std::uint64_t seed, int mode) {
         }
     }
     // training on some rows, then resets; the view of the embeddings; state_equals
+    tr.mark("table identities after the failing shard batches");
+    for (std::uint32_t s = 0; s < table.num_shards(); ++s)
+        for (auto v : NS::ident(table, s)) tr.out.push_back(v);
+    tr.mark("twin identities after the failing shard batches");
+    for (std::uint32_t s = 0; s < table.num_shards(); ++s)
+        for (auto v : NS::ident(twin, s)) tr.out.push_back(v);
+    tr.mark("sgd / reset / state_equals");
     std::sort(rows.begin(), rows.end());
     rows.erase(std::unique(rows.begin(), rows.end()), rows.end());
     std::vector<std::uint64_t> some(rows.begin(), rows.begin() + std::min<std::size_t>(rows.size(), 16));
@@ -311,6 +376,7 @@ Trace run_surface(std::uint64_t seed, int mode) {
         std::memcpy(&u, &f, 4);
         tr.out.push_back(u);
     };
+    tr.mark("embeddings view");
     const auto& emb = table.embeddings();
     tr.out.push_back(emb.rows());
     tr.out.push_back(emb.dim());
@@ -320,7 +386,9 @@ Trace run_surface(std::uint64_t seed, int mode) {
     for (float v : emb.momentum_row(some[0])) bits(v);
     for (float v : emb.momentum_row(some[1])) bits(v);
     tr.out.push_back(emb.trained(some[1]));
+    tr.mark("gather");
     for (float v : emb.gather(some)) bits(v);
+    tr.mark("row_identity / identities / metadata");
     for (std::uint64_t r = 0; r < table.total_rows(); r += 37) tr.out.push_back(table.row_identity(r));
     for (std::uint32_t s = 0; s < table.num_shards(); ++s) {
         for (auto v : NS::ident(table, s)) tr.out.push_back(v);
@@ -339,6 +407,7 @@ int main(int argc, char** argv) {
         if (a.out != b.out || a.error != b.error) {
             std::printf("MISMATCH case %d (mode %d): %zu vs %zu words, '%s' vs '%s'\n", c, c % 3,
                         a.out.size(), b.out.size(), a.error.c_str(), b.error.c_str());
+            report_diff(a, b);
             ++bad;
         }
         checked += a.out.size();
@@ -347,6 +416,7 @@ int main(int argc, char** argv) {
         if (sa.out != sb.out || sa.error != sb.error) {
             std::printf("MISMATCH surface case %d (mode %d): %zu vs %zu words, '%s' vs '%s'\n", c, c % 3,
                         sa.out.size(), sb.out.size(), sa.error.c_str(), sb.error.c_str());
+            report_diff(sa, sb);
             ++bad;
         }
         checked += sa.out.size();
