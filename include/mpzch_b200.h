@@ -377,6 +377,19 @@ mpzch_status mpzch_shard_config(const mpzch_table* t, uint32_t shard, uint64_t* 
 
 /* ---- execution control / introspection */
 mpzch_status mpzch_set_path(mpzch_table* t, int path);
+/* Embedding-row reset of evicted slots ("fused sgd_step with reset").
+ * EAGER (default): the batch writes every evicted row -- draw_row, momentum 0, trained 0 --
+ * as the reference does inside process_batch (table.cpp:142 -> embedding_store.cpp:62-68).
+ * DEFERRED: the batch only marks the row reset-pending; the next sgd_step that touches it
+ * computes from the closed-form draw_row and momentum 0 without reading the row (reset and
+ * update share one write of the row), gathers (mpzch_gather, mpzch_lookup_gather_device)
+ * return the drawn row, and every other reader (copies, snapshot, delta, state_equals,
+ * mpzch_device_arrays' weights pointer) materialises the pending resets first.  Every
+ * observable value is bit-identical to EAGER.  Switching back to EAGER flushes. */
+enum { MPZCH_RESET_EAGER = 0, MPZCH_RESET_DEFERRED = 1 };
+mpzch_status mpzch_set_reset_mode(mpzch_table* t, int mode);
+/* write every pending reset now (DEFERRED mode; a no-op otherwise) */
+mpzch_status mpzch_flush_resets(mpzch_table* t);
 mpzch_status mpzch_last_stats(const mpzch_table* t, mpzch_batch_stats* out);
 /* number of kernels this handle launched since creation (bench gpu_launches) */
 uint64_t mpzch_kernel_launches(const mpzch_table* t);

@@ -424,6 +424,11 @@ public:
         check(mpzch_sgd_step(t_, rows.data(), rows.size(), grads.data(), grads.size(), lr, beta));
     }
 
+    // B200 extension: fuse each evicted row's reset into its next
+    // sgd_step / gather (MPZCH_RESET_DEFERRED); observable state is unchanged
+    void set_reset_mode(int mode) { check(mpzch_set_reset_mode(t_, mode)); }
+    void flush_resets() { check(mpzch_flush_resets(t_)); }
+
     PublishCursor make_cursor() {
         PublishCursor c;
         check(mpzch_make_cursor(t_, &c.generation));

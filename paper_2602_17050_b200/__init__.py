@@ -187,6 +187,8 @@ _SIGS = {
     "mpzch_serialize_delta": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
                                              _vp, ctypes.c_uint64, _u64p, _u64p]),
     "mpzch_set_path": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "mpzch_set_reset_mode": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "mpzch_flush_resets": (ctypes.c_int, [_vp]),
     "mpzch_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),
     "mpzch_get_profile": (ctypes.c_int, [_vp, ctypes.POINTER(_Profile)]),
     "mpzch_last_stats": (ctypes.c_int, [_vp, ctypes.POINTER(_Stats)]),
@@ -760,6 +762,16 @@ class MpzchTable:
     def set_path(self, path: str):
         _check(self._lib.mpzch_set_path(self._h, {"auto": 0, "ordered": 1, "rounds": 2}[path]))
 
+    def set_reset_mode(self, mode: str):
+        """'eager' (default: the batch writes every evicted row, as the reference does) or
+        'deferred' (evicted rows are marked reset-pending; the next sgd_step of a row starts
+        from the closed-form draw_row without reading it; gathers draw pending rows; every
+        other reader flushes first -- observable state identical to 'eager')."""
+        _check(self._lib.mpzch_set_reset_mode(self._h, {"eager": 0, "deferred": 1}[mode]))
+
+    def flush_resets(self):
+        _check(self._lib.mpzch_flush_resets(self._h))
+
     def last_stats(self) -> dict:
         s = _Stats()
         _check(self._lib.mpzch_last_stats(self._h, ctypes.byref(s)))
@@ -841,6 +853,13 @@ def crc32_device(t) -> int:
     _check(load_library().mpzch_crc32_device(ctypes.c_void_p(t.data_ptr()),
                                              t.numel() * t.element_size(), ctypes.byref(c),
                                              ctypes.c_void_p(st.cuda_stream)))
+    return c.value
+
+
+def crc32_device_ptr(ptr: int, nbytes: int) -> int:
+    """crc32 of `nbytes` device bytes at a raw device address (e.g. from device_arrays())."""
+    c = ctypes.c_uint32(0)
+    _check(load_library().mpzch_crc32_device(ctypes.c_void_p(ptr), nbytes, ctypes.byref(c), None))
     return c.value
 
 

@@ -86,7 +86,63 @@ struct TableDev {
     double bound;        // 1/sqrt(dim), computed on the host exactly as draw_row does
     uint32_t P;          // max_probe
     uint32_t dim;
+    uint32_t* pend_bits; // MPZCH_RESET_DEFERRED: one bit per held row (row - row_lo), set while
+                         // the row's reset (draw_row, momentum 0, trained 0) is not yet written;
+                         // null in eager mode.  1 bit per row keeps the map L2-resident (16 MiB
+                         // at 2^27 rows), so reset-aware readers pay an L2 hit, not a DRAM access
 };
+
+// draw_row (proj/src/embedding_store.cpp:12-18), element with SplitMix64 state `state`
+// (= mix64(row, init_seed) + (j+1) * golden for element j); see rows.cu
+__device__ __forceinline__ float draw_at(uint64_t state, double bound) {
+    const uint64_t z = splitmix_out(state);
+    // 2u - 1 with u = (z >> 11) * 2^-53 is exactly ((z >> 11) - 2^52) * 2^-52: one exact
+    // integer -> double conversion instead of a multiply and an add (both exact as well)
+    const double t = (double)((int64_t)(z >> 11) - (1ll << 52)) * 0x1.0p-52;
+    return __double2float_rn(__dmul_rn(t, bound));
+}
+
+__device__ __forceinline__ float draw_elem(uint64_t s0, uint64_t j, double bound) {
+    return draw_at(s0 + (j + 1) * kGolden, bound);
+}
+
+// elements 4q .. 4q+3 of draw_row(row): one multiply, then golden increments
+__device__ __forceinline__ float4 draw_quad(uint64_t s0, uint32_t q, double bound) {
+    const uint64_t s1 = s0 + ((uint64_t)q * 4 + 1) * kGolden;
+    float4 v;
+    v.x = draw_at(s1, bound);
+    v.y = draw_at(s1 + kGolden, bound);
+    v.z = draw_at(s1 + 2 * kGolden, bound);
+    v.w = draw_at(s1 + 3 * kGolden, bound);
+    return v;
+}
+
+// is the row's reset pending (deferred mode only)
+__device__ __forceinline__ bool reset_pending(const TableDev& t, uint64_t row) {
+    if (!t.pend_bits) return false;
+    const uint64_t r = row - t.row_lo;
+    return (__ldcg(t.pend_bits + (r >> 5)) >> (r & 31)) & 1u;
+}
+
+__device__ __forceinline__ void clear_pending(const TableDev& t, uint64_t row) {
+    const uint64_t r = row - t.row_lo;
+    atomicAnd(t.pend_bits + (r >> 5), ~(1u << (r & 31)));
+}
+
+// a warp copies one row's weights to dst (16-byte accesses when dim % 4 == 0); a row whose
+// reset is pending is drawn in closed form instead (EmbeddingTable::gather after reset_row)
+__device__ __forceinline__ void copy_row_or_draw(const TableDev& t, uint64_t row, float* dst, unsigned lane) {
+    const float* src = t.weights + row * t.dim;
+    const bool pend = reset_pending(t, row);
+    const uint64_t s0 = pend ? mix64(row, t.init_seed) : 0;
+    if ((t.dim & 3u) == 0) {
+        for (uint32_t q = lane; q < t.dim / 4; q += 32)
+            reinterpret_cast<float4*>(dst)[q] =
+                pend ? draw_quad(s0, q, t.bound) : __ldg(reinterpret_cast<const float4*>(src) + q);
+    } else {
+        for (uint32_t j = lane; j < t.dim; j += 32) dst[j] = pend ? draw_elem(s0, j, t.bound) : __ldg(src + j);
+    }
+}
 
 __device__ __forceinline__ uint32_t shard_of(uint64_t id, const TableDev& t) {
     return (uint32_t)fastmod(mix64(id ^ kShardSalt, t.seed), t.nshards);

@@ -228,19 +228,11 @@ __global__ void __launch_bounds__(256) k_lookup_gather(TableDev t, const uint64_
             }
         }
         // cooperative row copy
-        const uint32_t quads = t.dim / 4;
         for (int r = 0; r < 32; ++r) {
             const uint64_t sr = __shfl_sync(0xffffffffu, slot, r);
             const uint64_t ir = w * 32 + r;
             if (ir >= n || sr == kEmpty) continue;
-            const float* src = t.weights + sr * t.dim;
-            float* dst = out_rows + ir * t.dim;
-            if ((t.dim & 3u) == 0) {
-                for (uint32_t q = lane; q < quads; q += 32)
-                    reinterpret_cast<float4*>(dst)[q] = __ldg(reinterpret_cast<const float4*>(src) + q);
-            } else {
-                for (uint32_t j = lane; j < t.dim; j += 32) dst[j] = __ldg(src + j);
-            }
+            copy_row_or_draw(t, sr, out_rows + ir * t.dim, lane);
         }
     }
 }

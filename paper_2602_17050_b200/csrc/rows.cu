@@ -7,7 +7,9 @@
 // independently and stored as 16-byte vectors.  2*u-1 is exact; the product
 // is one FP64 rounding (__dmul_rn: no contraction), then __double2float_rn,
 // exactly the reference's static_cast<float> sequence.
-// reset_row (embedding_store.cpp:62-68): redraw + momentum 0 + trained 0.
+// reset_row (embedding_store.cpp:62-68): redraw + momentum 0 + trained 0 -- written by the batch
+// (MPZCH_RESET_EAGER, the reference's order) or marked pending and fused into the next
+// sgd_step / gather of the row (MPZCH_RESET_DEFERRED: same observable state, one row write).
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -16,19 +18,6 @@
 namespace mpzch_b200 {
 
 namespace {
-
-// element with SplitMix64 state `state` (= s0 + (j+1) * golden for element j)
-__device__ __forceinline__ float draw_at(uint64_t state, double bound) {
-    const uint64_t z = splitmix_out(state);
-    // 2u - 1 with u = (z >> 11) * 2^-53 is exactly ((z >> 11) - 2^52) * 2^-52: one exact
-    // integer -> double conversion instead of a multiply and an add (both exact as well)
-    const double t = (double)((int64_t)(z >> 11) - (1ll << 52)) * 0x1.0p-52;
-    return __double2float_rn(__dmul_rn(t, bound));
-}
-
-__device__ __forceinline__ float draw_elem(uint64_t s0, uint64_t j, double bound) {
-    return draw_at(s0 + (j + 1) * kGolden, bound);
-}
 
 // init: grid-stride over (row, quad) for dim % 4 == 0, else over elements
 __global__ void __launch_bounds__(256) k_draw_all(TableDev t) {
@@ -60,6 +49,28 @@ __global__ void __launch_bounds__(256) k_draw_all(TableDev t) {
     }
 }
 
+// one row's reset by a warp: draw_row, momentum 0, trained 0 (embedding_store.cpp:62-68)
+__device__ __forceinline__ void reset_row_warp(const TableDev& t, uint64_t row, unsigned lane) {
+    const uint64_t s0 = mix64(row, t.init_seed);
+    float* w = t.weights + row * t.dim;
+    float* m = t.momentum + row * t.dim;
+    if ((t.dim & 3u) == 0) {
+        float4* w4 = reinterpret_cast<float4*>(w);
+        float4* m4 = reinterpret_cast<float4*>(m);
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (uint32_t q = lane; q < t.dim / 4; q += 32) {
+            w4[q] = draw_quad(s0, q, t.bound);
+            m4[q] = z;
+        }
+    } else {
+        for (uint32_t j = lane; j < t.dim; j += 32) {
+            w[j] = draw_elem(s0, j, t.bound);
+            m[j] = 0.f;
+        }
+    }
+    if (lane == 0) t.trained[row] = 0;
+}
+
 // reset: a warp takes 32 listed rows at a time (one coalesced load of their indices, so no
 // row waits on its own index load) and resets them one after another, a row's dim floats
 // spread over the lanes; rows may repeat (LRU double eviction), the operation is idempotent.
@@ -73,91 +84,44 @@ __global__ void __launch_bounds__(256) k_reset_rows(TableDev t, const uint64_t* 
     for (uint64_t r0 = warp * 32; r0 < n; r0 += nwarps * 32) {
         const uint64_t mine = r0 + lane < n ? rows[r0 + lane] : 0;
         const unsigned cnt = n - r0 < 32 ? (unsigned)(n - r0) : 32u;
-        for (unsigned k = 0; k < cnt; ++k) {
-            const uint64_t row = __shfl_sync(0xffffffffu, mine, k);
-            const uint64_t s0 = mix64(row, t.init_seed);
-            float* w = t.weights + row * t.dim;
-            float* m = t.momentum + row * t.dim;
-            if ((t.dim & 3u) == 0) {
-                float4* w4 = reinterpret_cast<float4*>(w);
-                float4* m4 = reinterpret_cast<float4*>(m);
-                const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-                for (uint32_t q = lane; q < t.dim / 4; q += 32) {
-                    // states of elements 4q .. 4q+3: one multiply, then golden increments
-                    const uint64_t s1 = s0 + ((uint64_t)q * 4 + 1) * kGolden;
-                    float4 v;
-                    v.x = draw_at(s1, t.bound);
-                    v.y = draw_at(s1 + kGolden, t.bound);
-                    v.z = draw_at(s1 + 2 * kGolden, t.bound);
-                    v.w = draw_at(s1 + 3 * kGolden, t.bound);
-                    w4[q] = v;
-                    m4[q] = z;
-                }
-            } else {
-                for (uint32_t j = lane; j < t.dim; j += 32) {
-                    w[j] = draw_elem(s0, j, t.bound);
-                    m[j] = 0.f;
-                }
-            }
-            if (lane == 0) t.trained[row] = 0;
-        }
+        for (unsigned k = 0; k < cnt; ++k) reset_row_warp(t, __shfl_sync(0xffffffffu, mine, k), lane);
     }
 }
 
-__global__ void k_write_slots(TableDev t, const uint64_t* __restrict__ g, const uint64_t* __restrict__ ids,
-                              const uint64_t* __restrict__ metas, uint64_t n) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        t.ident[g[i]] = ids[i];
-        t.meta[g[i]] = metas[i];
+// deferred mode: the batch only marks its evicted rows reset-pending (one bit per row); the
+// next sgd_step that touches a row computes from the closed-form draw instead of reading the
+// row (train.cu), gathers draw it on the fly, other readers flush first (k_flush_pending)
+__global__ void __launch_bounds__(256) k_mark_pending(TableDev t, const uint64_t* __restrict__ rows,
+                                                      const unsigned* __restrict__ count) {
+    pdl_wait();
+    const unsigned n = *count;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = rows[i] - t.row_lo;
+        atomicOr(t.pend_bits + (r >> 5), 1u << (r & 31));
     }
 }
 
-// Hole check: every id stored inside its own probe window at
-// offset o must see neither EMPTY nor another copy of itself in [home, home+o).
-__global__ void __launch_bounds__(256) k_hole_check(TableDev t, unsigned* bad) {
-    for (uint64_t g = t.row_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < t.row_hi;
-         g += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t id = t.ident[g];
-        if (id == kEmpty) continue;
-        if (id >> 63) { atomicExch(bad, 1u); continue; }  // stray claim word
-        const uint32_t s = shard_of(id, t);
-        const ShardDev sd = t.shards[s];
-        // the id must live in its own shard's segment to be reachable; if it does
-        // not, it is a foreign occupant for everybody and cannot create a hole
-        if (g < sd.offset || g >= sd.offset + sd.cap.d) continue;
-        const uint64_t h = home_of(id, sd, t.seed);
-        const uint64_t loc = g - sd.offset;
-        const uint64_t o = loc >= h ? loc - h : loc + sd.cap.d - h;
-        if (o >= t.P) continue;  // outside its window: invisible, harmless
-        uint64_t x = h;
-        for (uint64_t k = 0; k < o; ++k) {
-            const uint64_t v = t.ident[sd.offset + x];
-            if (v == kEmpty || v == id) { atomicExch(bad, 1u); break; }
-            if (++x == sd.cap.d) x = 0;
-        }
-    }
-}
-
-// Delta cut gather (DeltaSource::cut, proj/src/publish.cpp:288-305): for each dirty row,
-// its identity word and its weights.  One warp per row, 16-byte copies.
-__global__ void __launch_bounds__(256) k_gather_rows(TableDev t, const uint64_t* __restrict__ rows,
-                                                     uint64_t n, uint64_t* __restrict__ out_ids,
-                                                     float* __restrict__ out_w) {
+// materialise every pending reset: a warp reads 32 bitmap words (1024 rows) per step and
+// resets the pending rows among them, then clears the words
+__global__ void __launch_bounds__(256) k_flush_pending(TableDev t) {
     const unsigned lane = lane_id();
     const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
-        const uint64_t row = rows[r];
-        if (lane == 0) out_ids[r] = t.ident[row];
-        if (!out_w) continue;
-        const float* src = t.weights + row * t.dim;
-        float* dst = out_w + r * t.dim;
-        if ((t.dim & 3u) == 0) {
-            for (uint32_t q = lane; q < t.dim / 4; q += 32)
-                reinterpret_cast<float4*>(dst)[q] = reinterpret_cast<const float4*>(src)[q];
-        } else {
-            for (uint32_t j = lane; j < t.dim; j += 32) dst[j] = src[j];
+    const uint64_t words = (t.row_hi - t.row_lo + 31) / 32;
+    for (uint64_t w0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; w0 < words; w0 += warps * 32) {
+        const uint32_t mine = w0 + lane < words ? t.pend_bits[w0 + lane] : 0u;
+        unsigned any = __ballot_sync(0xffffffffu, mine != 0);
+        while (any) {
+            const unsigned src = __ffs(any) - 1;
+            any &= any - 1;
+            uint32_t bits = __shfl_sync(0xffffffffu, mine, src);
+            const uint64_t rb = t.row_lo + (w0 + src) * 32;
+            while (bits) {
+                const unsigned b = __ffs(bits) - 1;
+                bits &= bits - 1;
+                reset_row_warp(t, rb + b, lane);
+            }
         }
+        if (mine) t.pend_bits[w0 + lane] = 0u;
     }
 }
 
@@ -177,8 +141,21 @@ void launch_init_table(Table& t) {
 }
 
 void launch_reset_rows(Table& t, const uint64_t* rows, const unsigned* count, cudaStream_t st) {
-    launch_pdl(k_reset_rows, 148 * 8, 256, st, t.dev, rows, count);
+    if (t.dev.pend_bits) {
+        launch_pdl(k_mark_pending, 148 * 8, 256, st, t.dev, rows, count);
+        t.resets_pending = true;
+    } else {
+        launch_pdl(k_reset_rows, 148 * 8, 256, st, t.dev, rows, count);
+    }
     ++t.launches;
+}
+
+void flush_resets(Table& t, cudaStream_t st) {
+    if (!t.resets_pending || t.dim == 0) return;
+    k_flush_pending<<<grid_for((t.held_rows() + 1023) / 1024 * 32, 256, 148u * 16u), 256, 0, st>>>(t.dev);
+    ++t.launches;
+    MPZCH_CUDA(cudaGetLastError());
+    t.resets_pending = false;
 }
 
 void launch_write_slots(Table& t, const uint64_t* g, const uint64_t* ids, const uint64_t* metas,

@@ -168,14 +168,7 @@ __global__ void __launch_bounds__(256) k_gather_weights(TableDev t, const uint64
     const unsigned lane = lane_id();
     const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
-        const float* src = t.weights + rows[r] * t.dim;
-        float* dst = out + r * t.dim;
-        if ((t.dim & 3u) == 0) {
-            for (uint32_t q = lane; q < t.dim / 4; q += 32)
-                reinterpret_cast<float4*>(dst)[q] = __ldg(reinterpret_cast<const float4*>(src) + q);
-        } else {
-            for (uint32_t j = lane; j < t.dim; j += 32) dst[j] = __ldg(src + j);
-        }
+        copy_row_or_draw(t, rows[r], out + r * t.dim, lane);
     }
 }
 

@@ -621,6 +621,18 @@ extern "C" {
 
 static void order_after_last_batch(Table& T, cudaStream_t st);
 
+// Readers that are not reset-aware (copies, snapshots, deltas, state_equals, raw pointers)
+// first materialise the resets a deferred-mode batch left pending (rows.cu); observable state
+// is then exactly the eager (reference) state.  Synchronous on the handle's stream.
+static void flush_for_read(const Table& Tc) {
+    Table& T = const_cast<Table&>(Tc);
+    if (!T.resets_pending) return;
+    DeviceGuard g(T.device);
+    order_after_last_batch(T, T.stream);
+    flush_resets(T, T.stream);
+    MPZCH_CUDA(cudaStreamSynchronize(T.stream));
+}
+
 const char* mpzch_last_error(void) { return g_last_error.c_str(); }
 
 const char* mpzch_build_info(void) { return MPZCH_BUILD_INFO; }
@@ -1085,6 +1097,7 @@ mpzch_status mpzch_copy_weights(const mpzch_table* t, uint64_t row0, uint64_t nr
     CHECK_T(t);
     return guarded([&] {
         const Table& T = *t->t;
+        flush_for_read(T);
         check_rows(T, row0, nrows);
         DeviceGuard g(T.device);
         MPZCH_CUDA(cudaStreamSynchronize(T.stream));
@@ -1096,6 +1109,7 @@ mpzch_status mpzch_copy_momentum(const mpzch_table* t, uint64_t row0, uint64_t n
     CHECK_T(t);
     return guarded([&] {
         const Table& T = *t->t;
+        flush_for_read(T);
         check_rows(T, row0, nrows);
         DeviceGuard g(T.device);
         MPZCH_CUDA(cudaStreamSynchronize(T.stream));
@@ -1107,6 +1121,7 @@ mpzch_status mpzch_copy_trained(const mpzch_table* t, uint8_t* out) {
     CHECK_T(t);
     return guarded([&] {
         const Table& T = *t->t;
+        flush_for_read(T);
         check_rows(T, T.row_lo, 0);
         DeviceGuard g(T.device);
         MPZCH_CUDA(cudaStreamSynchronize(T.stream));
@@ -1126,6 +1141,10 @@ mpzch_status mpzch_copy_row_generation(const mpzch_table* t, uint64_t* out) {
 mpzch_status mpzch_device_arrays(const mpzch_table* t, uint64_t** identities, uint64_t** metadata,
                                  float** weights) {
     CHECK_T(t);
+    if (weights) {  // a raw weights pointer: no reset may stay pending behind it
+        const mpzch_status st = guarded([&] { flush_for_read(*t->t); });
+        if (st != MPZCH_OK) return st;
+    }
     if (identities) *identities = t->t->ident;
     if (metadata) *metadata = t->t->meta;
     if (weights) *weights = t->t->weights;
@@ -1182,6 +1201,7 @@ mpzch_status mpzch_write_row(mpzch_table* t, uint64_t row, const float* w, const
     return guarded([&] {
         Table& T = *t->t;
         check_rows(T, row, 1);
+        flush_for_read(T);
         DeviceGuard g(T.device);
         MPZCH_CUDA(cudaStreamSynchronize(T.stream));
         if (w) MPZCH_CUDA(cudaMemcpy(T.dev.weights + row * T.dim, w, T.dim * 4, cudaMemcpyHostToDevice));
@@ -1333,6 +1353,7 @@ mpzch_status mpzch_delta_cut(mpzch_table* t, uint64_t generation, uint64_t* out_
         DeviceGuard g(T.device);
         cudaStream_t st = T.stream;
         order_after_last_batch(T, st);
+        flush_for_read(T);
         const unsigned nn = run_dirty_compact(T, generation, st);
         const uint64_t k = std::min<uint64_t>(nn, cap);
         if (k) {
@@ -1402,6 +1423,7 @@ mpzch_status mpzch_serialize_snapshot(const mpzch_table* t, uint8_t* out, uint64
         DeviceGuard g(T.device);
         cudaStream_t st = T.stream;
         order_after_last_batch(T, st);
+        flush_for_read(T);
         // CRC over header | identities | weight count | weights (device sections on the GPU)
         uint32_t raw = crc32_raw_host(0, h.data(), h.size());
         raw = crc32_shift(raw, id_bytes) ^ crc32_raw_device((const uint8_t*)T.dev.ident, id_bytes, st, T.device);
@@ -1434,6 +1456,7 @@ mpzch_status mpzch_serialize_delta(mpzch_table* t, uint64_t generation, uint32_t
         DeviceGuard g(T.device);
         cudaStream_t st = T.stream;
         order_after_last_batch(T, st);
+        flush_for_read(T);
         const unsigned k = run_dirty_compact(T, generation, st);
         const uint64_t rec = 16 + 4ull * T.dim, body = k * rec;
         const uint64_t need = 32 + body + 4;
@@ -1461,6 +1484,33 @@ mpzch_status mpzch_serialize_delta(mpzch_table* t, uint64_t generation, uint32_t
         MPZCH_CUDA(cudaStreamSynchronize(st));
         *out_next_generation = T.gen_clock++;  // DeltaSource::cut: cursor_ = make_cursor()
     });
+}
+
+mpzch_status mpzch_set_reset_mode(mpzch_table* t, int mode) {
+    CHECK_T(t);
+    if (mode != MPZCH_RESET_EAGER && mode != MPZCH_RESET_DEFERRED) {
+        g_last_error = "unknown reset mode";
+        return MPZCH_EINVAL;
+    }
+    return guarded([&] {
+        Table& T = *t->t;
+        if (mode == MPZCH_RESET_EAGER) {
+            flush_for_read(T);
+            T.dev.pend_bits = nullptr;
+        } else if (T.dim > 0 && !T.dev.pend_bits) {
+            DeviceGuard g(T.device);
+            const uint64_t bytes = (T.held_rows() + 31) / 32 * 4;
+            T.pend_map.reserve(bytes);
+            MPZCH_CUDA(cudaMemsetAsync(T.pend_map.p, 0, bytes, T.stream));
+            MPZCH_CUDA(cudaStreamSynchronize(T.stream));
+            T.dev.pend_bits = T.pend_map.as<uint32_t>();
+        }
+    });
+}
+
+mpzch_status mpzch_flush_resets(mpzch_table* t) {
+    CHECK_T(t);
+    return guarded([&] { flush_for_read(*t->t); });
 }
 
 mpzch_status mpzch_set_path(mpzch_table* t, int path) {
@@ -1618,6 +1668,8 @@ mpzch_status mpzch_state_equals(const mpzch_table* a, const mpzch_table* b, int*
     return guarded([&] {
         const Table& A = *a->t;
         const Table& B = *b->t;
+        flush_for_read(A);
+        flush_for_read(B);
         *out_equal = 0;
         // table.cpp:249-260: capacities, dim, identities of every shard, weights (bitwise)
         if (A.caps != B.caps || A.dim != B.dim) return;
@@ -1693,6 +1745,7 @@ mpzch_status mpzch_copy_trained_range(const mpzch_table* t, uint64_t row0, uint6
     CHECK_T(t);
     return guarded([&] {
         const Table& T = *t->t;
+        flush_for_read(T);
         check_rows(T, row0, nrows);
         DeviceGuard g(T.device);
         MPZCH_CUDA(cudaStreamSynchronize(T.stream));

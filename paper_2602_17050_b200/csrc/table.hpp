@@ -107,6 +107,7 @@ public:
     uint64_t held_rows() const { return row_hi - row_lo; }
     uint64_t gen_clock = 1;  // MpzchTable::generation_clock_
     bool hole_free = true;   // SURVEY A.2 invariant; false after raw imports
+    bool resets_pending = false;  // MPZCH_RESET_DEFERRED: a batch may have marked rows pending
     int path_override = MPZCH_PATH_AUTO;
     uint64_t lru_fallbacks = 0;  // LRU batches that needed an eviction (claim attempt reverted)
     uint32_t lru_backoff = 0, lru_skip_left = 0;  // claim-attempt backoff after evictions
@@ -165,6 +166,7 @@ public:
     // a lock, so concurrent const lookups on one handle never share scratch or the error word
     DevBuf s_ldefer, l_ids, l_oslot, l_ooc;
     DevBuf sb_buf;  // process_shard_batch / reset_row / gather staging
+    DevBuf pend_map;  // MPZCH_RESET_DEFERRED: reset-pending bit per held row (dev.pend_bits)
     std::mutex lookup_mu;
     DevBuf s_tent;                                   // id table: 64-byte entries
     uint64_t tcap = 0;                               // allocated id-table capacity (pow2)
@@ -205,7 +207,10 @@ public:
 
 // kernel entry points (each .cu file), all enqueued on t.stream / stream
 void launch_init_table(Table& t);
+// eager: resets the listed rows; deferred (t.dev.deferred): marks them reset-pending
 void launch_reset_rows(Table& t, const uint64_t* rows, const unsigned int* count, cudaStream_t st);
+// writes every pending reset (deferred mode) before a reader that is not reset-aware
+void flush_resets(Table& t, cudaStream_t st);
 void launch_write_slots(Table& t, const uint64_t* gslots, const uint64_t* ids, const uint64_t* metas,
                         uint64_t n, cudaStream_t st);
 bool run_hole_check(Table& t);

@@ -19,6 +19,9 @@
 //                     warp applies them one after another (the reference's order);
 //   G6 k_sgd_clean    clears the used hash entries.
 // Positions at or after the first bad one are not applied, and no row is touched then.
+// Deferred resets (MPZCH_RESET_DEFERRED, rows.cu): a row the batch evicted is still marked
+// pending; its update starts from the closed-form draw_row and momentum 0 instead of reading
+// the row -- the reset and the step share one write of the row.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -41,27 +44,39 @@ __device__ __forceinline__ void sgd_quad(float4& w, float4& m, const float4 g, f
     w.w = __fsub_rn(w.w, __fmul_rn(lr, m.w));
 }
 
-// one position's update by `width` cooperating lanes (lane index `sub`)
+// one position's update by `width` cooperating lanes (lane index `sub`).  pend: the row's
+// eviction reset is deferred (rows.cu) -- the old row is the closed-form draw_row and momentum
+// 0, exactly what the reset would have written, so nothing is read and the row is written once
 __device__ __forceinline__ void apply_row(const TableDev& t, uint64_t row, const float* g,
                                           float lr, float beta, bool vec, unsigned sub,
-                                          unsigned width) {
+                                          unsigned width, bool pend) {
     float* w = t.weights + row * t.dim;
     float* m = t.momentum + row * t.dim;
+    const uint64_t s0 = pend ? mix64(row, t.init_seed) : 0;
     if (vec) {
         float4* w4 = reinterpret_cast<float4*>(w);
         float4* m4 = reinterpret_cast<float4*>(m);
         const float4* g4 = reinterpret_cast<const float4*>(g);
         for (uint32_t q = sub; q < t.dim / 4; q += width) {
-            float4 wv = w4[q], mv = m4[q];
+            float4 wv, mv;
+            if (pend) {
+                wv = draw_quad(s0, q, t.bound);
+                mv = make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+                wv = w4[q];
+                mv = m4[q];
+            }
             sgd_quad(wv, mv, __ldg(g4 + q), lr, beta);
             m4[q] = mv;
             w4[q] = wv;
         }
     } else {
         for (uint32_t j = sub; j < t.dim; j += width) {
-            const float mv = __fadd_rn(__fmul_rn(beta, m[j]), __ldg(g + j));
+            const float m0 = pend ? 0.f : m[j];
+            const float w0 = pend ? draw_elem(s0, j, t.bound) : w[j];
+            const float mv = __fadd_rn(__fmul_rn(beta, m0), __ldg(g + j));
             m[j] = mv;
-            w[j] = __fsub_rn(w[j], __fmul_rn(lr, mv));
+            w[j] = __fsub_rn(w0, __fmul_rn(lr, mv));
         }
     }
 }
@@ -137,10 +152,14 @@ __global__ void __launch_bounds__(256) k_sgd_apply(TableDev t, const uint64_t* _
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x / width;
     for (uint64_t i = gtid / width; i < lim; i += stride) {
         const uint32_t e = pe[i];
-        if (cnt[e] != 1) continue;  // repeated rows: k_sgd_dups
         const uint64_t row = rows[i];
-        apply_row(t, row, grads + i * t.dim, lr, beta, vec, sub, width);
+        // the pending bit (an L2 hit) is loaded in the same round as the occurrence count, so
+        // the deferred reset adds no dependent round trip (only this group touches the bit)
+        const bool pend = reset_pending(t, row);
+        if (cnt[e] != 1) continue;  // repeated rows: k_sgd_dups
+        apply_row(t, row, grads + i * t.dim, lr, beta, vec, sub, width, pend);
         if (sub == 0) {
+            if (pend) clear_pending(t, row);
             t.trained[row] = 1;
             if (bad == kEmpty) t.row_gen[row] = gen_clock;  // table.cpp:179
         }
@@ -175,14 +194,18 @@ __global__ void __launch_bounds__(256) k_sgd_dups(TableDev t, const uint64_t* __
         __syncwarp();
         const uint64_t row = rows[seg[0]];
         bool any = false;
+        const bool pend0 = reset_pending(t, row);
+        bool pend = pend0;
         for (unsigned a = 0; a < k; ++a) {
             const uint64_t i = seg[a];
             if (i >= bad) break;
-            apply_row(t, row, grads + i * t.dim, lr, beta, vec, lane, 32);
+            apply_row(t, row, grads + i * t.dim, lr, beta, vec, lane, 32, pend);
             __syncwarp();
+            pend = false;  // later occurrences read what the first one wrote
             any = true;
         }
         if (lane == 0 && any) {
+            if (pend0) clear_pending(t, row);
             t.trained[row] = 1;
             if (bad == kEmpty) t.row_gen[row] = gen_clock;
         }

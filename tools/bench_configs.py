@@ -426,14 +426,16 @@ def publish():
                 delta_gbs=len(delta) / delta_s / 1e9, crc32_device_gbs=rows * dim * 4 / crc_s / 1e9)
 
 
-def train():
+def train(reset_mode="eager", reference=True):
     """Not a BASELINE config: the reference's churn training loop (proj/src/experiments.cpp:86-125)
     at scale -- remap a batch (TTL evictions reset rows), then sgd_step over the distinct
     remapped rows -- on a 2^24-row dim-128 table (weights + momentum 16 GiB).  The reference
-    runs the same loop (process_batch + sgd_step) on a 2^20-row sample."""
+    runs the same loop (process_batch + sgd_step) on a 2^20-row sample.  reset_mode "deferred"
+    fuses each evicted row's reset into its sgd_step."""
     rows, dim, B = 1 << 24, 128, 1 << 20
     caps = mz.even_capacities(rows, 8)
     t = mz.MpzchTable(mz.TableConfig(caps, 128, 7, dim, 11))
+    t.set_reset_mode(reset_mode)
     pol = mz.EvictionPolicy.ttl(mz.TtlPolicy(3600))
     st = torch.cuda.current_stream()
     npre = int(0.8 * rows)
@@ -470,14 +472,14 @@ def train():
     steps = nb - 2
     step_ms = sum(tm.values()) / steps
     sgd_bytes = urows / steps * dim * 4 * 5  # grad read + weights/momentum read and write
-    out = dict(config="train (churn loop, 2^24 rows, dim 128, 1M-position batches)",
+    out = dict(config=f"train (churn loop, 2^24 rows, dim 128, 1M-position batches, {reset_mode} resets)",
                ids_per_s=B / (step_ms / 1e3), step_ms=step_ms,
                split_ms={k: v / steps for k, v in tm.items()}, distinct_rows=urows / steps,
                evicted_rows=evicted / nb,
                sgd_gbs=sgd_bytes / (tm["sgd"] / steps / 1e3) / 1e9)
     # reference: the same loop on a 2^20-row sample, 64K-position batches
     import pyoracle
-    if pyoracle.available("reference"):
+    if reference and pyoracle.available("reference"):
         pyoracle.lib("reference")["set_threads"](os.cpu_count() or 1)
         rrows, rB = 1 << 20, 1 << 16
         ref = pyoracle.OracleTable(mz.even_capacities(rrows, 8), 128, 7, dim, 11, kind="reference")
@@ -506,7 +508,12 @@ if __name__ == "__main__":
     out = []
     for w in which:
         torch.cuda.empty_cache()
-        res = [c1(1), c1(8)] if w == "c1" else [globals()[w]()]
+        if w == "c1":
+            res = [c1(1), c1(8)]
+        elif w == "train_deferred":
+            res = [train("deferred", reference=False)]
+        else:
+            res = [globals()[w]()]
         for r in res:
             out.append(r)
             print(json.dumps(r), flush=True)
