@@ -125,6 +125,63 @@ __global__ void __launch_bounds__(256) k_flush_pending(TableDev t) {
     }
 }
 
+__global__ void k_write_slots(TableDev t, const uint64_t* __restrict__ g, const uint64_t* __restrict__ ids,
+                              const uint64_t* __restrict__ metas, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        t.ident[g[i]] = ids[i];
+        t.meta[g[i]] = metas[i];
+    }
+}
+
+// Hole check: every id stored inside its own probe window at
+// offset o must see neither EMPTY nor another copy of itself in [home, home+o).
+__global__ void __launch_bounds__(256) k_hole_check(TableDev t, unsigned* bad) {
+    for (uint64_t g = t.row_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < t.row_hi;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t id = t.ident[g];
+        if (id == kEmpty) continue;
+        if (id >> 63) { atomicExch(bad, 1u); continue; }  // stray claim word
+        const uint32_t s = shard_of(id, t);
+        const ShardDev sd = t.shards[s];
+        // the id must live in its own shard's segment to be reachable; if it does
+        // not, it is a foreign occupant for everybody and cannot create a hole
+        if (g < sd.offset || g >= sd.offset + sd.cap.d) continue;
+        const uint64_t h = home_of(id, sd, t.seed);
+        const uint64_t loc = g - sd.offset;
+        const uint64_t o = loc >= h ? loc - h : loc + sd.cap.d - h;
+        if (o >= t.P) continue;  // outside its window: invisible, harmless
+        uint64_t x = h;
+        for (uint64_t k = 0; k < o; ++k) {
+            const uint64_t v = t.ident[sd.offset + x];
+            if (v == kEmpty || v == id) { atomicExch(bad, 1u); break; }
+            if (++x == sd.cap.d) x = 0;
+        }
+    }
+}
+
+// Delta cut gather (DeltaSource::cut, proj/src/publish.cpp:288-305): for each dirty row,
+// its identity word and its weights.  One warp per row, 16-byte copies.
+__global__ void __launch_bounds__(256) k_gather_rows(TableDev t, const uint64_t* __restrict__ rows,
+                                                     uint64_t n, uint64_t* __restrict__ out_ids,
+                                                     float* __restrict__ out_w) {
+    const unsigned lane = lane_id();
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+        const uint64_t row = rows[r];
+        if (lane == 0) out_ids[r] = t.ident[row];
+        if (!out_w) continue;
+        const float* src = t.weights + row * t.dim;
+        float* dst = out_w + r * t.dim;
+        if ((t.dim & 3u) == 0) {
+            for (uint32_t q = lane; q < t.dim / 4; q += 32)
+                reinterpret_cast<float4*>(dst)[q] = reinterpret_cast<const float4*>(src)[q];
+        } else {
+            for (uint32_t j = lane; j < t.dim; j += 32) dst[j] = src[j];
+        }
+    }
+}
+
 }  // namespace
 
 void run_gather_rows(const Table& t, const uint64_t* rows, uint64_t n, uint64_t* out_ids, float* out_w,
