@@ -21,11 +21,12 @@ run_latency_bench does, proj/src/experiments.cpp:325,347).
             cpu_baseline times 3 of those batches, --impl reference K of them.
 
 Multi-GPU (torchrun, N>1): the same 1B-slot table row-sharded over the N ranks (each holds
-8/N logical shards), every 4M-position batch split into N slices, ids routed to owners and
-results routed back over peer memory (route-scatter / return-scatter kernels storing into the
-other ranks' CUDA-IPC-mapped buffers over NVLink; MPZCH_TRANSPORT=collective uses the NCCL
-all-to-all instead, paper_2602_17050_b200/sharded.py) -- strong scaling of the fixed C5
-workload.
+8/N logical shards), every 4M-position batch split into N slices -- strong scaling of the fixed
+C5 workload.  Default MPZCH_TRANSPORT=device: the device-side protocol of csrc/sharded.cu (ids to
+owners and results back by stores into the other ranks' CUDA-IPC-mapped exchange regions over
+NVLink, system-scope flags between the phases, every phase on the stream, one host wait per
+batch, batches pipelined by ticket); MPZCH_TRANSPORT=peer|collective run the host-driven
+protocol of paper_2602_17050_b200/sharded.py (peer stores or the NCCL all-to-all).
 """
 import argparse
 import json
@@ -296,14 +297,17 @@ def run_reference(steps: int, warmup: int, rows: int = ROWS, log=print):
                 threads_effective=min(cores, SHARDS) if kind == "reference" else 1)
 
 
-def c5_config(rows, world, backend="nccl", transport="peer"):
+def c5_config(rows, world, backend="nccl", transport="device"):
     """The workload dict both arms print (same_config)."""
     return {"workload": ("C5: 1B-slot (2^30-row) table" if rows == ROWS else
                          f"C5-shaped {rows}-row table") + ", S=8 logical shards, "
                         "max_probe=128, load 0.8 prefilled via the API, 4M-position "
                         "batches 90% hit / 10% fresh, eviction Disabled"
                         + ("" if world == 1 else f"; row-sharded over {world} GPUs, "
-                           + ("peer-memory id routing (IPC stores, "
+                           + ("device-side protocol (ids and results by stores into the peers' "
+                              "exchange regions over NVLink / CUDA IPC, system-scope flags, one "
+                              "host wait per batch)" if transport == "device" else
+                              "peer-memory id routing (IPC stores, "
                               f"{backend} barrier)" if transport == "peer" else
                               f"{backend} all-to-all id routing")),
             "rows": rows, "num_shards": SHARDS, "max_probe": MAX_PROBE,
@@ -339,7 +343,7 @@ def main():
                 "vs_baseline": None, "dtype": "u64",
                 "data": "synthetic (DistinctIdStream ids, SplitMix64 sampler)",
                 "config": c5_config(args.rows, world, os.environ.get("MPZCH_DIST_BACKEND", "nccl"),
-                                    os.environ.get("MPZCH_TRANSPORT", "peer")),
+                                    os.environ.get("MPZCH_TRANSPORT", "device")),
                 "cpu_baseline": {"value": r["value"], "unit": "IDs/s", "cores": r["cores"],
                                  "threads_effective": r["threads_effective"],
                                  "kind": r["kind"], "sample": r["sample"], "host": host_cpu()},
@@ -354,7 +358,7 @@ def main():
     # on cuda:0 and collectives staged through the host: a functional check of the N>1 code
     # on a single-GPU box, never a scaling number
     backend = os.environ.get("MPZCH_DIST_BACKEND", "nccl")
-    transport = os.environ.get("MPZCH_TRANSPORT", "peer")
+    transport = os.environ.get("MPZCH_TRANSPORT", "device")
     share = os.environ.get("MPZCH_SHARE_GPU", "0") == "1"
     if world > 1:
         import torch.distributed as dist
@@ -385,9 +389,27 @@ def main():
 
         def remap_async(ids, now):  # enqueue only; the ticket is waited after the loop
             return table.process_batch_device_async(ids, now, pol, None, out_s, out_o, None, stream)
-    else:
+    elif transport == "device":
         # C5 row-sharded: the S=8 logical shards of ONE 1B-slot table spread over the ranks;
-        # every global batch of BATCH positions is split into rank slices (strong scaling)
+        # every global batch of BATCH positions is split into rank slices (strong scaling).
+        # The device-side protocol (csrc/sharded.cu): ids out / results back by stores into the
+        # peers' exchange regions (CUDA IPC over NVLink), every phase on the stream, one host
+        # wait per batch; torch.distributed only carries the 128-byte export records once
+        sharded = mz.ShardedRank(cfg, rank, world, BATCH, device=dev)
+        recs = [None] * world
+        torch.distributed.all_gather_object(recs, sharded.export())
+        sharded.connect_ipc(recs)
+        probe_table = sharded.table
+        table = sharded  # .wait(ticket)
+
+        def remap(ids, now):
+            sharded.process_batch_device(ids, now, pol, None, out_s, out_o, None, stream)
+
+        def remap_async(ids, now):
+            return sharded.process_batch_device_async(ids, now, pol, None, out_s, out_o, None, stream)
+    else:
+        # the host-driven protocol (paper_2602_17050_b200/sharded.py): peer stores or NCCL
+        # all-to-all, with host collectives between the phases
         from paper_2602_17050_b200.sharded import ShardedMpzchTable, TorchComm
         sharded = ShardedMpzchTable(cfg, TorchComm(), device=dev, transport=transport)
         probe_table = sharded.engine.table
@@ -396,6 +418,7 @@ def main():
             sharded.process_batch(ids, now, pol)
 
         remap_async = None  # the sharded protocol synchronises on its collectives
+    stats_of = sharded.last_stats if (world > 1 and transport == "device") else probe_table.last_stats
 
     def my_slice(lo, hi):
         n = hi - lo
@@ -446,11 +469,11 @@ def main():
             tickets = [remap_async(batches[b], 2 + b) for b in timed]
             for tk in tickets:
                 table.wait(tk)
-                stats.append(probe_table.last_stats())
+                stats.append(stats_of())
         else:
             for b in timed:
                 remap(batches[b], 2 + b)
-                stats.append(probe_table.last_stats())
+                stats.append(stats_of())
         ev1.record(stream)
         torch.cuda.synchronize(dev)
         ms_total = ev0.elapsed_time(ev1)
@@ -578,6 +601,18 @@ def main():
                                 out_slots=pin_s.numpy().view(np.uint64), out_outcomes=pin_o.numpy(),
                                 out_evicted=pin_ev)
         e2e_sync_value = BATCH * min(3, e2e_steps) / (time.perf_counter() - t1)
+    elif transport == "device":
+        t0 = time.perf_counter()
+        for i in range(e2e_steps):
+            d = e2e_batches[i].to(dev, non_blocking=True)
+            sharded.process_batch_device(d, 100 + i, pol, None, out_s, out_o, None, stream)
+            pin_s.copy_(out_s[:nloc], non_blocking=True)
+            pin_o.copy_(out_o[:nloc], non_blocking=True)
+            torch.cuda.synchronize(dev)
+        e2e_s = time.perf_counter() - t0
+        e2e_api = "mpzch_sharded_process_batch (pinned host slices, H2D/D2H timed)"
+        e2e_sync_value = None
+        pcie_bound = None
     else:
         t0 = time.perf_counter()
         for i in range(e2e_steps):

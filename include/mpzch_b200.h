@@ -375,6 +375,60 @@ mpzch_status mpzch_gather(const mpzch_table* t, const uint64_t* rows, uint64_t n
 mpzch_status mpzch_shard_config(const mpzch_table* t, uint32_t shard, uint64_t* capacity,
                                 uint32_t* max_probe, uint64_t* seed);
 
+/* ---- row-sharded table, device-side protocol (replaces the reference's shard loop
+ * proj/src/batch_engine.cpp:160-211 across GPUs).  One mpzch_sharded per rank (one process per
+ * GPU, or several ranks in one process): rank r of G holds the logical shards {s : s*G/S == r}
+ * (global rows of the single-table layout, so every slot is identical for any G).  Each rank
+ * passes its contiguous slice of the global batch (slices in rank order); ids go to their
+ * owners and results come back by stores into peer memory (NVLink P2P / CUDA IPC), with every
+ * phase enqueued on `stream`: one host wait per batch (the wait call).  Errors are agreed on the
+ * device and raised on every rank with the reference's text and precedence ("invalid id at
+ * batch position N" with the GLOBAL position, length, TTL overflow).  The evicted list is the
+ * global canonical one on every rank.  max_batch bounds the GLOBAL batch (exchange buffers).
+ * Every rank must call process_batch the same number of times (a collective); a peer that
+ * stops answering fails the batch after MPZCH_PEER_TIMEOUT_MS (default 60000) with MPZCH_ENCCL.
+ * LRU batches, tables with raw-imported holes and forced paths take one extra host round trip. */
+typedef struct mpzch_sharded mpzch_sharded;
+#define MPZCH_SHARDED_RECORD_BYTES 128
+mpzch_status mpzch_sharded_create(const uint64_t* capacities, uint32_t num_shards, uint32_t max_probe,
+                                  uint64_t seed, uint32_t dim, uint64_t init_seed, int device,
+                                  uint32_t rank, uint32_t world, uint64_t max_batch,
+                                  mpzch_sharded** out);
+mpzch_status mpzch_sharded_destroy(mpzch_sharded* s);
+/* the rank's table (held shards only) for the accessors; owned by `s`, never destroy it */
+mpzch_table* mpzch_sharded_table(mpzch_sharded* s);
+mpzch_status mpzch_sharded_held_shards(const mpzch_sharded* s, uint32_t* shard_lo, uint32_t* shard_hi);
+/* multi-process: export this rank's exchange region (CUDA IPC), gather every rank's record in
+ * rank order by any host channel, then connect */
+mpzch_status mpzch_sharded_export(const mpzch_sharded* s, uint8_t* out_record);
+mpzch_status mpzch_sharded_connect_ipc(mpzch_sharded* s, const uint8_t* records);
+/* single process: connect `world` ranks (rank order; P2P is enabled between their GPUs) */
+mpzch_status mpzch_sharded_connect_local(mpzch_sharded* const* ranks, uint32_t world);
+/* device buffers, stream-ordered; the ticket is waited by mpzch_sharded_wait */
+mpzch_status mpzch_sharded_process_batch_async(mpzch_sharded* s, const uint64_t* ids,
+                                               const uint32_t* features, uint64_t n, uint64_t now,
+                                               const mpzch_policy* policy, uint64_t* out_slots,
+                                               uint8_t* out_outcomes, uint64_t* out_evicted,
+                                               uint64_t evicted_cap, void* stream, uint64_t* out_ticket);
+mpzch_status mpzch_sharded_wait(mpzch_sharded* s, uint64_t ticket, uint64_t* out_evicted_n);
+mpzch_status mpzch_sharded_process_batch(mpzch_sharded* s, const uint64_t* ids, const uint32_t* features,
+                                         uint64_t n, uint64_t now, const mpzch_policy* policy,
+                                         uint64_t* out_slots, uint8_t* out_outcomes,
+                                         uint64_t* out_evicted, uint64_t evicted_cap,
+                                         uint64_t* out_evicted_n, void* stream);
+/* single process, whole batch: process_batch (batch_engine.hpp:44-46) over `world` connected
+ * ranks (rank order) with HOST buffers -- the batch is split into contiguous slices, staged,
+ * every rank's batch enqueued before any wait, results copied back (the evicted list from
+ * rank 0; every rank holds the same one).  The reference's call, spread over the GPUs. */
+mpzch_status mpzch_sharded_group_process_batch(mpzch_sharded* const* ranks, uint32_t world,
+                                               const uint64_t* ids, const uint32_t* features, uint64_t n,
+                                               uint64_t now, const mpzch_policy* policy,
+                                               uint64_t* out_slots, uint8_t* out_outcomes,
+                                               uint64_t* out_evicted, uint64_t evicted_cap,
+                                               uint64_t* out_evicted_n);
+/* the last waited batch: this rank's owner-side counts; host_waits = host round trips it took */
+mpzch_status mpzch_sharded_last_stats(const mpzch_sharded* s, mpzch_batch_stats* out, int* out_host_waits);
+
 /* ---- execution control / introspection */
 mpzch_status mpzch_set_path(mpzch_table* t, int path);
 /* Embedding-row reset of evicted slots ("fused sgd_step with reset").

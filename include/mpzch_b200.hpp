@@ -19,6 +19,7 @@
 // process_batch_with_evicted().
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <map>
 #include <new>
@@ -584,6 +585,101 @@ inline std::vector<ProbeResult> process_batch(MpzchTable& table, const IdBatch& 
                                               const EvictionPolicy& policy,
                                               ExecMode = ExecMode::Parallel) {
     return process_batch_with_evicted(table, batch, policy, nullptr);
+}
+
+// The row-sharded table over several GPUs of one process (mpzch_sharded_* in
+// mpzch_b200.h): rank r holds the logical shards {s : s*G/S == r} on devices[r] (a device may
+// repeat), global rows are the single table's, and process_batch takes the reference's whole
+// batch -- split into rank slices, every rank's protocol enqueued before any wait -- and returns
+// exactly what mpzch::process_batch returns for the same layout.  A B200 extension: the
+// reference runs its shards in one process (proj/src/batch_engine.cpp:203-211).
+class ShardedMpzchTable {
+public:
+    ShardedMpzchTable(const TableConfig& cfg, const std::vector<int>& devices, std::uint64_t max_batch)
+        : cfg_(cfg) {
+        const std::uint32_t G = static_cast<std::uint32_t>(devices.size());
+        ranks_.assign(G, nullptr);
+        try {
+            for (std::uint32_t r = 0; r < G; ++r)
+                check(mpzch_sharded_create(cfg.shard_capacities.data(),
+                                           static_cast<std::uint32_t>(cfg.shard_capacities.size()),
+                                           cfg.max_probe, cfg.seed, cfg.dim, cfg.init_seed, devices[r], r, G,
+                                           max_batch, &ranks_[r]));
+            check(mpzch_sharded_connect_local(ranks_.data(), G));
+        } catch (...) {
+            release();
+            throw;
+        }
+    }
+    ShardedMpzchTable(const ShardedMpzchTable&) = delete;
+    ShardedMpzchTable& operator=(const ShardedMpzchTable&) = delete;
+    ~ShardedMpzchTable() { release(); }
+
+    std::uint32_t num_ranks() const { return static_cast<std::uint32_t>(ranks_.size()); }
+    std::uint32_t num_shards() const { return static_cast<std::uint32_t>(cfg_.shard_capacities.size()); }
+    // the rank holding logical shard s (contiguous blocks)
+    std::uint32_t owner_of(std::uint32_t s) const {
+        return static_cast<std::uint32_t>(std::uint64_t(s) * num_ranks() / num_shards());
+    }
+    mpzch_table* rank_table(std::uint32_t r) const { return mpzch_sharded_table(ranks_.at(r)); }
+
+    // MpzchTable::identities(s) / metadata(s) (table.hpp:89-90), from the owning rank
+    std::vector<std::uint64_t> identities(std::uint32_t s) const { return shard_words(s, false); }
+    std::vector<std::uint64_t> metadata(std::uint32_t s) const { return shard_words(s, true); }
+
+    std::vector<ProbeResult> process_batch(const IdBatch& batch, const EvictionPolicy& policy,
+                                           std::vector<std::uint64_t>* evicted = nullptr) {
+        const std::size_t n = batch.ids.size();
+        std::vector<std::uint64_t> ids(n), slots(n);
+        std::vector<std::uint32_t> feats(n);
+        std::vector<std::uint8_t> oc(n);
+        bool any_feature = false;
+        for (std::size_t i = 0; i < n; ++i) {
+            ids[i] = batch.ids[i].id;
+            feats[i] = batch.ids[i].feature;
+            any_feature |= feats[i] != 0;
+        }
+        std::vector<std::uint64_t> ev(evicted ? std::max<std::size_t>(n, 1) : 0);
+        std::uint64_t nev = 0;
+        check(mpzch_sharded_group_process_batch(ranks_.data(), num_ranks(), ids.data(),
+                                                any_feature ? feats.data() : nullptr, n, batch.now,
+                                                policy.c_policy(), slots.data(), oc.data(),
+                                                evicted ? ev.data() : nullptr, ev.size(), &nev));
+        std::vector<ProbeResult> out(n);
+        for (std::size_t i = 0; i < n; ++i)
+            out[i] = {slots[i], oc[i] == MPZCH_EVICTED, static_cast<Outcome>(oc[i])};
+        if (evicted) {
+            ev.resize(nev);
+            *evicted = std::move(ev);
+        }
+        return out;
+    }
+
+private:
+    std::vector<std::uint64_t> shard_words(std::uint32_t s, bool meta) const {
+        if (s >= num_shards()) throw std::out_of_range("shard index out of range");
+        std::uint64_t off = 0;
+        for (std::uint32_t k = 0; k < s; ++k) off += cfg_.shard_capacities[k];
+        std::vector<std::uint64_t> v(cfg_.shard_capacities[s]);
+        const mpzch_table* t = rank_table(owner_of(s));
+        check(meta ? mpzch_copy_metadata_range(t, off, v.size(), v.data())
+                   : mpzch_copy_identities_range(t, off, v.size(), v.data()));
+        return v;
+    }
+    void release() {
+        for (auto*& r : ranks_)
+            if (r) {
+                mpzch_sharded_destroy(r);
+                r = nullptr;
+            }
+    }
+    TableConfig cfg_;
+    std::vector<mpzch_sharded*> ranks_;
+};
+
+inline std::vector<ProbeResult> process_batch(ShardedMpzchTable& table, const IdBatch& batch,
+                                              const EvictionPolicy& policy, ExecMode = ExecMode::Parallel) {
+    return table.process_batch(batch, policy);
 }
 
 }  // namespace mpzch_b200

@@ -188,6 +188,22 @@ _SIGS = {
                                              _vp, ctypes.c_uint64, _u64p, _u64p]),
     "mpzch_set_path": (ctypes.c_int, [_vp, ctypes.c_int]),
     "mpzch_set_reset_mode": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "mpzch_sharded_create": (ctypes.c_int, [_u64p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64,
+                                            ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint32,
+                                            ctypes.c_uint32, ctypes.c_uint64, ctypes.POINTER(_vp)]),
+    "mpzch_sharded_destroy": (ctypes.c_int, [_vp]),
+    "mpzch_sharded_table": (_vp, [_vp]),
+    "mpzch_sharded_held_shards": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_uint32),
+                                                 ctypes.POINTER(ctypes.c_uint32)]),
+    "mpzch_sharded_export": (ctypes.c_int, [_vp, _vp]),
+    "mpzch_sharded_connect_ipc": (ctypes.c_int, [_vp, _vp]),
+    "mpzch_sharded_connect_local": (ctypes.c_int, [ctypes.POINTER(_vp), ctypes.c_uint32]),
+    "mpzch_sharded_process_batch_async": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_uint64, ctypes.c_uint64, _vp,
+                                                         _vp, _vp, _vp, ctypes.c_uint64, _vp, _u64p]),
+    "mpzch_sharded_wait": (ctypes.c_int, [_vp, ctypes.c_uint64, _u64p]),
+    "mpzch_sharded_process_batch": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_uint64, ctypes.c_uint64, _vp,
+                                                   _vp, _vp, _vp, ctypes.c_uint64, _u64p, _vp]),
+    "mpzch_sharded_last_stats": (ctypes.c_int, [_vp, ctypes.POINTER(_Stats), ctypes.POINTER(ctypes.c_int)]),
     "mpzch_flush_resets": (ctypes.c_int, [_vp]),
     "mpzch_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),
     "mpzch_get_profile": (ctypes.c_int, [_vp, ctypes.POINTER(_Profile)]),
@@ -375,7 +391,19 @@ class MpzchTable:
             _check(lib.mpzch_table_create_sharded(cp, len(caps), cfg.max_probe, cfg.seed, cfg.dim,
                                                   cfg.init_seed, device, shard_range[0],
                                                   shard_range[1], ctypes.byref(h)))
+        self._attach(h, lib, cfg, device, owned=True)
+
+    @classmethod
+    def _view(cls, h, cfg: TableConfig, device: int) -> "MpzchTable":
+        """A non-owning wrapper of a handle another object owns (a row-sharded rank's table)."""
+        t = cls.__new__(cls)
+        t._attach(h, load_library(), cfg, device, owned=False)
+        return t
+
+    def _attach(self, h, lib, cfg: TableConfig, device: int, owned: bool):
+        caps = np.ascontiguousarray(np.array(list(cfg.shard_capacities), dtype=np.uint64))
         self._h = h
+        self._owned = owned
         self._lib = lib
         self.cfg = cfg
         self.device = device
@@ -397,7 +425,8 @@ class MpzchTable:
 
     def close(self):
         if getattr(self, "_h", None):
-            self._lib.mpzch_table_destroy(self._h)
+            if getattr(self, "_owned", True):
+                self._lib.mpzch_table_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -854,6 +883,106 @@ def crc32_device(t) -> int:
                                              t.numel() * t.element_size(), ctypes.byref(c),
                                              ctypes.c_void_p(st.cuda_stream)))
     return c.value
+
+
+SHARDED_RECORD_BYTES = 128
+
+
+class ShardedRank:
+    """One rank of a row-sharded table with the device-side protocol (mpzch_sharded_*):
+    rank r of `world` holds the logical shards {s : s*world//S == r}; every process_batch is a
+    collective over the ranks (each passes its contiguous slice of the global batch, slices in
+    rank order), enqueued on the stream with one host wait.  Returns this slice's slots and
+    outcomes and the GLOBAL canonical evicted list (identical on every rank).  Errors are raised
+    on every rank with the reference's text (the GLOBAL position of the first invalid id)."""
+
+    def __init__(self, cfg: TableConfig, rank: int, world: int, max_batch: int, device: int = 0):
+        lib = load_library()
+        caps = np.ascontiguousarray(np.array(list(cfg.shard_capacities), dtype=np.uint64))
+        h = _vp()
+        _check(lib.mpzch_sharded_create(caps.ctypes.data_as(_u64p), len(caps), cfg.max_probe, cfg.seed,
+                                        cfg.dim, cfg.init_seed, device, rank, world, max_batch,
+                                        ctypes.byref(h)))
+        self._h, self._lib = h, lib
+        self.rank, self.world, self.device, self.max_batch = rank, world, device, max_batch
+        self.cfg = cfg
+        self.table = MpzchTable._view(_vp(lib.mpzch_sharded_table(h)), cfg, device)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.table._h = None
+            self._lib.mpzch_sharded_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def export(self) -> bytes:
+        buf = (ctypes.c_uint8 * SHARDED_RECORD_BYTES)()
+        _check(self._lib.mpzch_sharded_export(self._h, buf))
+        return bytes(buf)
+
+    def connect_ipc(self, records):
+        """records: every rank's export() in rank order (gathered by any host channel)."""
+        blob = b"".join(records)
+        buf = (ctypes.c_uint8 * len(blob)).from_buffer_copy(blob)
+        _check(self._lib.mpzch_sharded_connect_ipc(self._h, buf))
+
+    @staticmethod
+    def connect_local(ranks):
+        arr = (_vp * len(ranks))(*[r._h for r in ranks])
+        _check(load_library().mpzch_sharded_connect_local(arr, len(ranks)))
+
+    def process_batch_device_async(self, ids, now: int, policy: EvictionPolicy, features=None,
+                                   out_slots=None, out_outcomes=None, out_evicted=None, stream=None) -> int:
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        tk = ctypes.c_uint64(0)
+        _check(self._lib.mpzch_sharded_process_batch_async(
+            self._h, ctypes.c_void_p(ids.data_ptr()),
+            ctypes.c_void_p(features.data_ptr()) if features is not None else None, ids.numel(), now,
+            ctypes.byref(policy._c), ctypes.c_void_p(out_slots.data_ptr()),
+            ctypes.c_void_p(out_outcomes.data_ptr()),
+            ctypes.c_void_p(out_evicted.data_ptr()) if out_evicted is not None else None,
+            out_evicted.numel() if out_evicted is not None else 0, ctypes.c_void_p(st.cuda_stream),
+            ctypes.byref(tk)))
+        return tk.value
+
+    def wait(self, ticket: int) -> int:
+        nev = ctypes.c_uint64(0)
+        _check(self._lib.mpzch_sharded_wait(self._h, ticket, ctypes.byref(nev)))
+        return nev.value
+
+    def process_batch_device(self, ids, now: int, policy: EvictionPolicy, features=None, out_slots=None,
+                             out_outcomes=None, out_evicted=None, stream=None) -> int:
+        return self.wait(self.process_batch_device_async(ids, now, policy, features, out_slots,
+                                                         out_outcomes, out_evicted, stream))
+
+    def process_batch(self, ids, now: int, policy: EvictionPolicy, features=None):
+        """Host arrays in, host arrays out: (slots, outcomes, global evicted list)."""
+        import torch
+        dev = f"cuda:{self.device}"
+        n = int(np.asarray(ids).size)
+        ids_t = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.uint64).view(np.int64)).to(dev)
+        f_t = None if features is None else torch.from_numpy(
+            np.ascontiguousarray(features, dtype=np.uint32).view(np.int32)).to(dev)
+        s_t = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        o_t = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+        e_t = torch.empty(self.max_batch, dtype=torch.int64, device=dev)
+        k = self.process_batch_device(ids_t, now, policy, f_t, s_t, o_t, e_t)
+        return (s_t[:n].cpu().numpy().view(np.uint64), o_t[:n].cpu().numpy(),
+                e_t[:min(k, self.max_batch)].cpu().numpy().view(np.uint64))
+
+    def last_stats(self) -> dict:
+        s = _Stats()
+        hw = ctypes.c_int(0)
+        _check(self._lib.mpzch_sharded_last_stats(self._h, ctypes.byref(s), ctypes.byref(hw)))
+        d = {f: getattr(s, f) for f, _ in _Stats._fields_}
+        d["host_waits"] = hw.value
+        return d
 
 
 def crc32_device_ptr(ptr: int, nbytes: int) -> int:

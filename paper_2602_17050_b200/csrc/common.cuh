@@ -165,6 +165,13 @@ struct BatchErr {
     unsigned long long foreign_pos;  // min position whose shard this handle does not hold
 };
 
+// The part of a row-sharded rank's per-batch device state the owner's remap reads
+// (sharded.cu keeps the full record; this is its prefix).
+struct ShStateView {
+    unsigned long long failed;  // some rank's slice failed validation (or a peer timed out)
+    unsigned long long R;       // positions received by this owner in this batch
+};
+
 __device__ __forceinline__ bool batch_failed(const BatchErr* e) {
     return e->bad_pos != ~0ull || e->overflow != 0 || e->too_many != 0 || e->foreign_pos != ~0ull;
 }
@@ -194,6 +201,16 @@ __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 // predecessor in the stream drains; it waits here (before touching anything the predecessor
 // wrote) for the predecessor's completion and memory flush.  A no-op without the attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Lazy module loading (the CUDA 12 default) loads a kernel at its first launch, and a load can
+// wait for the device's running work.  The row-sharded protocol has kernels that spin until a
+// peer's kernels run, so every kernel a batch can launch is loaded up front (cudaFuncGetAttributes
+// forces the load); see preload_all_kernels.
+inline void preload_kernel(const void* k) {
+    cudaFuncAttributes a;
+    const cudaError_t e = cudaFuncGetAttributes(&a, k);
+    if (e != cudaSuccess) (void)cudaGetLastError();
+}
 
 template <class T>
 struct same_type { using type = T; };

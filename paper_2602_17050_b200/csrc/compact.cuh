@@ -138,4 +138,12 @@ inline void compact_flags(uint8_t* flags, uint64_t n, unsigned* blk, unsigned* t
     launches += 3;
 }
 
+// force-load this translation unit's compaction kernels for Emit (see preload_all_kernels)
+template <class Emit>
+inline void preload_compact() {
+    preload_kernel((const void*)k_compact_count);
+    preload_kernel((const void*)k_compact_scan);
+    preload_kernel((const void*)k_compact_write<Emit>);
+}
+
 }  // namespace mpzch_b200

@@ -120,7 +120,19 @@ __global__ void k_init_counters(BatchCounters* c) {
         BatchCounters z{};
         z.err.bad_pos = ~0ull;
         z.err.foreign_pos = ~0ull;
+        z.n_live = ~0ull;
         *c = z;
+    }
+}
+
+// row-sharded owner (sharded.cu): the batch's fate was decided by the ranks together -- on any
+// error every kernel below skips (the host reports it from the shared state); otherwise the
+// received count bounds every position loop (n_live)
+__global__ void k_sh_adopt(BatchCounters* c, const ShStateView* st) {
+    pdl_wait();
+    if (threadIdx.x == 0) {
+        if (st->failed) c->err.overflow = 1;
+        else c->n_live = st->R;
     }
 }
 
@@ -194,7 +206,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
     const unsigned lane = lane_id();
     const uint64_t tile = (uint64_t)blockDim.x * U;
     unsigned long long my_found = 0, my_coll = 0, my_isec = 0, my_msec = 0;
-    const uint64_t total = RESUME ? (uint64_t)*(volatile unsigned*)&ctr->deferred : n;
+    const uint64_t total = RESUME ? (uint64_t)*(volatile unsigned*)&ctr->deferred : min(n, (uint64_t)ctr->n_live);
     for (uint64_t t0 = (uint64_t)blockIdx.x * tile; t0 < total; t0 += (uint64_t)gridDim.x * tile) {
         uint64_t id[U], g[U], base[U], cap[U], h[U];
         uint32_t pos[RESUME ? U : 1];  // RESUME: the handed-over positions
@@ -398,7 +410,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
     const uint64_t qib = threadIdx.x >> 2;
     const uint64_t tile = qpb * U;
     unsigned long long my_found = 0, my_coll = 0, my_isec = 0, my_msec = 0;
-    const uint64_t total = RESUME ? (uint64_t)*(volatile unsigned*)&ctr->deferred : n;
+    const uint64_t total = RESUME ? (uint64_t)*(volatile unsigned*)&ctr->deferred : min(n, (uint64_t)ctr->n_live);
     for (uint64_t t0 = (uint64_t)blockIdx.x * tile; t0 < total; t0 += (uint64_t)gridDim.x * tile) {
         uint64_t id[U], g[U];
         uint32_t pos[RESUME ? U : 1];
@@ -913,6 +925,7 @@ __global__ void __launch_bounds__(256) k_pf_group(const BatchCounters* ctr, cons
                                                   PfEntry* tab, uint64_t mask, uint32_t* __restrict__ ent) {
     pdl_wait();
     if (batch_failed(&ctr->err)) return;
+    n = min(n, (uint64_t)ctr->n_live);
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t id = ids[i];
         const uint32_t f = feats[i];
@@ -929,6 +942,7 @@ __global__ void __launch_bounds__(256) k_pf_slot(const BatchCounters* ctr, uint6
                                                  uint64_t mask, uint32_t* __restrict__ sent) {
     pdl_wait();
     if (batch_failed(&ctr->err)) return;
+    n = min(n, (uint64_t)ctr->n_live);
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         if (~(uint32_t)__ldcg(&gtab[gent[i]].rank) != (uint32_t)i) continue;  // not its group's first
         const uint64_t g = out_slots[i];
@@ -948,6 +962,7 @@ __global__ void __launch_bounds__(256) k_pf_write(TableDev t, const BatchCounter
                                                   uint32_t nk) {
     pdl_wait();
     if (batch_failed(&ctr->err)) return;
+    n = min(n, (uint64_t)ctr->n_live);
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         if (~(uint32_t)__ldcg(&gtab[gent[i]].rank) != (uint32_t)i) continue;
         if ((uint32_t)__ldcg(&stab[sent[i]].rank) != (uint32_t)i) continue;  // a later group wrote last
@@ -985,6 +1000,7 @@ __global__ void __launch_bounds__(256) k_lru_found(BatchCounters* ctr, uint64_t 
                                                    PfEntry* ftab, uint64_t mask, uint32_t ep) {
     pdl_wait();
     if (batch_failed(&ctr->err) || ctr->lru_evict == 0) return;
+    n = min(n, (uint64_t)ctr->n_live);
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         if (out_oc[i] != kFound) continue;
         const uint64_t g = out_slots[i];
@@ -1079,6 +1095,7 @@ __global__ void __launch_bounds__(256) k_lru_meta(TableDev t, const BatchCounter
                                                   uint64_t meta_value) {
     pdl_wait();
     if (batch_failed(&ctr->err) || ctr->lru_abort) return;
+    n = min(n, (uint64_t)ctr->n_live);
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         t.meta[out_slots[i]] = meta_value;
 }
@@ -1121,6 +1138,23 @@ __global__ void __launch_bounds__(256) k_finalize(BatchCounters* ctr,
 
 }  // namespace
 
+void preload_remap_kernels() {
+#define PL(k) preload_kernel((const void*)(k))
+    PL(k_init_counters); PL(k_sh_adopt); PL(k_validate);
+    PL((k_probe_line<kModeTtl, 2, 3, true>)); PL((k_probe_line<kModeTtl, 2, 3>));
+    PL((k_probe_line<kModeLru, 2, 4>)); PL((k_probe_line<kModeDisabled, 1, 8>));
+    PL((k_probe_line<kModeDisabled, 2, 4>)); PL((k_probe_line<kModeTtl, 1, 4, true, true>));
+    PL((k_probe_line<kModeTtl, 1, 4, false, true>));
+    PL((k_probe<kModeTtl, 2, 3, true, false, true>)); PL((k_probe<kModeTtl, 2, 3, true>));
+    PL((k_probe<kModeTtl, 2, 3, false, false, true>)); PL((k_probe<kModeTtl, 2, 3>));
+    PL((k_probe<kModeLru, 1, 6>)); PL((k_probe<kModeDisabled, 1, 6>));
+    PL(k_dedup); PL(k_claim<kModeDisabled>); PL(k_claim<kModeTtl>); PL(k_claim<kModeLru>);
+    PL((k_commit<kModeDisabled>)); PL((k_commit<kModeTtl>)); PL((k_commit<kModeTtl, true>));
+    PL((k_commit<kModeLru>)); PL(k_lru_found); PL(k_lru_victim); PL(k_lru_revert); PL(k_lru_meta);
+    PL(k_finalize); PL(k_pf_group); PL(k_pf_slot); PL(k_pf_write);
+#undef PL
+}
+
 void run_validate(Table& t, const uint64_t* ids, uint64_t n, cudaStream_t st) {
     k_init_counters<<<1, 32, 0, st>>>(t.d_aux);
     k_validate<<<grid_for(n / 2 + 1, 256, 148u * 8u), 256, 0, st>>>(t.dev, ids, n, t.d_aux);
@@ -1150,7 +1184,10 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     uint32_t* newent = t.s_newent.as<uint32_t>();
     if (t.profiling) cudaEventRecord(t.ev[7], st);
     k_init_counters<<<1, 32, 0, st>>>(t.d_ctr);
-    launch_pdl(k_validate, grid_for(n / 2 + 1, B, 148u * 8u), B, st, t.dev, a.ids, n, t.d_ctr);
+    if (a.sh_state)  // row-sharded owner: the sources validated; adopt the ranks' decision
+        launch_pdl(k_sh_adopt, 1, 32, st, t.d_ctr, (const ShStateView*)a.sh_state);
+    else
+        launch_pdl(k_validate, grid_for(n / 2 + 1, B, 148u * 8u), B, st, t.dev, a.ids, n, t.d_ctr);
     t.launches += 2;
     if (a.overflow_all) return;  // validation only; the host reports the error
     if (t.profiling) cudaEventRecord(t.ev[0], st);
@@ -1286,7 +1323,9 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
         if (ttl || lru) MPZCH_CUDA(cudaMemcpyAsync(a.out_mark, t.s_evflag.p, n, cudaMemcpyDeviceToDevice, st));
         else MPZCH_CUDA(cudaMemsetAsync(a.out_mark, 0, n, st));
     }
-    if (ttl || lru) enqueue_compact_evicted(t, n, a.out_ev, a.ev_cap, st, lru ? &t.d_ctr->lru_evict : nullptr);
+    // (row-sharded owner: the return scatter reads and clears the evicted flags)
+    if ((ttl || lru) && !a.sh_state)
+        enqueue_compact_evicted(t, n, a.out_ev, a.ev_cap, st, lru ? &t.d_ctr->lru_evict : nullptr);
     if (t.profiling) cudaEventRecord(t.ev[3], st);
 }
 

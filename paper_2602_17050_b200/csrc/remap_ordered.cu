@@ -381,6 +381,16 @@ __global__ void __launch_bounds__(256) k_cleanup_o(uint64_t n, const uint32_t* _
 
 }  // namespace
 
+void preload_ordered_kernels() {
+#define PL(k) preload_kernel((const void*)(k))
+    PL(k_init_counters_o); PL(k_validate_dedup); PL(k_first_flags); PL(k_prep);
+    PL(k_ordered<kModeDisabled>); PL(k_ordered<kModeTtl>); PL(k_ordered<kModeLru>);
+    PL(k_ordered_hf<kModeDisabled>); PL(k_ordered_hf<kModeTtl>); PL(k_ordered_hf<kModeLru>);
+    PL(k_scatter); PL(k_mark_first); PL(k_cleanup_o);
+#undef PL
+    preload_compact<EmitUnique>();
+}
+
 void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st, bool rounds) {
     const uint64_t n = a.n;
     t.ensure_ordered_scratch(n);

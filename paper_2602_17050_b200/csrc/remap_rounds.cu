@@ -359,11 +359,15 @@ int rounds_grid(uint64_t n) {
 
 }  // namespace
 
-// Enqueues the rounds kernel for the uniques prepared by enqueue_ordered_batch (no host sync).
-// The uniques it leaves (if any) are flagged in `todo` and counted in BatchCounters::r_left.
-void enqueue_rounds(Table& t, const BatchArgs& a, cudaStream_t st, uint8_t* todo) {
-    const Policy& p = *a.pol;
-    const uint64_t n = a.n;
+void preload_rounds_kernels() {
+    preload_kernel((const void*)k_rounds<kModeDisabled>);
+    preload_kernel((const void*)k_rounds<kModeTtl>);
+    preload_kernel((const void*)k_rounds<kModeLru>);
+}
+
+// The rounds path's scratch: epoch-keyed mark arrays over the held rows (<= 2^27 words each)
+// and per-unique lists for n uniques.
+void ensure_rounds_scratch(Table& t, uint64_t n, cudaStream_t st) {
     const uint64_t held = t.held_rows();
     uint64_t msize = 1024;
     while (msize < held && msize < (1ull << 27)) msize <<= 1;
@@ -383,6 +387,15 @@ void enqueue_rounds(Table& t, const BatchArgs& a, cudaStream_t st, uint8_t* todo
     t.r_oc.reserve(n);
     t.r_d.reserve(n * 4);
     t.r_susp.reserve(n);
+    t.o_todo.reserve(n);
+}
+
+// Enqueues the rounds kernel for the uniques prepared by enqueue_ordered_batch (no host sync).
+// The uniques it leaves (if any) are flagged in `todo` and counted in BatchCounters::r_left.
+void enqueue_rounds(Table& t, const BatchArgs& a, cudaStream_t st, uint8_t* todo) {
+    const Policy& p = *a.pol;
+    const uint64_t n = a.n;
+    ensure_rounds_scratch(t, n, st);
     RoundsArgs r;
     r.t = t.dev;
     r.ctr = t.d_ctr;

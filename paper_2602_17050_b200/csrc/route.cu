@@ -79,6 +79,8 @@ __global__ void __launch_bounds__(256) k_route_write(TableDev t, const uint64_t*
 // Destinations by value (kernel parameters): one entry per part.
 struct PeerDst {
     uint64_t ids[kMaxParts], feats[kMaxParts], src[kMaxParts], off[kMaxParts];
+    const uint64_t* dev_off;  // row-sharded device protocol: offsets on the device (or null)
+    const uint64_t* gate;     // nonzero word: the batch failed, store nothing (or null)
 };
 
 __global__ void __launch_bounds__(256) k_route_scatter(TableDev t, const uint64_t* __restrict__ ids,
@@ -89,12 +91,16 @@ __global__ void __launch_bounds__(256) k_route_scatter(TableDev t, const uint64_
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned lane = lane_id();
     if (warp >= nchunks) return;
+    if (d.gate && *(volatile const uint64_t*)d.gate) return;
     // index inside the owner's buffer: this rank's offset there + the position's rank among
     // this rank's positions of that part (the part-major scan minus the part's start)
     uint64_t base = 0, base2 = 0;
-    if (lane < parts) base = d.off[lane] + off[(uint64_t)lane * nchunks + warp] - off[(uint64_t)lane * nchunks];
+    if (lane < parts)
+        base = (d.dev_off ? d.dev_off[lane] : d.off[lane]) + off[(uint64_t)lane * nchunks + warp] -
+               off[(uint64_t)lane * nchunks];
     if (lane + 32 < parts)
-        base2 = d.off[lane + 32] + off[(uint64_t)(lane + 32) * nchunks + warp] - off[(uint64_t)(lane + 32) * nchunks];
+        base2 = (d.dev_off ? d.dev_off[lane + 32] : d.off[lane + 32]) +
+                off[(uint64_t)(lane + 32) * nchunks + warp] - off[(uint64_t)(lane + 32) * nchunks];
     for (uint64_t i0 = warp * kChunk; i0 < (warp + 1) * kChunk && i0 < n; i0 += 32) {
         const uint64_t i = i0 + lane;
         const uint64_t id = i < n ? ids[i] : 0;
@@ -112,6 +118,9 @@ __global__ void __launch_bounds__(256) k_route_scatter(TableDev t, const uint64_
             if (lane == (q & 31)) (q < 32 ? base : base2) += __popc(m);
         }
     }
+    // device protocol: the stores reach the owners (NVLink / IPC) before the ready flag, which
+    // a later kernel on this stream releases at system scope
+    if (d.dev_off) __threadfence_system();
 }
 
 struct PeerBack {
@@ -184,6 +193,48 @@ __global__ void __launch_bounds__(1024) k_route_scan(unsigned* cnt, uint64_t tot
     }
 }
 
+void preload_route_kernels() {
+    preload_kernel((const void*)k_route_count);
+    preload_kernel((const void*)k_route_scan);
+    preload_kernel((const void*)k_route_write);
+    preload_kernel((const void*)k_route_scatter);
+}
+
+void upload_route_map(Table& t, const uint32_t* shard_to_part, uint32_t parts) {
+    if (parts == 0 || parts > kMaxParts) throw Error{MPZCH_EINVAL, "route: 1..64 parts"};
+    std::vector<uint8_t> h(t.S);
+    for (uint32_t s = 0; s < t.S; ++s) {
+        if (shard_to_part[s] >= parts) throw Error{MPZCH_EINVAL, "route: shard mapped to no part"};
+        h[s] = (uint8_t)shard_to_part[s];
+    }
+    t.rt_s2p.reserve(t.S);
+    t.rt_tot.reserve(parts * 4);
+    if (h != t.rt_map) {
+        MPZCH_CUDA(cudaMemcpyAsync(t.rt_s2p.p, h.data(), t.S, cudaMemcpyHostToDevice, t.stream));
+        MPZCH_CUDA(cudaStreamSynchronize(t.stream));  // h is pageable and about to go out of scope
+        t.rt_map = h;
+    }
+}
+
+void enqueue_route_count(Table& t, const uint64_t* ids, uint64_t n, uint32_t parts, cudaStream_t st) {
+    const uint64_t nchunks = (n + kChunk - 1) / kChunk;
+    t.rt_cnt.reserve(std::max<uint64_t>(1, nchunks * parts) * 4);
+    t.rt_tot.reserve(parts * 4);
+    if (n) {
+        const unsigned blocks = (unsigned)((nchunks * 32 + 255) / 256);
+        k_route_count<<<blocks, 256, 0, st>>>(t.dev, ids, n, t.rt_s2p.as<uint8_t>(), parts,
+                                              t.rt_cnt.as<unsigned>(), nchunks);
+        k_route_scan<<<1, 1024, 0, st>>>(t.rt_cnt.as<unsigned>(), nchunks * parts, t.rt_tot.as<unsigned>(),
+                                         parts, nchunks);
+        t.launches += 2;
+        MPZCH_CUDA(cudaGetLastError());
+    }
+    t.rt_ids = ids;  // arms run_route_scatter
+    t.rt_n = n;
+    t.rt_nchunks = nchunks;
+    t.rt_parts = parts;
+}
+
 void run_route(Table& t, const uint64_t* ids, uint64_t n, const uint32_t* shard_to_part,
                uint32_t parts, uint32_t* perm, uint64_t* counts, cudaStream_t st) {
     if (parts == 0 || parts > kMaxParts) throw Error{MPZCH_EINVAL, "route: 1..64 parts"};
@@ -240,8 +291,10 @@ void run_route_scatter(Table& t, const uint64_t* ids, const uint32_t* feats, uin
         pd.ids[q] = d.ids_to[q];
         pd.feats[q] = feats ? d.feats_to[q] : 0;
         pd.src[q] = d.src_to[q];
-        pd.off[q] = d.offset[q];
+        pd.off[q] = d.offset ? d.offset[q] : 0;
     }
+    pd.dev_off = d.dev_offset;
+    pd.gate = d.gate;
     t.rt_ids = nullptr;
     if (n == 0) return;
     const uint64_t nchunks = t.rt_nchunks;

@@ -184,6 +184,12 @@ __global__ void __launch_bounds__(256) k_gather_rows(TableDev t, const uint64_t*
 
 }  // namespace
 
+void preload_row_kernels() {
+    preload_kernel((const void*)k_reset_rows);
+    preload_kernel((const void*)k_mark_pending);
+    preload_kernel((const void*)k_flush_pending);
+}
+
 void run_gather_rows(const Table& t, const uint64_t* rows, uint64_t n, uint64_t* out_ids, float* out_w,
                      cudaStream_t st) {
     if (!n) return;

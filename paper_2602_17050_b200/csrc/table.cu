@@ -11,6 +11,8 @@
 #include <cuda.h>  // CUresult / CUdeviceptr types only (driver entry point, no -lcuda)
 #include <cuda_runtime.h>
 
+#include <functional>
+
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -306,6 +308,8 @@ unsigned run_dirty_compact(Table& T, uint64_t gen, cudaStream_t st) {
     return T.h_aux->pad;
 }
 
+}  // namespace
+
 Policy parse_policy(const mpzch_policy* p) {
     Policy pol;
     if (!p) return pol;  // Disabled
@@ -417,45 +421,10 @@ void complete_slot(Table& t, int si) {
     sl.busy = false;
 }
 
-// Enqueue one batch on `st`; returns its ticket.  Host-detectable argument errors throw
-// here; device-detected ones (invalid id, ...) are reported by wait_batch.
-uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n,
-                       uint64_t now, const Policy& pol, uint64_t* out_slots, uint8_t* out_oc,
-                       uint64_t* out_ev, uint64_t ev_cap, cudaStream_t st,
-                       uint8_t* out_mark = nullptr) {
-    if (n > 0xffffffffull) throw Error{MPZCH_ELENGTH, "batch exceeds 2^32 - 1 positions"};
-    const uint64_t ticket = t.next_ticket++;
-    const int si = (int)(ticket % Table::kRing);
-    if (n == 0) {
-        Table::Result r;
-        r.ticket = ticket;
-        t.results[ticket % Table::kResults] = r;
-        return ticket;
-    }
-    complete_slot(t, si);  // the ring wrapped: retire the batch that used this block
-    // batches of one handle share scratch: order a new stream after the previous batch
-    if (t.last_ticket && st != t.last_stream) {
-        const Table::Slot& prev = t.slots[t.last_ticket % Table::kRing];
-        if (prev.busy && prev.ticket == t.last_ticket) MPZCH_CUDA(cudaStreamWaitEvent(st, prev.done, 0));
-    }
-    Table::Slot& sl = t.slots[si];
-    t.d_ctr = t.d_ring + si;
-    t.h_ctr = t.h_ring + si;
-    if (t.profiling && !sl.ev[0])
-        for (auto& e : sl.ev) MPZCH_CUDA(cudaEventCreate(&e));
-    t.ev = sl.ev;
-    BatchArgs a{};
-    a.ids = ids;
-    a.feats = feats;
-    a.n = n;
-    a.now = now;
-    a.pol = &pol;
-    a.out_slots = out_slots;
-    a.out_oc = out_oc;
-    a.out_ev = out_ev;
-    a.ev_cap = out_ev ? ev_cap : 0;
-    a.out_mark = out_mark;
-    // one metadata value for the whole batch? (make_metadata, eviction.cpp:20-30)
+// one metadata value for the batch, or per-feature values through the fast path's last-writer
+// pass (make_metadata, eviction.cpp:20-30); uploads the per-feature map
+void fill_policy_args(Table& t, const Policy& pol, uint64_t now, const uint32_t* feats, BatchArgs& a,
+                      cudaStream_t st) {
     a.uniform = true;
     uint64_t ttl = 0;
     if (pol.mode == kModeTtl) {
@@ -497,6 +466,47 @@ uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uin
         a.per_feature = !ovf;
         a.uniform_meta = 0;
     }
+}
+
+// Enqueue one batch on `st`; returns its ticket.  Host-detectable argument errors throw
+// here; device-detected ones (invalid id, ...) are reported by wait_batch.
+uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n,
+                       uint64_t now, const Policy& pol, uint64_t* out_slots, uint8_t* out_oc,
+                       uint64_t* out_ev, uint64_t ev_cap, cudaStream_t st,
+                       uint8_t* out_mark = nullptr) {
+    if (n > 0xffffffffull) throw Error{MPZCH_ELENGTH, "batch exceeds 2^32 - 1 positions"};
+    const uint64_t ticket = t.next_ticket++;
+    const int si = (int)(ticket % Table::kRing);
+    if (n == 0) {
+        Table::Result r;
+        r.ticket = ticket;
+        t.results[ticket % Table::kResults] = r;
+        return ticket;
+    }
+    complete_slot(t, si);  // the ring wrapped: retire the batch that used this block
+    // batches of one handle share scratch: order a new stream after the previous batch
+    if (t.last_ticket && st != t.last_stream) {
+        const Table::Slot& prev = t.slots[t.last_ticket % Table::kRing];
+        if (prev.busy && prev.ticket == t.last_ticket) MPZCH_CUDA(cudaStreamWaitEvent(st, prev.done, 0));
+    }
+    Table::Slot& sl = t.slots[si];
+    t.d_ctr = t.d_ring + si;
+    t.h_ctr = t.h_ring + si;
+    if (t.profiling && !sl.ev[0])
+        for (auto& e : sl.ev) MPZCH_CUDA(cudaEventCreate(&e));
+    t.ev = sl.ev;
+    BatchArgs a{};
+    a.ids = ids;
+    a.feats = feats;
+    a.n = n;
+    a.now = now;
+    a.pol = &pol;
+    a.out_slots = out_slots;
+    a.out_oc = out_oc;
+    a.out_ev = out_ev;
+    a.ev_cap = out_ev ? ev_cap : 0;
+    a.out_mark = out_mark;
+    fill_policy_args(t, pol, now, feats, a, st);
     bool fast = t.path_override == MPZCH_PATH_AUTO && t.hole_free && (a.uniform || a.per_feature) &&
                 n <= (1ull << 29);
     const bool profiled = t.profiling;
@@ -575,6 +585,8 @@ void run_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n,
     if (n == 0) t.last = mpzch_batch_stats{};
 }
 
+namespace {
+
 template <class F>
 mpzch_status guarded(F&& f) {
     try {
@@ -594,6 +606,19 @@ mpzch_status guarded(F&& f) {
 
 }  // namespace
 
+mpzch_status run_guarded(const std::function<void()>& f) { return guarded(f); }
+
+// every kernel a batch can launch, loaded on the current device (lazy loading, common.cuh)
+void preload_all_kernels() {
+    preload_remap_kernels();
+    preload_ordered_kernels();
+    preload_rounds_kernels();
+    preload_row_kernels();
+    preload_route_kernels();
+    preload_compact<EmitEvicted>();
+    preload_compact<EmitIndex>();
+}
+
 void enqueue_compact_evicted(Table& t, uint64_t n, uint64_t* out_ev, uint64_t ev_cap, cudaStream_t st,
                              const unsigned* gate) {
     EmitEvicted em{t.s_evslot.as<uint64_t>(), out_ev, ev_cap};
@@ -605,9 +630,6 @@ void enqueue_compact_evicted(Table& t, uint64_t n, uint64_t* out_ev, uint64_t ev
 
 using namespace mpzch_b200;
 
-struct mpzch_table {
-    Table* t;
-};
 
 #define CHECK_T(t)                                                     \
     do {                                                               \

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -66,6 +67,8 @@ struct BatchCounters {
     unsigned int r_marked, r_checked;  // closure steps / windows marked / range checks (diagnostics)
     unsigned int deferred;             // TTL probe: walks handed to the resume pass
     unsigned int ldeferred;            // synchronous lookups: walks handed to the resume pass
+    unsigned long long n_live;         // positions of the batch when only the device knows them
+                                       // (row-sharded owner: the received count); ~0 = kernel arg
 };
 
 // sgd_step scratch counters (train.cu)
@@ -256,12 +259,42 @@ struct BatchArgs {
     bool per_feature = false;     // TTL with differing per-feature values on the fast path:
                                   // metadata written by the last-writer pass (remap_fast.cu)
     uint32_t nk = 0;              // per-feature map size
+    // row-sharded owner (sharded.cu): n is only an upper bound; the batch's errors and its
+    // received count come from this device state (k_sh_adopt replaces validation), and the
+    // evicted flags are left set for the return scatter instead of compacted here
+    const void* sh_state = nullptr;
 };
+
+// table.cu: the batch machinery the row-sharded layer (sharded.cu) reuses
+Policy parse_policy(const mpzch_policy* p);
+uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n, uint64_t now,
+                       const Policy& pol, uint64_t* out_slots, uint8_t* out_oc, uint64_t* out_ev,
+                       uint64_t ev_cap, cudaStream_t st, uint8_t* out_mark);
+uint64_t wait_batch(Table& t, uint64_t ticket);
+// force-load kernels (lazy module loading can wait for running work; see common.cuh)
+void preload_remap_kernels();
+void preload_ordered_kernels();
+void preload_rounds_kernels();
+void preload_row_kernels();
+void preload_route_kernels();
+void preload_all_kernels();
+// C-ABI error mapping: runs f, maps Error / bad_alloc / exceptions to a status + mpzch_last_error
+mpzch_status run_guarded(const std::function<void()>& f);
+
+// one-metadata-value / per-feature decision and the per-feature map upload of a batch
+// (make_metadata, eviction.cpp:20-30); shared by enqueue_batch and the row-sharded owner
+void fill_policy_args(Table& t, const Policy& pol, uint64_t now, const uint32_t* feats, BatchArgs& a,
+                      cudaStream_t st);
+// count-only route (route.cu) without a host sync: per-chunk offsets and per-part totals
+// stay on the device (t.rt_cnt, t.rt_tot); the shard -> part map must be uploaded already
+void enqueue_route_count(Table& t, const uint64_t* ids, uint64_t n, uint32_t parts, cudaStream_t st);
+void upload_route_map(Table& t, const uint32_t* shard_to_part, uint32_t parts);
 
 // enqueue the whole batch; counters land in t.h_ctr after the stream syncs
 void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st);
 void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st, bool rounds = false);
 void enqueue_rounds(Table& t, const BatchArgs& a, cudaStream_t st, uint8_t* todo);
+void ensure_rounds_scratch(Table& t, uint64_t n, cudaStream_t st);
 // gate (nullable): device word, 0 = no evicted flag can be set (LRU batches without evictors)
 void enqueue_compact_evicted(Table& t, uint64_t n, uint64_t* out_ev, uint64_t ev_cap, cudaStream_t st,
                              const unsigned* gate = nullptr);
@@ -275,6 +308,10 @@ struct PeerScatter {
     const uint64_t* feats_to;   // [parts] u32 feature arrays (0: no features)
     const uint64_t* src_to;     // [parts] u32 source-position arrays
     const uint64_t* offset;     // [parts] this rank's first index in each owner's buffers
+    // row-sharded device protocol: offsets read on the device (overrides `offset`), a gate word
+    // (nonzero: the batch failed, store nothing) and a system-scope fence after the stores
+    const uint64_t* dev_offset = nullptr;
+    const uint64_t* gate = nullptr;
 };
 void run_route_scatter(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n,
                        uint32_t parts, const PeerScatter& d, cudaStream_t st);
@@ -293,6 +330,15 @@ uint64_t run_dedup(const uint64_t* ids, const uint32_t* feats, uint64_t n, uint6
                    uint32_t* inverse, uint64_t* bad_pos, cudaStream_t st);
 bool run_words_equal(const void* a, const void* b, uint64_t bytes, cudaStream_t st);
 void run_gather_weights(const Table& t, const uint64_t* rows, uint64_t n, float* out, cudaStream_t st);
+
+}  // namespace mpzch_b200
+
+// The C-ABI handle (include/mpzch_b200.h): one device-resident table.
+struct mpzch_table {
+    mpzch_b200::Table* t;
+};
+
+namespace mpzch_b200 {
 
 inline unsigned grid_for(uint64_t n, unsigned block, unsigned max_blocks = 148u * 32u) {
     uint64_t g = (n + block - 1) / block;

@@ -8,6 +8,12 @@ import sys
 
 import pytest
 
+# row-sharded tests run several ranks (streams) of one process on one GPU: give every stream its
+# own hardware queue (a rank's spinning wait must never sit in front of a peer's kernel), and
+# turn a protocol bug into a quick failure instead of a long wait
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+os.environ.setdefault("MPZCH_PEER_TIMEOUT_MS", "20000")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -44,6 +45,9 @@ struct Ref {
     static auto dd(const std::vector<mpzch::BatchEntry>& e) { return mpzch::dedup(e); }
     using Result = mpzch::ProbeResult;
     using Entry = mpzch::BatchEntry;
+    // the row-sharded run: the reference holds every shard in one process
+    using Sharded = mpzch::MpzchTable;
+    static std::unique_ptr<Sharded> sharded(const Config& c, std::uint32_t) { return std::make_unique<Sharded>(c); }
 };
 
 struct Gpu {
@@ -67,6 +71,14 @@ struct Gpu {
     static auto dd(const std::vector<mpzch_b200::BatchEntry>& e) { return mpzch_b200::dedup(e); }
     using Result = mpzch_b200::ProbeResult;
     using Entry = mpzch_b200::BatchEntry;
+    // the row-sharded run: G ranks (all on GPU 0 here; one per GPU on an NVLink box)
+    using Sharded = mpzch_b200::ShardedMpzchTable;
+    static std::unique_ptr<Sharded> sharded(const Config& c, std::uint32_t G) {
+        return std::make_unique<Sharded>(c, std::vector<int>(G, 0), 4096);
+    }
+    static std::vector<std::uint64_t> ident(const Sharded& t, std::uint32_t s) { return t.identities(s); }
+    static std::vector<std::uint64_t> meta(const Sharded& t, std::uint32_t s) { return t.metadata(s); }
+    static auto pb(Sharded& t, const Batch& b, const Policy& p) { return mpzch_b200::process_batch(t, b, p); }
 };
 
 struct Trace {
@@ -189,6 +201,64 @@ Trace run(std::uint64_t seed, int mode) {
     bad.ids = {{1, 0}, {1ull << 63, 0}};
     try {
         NS::pb(table, bad, pol);
+    } catch (const std::invalid_argument& e) {
+        tr.error = e.what();
+    }
+    return tr;
+}
+
+// The row-sharded table: the same batches through mpzch_b200::ShardedMpzchTable
+// (G ranks, the device-side protocol) must give exactly what the reference's single-process
+// process_batch gives -- every position's result, every shard's identities and metadata, and the
+// invalid-id error with its global position.
+template <class NS>
+Trace run_sharded(std::uint64_t seed, int mode) {
+    Trace tr;
+    mpzch::SplitMix64 rng(seed);
+    const std::uint32_t S = 4 << rng.next_below(2);  // 4 or 8 logical shards
+    const std::uint32_t G = 2 << rng.next_below(2);  // 2 or 4 ranks
+    typename NS::Config cfg = NS::Config::even(S * (150 + rng.next_below(300)), S, 1 + rng.next_below(24),
+                                               rng.next(), 0, rng.next());
+    auto table = NS::sharded(cfg, G);
+    typename NS::Ttl ttl;
+    ttl.default_ttl_seconds = 12;
+    ttl.per_feature_ttl = {{2, 3}};
+    const typename NS::Policy pol = mode == 0   ? NS::Policy::disabled()
+                                    : mode == 1 ? NS::Policy::lru()
+                                                : NS::Policy::ttl(ttl);
+    mpzch::DistinctIdStream ids(rng.next());
+    std::uint64_t now = 1;
+    tr.mark("sharded batches");
+    for (int b = 0; b < 12; ++b) {
+        now += rng.next_below(6);
+        typename NS::Batch batch;
+        batch.now = now;
+        const std::uint64_t len = 1 + rng.next_below(900);
+        for (std::uint64_t k = 0; k < len; ++k)
+            batch.ids.push_back({ids.at(rng.next_below(cfg.shard_capacities[0] * S + 200)),
+                                 static_cast<std::uint32_t>(rng.next_below(3))});
+        try {
+            for (const auto& r : NS::pb(*table, batch, pol)) {
+                tr.out.push_back(r.slot);
+                tr.out.push_back(r.evicted);
+                tr.out.push_back(static_cast<std::uint64_t>(r.outcome));
+            }
+        } catch (const std::exception& e) {
+            tr.error = e.what();
+            return tr;
+        }
+    }
+    tr.mark("sharded state");
+    for (std::uint32_t s = 0; s < S; ++s) {
+        for (auto v : NS::ident(*table, s)) tr.out.push_back(v);
+        for (auto v : NS::meta(*table, s)) tr.out.push_back(v);
+    }
+    typename NS::Batch bad;
+    bad.now = now;
+    for (int k = 0; k < 40; ++k) bad.ids.push_back({ids.at(5000 + k), 0});
+    bad.ids[29].id = 1ull << 63;  // in a later rank's slice: every rank reports position 29
+    try {
+        NS::pb(*table, bad, pol);
     } catch (const std::invalid_argument& e) {
         tr.error = e.what();
     }
@@ -420,6 +490,17 @@ int main(int argc, char** argv) {
             ++bad;
         }
         checked += sa.out.size();
+        if (c < 24) {
+            const Trace ha = run_sharded<Ref>(0x5a4d0000 + c, c % 3);
+            const Trace hb = run_sharded<Gpu>(0x5a4d0000 + c, c % 3);
+            if (ha.out != hb.out || ha.error != hb.error) {
+                std::printf("MISMATCH sharded case %d (mode %d): %zu vs %zu words, '%s' vs '%s'\n", c, c % 3,
+                            ha.out.size(), hb.out.size(), ha.error.c_str(), hb.error.c_str());
+                report_diff(ha, hb);
+                ++bad;
+            }
+            checked += ha.out.size();
+        }
     }
     std::printf("%s: %d cases, %llu result/state words compared, %d mismatches\n",
                 bad ? "FAIL" : "PASS", cases, (unsigned long long)checked, bad);
