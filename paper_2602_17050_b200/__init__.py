@@ -204,6 +204,9 @@ _SIGS = {
     "mpzch_sharded_process_batch": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_uint64, ctypes.c_uint64, _vp,
                                                    _vp, _vp, _vp, ctypes.c_uint64, _u64p, _vp]),
     "mpzch_sharded_last_stats": (ctypes.c_int, [_vp, ctypes.POINTER(_Stats), ctypes.POINTER(ctypes.c_int)]),
+    "mpzch_sharded_group_process_batch": (ctypes.c_int, [ctypes.POINTER(_vp), ctypes.c_uint32, _vp, _vp,
+                                                         ctypes.c_uint64, ctypes.c_uint64, _vp, _vp, _vp, _vp,
+                                                         ctypes.c_uint64, _u64p]),
     "mpzch_flush_resets": (ctypes.c_int, [_vp]),
     "mpzch_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),
     "mpzch_get_profile": (ctypes.c_int, [_vp, ctypes.POINTER(_Profile)]),
