@@ -36,15 +36,19 @@ __device__ __forceinline__ uint32_t part_of(uint64_t id, const TableDev& t, cons
 __global__ void __launch_bounds__(256) k_route_count(TableDev t, const uint64_t* __restrict__ ids,
                                                      uint64_t n, const uint8_t* __restrict__ s2p,
                                                      uint32_t parts, unsigned* __restrict__ cnt,
-                                                     uint64_t nchunks) {
+                                                     uint64_t nchunks, unsigned long long* bad) {
+    pdl_wait();
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned lane = lane_id();
     if (warp >= nchunks) return;
     unsigned c = 0;  // lane p accumulates part p (parts <= 32 per lane slot, see below)
     unsigned c2 = 0; // parts 32..63
+    unsigned long long first_bad = ~0ull;  // (bad != null: the validation pass, fused)
     for (uint64_t i0 = warp * kChunk; i0 < (warp + 1) * kChunk && i0 < n; i0 += 32) {
         const uint64_t i = i0 + lane;
-        const uint32_t p = i < n ? part_of(ids[i], t, s2p) : kNone32;
+        const uint64_t id = i < n ? ids[i] : 0;
+        if (bad && (id >> 63) && first_bad == ~0ull) first_bad = i;
+        const uint32_t p = i < n ? part_of(id, t, s2p) : kNone32;
         for (uint32_t q = 0; q < parts; ++q) {
             const unsigned m = __ballot_sync(0xffffffffu, p == q);
             if (lane == (q & 31)) (q < 32 ? c : c2) += __popc(m);
@@ -52,6 +56,10 @@ __global__ void __launch_bounds__(256) k_route_count(TableDev t, const uint64_t*
     }
     if (lane < parts) cnt[(uint64_t)lane * nchunks + warp] = c;
     if (lane + 32 < parts) cnt[(uint64_t)(lane + 32) * nchunks + warp] = c2;
+    if (bad) {
+        for (int o = 16; o; o >>= 1) first_bad = min(first_bad, __shfl_xor_sync(0xffffffffu, first_bad, o));
+        if (lane == 0 && first_bad != ~0ull) atomicMin(bad, first_bad);
+    }
 }
 
 __global__ void __launch_bounds__(256) k_route_write(TableDev t, const uint64_t* __restrict__ ids,
@@ -88,6 +96,7 @@ __global__ void __launch_bounds__(256) k_route_scatter(TableDev t, const uint64_
                                                        const uint8_t* __restrict__ s2p, uint32_t parts,
                                                        const unsigned* __restrict__ off, uint64_t nchunks,
                                                        const PeerDst d) {
+    pdl_wait();
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned lane = lane_id();
     if (warp >= nchunks) return;
@@ -155,6 +164,7 @@ __global__ void k_route_scan(unsigned* cnt, uint64_t total, unsigned* part_total
 __global__ void __launch_bounds__(1024) k_route_scan(unsigned* cnt, uint64_t total,
                                                      unsigned* part_totals, uint32_t parts,
                                                      uint64_t nchunks) {
+    pdl_wait();
     __shared__ unsigned wsum[32];
     __shared__ unsigned carry;
     if (threadIdx.x == 0) carry = 0;
@@ -216,16 +226,17 @@ void upload_route_map(Table& t, const uint32_t* shard_to_part, uint32_t parts) {
     }
 }
 
-void enqueue_route_count(Table& t, const uint64_t* ids, uint64_t n, uint32_t parts, cudaStream_t st) {
+void enqueue_route_count(Table& t, const uint64_t* ids, uint64_t n, uint32_t parts, cudaStream_t st,
+                         unsigned long long* bad) {
     const uint64_t nchunks = (n + kChunk - 1) / kChunk;
     t.rt_cnt.reserve(std::max<uint64_t>(1, nchunks * parts) * 4);
     t.rt_tot.reserve(parts * 4);
     if (n) {
         const unsigned blocks = (unsigned)((nchunks * 32 + 255) / 256);
-        k_route_count<<<blocks, 256, 0, st>>>(t.dev, ids, n, t.rt_s2p.as<uint8_t>(), parts,
-                                              t.rt_cnt.as<unsigned>(), nchunks);
-        k_route_scan<<<1, 1024, 0, st>>>(t.rt_cnt.as<unsigned>(), nchunks * parts, t.rt_tot.as<unsigned>(),
-                                         parts, nchunks);
+        launch_pdl(k_route_count, blocks, 256, st, t.dev, ids, n, (const uint8_t*)t.rt_s2p.as<uint8_t>(), parts,
+                   t.rt_cnt.as<unsigned>(), nchunks, bad);
+        launch_pdl(k_route_scan, 1, 1024, st, t.rt_cnt.as<unsigned>(), (uint64_t)(nchunks * parts),
+                   t.rt_tot.as<unsigned>(), parts, nchunks);
         t.launches += 2;
         MPZCH_CUDA(cudaGetLastError());
     }
@@ -260,7 +271,7 @@ void run_route(Table& t, const uint64_t* ids, uint64_t n, const uint32_t* shard_
     if (n) {
         const unsigned blocks = (unsigned)((nchunks * 32 + 255) / 256);
         k_route_count<<<blocks, 256, 0, st>>>(t.dev, ids, n, s2p.as<uint8_t>(), parts,
-                                              cnt.as<unsigned>(), nchunks);
+                                              cnt.as<unsigned>(), nchunks, nullptr);
         k_route_scan<<<1, 1024, 0, st>>>(cnt.as<unsigned>(), nchunks * parts, tot.as<unsigned>(), parts,
                                          nchunks);
         if (perm) {
@@ -299,8 +310,8 @@ void run_route_scatter(Table& t, const uint64_t* ids, const uint32_t* feats, uin
     if (n == 0) return;
     const uint64_t nchunks = t.rt_nchunks;
     const unsigned blocks = (unsigned)((nchunks * 32 + 255) / 256);
-    k_route_scatter<<<blocks, 256, 0, st>>>(t.dev, ids, feats, n, t.rt_s2p.as<uint8_t>(), parts,
-                                            t.rt_cnt.as<unsigned>(), nchunks, pd);
+    launch_pdl(k_route_scatter, blocks, 256, st, t.dev, ids, feats, n, (const uint8_t*)t.rt_s2p.as<uint8_t>(),
+               parts, (const unsigned*)t.rt_cnt.as<unsigned>(), nchunks, pd);
     ++t.launches;
     MPZCH_CUDA(cudaGetLastError());
 }

@@ -158,9 +158,10 @@ __device__ bool wait_all(const uint64_t* flags, uint32_t G, uint64_t e, uint64_t
     return true;
 }
 
-__global__ void k_sh_begin(ShState* st) {
-    if (threadIdx.x != 0) return;
-    st->failed = st->timeout ? 1 : 0;  // a rank that stopped answering fails every later batch
+// the per-batch state back to its start (run by the previous batch's last kernel, and once at
+// creation): a rank that stopped answering fails every later batch
+__device__ __forceinline__ void reset_state(ShState* st) {
+    st->failed = st->timeout ? 1 : 0;
     st->R = 0;
     st->local_bad = ~0ull;
     st->local_over = 0;
@@ -170,46 +171,43 @@ __global__ void k_sh_begin(ShState* st) {
     st->ev_off = st->ev_total = 0;
 }
 
-// P1a: first invalid position of the slice (ids.hpp:25-31) and, for per-feature TTLs that can
-// overflow at this `now`, whether any position's feature does (eviction.cpp:20-30)
-__global__ void __launch_bounds__(256) k_sh_validate(const uint64_t* __restrict__ ids,
-                                                     const uint32_t* __restrict__ feats, uint64_t n,
+__global__ void k_sh_reset(ShState* st) {
+    if (threadIdx.x == 0) reset_state(st);
+}
+
+// P1a' (per-feature TTLs that can overflow at this `now` only): does any position's feature
+// (eviction.cpp:20-30).  The first invalid position is found by the route count (route.cu).
+__global__ void __launch_bounds__(256) k_sh_overflow(const uint32_t* __restrict__ feats, uint64_t n,
                                                      uint64_t limit, uint64_t def_ttl, const uint32_t* keys,
-                                                     const uint64_t* vals, uint32_t nk, int check_over,
-                                                     ShState* st) {
-    unsigned long long bad = ~0ull;
+                                                     const uint64_t* vals, uint32_t nk, ShState* st) {
+    pdl_wait();
     bool over = false;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        if (ids[i] >> 63) bad = min(bad, (unsigned long long)i);
-        if (check_over) {
-            const uint32_t f = feats ? feats[i] : 0;
-            uint64_t ttl = def_ttl;
-            for (uint32_t k = 0; k < nk; ++k)
-                if (keys[k] == f) ttl = vals[k];
-            over |= ttl > limit;
-        }
+        const uint32_t f = feats ? feats[i] : 0;
+        uint64_t ttl = def_ttl;
+        for (uint32_t k = 0; k < nk; ++k)
+            if (keys[k] == f) ttl = vals[k];
+        over |= ttl > limit;
     }
-    if (bad != ~0ull) atomicMin(&st->local_bad, bad);
     if (__any_sync(0xffffffffu, over) && lane_id() == 0) atomicExch(&st->local_over, 1ull);
 }
 
-// P1b: publish this slice's record into every rank's header, then raise the control flag
-__global__ void k_sh_publish(ShPeers P, uint32_t rank, uint32_t G, uint64_t e, uint64_t n, uint64_t over_all,
-                             const unsigned* part_totals, const ShState* st) {
+// P1b: publish this slice's record into every rank's header, raise the control flags, wait for
+// every rank's record and derive the batch's fate, this slice's offsets and the received count
+__global__ void k_sh_publish_plan(ShPeers P, ShHeader* mine, uint32_t rank, uint32_t G, uint64_t e, uint64_t n,
+                                  uint64_t over_all, const unsigned* part_totals, uint64_t cap,
+                                  uint64_t timeout_ns, ShState* st) {
+    pdl_wait();
     const uint32_t q = threadIdx.x;
-    if (q >= G) return;
-    ShCtrl* c = &hdr(P, q)->ctrl[rank];
-    c->n = n;
-    c->bad = st->local_bad;
-    c->over = over_all | st->local_over;
-    for (uint32_t p = 0; p < G; ++p) c->counts[p] = (n && part_totals) ? part_totals[p] : 0;
-    __threadfence_system();
-    st_release_sys(&hdr(P, q)->flag[kFCtrl][rank], e);
-}
-
-// P1c: every rank's record -> the batch's fate, this slice's offsets, the received count
-__global__ void k_sh_plan(ShHeader* mine, uint32_t rank, uint32_t G, uint64_t e, uint64_t cap,
-                          uint64_t timeout_ns, ShState* st) {
+    if (q < G) {
+        ShCtrl* c = &hdr(P, q)->ctrl[rank];
+        c->n = n;
+        c->bad = st->local_bad;
+        c->over = over_all | st->local_over;
+        for (uint32_t p = 0; p < G; ++p) c->counts[p] = (n && part_totals) ? part_totals[p] : 0;
+        __threadfence_system();
+        st_release_sys(&hdr(P, q)->flag[kFCtrl][rank], e);
+    }
     if (!wait_all(mine->flag[kFCtrl], G, e, timeout_ns, st, kFCtrl, rank)) return;
     if (threadIdx.x != 0) return;
     const volatile ShCtrl* c = mine->ctrl;
@@ -231,10 +229,10 @@ __global__ void k_sh_plan(ShHeader* mine, uint32_t rank, uint32_t G, uint64_t e,
         st->failed = 1;
         return;
     }
-    for (uint32_t q = 0; q < G; ++q) {
+    for (uint32_t q2 = 0; q2 < G; ++q2) {
         unsigned long long off = 0;
-        for (uint32_t s = 0; s < rank; ++s) off += c[s].counts[q];
-        st->my_off[q] = off;
+        for (uint32_t s = 0; s < rank; ++s) off += c[s].counts[q2];
+        st->my_off[q2] = off;
     }
     unsigned long long r = 0;
     for (uint32_t s = 0; s < G; ++s) {
@@ -245,15 +243,17 @@ __global__ void k_sh_plan(ShHeader* mine, uint32_t rank, uint32_t G, uint64_t e,
     st->R = r;
 }
 
-__global__ void k_sh_signal(ShPeers P, uint32_t kind, uint32_t rank, uint32_t G, uint64_t e) {
+// raise this rank's `kind` flag in every rank's header (the previous kernel's peer stores are
+// flushed: PDL waits for its completion, and the release is system scope), then wait for
+// every rank's
+__global__ void k_sh_signal_wait(ShPeers P, ShHeader* mine, uint32_t kind, uint32_t rank, uint32_t G, uint64_t e,
+                                 uint64_t timeout_ns, ShState* st) {
+    pdl_wait();
     const uint32_t q = threadIdx.x;
-    if (q >= G) return;
-    __threadfence_system();
-    st_release_sys(&hdr(P, q)->flag[kind][rank], e);
-}
-
-__global__ void k_sh_wait(ShHeader* mine, uint32_t kind, uint32_t rank, uint32_t G, uint64_t e,
-                          uint64_t timeout_ns, ShState* st) {
+    if (q < G) {
+        __threadfence_system();
+        st_release_sys(&hdr(P, q)->flag[kind][rank], e);
+    }
     wait_all(mine->flag[kind], G, e, timeout_ns, st, kind, rank);
 }
 
@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(256) k_sh_return(const ShState* st, const uint
                                                    const uint64_t* __restrict__ slots,
                                                    const uint8_t* __restrict__ oc, uint8_t* mark, int clear,
                                                    ShPeers P, Layout L, uint32_t G) {
+    pdl_wait();
     __shared__ unsigned long long roff[kMaxG + 1];
     for (uint32_t s = threadIdx.x; s <= G; s += blockDim.x) roff[s] = st->roff[s];
     __syncthreads();
@@ -287,22 +288,16 @@ __global__ void __launch_bounds__(256) k_sh_return(const ShState* st, const uint
     __threadfence_system();
 }
 
-struct EmitSlots {
-    const uint64_t* slots;
-    uint64_t* out;
-    __device__ void operator()(uint64_t i, unsigned k) const { out[k] = slots[i]; }
-};
-
-__global__ void k_sh_publish_evc(ShPeers P, uint32_t rank, uint32_t G, uint64_t e, const ShState* st) {
+// P5a: the evicted-list counts (published + planned in one kernel)
+__global__ void k_sh_evc_plan(ShPeers P, ShHeader* mine, uint32_t rank, uint32_t G, uint64_t e,
+                              uint64_t timeout_ns, ShState* st) {
+    pdl_wait();
     const uint32_t q = threadIdx.x;
-    if (q >= G) return;
-    hdr(P, q)->ctrl[rank].evc = st->failed ? 0 : st->ev_mine;
-    __threadfence_system();
-    st_release_sys(&hdr(P, q)->flag[kFEvc][rank], e);
-}
-
-__global__ void k_sh_evplan(ShHeader* mine, uint32_t rank, uint32_t G, uint64_t e, uint64_t timeout_ns,
-                            ShState* st) {
+    if (q < G) {
+        hdr(P, q)->ctrl[rank].evc = st->failed ? 0 : st->ev_mine;
+        __threadfence_system();
+        st_release_sys(&hdr(P, q)->flag[kFEvc][rank], e);
+    }
     if (!wait_all(mine->flag[kFEvc], G, e, timeout_ns, st, kFEvc, rank)) return;
     if (threadIdx.x != 0) return;
     const volatile ShCtrl* c = mine->ctrl;
@@ -315,9 +310,10 @@ __global__ void k_sh_evplan(ShHeader* mine, uint32_t rank, uint32_t G, uint64_t 
     st->ev_total = total;
 }
 
-// P5: this slice's segment of the canonical evicted list into every rank's list
+// P5b: this slice's segment of the canonical evicted list into every rank's list
 __global__ void __launch_bounds__(256) k_sh_ev_scatter(const ShState* st, const uint64_t* __restrict__ mine,
                                                        ShPeers P, size_t ev_at, uint32_t G) {
+    pdl_wait();
     if (st->failed) return;
     const uint64_t m = st->ev_mine, off = st->ev_off;
     for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < m * G; x += (uint64_t)gridDim.x * blockDim.x) {
@@ -328,13 +324,46 @@ __global__ void __launch_bounds__(256) k_sh_ev_scatter(const ShState* st, const 
     __threadfence_system();
 }
 
-__global__ void __launch_bounds__(256) k_sh_ev_out(const ShState* st, const uint64_t* __restrict__ all,
-                                                   uint64_t* __restrict__ out, uint64_t cap) {
-    if (st->failed) return;
-    const uint64_t m = min((uint64_t)st->ev_total, cap);
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (uint64_t)gridDim.x * blockDim.x)
-        out[k] = all[k];
+// last kernel of a batch: this slice's results (and the evicted list) to the caller's buffers,
+// the batch's state and owner-side counters straight into the pinned result slot (mapped host
+// memory: no copy operation), then the state back to its start for the next batch
+__global__ void __launch_bounds__(256) k_sh_finish(ShState* st, const BatchCounters* ctr, uint64_t n,
+                                                   const uint64_t* __restrict__ rslots,
+                                                   const uint8_t* __restrict__ roc, uint64_t* __restrict__ out_slots,
+                                                   uint8_t* __restrict__ out_oc, const uint64_t* __restrict__ ev_all,
+                                                   uint64_t* __restrict__ out_ev, uint64_t ev_cap, ShState* h_st,
+                                                   BatchCounters* h_ctr) {
+    pdl_wait();
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    if (!st->failed) {
+        for (uint64_t i = tid; i < n; i += stride) {
+            out_slots[i] = rslots[i];
+            out_oc[i] = roc[i];
+        }
+        if (out_ev) {
+            const uint64_t m = min((uint64_t)st->ev_total, ev_cap);
+            for (uint64_t k = tid; k < m; k += stride) out_ev[k] = ev_all[k];
+        }
+    }
+    // every block has read the state before block 0 resets it: the reset happens in a grid of
+    // one block or after the counters below, so do it in a separate tail (see the host)
+    if (tid == 0) {
+        *h_st = *st;
+        if (ctr) *h_ctr = *ctr;
+    }
 }
+
+__global__ void k_sh_tail(ShState* st) {
+    pdl_wait();
+    if (threadIdx.x == 0) reset_state(st);
+}
+
+struct EmitSlots {
+    const uint64_t* slots;
+    uint64_t* out;
+    __device__ void operator()(uint64_t i, unsigned k) const { out[k] = slots[i]; }
+};
 
 struct ShRecord {  // what mpzch_sharded_export hands to the other ranks
     cudaIpcMemHandle_t handle;
@@ -374,8 +403,10 @@ struct ShardedRank {
         mpzch_status fallback_status = MPZCH_OK;
     };
     Slot slots[kRing];
-    ShState* h_state = nullptr;         // pinned ring
-    BatchCounters* h_ctr = nullptr;     // pinned ring
+    ShState* h_state = nullptr;         // pinned ring (mapped)
+    BatchCounters* h_ctr = nullptr;     // pinned ring (mapped)
+    ShState* hd_state = nullptr;        // their device addresses
+    BatchCounters* hd_ctr = nullptr;
     cudaStream_t last_stream = nullptr;
     cudaEvent_t last_done = nullptr;
     // results of completed batches (by ticket, like the table's ring)
@@ -416,10 +447,9 @@ struct ShardedRank {
         MPZCH_CUDA(cudaSetDevice(dev));
         // a kernel loaded lazily at its first launch could wait for a peer's spinning kernel
         preload_all_kernels();
-        for (const void* k : {(const void*)k_sh_begin, (const void*)k_sh_validate, (const void*)k_sh_publish,
-                              (const void*)k_sh_plan, (const void*)k_sh_signal, (const void*)k_sh_wait,
-                              (const void*)k_sh_return, (const void*)k_sh_publish_evc, (const void*)k_sh_evplan,
-                              (const void*)k_sh_ev_scatter, (const void*)k_sh_ev_out})
+        for (const void* k : {(const void*)k_sh_reset, (const void*)k_sh_overflow, (const void*)k_sh_publish_plan,
+                              (const void*)k_sh_signal_wait, (const void*)k_sh_return, (const void*)k_sh_evc_plan,
+                              (const void*)k_sh_ev_scatter, (const void*)k_sh_finish, (const void*)k_sh_tail})
             preload_kernel(k);
         preload_compact<EmitSlots>();
         upload_route_map(*t, s2p.data(), G);
@@ -429,8 +459,13 @@ struct ShardedRank {
         MPZCH_CUDA(cudaMalloc(&d_state, sizeof(ShState)));
         MPZCH_CUDA(cudaMemset(d_state, 0, sizeof(ShState)));
         MPZCH_CUDA(cudaMalloc(&d_ctr, sizeof(BatchCounters)));
-        MPZCH_CUDA(cudaMallocHost(&h_state, sizeof(ShState) * kRing));
-        MPZCH_CUDA(cudaMallocHost(&h_ctr, sizeof(BatchCounters) * kRing));
+        // pinned result slots the last kernel of a batch writes directly (mapped host memory)
+        MPZCH_CUDA(cudaHostAlloc(&h_state, sizeof(ShState) * kRing, cudaHostAllocMapped));
+        MPZCH_CUDA(cudaHostAlloc(&h_ctr, sizeof(BatchCounters) * kRing, cudaHostAllocMapped));
+        MPZCH_CUDA(cudaHostGetDevicePointer((void**)&hd_state, h_state, 0));
+        MPZCH_CUDA(cudaHostGetDevicePointer((void**)&hd_ctr, h_ctr, 0));
+        std::memset(h_ctr, 0, sizeof(BatchCounters) * kRing);
+        k_sh_reset<<<1, 32>>>(d_state);
         for (auto& s : slots) MPZCH_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
         loc_slots.reserve(cap * 8);
         loc_oc.reserve(cap);
@@ -600,18 +635,18 @@ uint64_t ShardedRank::enqueue(const uint64_t* ids, const uint32_t* feats, uint64
     const unsigned B = 256;
     ShHeader* mh = reinterpret_cast<ShHeader*>(region);
 
-    // P1
-    k_sh_begin<<<1, 32, 0, st>>>(d_state);
+    // P1: the route count with the validation pass fused in, then publish + plan
     if (n && !too_big) {
-        k_sh_validate<<<grid_for(n, B, 148u * 8u), B, 0, st>>>(ids, feats, n, limit, pol.default_ttl, a.d_featk,
-                                                               a.d_featv, a.nk, may_over ? 1 : 0, d_state);
-        enqueue_route_count(T, ids, n, G, st);
+        if (may_over)
+            launch_pdl(k_sh_overflow, grid_for(n, B, 148u * 8u), B, st, feats, n, limit, pol.default_ttl,
+                       (const uint32_t*)a.d_featk, (const uint64_t*)a.d_featv, a.nk, d_state);
+        enqueue_route_count(T, ids, n, G, st, &d_state->local_bad);
     }
-    k_sh_publish<<<1, kMaxG, 0, st>>>(peers, rank, G, e, n, (pol.mode == kModeTtl && a.uniform && a.overflow_all) ? 1 : 0,
-                                      (n && !too_big) ? T.rt_tot.as<unsigned>() : nullptr, d_state);
-    k_sh_plan<<<1, kMaxG, 0, st>>>(mh, rank, G, e, cap, timeout_ns, d_state);
-    T.launches += 4;
-    // P2
+    launch_pdl(k_sh_publish_plan, 1, kMaxG, st, peers, mh, rank, G, e, n,
+               (uint64_t)((pol.mode == kModeTtl && a.uniform && a.overflow_all) ? 1 : 0),
+               (const unsigned*)((n && !too_big) ? T.rt_tot.as<unsigned>() : nullptr), cap, timeout_ns, d_state);
+    T.launches += 1;
+    // P2: route-scatter straight into the owners' receive buffers
     if (n && !too_big) {
         std::vector<uint64_t> ids_to(G), feats_to(G), src_to(G);
         for (uint32_t q = 0; q < G; ++q) {
@@ -624,9 +659,8 @@ uint64_t ShardedRank::enqueue(const uint64_t* ids, const uint32_t* feats, uint64
         d.gate = reinterpret_cast<const uint64_t*>(&d_state->failed);
         run_route_scatter(T, ids, feats, n, G, d, st);
     }
-    k_sh_signal<<<1, kMaxG, 0, st>>>(peers, kFScat, rank, G, e);
-    k_sh_wait<<<1, kMaxG, 0, st>>>(mh, kFScat, rank, G, e, timeout_ns, d_state);
-    T.launches += 2;
+    launch_pdl(k_sh_signal_wait, 1, kMaxG, st, peers, mh, (uint32_t)kFScat, rank, G, e, timeout_ns, d_state);
+    T.launches += 1;
     // P3: the owner's remap of its received positions
     const uint64_t* rids = reinterpret_cast<const uint64_t*>(region + L.ids);
     const uint32_t* rfeats = feats ? reinterpret_cast<const uint32_t*>(region + L.feats) : nullptr;
@@ -653,10 +687,9 @@ uint64_t ShardedRank::enqueue(const uint64_t* ids, const uint32_t* feats, uint64
         }
     } else {
         // one more host round trip: the ordinary remap needs R on the host
-        ShState hs;
         MPZCH_CUDA(cudaMemcpyAsync(&h_state[si], d_state, sizeof(ShState), cudaMemcpyDeviceToHost, st));
         MPZCH_CUDA(cudaStreamSynchronize(st));
-        hs = h_state[si];
+        const ShState hs = h_state[si];
         ++sl.host_waits;
         if (!hs.failed && hs.R) {
             try {
@@ -671,17 +704,12 @@ uint64_t ShardedRank::enqueue(const uint64_t* ids, const uint32_t* feats, uint64
         }
         if (pol.mode != kModeDisabled) mark = loc_mark.as<uint8_t>();
     }
-    // P4
-    k_sh_return<<<grid_for(cap, B, 148u * 8u), B, 0, st>>>(d_state, reinterpret_cast<const uint32_t*>(region + L.src),
-                                                          loc_slots.as<uint64_t>(), loc_oc.as<uint8_t>(), mark, clear,
-                                                          peers, L, G);
-    k_sh_signal<<<1, kMaxG, 0, st>>>(peers, kFRes, rank, G, e);
-    k_sh_wait<<<1, kMaxG, 0, st>>>(mh, kFRes, rank, G, e, timeout_ns, d_state);
-    T.launches += 3;
-    if (n && !too_big) {
-        MPZCH_CUDA(cudaMemcpyAsync(out_slots, region + L.rslots, n * 8, cudaMemcpyDeviceToDevice, st));
-        MPZCH_CUDA(cudaMemcpyAsync(out_oc, region + L.roc, n, cudaMemcpyDeviceToDevice, st));
-    }
+    // P4: results straight back into the sources' result buffers
+    launch_pdl(k_sh_return, grid_for(cap, B, 148u * 8u), B, st, (const ShState*)d_state,
+               (const uint32_t*)(region + L.src), (const uint64_t*)loc_slots.as<uint64_t>(),
+               (const uint8_t*)loc_oc.as<uint8_t>(), mark, clear, peers, L, G);
+    launch_pdl(k_sh_signal_wait, 1, kMaxG, st, peers, mh, (uint32_t)kFRes, rank, G, e, timeout_ns, d_state);
+    T.launches += 2;
     // P5: the canonical evicted list (only TTL / LRU batches can evict; the policy is the same on
     // every rank, so every rank runs this phase or none does)
     if (pol.mode != kModeDisabled) {
@@ -689,21 +717,21 @@ uint64_t ShardedRank::enqueue(const uint64_t* ids, const uint32_t* feats, uint64
             EmitSlots em{reinterpret_cast<const uint64_t*>(region + L.rslots), my_ev.as<uint64_t>()};
             compact_flags(region + L.rmark, n, blk.as<unsigned>(), &d_state->ev_mine, true, em, st, T.launches);
         }
-        k_sh_publish_evc<<<1, kMaxG, 0, st>>>(peers, rank, G, e, d_state);
-        k_sh_evplan<<<1, kMaxG, 0, st>>>(mh, rank, G, e, timeout_ns, d_state);
-        k_sh_ev_scatter<<<148u * 4u, B, 0, st>>>(d_state, my_ev.as<uint64_t>(), peers, L.ev, G);
-        k_sh_signal<<<1, kMaxG, 0, st>>>(peers, kFEv, rank, G, e);
-        k_sh_wait<<<1, kMaxG, 0, st>>>(mh, kFEv, rank, G, e, timeout_ns, d_state);
-        T.launches += 5;
-        if (out_ev && ev_cap) {
-            k_sh_ev_out<<<148u * 2u, B, 0, st>>>(d_state, reinterpret_cast<const uint64_t*>(region + L.ev), out_ev,
-                                                 ev_cap);
-            ++T.launches;
-        }
+        launch_pdl(k_sh_evc_plan, 1, kMaxG, st, peers, mh, rank, G, e, timeout_ns, d_state);
+        launch_pdl(k_sh_ev_scatter, 148u * 4u, B, st, (const ShState*)d_state, (const uint64_t*)my_ev.as<uint64_t>(),
+                   peers, L.ev, G);
+        launch_pdl(k_sh_signal_wait, 1, kMaxG, st, peers, mh, (uint32_t)kFEv, rank, G, e, timeout_ns, d_state);
+        T.launches += 3;
     }
+    // results to the caller, the state to the mapped result slot, then reset for the next batch
+    const bool want_ev = pol.mode != kModeDisabled && out_ev && ev_cap;
+    launch_pdl(k_sh_finish, grid_for(std::max<uint64_t>(too_big ? 0 : n, want_ev ? ev_cap : 0), B, 148u * 8u), B, st,
+               d_state, (const BatchCounters*)(fast ? d_ctr : nullptr), too_big ? 0 : n,
+               (const uint64_t*)(region + L.rslots), (const uint8_t*)(region + L.roc), out_slots, out_oc,
+               (const uint64_t*)(region + L.ev), want_ev ? out_ev : nullptr, ev_cap, hd_state + si, hd_ctr + si);
+    launch_pdl(k_sh_tail, 1, 32, st, d_state);
+    T.launches += 2;
     MPZCH_CUDA(cudaGetLastError());
-    MPZCH_CUDA(cudaMemcpyAsync(&h_state[si], d_state, sizeof(ShState), cudaMemcpyDeviceToHost, st));
-    MPZCH_CUDA(cudaMemcpyAsync(&h_ctr[si], d_ctr, sizeof(BatchCounters), cudaMemcpyDeviceToHost, st));
     MPZCH_CUDA(cudaEventRecord(sl.done, st));
     sl.busy = true;
     sl.ticket = e;

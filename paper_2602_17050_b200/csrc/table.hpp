@@ -287,7 +287,9 @@ void fill_policy_args(Table& t, const Policy& pol, uint64_t now, const uint32_t*
                       cudaStream_t st);
 // count-only route (route.cu) without a host sync: per-chunk offsets and per-part totals
 // stay on the device (t.rt_cnt, t.rt_tot); the shard -> part map must be uploaded already
-void enqueue_route_count(Table& t, const uint64_t* ids, uint64_t n, uint32_t parts, cudaStream_t st);
+// bad (nullable): the validation pass fused in -- atomicMin of the first invalid position
+void enqueue_route_count(Table& t, const uint64_t* ids, uint64_t n, uint32_t parts, cudaStream_t st,
+                         unsigned long long* bad = nullptr);
 void upload_route_map(Table& t, const uint32_t* shard_to_part, uint32_t parts);
 
 // enqueue the whole batch; counters land in t.h_ctr after the stream syncs
