@@ -72,7 +72,9 @@ struct TableDev {
     uint64_t* meta;      // metadata per global row
     float* weights;      // rows x dim (dim > 0)
     float* momentum;     // rows x dim
-    uint8_t* trained;    // rows
+    uint32_t* trained;   // one bit per held row (row - row_lo): EmbeddingTable::trained_
+                         // (embedding_store.hpp, a byte per row there); bits keep the flag words
+                         // L2-resident, so resets and steps pay no DRAM fill for a 1-byte store
     uint64_t* row_gen;   // rows
     const ShardDev* shards;
     FastMod nshards;
@@ -115,6 +117,15 @@ __device__ __forceinline__ float4 draw_quad(uint64_t s0, uint32_t q, double boun
     v.z = draw_at(s1 + 2 * kGolden, bound);
     v.w = draw_at(s1 + 3 * kGolden, bound);
     return v;
+}
+
+__device__ __forceinline__ void set_trained(const TableDev& t, uint64_t row) {
+    const uint64_t r = row - t.row_lo;
+    atomicOr(t.trained + (r >> 5), 1u << (r & 31));
+}
+__device__ __forceinline__ void clear_trained(const TableDev& t, uint64_t row) {
+    const uint64_t r = row - t.row_lo;
+    atomicAnd(t.trained + (r >> 5), ~(1u << (r & 31)));
 }
 
 // is the row's reset pending (deferred mode only)

@@ -68,7 +68,7 @@ __device__ __forceinline__ void reset_row_warp(const TableDev& t, uint64_t row, 
             m[j] = 0.f;
         }
     }
-    if (lane == 0) t.trained[row] = 0;
+    if (lane == 0) clear_trained(t, row);
 }
 
 // reset: a warp takes 32 listed rows at a time (one coalesced load of their indices, so no
@@ -183,6 +183,36 @@ __global__ void __launch_bounds__(256) k_gather_rows(TableDev t, const uint64_t*
 }
 
 }  // namespace
+
+__global__ void k_trained_bytes(TableDev t, uint64_t row0, uint64_t n, uint8_t* __restrict__ out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = row0 + i - t.row_lo;
+        out[i] = (uint8_t)((t.trained[r >> 5] >> (r & 31)) & 1u);
+    }
+}
+
+__global__ void k_set_trained_flag(TableDev t, uint64_t row, int v) {
+    if (v) set_trained(t, row);
+    else clear_trained(t, row);
+}
+
+// the trained flags of rows [row0, row0 + n) as bytes (the reference's layout), synchronous
+void copy_trained_bytes(Table& t, uint64_t row0, uint64_t n, uint8_t* host_out) {
+    if (!n) return;
+    t.sb_buf.reserve(n);
+    k_trained_bytes<<<grid_for(n, 256, 148u * 8u), 256, 0, t.stream>>>(t.dev, row0, n, t.sb_buf.as<uint8_t>());
+    ++t.launches;
+    MPZCH_CUDA(cudaGetLastError());
+    MPZCH_CUDA(cudaMemcpyAsync(host_out, t.sb_buf.p, n, cudaMemcpyDeviceToHost, t.stream));
+    MPZCH_CUDA(cudaStreamSynchronize(t.stream));
+}
+
+void set_trained_flag(Table& t, uint64_t row, bool v) {
+    k_set_trained_flag<<<1, 1, 0, t.stream>>>(t.dev, row, v ? 1 : 0);
+    ++t.launches;
+    MPZCH_CUDA(cudaGetLastError());
+    MPZCH_CUDA(cudaStreamSynchronize(t.stream));
+}
 
 void preload_row_kernels() {
     preload_kernel((const void*)k_reset_rows);

@@ -134,9 +134,9 @@ Table::Table(const uint64_t* cap_in, uint32_t num_shards, uint32_t max_probe, ui
     if (dim > 0) {
         MPZCH_CUDA(cudaMalloc((void**)&weights, held * dim * sizeof(float)));
         MPZCH_CUDA(cudaMalloc((void**)&momentum, held * dim * sizeof(float)));
-        MPZCH_CUDA(cudaMalloc((void**)&trained, held));
+        MPZCH_CUDA(cudaMalloc((void**)&trained, (held + 31) / 32 * 4));
         MPZCH_CUDA(cudaMemsetAsync(momentum, 0, held * dim * sizeof(float), stream));
-        MPZCH_CUDA(cudaMemsetAsync(trained, 0, held, stream));
+        MPZCH_CUDA(cudaMemsetAsync(trained, 0, (held + 31) / 32 * 4, stream));
     }
     std::vector<ShardDev> hs(S);
     for (uint32_t s = 0; s < S; ++s) hs[s] = ShardDev{offsets[s], make_fastmod(caps[s])};
@@ -147,7 +147,7 @@ Table::Table(const uint64_t* cap_in, uint32_t num_shards, uint32_t max_probe, ui
     dev.meta = meta - row_base;
     dev.weights = weights ? weights - row_lo * dim : nullptr;
     dev.momentum = momentum ? momentum - row_lo * dim : nullptr;
-    dev.trained = trained ? trained - row_lo : nullptr;
+    dev.trained = trained;  // bit (row - row_lo)
     dev.row_gen = row_gen - row_lo;
     dev.row_lo = row_lo;
     dev.row_hi = row_hi;
@@ -1146,8 +1146,7 @@ mpzch_status mpzch_copy_trained(const mpzch_table* t, uint8_t* out) {
         flush_for_read(T);
         check_rows(T, T.row_lo, 0);
         DeviceGuard g(T.device);
-        MPZCH_CUDA(cudaStreamSynchronize(T.stream));
-        MPZCH_CUDA(cudaMemcpy(out, T.trained, T.held_rows(), cudaMemcpyDeviceToHost));
+        copy_trained_bytes(const_cast<Table&>(T), T.row_lo, T.held_rows(), out);
     });
 }
 
@@ -1228,7 +1227,7 @@ mpzch_status mpzch_write_row(mpzch_table* t, uint64_t row, const float* w, const
         MPZCH_CUDA(cudaStreamSynchronize(T.stream));
         if (w) MPZCH_CUDA(cudaMemcpy(T.dev.weights + row * T.dim, w, T.dim * 4, cudaMemcpyHostToDevice));
         if (m) MPZCH_CUDA(cudaMemcpy(T.dev.momentum + row * T.dim, m, T.dim * 4, cudaMemcpyHostToDevice));
-        MPZCH_CUDA(cudaMemcpy(T.dev.trained + row, &trained, 1, cudaMemcpyHostToDevice));
+        set_trained_flag(T, row, trained != 0);
         // a training write stamps the row dirty, as sgd_step does (table.cpp:170-176)
         MPZCH_CUDA(cudaMemcpy(T.dev.row_gen + row, &T.gen_clock, 8, cudaMemcpyHostToDevice));
     });
@@ -1770,8 +1769,7 @@ mpzch_status mpzch_copy_trained_range(const mpzch_table* t, uint64_t row0, uint6
         flush_for_read(T);
         check_rows(T, row0, nrows);
         DeviceGuard g(T.device);
-        MPZCH_CUDA(cudaStreamSynchronize(T.stream));
-        if (nrows) MPZCH_CUDA(cudaMemcpy(out, T.dev.trained + row0, nrows, cudaMemcpyDeviceToHost));
+        if (nrows) copy_trained_bytes(const_cast<Table&>(T), row0, nrows, out);
     });
 }
 

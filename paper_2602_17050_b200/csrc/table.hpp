@@ -153,7 +153,7 @@ public:
     uint64_t* meta = nullptr;
     float* weights = nullptr;
     float* momentum = nullptr;
-    uint8_t* trained = nullptr;
+    uint32_t* trained = nullptr;  // bitmap: one bit per held row
     uint64_t* row_gen = nullptr;
     ShardDev* d_shards = nullptr;
     TableDev dev{};
@@ -212,6 +212,9 @@ public:
 void launch_init_table(Table& t);
 // eager: resets the listed rows; deferred (t.dev.deferred): marks them reset-pending
 void launch_reset_rows(Table& t, const uint64_t* rows, const unsigned int* count, cudaStream_t st);
+// trained flags (bitmap) <-> the reference's bytes (synchronous on t.stream)
+void copy_trained_bytes(Table& t, uint64_t row0, uint64_t n, uint8_t* host_out);
+void set_trained_flag(Table& t, uint64_t row, bool v);
 // writes every pending reset (deferred mode) before a reader that is not reset-aware
 void flush_resets(Table& t, cudaStream_t st);
 void launch_write_slots(Table& t, const uint64_t* gslots, const uint64_t* ids, const uint64_t* metas,

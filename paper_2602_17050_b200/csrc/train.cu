@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(256) k_sgd_apply(TableDev t, const uint64_t* _
         apply_row(t, row, grads + i * t.dim, lr, beta, vec, sub, width, pend);
         if (sub == 0) {
             if (pend) clear_pending(t, row);
-            t.trained[row] = 1;
+            set_trained(t, row);
             if (bad == kEmpty) t.row_gen[row] = gen_clock;  // table.cpp:179
         }
     }
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(256) k_sgd_dups(TableDev t, const uint64_t* __
         }
         if (lane == 0 && any) {
             if (pend0) clear_pending(t, row);
-            t.trained[row] = 1;
+            set_trained(t, row);
             if (bad == kEmpty) t.row_gen[row] = gen_clock;
         }
     }
