@@ -39,8 +39,35 @@ __global__ void k_init_counters_o(BatchCounters* c) {
         BatchCounters z{};
         z.err.bad_pos = ~0ull;
         z.err.foreign_pos = ~0ull;
+        z.n_live = ~0ull;
+        z.path_taken = 1;
         *c = z;
     }
+}
+
+// gated start (behind an LRU claim attempt): the path runs only if the attempt aborted; else
+// its counter block is marked failed, and every kernel below returns at once
+__global__ void k_init_counters_gated(BatchCounters* c, const BatchCounters* attempt) {
+    if (threadIdx.x == 0) {
+        BatchCounters z{};
+        z.err.bad_pos = ~0ull;
+        z.err.foreign_pos = ~0ull;
+        z.n_live = ~0ull;
+        z.path_taken = 1;
+        if (!(attempt->lru_abort && !batch_failed(&attempt->err))) z.err.too_many = 3;  // skip
+        *c = z;
+    }
+}
+
+// after the gated path: its counters become the batch's if it ran
+__global__ void k_adopt_counters(BatchCounters* attempt, const BatchCounters* alt) {
+    if (threadIdx.x == 0 && alt->err.too_many != 3) *attempt = *alt;
+}
+
+__global__ void k_zero_marks(const BatchCounters* ctr, uint64_t n, uint8_t* __restrict__ mark) {
+    if (batch_failed(&ctr->err)) return;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        mark[i] = 0;
 }
 
 __global__ void __launch_bounds__(256) k_validate_dedup(TableDev t, const uint64_t* __restrict__ ids,
@@ -50,6 +77,7 @@ __global__ void __launch_bounds__(256) k_validate_dedup(TableDev t, const uint64
                                                         uint32_t nk, BatchCounters* ctr, u128* key,
                                                         unsigned* kmin, uint32_t* posent,
                                                         uint64_t mask) {
+    if (ctr->err.too_many == 3) return;  // gated off
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t id = ids[i];
@@ -88,6 +116,7 @@ __global__ void __launch_bounds__(256) k_first_flags(const BatchCounters* ctr, u
                                                      const uint32_t* __restrict__ posent,
                                                      const unsigned* __restrict__ kmin,
                                                      uint8_t* __restrict__ flag) {
+    if (ctr->err.too_many == 3) return;  // gated off (the flags stay all zero)
     const bool failed = batch_failed(&ctr->err);
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -114,6 +143,7 @@ __global__ void __launch_bounds__(256) k_prep(TableDev t, const BatchCounters* c
                                               const uint64_t* fv, uint32_t nk,
                                               uint32_t* __restrict__ ushard,
                                               uint64_t* __restrict__ umeta) {
+    if (ctr->err.too_many == 3) return;  // gated off
     const unsigned u = ctr->entry_count;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < u; k += gridDim.x * blockDim.x) {
         const uint32_t pos = upos[k];
@@ -368,8 +398,10 @@ __global__ void __launch_bounds__(256) k_mark_first(const BatchCounters* ctr,
         if (evflag[k]) mark[upos[k]] = 1;
 }
 
-__global__ void __launch_bounds__(256) k_cleanup_o(uint64_t n, const uint32_t* __restrict__ posent,
+__global__ void __launch_bounds__(256) k_cleanup_o(const BatchCounters* ctr, uint64_t n,
+                                                   const uint32_t* __restrict__ posent,
                                                    u128* key, unsigned* kmin) {
+    if (ctr->err.too_many == 3) return;  // gated off: validate_dedup wrote nothing
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t e = posent[i];
@@ -383,12 +415,18 @@ __global__ void __launch_bounds__(256) k_cleanup_o(uint64_t n, const uint32_t* _
 
 void preload_ordered_kernels() {
 #define PL(k) preload_kernel((const void*)(k))
-    PL(k_init_counters_o); PL(k_validate_dedup); PL(k_first_flags); PL(k_prep);
+    PL(k_init_counters_o); PL(k_init_counters_gated); PL(k_adopt_counters); PL(k_zero_marks);
+    PL(k_validate_dedup); PL(k_first_flags); PL(k_prep);
     PL(k_ordered<kModeDisabled>); PL(k_ordered<kModeTtl>); PL(k_ordered<kModeLru>);
     PL(k_ordered_hf<kModeDisabled>); PL(k_ordered_hf<kModeTtl>); PL(k_ordered_hf<kModeLru>);
     PL(k_scatter); PL(k_mark_first); PL(k_cleanup_o);
 #undef PL
     preload_compact<EmitUnique>();
+}
+
+void adopt_gated_counters(Table& t, BatchCounters* attempt, const BatchCounters* alt, cudaStream_t st) {
+    k_adopt_counters<<<1, 32, 0, st>>>(attempt, alt);
+    ++t.launches;
 }
 
 void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st, bool rounds) {
@@ -398,7 +436,8 @@ void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st, bool r
     const unsigned gN = grid_for(n, B);
     const Policy& p = *a.pol;
     const uint32_t nk = (uint32_t)p.keys.size();
-    k_init_counters_o<<<1, 32, 0, st>>>(t.d_ctr);
+    if (a.gate_ctr) k_init_counters_gated<<<1, 32, 0, st>>>(t.d_ctr, a.gate_ctr);
+    else k_init_counters_o<<<1, 32, 0, st>>>(t.d_ctr);
     uint64_t mask = 1024;
     while (mask < 2 * n) mask <<= 1;
     mask -= 1;
@@ -439,13 +478,13 @@ void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st, bool r
     t.launches += 2;
     if (t.dim > 0) launch_reset_rows(t, t.s_reset.as<uint64_t>(), &t.d_ctr->reset_count, st);
     if (a.out_mark) {  // unique k's first position is upos[k]
-        MPZCH_CUDA(cudaMemsetAsync(a.out_mark, 0, n, st));
+        k_zero_marks<<<grid_for(n, B, 148u * 8u), B, 0, st>>>(t.d_ctr, n, a.out_mark);
         k_mark_first<<<gN, B, 0, st>>>(t.d_ctr, t.o_upos.as<uint32_t>(), t.s_evflag.as<uint8_t>(),
                                        a.out_mark);
         ++t.launches;
     }
     if (p.mode != kModeDisabled) enqueue_compact_evicted(t, n, a.out_ev, a.ev_cap, st);
-    k_cleanup_o<<<gN, B, 0, st>>>(n, posent, key, kmin);
+    k_cleanup_o<<<gN, B, 0, st>>>(t.d_ctr, n, posent, key, kmin);
     ++t.launches;
 }
 

@@ -694,7 +694,8 @@ uint64_t ShardedRank::enqueue(const uint64_t* ids, const uint32_t* feats, uint64
         if (!hs.failed && hs.R) {
             try {
                 const uint64_t tk = enqueue_batch(T, rids, rfeats, hs.R, now, pol, loc_slots.as<uint64_t>(),
-                                                  loc_oc.as<uint8_t>(), nullptr, 0, st, loc_mark.as<uint8_t>());
+                                                  loc_oc.as<uint8_t>(), nullptr, 0, st, loc_mark.as<uint8_t>(),
+                                                  /*host_waits*/ true);
                 wait_batch(T, tk);
                 ++sl.host_waits;
             } catch (const Error& err) {

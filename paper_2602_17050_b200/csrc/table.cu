@@ -116,9 +116,10 @@ Table::Table(const uint64_t* cap_in, uint32_t num_shards, uint32_t max_probe, ui
     DeviceGuard g(device);
     MPZCH_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     MPZCH_CUDA(cudaMallocHost((void**)&h_ring, (kRing + 1) * sizeof(BatchCounters)));
-    MPZCH_CUDA(cudaMalloc((void**)&d_ring, (kRing + 1) * sizeof(BatchCounters)));
+    MPZCH_CUDA(cudaMalloc((void**)&d_ring, (kRing + 2) * sizeof(BatchCounters)));
     h_aux = h_ring + kRing;
     d_aux = d_ring + kRing;
+    d_alt = d_ring + kRing + 1;
     h_ctr = h_ring;
     d_ctr = d_ring;
     for (auto& sl : slots) MPZCH_CUDA(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
@@ -163,6 +164,17 @@ Table::Table(const uint64_t* cap_in, uint32_t num_shards, uint32_t max_probe, ui
     dev.P = P;
     dev.dim = dim;
     launch_init_table(*this);
+    // every kernel loaded now, once per device: lazy loading would put a one-off load (18 ms
+    // for the LRU rounds path) into some batch's latency instead
+    static std::mutex mu;
+    static std::vector<int> loaded;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (std::find(loaded.begin(), loaded.end(), device) == loaded.end()) {
+            preload_all_kernels();
+            loaded.push_back(device);
+        }
+    }
     MPZCH_CUDA(cudaStreamSynchronize(stream));
 }
 
@@ -363,20 +375,32 @@ void complete_slot(Table& t, int si) {
         r.status = MPZCH_EOVERFLOW;
         r.msg = "TTL expiry overflows the 64-bit timestamp range";
     }
+    uint32_t path = sl.path;
+    if (sl.lru_try) {  // the claim attempt aborted on the device -> the gated rounds path ran
+        path = c.path_taken ? MPZCH_PATH_ROUNDS : MPZCH_PATH_AUTO;
+        t.lru_recent_abort = c.path_taken != 0;
+        if (c.path_taken) {  // skip the attempt for 1, 3, 7, ... (at most 15) LRU batches
+            ++t.lru_fallbacks;
+            t.lru_backoff = std::min<uint32_t>(2 * t.lru_backoff + 1, 15);
+            t.lru_skip_left = t.lru_backoff;
+        } else if (r.status == MPZCH_OK) {
+            t.lru_backoff = 0;
+        }
+    }
     if (r.status == MPZCH_OK) {
         r.evicted_n = c.evicted_count;
         mpzch_batch_stats& s = r.stats;
         s.positions = sl.n;
-        s.new_positions = sl.fast ? c.new_count : 0;
+        s.new_positions = (sl.fast && path == MPZCH_PATH_AUTO) ? c.new_count : 0;
         s.new_ids = c.entry_count;
         s.found = c.found;
         s.inserted = c.inserted;
         s.evicted = c.evicted;
         s.collision = c.collision;
         s.evicted_rows = c.evicted_count;
-        s.path = sl.path;
-        s.rounds = sl.path == MPZCH_PATH_ROUNDS ? c.r_rounds : 0;
-        if (sl.path == MPZCH_PATH_ROUNDS && getenv("MPZCH_DEBUG_ROUNDS"))
+        s.path = path;
+        s.rounds = path == MPZCH_PATH_ROUNDS ? c.r_rounds : 0;
+        if (path == MPZCH_PATH_ROUNDS && getenv("MPZCH_DEBUG_ROUNDS"))
             fprintf(stderr, "rounds u=%u rounds=%u iters=%u marked=%u left=%u\n", c.entry_count,
                     c.r_rounds, c.r_iters, c.r_marked, c.r_left);
         if (sl.profiled && sl.fast) {
@@ -473,7 +497,7 @@ void fill_policy_args(Table& t, const Policy& pol, uint64_t now, const uint32_t*
 uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n,
                        uint64_t now, const Policy& pol, uint64_t* out_slots, uint8_t* out_oc,
                        uint64_t* out_ev, uint64_t ev_cap, cudaStream_t st,
-                       uint8_t* out_mark = nullptr) {
+                       uint8_t* out_mark, bool host_waits) {
     if (n > 0xffffffffull) throw Error{MPZCH_ELENGTH, "batch exceeds 2^32 - 1 positions"};
     const uint64_t ticket = t.next_ticket++;
     const int si = (int)(ticket % Table::kRing);
@@ -519,11 +543,24 @@ uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uin
         lru_try = false;
         fast = false;
     }
-    if (lru_try) {
-        // LRU differs from Disabled only when a new id finds its window full (it evicts the
-        // least recently used slot, which depends on the batch's own refreshes).  Try the
-        // claim path with metadata writes held back; if any window is full it reverts its
-        // claims on the device and the batch goes to the rounds path (one host round trip).
+    // LRU differs from Disabled only when a new id finds its window full (it evicts the least
+    // recently used slot, which depends on the batch's own refreshes).  The claim path runs with
+    // its metadata writes held back; if an eviction cannot be placed exactly it reverts its
+    // claims on the device and the batch takes the rounds path.  Who decides:
+    //  * gated (asynchronous calls, or after a recent abort): the rounds path is enqueued right
+    //    behind the attempt and runs only if the attempt's abort flag is set -- the host never
+    //    waits and the rounds path's launches overlap the attempt (LRU pool 1.2 x rows: 142 ->
+    //    210 M/s), but an attempt that succeeds still pays the gated launches;
+    //  * host (a synchronous call whose recent attempts succeeded): one round trip for the flag,
+    //    the rounds path enqueued only if needed (LRU pool 0.8 x rows: 699 vs 498 M/s gated).
+    if (lru_try) {  // the rounds path's scratch, sized before any batch may need it
+        t.ensure_ordered_scratch(n);
+        ensure_rounds_scratch(t, n, t.stream);
+        MPZCH_CUDA(cudaStreamSynchronize(t.stream));
+    }
+    const bool gated = lru_try && (!host_waits || t.lru_recent_abort);
+    const bool lru_attempted = lru_try;
+    if (lru_try && !gated) {
         t.profiling = false;
         enqueue_fast_batch(t, a, st);
         MPZCH_CUDA(cudaMemcpyAsync(t.h_ctr, t.d_ctr, sizeof(BatchCounters), cudaMemcpyDeviceToHost, st));
@@ -531,13 +568,25 @@ uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uin
         const BatchErr& e = t.h_ctr->err;
         const bool failed = e.bad_pos != ~0ull || e.overflow || e.too_many || e.foreign_pos != ~0ull;
         fast = failed || !t.h_ctr->lru_abort;
+        lru_try = false;  // decided here
         if (!fast) {
             ++t.lru_fallbacks;
+            t.lru_recent_abort = true;
             t.lru_backoff = std::min<uint32_t>(2 * t.lru_backoff + 1, 15);
             t.lru_skip_left = t.lru_backoff;
         } else {
             t.lru_backoff = 0;
         }
+    } else if (gated) {
+        t.profiling = false;
+        enqueue_fast_batch(t, a, st);
+        BatchArgs g = a;
+        g.gate_ctr = t.d_ctr;
+        BatchCounters* attempt = t.d_ctr;
+        t.d_ctr = t.d_alt;
+        enqueue_ordered_batch(t, g, st, /*rounds*/ true);
+        t.d_ctr = attempt;
+        adopt_gated_counters(t, attempt, t.d_alt, st);
     } else if (fast) {
         enqueue_fast_batch(t, a, st);
     }
@@ -555,8 +604,9 @@ uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uin
     sl.n = n;
     sl.fast = fast;
     sl.path = fast ? MPZCH_PATH_AUTO : (rounds ? MPZCH_PATH_ROUNDS : MPZCH_PATH_ORDERED);
+    sl.lru_try = lru_try;  // path decided on the device (complete_slot reads it)
     sl.overflow_all = a.overflow_all;
-    sl.profiled = profiled && fast && !lru_try;  // per-kernel events: plain fast batches only
+    sl.profiled = profiled && fast && !lru_attempted;  // per-kernel events: plain fast batches only
     sl.lookup = false;
     t.last_stream = st;
     t.last_ticket = ticket;
@@ -579,7 +629,7 @@ void run_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n,
                uint64_t ev_cap, uint64_t* out_ev_n, cudaStream_t st, uint8_t* out_mark = nullptr) {
     if (out_ev_n) *out_ev_n = 0;
     const uint64_t tk = enqueue_batch(t, ids, feats, n, now, pol, out_slots, out_oc, out_ev, ev_cap,
-                                      st, out_mark);
+                                      st, out_mark, /*host_waits*/ true);
     const uint64_t nev = wait_batch(t, tk);
     if (out_ev_n) *out_ev_n = nev;
     if (n == 0) t.last = mpzch_batch_stats{};

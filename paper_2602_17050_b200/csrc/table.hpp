@@ -69,6 +69,9 @@ struct BatchCounters {
     unsigned int ldeferred;            // synchronous lookups: walks handed to the resume pass
     unsigned long long n_live;         // positions of the batch when only the device knows them
                                        // (row-sharded owner: the received count); ~0 = kernel arg
+    unsigned int path_taken;           // 0: the claim path; 1: the ordered / rounds path ran
+                                       // (an LRU claim attempt that aborted, decided on the device)
+    unsigned int pad2;
 };
 
 // sgd_step scratch counters (train.cu)
@@ -114,6 +117,7 @@ public:
     int path_override = MPZCH_PATH_AUTO;
     uint64_t lru_fallbacks = 0;  // LRU batches that needed an eviction (claim attempt reverted)
     uint32_t lru_backoff = 0, lru_skip_left = 0;  // claim-attempt backoff after evictions
+    bool lru_recent_abort = false;  // the last decided LRU attempt aborted (gated decision next)
     mpzch_batch_stats last{};
     uint64_t launches = 0;
     bool profiling = false;
@@ -129,6 +133,7 @@ public:
         uint64_t ticket = 0, n = 0;
         cudaEvent_t done = nullptr;
         bool lookup = false;  // a batched read-only lookup (mpzch_lookup_device_async)
+        bool lru_try = false; // an LRU claim attempt with the gated rounds path behind it
         cudaEvent_t ev[8] = {};
     };
     struct Result {
@@ -146,6 +151,7 @@ public:
     BatchCounters* d_ring = nullptr;  // kRing blocks
     BatchCounters* h_ring = nullptr;  // pinned
     BatchCounters* d_aux = nullptr;   // synchronous helpers (lookup, validate, dirty rows)
+    BatchCounters* d_alt = nullptr;   // the gated ordered / rounds path's counters (LRU attempts)
     BatchCounters* h_aux = nullptr;
 
     // resident arrays
@@ -266,13 +272,16 @@ struct BatchArgs {
     // received count come from this device state (k_sh_adopt replaces validation), and the
     // evicted flags are left set for the return scatter instead of compacted here
     const void* sh_state = nullptr;
+    // LRU claim attempt followed on the same stream by the ordered / rounds path, which runs only
+    // if the attempt aborted (read from this counter block on the device: no host round trip)
+    const BatchCounters* gate_ctr = nullptr;
 };
 
 // table.cu: the batch machinery the row-sharded layer (sharded.cu) reuses
 Policy parse_policy(const mpzch_policy* p);
 uint64_t enqueue_batch(Table& t, const uint64_t* ids, const uint32_t* feats, uint64_t n, uint64_t now,
                        const Policy& pol, uint64_t* out_slots, uint8_t* out_oc, uint64_t* out_ev,
-                       uint64_t ev_cap, cudaStream_t st, uint8_t* out_mark);
+                       uint64_t ev_cap, cudaStream_t st, uint8_t* out_mark = nullptr, bool host_waits = false);
 uint64_t wait_batch(Table& t, uint64_t ticket);
 // force-load kernels (lazy module loading can wait for running work; see common.cuh)
 void preload_remap_kernels();
@@ -298,6 +307,8 @@ void upload_route_map(Table& t, const uint32_t* shard_to_part, uint32_t parts);
 // enqueue the whole batch; counters land in t.h_ctr after the stream syncs
 void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st);
 void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st, bool rounds = false);
+// after a gated ordered path run on t.d_ctr: its counters replace `attempt`'s if it ran
+void adopt_gated_counters(Table& t, BatchCounters* attempt, const BatchCounters* alt, cudaStream_t st);
 void enqueue_rounds(Table& t, const BatchArgs& a, cudaStream_t st, uint8_t* todo);
 void ensure_rounds_scratch(Table& t, uint64_t n, cudaStream_t st);
 // gate (nullable): device word, 0 = no evicted flag can be set (LRU batches without evictors)
