@@ -54,23 +54,29 @@ constexpr uint8_t kStateCollided = 1;
 constexpr uint8_t kStateEvict = 2;     // LRU: the entry evicts the slot at offset `held` (K3b)
 constexpr uint8_t kPendingOc = 0xFF;   // LRU: out_oc of a position on the new list until K4/K5
 
-// Id table (one entry per distinct new id): an epoch-tagged 128-bit key (epoch << 64 | id)
-// -- any entry whose epoch is not the current batch's is empty, so no cleanup pass is
-// needed -- and an epoch-tagged rank word (epoch << 32 | ~first_position) updated with
-// atomicMax, which keeps the current epoch and the smallest first position.
+// Distinct new ids: a hash index of 16-byte keys (id | (epoch32 << 32 | e) << 64 -- a key whose
+// epoch is not the current batch's is empty, so no cleanup pass is needed) and DENSE entry
+// records, entry e = the new-list index of the item that inserted the id.  Most ids occur
+// once, so item k's entry is te[k]: the claim / commit / finalize passes over the new list read
+// their records coalesced instead of at random hash slots (C3: a 256 MB hash-addressed record
+// table for 1.5 M new ids, read at random by every pass).  The rank word (epoch << 32 |
+// ~first position) is updated with atomicMax, which keeps the current epoch and the smallest
+// first position without an initialising write.
 typedef unsigned __int128 u128;
 
-__device__ __forceinline__ u128 make_key(uint64_t epoch, uint64_t id) {
-    return ((u128)epoch << 64) | (u128)id;
+__device__ __forceinline__ u128 make_key(uint32_t epoch32, uint32_t e, uint64_t id) {
+    return ((u128)(((uint64_t)epoch32 << 32) | e) << 64) | (u128)id;
 }
 __device__ __forceinline__ uint64_t key_id(u128 k) { return (uint64_t)k; }
-__device__ __forceinline__ uint64_t key_epoch(u128 k) { return (uint64_t)(k >> 64); }
+__device__ __forceinline__ uint32_t key_epoch(u128 k) { return (uint32_t)(k >> 96); }
+__device__ __forceinline__ uint32_t key_entry(u128 k) { return (uint32_t)(k >> 64); }
 __device__ __forceinline__ uint32_t rank_of(uint64_t tr) { return ~(uint32_t)tr; }
 
-// One id-table entry in one 64-byte record, so every kernel's accesses to an entry
-// (insert, rank, claim bookkeeping, result) land in the same DRAM burst.
+// One entry in one 64-byte record, so every kernel's accesses to an entry (rank, claim
+// bookkeeping, result) land in the same DRAM burst.
 struct __align__(64) IdEntry {
-    u128 key;                 // epoch << 64 | id
+    uint64_t id;
+    uint64_t pad2;
     unsigned long long rank;  // epoch << 32 | ~first position   (atomicMax)
     uint32_t a;               // first available offset (taker start)
     uint32_t m;               // owner: offset of the expired own slot, else kNone32
@@ -577,34 +583,38 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
     }
 }
 
-// K2: distinct-id table over the new positions (128-bit CAS on an epoch-tagged key).
+// K2: distinct ids over the new positions: a 128-bit CAS inserts (id, epoch, e = this item's
+// new-list index) into the hash index; the inserter initialises te[e]; every item (inserter or
+// repeat) takes the id's first position into te[e].rank and records its entry.
 __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap, uint64_t epoch,
                                                const uint32_t* __restrict__ newpos,
                                                const uint64_t* __restrict__ newid,
                                                const uint32_t* __restrict__ newa,
                                                const uint32_t* __restrict__ newm,
-                                               uint32_t* __restrict__ newent, IdEntry* te) {
+                                               uint32_t* __restrict__ newent, u128* hk, IdEntry* te) {
     pdl_wait();
     if (batch_failed(&ctr->err)) return;
     const unsigned cnt = ctr->new_count;
     const uint64_t mask = table_mask(cnt, tcap);
+    const uint32_t ep32 = (uint32_t)epoch;
     unsigned dups = 0;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
         const uint64_t id = newid[k];
-        const u128 mine = make_key(epoch, id);
+        const u128 mine = make_key(ep32, k, id);
         uint64_t h = te_home(id, mask);
         uint32_t e;
         for (;;) {
             // a plain 16-byte L2 load first (one round trip less than an atomic read on the
-            // common path, a stale entry of an older epoch).  It is not single-copy atomic: a
+            // common path, a stale key of an older epoch).  It is not single-copy atomic: a
             // torn value can only fail the CAS below, or -- if it shows the current epoch --
             // is re-read atomically before it is trusted.
-            u128 cur = ld_cg_u128(&te[h].key);
-            if (key_epoch(cur) == epoch) cur = atomicCAS(&te[h].key, (u128)0, (u128)0);
-            if (key_epoch(cur) != epoch) {  // empty for this batch: try to take it
-                const u128 old = atomicCAS(&te[h].key, cur, mine);
-                if (old == cur) {  // inserted: publish the entry's probe facts
-                    e = (uint32_t)h;
+            u128 cur = ld_cg_u128(&hk[h]);
+            if (key_epoch(cur) == ep32) cur = atomicCAS(&hk[h], (u128)0, (u128)0);
+            if (key_epoch(cur) != ep32) {  // empty for this batch: try to take it
+                const u128 old = atomicCAS(&hk[h], cur, mine);
+                if (old == cur) {  // inserted: this item's record is the id's entry
+                    e = k;
+                    te[e].id = id;
                     // a | m << 32, then held = state = oc = 0: two 8-byte stores
                     uint64_t* w = reinterpret_cast<uint64_t*>(&te[e].a);
                     w[0] = (uint64_t)newa[k] | ((uint64_t)newm[k] << 32);
@@ -612,10 +622,10 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
                     break;
                 }
                 cur = old;
-                if (key_epoch(cur) != epoch) continue;  // raced with a stale value: retry
+                if (key_epoch(cur) != ep32) continue;  // raced with a stale value: retry
             }
             if (key_id(cur) == id) {
-                e = (uint32_t)h;
+                e = key_entry(cur);
                 ++dups;
                 break;
             }
@@ -670,7 +680,7 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
         uint32_t resume = 0;
         for (;;) {
             if (!fresh) ev = load_entry(te, e);  // a taken-over entry
-            const uint64_t id = *reinterpret_cast<const uint64_t*>(&te[e].key);
+            const uint64_t id = te[e].id;
             const uint32_t rank = rank_of(ev.rank);
             const uint32_t s = shard_of(id, t);
             const ShardDev sd = t.shards[s];
@@ -769,7 +779,7 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
             // or -- if it was an owner losing its own id's slot -- as a taker from its
             // first available offset.
             {
-                const uint64_t id2 = key_id(te[next].key);
+                const uint64_t id2 = te[next].id;
                 const uint64_t h2 = home_of(id2, sd, t.seed);  // same shard as the slot
                 const uint64_t loc = gnext - base;
                 const uint32_t off2 = (uint32_t)(loc >= h2 ? loc - h2 : loc + cap - h2);
@@ -1023,7 +1033,7 @@ __global__ void __launch_bounds__(256) k_lru_victim(TableDev t, uint64_t now, Ba
     const unsigned warps = gridDim.x * (blockDim.x >> 5);
     for (unsigned k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < cnt; k += warps) {
         const uint32_t e = evl[k];
-        const uint64_t id = key_id(te[e].key);
+        const uint64_t id = te[e].id;
         const uint32_t rank = rank_of(te[e].rank);
         const ShardDev sd = t.shards[shard_of(id, t)];
         const uint64_t cap = sd.cap.d, base = sd.offset, h = home_of(id, sd, t.seed);
@@ -1079,7 +1089,7 @@ __global__ void __launch_bounds__(256) k_lru_revert(TableDev t, BatchCounters* c
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
         const uint32_t e = newent[k];
         if (!is_primary(te, e, newpos[k]) || te[e].state == kStateCollided) continue;
-        const uint64_t id = key_id(te[e].key);
+        const uint64_t id = te[e].id;
         const ShardDev sd = t.shards[shard_of(id, t)];
         const uint64_t g = sd.offset + wrap_add(home_of(id, sd, t.seed), te[e].held, sd.cap.d);
         const uint64_t v = t.ident[g];
@@ -1170,7 +1180,14 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     const uint64_t n = a.n;
     t.ensure_fast_scratch(n);
     if (a.pol->mode == kModeLru) t.ensure_pf_scratch(n);  // the found map and victim set (K3a/K3b)
-    const uint64_t epoch = ++t.epoch;
+    uint64_t epoch = ++t.epoch;
+    if ((uint32_t)epoch == 0) {  // the keys' 32-bit epoch wrapped: start the index and records over
+        MPZCH_CUDA(cudaMemsetAsync(t.s_hkey.p, 0, t.s_hkey.bytes, st));
+        MPZCH_CUDA(cudaMemsetAsync(t.s_tent.p, 0, t.s_tent.bytes, st));
+        if (t.mf_tab.p) MPZCH_CUDA(cudaMemsetAsync(t.mf_tab.p, 0, t.mf_tab.bytes, st));
+        if (t.sl_tab.p) MPZCH_CUDA(cudaMemsetAsync(t.sl_tab.p, 0, t.sl_tab.bytes, st));
+        t.epoch = epoch = 1;
+    }
     const unsigned B = 256;
     const unsigned gW = grid_for(n, B, 148u * 8u);  // count-driven kernels (4/16/32 x 148: same)
     // 24 blocks per SM of grid (4 waves at 6 resident): 18 / 30 / 36 / 48 measured slower
@@ -1253,7 +1270,8 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     ++t.launches;
     if (t.profiling) cudaEventRecord(t.ev[1], st);
     IdEntry* te = t.s_tent.as<IdEntry>();
-    launch_pdl(k_dedup, gW, B, st, t.d_ctr, t.tcap, epoch, newpos, newid, newa, newm, newent, te);
+    launch_pdl(k_dedup, gW, B, st, t.d_ctr, t.tcap, epoch, (const uint32_t*)newpos, (const uint64_t*)newid,
+               (const uint32_t*)newa, (const uint32_t*)newm, newent, t.s_hkey.as<u128>(), te);
     if (t.profiling) cudaEventRecord(t.ev[4], st);
 #define MPZCH_CLAIM_COMMIT(MODE)                                                                   \
     launch_pdl(k_claim<MODE>, gW, B, st, t.dev, a.now, t.d_ctr, newpos, newent, te, nullptr);     \

@@ -207,10 +207,15 @@ void Table::ensure_fast_scratch(uint64_t n) {
     s_defer.reserve(n * 12);
     const uint64_t want = pow2_at_least(2 * n);
     if (want > tcap) {
-        s_tent.reserve(want * 64);  // epoch-tagged 64-byte entries: epoch 0 = empty
-        MPZCH_CUDA(cudaMemsetAsync(s_tent.p, 0, want * 64, stream));
+        // hash index: epoch-tagged 16-byte keys (epoch 0 = empty); dense 64-byte entry records,
+        // one per new-list item (their rank words are epoch-tagged too: zeroed once)
+        s_hkey.reserve(want * 16);
+        MPZCH_CUDA(cudaMemsetAsync(s_hkey.p, 0, want * 16, stream));
         tcap = want;
-        epoch = 0;
+    }
+    if (s_tent.bytes < std::max<uint64_t>(n, 1) * 64) {
+        s_tent.reserve(std::max<uint64_t>(n, 1) * 64);
+        MPZCH_CUDA(cudaMemsetAsync(s_tent.p, 0, s_tent.bytes, stream));
     }
     s_reset.reserve(n * 8);
     const size_t fl = ((n + 15) & ~15ull) + 16;

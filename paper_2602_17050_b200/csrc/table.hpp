@@ -177,8 +177,9 @@ public:
     DevBuf sb_buf;  // process_shard_batch / reset_row / gather staging
     DevBuf pend_map;  // MPZCH_RESET_DEFERRED: reset-pending bit per held row (dev.pend_bits)
     std::mutex lookup_mu;
-    DevBuf s_tent;                                   // id table: 64-byte entries
-    uint64_t tcap = 0;                               // allocated id-table capacity (pow2)
+    DevBuf s_tent;                                   // dense 64-byte entry records (fast path)
+    DevBuf s_hkey;                                   // hash index of the new ids: 16-byte keys
+    uint64_t tcap = 0;                               // allocated hash-index capacity (pow2)
     uint64_t epoch = 0;                              // id-table batch epoch (0 = never used)
     uint64_t fast_ready = 0;                         // largest n the fast scratch is ready for
     DevBuf s_reset;                                  // rows to reset
