@@ -583,6 +583,142 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
     }
 }
 
+// K1 (long windows, Disabled): the quad line walk with a one-line lookahead.  At 0.95 load a
+// miss walks ~6 lines of its 256-slot window one dependent 128-byte load after another; here
+// every round loads the current line AND the next line of the window (independent loads, so a
+// long walk takes half the round trips).  Decisions and the sector count are those of
+// k_probe_line: the second line is consulted only when the first holds neither the id nor an
+// EMPTY, so the extra load of a walk that stops in its first line is pure prefetch.
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_probe_line_la(TableDev t, const uint64_t* __restrict__ ids,
+                                                             uint64_t n, uint64_t now, uint64_t meta_value,
+                                                             BatchCounters* ctr,
+                                                             uint64_t* __restrict__ out_slots,
+                                                             uint8_t* __restrict__ out_oc,
+                                                             uint32_t* __restrict__ newpos,
+                                                             uint64_t* __restrict__ newid,
+                                                             uint32_t* __restrict__ newa,
+                                                             uint32_t* __restrict__ newm,
+                                                             const uint32_t* __restrict__ dlist = nullptr) {
+    pdl_wait();
+    if (batch_failed(&ctr->err)) return;
+    constexpr uint8_t kPending = 0, kHit = 1, kEmptyHit = 2, kExhausted = 3, kIdle = 4;
+    const unsigned lane = lane_id();
+    const unsigned j = quad_lane(), qm = quad_mask();
+    const uint64_t qpb = blockDim.x >> 2;
+    const uint64_t qib = threadIdx.x >> 2;
+    unsigned long long my_found = 0, my_coll = 0, my_isec = 0;
+    const uint64_t total = min(n, (uint64_t)ctr->n_live);
+    // (t0 is block-uniform, so every warp runs every iteration: the ballot below is full-warp)
+    for (uint64_t t0 = (uint64_t)blockIdx.x * qpb; t0 < total; t0 += (uint64_t)gridDim.x * qpb) {
+        const uint64_t i = t0 + qib;
+        uint8_t st = kIdle;
+        uint64_t id = 0, g = 0, base = 0, end = 0, h = 0;
+        uint32_t off = 0;
+        if (i < total) {
+            id = ids[i];
+            const ShardDev sd = t.shards[shard_of(id, t)];
+            base = sd.offset;
+            end = base + sd.cap.d;
+            h = home_of(id, sd, t.seed);
+            g = base + h;
+            st = kPending;
+        }
+        while (st == kPending) {
+            const LineSpan sp = line_span(g, end, off, t.P);
+            uint64_t g2 = g + sp.c;
+            if (g2 == end) g2 = base;
+            const uint32_t off2 = off + sp.c;
+            uint64_t w[4], w2[4];
+            ld_line_part(t.ident, g, j, w);
+            const bool second = off2 < t.P;
+            if (second) ld_line_part(t.ident, g2, j, w2);
+            unsigned m = 0, e = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                m |= (unsigned)(w[k] == id) << k;
+                e |= (unsigned)(w[k] == kEmpty) << k;
+            }
+            unsigned x = quad_gather(m, e, j, qm);
+            unsigned hit = (x | (x >> 16)) & sp.range();
+            if (hit) {
+                const unsigned q = __ffs(hit) - 1;
+                st = (x >> q) & 1u ? kHit : kEmptyHit;
+                off += q - sp.s;
+                g += q - sp.s;
+                my_isec += sp.sectors_to(q);
+                break;
+            }
+            my_isec += sp.sectors_to(sp.s + sp.c - 1);
+            if (!second) {
+                st = kExhausted;
+                break;
+            }
+            const LineSpan sp2 = line_span(g2, end, off2, t.P);
+            m = e = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                m |= (unsigned)(w2[k] == id) << k;
+                e |= (unsigned)(w2[k] == kEmpty) << k;
+            }
+            x = quad_gather(m, e, j, qm);
+            hit = (x | (x >> 16)) & sp2.range();
+            if (hit) {
+                const unsigned q = __ffs(hit) - 1;
+                st = (x >> q) & 1u ? kHit : kEmptyHit;
+                off = off2 + q - sp2.s;
+                g = g2 + q - sp2.s;
+                my_isec += sp2.sectors_to(q);
+                break;
+            }
+            my_isec += sp2.sectors_to(sp2.s + sp2.c - 1);
+            off = off2 + sp2.c;
+            g = g2 + sp2.c;
+            if (g == end) g = base;
+            if (off >= t.P) st = kExhausted;
+        }
+        bool is_new = false;
+        uint32_t a_off = 0;
+        if (st != kIdle && j == 0) {
+            uint64_t fslot = kEmpty;
+            uint8_t foc = kFound;
+            if (st == kHit) fslot = g;
+            else if (st == kEmptyHit) { is_new = true; a_off = off; }
+            else { fslot = base + h; foc = kCollision; }
+            if (fslot != kEmpty) {
+                out_slots[i] = fslot;
+                out_oc[i] = foc;
+                t.meta[fslot] = meta_value;
+                if (foc == kFound) ++my_found; else ++my_coll;
+            }
+        }
+        const unsigned mask = __ballot_sync(0xffffffffu, is_new);
+        if (mask) {
+            unsigned basek = 0;
+            if (lane == 0) basek = atomicAdd(&ctr->new_count, (unsigned)__popc(mask));
+            basek = __shfl_sync(0xffffffffu, basek, 0);
+            if (is_new) {
+                const unsigned k = basek + __popc(mask & ((1u << lane) - 1));
+                newpos[k] = (uint32_t)i;
+                newid[k] = id;
+                newa[k] = a_off;
+                newm[k] = kNone32;
+            }
+        }
+    }
+    if (j != 0) my_isec = 0;  // every lane of a quad counted the same sectors
+    for (int o = 16; o; o >>= 1) {
+        my_found += __shfl_xor_sync(0xffffffffu, my_found, o);
+        my_coll += __shfl_xor_sync(0xffffffffu, my_coll, o);
+        my_isec += __shfl_xor_sync(0xffffffffu, my_isec, o);
+    }
+    if (lane == 0) {
+        if (my_found) atomicAdd(&ctr->found, my_found);
+        if (my_coll) atomicAdd(&ctr->collision, my_coll);
+        if (my_isec) atomicAdd(&ctr->id_sectors, my_isec);
+    }
+}
+
 // K2: distinct ids over the new positions: a 128-bit CAS inserts (id, epoch, e = this item's
 // new-list index) into the hash index; the inserter initialises te[e]; every item (inserter or
 // repeat) takes the id's first position into te[e].rank and records its entry.
@@ -714,8 +850,52 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
             } else {
                 off = fresh ? ev.a : resume;
             }
-            if (!held) {
-                // sector-wide scan: one L2 read per 4 slots; a slot is re-read only through
+            if (!held && MODE != kModeTtl) {
+                // Disabled / LRU: only EMPTY slots and claim words of a higher rank are
+                // claimable.  Sector by sector: one L2 read, a 4-bit mask of the claimable slots
+                // in the window part of the sector, then atomicMin on them in order -- the
+                // occupied slots (95% of a window at C3's load) cost no per-slot iteration.
+                const uint64_t end = base + cap;
+                while (off < t.P) {
+                    const uint64_t g = base + wrap_add(h, off, cap);
+                    const uint64_t a4 = g & ~3ull;
+                    const uint32_t j0 = (uint32_t)(g - a4);
+                    uint32_t lim = 4 - j0;  // slots of this sector inside the window and the shard
+                    if (t.P - off < lim) lim = t.P - off;
+                    if (end - g < lim) lim = (uint32_t)(end - g);
+                    uint64_t w[4];
+                    ld_sector_cg(t.ident + a4, w[0], w[1], w[2], w[3]);
+                    unsigned cand = 0;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint64_t v = w[k];
+                        cand |= (unsigned)((v >> 63) && (v == kEmpty || claim_rank(v) >= rank)) << k;
+                    }
+                    cand &= ((1u << lim) - 1u) << j0;
+                    while (cand) {
+                        const unsigned k = __ffs(cand) - 1;
+                        cand &= cand - 1;
+                        const uint64_t v = pick4(k, w[0], w[1], w[2], w[3]);
+                        const uint64_t gk = a4 + k;
+                        const uint64_t nv = cv | (v == kEmpty ? kFlagEmpty : (v & kFlagEmpty));
+                        const uint64_t old = atomicMin((unsigned long long*)(t.ident + gk), (unsigned long long)nv);
+                        if (old < nv) continue;  // an id, or a lower rank got here first
+                        atomicMax(&te[e].held, off + (k - j0));
+                        held = true;
+                        if (old != kEmpty) { next = claim_entry(old); gnext = gk; }
+                        break;
+                    }
+                    if (held) break;
+                    off += lim;
+                }
+                if (!held) {
+                    te[e].state = kStateCollided;
+                    // LRU: a full window evicts its least recently used slot: K3b picks it
+                    // (a collided entry holds nothing, so it is never taken over again)
+                    if (MODE == kModeLru) evl[atomicAdd(&ctr->lru_evict, 1u)] = e;
+                }
+            } else if (!held) {
+                // TTL: sector-wide scan: one L2 read per 4 slots; a slot is re-read only through
                 // the CAS that tries it
                 uint64_t sec_a4 = ~0ull, w0 = 0, w1 = 0, w2 = 0, w3 = 0;
                 for (; off < t.P; ++off) {
@@ -1152,7 +1332,7 @@ void preload_remap_kernels() {
 #define PL(k) preload_kernel((const void*)(k))
     PL(k_init_counters); PL(k_sh_adopt); PL(k_validate);
     PL((k_probe_line<kModeTtl, 2, 3, true>)); PL((k_probe_line<kModeTtl, 2, 3>));
-    PL((k_probe_line<kModeLru, 2, 4>)); PL((k_probe_line<kModeDisabled, 1, 8>));
+    PL((k_probe_line<kModeLru, 2, 4>)); PL((k_probe_line<kModeDisabled, 1, 8>)); PL(k_probe_line_la<8>);
     PL((k_probe_line<kModeDisabled, 2, 4>)); PL((k_probe_line<kModeTtl, 1, 4, true, true>));
     PL((k_probe_line<kModeTtl, 1, 4, false, true>));
     PL((k_probe<kModeTtl, 2, 3, true, false, true>)); PL((k_probe<kModeTtl, 2, 3, true>));
@@ -1218,6 +1398,10 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     // small batches (C1: 64K positions) cannot fill the GPU with one thread per position: the
     // quad kernel runs 4x the threads and a quarter of the rounds per walk
     const bool line = forced >= 0 ? forced == 1 : (t.P >= 256 || n <= (1ull << 18));
+    static const bool la_env = [] {  // the one-line lookahead for long Disabled walks (MPZCH_LOOKAHEAD=0: off)
+        const char* e = std::getenv("MPZCH_LOOKAHEAD");
+        return !(e && std::string(e) == "0");
+    }();
 #define MPZCH_PROBE_ARGS t.dev, a.ids, n, a.now, a.uniform_meta, t.d_ctr, a.out_slots, a.out_oc, newpos, newid, newa, newm
     if (line) {
         constexpr int kUL = 2;
@@ -1228,6 +1412,8 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
         else if (lru) launch_pdl(k_probe_line<kModeLru, kUL, 4>, gl, B, st, MPZCH_PROBE_ARGS, nol);
         // long windows: one position per quad at 8 blocks/SM (C3 insert-heavy 1.88 -> 2.07 G/s);
         // small batches keep 2 per quad (C1 1.10 vs 1.04 G/s pipelined)
+        else if (t.P >= 256 && la_env)
+            launch_pdl(k_probe_line_la<8>, grid_for(4 * n, B, 148u * 32u), B, st, MPZCH_PROBE_ARGS, nol);
         else if (t.P >= 256)
             launch_pdl(k_probe_line<kModeDisabled, 1, 8>, grid_for(4 * n, B, 148u * 32u), B, st, MPZCH_PROBE_ARGS, nol);
         else launch_pdl(k_probe_line<kModeDisabled, kUL, 4>, gl, B, st, MPZCH_PROBE_ARGS, nol);
