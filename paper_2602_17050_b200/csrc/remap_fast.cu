@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
         uint32_t off[U];
         uint32_t fe[U];  // TTL: offset of the first expired slot walked before the stop
         bool hexp[U];    // TTL: the matched slot itself is expired
+        uint64_t hmv[MODE == kModeTtl ? U : 1];  // TTL: the matched slot's metadata word
         bool mld[U];     // TTL: this round's metadata sector was loaded
         uint8_t st[U];
 #pragma unroll
@@ -278,9 +279,11 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
                     const uint64_t v = pick4(jj, w[u][0], w[u][1], w[u][2], w[u][3]);
                     if (v == id[u]) {
                         st[u] = kHit;
-                        if (MODE == kModeTtl)
-                            hexp[u] = mld[u] ? pick4(jj, mw[u][0], mw[u][1], mw[u][2], mw[u][3]) < now
-                                             : __ldg(t.meta + g[u]) < now;
+                        if (MODE == kModeTtl) {
+                            hmv[MODE == kModeTtl ? u : 0] =
+                                mld[u] ? pick4(jj, mw[u][0], mw[u][1], mw[u][2], mw[u][3]) : __ldg(t.meta + g[u]);
+                            hexp[u] = hmv[MODE == kModeTtl ? u : 0] < now;
+                        }
                         break;
                     }
                     if (v == kEmpty) { st[u] = kEmptyHit; break; }
@@ -352,7 +355,12 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
                     // Found refresh / Collision at home (LRU: deferred to k_lru_meta, the
                     // batch may still turn out to need an eviction)
                     // (per-feature TTL: the last-writer pass after K5 writes it)
-                    if (MODE != kModeLru && !PF) t.meta[fslot] = meta_value;
+                    // (TTL: a live hit whose word already holds the batch's value -- a hot id's
+                    // later positions under skewed traffic -- skips the store: thousands of
+                    // stores to one word serialise in the L2)
+                    if (MODE != kModeLru && !PF &&
+                        !(MODE == kModeTtl && foc == kFound && hmv[MODE == kModeTtl ? u : 0] == meta_value))
+                        t.meta[fslot] = meta_value;
                     if (foc == kFound) ++my_found; else ++my_coll;
                 } else if (MODE == kModeLru) {
                     out_oc[i] = kPendingOc;  // K3a tells Found positions apart by this byte
@@ -1098,7 +1106,12 @@ __device__ __forceinline__ uint64_t pf_ttl(uint32_t f, uint64_t def, const uint3
 __device__ __forceinline__ uint32_t pf_find(PfEntry* tab, uint64_t mask, u128 mine, uint64_t h) {
     const uint32_t ep = (uint32_t)(mine >> 96);
     for (;;) {
-        u128 cur = atomicCAS(&tab[h].key, (u128)0, (u128)0);
+        // a plain L2 load first: under skewed traffic thousands of positions look up one hot
+        // record, and atomic reads of one address serialise.  A torn read equal to `mine` can only
+        // come from a record that holds `mine` (the halves of any other value differ from it)
+        u128 cur = ld_cg_u128(&tab[h].key);
+        if (cur == mine) return (uint32_t)h;
+        cur = atomicCAS(&tab[h].key, (u128)0, (u128)0);
         if ((uint32_t)(cur >> 96) != ep) {
             const u128 old = atomicCAS(&tab[h].key, cur, mine);
             if (old == cur) return (uint32_t)h;
@@ -1121,7 +1134,8 @@ __global__ void __launch_bounds__(256) k_pf_group(const BatchCounters* ctr, cons
         const uint32_t f = feats[i];
         const u128 mine = (u128)id | ((u128)f << 64) | ((u128)ep << 96);
         const uint32_t e = pf_find(tab, mask, mine, mix64(id ^ ((uint64_t)f * 0x9E3779B97F4A7C15ull), 0x51ED27ull) & mask);
-        atomicMax(&tab[e].rank, ((unsigned long long)ep << 32) | (uint32_t)~(uint32_t)i);
+        const unsigned long long r = ((unsigned long long)ep << 32) | (uint32_t)~(uint32_t)i;
+        if (__ldcg(&tab[e].rank) < r) atomicMax(&tab[e].rank, r);  // (skip the hot records' no-op atomics)
         ent[i] = e;
     }
 }
@@ -1195,7 +1209,8 @@ __global__ void __launch_bounds__(256) k_lru_found(BatchCounters* ctr, uint64_t 
         if (out_oc[i] != kFound) continue;
         const uint64_t g = out_slots[i];
         const uint32_t r = pf_find(ftab, mask, (u128)g | ((u128)ep << 96), mix64(g, 0xF0D5ull) & mask);
-        atomicMax(&ftab[r].rank, ((unsigned long long)ep << 32) | (uint32_t)~(uint32_t)i);
+        const unsigned long long v = ((unsigned long long)ep << 32) | (uint32_t)~(uint32_t)i;
+        if (__ldcg(&ftab[r].rank) < v) atomicMax(&ftab[r].rank, v);  // (hot slots: skip no-op atomics)
     }
 }
 
