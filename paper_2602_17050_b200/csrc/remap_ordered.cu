@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(256) k_validate_dedup(TableDev t, const uint64
             if (cur == k) break;
             h = (h + 1) & mask;
         }
-        atomicMin(kmin + h, (unsigned)i);
+        // (a plain read first: a hot id's thousands of positions would serialise on no-op atomics)
+        if (__ldcg(kmin + h) > (unsigned)i) atomicMin(kmin + h, (unsigned)i);
         posent[i] = (uint32_t)h;
     }
 }
