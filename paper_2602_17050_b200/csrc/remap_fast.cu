@@ -745,8 +745,22 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
         const uint64_t id = newid[k];
         const u128 mine = make_key(ep32, k, id);
+        const unsigned long long myrank = (epoch << 32) | (uint32_t)~newpos[k];
+        // this item's record is written BEFORE its key can be published: a repeat of the id that
+        // finds the key then only needs an atomicMax on a record that already holds this rank,
+        // and the inserter itself needs no atomic (a record whose key loses the race is never
+        // referenced)
+        te[k].id = id;
+        te[k].rank = myrank;
+        {
+            uint64_t* w = reinterpret_cast<uint64_t*>(&te[k].a);
+            w[0] = (uint64_t)newa[k] | ((uint64_t)newm[k] << 32);
+            w[1] = 0;  // held = state = oc = 0
+        }
+        __threadfence();
         uint64_t h = te_home(id, mask);
         uint32_t e;
+        bool inserted = false;
         for (;;) {
             // a plain 16-byte L2 load first (one round trip less than an atomic read on the
             // common path, a stale key of an older epoch).  It is not single-copy atomic: a
@@ -758,11 +772,7 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
                 const u128 old = atomicCAS(&hk[h], cur, mine);
                 if (old == cur) {  // inserted: this item's record is the id's entry
                     e = k;
-                    te[e].id = id;
-                    // a | m << 32, then held = state = oc = 0: two 8-byte stores
-                    uint64_t* w = reinterpret_cast<uint64_t*>(&te[e].a);
-                    w[0] = (uint64_t)newa[k] | ((uint64_t)newm[k] << 32);
-                    w[1] = 0;
+                    inserted = true;
                     break;
                 }
                 cur = old;
@@ -775,7 +785,7 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
             }
             h = (h + 1) & mask;
         }
-        atomicMax(&te[e].rank, (unsigned long long)((epoch << 32) | (uint32_t)~newpos[k]));
+        if (!inserted && __ldcg(&te[e].rank) < myrank) atomicMax(&te[e].rank, myrank);
         newent[k] = e;
     }
     for (int o = 16; o; o >>= 1) dups += __shfl_xor_sync(0xffffffffu, dups, o);
