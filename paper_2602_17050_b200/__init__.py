@@ -44,7 +44,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def lib_path() -> str:
-    return os.path.join(_HERE, "_lib", "libmpzch_b200.so")
+    # MPZCH_LIB_PATH: another build of the same sm_100a library (A/B measurements)
+    return os.environ.get("MPZCH_LIB_PATH") or os.path.join(_HERE, "_lib", "libmpzch_b200.so")
 
 
 class MpzchError(RuntimeError):

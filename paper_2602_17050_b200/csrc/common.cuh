@@ -85,7 +85,8 @@ struct TableDev {
     uint64_t row_hi;
     uint32_t shard_lo;   // logical shards this handle holds: [shard_lo, shard_hi)
     uint32_t shard_hi;
-    double bound;        // 1/sqrt(dim), computed on the host exactly as draw_row does
+    double bound;        // 1/sqrt(dim) * 2^-52 (draw_row's bound, computed on the host exactly as
+                         // the reference does, then scaled by a power of two: see draw_at)
     uint32_t P;          // max_probe
     uint32_t dim;
     uint32_t* pend_bits; // MPZCH_RESET_DEFERRED: one bit per held row (row - row_lo), set while
@@ -96,12 +97,14 @@ struct TableDev {
 
 // draw_row (proj/src/embedding_store.cpp:12-18), element with SplitMix64 state `state`
 // (= mix64(row, init_seed) + (j+1) * golden for element j); see rows.cu
-__device__ __forceinline__ float draw_at(uint64_t state, double bound) {
+__device__ __forceinline__ float draw_at(uint64_t state, double bound_s) {
     const uint64_t z = splitmix_out(state);
-    // 2u - 1 with u = (z >> 11) * 2^-53 is exactly ((z >> 11) - 2^52) * 2^-52: one exact
-    // integer -> double conversion instead of a multiply and an add (both exact as well)
-    const double t = (double)((int64_t)(z >> 11) - (1ll << 52)) * 0x1.0p-52;
-    return __double2float_rn(__dmul_rn(t, bound));
+    // (2u - 1) * bound with u = (z >> 11) * 2^-53: 2u - 1 = k * 2^-52 exactly, k = (z >> 11) - 2^52
+    // an integer, so the product is k * (bound * 2^-52) -- bound_s, scaled on the host by a power
+    // of two (exact) -- rounded once: the reference's single FP64 rounding with one FP64 multiply
+    // instead of two (the FP64 pipe bounds the reset kernel), bit for bit the same value
+    const double k = (double)((int64_t)(z >> 11) - (1ll << 52));
+    return __double2float_rn(__dmul_rn(k, bound_s));
 }
 
 __device__ __forceinline__ float draw_elem(uint64_t s0, uint64_t j, double bound) {

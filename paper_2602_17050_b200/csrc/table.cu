@@ -160,7 +160,7 @@ Table::Table(const uint64_t* cap_in, uint32_t num_shards, uint32_t max_probe, ui
     dev.init_seed = init_seed;
     dev.total = total;
     // draw_row's bound, embedding_store.cpp:14 (IEEE sqrt and division are exact-rounded on the host)
-    dev.bound = dim ? 1.0 / std::sqrt(static_cast<double>(dim)) : 0.0;
+    dev.bound = dim ? std::ldexp(1.0 / std::sqrt(static_cast<double>(dim)), -52) : 0.0;
     dev.P = P;
     dev.dim = dim;
     launch_init_table(*this);
