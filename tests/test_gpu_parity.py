@@ -797,3 +797,33 @@ def test_random_configurations(oracle, seed):
         assert (go == oo).all(), f"outcomes differ: batch {b}"
         assert (ge == oe).all(), f"evicted list differs: batch {b}"
         assert_same_state(gpu_state(t, dim), oracle_state(o, dim), f"batch {b}")
+
+
+@pytest.mark.parametrize("P", [256, 300])
+def test_high_load_insert_heavy_long_windows(oracle, P):
+    """C3's shape at 2^18 rows: prefilled to 0.95, then insert-heavy batches (50% fresh) with long
+    windows -- the one-line-lookahead probe, the 4-sector claim scan, takeover chains and ~30%
+    collisions -- over uneven shards (wrap-around at every shard end), against the oracle."""
+    caps = [40000, 70001, 65536, 86607]
+    rows = sum(caps)
+    t = mz.MpzchTable(mz.TableConfig(caps, P, 17))
+    o = oracle.OracleTable(caps, P, 17)
+    pol = mz.EvictionPolicy.disabled()
+    ids = oracle.distinct_ids(23, 0, rows + 200000)
+    npre = int(0.95 * rows)
+    for a in range(0, npre, 60000):
+        t.process_batch(ids[a:min(a + 60000, npre)], 1, pol)
+        o.process_batch(ids[a:min(a + 60000, npre)], 1, 0)
+    rng = np.random.default_rng(P)
+    fresh = npre
+    for b in range(4):
+        hits = ids[rng.integers(0, npre, 20000)]
+        new = ids[fresh:fresh + 20000]
+        fresh += 20000
+        batch = np.concatenate([hits, new])[rng.permutation(40000)]
+        gs, go, _ = t.process_batch(batch, 2 + b, pol)
+        os_, oo, _ = o.process_batch(batch, 2 + b, 0)
+        assert (gs == os_).all() and (go == oo).all(), f"batch {b}: {(gs != os_).sum()} slots differ"
+        assert (oo == 3).sum() > 1000  # the windows are full for many new ids
+    assert (t.identities_all() == o.identities_all()).all()
+    assert (t.metadata_all() == o.metadata_all()).all()
