@@ -406,7 +406,9 @@ __global__ void __launch_bounds__(256) k_cleanup_o(const BatchCounters* ctr, uin
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t e = posent[i];
-        if (e == kNone32) continue;
+        // only the unique's first position clears its entry: a hot id's thousands of positions
+        // would otherwise store to one record
+        if (e == kNone32 || __ldcg(kmin + e) != (unsigned)i) continue;
         key[e] = kKeyEmpty;
         kmin[e] = kNone32;
     }
