@@ -217,3 +217,38 @@ def test_device_protocol_two_processes(oracle, tmp_path):
         for g in got:
             assert (g["e"] == oe).all()
             assert int(g["hw"]) == 1
+
+
+def test_device_protocol_ttl_overflow_and_precedence(oracle):
+    """TTL expiry overflow (eviction.cpp:26-28) decided by every rank alike: a per-feature TTL that
+    overflows at `now` for a feature present only in rank 1's slice fails every rank; a uniform
+    TTL that overflows fails every rank; an invalid id anywhere takes precedence over the
+    overflow (the reference validates first, batch_engine.cpp:90-94); nothing is mutated."""
+    world = 2
+    caps = mz.even_capacities(1 << 12, 4)
+    cfg = mz.TableConfig(caps, 16, 7, 4, 3)
+    ranks = make_ranks(cfg, world, 4000)
+    ids = oracle.distinct_ids(8, 0, 1000)
+    now = (1 << 64) - 100
+    per = mz.EvictionPolicy.ttl(mz.TtlPolicy(10, {5: 1000}))   # feature 5 overflows, others do not
+    feats = np.zeros(1000, np.uint32)
+    feats[700] = 5                                               # rank 1's slice
+    out = run_batch(ranks, ids, feats, now, per, split(1000, world), threads=True)
+    for r in range(world):
+        assert isinstance(out[r], mz.OverflowError_), out[r]
+    feats[700] = 0
+    out = run_batch(ranks, ids, feats, now, per, split(1000, world), threads=True)  # no overflowing feature present
+    for r in range(world):
+        assert not isinstance(out[r], Exception), out[r]
+    uni = mz.EvictionPolicy.ttl(mz.TtlPolicy(1000))
+    out = run_batch(ranks, oracle.distinct_ids(9, 0, 800), None, now, uni, split(800, world), threads=True)
+    for r in range(world):
+        assert isinstance(out[r], mz.OverflowError_), out[r]
+    bad = oracle.distinct_ids(10, 0, 800)
+    bad[650] = np.uint64((1 << 64) - 1)
+    out = run_batch(ranks, bad, None, now, uni, split(800, world), threads=True)
+    for r in range(world):
+        assert isinstance(out[r], mz.InvalidArgument) and str(out[r]) == "invalid id at batch position 650", out[r]
+    o = oracle.OracleTable(caps, 16, 7, 4, 3)
+    o.process_batch(ids, now, 1, 10, {5: 1000}, feats)  # the one batch that went through
+    check_state(ranks, o, 4)
