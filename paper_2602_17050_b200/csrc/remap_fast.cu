@@ -311,7 +311,13 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (st[u] != kDeferred) continue;
-                const unsigned k = atomicAdd(&ctr->deferred, 1u);
+                // one counter update per group of deferring lanes
+                const unsigned am = __activemask();
+                const unsigned leader = __ffs(am) - 1;
+                unsigned b0 = 0;
+                if (lane == leader) b0 = atomicAdd(&ctr->deferred, (unsigned)__popc(am));
+                b0 = __shfl_sync(am, b0, leader);
+                const unsigned k = b0 + __popc(am & ((1u << lane) - 1));
                 dlist[3 * k] = (uint32_t)(t0 + (uint64_t)u * blockDim.x + threadIdx.x);
                 dlist[3 * k + 1] = off[u];
                 dlist[3 * k + 2] = fe[u];
@@ -910,7 +916,14 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                     te[e].state = kStateCollided;
                     // LRU: a full window evicts its least recently used slot: K3b picks it
                     // (a collided entry holds nothing, so it is never taken over again)
-                    if (MODE == kModeLru) evl[atomicAdd(&ctr->lru_evict, 1u)] = e;
+                    if (MODE == kModeLru) {  // one counter update per warp (Zipf: ~166 K evictors)
+                        const unsigned am = __activemask();
+                        const unsigned leader = __ffs(am) - 1;
+                        unsigned b0 = 0;
+                        if (lane_id() == leader) b0 = atomicAdd(&ctr->lru_evict, (unsigned)__popc(am));
+                        b0 = __shfl_sync(am, b0, leader);
+                        evl[b0 + __popc(am & ((1u << lane_id()) - 1))] = e;
+                    }
                 }
             } else if (!held) {
                 // TTL: sector-wide scan: one L2 read per 4 slots; a slot is re-read only through
@@ -969,7 +982,14 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                     te[e].state = kStateCollided;
                     // LRU: a full window evicts its least recently used slot: K3b picks it
                     // (a collided entry holds nothing, so it is never taken over again)
-                    if (MODE == kModeLru) evl[atomicAdd(&ctr->lru_evict, 1u)] = e;
+                    if (MODE == kModeLru) {  // one counter update per warp (Zipf: ~166 K evictors)
+                        const unsigned am = __activemask();
+                        const unsigned leader = __ffs(am) - 1;
+                        unsigned b0 = 0;
+                        if (lane_id() == leader) b0 = atomicAdd(&ctr->lru_evict, (unsigned)__popc(am));
+                        b0 = __shfl_sync(am, b0, leader);
+                        evl[b0 + __popc(am & ((1u << lane_id()) - 1))] = e;
+                    }
                 }
             }
             if (next == kNone32) break;

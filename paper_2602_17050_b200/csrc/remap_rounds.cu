@@ -259,11 +259,24 @@ __device__ __forceinline__ void commit(const RoundsArgs& r, uint32_t k) {
         t.row_gen[g] = r.gen_clock;
     }
     __stcg(t.meta + g, r.umeta[k]);
-    if (oc == kEvicted) {
-        if (t.dim) r.reset_rows[atomicAdd(&r.ctr->reset_count, 1u)] = g;
-        r.evflag[k] = 1;
-        r.evslot[k] = g;
-        atomicAdd(&r.ctr->evicted_count, 1u);
+    // the evicted uniques of the warp's active lanes: one counter update per warp (a Zipf LRU
+    // batch evicts ~166 K rows; same-address atomics serialise)
+    const unsigned am = __activemask();
+    const unsigned em = __ballot_sync(am, oc == kEvicted);
+    if (em) {
+        const unsigned leader = __ffs(em) - 1;
+        const unsigned below = __popc(em & ((1u << lane_id()) - 1));
+        unsigned r0 = 0;
+        if (lane_id() == leader) {
+            if (t.dim) r0 = atomicAdd(&r.ctr->reset_count, (unsigned)__popc(em));
+            atomicAdd(&r.ctr->evicted_count, (unsigned)__popc(em));
+        }
+        r0 = __shfl_sync(am, r0, leader);
+        if (oc == kEvicted) {
+            if (t.dim) r.reset_rows[r0 + below] = g;
+            r.evflag[k] = 1;
+            r.evslot[k] = g;
+        }
     }
     r.uslot[k] = g;
     r.uoc[k] = oc;
@@ -294,8 +307,8 @@ __global__ void __launch_bounds__(256) k_rounds(RoundsArgs r) {
         if (!npend) break;
         const uint32_t epoch = r.epoch0 + round;
         const uint32_t* pend = r.pend[par];
-        if (tid == 0) {
-            ctr->r_newc[0] = 0;
+        if (tid == 0) {  // closure pass c uses slot c % 3 (reset two passes ahead: see below)
+            ctr->r_newc[0] = ctr->r_newc[1] = 0;
             ctr->r_minrank = kNone32;
         }
         for (unsigned x = tid; x < npend; x += nth) tentative<MODE>(r, __ldcg(pend + x), epoch);
@@ -303,6 +316,10 @@ __global__ void __launch_bounds__(256) k_rounds(RoundsArgs r) {
         if (tid == 0) ctr->r_cnt[par ^ 1] = 0;
         for (int c = 0;; ++c) {  // suspicion closure: check and mark in one pass
             const bool last = c == r.closure_max;
+            // slot (c + 1) % 3 was last read (the break test) right after pass c - 2's barrier,
+            // which every thread has passed, so pass c may reset it for pass c + 1 (resetting it
+            // after this pass's barrier would race with pass c + 1's first updates)
+            if (tid == 0 && c > 0) ctr->r_newc[(c + 1) % 3] = 0;
             for (unsigned x = tid; x < npend; x += nth) {
                 const uint32_t k = __ldcg(pend + x);
                 if (ldcg_u8(r.susp + k) || !suspect<MODE>(r, k, epoch)) continue;
@@ -311,14 +328,18 @@ __global__ void __launch_bounds__(256) k_rounds(RoundsArgs r) {
                     atomicMin(&ctr->r_minrank, k);
                 } else {
                     mark_window(r, k, epoch);
-                    atomicAdd(&ctr->r_newc[c & 1], 1u);
-                    atomicAdd(&ctr->r_marked, 1u);
+                    // (hundreds of thousands of new suspects per batch under Zipf LRU: one
+                    // counter update per warp, not per suspect -- same-address atomics serialise)
+                    const unsigned am = __activemask();
+                    if (lane_id() == __ffs(am) - 1) {
+                        atomicAdd(&ctr->r_newc[c % 3], (unsigned)__popc(am));
+                        atomicAdd(&ctr->r_marked, (unsigned)__popc(am));
+                    }
                 }
             }
             grid.sync();
             if (tid == 0) ++ctr->r_iters;
-            if (last || !ldcg_u32(&ctr->r_newc[c & 1])) break;
-            if (tid == 0) ctr->r_newc[(c + 1) & 1] = 0;
+            if (last || !ldcg_u32(&ctr->r_newc[c % 3])) break;
         }
         const uint32_t bound = ldcg_u32(&ctr->r_minrank);
         uint32_t* next = r.pend[par ^ 1];
@@ -326,7 +347,13 @@ __global__ void __launch_bounds__(256) k_rounds(RoundsArgs r) {
             const uint32_t k = __ldcg(pend + x);
             if (ldcg_u8(r.susp + k) || k > bound) {
                 stcg_u8(r.susp + k, 0);
-                __stcg(next + atomicAdd(&ctr->r_cnt[par ^ 1], 1u), k);
+                // warp-aggregated append to the next round's pending list (its order is free)
+                const unsigned am = __activemask();
+                const unsigned leader = __ffs(am) - 1;
+                unsigned b0 = 0;
+                if (lane_id() == leader) b0 = atomicAdd(&ctr->r_cnt[par ^ 1], (unsigned)__popc(am));
+                b0 = __shfl_sync(am, b0, leader);
+                __stcg(next + b0 + __popc(am & ((1u << lane_id()) - 1)), k);
             } else {
                 commit(r, k);
             }

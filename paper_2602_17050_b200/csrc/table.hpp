@@ -63,7 +63,7 @@ struct BatchCounters {
     // rounds path (device-driven): pending count per round parity, new suspects per closure
     // step parity, lowest rank among the unmarked last-step suspects, rounds run, uniques left
     // for the ordered kernel
-    unsigned int r_cnt[2], r_newc[2], r_minrank, r_rounds, r_left, r_iters;
+    unsigned int r_cnt[2], r_newc[3], r_minrank, r_rounds, r_left, r_iters;
     unsigned int r_marked, r_checked;  // closure steps / windows marked / range checks (diagnostics)
     unsigned int deferred;             // TTL probe: walks handed to the resume pass
     unsigned int ldeferred;            // synchronous lookups: walks handed to the resume pass
