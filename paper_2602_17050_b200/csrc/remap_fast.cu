@@ -136,9 +136,14 @@ __global__ void k_init_counters(BatchCounters* c) {
 // received count bounds every position loop (n_live)
 __global__ void k_sh_adopt(BatchCounters* c, const ShStateView* st) {
     pdl_wait();
-    if (threadIdx.x == 0) {
-        if (st->failed) c->err.overflow = 1;
-        else c->n_live = st->R;
+    if (threadIdx.x == 0) {  // the counters' initialisation and the ranks' decision, one launch
+        BatchCounters z{};
+        z.err.bad_pos = ~0ull;
+        z.err.foreign_pos = ~0ull;
+        z.n_live = ~0ull;
+        if (st->failed) z.err.overflow = 1;
+        else z.n_live = st->R;
+        *c = z;
     }
 }
 
@@ -1425,12 +1430,14 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     uint32_t* newm = t.s_newm.as<uint32_t>();
     uint32_t* newent = t.s_newent.as<uint32_t>();
     if (t.profiling) cudaEventRecord(t.ev[7], st);
-    k_init_counters<<<1, 32, 0, st>>>(t.d_ctr);
-    if (a.sh_state)  // row-sharded owner: the sources validated; adopt the ranks' decision
+    if (a.sh_state) {  // row-sharded owner: the sources validated; adopt the ranks' decision
         launch_pdl(k_sh_adopt, 1, 32, st, t.d_ctr, (const ShStateView*)a.sh_state);
-    else
+        t.launches += 1;
+    } else {
+        k_init_counters<<<1, 32, 0, st>>>(t.d_ctr);
         launch_pdl(k_validate, grid_for(n / 2 + 1, B, 148u * 8u), B, st, t.dev, a.ids, n, t.d_ctr);
-    t.launches += 2;
+        t.launches += 2;
+    }
     if (a.overflow_all) return;  // validation only; the host reports the error
     if (t.profiling) cudaEventRecord(t.ev[0], st);
     // probe kernel: the quad line walk when windows run long (max_probe >= 256: at 0.95 load

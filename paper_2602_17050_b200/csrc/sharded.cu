@@ -77,7 +77,7 @@ struct ShState {
     unsigned long long local_bad, local_over;
     unsigned long long err_len, err_cap, err_bad, err_over, timeout;
     unsigned long long base, ntotal;
-    unsigned int ev_mine, pad;
+    unsigned int ev_mine, done;  // done: k_sh_finish's finished-block count
     unsigned long long ev_off, ev_total;
     unsigned long long my_off[kMaxG];
     unsigned long long roff[kMaxG + 1];
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(256) k_sh_finish(ShState* st, const BatchCount
                                                    const uint8_t* __restrict__ roc, uint64_t* __restrict__ out_slots,
                                                    uint8_t* __restrict__ out_oc, const uint64_t* __restrict__ ev_all,
                                                    uint64_t* __restrict__ out_ev, uint64_t ev_cap, ShState* h_st,
-                                                   BatchCounters* h_ctr) {
+                                                   BatchCounters* h_ctr, unsigned* done) {
     pdl_wait();
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -346,17 +346,19 @@ __global__ void __launch_bounds__(256) k_sh_finish(ShState* st, const BatchCount
             for (uint64_t k = tid; k < m; k += stride) out_ev[k] = ev_all[k];
         }
     }
-    // every block has read the state before block 0 resets it: the reset happens in a grid of
-    // one block or after the counters below, so do it in a separate tail (see the host)
     if (tid == 0) {
         *h_st = *st;
         if (ctr) *h_ctr = *ctr;
     }
-}
-
-__global__ void k_sh_tail(ShState* st) {
-    pdl_wait();
-    if (threadIdx.x == 0) reset_state(st);
+    // the last block to finish resets the state for the next batch (every block has read it)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(done, 1u) == gridDim.x - 1) {
+            reset_state(st);
+            *done = 0;
+        }
+    }
 }
 
 struct EmitSlots {
@@ -449,7 +451,7 @@ struct ShardedRank {
         preload_all_kernels();
         for (const void* k : {(const void*)k_sh_reset, (const void*)k_sh_overflow, (const void*)k_sh_publish_plan,
                               (const void*)k_sh_signal_wait, (const void*)k_sh_return, (const void*)k_sh_evc_plan,
-                              (const void*)k_sh_ev_scatter, (const void*)k_sh_finish, (const void*)k_sh_tail})
+                              (const void*)k_sh_ev_scatter, (const void*)k_sh_finish})
             preload_kernel(k);
         preload_compact<EmitSlots>();
         upload_route_map(*t, s2p.data(), G);
@@ -729,9 +731,9 @@ uint64_t ShardedRank::enqueue(const uint64_t* ids, const uint32_t* feats, uint64
     launch_pdl(k_sh_finish, grid_for(std::max<uint64_t>(too_big ? 0 : n, want_ev ? ev_cap : 0), B, 148u * 8u), B, st,
                d_state, (const BatchCounters*)(fast ? d_ctr : nullptr), too_big ? 0 : n,
                (const uint64_t*)(region + L.rslots), (const uint8_t*)(region + L.roc), out_slots, out_oc,
-               (const uint64_t*)(region + L.ev), want_ev ? out_ev : nullptr, ev_cap, hd_state + si, hd_ctr + si);
-    launch_pdl(k_sh_tail, 1, 32, st, d_state);
-    T.launches += 2;
+               (const uint64_t*)(region + L.ev), want_ev ? out_ev : nullptr, ev_cap, hd_state + si, hd_ctr + si,
+               &d_state->done);
+    T.launches += 1;
     MPZCH_CUDA(cudaGetLastError());
     MPZCH_CUDA(cudaEventRecord(sl.done, st));
     sl.busy = true;
