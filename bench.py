@@ -202,6 +202,30 @@ def probe_dram_accesses():
         return None
 
 
+def independent_ceiling(probe_ms):
+    """k_probe against the random-access ceiling measured with PyTorch's OWN gather / scatter
+    kernels (profiles/random_ceiling_torch_r02.json: index_select / index_put_ of 8-byte rows at
+    random over a 16 GiB array -- independent of this repo's code): the launch's DRAM reads
+    (128-byte line fetches) at the read rate plus its written sectors at the write rate, done one
+    after the other, is the time the memory system needs for that access mix; frac > 1 means the
+    reads and writes overlapped."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "random_ceiling_torch_r02.json")))
+        rows = [r for r in d["rows"] if r["gib"] == 16]
+        rd = next(r["G_accesses_s"] for r in rows if r["op"] == "index_select 8 B rows")
+        wr = next(r["G_accesses_s"] for r in rows if r["op"] == "index_put_ 8 B rows")
+        p = json.load(open(os.path.join(ROOT, "profiles", "ncu_probe_summary.json")))
+        reads, writes = p["dram_read_bytes"] / 128.0, p["dram_write_bytes"] / 32.0
+        ceil_ms = (reads / (rd * 1e9) + writes / (wr * 1e9)) * 1e3
+        return {"read_g_per_s": rd, "write_g_per_s": wr, "probe_dram_line_reads": reads,
+                "probe_dram_sector_writes": writes, "ceiling_ms": ceil_ms,
+                "frac": ceil_ms / probe_ms if probe_ms else None,
+                "source": "PyTorch index_select / index_put_ over 16 GiB (profiles/random_ceiling_torch_r02.json); "
+                          "probe DRAM counts from ncu (profiles/ncu_probe_summary.json)"}
+    except Exception:
+        return None
+
+
 def ncu_traffic():
     """dram bytes per probe launch from the committed ncu --set full summary, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_probe_summary.json")
@@ -677,6 +701,7 @@ def main():
                          "random_access_ceiling": random_access_ceiling(),
                          # (the ncu access count is for the single-GPU C5 launch)
                          "random_access_frac": _access_frac(probe_ms) if (world == 1 and rows == ROWS) else None,
+                         "independent_ceiling": independent_ceiling(probe_ms) if (world == 1 and rows == ROWS) else None,
                          "share_of_step": probe_ms / ms_step,
                          "batch_algorithmic_bytes": batch_bytes,
                          "batch_gbs": batch_bytes / (batch_ms / 1e3) / 1e9 if batch_ms else 0.0,
