@@ -931,57 +931,71 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                     }
                 }
             } else if (!held) {
-                // TTL: sector-wide scan: one L2 read per 4 slots; a slot is re-read only through
-                // the CAS that tries it
-                uint64_t sec_a4 = ~0ull, w0 = 0, w1 = 0, w2 = 0, w3 = 0;
-                for (; off < t.P; ++off) {
+                // TTL: the same sector mask with the metadata sector in the same round --
+                // claimable: EMPTY or a higher-rank claim word (atomicMin, as above), or an
+                // expired id (CAS, re-evaluated on failure) -- so the scan takes no dependent
+                // metadata load per occupied slot
+                const uint64_t end = base + cap;
+                while (off < t.P) {
                     const uint64_t g = base + wrap_add(h, off, cap);
-                    if ((g & ~3ull) != sec_a4) {
-                        sec_a4 = g & ~3ull;
-                        ld_sector_cg(t.ident + sec_a4, w0, w1, w2, w3);
+                    const uint64_t a4 = g & ~3ull;
+                    const uint32_t j0 = (uint32_t)(g - a4);
+                    uint32_t lim = 4 - j0;
+                    if (t.P - off < lim) lim = t.P - off;
+                    if (end - g < lim) lim = (uint32_t)(end - g);
+                    uint64_t w[4], mt[4];
+                    ld_sector_cg(t.ident + a4, w[0], w[1], w[2], w[3]);
+                    ld_sector_cg(t.meta + a4, mt[0], mt[1], mt[2], mt[3]);
+                    unsigned cand = 0;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint64_t v = w[k];
+                        const bool c = (v >> 63) ? (v == kEmpty || claim_rank(v) >= rank) : (mt[k] < now);
+                        cand |= (unsigned)c << k;
                     }
-                    uint64_t v = pick4((uint32_t)(g - sec_a4), w0, w1, w2, w3);
-                    if (MODE != kModeTtl || (v >> 63)) {
-                        // an EMPTY slot or a claim word: the lowest rank wins with one atomicMin --
-                        // no CAS retry loop under contention (EMPTY = ~0 and ids < 2^63 order
-                        // correctly around claim words, which order by rank; a slot's claim words
-                        // all carry its was-EMPTY flag).  Outside TTL only EMPTY slots are
-                        // claimable; under TTL an expired id is claimed by the CAS below.
-                        if (!(v >> 63) || (v != kEmpty && claim_rank(v) < rank)) continue;
-                        const uint64_t nv = cv | (v == kEmpty ? kFlagEmpty : (v & kFlagEmpty));
-                        const uint64_t old = atomicMin((unsigned long long*)(t.ident + g), (unsigned long long)nv);
-                        if (old < nv) continue;  // an id, or a lower rank got here first
-                        atomicMax(&te[e].held, off);
-                        held = true;
-                        if (old != kEmpty) { next = claim_entry(old); gnext = g; }
-                        break;
-                    }
-                    for (;;) {
-                        uint64_t nv;
-                        if (v == kEmpty) {
-                            nv = cv | kFlagEmpty;
-                        } else if (v >> 63) {
-                            if (claim_rank(v) < rank) break;  // a lower rank holds it for good
-                            nv = cv | (v & kFlagEmpty);
-                        } else {
-                            if (MODE != kModeTtl) break;           // occupied
-                            if (!(ld_cg(t.meta + g) < now)) break;  // live
-                            nv = cv;                                 // expired foreign id
-                        }
-                        const uint64_t old = atomicCAS((unsigned long long*)(t.ident + g),
-                                                       (unsigned long long)v,
-                                                       (unsigned long long)nv);
-                        if (old == v) {
-                            // taker claims of one entry move strictly forward, so the max is the
-                            // slot it holds last (a late max from a displaced claim is harmless)
-                            atomicMax(&te[e].held, off);
+                    cand &= ((1u << lim) - 1u) << j0;
+                    while (cand) {
+                        const unsigned k = __ffs(cand) - 1;
+                        cand &= cand - 1;
+                        uint64_t v = pick4(k, w[0], w[1], w[2], w[3]);
+                        const uint64_t gk = a4 + k;
+                        const uint32_t offk = off + (k - j0);
+                        if (v >> 63) {
+                            const uint64_t nv = cv | (v == kEmpty ? kFlagEmpty : (v & kFlagEmpty));
+                            const uint64_t old = atomicMin((unsigned long long*)(t.ident + gk), (unsigned long long)nv);
+                            if (old < nv) continue;  // an id, or a lower rank got here first
+                            atomicMax(&te[e].held, offk);
                             held = true;
-                            if (is_claim(v)) { next = claim_entry(v); gnext = g; }
+                            if (old != kEmpty) { next = claim_entry(old); gnext = gk; }
                             break;
                         }
-                        v = old;
+                        for (;;) {  // an expired foreign id
+                            uint64_t nv;
+                            if (v == kEmpty) {
+                                nv = cv | kFlagEmpty;
+                            } else if (v >> 63) {
+                                if (claim_rank(v) < rank) break;  // a lower rank holds it for good
+                                nv = cv | (v & kFlagEmpty);
+                            } else {
+                                if (!(ld_cg(t.meta + gk) < now)) break;  // live
+                                nv = cv;
+                            }
+                            const uint64_t old = atomicCAS((unsigned long long*)(t.ident + gk),
+                                                           (unsigned long long)v, (unsigned long long)nv);
+                            if (old == v) {
+                                // taker claims of one entry move strictly forward, so the max is the
+                                // slot it holds last (a late max from a displaced claim is harmless)
+                                atomicMax(&te[e].held, offk);
+                                held = true;
+                                if (is_claim(v)) { next = claim_entry(v); gnext = gk; }
+                                break;
+                            }
+                            v = old;
+                        }
+                        if (held) break;
                     }
                     if (held) break;
+                    off += lim;
                 }
                 if (!held) {
                     te[e].state = kStateCollided;
