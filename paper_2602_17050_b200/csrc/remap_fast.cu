@@ -740,7 +740,8 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line_la(TableDev t, const u
 
 // K2: distinct ids over the new positions: a 128-bit CAS inserts (id, epoch, e = this item's
 // new-list index) into the hash index; the inserter initialises te[e]; every item (inserter or
-// repeat) takes the id's first position into te[e].rank and records its entry.
+// repeat) takes the id's first position into te[e].rank (atomicMax of epoch << 32 | ~position)
+// and records its entry.
 __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap, uint64_t epoch,
                                                const uint32_t* __restrict__ newpos,
                                                const uint64_t* __restrict__ newid,
@@ -757,18 +758,6 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
         const uint64_t id = newid[k];
         const u128 mine = make_key(ep32, k, id);
         const unsigned long long myrank = (epoch << 32) | (uint32_t)~newpos[k];
-        // this item's record is written BEFORE its key can be published: a repeat of the id that
-        // finds the key then only needs an atomicMax on a record that already holds this rank,
-        // and the inserter itself needs no atomic (a record whose key loses the race is never
-        // referenced)
-        te[k].id = id;
-        te[k].rank = myrank;
-        {
-            uint64_t* w = reinterpret_cast<uint64_t*>(&te[k].a);
-            w[0] = (uint64_t)newa[k] | ((uint64_t)newm[k] << 32);
-            w[1] = 0;  // held = state = oc = 0
-        }
-        __threadfence();
         uint64_t h = te_home(id, mask);
         uint32_t e;
         bool inserted = false;
@@ -796,7 +785,18 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
             }
             h = (h + 1) & mask;
         }
-        if (!inserted && __ldcg(&te[e].rank) < myrank) atomicMax(&te[e].rank, myrank);
+        if (inserted) {
+            // the inserter fills its record (read only by later kernels); the rank word takes
+            // every item's rank by atomicMax -- inserter and repeats alike, in any order, no
+            // fence: a word left by an older batch holds an older epoch, so it is smaller
+            te[k].id = id;
+            uint64_t* w = reinterpret_cast<uint64_t*>(&te[k].a);
+            w[0] = (uint64_t)newa[k] | ((uint64_t)newm[k] << 32);
+            w[1] = 0;  // held = state = oc = 0
+            atomicMax(&te[k].rank, myrank);
+        } else if (__ldcg(&te[e].rank) < myrank) {  // (a hot id's later positions skip the atomic)
+            atomicMax(&te[e].rank, myrank);
+        }
         newent[k] = e;
     }
     for (int o = 16; o; o >>= 1) dups += __shfl_xor_sync(0xffffffffu, dups, o);

@@ -45,7 +45,8 @@ __global__ void __launch_bounds__(256) k_read(const uint64_t* __restrict__ a, ui
 }
 
 // read one random 32-byte sector and write 8 bytes at: MODE 0 the same sector, MODE 1 the
-// other sector of the same 64-byte pair, MODE 2 an unrelated random sector (SoA metadata)
+// other sector of the same 64-byte pair, MODE 2 an unrelated random sector (SoA metadata),
+// MODE 3 a sector of the other 64-byte half of the same 128-byte line
 template <int MODE>
 __global__ void __launch_bounds__(256) k_read_write(uint64_t* a, uint64_t nsec, uint64_t n, uint64_t salt) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -55,6 +56,7 @@ __global__ void __launch_bounds__(256) k_read_write(uint64_t* a, uint64_t nsec, 
         uint64_t t;
         if (MODE == 0) t = 4 * s + 1;
         else if (MODE == 1) t = 4 * (s ^ 1) + 1;
+        else if (MODE == 3) t = 4 * (s ^ 2) + 1;
         else t = 4 * (mix(i + salt + 999) % nsec) + 1;
         a[t] = w0 + w1 + w2 + w3;
     }
@@ -99,14 +101,16 @@ int main(int argc, char** argv) {
             printf("%s{\"op\": \"read\", \"flavor\": \"%s\", \"unroll\": %d, \"bytes\": %d, \"l2_fetch_gran\": %zu, \"ms\": %.4f, \"useful_gbs\": %.1f, \"maccess_s\": %.1f}\n", first ? "" : ",", NAME, U, B, cur, ms, n * (double)B / ms / 1e6, n / ms / 1e3); first = false; }
         RUN(0, 1, 32, "default") RUN(0, 4, 32, "default") RUN(1, 4, 32, "nc") RUN(2, 1, 32, "cg") RUN(2, 4, 32, "cg")
         RUN(2, 8, 32, "cg") RUN(3, 4, 32, "cs") RUN(2, 4, 64, "cg") RUN(2, 2, 128, "cg") RUN(0, 4, 64, "default")
-        for (int mode = 0; mode < 3; ++mode) {
+        for (int mode = 0; mode < 4; ++mode) {
             const uint64_t nsec = bytes / 32;
             float ms = timeit([&] {
                 if (mode == 0) k_read_write<0><<<sms * 8, 256>>>(a, nsec, n, 4242);
                 else if (mode == 1) k_read_write<1><<<sms * 8, 256>>>(a, nsec, n, 4242);
-                else k_read_write<2><<<sms * 8, 256>>>(a, nsec, n, 4242);
+                else if (mode == 2) k_read_write<2><<<sms * 8, 256>>>(a, nsec, n, 4242);
+                else k_read_write<3><<<sms * 8, 256>>>(a, nsec, n, 4242);
             }, 5);
-            const char* nm[3] = {"read32+write8_same_sector", "read32+write8_pair_sector", "read32+write8_random_sector"};
+            const char* nm[4] = {"read32+write8_same_sector", "read32+write8_pair_sector", "read32+write8_random_sector",
+                                 "read32+write8_same_line_other_half"};
             printf(",{\"op\": \"%s\", \"l2_fetch_gran\": %zu, \"ms\": %.4f, \"maccess_s\": %.1f}\n", nm[mode], cur, ms, n / ms / 1e3);
         }
         {
