@@ -49,9 +49,9 @@ __global__ void __launch_bounds__(256) k_draw_all(TableDev t) {
     }
 }
 
-// one row's reset by a warp: draw_row, momentum 0, trained 0 (embedding_store.cpp:62-68)
-__device__ __forceinline__ void reset_row_warp(const TableDev& t, uint64_t row, unsigned lane) {
-    const uint64_t s0 = mix64(row, t.init_seed);
+// one row's reset by a warp: draw_row from the row's SplitMix64 seed s0 = mix64(row, init_seed),
+// momentum 0 (embedding_store.cpp:62-68); the trained bit is the caller's
+__device__ __forceinline__ void reset_row_body(const TableDev& t, uint64_t row, uint64_t s0, unsigned lane) {
     float* w = t.weights + row * t.dim;
     float* m = t.momentum + row * t.dim;
     if ((t.dim & 3u) == 0) {
@@ -68,6 +68,10 @@ __device__ __forceinline__ void reset_row_warp(const TableDev& t, uint64_t row, 
             m[j] = 0.f;
         }
     }
+}
+
+__device__ __forceinline__ void reset_row_warp(const TableDev& t, uint64_t row, unsigned lane) {
+    reset_row_body(t, row, mix64(row, t.init_seed), lane);
     if (lane == 0) clear_trained(t, row);
 }
 
@@ -82,9 +86,16 @@ __global__ void __launch_bounds__(256) k_reset_rows(TableDev t, const uint64_t* 
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t r0 = warp * 32; r0 < n; r0 += nwarps * 32) {
-        const uint64_t mine = r0 + lane < n ? rows[r0 + lane] : 0;
+        const bool have = r0 + lane < n;
+        const uint64_t mine = have ? rows[r0 + lane] : 0;
+        // each lane derives its own row's seed and clears its own row's trained bit, so the
+        // per-row work left is the draw and the stores (the kernel is issue-bound: ncu 69% of
+        // issue slots busy with the seed recomputed by every lane for every row)
+        const uint64_t s0m = mix64(mine, t.init_seed);
+        if (have) clear_trained(t, mine);
         const unsigned cnt = n - r0 < 32 ? (unsigned)(n - r0) : 32u;
-        for (unsigned k = 0; k < cnt; ++k) reset_row_warp(t, __shfl_sync(0xffffffffu, mine, k), lane);
+        for (unsigned k = 0; k < cnt; ++k)
+            reset_row_body(t, __shfl_sync(0xffffffffu, mine, k), __shfl_sync(0xffffffffu, s0m, k), lane);
     }
 }
 

@@ -67,6 +67,26 @@ __global__ void __launch_bounds__(256) k_write8(uint64_t* a, uint64_t nslots, ui
         a[mix(i + salt) % nslots] = i;
 }
 
+// the row reset's store pattern: a warp writes one random 512-byte row of each of two arrays
+// (weights, momentum) per step; HINT 1 uses streaming (.cs) stores, HINT 2 sequential rows
+template <int HINT>
+__global__ void __launch_bounds__(256) k_write_rows(float4* a, float4* b, uint64_t nrows, uint64_t n, uint64_t salt) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = warp; i < n; i += nw) {
+        const uint64_t r = HINT == 2 ? i % nrows : mix(i + salt) % nrows;
+        const float4 v = make_float4((float)i, 1.f, 2.f, 3.f), z = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (HINT == 1) {
+            __stcs(a + r * 32 + lane, v);
+            __stcs(b + r * 32 + lane, z);
+        } else {
+            a[r * 32 + lane] = v;
+            b[r * 32 + lane] = z;
+        }
+    }
+}
+
 template <class F>
 float timeit(F f, int reps) {
     cudaEvent_t e0, e1;
@@ -116,6 +136,20 @@ int main(int argc, char** argv) {
         {
             float ms = timeit([&] { k_write8<<<sms * 8, 256>>>(a, bytes / 8, n, 777); }, 5);
             printf(",{\"op\": \"write8\", \"l2_fetch_gran\": %zu, \"ms\": %.4f, \"useful_gbs\": %.1f, \"maccess_s\": %.1f}\n", cur, ms, n * 8.0 / ms / 1e6, n / ms / 1e3);
+        }
+    }
+    {   // two 8 GiB arrays of 512-byte rows, 1 M rows written per launch (1 GiB)
+        float4* a4 = reinterpret_cast<float4*>(a);
+        float4* b4 = reinterpret_cast<float4*>(reinterpret_cast<char*>(a) + (8ull << 30));
+        const uint64_t nrows = (8ull << 30) / 512, nw = 1ull << 20;
+        const char* nm[3] = {"write_rows512_x2_random", "write_rows512_x2_random_cs", "write_rows512_x2_sequential"};
+        for (int h = 0; h < 3; ++h) {
+            float ms = timeit([&] {
+                if (h == 0) k_write_rows<0><<<sms * 8, 256>>>(a4, b4, nrows, nw, 99);
+                else if (h == 1) k_write_rows<1><<<sms * 8, 256>>>(a4, b4, nrows, nw, 99);
+                else k_write_rows<2><<<sms * 8, 256>>>(a4, b4, nrows, nw, 99);
+            }, 5);
+            printf(",{\"op\": \"%s\", \"ms\": %.4f, \"gbs\": %.1f}\n", nm[h], ms, nw * 1024.0 / ms / 1e6);
         }
     }
     printf("]}\n");
