@@ -147,6 +147,17 @@ def c1(shards):
                 reference=ref)
 
 
+def zipf_cdf(universe, s=1.05):
+    """The Zipf(s) CDF over `universe` ranks, computed on the host (sequential float64 sums) and
+    moved to the GPU: a CUDA cumsum / sum of 2^27 doubles is not bitwise reproducible from run
+    to run, which made the sampled streams (and their outcome counts) differ in a few positions
+    between processes."""
+    w = np.arange(1, universe + 1, dtype=np.float64) ** -s
+    c = np.cumsum(w)
+    c /= c[-1]
+    return torch.from_numpy(c).cuda()
+
+
 def zipf_ranks(n, s, universe, seed):
     # inverse CDF on a precomputed table (SURVEY 8d C2), SplitMix64(3).next_unit()
     g = torch.Generator(device="cuda").manual_seed(seed)
@@ -157,9 +168,7 @@ def zipf_ranks(n, s, universe, seed):
 def c2():
     rows = 1 << 26
     universe = 1 << 27
-    w = torch.arange(1, universe + 1, dtype=torch.float64, device="cuda").pow_(-1.05)
-    zipf_ranks.cdf = torch.cumsum(w, 0) / w.sum()
-    del w
+    zipf_ranks.cdf = zipf_cdf(universe)
     B = 1 << 20
     # expected distinct ids of Zipf(1.05) over 2^27 reach 0.8 * 2^26 after ~700M draws, i.e.
     # ~700 batches at 60 s spacing: TTL 42,000 s targets a live occupancy near 0.8
@@ -191,9 +200,7 @@ def c2f():
     TTL: metadata values differ per feature, so batches take the A.4 rounds path)."""
     rows = 1 << 26
     universe = 1 << 27
-    w = torch.arange(1, universe + 1, dtype=torch.float64, device="cuda").pow_(-1.05)
-    zipf_ranks.cdf = torch.cumsum(w, 0) / w.sum()
-    del w
+    zipf_ranks.cdf = zipf_cdf(universe)
     B = 1 << 20
     pol = mz.EvictionPolicy.ttl(mz.TtlPolicy(42000, {1: 21000, 2: 84000}))
     st = torch.cuda.current_stream()
@@ -327,9 +334,7 @@ def lru_zipf():
     are cold tail ids, which the claim path places (K3b).  Beside it the same stream forced onto
     the rounds path."""
     rows, universe, B = 1 << 22, 1 << 27, 1 << 20
-    w = torch.arange(1, universe + 1, dtype=torch.float64, device="cuda").pow_(-1.05)
-    zipf_ranks.cdf = torch.cumsum(w, 0) / w.sum()
-    del w
+    zipf_ranks.cdf = zipf_cdf(universe)
     st = torch.cuda.current_stream()
     caps = mz.even_capacities(rows, 8)
     pol = mz.EvictionPolicy.lru()

@@ -13,7 +13,7 @@ import bench  # noqa: E402
 import paper_2602_17050_b200 as mz  # noqa: E402
 import pyoracle  # noqa: E402
 sys.path.insert(0, os.path.dirname(__file__))
-from bench_configs import zipf_ranks  # noqa: E402
+from bench_configs import zipf_cdf, zipf_ranks  # noqa: E402
 
 
 def main():
@@ -21,9 +21,7 @@ def main():
     nb = int(sys.argv[2]) if len(sys.argv) > 2 else 24
     path = sys.argv[3] if len(sys.argv) > 3 else "auto"
     universe, B = 1 << 27, 1 << 20
-    w = torch.arange(1, universe + 1, dtype=torch.float64, device="cuda").pow_(-1.05)
-    zipf_ranks.cdf = torch.cumsum(w, 0) / w.sum()
-    del w
+    zipf_ranks.cdf = zipf_cdf(universe)
     caps = mz.even_capacities(rows, 8)
     t = mz.MpzchTable(mz.TableConfig(caps, 128, 7))
     t.set_path(path)

@@ -11,14 +11,12 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import bench  # noqa: E402
 import paper_2602_17050_b200 as mz  # noqa: E402
-from bench_configs import zipf_ranks  # noqa: E402
+from bench_configs import zipf_cdf, zipf_ranks  # noqa: E402
 
 warm = int(sys.argv[1]) if len(sys.argv) > 1 else 12
 timed = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 rows, universe, B = 1 << 22, 1 << 27, 1 << 20
-w = torch.arange(1, universe + 1, dtype=torch.float64, device="cuda").pow_(-1.05)
-zipf_ranks.cdf = torch.cumsum(w, 0) / w.sum()
-del w
+zipf_ranks.cdf = zipf_cdf(universe)
 t = mz.MpzchTable(mz.TableConfig(mz.even_capacities(rows, 8), 128, 7))
 t.set_path("rounds")
 pol = mz.EvictionPolicy.lru()

@@ -20,12 +20,11 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import bench  # noqa: E402
 import paper_2602_17050_b200 as mz  # noqa: E402
 import pyoracle  # noqa: E402
-from bench_configs import zipf_ranks  # noqa: E402
+from bench_configs import zipf_cdf, zipf_ranks  # noqa: E402
 
 
 def zipf_setup(universe):
-    w = torch.arange(1, universe + 1, dtype=torch.float64, device="cuda").pow_(-1.05)
-    zipf_ranks.cdf = torch.cumsum(w, 0) / w.sum()
+    zipf_ranks.cdf = zipf_cdf(universe)
 
 
 def replay(name, caps, P, dim, init_seed, mode, ttl, pf, batches, feats=None):
