@@ -98,7 +98,8 @@ struct RoundsArgs {
     uint64_t* td_slot;
     uint8_t* td_oc;
     uint32_t* td_d;
-    uint8_t* susp;  // 0 clear, 1 suspect
+    uint64_t* pc;   // per pending entry x (same thread every pass): k | mark_win word << 32 |
+                    // wide << 62 | suspect << 63, written by the round's first closure pass
     uint8_t* todo;
     unsigned long long* mark_any;  // metadata-only writes
     unsigned long long* mark_id;   // ident-changing writes
@@ -187,14 +188,18 @@ __device__ __forceinline__ void tentative(const RoundsArgs& r, uint32_t k, uint3
 // R2 (rule in the header).  The read range's mark words are read 16 at a time (four
 // 32-byte loads of one 128-byte block of the mark array per round trip).
 template <int MODE>
-__device__ __forceinline__ bool suspect(const RoundsArgs& r, uint32_t k, uint32_t epoch) {
+__device__ __forceinline__ bool suspect(const RoundsArgs& r, uint32_t k, uint32_t epoch, uint32_t& win,
+                                        bool& wide) {
     const uint32_t dw = __ldcg(r.td_d + k);
     const uint64_t w = __ldcg(r.td_slot + k);
-    if (!(dw >> 31)) {  // the write slot decides (header): one word in each mark array
+    wide = dw >> 31;
+    if (!wide) {  // the write slot decides (header): one word in each mark array
         const uint64_t i = r.mi(w);
+        win = (uint32_t)(i >> 4);
         return mark_rank(__ldcg(r.mark_id + i), epoch) < k || mark_rank(__ldcg(r.mark_any + i), epoch) < k ||
                mark_rank(__ldcg(r.mark_win + (i >> 4)), epoch) < k;
     }
+    win = 0;
     const uint64_t id = r.ids[r.upos[k]];
     const ShardDev sd = r.t.shards[r.ushard[k]];
     const uint64_t h = home_of(id, sd, r.t.seed);
@@ -291,7 +296,6 @@ __global__ void __launch_bounds__(256) k_rounds(RoundsArgs r) {
     const unsigned u = ctr->entry_count;
     for (unsigned x = tid; x < u; x += nth) {
         __stcg(r.pend[0] + x, x);
-        stcg_u8(r.susp + x, 0);
         r.todo[x] = 0;
     }
     if (tid == 0) {
@@ -321,9 +325,32 @@ __global__ void __launch_bounds__(256) k_rounds(RoundsArgs r) {
             // after this pass's barrier would race with pass c + 1's first updates)
             if (tid == 0 && c > 0) ctr->r_newc[(c + 1) % 3] = 0;
             for (unsigned x = tid; x < npend; x += nth) {
-                const uint32_t k = __ldcg(pend + x);
-                if (ldcg_u8(r.susp + k) || !suspect<MODE>(r, k, epoch)) continue;
-                stcg_u8(r.susp + k, 1);
+                uint32_t k;
+                if (c == 0) {  // the full check (R2), its outcome and mark word cached for later passes
+                    k = __ldcg(pend + x);
+                    uint32_t win;
+                    bool wide;
+                    const bool s = suspect<MODE>(r, k, epoch, win, wide);
+                    __stcg(r.pc + x, (uint64_t)k | ((uint64_t)win << 32) | ((uint64_t)wide << 62) |
+                                         ((uint64_t)s << 63));
+                    if (!s) continue;
+                } else {
+                    // later passes: only suspects' window marks were added since the first pass,
+                    // so a non-wide unique re-reads the one window word over its write slot
+                    const uint64_t cw = __ldcg(r.pc + x);
+                    if (cw >> 63) continue;
+                    k = (uint32_t)cw;
+                    bool s;
+                    if ((cw >> 62) & 1) {
+                        uint32_t win;
+                        bool wide;
+                        s = suspect<MODE>(r, k, epoch, win, wide);
+                    } else {
+                        s = mark_rank(__ldcg(r.mark_win + ((cw >> 32) & 0x3fffffffu)), epoch) < k;
+                    }
+                    if (!s) continue;
+                    __stcg(r.pc + x, cw | (1ull << 63));
+                }
                 if (last) {
                     atomicMin(&ctr->r_minrank, k);
                 } else {
@@ -344,9 +371,9 @@ __global__ void __launch_bounds__(256) k_rounds(RoundsArgs r) {
         const uint32_t bound = ldcg_u32(&ctr->r_minrank);
         uint32_t* next = r.pend[par ^ 1];
         for (unsigned x = tid; x < npend; x += nth) {
-            const uint32_t k = __ldcg(pend + x);
-            if (ldcg_u8(r.susp + k) || k > bound) {
-                stcg_u8(r.susp + k, 0);
+            const uint64_t cw = __ldcg(r.pc + x);
+            const uint32_t k = (uint32_t)cw;
+            if ((cw >> 63) || k > bound) {
                 // warp-aggregated append to the next round's pending list (its order is free)
                 const unsigned am = __activemask();
                 const unsigned leader = __ffs(am) - 1;
@@ -413,7 +440,7 @@ void ensure_rounds_scratch(Table& t, uint64_t n, cudaStream_t st) {
     t.r_slot.reserve(n * 8);
     t.r_oc.reserve(n);
     t.r_d.reserve(n * 4);
-    t.r_susp.reserve(n);
+    t.r_susp.reserve(n * 8);
     t.o_todo.reserve(n);
 }
 
@@ -439,7 +466,7 @@ void enqueue_rounds(Table& t, const BatchArgs& a, cudaStream_t st, uint8_t* todo
     r.td_slot = t.r_slot.as<uint64_t>();
     r.td_oc = t.r_oc.as<uint8_t>();
     r.td_d = t.r_d.as<uint32_t>();
-    r.susp = t.r_susp.as<uint8_t>();
+    r.pc = t.r_susp.as<uint64_t>();
     r.todo = todo;
     r.mark_any = t.r_mark_any.as<unsigned long long>();
     r.mark_id = t.r_mark_id.as<unsigned long long>();
