@@ -1099,8 +1099,7 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
                 if (lane_id() == leader) r0 = atomicAdd(&ctr->reset_count, (unsigned)__popc(em));
                 r0 = __shfl_sync(em, r0, leader);
                 reset_rows[r0 + __popc(em & ((1u << lane_id()) - 1))] = g;
-                evflag[rank] = 1;
-                evslot[rank] = g;
+                evflag[rank] = 1;  // (the compaction reads the slot from out_slots[rank])
             }
         }
         if (dups) {  // K5 reads the entry's result for the later positions of its id
@@ -1595,7 +1594,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     }
     // (row-sharded owner: the return scatter reads and clears the evicted flags)
     if ((ttl || lru) && !a.sh_state)
-        enqueue_compact_evicted(t, n, a.out_ev, a.ev_cap, st, lru ? &t.d_ctr->lru_evict : nullptr);
+        enqueue_compact_evicted(t, n, a.out_ev, a.ev_cap, st, lru ? &t.d_ctr->lru_evict : nullptr, a.out_slots);
     if (t.profiling) cudaEventRecord(t.ev[3], st);
 }
 

@@ -675,8 +675,8 @@ void preload_all_kernels() {
 }
 
 void enqueue_compact_evicted(Table& t, uint64_t n, uint64_t* out_ev, uint64_t ev_cap, cudaStream_t st,
-                             const unsigned* gate) {
-    EmitEvicted em{t.s_evslot.as<uint64_t>(), out_ev, ev_cap};
+                             const unsigned* gate, const uint64_t* slots) {
+    EmitEvicted em{slots ? slots : t.s_evslot.as<uint64_t>(), out_ev, ev_cap};
     compact_flags(t.s_evflag.as<uint8_t>(), n, t.s_blk.as<unsigned>(), &t.d_ctr->evicted_count, true,
                   em, st, t.launches, gate);
 }

@@ -312,9 +312,11 @@ void enqueue_ordered_batch(Table& t, const BatchArgs& a, cudaStream_t st, bool r
 void adopt_gated_counters(Table& t, BatchCounters* attempt, const BatchCounters* alt, cudaStream_t st);
 void enqueue_rounds(Table& t, const BatchArgs& a, cudaStream_t st, uint8_t* todo);
 void ensure_rounds_scratch(Table& t, uint64_t n, cudaStream_t st);
-// gate (nullable): device word, 0 = no evicted flag can be set (LRU batches without evictors)
+// gate (nullable): device word, 0 = no evicted flag can be set (LRU batches without evictors);
+// slots (nullable): the slot of flagged index i (the fast path: the batch's out_slots, flags by
+// position), else the rounds / ordered paths' per-unique s_evslot
 void enqueue_compact_evicted(Table& t, uint64_t n, uint64_t* out_ev, uint64_t ev_cap, cudaStream_t st,
-                             const unsigned* gate = nullptr);
+                             const unsigned* gate = nullptr, const uint64_t* slots = nullptr);
 void run_route(Table& t, const uint64_t* ids, uint64_t n, const uint32_t* shard_to_part,
                uint32_t parts, uint32_t* perm, uint64_t* counts, cudaStream_t st);
 void run_validate(Table& t, const uint64_t* ids, uint64_t n, cudaStream_t st);
