@@ -747,13 +747,13 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
                                                const uint64_t* __restrict__ newid,
                                                const uint32_t* __restrict__ newa,
                                                const uint32_t* __restrict__ newm,
-                                               uint32_t* __restrict__ newent, u128* hk, IdEntry* te) {
+                                               uint32_t* __restrict__ newent, u128* hk, IdEntry* te,
+                                               uint32_t* __restrict__ dupl) {
     pdl_wait();
     if (batch_failed(&ctr->err)) return;
     const unsigned cnt = ctr->new_count;
     const uint64_t mask = table_mask(cnt, tcap);
     const uint32_t ep32 = (uint32_t)epoch;
-    unsigned dups = 0;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
         const uint64_t id = newid[k];
         const u128 mine = make_key(ep32, k, id);
@@ -780,7 +780,6 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
             }
             if (key_id(cur) == id) {
                 e = key_entry(cur);
-                ++dups;
                 break;
             }
             h = (h + 1) & mask;
@@ -798,9 +797,16 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
             atomicMax(&te[e].rank, myrank);
         }
         newent[k] = e;
+        if (!inserted) {  // a repeat item (not the inserter): listed for K5, one counter update
+                          // per group of converged repeat lanes
+            const unsigned am = __activemask();
+            const unsigned lane = lane_id(), leader = __ffs(am) - 1;
+            unsigned b0 = 0;
+            if (lane == leader) b0 = atomicAdd(&ctr->dup_items, (unsigned)__popc(am));
+            b0 = __shfl_sync(am, b0, leader);
+            dupl[b0 + __popc(am & ((1u << lane) - 1))] = k;
+        }
     }
-    for (int o = 16; o; o >>= 1) dups += __shfl_xor_sync(0xffffffffu, dups, o);
-    if (lane_id() == 0 && dups) atomicAdd(&ctr->dup_items, dups);
 }
 
 // The entry's bookkeeping words in two 16-byte loads: (rank, a | m << 32) and
@@ -1356,23 +1362,28 @@ __global__ void __launch_bounds__(256) k_lru_meta(TableDev t, const BatchCounter
 // K5: results of the non-primary items -- later positions of a repeated new id: the
 // primary's slot and outcome, or, for an (id, f') secondary (same id, other feature, later
 // first position), Found on the primary's slot / Collision if the primary collided.  Primary
-// items got their result in K4; without repeated ids (dup_items == 0) this is a no-op.
+// items got their result in K4.  Only the repeat items K2 listed are visited: a repeat that is
+// not its entry's primary writes its own position; a repeat that IS the primary (an earlier
+// position than the inserting item) writes the inserter's position instead, which is then the
+// entry's one non-primary item not on the list.
 __global__ void __launch_bounds__(256) k_finalize(BatchCounters* ctr,
                                                   const uint32_t* __restrict__ feats,
                                                   const uint32_t* __restrict__ newpos,
                                                   const uint32_t* __restrict__ newent,
+                                                  const uint32_t* __restrict__ dupl,
                                                   const IdEntry* te,
                                                   uint64_t* __restrict__ out_slots,
                                                   uint8_t* __restrict__ out_oc) {
     pdl_wait();
     if (batch_failed(&ctr->err) || ctr->dup_items == 0 || ctr->lru_abort) return;
-    const unsigned cnt = ctr->new_count;
+    const unsigned cnt = ctr->dup_items;
     unsigned long long c[4] = {0, 0, 0, 0};
-    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x) {
-        const uint32_t pos = newpos[k];
+    for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < cnt; q += gridDim.x * blockDim.x) {
+        const uint32_t k = dupl[q];
         const uint32_t e = newent[k];
         const uint32_t first = rank_of(te[e].rank);
-        if (first == pos) continue;  // primary: done in K4
+        uint32_t pos = newpos[k];
+        if (first == pos) pos = newpos[e];  // k is the primary: the inserter's position is the later one
         uint8_t oc = te[e].oc;
         if (feats && feats[pos] != feats[first]) oc = oc == kCollision ? kCollision : kFound;
         out_slots[pos] = te[e].slot;
@@ -1522,7 +1533,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
     if (t.profiling) cudaEventRecord(t.ev[1], st);
     IdEntry* te = t.s_tent.as<IdEntry>();
     launch_pdl(k_dedup, gW, B, st, t.d_ctr, t.tcap, epoch, (const uint32_t*)newpos, (const uint64_t*)newid,
-               (const uint32_t*)newa, (const uint32_t*)newm, newent, t.s_hkey.as<u128>(), te);
+               (const uint32_t*)newa, (const uint32_t*)newm, newent, t.s_hkey.as<u128>(), te, t.s_dupl.as<uint32_t>());
     if (t.profiling) cudaEventRecord(t.ev[4], st);
 #define MPZCH_CLAIM_COMMIT(MODE)                                                                   \
     launch_pdl(k_claim<MODE>, gW, B, st, t.dev, a.now, t.d_ctr, newpos, newent, te, nullptr);     \
@@ -1561,7 +1572,8 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
 #undef MPZCH_CLAIM_COMMIT
     t.launches += 3;
     if (t.profiling) cudaEventRecord(t.ev[2], st);
-    launch_pdl(k_finalize, gW, B, st, t.d_ctr, a.feats, newpos, newent, te, a.out_slots, a.out_oc);
+    launch_pdl(k_finalize, gW, B, st, t.d_ctr, a.feats, (const uint32_t*)newpos, (const uint32_t*)newent,
+               (const uint32_t*)t.s_dupl.as<uint32_t>(), (const IdEntry*)te, a.out_slots, a.out_oc);
     if (t.profiling) cudaEventRecord(t.ev[6], st);
     ++t.launches;
     if (lru) {

@@ -204,6 +204,7 @@ void Table::ensure_fast_scratch(uint64_t n) {
     s_newa.reserve(n * 4);
     s_newm.reserve(n * 4);
     s_newent.reserve(n * 4);
+    s_dupl.reserve(n * 4);
     s_defer.reserve(n * 12);
     const uint64_t want = pow2_at_least(2 * n);
     if (want > tcap) {

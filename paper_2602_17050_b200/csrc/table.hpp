@@ -170,6 +170,7 @@ public:
 
     // scratch
     DevBuf s_newpos, s_newid, s_newa, s_newm, s_newent;  // new-list (fast path)
+    DevBuf s_dupl;                                   // new-list items whose id an earlier item inserted
     DevBuf s_defer;  // TTL probe: (position, offset, first expired) of walks handed to the resume pass
     // synchronous lookups (mpzch_lookup[_device], lookup_gather): their own hand-over list and
     // a lock, so concurrent const lookups on one handle never share scratch or the error word
