@@ -89,6 +89,10 @@ struct TableDev {
                          // the reference does, then scaled by a power of two: see draw_at)
     uint32_t P;          // max_probe
     uint32_t dim;
+    uint8_t* tag;        // max_probe >= kTagMinProbe: one byte per global row, 0 for EMPTY, else
+                         // tag_of(identity) -- a 1/128-size image of the identity array that the
+                         // long-window probe scans (128 slots per 128-byte line) instead of the
+                         // identities (16 slots per line); null for shorter windows
     uint32_t* pend_bits; // MPZCH_RESET_DEFERRED: one bit per held row (row - row_lo), set while
                          // the row's reset (draw_row, momentum 0, trained 0) is not yet written;
                          // null in eager mode.  1 bit per row keeps the map L2-resident (16 MiB
@@ -168,6 +172,22 @@ __device__ __forceinline__ bool holds_shard(const TableDev& t, uint32_t s) {
 
 __device__ __forceinline__ uint64_t home_of(uint64_t id, const ShardDev& s, uint64_t seed) {
     return fastmod(mix64(id ^ kHomeSalt, seed), s.cap);
+}
+
+// Identity tags (TableDev::tag): kept for tables whose windows run long (C3: P = 256 at 0.95
+// load, where an absent id walks ~13 identity lines to its first EMPTY but ~2 tag lines).
+constexpr uint32_t kTagMinProbe = 256;
+constexpr uint64_t kTagSalt = 0x6A09E667F3BCC909ull;
+
+__host__ __device__ __forceinline__ uint8_t tag_of(uint64_t id) {
+    const uint8_t x = (uint8_t)(mix64(id ^ kTagSalt, 0) >> 56);
+    return x ? x : 1;  // 0 marks an EMPTY slot
+}
+
+// every identity store goes through here (or pairs its store with this), so the tags of a
+// table that keeps them always describe its identity array
+__device__ __forceinline__ void store_tag(const TableDev& t, uint64_t g, uint64_t id) {
+    if (t.tag) t.tag[g] = id == kEmpty ? 0 : tag_of(id);
 }
 
 // Error word shared by all kernels of one batch.  Mutating kernels return

@@ -14,7 +14,8 @@
 //                 mutates a batch that failed here.
 //   K1 probe      one thread per POSITION, 32-byte sector loads from the home slot up to
 //                 the first match or EMPTY (hole-free early exit); long
-//                 windows and small batches: one quad per position, 128-byte lines.  TTL:
+//                 windows and small batches: one quad per position, 128-byte lines (long
+//                 Disabled windows past their first line: 128-slot tag lines).  TTL:
 //                 walks still pending after 8 sector rounds resume in a quad-line launch.
 //                 Hits on live slots and full windows are final here and write their
 //                 metadata word; everything else goes to the new list.
@@ -738,6 +739,241 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line_la(TableDev t, const u
     }
 }
 
+// K1 (long windows, Disabled, tables that keep identity tags): the first identity line of the
+// window as in k_probe_line_la -- most hits end there -- then the rest of the window 128 slots
+// per round from the TAG lines (common.cuh: one byte per slot, 0 = EMPTY): lane j of the quad
+// loads tag bytes [32j, 32j + 32) of the line, and the quad finds the first EMPTY of the window
+// part and the slots before it whose tag equals the id's.  Only those candidates are read from
+// the identity array (1/255 of the occupied slots), in order, until one holds the id.  At 0.95
+// load an absent id's walk to its first EMPTY (~200 slots) costs one identity line and two tag
+// lines instead of ~13 identity lines.  Decisions are k_probe_line_la's: the walk stops at the
+// same slot (the first holding the id, or the first EMPTY, in window order).
+// C3 insert-heavy (ncu): DRAM sectors read 88.6 M -> 38.2 M per batch, probe 0.90 -> 0.73 ms; what
+// remains is issue-bound (62% issue-active, half of it the tag byte masks).  Swept: loading 1 or
+// 2 tag lines with the identity line (0.76 / 0.71 ms, 48 / 64 registers), 6 or 8 blocks/SM (0.72 /
+// 0.80 ms): none clearly better than this plain variant at 5 blocks/SM.
+// 0x80 in every zero byte of x, 0 elsewhere (exact: no borrow between bytes)
+__device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {
+    const uint32_t t = (x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+    return ~(t | x | 0x7F7F7F7Fu);
+}
+// 0x80-per-byte flags -> 4 bits (byte k -> bit k): the multiply moves bit 8k+7 to bit 28+k, and
+// its partial products land on distinct bits, so nothing carries
+__device__ __forceinline__ uint32_t msb_bits4(uint32_t y) { return (y * 0x00204081u) >> 28; }
+
+__device__ __forceinline__ unsigned quad_min(unsigned x, unsigned qm) {
+    x = min(x, __shfl_xor_sync(qm, x, 1));
+    return min(x, __shfl_xor_sync(qm, x, 2));
+}
+
+// bits [a, b) of a 32-bit word (0 <= a, b <= 32)
+__device__ __forceinline__ unsigned bit_range(int a, int b) {
+    if (b <= a) return 0u;
+    const unsigned w = (unsigned)(b - a);
+    return (w >= 32 ? 0xffffffffu : ((1u << w) - 1u)) << a;
+}
+
+// One window segment of tag line `tl`: slots [s, s + c) of the line.  Returns the line slot
+// of the first one holding the id (its candidates -- tag matches before the segment's first
+// EMPTY -- verified against the identity array in slot order) or 128, and in `fe` the
+// segment's first EMPTY (or 128).  Quad-uniform arguments; lane j holds tag bytes [32j, +32).
+__device__ __forceinline__ unsigned tag_segment(const TableDev& t, const uint64_t (&v)[4], uint32_t pat, uint64_t id,
+                                                uint64_t tl, int s, int c, int jb, unsigned j, unsigned qm,
+                                                unsigned& fe, unsigned long long& isec) {
+    unsigned mm = 0, ee = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t x = (uint32_t)(v[k >> 1] >> (32 * (k & 1)));
+        mm |= msb_bits4(zero_bytes(x ^ pat)) << (4 * k);
+        ee |= msb_bits4(zero_bytes(x)) << (4 * k);
+    }
+    const unsigned r = bit_range(max(s, jb) - jb, min(s + c, jb + 32) - jb);
+    mm &= r;
+    ee &= r;
+    fe = quad_min(ee ? (unsigned)jb + __ffs(ee) - 1 : 128u, qm);
+    mm &= bit_range(0, min(max((int)fe - jb, 0), 32));
+    for (;;) {  // every lane verifies its lowest candidate; the lowest verified match wins
+                // unless a lower lane still holds an unverified candidate (rare: ~0.5 per line)
+        const bool have = mm != 0;
+        const unsigned cq = have ? (unsigned)jb + __ffs(mm) - 1 : 128u;
+        const bool match = have && t.ident[tl + cq] == id;
+        isec += have;
+        const unsigned qmatch = quad_min(match ? cq : 128u, qm);
+        if (have && !match) mm &= mm - 1;
+        // lowest candidate still unverified after this step
+        const unsigned rest = quad_min(mm && !match ? (unsigned)jb + __ffs(mm) - 1 : 128u, qm);
+        if (qmatch < rest || rest == 128u) return qmatch;
+    }
+}
+
+// the window part inside g's tag line: [g, g + c), c bounded by the line, the shard end and the
+// remaining max_probe budget
+__device__ __forceinline__ uint32_t tag_seg_len(uint64_t g, uint64_t end, uint32_t off, uint32_t P) {
+    uint64_t c = 128 - (g & 127u);
+    if (end - g < c) c = end - g;
+    const uint32_t left = off < P ? P - off : 0u;
+    if (left < c) c = left;
+    return (uint32_t)c;
+}
+
+// PF: tag lines loaded in round 0 together with the identity line (the rest one round trip each)
+template <int MINB, int PF>
+__global__ void __launch_bounds__(256, MINB) k_probe_tag(TableDev t, const uint64_t* __restrict__ ids,
+                                                         uint64_t n, uint64_t now, uint64_t meta_value,
+                                                         BatchCounters* ctr,
+                                                         uint64_t* __restrict__ out_slots,
+                                                         uint8_t* __restrict__ out_oc,
+                                                         uint32_t* __restrict__ newpos,
+                                                         uint64_t* __restrict__ newid,
+                                                         uint32_t* __restrict__ newa,
+                                                         uint32_t* __restrict__ newm,
+                                                         const uint32_t* __restrict__ dlist = nullptr) {
+    pdl_wait();
+    if (batch_failed(&ctr->err)) return;
+    constexpr uint8_t kPending = 0, kHit = 1, kEmptyHit = 2, kExhausted = 3, kIdle = 4;
+    const unsigned lane = lane_id();
+    const unsigned j = quad_lane(), qm = quad_mask();
+    const int jb = 32 * (int)j;  // this lane's first slot of a tag line
+    const uint64_t qpb = blockDim.x >> 2;
+    const uint64_t qib = threadIdx.x >> 2;
+    unsigned long long my_found = 0, my_coll = 0, my_isec = 0, my_tsec = 0;
+    const uint64_t total = min(n, (uint64_t)ctr->n_live);
+    for (uint64_t t0 = (uint64_t)blockIdx.x * qpb; t0 < total; t0 += (uint64_t)gridDim.x * qpb) {
+        const uint64_t i = t0 + qib;
+        uint8_t st = kIdle;
+        uint64_t id = 0, g = 0, base = 0, end = 0, h = 0;
+        uint32_t off = 0;
+        if (i < total) {
+            id = ids[i];
+            const ShardDev sd = t.shards[shard_of(id, t)];
+            base = sd.offset;
+            end = base + sd.cap.d;
+            h = home_of(id, sd, t.seed);
+            g = base + h;
+            st = kPending;
+        }
+        const uint32_t pat = (uint32_t)tag_of(id) * 0x01010101u;
+        uint64_t vp[PF > 0 ? PF : 1][4];
+        if (st == kPending) {  // round 0: the home slot's identity line (+ PF tag lines after it)
+            const LineSpan sp = line_span(g, end, off, t.P);
+            uint64_t w[4];
+            ld_line_part(t.ident, g, j, w);
+            {
+                uint64_t gq = g + sp.c;
+                uint32_t oq = off + sp.c;
+                if (gq == end) gq = base;
+#pragma unroll
+                for (int p = 0; p < PF; ++p) {
+                    if (oq < t.P) {
+                        ld_sector(reinterpret_cast<const uint64_t*>(t.tag + (gq & ~127ull)) + 4 * j,
+                                  vp[p][0], vp[p][1], vp[p][2], vp[p][3]);
+                        ++my_tsec;
+                    }
+                    const uint32_t cq = tag_seg_len(gq, end, oq, t.P);
+                    oq += cq;
+                    gq += cq;
+                    if (gq == end) gq = base;
+                }
+            }
+            unsigned m = 0, e = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                m |= (unsigned)(w[k] == id) << k;
+                e |= (unsigned)(w[k] == kEmpty) << k;
+            }
+            const unsigned x = quad_gather(m, e, j, qm);
+            const unsigned hit = (x | (x >> 16)) & sp.range();
+            if (hit) {
+                const unsigned q = __ffs(hit) - 1;
+                st = (x >> q) & 1u ? kHit : kEmptyHit;
+                off += q - sp.s;
+                g += q - sp.s;
+                my_isec += sp.sectors_to(q);
+            } else {
+                my_isec += sp.sectors_to(sp.s + sp.c - 1);
+                off += sp.c;
+                g += sp.c;
+                if (g == end) g = base;
+                if (off >= t.P) st = kExhausted;
+            }
+        }
+        // the rest of the window on the tag lines, 128 slots per segment
+        int seg = 0;
+        while (st == kPending) {
+            const uint64_t tl = g & ~127ull;
+            const int s0 = (int)(g & 127u);
+            const int c0 = (int)tag_seg_len(g, end, off, t.P);
+            unsigned q, fe;
+            uint64_t v[4];
+            if (seg < PF) {  // (register selects: no dynamic index into vp)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) v[k] = seg == 0 ? vp[0][k] : vp[PF > 1 ? 1 : 0][k];
+            } else {
+                ld_sector(reinterpret_cast<const uint64_t*>(t.tag + tl) + 4 * j, v[0], v[1], v[2], v[3]);
+                ++my_tsec;
+            }
+            q = tag_segment(t, v, pat, id, tl, s0, c0, jb, j, qm, fe, my_isec);
+            ++seg;
+            if (q != 128u) {
+                st = kHit;
+                off += q - (unsigned)s0;
+                g = tl + q;
+            } else if (fe != 128u) {
+                st = kEmptyHit;
+                off += fe - (unsigned)s0;
+                g = tl + fe;
+            } else {
+                off += (uint32_t)c0;
+                g += (uint64_t)c0;
+                if (g == end) g = base;
+                if (off >= t.P) st = kExhausted;
+            }
+        }
+        bool is_new = false;
+        uint32_t a_off = 0;
+        if (st != kIdle && j == 0) {
+            uint64_t fslot = kEmpty;
+            uint8_t foc = kFound;
+            if (st == kHit) fslot = g;
+            else if (st == kEmptyHit) { is_new = true; a_off = off; }
+            else { fslot = base + h; foc = kCollision; }
+            if (fslot != kEmpty) {
+                out_slots[i] = fslot;
+                out_oc[i] = foc;
+                t.meta[fslot] = meta_value;
+                if (foc == kFound) ++my_found; else ++my_coll;
+            }
+        }
+        const unsigned mask = __ballot_sync(0xffffffffu, is_new);
+        if (mask) {
+            unsigned basek = 0;
+            if (lane == 0) basek = atomicAdd(&ctr->new_count, (unsigned)__popc(mask));
+            basek = __shfl_sync(0xffffffffu, basek, 0);
+            if (is_new) {
+                const unsigned k = basek + __popc(mask & ((1u << lane) - 1));
+                newpos[k] = (uint32_t)i;
+                newid[k] = id;
+                newa[k] = a_off;
+                newm[k] = kNone32;
+            }
+        }
+    }
+    // every lane of a quad counted the same identity sectors; each read its own tag sector
+    if (j != 0) my_isec = 0;
+    for (int o = 16; o; o >>= 1) {
+        my_found += __shfl_xor_sync(0xffffffffu, my_found, o);
+        my_coll += __shfl_xor_sync(0xffffffffu, my_coll, o);
+        my_isec += __shfl_xor_sync(0xffffffffu, my_isec, o);
+        my_tsec += __shfl_xor_sync(0xffffffffu, my_tsec, o);
+    }
+    if (lane == 0) {
+        if (my_found) atomicAdd(&ctr->found, my_found);
+        if (my_coll) atomicAdd(&ctr->collision, my_coll);
+        if (my_isec) atomicAdd(&ctr->id_sectors, my_isec);
+        if (my_tsec) atomicAdd(&ctr->meta_sectors, my_tsec);  // (Disabled reads no metadata)
+    }
+}
+
 // K2: distinct ids over the new positions: a 128-bit CAS inserts (id, epoch, e = this item's
 // new-list index) into the hash index; the inserter initialises te[e]; every item (inserter or
 // repeat) takes the id's first position into te[e].rank (atomicMax of epoch << 32 | ~position)
@@ -1090,7 +1326,10 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
             atomicExch(&ctr->err.too_many, 2u);  // internal invariant violated
             continue;
         }
-        if (oc != kCollision) t.ident[g] = id;
+        if (oc != kCollision) {
+            t.ident[g] = id;
+            store_tag(t, g, id);
+        }
         if (!PF) t.meta[g] = meta_value;  // per-feature TTL: the last-writer pass
         if (oc == kInserted || oc == kEvicted) t.row_gen[g] = gen_clock;
         {   // reset list: one warp-aggregated append (a per-row atomic on one counter word
@@ -1406,7 +1645,7 @@ void preload_remap_kernels() {
 #define PL(k) preload_kernel((const void*)(k))
     PL(k_init_counters); PL(k_sh_adopt); PL(k_validate);
     PL((k_probe_line<kModeTtl, 2, 3, true>)); PL((k_probe_line<kModeTtl, 2, 3>));
-    PL((k_probe_line<kModeLru, 2, 4>)); PL((k_probe_line<kModeDisabled, 1, 8>)); PL(k_probe_line_la<8>);
+    PL((k_probe_line<kModeLru, 2, 4>)); PL((k_probe_line<kModeDisabled, 1, 8>)); PL(k_probe_line_la<8>); PL((k_probe_tag<5, 0>));
     PL((k_probe_line<kModeDisabled, 2, 4>)); PL((k_probe_line<kModeTtl, 1, 4, true, true>));
     PL((k_probe_line<kModeTtl, 1, 4, false, true>));
     PL((k_probe<kModeTtl, 2, 3, true, false, true>)); PL((k_probe<kModeTtl, 2, 3, true>));
@@ -1478,6 +1717,10 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
         const char* e = std::getenv("MPZCH_LOOKAHEAD");
         return !(e && std::string(e) == "0");
     }();
+    static const bool tag_env = [] {  // the tag walk for long Disabled windows (MPZCH_TAGS=0: off)
+        const char* e = std::getenv("MPZCH_TAGS");
+        return !(e && std::string(e) == "0");
+    }();
 #define MPZCH_PROBE_ARGS t.dev, a.ids, n, a.now, a.uniform_meta, t.d_ctr, a.out_slots, a.out_oc, newpos, newid, newa, newm
     if (line) {
         constexpr int kUL = 2;
@@ -1488,6 +1731,8 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
         else if (lru) launch_pdl(k_probe_line<kModeLru, kUL, 4>, gl, B, st, MPZCH_PROBE_ARGS, nol);
         // long windows: one position per quad at 8 blocks/SM (C3 insert-heavy 1.88 -> 2.07 G/s);
         // small batches keep 2 per quad (C1 1.10 vs 1.04 G/s pipelined)
+        else if (t.P >= 256 && t.dev.tag && tag_env)
+            launch_pdl(k_probe_tag<5, 0>, grid_for(4 * n, B, 148u * 32u), B, st, MPZCH_PROBE_ARGS, nol);
         else if (t.P >= 256 && la_env)
             launch_pdl(k_probe_line_la<8>, grid_for(4 * n, B, 148u * 32u), B, st, MPZCH_PROBE_ARGS, nol);
         else if (t.P >= 256)

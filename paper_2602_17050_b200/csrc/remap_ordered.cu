@@ -189,7 +189,10 @@ __global__ void __launch_bounds__(256) k_ordered(TableDev t, BatchCounters* ctr,
             uint8_t oc;
             two_pass_probe<MODE>(t, base, cap, h, id, now, lane, gslot, oc);
             if (lane == 0) {
-                if (oc == kInserted || oc == kEvicted) t.ident[gslot] = id;
+                if (oc == kInserted || oc == kEvicted) {
+                    t.ident[gslot] = id;
+                    store_tag(t, gslot, id);
+                }
                 t.meta[gslot] = meta_in;  // Found refresh / insert / evict / Collision at home
                 if (oc == kInserted || oc == kEvicted) t.row_gen[gslot] = gen_clock;
                 if (oc == kEvicted) {
@@ -337,7 +340,10 @@ __global__ void __launch_bounds__(256) k_ordered_hf(TableDev t, BatchCounters* c
                 }
             }
             if (lane == 0) {
-                if (oc == kInserted || oc == kEvicted) t.ident[gslot] = id;
+                if (oc == kInserted || oc == kEvicted) {
+                    t.ident[gslot] = id;
+                    store_tag(t, gslot, id);
+                }
                 t.meta[gslot] = meta_in;
                 if (oc == kInserted || oc == kEvicted) t.row_gen[gslot] = gen_clock;
                 if (oc == kEvicted) {

@@ -261,6 +261,7 @@ __device__ __forceinline__ void commit(const RoundsArgs& r, uint32_t k) {
     const uint8_t oc = ldcg_u8(r.td_oc + k);
     if (oc == kInserted || oc == kEvicted) {
         __stcg(t.ident + g, r.ids[r.upos[k]]);
+        store_tag(t, g, r.ids[r.upos[k]]);
         t.row_gen[g] = r.gen_clock;
     }
     __stcg(t.meta + g, r.umeta[k]);

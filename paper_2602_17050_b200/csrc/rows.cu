@@ -145,6 +145,14 @@ __global__ void k_write_slots(TableDev t, const uint64_t* __restrict__ g, const 
     }
 }
 
+// the tags of written slots, from the identity array once every store above has landed (a slot
+// listed twice holds one of its writers' ids; the tag follows whichever it is)
+__global__ void k_retag_slots(TableDev t, const uint64_t* __restrict__ g, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        store_tag(t, g[i], t.ident[g[i]]);
+}
+
 // Hole check: every id stored inside its own probe window at
 // offset o must see neither EMPTY nor another copy of itself in [home, home+o).
 __global__ void __launch_bounds__(256) k_hole_check(TableDev t, unsigned* bad) {
@@ -267,6 +275,10 @@ void launch_write_slots(Table& t, const uint64_t* g, const uint64_t* ids, const 
     if (!n) return;
     k_write_slots<<<grid_for(n, 256), 256, 0, st>>>(t.dev, g, ids, metas, n);
     ++t.launches;
+    if (t.dev.tag) {
+        k_retag_slots<<<grid_for(n, 256), 256, 0, st>>>(t.dev, g, n);
+        ++t.launches;
+    }
 }
 
 bool run_hole_check(Table& t) {

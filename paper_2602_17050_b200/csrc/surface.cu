@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(32) k_shard_batch(TableDev t, uint32_t shard, 
         if (lane == 0) {
             if (oc == kInserted || oc == kEvicted) {
                 t.ident[gslot] = id;
+                store_tag(t, gslot, id);
                 t.row_gen[gslot] = gen_clock;  // touch_row, table.cpp:143-144
             }
             t.meta[gslot] = meta_in;

@@ -132,6 +132,14 @@ Table::Table(const uint64_t* cap_in, uint32_t num_shards, uint32_t max_probe, ui
     MPZCH_CUDA(cudaMemsetAsync(ident, 0xff, padded * sizeof(uint64_t), stream));
     MPZCH_CUDA(cudaMemsetAsync(meta, 0, padded * sizeof(uint64_t), stream));
     MPZCH_CUDA(cudaMemsetAsync(row_gen, 0, held * sizeof(uint64_t), stream));
+    // identity tags (common.cuh) for long windows: 128-row (one 128-byte tag line) aligned in
+    // global rows and padded by a line, so the probe's tag-line reads stay in bounds
+    const uint64_t tag_base = row_lo & ~127ull;
+    if (P >= kTagMinProbe) {
+        const uint64_t tag_rows = ((row_hi - tag_base + 127) & ~127ull) + 128;
+        MPZCH_CUDA(cudaMalloc((void**)&tags, tag_rows));
+        MPZCH_CUDA(cudaMemsetAsync(tags, 0, tag_rows, stream));
+    }
     if (dim > 0) {
         MPZCH_CUDA(cudaMalloc((void**)&weights, held * dim * sizeof(float)));
         MPZCH_CUDA(cudaMalloc((void**)&momentum, held * dim * sizeof(float)));
@@ -150,6 +158,7 @@ Table::Table(const uint64_t* cap_in, uint32_t num_shards, uint32_t max_probe, ui
     dev.momentum = momentum ? momentum - row_lo * dim : nullptr;
     dev.trained = trained;  // bit (row - row_lo)
     dev.row_gen = row_gen - row_lo;
+    dev.tag = tags ? tags - tag_base : nullptr;
     dev.row_lo = row_lo;
     dev.row_hi = row_hi;
     dev.shard_lo = shard_lo;
@@ -183,6 +192,7 @@ Table::~Table() {
     if (stream) cudaStreamSynchronize(stream);
     cudaFree(ident);
     cudaFree(meta);
+    cudaFree(tags);
     cudaFree(row_gen);
     cudaFree(weights);
     cudaFree(momentum);

@@ -157,6 +157,7 @@ public:
     // resident arrays
     uint64_t* ident = nullptr;
     uint64_t* meta = nullptr;
+    uint8_t* tags = nullptr;  // P >= kTagMinProbe: identity tags from tag_base (128-row aligned)
     float* weights = nullptr;
     float* momentum = nullptr;
     uint32_t* trained = nullptr;  // bitmap: one bit per held row

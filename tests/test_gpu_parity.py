@@ -827,3 +827,65 @@ def test_high_load_insert_heavy_long_windows(oracle, P):
         assert (oo == 3).sum() > 1000  # the windows are full for many new ids
     assert (t.identities_all() == o.identities_all()).all()
     assert (t.metadata_all() == o.metadata_all()).all()
+
+
+# ---------------------------------------------------------------- identity tags (P >= 256)
+# Tables with max_probe >= 256 keep one tag byte per slot; Disabled batches on the claim path
+# walk the window past its first identity line on the tags (k_probe_tag).  Every identity
+# writer keeps them: the claim path, the rounds and ordered paths (any policy), raw writes.
+
+@pytest.mark.parametrize("P", [256, 300])
+def test_tags_follow_every_writer(oracle, P):
+    """Batches cycling through every policy and path on one long-window table at high load
+    (TTL and LRU evictions rewrite identities; forced ordered / rounds paths write them their
+    own way), each followed by Disabled claim-path batches that walk the tags; results and
+    the full state against the oracle after every batch."""
+    caps = [3001, 4100, 2500]
+    rows = sum(caps)
+    t = mz.MpzchTable(mz.TableConfig(caps, P, 31))
+    o = oracle.OracleTable(caps, P, 31)
+    pool = oracle.distinct_ids(77, 0, int(rows * 1.3))
+    rng = np.random.default_rng(P)
+    plan = [(0, "auto"), (1, "auto"), (0, "auto"), (2, "auto"), (0, "auto"), (1, "ordered"),
+            (0, "auto"), (2, "rounds"), (0, "auto"), (0, "ordered"), (0, "auto"), (1, "rounds"),
+            (0, "auto"), (2, "ordered"), (0, "auto"), (0, "auto")]
+    now = 1
+    for b, (mode, path) in enumerate(plan):
+        t.set_path(path)
+        n = int(rng.choice([3000, 9000]))
+        ids = pool[rng.integers(0, pool.size, n)]
+        now += int(rng.integers(1, 6))
+        p = pol(mode, 7)
+        gs, go, ge = t.process_batch(ids, now, p)
+        os_, oo, oe = o.process_batch(ids, now, mode, 7)
+        assert (gs == os_).all(), f"slots differ: batch {b} ({mode}, {path}), {(gs != os_).sum()}"
+        assert (go == oo).all(), f"outcomes differ: batch {b} ({mode}, {path})"
+        assert (ge == oe).all(), f"evicted list differs: batch {b}"
+        assert_same_state(gpu_state(t, 0), oracle_state(o, 0), f"batch {b}")
+    t.set_path("auto")
+    # the tag walk itself: lookups of every pooled id match after all of it
+    s, oc = t.lookup(pool)
+    os_, oo = o.lookup(pool)
+    assert (s == os_).all() and (oc == oo).all()
+
+
+def test_tags_raw_writes(oracle):
+    """Raw slot writes (mpzch_write_slots) retag their slots: an id written 40 slots past its
+    home -- beyond the first identity line, so only the tag walk can reach it -- is Found there;
+    overwritten by another id, it becomes absent and inserts at the first EMPTY."""
+    cap, P, seed = 4096, 256, 5
+    h = 100
+    q = find_id_with_home(oracle, h, cap, seed)
+    fill = [find_id_with_home(oracle, s, cap, seed, 1 << 20) for s in range(h, h + 40)]
+    t = mz.MpzchTable(mz.TableConfig([cap], P, seed))
+    t.write_slots(0, list(range(h, h + 40)) + [h + 40], fill + [q], [0] * 41)
+    assert t.check_hole_free()
+    r = find_id_with_home(oracle, h, cap, seed, q + 1)
+    dis = mz.EvictionPolicy.disabled()
+    s, oc, _ = t.process_batch(np.array([q, r], dtype=np.uint64), 1, dis)
+    assert [int(x) for x in s] == [h + 40, h + 41] and [int(x) for x in oc] == [mz.FOUND, mz.INSERTED]
+    z = find_id_with_home(oracle, h + 40, cap, seed, 1 << 21)
+    t.write_slots(0, [h + 40], [z], [0])
+    assert t.check_hole_free()
+    s, oc, _ = t.process_batch(np.array([q, z], dtype=np.uint64), 2, dis)
+    assert [int(x) for x in s] == [h + 42, h + 40] and [int(x) for x in oc] == [mz.INSERTED, mz.FOUND]
