@@ -12,6 +12,7 @@
 
 #include "common.cuh"
 #include "line_scan.cuh"
+#include "tag_scan.cuh"
 #include "table.hpp"
 
 namespace mpzch_b200 {
@@ -183,6 +184,97 @@ __global__ void __launch_bounds__(256, U == 1 ? 6 : 4) k_lookup_line(TableDev t,
     }
 }
 
+// Long-window lookups on hole-free tables that keep identity tags: the first identity line of
+// the window, then 128-slot tag lines (tag_scan.cuh) -- k_probe_tag's walk without its writes.
+// An absent id at 0.95 load reads one identity line and ~2 tag lines instead of ~13 identity
+// lines to reach its first EMPTY.
+__global__ void __launch_bounds__(256, 5) k_lookup_tag(TableDev t, const uint64_t* __restrict__ ids, uint64_t n,
+                                                       uint64_t* __restrict__ out_slots,
+                                                       uint8_t* __restrict__ out_oc, BatchErr* err) {
+    constexpr uint8_t kPending = 0, kHit = 1, kStop = 2, kIdle = 3;
+    const unsigned j = quad_lane(), qm = quad_mask();
+    const int jb = 32 * (int)j;
+    const uint64_t qpb = blockDim.x >> 2, qib = threadIdx.x >> 2;
+    unsigned long long isec = 0;  // (not reported by lookups)
+    for (uint64_t t0 = (uint64_t)blockIdx.x * qpb; t0 < n; t0 += (uint64_t)gridDim.x * qpb) {
+        const uint64_t i = t0 + qib;
+        uint8_t st = kIdle;
+        uint64_t id = 0, g = 0, home = 0, base = 0, end = 0;
+        uint32_t off = 0;
+        if (i < n) {
+            id = ids[i];
+            if (id >> 63) {
+                if (j == 0) atomicMin(&err->bad_pos, (unsigned long long)i);
+            } else {
+                const uint32_t sh = shard_of(id, t);
+                if (!holds_shard(t, sh)) {
+                    if (j == 0) atomicMin(&err->foreign_pos, (unsigned long long)i);
+                } else {
+                    const ShardDev sd = t.shards[sh];
+                    base = sd.offset;
+                    end = base + sd.cap.d;
+                    home = base + home_of(id, sd, t.seed);
+                    g = home;
+                    st = kPending;
+                }
+            }
+        }
+        if (st == kPending) {  // the home slot's identity line
+            const LineSpan sp = line_span(g, end, off, t.P);
+            uint64_t w[4];
+            ld_line_part(t.ident, g, j, w);
+            unsigned m = 0, e = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                m |= (unsigned)(w[k] == id) << k;
+                e |= (unsigned)(w[k] == kEmpty) << k;
+            }
+            const unsigned x = quad_gather(m, e, j, qm);
+            const unsigned hit = (x | (x >> 16)) & sp.range();
+            if (hit) {
+                const unsigned q = __ffs(hit) - 1;
+                st = (x >> q) & 1u ? kHit : kStop;
+                g += q - sp.s;
+            } else {
+                off += sp.c;
+                g += sp.c;
+                if (g == end) g = base;
+                if (off >= t.P) st = kStop;
+            }
+        }
+        const uint32_t pat = (uint32_t)tag_of(id) * 0x01010101u;
+        while (st == kPending) {  // then 128 slots of tags per round
+            const uint64_t tl = g & ~127ull;
+            const int s0 = (int)(g & 127u);
+            const int c0 = (int)tag_seg_len(g, end, off, t.P);
+            uint64_t v[4];
+            ld_tag_part(t, tl, j, v);
+            unsigned fe;
+            const unsigned q = tag_segment(t, v, pat, id, tl, s0, c0, jb, j, qm, fe, isec);
+            if (q != 128u) {
+                st = kHit;
+                g = tl + q;
+            } else if (fe != 128u) {
+                st = kStop;
+            } else {
+                off += (uint32_t)c0;
+                g += (uint64_t)c0;
+                if (g == end) g = base;
+                if (off >= t.P) st = kStop;
+            }
+        }
+        if (j == 0) {
+            if (st == kHit) {
+                out_slots[i] = g;
+                out_oc[i] = kFound;
+            } else if (st == kStop) {
+                out_slots[i] = home;
+                out_oc[i] = kCollision;
+            }
+        }
+    }
+}
+
 // Fused lookup + gather (the frozen-replica read path, MpzchTable::lookup
 // table.cpp:150-156 then MpzchTable::gather table.cpp:158-163 / EmbeddingTable::gather
 // embedding_store.cpp:95-103): each lane of a warp probes one position, then the warp copies
@@ -275,7 +367,13 @@ void run_lookup(const Table& t, const uint64_t* ids, uint64_t n, uint64_t* out_s
                 BatchErr* err, cudaStream_t st, DevBuf* ldefer, unsigned* dcount) {
     // long windows (max_probe >= 256, or the full-window scan of a table with holes): quad
     // line walk; else the per-thread sector walk (remap_fast.cu has the same rule)
-    if (t.P >= 256 || !t.hole_free) {
+    static const bool tag_env = [] {  // the tag walk for long windows (MPZCH_TAGS=0: off)
+        const char* e = getenv("MPZCH_TAGS");
+        return !(e && e[0] == '0' && e[1] == 0);
+    }();
+    if (t.P >= 256 && t.hole_free && t.dev.tag && tag_env) {
+        k_lookup_tag<<<grid_for(4 * n, 256, 148u * 32u), 256, 0, st>>>(t.dev, ids, n, out_slots, out_oc, err);
+    } else if (t.P >= 256 || !t.hole_free) {
         const unsigned gl = grid_for(4 * ((n + 1) / 2), 256, 148u * 16u);
         // one position per quad, 6 blocks/SM (C3 lookups 7.15 -> 8.68 G/s vs 2 per quad)
         static const unsigned defer = [] {
