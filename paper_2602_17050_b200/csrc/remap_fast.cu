@@ -1058,7 +1058,65 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
             } else {
                 off = fresh ? ev.a : resume;
             }
-            if (!held && MODE != kModeTtl) {
+            if (!held && MODE != kModeTtl && t.tag) {
+                // Disabled / LRU on a table that keeps identity tags: the claimable slots (EMPTY or
+                // claim words) are exactly the slots EMPTY at the batch start -- tag 0 (no identity
+                // changes before K4) -- so the scan reads 32 tags per load instead of 4
+                // identities, and tries atomicMin on each tag-0 slot in order (a lower-rank claim
+                // word stays: atomicMin leaves a smaller word).  A fresh entry's first available
+                // slot was EMPTY when probed: its first attempt reads nothing.
+                const uint64_t end = base + cap;
+                const uint64_t nv = cv | kFlagEmpty;
+                if (fresh && off < t.P) {
+                    const uint64_t g = base + wrap_add(h, off, cap);
+                    const uint64_t old = atomicMin((unsigned long long*)(t.ident + g), (unsigned long long)nv);
+                    if (old >= nv) {
+                        atomicMax(&te[e].held, off);
+                        held = true;
+                        if (old != kEmpty) { next = claim_entry(old); gnext = g; }
+                    } else {
+                        ++off;
+                    }
+                }
+                while (!held && off < t.P) {
+                    const uint64_t g = base + wrap_add(h, off, cap);
+                    const uint64_t c32 = g & ~31ull;
+                    const uint32_t j0 = (uint32_t)(g - c32);
+                    uint32_t lim = 32 - j0;
+                    if (t.P - off < lim) lim = t.P - off;
+                    if (end - g < lim) lim = (uint32_t)(end - g);
+                    uint64_t v[4];
+                    ld_sector(reinterpret_cast<const uint64_t*>(t.tag + c32), v[0], v[1], v[2], v[3]);
+                    unsigned z = 0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        z |= msb_bits4(zero_bytes((uint32_t)(v[k >> 1] >> (32 * (k & 1))))) << (4 * k);
+                    z &= bit_range((int)j0, (int)(j0 + lim));
+                    while (z) {
+                        const unsigned k = __ffs(z) - 1;
+                        z &= z - 1;
+                        const uint64_t gk = c32 + k;
+                        const uint64_t old = atomicMin((unsigned long long*)(t.ident + gk), (unsigned long long)nv);
+                        if (old < nv) continue;  // a lower rank holds it
+                        atomicMax(&te[e].held, off + (k - j0));
+                        held = true;
+                        if (old != kEmpty) { next = claim_entry(old); gnext = gk; }
+                        break;
+                    }
+                    if (!held) off += lim;
+                }
+                if (!held) {
+                    te[e].state = kStateCollided;
+                    if (MODE == kModeLru) {  // (as below)
+                        const unsigned am = __activemask();
+                        const unsigned leader = __ffs(am) - 1;
+                        unsigned b0 = 0;
+                        if (lane_id() == leader) b0 = atomicAdd(&ctr->lru_evict, (unsigned)__popc(am));
+                        b0 = __shfl_sync(am, b0, leader);
+                        evl[b0 + __popc(am & ((1u << lane_id()) - 1))] = e;
+                    }
+                }
+            } else if (!held && MODE != kModeTtl) {
                 // Disabled / LRU: only EMPTY slots and claim words of a higher rank are
                 // claimable.  Sector by sector: one L2 read, a 4-bit mask of the claimable slots
                 // in the window part of the sector, then atomicMin on them in order -- the
