@@ -1121,8 +1121,23 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                 // claimable.  Sector by sector: one L2 read, a 4-bit mask of the claimable slots
                 // in the window part of the sector, then atomicMin on them in order -- the
                 // occupied slots (95% of a window at C3's load) cost no per-slot iteration.
+                // A fresh entry's first available slot was EMPTY when probed (claim words only
+                // ever land on such slots, all flagged kFlagEmpty): its first attempt is a blind
+                // atomicMin, no read before it.
                 const uint64_t end = base + cap;
-                while (off < t.P) {
+                if (fresh && off < t.P) {
+                    const uint64_t g = base + wrap_add(h, off, cap);
+                    const uint64_t nv = cv | kFlagEmpty;
+                    const uint64_t old = atomicMin((unsigned long long*)(t.ident + g), (unsigned long long)nv);
+                    if (old >= nv) {
+                        atomicMax(&te[e].held, off);
+                        held = true;
+                        if (old != kEmpty) { next = claim_entry(old); gnext = g; }
+                    } else {
+                        ++off;
+                    }
+                }
+                while (!held && off < t.P) {
                     const uint64_t g = base + wrap_add(h, off, cap);
                     const uint64_t a4 = g & ~3ull;
                     const uint32_t j0 = (uint32_t)(g - a4);
