@@ -255,3 +255,33 @@ def test_device_protocol_ttl_overflow_and_precedence(oracle):
     o = oracle.OracleTable(caps, 16, 7, 4, 3)
     o.process_batch(ids, now, 1, 10, {5: 1000}, feats)  # the one batch that went through
     check_state(ranks, o, 4)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_device_protocol_long_windows_tags(oracle, world):
+    """max_probe 256 (the owners keep identity tags: tag walks, tag-guided claims) over uneven
+    shard capacities (a rank's held rows start off a 128-row tag line), at high load, Disabled
+    and TTL batches alternating: every slice and each rank's held state against the oracle."""
+    rng = np.random.default_rng(300 + world)
+    caps = [3001, 2500, 4100, 1777, 2999]
+    cfg = mz.TableConfig(caps, 256, 11)
+    ranks = make_ranks(cfg, world, 20000)
+    o = oracle.OracleTable(caps, 256, 11)
+    uni = oracle.distinct_ids(90 + world, 0, int(sum(caps) * 1.1))
+    for b in range(8):
+        mode = b % 2
+        pol = mz.EvictionPolicy.ttl(mz.TtlPolicy(5)) if mode else mz.EvictionPolicy.disabled()
+        n = int(rng.choice([4000, 12000]))
+        ids = uni[rng.integers(0, uni.size, n)]
+        now = 1 + 3 * b
+        slices = split(n, world, rng)
+        out = run_batch(ranks, ids, None, now, pol, slices)
+        os_, oo, oe = o.process_batch(ids, now, mode, 5 if mode else 0)
+        for r in range(world):
+            assert not isinstance(out[r], Exception), f"rank {r}: {out[r]!r}"
+            s_, o_, e_ = out[r]
+            assert (s_ == os_[slices[r]]).all() and (o_ == oo[slices[r]]).all(), f"batch {b} rank {r}"
+            assert e_.size == oe.size and (e_ == oe).all(), f"batch {b} rank {r}: evicted list"
+    check_state(ranks, o, 0)
+    for rk in ranks:
+        rk.close()
