@@ -55,6 +55,9 @@ constexpr uint64_t kEntryMask = (1ull << 30) - 1;
 constexpr uint8_t kStateCollided = 1;
 constexpr uint8_t kStateEvict = 2;     // LRU: the entry evicts the slot at offset `held` (K3b)
 constexpr uint8_t kPendingOc = 0xFF;   // LRU: out_oc of a position on the new list until K4/K5
+// TTL: newa's flag for "the first available slot was EMPTY when probed" (not expired): K3 tries
+// it with a blind atomicMin; K2 moves the flag into the entry record (IdEntry::aempty)
+constexpr uint32_t kAEmpty = 1u << 31;
 
 // Distinct new ids: a hash index of 16-byte keys (id | (epoch32 << 32 | e) << 64 -- a key whose
 // epoch is not the current batch's is empty, so no cleanup pass is needed) and DENSE entry
@@ -85,7 +88,8 @@ struct __align__(64) IdEntry {
     uint32_t held;            // last taker claim offset          (atomicMax)
     uint8_t state;            // kStateCollided when the window is exhausted
     uint8_t oc;               // committed outcome
-    uint8_t pad0[2];
+    uint8_t aempty;           // TTL: slot a was EMPTY when probed (newa's kAEmpty)
+    uint8_t pad0;
     uint64_t slot;            // committed global slot
     uint64_t pad1[2];
 };
@@ -358,7 +362,10 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
                     } else {
                         const uint32_t lim = st[u] == kEmptyHit ? off[u] : t.P;
                         const uint32_t x = fe[u] != kNone32 ? fe[u] : lim;
-                        if (x < lim || st[u] == kEmptyHit) { is_new = true; a_off = x; }
+                        if (x < lim || st[u] == kEmptyHit) {
+                            is_new = true;
+                            a_off = x | (x == lim ? kAEmpty : 0u);  // (x == lim: the walk's EMPTY)
+                        }
                         else { fslot = base[u] + h[u]; foc = kCollision; }
                     }
                 }
@@ -560,7 +567,10 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
                     } else {
                         const uint32_t lim = st[u] == kEmptyHit ? off[u] : t.P;
                         const uint32_t xo = fe[u] != kNone32 ? fe[u] : lim;
-                        if (xo < lim || st[u] == kEmptyHit) { is_new = true; a_off = xo; }
+                        if (xo < lim || st[u] == kEmptyHit) {
+                            is_new = true;
+                            a_off = xo | (xo == lim ? kAEmpty : 0u);  // (xo == lim: the walk's EMPTY)
+                        }
                         else { fslot = base + h; foc = kCollision; }
                     }
                 }
@@ -963,8 +973,9 @@ __global__ void __launch_bounds__(256) k_dedup(BatchCounters* ctr, uint64_t tcap
             // fence: a word left by an older batch holds an older epoch, so it is smaller
             te[k].id = id;
             uint64_t* w = reinterpret_cast<uint64_t*>(&te[k].a);
-            w[0] = (uint64_t)newa[k] | ((uint64_t)newm[k] << 32);
-            w[1] = 0;  // held = state = oc = 0
+            const uint32_t na = newa[k];
+            w[0] = (uint64_t)(na & ~kAEmpty) | ((uint64_t)newm[k] << 32);
+            w[1] = (na & kAEmpty) ? (1ull << 48) : 0ull;  // held = state = oc = 0, aempty
             atomicMax(&te[k].rank, myrank);
         } else if (__ldcg(&te[e].rank) < myrank) {  // (a hot id's later positions skip the atomic)
             atomicMax(&te[e].rank, myrank);
@@ -988,6 +999,7 @@ struct EntryView {
     unsigned long long rank;
     uint32_t a, m, held;
     uint8_t state;
+    bool aempty;
 };
 __device__ __forceinline__ EntryView load_entry(const IdEntry* te, uint32_t e) {
     const ulonglong2* p = reinterpret_cast<const ulonglong2*>(&te[e].rank);
@@ -998,6 +1010,7 @@ __device__ __forceinline__ EntryView load_entry(const IdEntry* te, uint32_t e) {
     v.m = (uint32_t)(w1.y >> 32);
     v.held = (uint32_t)w2.x;
     v.state = (uint8_t)(w2.x >> 32);
+    v.aempty = ((w2.x >> 48) & 0xFF) != 0;
     return v;
 }
 
@@ -1183,6 +1196,22 @@ __global__ void __launch_bounds__(256) k_claim(TableDev t, uint64_t now, BatchCo
                     }
                 }
             } else if (!held) {
+                // TTL, a fresh taker whose first available slot was EMPTY when probed: a blind
+                // atomicMin first (EMPTY slots only ever become claim words, all flagged EMPTY)
+                if (MODE == kModeTtl && fresh && ev.aempty && off < t.P) {
+                    const uint64_t g = base + wrap_add(h, off, cap);
+                    const uint64_t nv = cv | kFlagEmpty;
+                    const uint64_t old = atomicMin((unsigned long long*)(t.ident + g), (unsigned long long)nv);
+                    if (old >= nv) {
+                        atomicMax(&te[e].held, off);
+                        held = true;
+                        if (old != kEmpty) { next = claim_entry(old); gnext = g; }
+                    } else {
+                        ++off;
+                    }
+                }
+            }
+            if (!held && MODE == kModeTtl) {
                 // TTL: the same sector mask with the metadata sector in the same round --
                 // claimable: EMPTY or a higher-rank claim word (atomicMin, as above), or an
                 // expired id (CAS, re-evaluated on failure) -- so the scan takes no dependent
