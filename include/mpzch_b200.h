@@ -167,7 +167,9 @@ mpzch_status mpzch_copy_momentum(const mpzch_table* t, uint64_t row0, uint64_t n
                                  float* host_out);
 mpzch_status mpzch_copy_trained(const mpzch_table* t, uint8_t* host_out);
 mpzch_status mpzch_copy_row_generation(const mpzch_table* t, uint64_t* host_out);
-/* device pointers of the resident arrays (for fused consumers and the bench) */
+/* device pointers of the resident arrays (for fused consumers and the bench): READ views --
+ * identities and metadata change only through the calls of this header (raw writes through
+ * mpzch_write_slots, which also keeps the identity tags of max_probe >= 256 tables) */
 mpzch_status mpzch_device_arrays(const mpzch_table* t, uint64_t** identities,
                                  uint64_t** metadata, float** weights);
 
@@ -175,7 +177,8 @@ mpzch_status mpzch_device_arrays(const mpzch_table* t, uint64_t** identities,
  *      directly, e.g. proj/tests/test_probe_core.cpp:113-121).  Writing raw
  *      slots may create probe-window holes, so it switches the handle to the
  *      hole-tolerant full-window semantics until mpzch_check_hole_free()
- *      proves the no-hole invariant again. */
+ *      proves the no-hole invariant again.  Tables with max_probe >= 256 retag
+ *      the written slots (the probe's identity-tag index). */
 mpzch_status mpzch_write_slots(mpzch_table* t, uint32_t shard, const uint64_t* local_slots,
                                const uint64_t* identities, const uint64_t* metadata, uint64_t n);
 mpzch_status mpzch_check_hole_free(mpzch_table* t, int* out_hole_free);
