@@ -763,8 +763,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line_la(TableDev t, const u
 // remains is issue-bound (62% issue-active, half of it the tag byte masks).  Swept: loading 1 or
 // 2 tag lines with the identity line (0.76 / 0.71 ms, 48 / 64 registers), 6 or 8 blocks/SM (0.72 /
 // 0.80 ms): none clearly better than this plain variant at 5 blocks/SM.
-// PF: tag lines loaded in round 0 together with the identity line (the rest one round trip each)
-template <int MINB, int PF>
+template <int MINB>
 __global__ void __launch_bounds__(256, MINB) k_probe_tag(TableDev t, const uint64_t* __restrict__ ids,
                                                          uint64_t n, uint64_t now, uint64_t meta_value,
                                                          BatchCounters* ctr,
@@ -800,28 +799,10 @@ __global__ void __launch_bounds__(256, MINB) k_probe_tag(TableDev t, const uint6
             st = kPending;
         }
         const uint32_t pat = (uint32_t)tag_of(id) * 0x01010101u;
-        uint64_t vp[PF > 0 ? PF : 1][4];
-        if (st == kPending) {  // round 0: the home slot's identity line (+ PF tag lines after it)
+        if (st == kPending) {  // round 0: the home slot's identity line
             const LineSpan sp = line_span(g, end, off, t.P);
             uint64_t w[4];
             ld_line_part(t.ident, g, j, w);
-            {
-                uint64_t gq = g + sp.c;
-                uint32_t oq = off + sp.c;
-                if (gq == end) gq = base;
-#pragma unroll
-                for (int p = 0; p < PF; ++p) {
-                    if (oq < t.P) {
-                        ld_sector(reinterpret_cast<const uint64_t*>(t.tag + (gq & ~127ull)) + 4 * j,
-                                  vp[p][0], vp[p][1], vp[p][2], vp[p][3]);
-                        ++my_tsec;
-                    }
-                    const uint32_t cq = tag_seg_len(gq, end, oq, t.P);
-                    oq += cq;
-                    gq += cq;
-                    if (gq == end) gq = base;
-                }
-            }
             unsigned m = 0, e = 0;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -844,23 +825,16 @@ __global__ void __launch_bounds__(256, MINB) k_probe_tag(TableDev t, const uint6
                 if (off >= t.P) st = kExhausted;
             }
         }
-        // the rest of the window on the tag lines, 128 slots per segment
-        int seg = 0;
+        // the rest of the window on the tag lines, 128 slots per round
         while (st == kPending) {
             const uint64_t tl = g & ~127ull;
             const int s0 = (int)(g & 127u);
             const int c0 = (int)tag_seg_len(g, end, off, t.P);
-            unsigned q, fe;
             uint64_t v[4];
-            if (seg < PF) {  // (register selects: no dynamic index into vp)
-#pragma unroll
-                for (int k = 0; k < 4; ++k) v[k] = seg == 0 ? vp[0][k] : vp[PF > 1 ? 1 : 0][k];
-            } else {
-                ld_sector(reinterpret_cast<const uint64_t*>(t.tag + tl) + 4 * j, v[0], v[1], v[2], v[3]);
-                ++my_tsec;
-            }
-            q = tag_segment(t, v, pat, id, tl, s0, c0, jb, j, qm, fe, my_isec);
-            ++seg;
+            ld_tag_part(t, tl, j, v);
+            ++my_tsec;
+            unsigned fe;
+            const unsigned q = tag_segment(t, v, pat, id, tl, s0, c0, jb, j, qm, fe, my_isec);
             if (q != 128u) {
                 st = kHit;
                 off += q - (unsigned)s0;
@@ -1684,7 +1658,7 @@ void preload_remap_kernels() {
 #define PL(k) preload_kernel((const void*)(k))
     PL(k_init_counters); PL(k_sh_adopt); PL(k_validate);
     PL((k_probe_line<kModeTtl, 2, 3, true>)); PL((k_probe_line<kModeTtl, 2, 3>));
-    PL((k_probe_line<kModeLru, 2, 4>)); PL((k_probe_line<kModeDisabled, 1, 8>)); PL(k_probe_line_la<8>); PL((k_probe_tag<5, 0>));
+    PL((k_probe_line<kModeLru, 2, 4>)); PL((k_probe_line<kModeDisabled, 1, 8>)); PL(k_probe_line_la<8>); PL((k_probe_tag<5>));
     PL((k_probe_line<kModeDisabled, 2, 4>)); PL((k_probe_line<kModeTtl, 1, 4, true, true>));
     PL((k_probe_line<kModeTtl, 1, 4, false, true>));
     PL((k_probe<kModeTtl, 2, 3, true, false, true>)); PL((k_probe<kModeTtl, 2, 3, true>));
@@ -1771,7 +1745,7 @@ void enqueue_fast_batch(Table& t, const BatchArgs& a, cudaStream_t st) {
         // long windows: one position per quad at 8 blocks/SM (C3 insert-heavy 1.88 -> 2.07 G/s);
         // small batches keep 2 per quad (C1 1.10 vs 1.04 G/s pipelined)
         else if (t.P >= 256 && t.dev.tag && tag_env)
-            launch_pdl(k_probe_tag<5, 0>, grid_for(4 * n, B, 148u * 32u), B, st, MPZCH_PROBE_ARGS, nol);
+            launch_pdl(k_probe_tag<5>, grid_for(4 * n, B, 148u * 32u), B, st, MPZCH_PROBE_ARGS, nol);
         else if (t.P >= 256 && la_env)
             launch_pdl(k_probe_line_la<8>, grid_for(4 * n, B, 148u * 32u), B, st, MPZCH_PROBE_ARGS, nol);
         else if (t.P >= 256)
