@@ -345,7 +345,13 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
                 uint8_t foc = kFound;
                 if (MODE != kModeTtl) {
                     if (st[u] == kHit) fslot = g[u];
-                    else if (st[u] == kEmptyHit) { is_new = true; a_off = off[u]; }
+                    else if (st[u] == kEmptyHit) {
+                        is_new = true;
+                        a_off = off[u];
+                        // Disabled: the likely result -- Inserted at the walk's EMPTY -- written
+                        // with this warp's other results; K4 rewrites only positions it differs for
+                        if (MODE == kModeDisabled) { out_slots[i] = g[u]; out_oc[i] = kInserted; }
+                    }
                     // LRU full window: an evictor -- its claim finds nothing (a = P) and K3b
                     // picks the least recently used slot
                     else if (MODE == kModeLru) { is_new = true; a_off = t.P; }
@@ -552,7 +558,11 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
                 uint8_t foc = kFound;
                 if (MODE != kModeTtl) {
                     if (st[u] == kHit) fslot = g[u];
-                    else if (st[u] == kEmptyHit) { is_new = true; a_off = off[u]; }
+                    else if (st[u] == kEmptyHit) {
+                        is_new = true;
+                        a_off = off[u];
+                        if (MODE == kModeDisabled && j == 0) { out_slots[i] = g[u]; out_oc[i] = kInserted; }  // (as k_probe)
+                    }
                     else if (MODE == kModeLru) { is_new = true; a_off = t.P; }  // evictor (K3b)
                     else { fslot = base + h; foc = kCollision; }
                 } else {  // TTL with one metadata value per batch (expiry read with the walk)
@@ -714,7 +724,12 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line_la(TableDev t, const u
             uint64_t fslot = kEmpty;
             uint8_t foc = kFound;
             if (st == kHit) fslot = g;
-            else if (st == kEmptyHit) { is_new = true; a_off = off; }
+            else if (st == kEmptyHit) {
+                is_new = true;
+                a_off = off;
+                out_slots[i] = g;  // the likely result (as k_probe)
+                out_oc[i] = kInserted;
+            }
             else { fslot = base + h; foc = kCollision; }
             if (fslot != kEmpty) {
                 out_slots[i] = fslot;
@@ -856,7 +871,12 @@ __global__ void __launch_bounds__(256, MINB) k_probe_tag(TableDev t, const uint6
             uint64_t fslot = kEmpty;
             uint8_t foc = kFound;
             if (st == kHit) fslot = g;
-            else if (st == kEmptyHit) { is_new = true; a_off = off; }
+            else if (st == kEmptyHit) {
+                is_new = true;
+                a_off = off;
+                out_slots[i] = g;  // the likely result (as k_probe)
+                out_oc[i] = kInserted;
+            }
             else { fslot = base + h; foc = kCollision; }
             if (fslot != kEmpty) {
                 out_slots[i] = fslot;
@@ -1365,9 +1385,13 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
             te[e].oc = oc;
         }
         // the primary item's own position (its feature is the entry's): result written
-        // here, so K5 only has items of repeated ids left
-        out_slots[rank] = g;
-        out_oc[rank] = oc;
+        // here, so K5 only has items of repeated ids left.  Disabled: the probe already wrote
+        // Inserted at the first available slot -- rewritten only where the claims moved it (a
+        // random write per new id saved: C5 / C3 commit)
+        if (MODE != kModeDisabled || oc != kInserted || ev.held != ev.a) {
+            out_slots[rank] = g;
+            out_oc[rank] = oc;
+        }
         ++c[oc];
         ++np;
     }
