@@ -371,6 +371,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe(TableDev t, const uint64_t*
                         if (x < lim || st[u] == kEmptyHit) {
                             is_new = true;
                             a_off = x | (x == lim ? kAEmpty : 0u);  // (x == lim: the walk's EMPTY)
+                            if (x == lim) { out_slots[i] = g[u]; out_oc[i] = kInserted; }  // likely result
                         }
                         else { fslot = base[u] + h[u]; foc = kCollision; }
                     }
@@ -580,6 +581,7 @@ __global__ void __launch_bounds__(256, MINB) k_probe_line(TableDev t, const uint
                         if (xo < lim || st[u] == kEmptyHit) {
                             is_new = true;
                             a_off = xo | (xo == lim ? kAEmpty : 0u);  // (xo == lim: the walk's EMPTY)
+                            if (xo == lim && j == 0) { out_slots[i] = g[u]; out_oc[i] = kInserted; }  // likely result
                         }
                         else { fslot = base + h; foc = kCollision; }
                     }
@@ -1385,10 +1387,10 @@ __global__ void __launch_bounds__(256) k_commit(TableDev t, BatchCounters* ctr,
             te[e].oc = oc;
         }
         // the primary item's own position (its feature is the entry's): result written
-        // here, so K5 only has items of repeated ids left.  Disabled: the probe already wrote
-        // Inserted at the first available slot -- rewritten only where the claims moved it (a
-        // random write per new id saved: C5 / C3 commit)
-        if (MODE != kModeDisabled || oc != kInserted || ev.held != ev.a) {
+        // here, so K5 only has items of repeated ids left.  Disabled, and TTL takers whose first
+        // available slot was EMPTY: the probe already wrote Inserted at that slot -- rewritten
+        // only where the claims moved it (a random write pair per new id saved)
+        if (!((MODE == kModeDisabled || (MODE == kModeTtl && ev.aempty)) && oc == kInserted && ev.held == ev.a)) {
             out_slots[rank] = g;
             out_oc[rank] = oc;
         }
